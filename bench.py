@@ -1,0 +1,335 @@
+#!/usr/bin/env python
+"""Benchmark of the Fast-SNARF deformer hot path on B200 (driver contract: one JSON line).
+
+Metric (BASELINE.json): (point x bone-init) correspondences/sec — one Broyden solve per
+(posed point, bone-init) pair. A step is one pass of the hot path over one batch:
+K1 precompute_transform_grid + spatial sort + K2 correspondence search + dedup, for the
+configuration BASELINE.json's metric is quoted on (configs[1]): 200k posed points x 24
+bone inits, 32^3 grid, reference default max_iters=50. Weak scaling: every rank
+processes its own 200k points (points shard with no data-path collective).
+
+  python bench.py [--gpus N --steps K --warmup W]            # our arm
+  python bench.py --impl reference [...]                      # the reference CPU path
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2211_15601_b200 import synthetic as S  # noqa: E402
+
+METRIC = "(point x bone-init) correspondences/sec"
+UNIT = "solves/s"
+# Algorithmic FP32 flops per solve of K2 (counted from the kernel's op sequence; FMA = 2;
+# derivation in DESIGN.md §K2): init, per Broyden iteration, and the saving of a
+# terminating (converged) iteration that skips the rank-one update.
+FLOPS_INIT, FLOPS_ITER, FLOPS_FINAL_SAVING = 674, 332, 66
+GATHER_BYTES = 384  # 8 corners x 48 B of transform grid per d(x) evaluation
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--points", type=int, default=200_000, help="posed points per GPU")
+    ap.add_argument("--grid", default="32,32,32")
+    ap.add_argument("--max-iters", type=int, default=50)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--no-sort", action="store_true", help="ablation: no spatial ordering")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-baseline sample duration")
+    return ap.parse_args()
+
+
+def scene_for_rank(args, rank):
+    dims = tuple(int(v) for v in args.grid.split(","))
+    # same skeleton/pose/grid on every rank; each rank owns a distinct point shard
+    sc = S.make_scene(dims, args.points, seed=args.seed)
+    if rank:
+        rng = np.random.default_rng(args.seed * 1000 + rank)
+        lo, hi = S.posed_sampling_box(S.smpl_like_skeleton(), S.forward_kinematics(S.smpl_like_skeleton(), sc.angles))
+        sc.points = S.uniform_points(lo, hi, args.points, rng).astype(np.float32)
+    return sc
+
+
+def workload_name(args):
+    return (f"C2: {args.points // 1000}k posed points x 24 bone inits per GPU, {args.grid.replace(',', 'x')} grid, "
+            f"max_iters {args.max_iters}; step = precompute + sort + search + dedup")
+
+
+# ------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.proc, self.lines = index, None, []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------ CPU side
+def cpu_rate(sc, args, seconds, workers):
+    """Reference CPU path (the oracle's f64 restatement of batch_search, all host threads)
+    on a bounded sample of the same workload → (solves/s, points sampled, wall s)."""
+    import oracle
+    opts = sc.search_options(args.max_iters)
+    tg = oracle.precompute_transform_grid(sc.weights, sc.dims, sc.bbox, sc.bones, workers)
+    m = min(2000, sc.points.shape[0])
+    t0 = time.perf_counter()
+    oracle.batch_search(sc.weights, sc.dims, sc.bbox, sc.bones, sc.points[:m], workers=workers, tgrid=tg, **opts)
+    dt = time.perf_counter() - t0
+    m2 = int(min(sc.points.shape[0], max(m, m * seconds / max(dt, 1e-6))))
+    t0 = time.perf_counter()
+    tgt = oracle.precompute_transform_grid(sc.weights, sc.dims, sc.bbox, sc.bones, workers)  # per-pose precompute
+    oracle.batch_search(sc.weights, sc.dims, sc.bbox, sc.bones, sc.points[:m2], workers=workers, tgrid=tgt, **opts)
+    dt = time.perf_counter() - t0
+    return m2 * sc.n_bones / dt, m2, dt
+
+
+def run_reference(args, rank, world):
+    """``--impl reference``: the reference's CPU implementation of the path (the oracle port —
+    the reference itself cannot be built here) on this box's host cores."""
+    if rank != 0:
+        return
+    sc = scene_for_rank(args, 0)
+    workers = os.cpu_count() or 1
+    rate, m, dt = cpu_rate(sc, args, 2.0, workers)  # calibrate one step to ~2 s
+    import oracle
+    opts = sc.search_options(args.max_iters)
+    m = max(1, min(sc.points.shape[0], int(rate * 2.0 / sc.n_bones)))
+    times = []
+    for it in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        tg = oracle.precompute_transform_grid(sc.weights, sc.dims, sc.bbox, sc.bones, workers)
+        oracle.batch_search(sc.weights, sc.dims, sc.bbox, sc.bones, sc.points[:m], workers=workers, tgrid=tg, **opts)
+        if it >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    t = float(np.sum(times))
+    value = m * sc.n_bones * len(times) / t
+    sample = f"{m} of {sc.points.shape[0]} points x {sc.n_bones} inits per step (precompute + search + dedup)"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / len(times) * sc.points.shape[0] / m,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic SMPL-like skeleton, analytic capsule weights, uniform posed points",
+            "config": {"workload": workload_name(args), "points_per_gpu": args.points, "n_init": sc.n_bones,
+                       "grid": list(sc.dims), "max_iters": args.max_iters},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "note": "oracle/fskin_oracle.cpp: f64 restatement of the reference batch_search "
+                    "(reference needs Eigen3, absent; see DESIGN.md)"}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------ GPU side
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2211_15601_b200.deformer import Deformer, SearchOptions
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    D = Deformer(local_rank)
+    sc = scene_for_rank(args, rank)
+    nb, n = sc.n_bones, sc.points.shape[0]
+    w = torch.from_numpy(sc.weights).to(dev)
+    B = torch.from_numpy(sc.bones).to(dev)
+    x = torch.from_numpy(sc.points).to(dev)
+    tg = torch.empty((w.shape[0], 12), dtype=torch.float32, device=dev)
+    opts = SearchOptions(args.max_iters, **{k: v for k, v in sc.search_options(args.max_iters).items()
+                                           if k != "max_iters"})
+    opts.sort = not args.no_sort
+    out = D.alloc_search_out(n, nb)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+
+    def step():
+        D.precompute_transform_grid(w, sc.dims, sc.bbox, B, out=tg)
+        D.batch_search(tg, sc.dims, sc.bbox, B, x, opts, out=out)
+
+    peak_fp32 = D.measure_fp32_peak()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream(dev)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks = ClockSampler(local_rank)
+    D.prof_read(reset=True)
+    D.set_profiling(True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    launches0 = D.launch_count
+    for i in range(args.steps):
+        flush.fill_(float(i))  # L2 flush between steps, outside the per-step events
+        evs[i][0].record(stream)
+        step()
+        evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    launches = D.launch_count - launches0
+    D.set_profiling(False)
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = float(np.sum(step_ms))
+    k2_ms, k2_n = D.prof_read("k_search", reset=False)
+    k1_ms, k1_n = D.prof_read("k_precompute_tgrid", reset=False)
+    all_ms, _ = D.prof_read(None, reset=True)
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+
+    # algorithmic work of one K2 launch (deterministic: identical every step)
+    iters = out["iters"].to(torch.int64)
+    conv = out["converged"].to(torch.bool)
+    sum_iters = int(iters.sum().item())
+    n_final = int((conv & (iters > 0)).sum().item())
+    solves = n * nb
+    flops = solves * FLOPS_INIT + sum_iters * FLOPS_ITER - n_final * FLOPS_FINAL_SAVING
+    gather = (solves + sum_iters) * GATHER_BYTES
+    k2_avg = k2_ms / max(k2_n, 1)
+    achieved = flops / (k2_avg * 1e-3) / 1e12
+    V = w.shape[0]
+    k1_bytes = V * (4 * nb + 48)
+
+    value = world * solves * args.steps / (total_ms * 1e-3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic: SMPL-like 24-bone skeleton, random pose U(-0.5,0.5) rad, analytic capsule weight grid, "
+                "uniform posed points (seeded; same inputs the oracle parity tests use)",
+        "config": {"workload": workload_name(args), "points_per_gpu": n, "n_init": nb, "grid": list(sc.dims),
+                   "max_iters": args.max_iters, "sort": not args.no_sort,
+                   "l2": "flushed between steps (256 MiB fill outside the per-step CUDA events)",
+                   "parallelism": f"points sharded across {world} GPU(s), no data-path collective"},
+        "roofline": {"bound": "fp32", "kernel": "k_search", "achieved": achieved, "peak": peak_fp32,
+                     "unit": "TFLOP/s", "frac": achieved / peak_fp32, "traffic": None,
+                     "peak_source": "measured live: FFMA-chain kernel over all SMs (fsk_measure_fp32_peak); "
+                                    "MEASURED_PEAKS.json has no FP32 figure",
+                     "algorithmic_flops_per_launch": flops, "avg_launch_ms": k2_avg,
+                     "mean_iters_per_solve": sum_iters / solves, "converged_frac": float(conv.float().mean()),
+                     "gather": {"requested_bytes_per_launch": gather,
+                                "achieved_GBps": gather / (k2_avg * 1e-3) / 1e9},
+                     "k2_share_of_step": k2_ms / max(all_ms, 1e-9),
+                     "k1": {"bytes_per_launch": k1_bytes, "avg_launch_ms": k1_ms / max(k1_n, 1),
+                            "achieved_GBps": k1_bytes / (k1_ms / max(k1_n, 1) * 1e-3) / 1e9}},
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+
+    if rank == 0 and not args.no_e2e:
+        line["e2e"] = e2e_ours(D, sc, opts, args)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        workers = os.cpu_count() or 1
+        rate, m, dt = cpu_rate(sc, args, args.cpu_seconds, workers)
+        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": workers, "kind": "port",
+                                "sample": f"{m} of {n} points x {nb} inits (precompute + search + dedup), {dt:.1f} s, "
+                                          "f64 oracle restatement of batch_search, std::thread over all host cores"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    D.close()
+
+
+def e2e_ours(D, sc, opts, args, steps=None):
+    """Same metric through the C-ABI host-buffer entry point (fsk_deform_host): pinned host
+    weights/bones/points in, CorrespondenceSets (offsets + kept roots) out, copies inside."""
+    import torch
+    steps = steps or max(3, min(args.steps, 10))
+    n, nb = sc.points.shape[0], sc.n_bones
+    hw = torch.from_numpy(sc.weights).pin_memory()
+    hb = torch.from_numpy(sc.bones).pin_memory()
+    hx = torch.from_numpy(sc.points).pin_memory()
+    hoffs = torch.empty(n + 1, dtype=torch.int64).pin_memory()
+    hroots = torch.empty((n * nb, 16), dtype=torch.float32).pin_memory()
+    for _ in range(2):
+        total = D.deform_host(hw, sc.dims, sc.bbox, hb, hx, opts, hoffs, hroots)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        total = D.deform_host(hw, sc.dims, sc.bbox, hb, hx, opts, hoffs, hroots)
+    dt = (time.perf_counter() - t0) / steps
+    return {"value": n * nb / dt, "unit": UNIT, "ms_per_step": 1e3 * dt,
+            "h2d_bytes_per_step": int(hw.numel() * 4 + hb.numel() * 4 + hx.numel() * 4),
+            "d2h_bytes_per_step": int((n + 1) * 8 + total * 64),
+            "api": "fsk_deform_host (C-ABI, pinned host buffers; synchronous call timed on the host clock)"}
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

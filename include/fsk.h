@@ -1,0 +1,168 @@
+/* fsk.h — C-ABI of the B200-native Fast-SNARF deformer (sm_100a).
+ *
+ * Drop-in boundary for the reference's deformer/correspondence hot path
+ * (/root/reference/proj/include/fskin/deformer.hpp, correspondence.hpp). Every entry
+ * point is `extern "C"`, takes plain pointers and sizes, never throws, and returns
+ *   FSK_OK (0)            success
+ *   FSK_EINVAL (1)        invalid argument — fsk_last_error() holds the reference's
+ *                         std::invalid_argument message text where one exists
+ *   FSK_ECUDA (2)         CUDA / NCCL / allocation failure (std::runtime_error)
+ *   FSK_ENODEV (3)        no usable sm_100 device (the library has no CPU fallback)
+ * Device pointers ("dev") must live on the context's device. Calls are stream-ordered
+ * on `stream` (a cudaStream_t; NULL = legacy default stream) and asynchronous unless
+ * stated otherwise. A context is not thread-safe; distinct (ctx, stream) pairs are.
+ *
+ * Layouts (identical to the reference's storage, in float32):
+ *   weights  [V][n_b]     x-fastest vertex order, bone innermost (skinning.hpp:54-77)
+ *   tgrid    [V][12]      rows of the blended 3x4 [R|t], x-fastest (deformer.hpp:35-39)
+ *   bones    [n_b][12]    rows of RigidTransform [R|t] (geometry.hpp:42-78)
+ *   points   [N][3]
+ *   per-(point, init) outputs are point-major: [N][n_init][...], init i = bone i.
+ */
+#ifndef FSK_H_
+#define FSK_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FSK_OK 0
+#define FSK_EINVAL 1
+#define FSK_ECUDA 2
+#define FSK_ENODEV 3
+
+typedef struct fsk_ctx fsk_ctx;
+
+/* GridDims + canonical Aabb of a SkinningVoxelGrid / TransformGrid
+ * (skinning.hpp:45-52, :57-91; deformer.hpp:27-49). */
+typedef struct fsk_grid_desc {
+    int32_t nx, ny, nz;   /* >= 2 per axis (skinning.cpp:62-64) */
+    int32_t n_bones;      /* n_b of the weight grid */
+    float bbox_min[3];
+    float bbox_max[3];
+} fsk_grid_desc;
+
+/* SearchOptions (correspondence.hpp:14-26); fill from fsk_search_opts_defaults()
+ * = SearchOptions::defaults_for(bbox) (correspondence.cpp:10-17). */
+typedef struct fsk_search_opts {
+    int32_t max_iters;    /* >= 1, <= 255 */
+    float conv_eps;       /* > 0 */
+    float div_eps;        /* > conv_eps */
+    float dedup_dist;     /* >= 0 */
+    int32_t flags;        /* FSK_SEARCH_* */
+} fsk_search_opts;
+
+#define FSK_SEARCH_NO_SORT 0x1   /* ablation: skip the spatial ordering of queries */
+
+/* Dense per-(point, init) search result (the GPU form of Root / CorrespondenceSet,
+ * correspondence.hpp:29-42). All pointers dev, [N][n_b] point-major; any may be NULL
+ * except `converged`. `keep` is the dedup_roots mask (correspondence.cpp:162-176):
+ * keep=1 iff the init converged and survived greedy bone-order dedup. `n_roots`
+ * [N] int32 = number of kept roots per point. */
+typedef struct fsk_search_out {
+    float* x_c;           /* [N][n_b][3] canonical root (Root::x) */
+    float* jinv;          /* [N][n_b][9] Broyden inverse-Jacobian estimate (Root::inv_jacobian) */
+    float* resid;         /* [N][n_b] ||d(x)-x'|| at termination (Root::residual) */
+    uint8_t* iters;       /* [N][n_b] iterations executed (Root::iterations) */
+    uint8_t* converged;   /* [N][n_b] 1 iff residual < conv_eps was reached */
+    uint8_t* keep;        /* [N][n_b] dedup survivors (NULL: dedup skipped) */
+    int32_t* n_roots;     /* [N] kept roots per point (NULL allowed) */
+} fsk_search_out;
+
+/* Compact root record — one kept Root, in bone order per query (CorrespondenceSet). */
+typedef struct fsk_root {
+    float x[3];
+    float residual;
+    float inv_jacobian[9];
+    int32_t source_bone;
+    int32_t iterations;
+    int32_t _pad;
+} fsk_root; /* 64 bytes */
+
+/* ---- lifecycle ------------------------------------------------------------------ */
+int fsk_ctx_create(int device, fsk_ctx** out);
+int fsk_ctx_destroy(fsk_ctx* ctx);
+const char* fsk_last_error(void);                 /* thread-local, never NULL */
+int64_t fsk_ctx_launch_count(const fsk_ctx* ctx); /* kernels launched by this ctx so far */
+int fsk_device_sm_count(const fsk_ctx* ctx);
+
+/* Measurement hooks (bench.py): when profiling is on, every kernel launch of the context is
+ * bracketed by CUDA events on its stream; fsk_ctx_prof_read synchronizes and returns the
+ * summed device time and launch count of the kernels named `name` (NULL = all), and
+ * recycles the events when `reset` != 0. fsk_measure_fp32_peak times an FFMA-chain kernel
+ * over all SMs (the FP32 roofline denominator) and returns TFLOP/s. */
+int fsk_ctx_set_profiling(fsk_ctx* ctx, int on);
+int fsk_ctx_prof_read(fsk_ctx* ctx, const char* name, double* total_ms, int64_t* count, int reset);
+int fsk_measure_fp32_peak(fsk_ctx* ctx, double* tflops);
+
+/* SearchOptions::defaults_for (correspondence.cpp:10-17): conv 1e-5*diag,
+ * div 0.5*diag, dedup 1e-2*diag, max_iters 50. */
+fsk_search_opts fsk_search_opts_defaults(const fsk_grid_desc* desc);
+
+/* ---- K1: precompute_transform_grid (deformer.hpp:53-55; deformer.cpp:61-77) -------
+ * tgrid[v] = lbs_blend(weights[v], bones) (deformer.cpp:9-19). n_bones_pose must equal
+ * desc->n_bones ("precompute_transform_grid: bone count mismatch"). All dev. */
+int fsk_precompute_tgrid(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* desc,
+                         const float* bones, int32_t n_bones_pose, float* tgrid, void* stream);
+
+/* ---- K2: batch_search, voxel variant (correspondence.hpp:77-80; correspondence.cpp:178-192)
+ * One Broyden solve per (point, bone-init): x0 = B_i^-1 x' (:135), J~0 from the analytic
+ * grid Jacobian (:43-54), good-Broyden iterate (:97-124), converged mask, then dedup
+ * (:162-176) when out->keep != NULL. points, tgrid, bones dev. N may be 0. */
+int fsk_search_fwd(fsk_ctx* ctx, const float* tgrid, const fsk_grid_desc* desc,
+                   const float* bones, int32_t n_bones_pose, const float* points, int64_t n,
+                   const fsk_search_opts* opts, fsk_search_out* out, void* stream);
+
+/* Stream-compaction of the kept roots into CorrespondenceSet form: offsets [N+1] int64
+ * (dev), roots [total] fsk_root (dev, capacity `cap` records). *total_out (host) receives
+ * the number of kept roots; this call synchronizes `stream` to read it. Returns FSK_EINVAL
+ * if cap is too small (roots untouched, *total_out still set). */
+int fsk_compact_roots(fsk_ctx* ctx, const fsk_search_out* dense, int64_t n, int32_t n_init,
+                      int64_t* offsets, fsk_root* roots, int64_t cap, int64_t* total_out,
+                      void* stream);
+
+/* End-to-end host-buffer entry point (what cmd_deform / cmd_bench do per frame,
+ * fskin_cli.cpp:395-408, :663-678): H2D of weights, bones and points, K1, K2, dedup,
+ * compaction and D2H of the CorrespondenceSets. All pointers are HOST memory (pinned
+ * recommended). offsets [N+1]; roots capacity `cap`. Synchronous. */
+int fsk_deform_host(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* desc,
+                    const float* bones, int32_t n_bones_pose, const float* points, int64_t n,
+                    const fsk_search_opts* opts, int64_t* offsets, fsk_root* roots, int64_t cap,
+                    int64_t* total_out, void* stream);
+
+/* ---- point evaluators (batch forms of trilerp_transform / forward_deform /
+ * deform_jacobian, deformer.hpp:59-68): at points x [N][3] (dev) write T(x) [N][12],
+ * d(x) [N][3] and the analytic Jacobian dd/dx [N][9] (transform-grid form).
+ * Any output may be NULL. */
+int fsk_eval_points(fsk_ctx* ctx, const float* tgrid, const fsk_grid_desc* desc,
+                    const float* x, int64_t n, float* t12, float* d, float* jac, void* stream);
+
+/* init_states (correspondence.hpp:62-63; correspondence.cpp:58-70): for every (point, bone)
+ * x0 [N][n_b][3] = B_i^-1 x' and jinv0 [N][n_b][9] = J(x0)^-1, or I when |det J| < 1e-8.
+ * Either output may be NULL. */
+int fsk_init_states(fsk_ctx* ctx, const float* tgrid, const fsk_grid_desc* desc, const float* bones,
+                    int32_t n_bones_pose, const float* points, int64_t n, float* x0, float* jinv0,
+                    void* stream);
+
+/* ---- K3: implicit-differentiation backward (diff.cpp:43-51, :336-359), grid-routed.
+ * For each point p with root_sel[p] >= 0 (init index into the dense result), with
+ * v = grad_xc[p] (dL/dx*), u = -J~^T v and x* = x_c[p][sel]:
+ *    grad_tgrid[c] += phi_c(x*) * u (x*,1)^T        (3x4, 8 corners c of locate_cell(x*))
+ * grad_tgrid [V][12] dev is OVERWRITTEN (zeroed first). deterministic != 0 selects the
+ * bitwise-reproducible int64 fixed-point accumulation; 0 = float vector atomics. */
+int fsk_search_bwd(fsk_ctx* ctx, const fsk_grid_desc* desc, const float* x_c, const float* jinv,
+                   int32_t n_init, const float* grad_xc, const int32_t* root_sel, int64_t n,
+                   float* grad_tgrid, int deterministic, void* stream);
+
+/* dL/dw[v][i] = <dL/dT[v], B_i>_F  (chain rule through deformer.cpp:70-74). [V][n_b] dev. */
+int fsk_grad_weights(fsk_ctx* ctx, const fsk_grid_desc* desc, const float* grad_tgrid,
+                     const float* bones, int32_t n_bones_pose, float* grad_w, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FSK_H_ */

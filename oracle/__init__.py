@@ -1,0 +1,155 @@
+"""ctypes wrapper of the CPU oracle (``oracle/liboracle.so``).
+
+TEST INFRASTRUCTURE ONLY: imported by ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s CPU-baseline / ``--impl reference`` leg — never by the product package.
+See ``fskin_oracle.cpp`` for the reference lines each function restates and for the
+parity status ("parity unpinned" against reference outputs: the reference cannot be
+built here; pinned by SPEC.md known answers).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+_d = ctypes.POINTER(ctypes.c_double)
+_u8 = ctypes.POINTER(ctypes.c_uint8)
+_i32 = ctypes.POINTER(ctypes.c_int32)
+_i64 = ctypes.c_int64
+_int = ctypes.c_int
+
+
+def build(force: bool = False) -> str:
+    src = os.path.join(_HERE, "fskin_oracle.cpp")
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(src):
+        subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    return _LIB
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        L.orc_last_error.restype = ctypes.c_char_p
+        L.orc_precompute_tgrid.argtypes = [_d, _int, _int, _int, _int, _d, _d, _int, _d, _int]
+        L.orc_lbs_blend.argtypes = [_d, _d, _int, _int, _d]
+        L.orc_eval_points.argtypes = [_d, _int, _int, _int, _int, _d, _d, _d, _d, _i64, _d, _d, _d, _d, _d, _d]
+        L.orc_init_states.argtypes = [_d, _int, _int, _int, _int, _d, _d, _int, _d, _i64, _d, _d]
+        L.orc_batch_search.argtypes = [_d, _int, _int, _int, _int, _d, _d, _d, _int, _d, _i64, _int,
+                                       ctypes.c_double, ctypes.c_double, ctypes.c_double, _int,
+                                       _d, _d, _d, _i32, _u8, _u8]
+        L.orc_dedup_roots.argtypes = [_d, _int, ctypes.c_double, _u8]
+        L.orc_grid_vjp.argtypes = [_int, _int, _int, _int, _d, _d, _d, _d, _d, _i32, _i64, _d, _d]
+        L.orc_implicit_u_exact.argtypes = [_d, _int, _int, _int, _int, _d, _d, _d, _d, _i64, _d, _u8]
+        _lib = L
+    return _lib
+
+
+class OracleError(Exception):
+    pass
+
+
+class OracleInvalidArgument(OracleError, ValueError):
+    pass
+
+
+def _check(rc):
+    if rc != 0:
+        msg = lib().orc_last_error().decode()
+        raise (OracleInvalidArgument if rc == 1 else OracleError)(msg)
+
+
+def _p(a, t=_d):
+    return None if a is None else a.ctypes.data_as(t)
+
+
+def _f64(a):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def precompute_transform_grid(weights, dims, bbox, bones, workers=1):
+    """deformer.cpp:61-77 → tgrid [V,12] float64."""
+    w, bb, B = _f64(weights), _f64(bbox), _f64(bones).reshape(-1, 12)
+    nx, ny, nz = dims
+    nb = w.shape[1] if w.ndim == 2 else B.shape[0]
+    out = np.zeros((nx * ny * nz, 12))
+    _check(lib().orc_precompute_tgrid(_p(w), nx, ny, nz, nb, _p(bb), _p(B), B.shape[0], _p(out), workers))
+    return out
+
+
+def lbs_blend(weights, bones):
+    w, B = _f64(weights), _f64(bones).reshape(-1, 12)
+    out = np.zeros(12)
+    _check(lib().orc_lbs_blend(_p(w), _p(B), B.shape[0], w.shape[0], _p(out)))
+    return out
+
+
+def eval_points(weights, dims, bbox, bones, tgrid, x):
+    """Batched trilerp_weights, weight_spatial_gradient, trilerp_transform,
+    forward_deform (tgrid and weight-grid forms) and deform_jacobian at points x."""
+    w, bb, B, x = _f64(weights), _f64(bbox), _f64(bones).reshape(-1, 12), _f64(x).reshape(-1, 3)
+    tg = _f64(tgrid) if tgrid is not None else precompute_transform_grid(w, dims, bb, B)
+    n, nb = x.shape[0], B.shape[0]
+    out = dict(weights=np.zeros((n, nb)), wgrad=np.zeros((n, nb, 3)), t12=np.zeros((n, 12)),
+               d_tgrid=np.zeros((n, 3)), d_grid=np.zeros((n, 3)), jac=np.zeros((n, 3, 3)))
+    _check(lib().orc_eval_points(_p(w), *dims, nb, _p(bb), _p(B), _p(tg), _p(x), n,
+                                 *[_p(out[k]) for k in ("weights", "wgrad", "t12", "d_tgrid", "d_grid", "jac")]))
+    return out
+
+
+def init_states(weights, dims, bbox, bones, x_prime):
+    w, bb, B, x = _f64(weights), _f64(bbox), _f64(bones).reshape(-1, 12), _f64(x_prime).reshape(-1, 3)
+    n, nb = x.shape[0], B.shape[0]
+    x0, j0 = np.zeros((n, nb, 3)), np.zeros((n, nb, 3, 3))
+    _check(lib().orc_init_states(_p(w), *dims, w.shape[1], _p(bb), _p(B), nb, _p(x), n, _p(x0), _p(j0)))
+    return x0, j0
+
+
+def batch_search(weights, dims, bbox, bones, x_prime, max_iters, conv_eps, div_eps, dedup_dist,
+                 workers=1, tgrid=None):
+    """correspondence.cpp:178-192 with per-(point, init) dense outputs."""
+    w, bb, B, x = _f64(weights), _f64(bbox), _f64(bones).reshape(-1, 12), _f64(x_prime).reshape(-1, 3)
+    tg = _f64(tgrid) if tgrid is not None else precompute_transform_grid(w, dims, bb, B, workers)
+    n, nb = x.shape[0], B.shape[0]
+    out = dict(x_c=np.zeros((n, nb, 3)), jinv=np.zeros((n, nb, 3, 3)), resid=np.zeros((n, nb)),
+               iters=np.zeros((n, nb), np.int32), converged=np.zeros((n, nb), np.uint8),
+               keep=np.zeros((n, nb), np.uint8))
+    _check(lib().orc_batch_search(_p(w), *dims, w.shape[1], _p(bb), _p(tg), _p(B), nb, _p(x), n,
+                                  int(max_iters), conv_eps, div_eps, dedup_dist, workers,
+                                  _p(out["x_c"]), _p(out["jinv"]), _p(out["resid"]), _p(out["iters"], _i32),
+                                  _p(out["converged"], _u8), _p(out["keep"], _u8)))
+    return out
+
+
+def dedup_roots(xs, dedup_dist):
+    xs = _f64(xs).reshape(-1, 3)
+    keep = np.zeros(xs.shape[0], np.uint8)
+    _check(lib().orc_dedup_roots(_p(xs), xs.shape[0], dedup_dist, _p(keep, _u8)))
+    return keep
+
+
+def grid_vjp(dims, bbox, bones, x_star, jinv, v, sel=None, n_bones=None):
+    bb, B = _f64(bbox), _f64(bones).reshape(-1, 12)
+    xs, J, v = _f64(x_star).reshape(-1, 3), _f64(jinv).reshape(-1, 9), _f64(v).reshape(-1, 3)
+    n, nb = xs.shape[0], B.shape[0]
+    V = dims[0] * dims[1] * dims[2]
+    gT, gw = np.zeros((V, 12)), np.zeros((V, nb))
+    s = None if sel is None else np.ascontiguousarray(sel, dtype=np.int32)
+    _check(lib().orc_grid_vjp(*dims, nb, _p(bb), _p(B), _p(xs), _p(J), _p(v), _p(s, _i32), n, _p(gT), _p(gw)))
+    return gT, gw
+
+
+def implicit_u_exact(weights, dims, bbox, bones, x_star, v):
+    w, bb, B = _f64(weights), _f64(bbox), _f64(bones).reshape(-1, 12)
+    xs, v = _f64(x_star).reshape(-1, 3), _f64(v).reshape(-1, 3)
+    n = xs.shape[0]
+    u, ok = np.zeros((n, 3)), np.zeros(n, np.uint8)
+    _check(lib().orc_implicit_u_exact(_p(w), *dims, w.shape[1], _p(bb), _p(B), _p(xs), _p(v), n, _p(u), _p(ok, _u8)))
+    return u, ok

@@ -1,0 +1,257 @@
+"""Python host mirror of the reference deformer/correspondence API over the C-ABI.
+
+Names, argument meaning and error behaviour follow
+``proj/include/fskin/deformer.hpp`` and ``correspondence.hpp``; tensors are torch CUDA
+tensors (float32) resident on the context's device. All compute goes through
+``libfsk_b200.so`` (``include/fsk.h``) — there is no CPU path: without the library or
+an sm_100 GPU every call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import FskError, FskInvalidArgument, GridDesc, SearchOpts, SearchOut, check  # noqa: F401
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _stream(device):
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+@dataclass
+class GridDims:
+    """``GridDims`` (skinning.hpp:45-52)."""
+    nx: int = 64
+    ny: int = 64
+    nz: int = 16
+
+    def vertex_count(self) -> int:
+        return self.nx * self.ny * self.nz
+
+
+@dataclass
+class SearchOptions:
+    """``SearchOptions`` (correspondence.hpp:14-26)."""
+    max_iters: int = 50
+    conv_eps: float = 1e-5
+    div_eps: float = 0.5
+    dedup_dist: float = 1e-2
+    sort: bool = True  # spatial ordering of queries (performance only)
+
+    @staticmethod
+    def defaults_for(bbox) -> "SearchOptions":
+        """``SearchOptions::defaults_for`` (correspondence.cpp:10-17)."""
+        lo, hi = [float(v) for v in bbox[:3]], [float(v) for v in bbox[3:]]
+        diag = math.sqrt(sum((h - l) ** 2 for l, h in zip(lo, hi)))
+        return SearchOptions(50, 1e-5 * diag, 0.5 * diag, 1e-2 * diag)
+
+    def validate(self) -> None:
+        """``SearchOptions::validate`` (correspondence.cpp:19-25)."""
+        if self.max_iters < 1:
+            raise FskInvalidArgument("search: max_iters must be >= 1")
+        if not self.conv_eps > 0.0:
+            raise FskInvalidArgument("search: conv_eps must be > 0")
+        if not self.div_eps > self.conv_eps:
+            raise FskInvalidArgument("search: div_eps must exceed conv_eps")
+        if not self.dedup_dist >= 0.0:
+            raise FskInvalidArgument("search: dedup_dist must be >= 0")
+
+    def c(self) -> SearchOpts:
+        return SearchOpts(int(self.max_iters), float(self.conv_eps), float(self.div_eps), float(self.dedup_dist),
+                          0 if self.sort else _lib.FSK_SEARCH_NO_SORT)
+
+
+def grid_desc(dims, bbox, n_bones) -> GridDesc:
+    d = GridDesc()
+    d.nx, d.ny, d.nz = (int(v) for v in dims)
+    d.n_bones = int(n_bones)
+    for a in range(3):
+        d.bbox_min[a] = float(bbox[a])
+        d.bbox_max[a] = float(bbox[3 + a])
+    return d
+
+
+def _f32(t, name, device):
+    if not isinstance(t, torch.Tensor):
+        raise FskInvalidArgument(f"fsk: {name} must be a torch tensor")
+    if t.device != device or t.dtype != torch.float32 or not t.is_contiguous():
+        raise FskInvalidArgument(f"fsk: {name} must be a contiguous float32 tensor on {device}")
+    return t
+
+
+class Deformer:
+    """One context (``fsk_ctx``) on one GPU. The methods mirror the reference free
+    functions; results are dense per-(point, init) tensors plus dedup masks."""
+
+    def __init__(self, device=0):
+        self.L = _lib.load()
+        self.device = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
+        self._ctx = ctypes.c_void_p()
+        check(self.L.fsk_ctx_create(self.device.index or 0, ctypes.byref(self._ctx)))
+
+    def close(self):
+        if self._ctx:
+            self.L.fsk_ctx_destroy(self._ctx)
+            self._ctx = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def launch_count(self) -> int:
+        return int(self.L.fsk_ctx_launch_count(self._ctx))
+
+    @property
+    def sm_count(self) -> int:
+        return int(self.L.fsk_device_sm_count(self._ctx))
+
+    # ---------------------------------------------------------------- measurement hooks
+    def set_profiling(self, on: bool) -> None:
+        check(self.L.fsk_ctx_set_profiling(self._ctx, 1 if on else 0))
+
+    def prof_read(self, name=None, reset=True):
+        """(total device ms, launches) of this context's kernels named ``name`` (None = all)."""
+        ms, cnt = ctypes.c_double(), ctypes.c_int64()
+        check(self.L.fsk_ctx_prof_read(self._ctx, name.encode() if name else None, ctypes.byref(ms),
+                                       ctypes.byref(cnt), 1 if reset else 0))
+        return ms.value, cnt.value
+
+    def measure_fp32_peak(self) -> float:
+        t = ctypes.c_double()
+        check(self.L.fsk_measure_fp32_peak(self._ctx, ctypes.byref(t)))
+        return t.value
+
+    # ---------------------------------------------------------------- K1
+    def precompute_transform_grid(self, weights, dims, bbox, bones, out=None):
+        """``precompute_transform_grid`` (deformer.hpp:53-55) → tgrid [V,12] float32."""
+        weights = _f32(weights, "weights", self.device)
+        bones = _f32(bones, "bones", self.device)
+        nb = weights.shape[1] if weights.dim() == 2 else bones.shape[0]
+        desc = grid_desc(dims, bbox, nb)
+        V = desc.nx * desc.ny * desc.nz
+        if out is None:
+            out = torch.empty((V, 12), dtype=torch.float32, device=self.device)
+        check(self.L.fsk_precompute_tgrid(self._ctx, _ptr(weights), ctypes.byref(desc), _ptr(bones),
+                                          bones.numel() // 12, _ptr(out), _stream(self.device)))
+        return out
+
+    # ---------------------------------------------------------------- K2 + dedup
+    def alloc_search_out(self, n, nb, jinv=True, resid=True, iters=True, keep=True):
+        dev = self.device
+        return dict(
+            x_c=torch.empty((n, nb, 3), dtype=torch.float32, device=dev),
+            jinv=torch.empty((n, nb, 3, 3), dtype=torch.float32, device=dev) if jinv else None,
+            resid=torch.empty((n, nb), dtype=torch.float32, device=dev) if resid else None,
+            iters=torch.empty((n, nb), dtype=torch.uint8, device=dev) if iters else None,
+            converged=torch.empty((n, nb), dtype=torch.uint8, device=dev),
+            keep=torch.empty((n, nb), dtype=torch.uint8, device=dev) if keep else None,
+            n_roots=torch.empty((n,), dtype=torch.int32, device=dev) if keep else None,
+        )
+
+    @staticmethod
+    def _c_out(o) -> SearchOut:
+        return SearchOut(*[o[k].data_ptr() if o.get(k) is not None else None
+                           for k in ("x_c", "jinv", "resid", "iters", "converged", "keep", "n_roots")])
+
+    def batch_search(self, tgrid, dims, bbox, bones, points, opts: SearchOptions, out=None):
+        """``batch_search`` voxel variant (correspondence.hpp:77-80) → dense per-(point, init)
+        results: x_c, jinv, resid, iters, converged, keep (dedup), n_roots."""
+        tgrid = _f32(tgrid, "tgrid", self.device)
+        bones = _f32(bones, "bones", self.device)
+        points = _f32(points, "points", self.device)
+        nb = bones.numel() // 12
+        n = points.shape[0]
+        desc = grid_desc(dims, bbox, nb)
+        if out is None:
+            out = self.alloc_search_out(n, nb)
+        co = self._c_out(out)
+        check(self.L.fsk_search_fwd(self._ctx, _ptr(tgrid), ctypes.byref(desc), _ptr(bones), nb, _ptr(points), n,
+                                    ctypes.byref(opts.c()), ctypes.byref(co), _stream(self.device)))
+        return out
+
+    def compact_roots(self, dense, n, nb):
+        """Kept roots in CorrespondenceSet form: (offsets [N+1] int64, roots [M,16] float32 view of
+        fsk_root records: x(3), residual, J~(9), bone, iterations, pad)."""
+        offsets = torch.empty((n + 1,), dtype=torch.int64, device=self.device)
+        cap = int(dense["n_roots"].sum().item()) if n else 0
+        roots = torch.empty((max(cap, 1), 16), dtype=torch.float32, device=self.device)
+        total = ctypes.c_int64()
+        co = self._c_out(dense)
+        check(self.L.fsk_compact_roots(self._ctx, ctypes.byref(co), n, nb, _ptr(offsets), _ptr(roots), cap,
+                                       ctypes.byref(total), _stream(self.device)))
+        return offsets, roots[: total.value]
+
+    def init_states(self, tgrid, dims, bbox, bones, points):
+        """``init_states`` (correspondence.hpp:62-63) → x0 [N,nb,3], J~0 [N,nb,3,3]."""
+        nb = bones.numel() // 12
+        n = points.shape[0]
+        desc = grid_desc(dims, bbox, nb)
+        x0 = torch.empty((n, nb, 3), dtype=torch.float32, device=self.device)
+        j0 = torch.empty((n, nb, 3, 3), dtype=torch.float32, device=self.device)
+        check(self.L.fsk_init_states(self._ctx, _ptr(_f32(tgrid, "tgrid", self.device)), ctypes.byref(desc),
+                                     _ptr(_f32(bones, "bones", self.device)), nb,
+                                     _ptr(_f32(points, "points", self.device)), n, _ptr(x0), _ptr(j0),
+                                     _stream(self.device)))
+        return x0, j0
+
+    def eval_points(self, tgrid, dims, bbox, n_bones, x):
+        """Batched ``trilerp_transform`` / ``forward_deform`` / ``deform_jacobian``
+        (deformer.hpp:59-68): (T [N,12], d [N,3], J [N,3,3])."""
+        n = x.shape[0]
+        desc = grid_desc(dims, bbox, n_bones)
+        t12 = torch.empty((n, 12), dtype=torch.float32, device=self.device)
+        d = torch.empty((n, 3), dtype=torch.float32, device=self.device)
+        J = torch.empty((n, 3, 3), dtype=torch.float32, device=self.device)
+        check(self.L.fsk_eval_points(self._ctx, _ptr(_f32(tgrid, "tgrid", self.device)), ctypes.byref(desc),
+                                     _ptr(_f32(x, "x", self.device)), n, _ptr(t12), _ptr(d), _ptr(J),
+                                     _stream(self.device)))
+        return t12, d, J
+
+    # ---------------------------------------------------------------- K3 + GW
+    def search_bwd(self, dims, bbox, n_bones, dense, grad_xc, root_sel, deterministic=False, out=None):
+        """Implicit-differentiation backward (diff.cpp:43-51, :336-359), grid-routed:
+        dL/dT [V,12] from per-point cotangents dL/dx* and the selected root per point."""
+        desc = grid_desc(dims, bbox, n_bones)
+        V = desc.nx * desc.ny * desc.nz
+        n = grad_xc.shape[0]
+        if out is None:
+            out = torch.empty((V, 12), dtype=torch.float32, device=self.device)
+        rs = root_sel.to(device=self.device, dtype=torch.int32).contiguous()
+        check(self.L.fsk_search_bwd(self._ctx, ctypes.byref(desc), _ptr(dense["x_c"]), _ptr(dense["jinv"]),
+                                    dense["x_c"].shape[1], _ptr(_f32(grad_xc, "grad_xc", self.device)), _ptr(rs), n,
+                                    _ptr(out), 1 if deterministic else 0, _stream(self.device)))
+        return out
+
+    def grad_weights(self, dims, bbox, grad_tgrid, bones, out=None):
+        """dL/dw [V, n_b] = <dL/dT_v, B_i>_F."""
+        nb = bones.numel() // 12
+        desc = grid_desc(dims, bbox, nb)
+        V = desc.nx * desc.ny * desc.nz
+        if out is None:
+            out = torch.empty((V, nb), dtype=torch.float32, device=self.device)
+        check(self.L.fsk_grad_weights(self._ctx, ctypes.byref(desc), _ptr(_f32(grad_tgrid, "grad_tgrid", self.device)),
+                                      _ptr(_f32(bones, "bones", self.device)), nb, _ptr(out), _stream(self.device)))
+        return out
+
+    # ---------------------------------------------------------------- end to end (host buffers)
+    def deform_host(self, weights, dims, bbox, bones, points, opts: SearchOptions, offsets, roots):
+        """``fsk_deform_host``: host (pinned) buffers in, CorrespondenceSets out. Returns the
+        number of kept roots written into ``roots`` (a [cap,16] float32 pinned tensor)."""
+        nb = bones.numel() // 12
+        desc = grid_desc(dims, bbox, nb)
+        total = ctypes.c_int64()
+        check(self.L.fsk_deform_host(self._ctx, _ptr(weights), ctypes.byref(desc), _ptr(bones), nb, _ptr(points),
+                                     points.shape[0], ctypes.byref(opts.c()), _ptr(offsets), _ptr(roots),
+                                     roots.shape[0], ctypes.byref(total), _stream(self.device)))
+        return total.value

@@ -1,0 +1,282 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on identical f32 inputs.
+
+North-star bar (BASELINE.json): converged-mask agreement >= 99.99 % per (point, init);
+canonical positions and gradients within 1e-4 abs (FP32).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2211_15601_b200 import synthetic as S
+from paper_2211_15601_b200.deformer import FskInvalidArgument, SearchOptions
+
+pytestmark = pytest.mark.gpu
+
+TOL_X = 1e-4        # canonical positions, abs (north star)
+TOL_GRAD = 1e-4     # gradients, abs (north star)
+MASK_AGREE = 0.9999  # converged-mask agreement (north star)
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def opts_of(sc, max_iters):
+    return SearchOptions(max_iters=max_iters, **{k: v for k, v in sc.search_options(max_iters).items() if k != "max_iters"})
+
+
+def run_gpu(deformer, sc, max_iters, sort=True):
+    w, B, x = dev(sc.weights), dev(sc.bones), dev(sc.points)
+    tg = deformer.precompute_transform_grid(w, sc.dims, sc.bbox, B)
+    o = opts_of(sc, max_iters)
+    o.sort = sort
+    out = deformer.batch_search(tg, sc.dims, sc.bbox, B, x, o)
+    torch.cuda.synchronize()
+    return tg, {k: (v.cpu().numpy() if v is not None else None) for k, v in out.items()}
+
+
+def run_oracle(sc, max_iters):
+    return oracle.batch_search(sc.weights, sc.dims, sc.bbox, sc.bones, sc.points, workers=8,
+                               **sc.search_options(max_iters))
+
+
+@pytest.fixture(scope="module")
+def c1():
+    """Config 1 (BASELINE.json configs[0]): 24-bone SMPL-like, 32^3 grid, 10k points, max 10 iters."""
+    return S.make_scene((32, 32, 32), 10_000, seed=1)
+
+
+def test_precompute_tgrid_matches_oracle(deformer, c1):
+    w, B = dev(c1.weights), dev(c1.bones)
+    tg = deformer.precompute_transform_grid(w, c1.dims, c1.bbox, B).cpu().numpy()
+    ref = oracle.precompute_transform_grid(c1.weights, c1.dims, c1.bbox, c1.bones)
+    assert np.abs(tg - ref).max() < 2e-6
+
+
+def test_eval_points_matches_oracle(deformer, c1):
+    w, B = dev(c1.weights), dev(c1.bones)
+    tg = deformer.precompute_transform_grid(w, c1.dims, c1.bbox, B)
+    rng = np.random.default_rng(0)
+    lo, hi = c1.bbox[:3].astype(float), c1.bbox[3:].astype(float)
+    x = (lo - 0.1 + rng.random((4000, 3)) * (hi - lo + 0.2)).astype(np.float32)
+    t12, d, J = (t.cpu().numpy() for t in deformer.eval_points(tg, c1.dims, c1.bbox, c1.n_bones, dev(x)))
+    ref = oracle.eval_points(c1.weights, c1.dims, c1.bbox, c1.bones, None, x)
+    assert np.abs(t12 - ref["t12"]).max() < 2e-6
+    assert np.abs(d - ref["d_tgrid"]).max() < 5e-6
+    # J from the 12-wide transform grid (A.3) vs the reference's 24-wide weight-grid form
+    assert np.abs(J - ref["jac"]).max() < 5e-5
+
+
+def test_init_states_match_oracle(deformer, c1):
+    sc = S.make_scene((32, 32, 32), 500, seed=2)
+    w, B, x = dev(sc.weights), dev(sc.bones), dev(sc.points)
+    tg = deformer.precompute_transform_grid(w, sc.dims, sc.bbox, B)
+    x0, j0 = (t.cpu().numpy() for t in deformer.init_states(tg, sc.dims, sc.bbox, B, x))
+    rx0, rj0 = oracle.init_states(sc.weights, sc.dims, sc.bbox, sc.bones, sc.points)
+    assert np.abs(x0 - rx0).max() < 5e-6
+    rel = np.abs(j0 - rj0).max(axis=(2, 3)) / np.maximum(1.0, np.abs(rj0).max(axis=(2, 3)))
+    assert np.quantile(rel, 0.9999) < 1e-3
+
+
+def _parity(g, r, conv_eps):
+    agree = (g["converged"] == r["converged"]).mean()
+    both = (g["converged"] == 1) & (r["converged"] == 1)
+    dx = np.abs(g["x_c"] - r["x_c"])[both].max() if both.any() else 0.0
+    dj = np.abs(g["jinv"] - r["jinv"].reshape(g["jinv"].shape))[both].max() if both.any() else 0.0
+    keep_agree = (g["keep"] == r["keep"]).mean()
+    return agree, dx, dj, keep_agree, both
+
+
+def test_search_config1_parity(deformer, c1):
+    _, g = run_gpu(deformer, c1, 10)
+    r = run_oracle(c1, 10)
+    agree, dx, dj, keep_agree, both = _parity(g, r, c1.search_options(10)["conv_eps"])
+    print(f"\nC1 mask agreement {agree:.6f}  keep agreement {keep_agree:.6f}  max|dx| {dx:.3e}  max|dJ~| {dj:.3e}")
+    assert agree >= MASK_AGREE
+    assert dx <= TOL_X
+    assert keep_agree >= MASK_AGREE
+    # Broyden iteration counts agree wherever both converged, except trajectories that
+    # sit on the conv_eps boundary
+    assert (g["iters"][both] == r["iters"][both]).mean() > 0.999
+    # Root residual: the FP32 re-evaluation is sound (< conv_eps)
+    assert (g["resid"][g["converged"] == 1] < c1.search_options(10)["conv_eps"]).all()
+
+
+@pytest.mark.parametrize("seed,points", [(3, "uniform"), (4, "training")])
+def test_search_default_iters_parity(deformer, seed, points):
+    """Reference default max_iters=50 (C2 shape at oracle-friendly size), uniform and
+    training-shaped (half near-surface) point mixes."""
+    sc = S.make_scene((32, 32, 32), 8000, seed=seed, points=points)
+    _, g = run_gpu(deformer, sc, 50)
+    r = run_oracle(sc, 50)
+    agree, dx, dj, keep_agree, _ = _parity(g, r, sc.search_options(50)["conv_eps"])
+    print(f"\n{points} mask agreement {agree:.6f}  keep {keep_agree:.6f}  max|dx| {dx:.3e}  max|dJ~| {dj:.3e}")
+    assert agree >= MASK_AGREE
+    assert dx <= TOL_X
+
+
+def test_search_64_grid_parity(deformer):
+    sc = S.make_scene((64, 64, 16), 4000, seed=5, pose="bench")
+    _, g = run_gpu(deformer, sc, 50)
+    r = run_oracle(sc, 50)
+    agree, dx, _, keep_agree, _ = _parity(g, r, sc.search_options(50)["conv_eps"])
+    assert agree >= MASK_AGREE
+    assert dx <= TOL_X
+
+
+def test_search_is_order_independent_and_deterministic(deformer, c1):
+    _, a = run_gpu(deformer, c1, 50, sort=True)
+    _, b = run_gpu(deformer, c1, 50, sort=False)
+    _, c = run_gpu(deformer, c1, 50, sort=True)
+    for k in a:
+        np.testing.assert_array_equal(a[k], b[k])
+        np.testing.assert_array_equal(a[k], c[k])
+
+
+def test_identity_pose_roots_equal_queries(deformer):
+    sc = S.make_scene((16, 16, 16), 1000, seed=6, pose="rest")
+    lo, hi = sc.bbox[:3].astype(float), sc.bbox[3:].astype(float)
+    sc.points = (lo + np.random.default_rng(0).random((1000, 3)) * (hi - lo)).astype(np.float32)
+    _, g = run_gpu(deformer, sc, 50)
+    assert (g["n_roots"] == 1).all()
+    kept = g["x_c"][g["keep"] == 1]
+    np.testing.assert_allclose(kept, sc.points, atol=1e-5 * sc.diag)
+    assert g["iters"][g["keep"] == 1].max() <= 1
+
+
+def test_single_rigid_bone_exact_inverse(deformer):
+    rng = np.random.default_rng(12)
+    T = S.about_axis(np.array([0.1, 0.2, 0.3]), np.array([0.3, 1.0, 0.2]), 0.7)
+    dims, bbox = (6, 7, 5), np.array([0, 0, 0, 1, 2, 0.5], np.float32)
+    w = np.ones((6 * 7 * 5, 1), np.float32)
+    y = (bbox[:3] + rng.random((200, 3)) * (bbox[3:] - bbox[:3])).astype(np.float32)
+    xp = S.apply(T, y.astype(float)).astype(np.float32)
+    sc = S.Scene(dims, bbox, w, T.reshape(1, 12).astype(np.float32), xp, np.zeros(1),
+                 float(np.linalg.norm(bbox[3:] - bbox[:3])))
+    _, g = run_gpu(deformer, sc, 50)
+    assert g["keep"].all()
+    np.testing.assert_allclose(g["x_c"][:, 0], y, atol=1e-5 * sc.diag)
+
+
+def test_empty_and_validation(deformer, c1):
+    w, B = dev(c1.weights), dev(c1.bones)
+    tg = deformer.precompute_transform_grid(w, c1.dims, c1.bbox, B)
+    out = deformer.batch_search(tg, c1.dims, c1.bbox, B, torch.zeros((0, 3), device="cuda"), opts_of(c1, 10))
+    assert out["x_c"].shape[0] == 0
+    x = dev(c1.points[:10])
+    for bad, msg in [(dict(max_iters=0), "search: max_iters must be >= 1"),
+                     (dict(conv_eps=0.0), "search: conv_eps must be > 0"),
+                     (dict(div_eps=1e-9), "search: div_eps must exceed conv_eps"),
+                     (dict(dedup_dist=-1.0), "search: dedup_dist must be >= 0")]:
+        o = opts_of(c1, 10)
+        for k, v in bad.items():
+            setattr(o, k, v)
+        with pytest.raises(FskInvalidArgument, match=msg):
+            deformer.batch_search(tg, c1.dims, c1.bbox, B, x, o)
+    with pytest.raises(FskInvalidArgument, match="precompute_transform_grid: bone count mismatch"):
+        deformer.precompute_transform_grid(w, c1.dims, c1.bbox, B[:-1].contiguous())
+    with pytest.raises(FskInvalidArgument, match="search: grid bone count mismatch"):
+        _mismatch(deformer, tg, c1, B, x)
+
+
+def _mismatch(deformer, tg, sc, B, x):
+    import ctypes
+
+    from paper_2211_15601_b200 import _lib
+    from paper_2211_15601_b200.deformer import _ptr, _stream, grid_desc
+    desc = grid_desc(sc.dims, sc.bbox, sc.n_bones)
+    out = deformer.alloc_search_out(x.shape[0], sc.n_bones)
+    co = deformer._c_out(out)
+    _lib.check(deformer.L.fsk_search_fwd(deformer._ctx, _ptr(tg), ctypes.byref(desc), _ptr(B), sc.n_bones - 1,
+                                         _ptr(x), x.shape[0], ctypes.byref(opts_of(sc, 10).c()), ctypes.byref(co),
+                                         _stream(deformer.device)))
+
+
+def test_compaction_and_host_entry_point(deformer, c1):
+    w, B, x = dev(c1.weights), dev(c1.bones), dev(c1.points)
+    tg = deformer.precompute_transform_grid(w, c1.dims, c1.bbox, B)
+    o = opts_of(c1, 50)
+    dense = deformer.batch_search(tg, c1.dims, c1.bbox, B, x, o)
+    offs, roots = deformer.compact_roots(dense, x.shape[0], c1.n_bones)
+    offs, roots = offs.cpu().numpy(), roots.cpu().numpy()
+    d = {k: v.cpu().numpy() for k, v in dense.items()}
+    assert offs[-1] == d["keep"].sum() == roots.shape[0]
+    keep = np.argwhere(d["keep"] == 1)  # point-major, bone order: same order as the compact list
+    np.testing.assert_array_equal(roots[:, :3], d["x_c"][keep[:, 0], keep[:, 1]])
+    np.testing.assert_array_equal(roots[:, 13].view(np.int32), keep[:, 1])
+    np.testing.assert_array_equal(np.diff(offs), d["n_roots"])
+    # end-to-end host-buffer entry point gives the same CorrespondenceSets
+    n = c1.points.shape[0]
+    hoffs = torch.empty(n + 1, dtype=torch.int64).pin_memory()
+    hroots = torch.empty((n * c1.n_bones, 16), dtype=torch.float32).pin_memory()
+    total = deformer.deform_host(torch.from_numpy(c1.weights).pin_memory(), c1.dims, c1.bbox,
+                                 torch.from_numpy(c1.bones).pin_memory(), torch.from_numpy(c1.points).pin_memory(),
+                                 o, hoffs, hroots)
+    assert total == roots.shape[0]
+    np.testing.assert_array_equal(hoffs.numpy(), offs)
+    np.testing.assert_array_equal(hroots[:total].numpy(), roots)
+
+
+# ------------------------------------------------------------------ backward (K3 + grad_weights)
+@pytest.fixture(scope="module")
+def c3(deformer):
+    """Config 3 shape at oracle size: forward, then a cotangent on the first kept root."""
+    sc = S.make_scene((32, 32, 32), 20_000, seed=8, points="training")
+    w, B, x = dev(sc.weights), dev(sc.bones), dev(sc.points)
+    tg = deformer.precompute_transform_grid(w, sc.dims, sc.bbox, B)
+    dense = deformer.batch_search(tg, sc.dims, sc.bbox, B, x, opts_of(sc, 50))
+    keep = dense["keep"].cpu().numpy()
+    sel = np.where(keep.any(1), np.argmax(keep, 1), -1).astype(np.int32)
+    n = sc.points.shape[0]
+    v = (np.random.default_rng(9).normal(size=(n, 3)) / n).astype(np.float32)  # loss-mean scaling (diff.cpp:331)
+    return sc, B, dense, sel, v
+
+
+def test_backward_matches_oracle_grid_vjp(deformer, c3):
+    sc, B, dense, sel, v = c3
+    gT = deformer.search_bwd(sc.dims, sc.bbox, sc.n_bones, dense, dev(v), dev(sel)).cpu().numpy()
+    gTd = deformer.search_bwd(sc.dims, sc.bbox, sc.n_bones, dense, dev(v), dev(sel), deterministic=True).cpu().numpy()
+    n = sel.shape[0]
+    ok = sel >= 0
+    xs = dense["x_c"].cpu().numpy()[np.arange(n), np.maximum(sel, 0)]
+    J = dense["jinv"].cpu().numpy()[np.arange(n), np.maximum(sel, 0)]
+    rT, rw = oracle.grid_vjp(sc.dims, sc.bbox, sc.bones, xs, J, v, sel=np.where(ok, sel, -1))
+    scale = np.abs(rT).max()
+    print(f"\nbwd max|dT| fast {np.abs(gT - rT).max():.3e}  det {np.abs(gTd - rT).max():.3e}  (max|T| {scale:.3e})")
+    assert np.abs(gT - rT).max() <= TOL_GRAD
+    assert np.abs(gTd - rT).max() <= TOL_GRAD
+    assert np.abs(gT - rT).max() <= 1e-4 * scale + 1e-9
+    gw = deformer.grad_weights(sc.dims, sc.bbox, dev(gTd), B).cpu().numpy()
+    assert np.abs(gw - rw).max() <= TOL_GRAD
+    assert np.abs(gw - rw).max() <= 1e-4 * np.abs(rw).max() + 1e-9
+
+
+def test_backward_deterministic_mode_is_bitwise_reproducible(deformer, c3):
+    sc, B, dense, sel, v = c3
+    a = deformer.search_bwd(sc.dims, sc.bbox, sc.n_bones, dense, dev(v), dev(sel), deterministic=True).cpu().numpy()
+    perm = np.random.default_rng(0).permutation(sel.shape[0])  # different accumulation order
+    dense_p = {k: (t[torch.from_numpy(perm).cuda()].contiguous() if t is not None else None) for k, t in dense.items()}
+    b = deformer.search_bwd(sc.dims, sc.bbox, sc.n_bones, dense_p, dev(v[perm]), dev(sel[perm]),
+                            deterministic=True).cpu().numpy()
+    np.testing.assert_array_equal(a, b)
+
+
+def test_backward_end_to_end_against_oracle_forward(deformer, c3):
+    """Whole-step parity: oracle forward + oracle grid VJP vs GPU forward + GPU backward."""
+    sc, B, dense, sel, v = c3
+    m = 4000
+    sub = S.Scene(sc.dims, sc.bbox, sc.weights, sc.bones, sc.points[:m], sc.angles, sc.diag)
+    r = run_oracle(sub, 50)
+    rsel = np.where(r["keep"].any(1), np.argmax(r["keep"], 1), -1).astype(np.int32)
+    xs = r["x_c"][np.arange(m), np.maximum(rsel, 0)]
+    J = r["jinv"][np.arange(m), np.maximum(rsel, 0)]
+    rT, _ = oracle.grid_vjp(sc.dims, sc.bbox, sc.bones, xs, J, v[:m], sel=rsel)
+    dsub = {k: (t[:m].contiguous() if t is not None else None) for k, t in dense.items()}
+    gsel = sel[:m]
+    gT = deformer.search_bwd(sc.dims, sc.bbox, sc.n_bones, dsub, dev(v[:m]), dev(gsel), deterministic=True)
+    gT = gT.cpu().numpy()
+    same = (rsel == gsel).mean()
+    print(f"\nselected-root agreement {same:.5f}  max|dT| {np.abs(gT - rT).max():.3e}")
+    assert same >= MASK_AGREE - 1e-3
+    assert np.abs(gT - rT).max() <= TOL_GRAD
