@@ -1,0 +1,549 @@
+// fskin_api.cpp — the reference's C++ deformer/correspondence API (include/fskin/*.hpp)
+// implemented over the C-ABI (include/fsk.h). Hot-path entry points convert f64 → f32,
+// run on the GPU and rebuild the reference's value types; errors are rethrown as the
+// reference's exception types with its message text (std::invalid_argument for FSK_EINVAL,
+// std::runtime_error otherwise). There is no CPU implementation of the search here.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "fsk.h"
+#include "fskin/correspondence.hpp"
+#include "fskin/deformer.hpp"
+#include "fskin/geometry.hpp"
+#include "fskin/skinning.hpp"
+
+namespace fskin {
+
+namespace {
+
+void check(int rc) {
+    if (rc == FSK_OK) return;
+    const std::string msg = fsk_last_error();
+    if (rc == FSK_EINVAL) throw std::invalid_argument(msg);
+    throw std::runtime_error(msg);
+}
+
+void cuda_ok(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+/// Per-thread context on device $FSKIN_DEVICE (default 0): fsk contexts are not thread-safe.
+struct ThreadCtx {
+    fsk_ctx* ctx = nullptr;
+    ThreadCtx() {
+        const char* d = std::getenv("FSKIN_DEVICE");
+        check(fsk_ctx_create(d ? std::atoi(d) : 0, &ctx));
+    }
+    ~ThreadCtx() {
+        if (ctx) fsk_ctx_destroy(ctx);
+    }
+};
+fsk_ctx* ctx() {
+    thread_local ThreadCtx t;
+    return t.ctx;
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    explicit DevBuf(size_t bytes) {
+        ctx();  // selects the device
+        cuda_ok(cudaMalloc(&p, bytes ? bytes : 16), "cudaMalloc");
+    }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    template <typename T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+void h2d(void* dst, const void* src, size_t bytes) {
+    if (bytes) cuda_ok(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice), "cudaMemcpy H2D");
+}
+void d2h(void* dst, const void* src, size_t bytes) {
+    if (bytes) cuda_ok(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost), "cudaMemcpy D2H");
+}
+
+fsk_grid_desc desc_of(const GridDims& d, const Aabb& bb, int nb) {
+    fsk_grid_desc g;
+    g.nx = d.nx;
+    g.ny = d.ny;
+    g.nz = d.nz;
+    g.n_bones = nb;
+    for (int a = 0; a < 3; ++a) {
+        g.bbox_min[a] = static_cast<float>(bb.min[a]);
+        g.bbox_max[a] = static_cast<float>(bb.max[a]);
+    }
+    return g;
+}
+
+std::vector<float> bones_f32(std::span<const RigidTransform> bones) {
+    std::vector<float> b(bones.size() * 12);
+    for (size_t i = 0; i < bones.size(); ++i)
+        for (int r = 0; r < 3; ++r) {
+            for (int c = 0; c < 3; ++c) b[i * 12 + r * 4 + c] = static_cast<float>(bones[i].rotation(r, c));
+            b[i * 12 + r * 4 + 3] = static_cast<float>(bones[i].translation[r]);
+        }
+    return b;
+}
+
+std::vector<float> points_f32(std::span<const Vec3> x) {
+    std::vector<float> p(x.size() * 3);
+    for (size_t i = 0; i < x.size(); ++i)
+        for (int a = 0; a < 3; ++a) p[3 * i + a] = static_cast<float>(x[i][a]);
+    return p;
+}
+
+// check_context (correspondence.cpp:29-41)
+void check_context(const SearchContext& c, SearchVariant variant) {
+    if (c.bones.empty()) throw std::invalid_argument("search: no bone transforms");
+    if (variant == SearchVariant::Mlp) {
+        throw std::invalid_argument("search: the MLP variant is not provided by fskin-b200 (voxel variant only)");
+    }
+    if (c.grid == nullptr || c.tgrid == nullptr)
+        throw std::invalid_argument("search: voxel variant needs skinning and transform grids");
+    if (static_cast<size_t>(c.grid->bone_count()) != c.bones.size())
+        throw std::invalid_argument("search: grid bone count mismatch");
+}
+
+fsk_search_opts c_opts(const SearchOptions& o) {
+    fsk_search_opts c;
+    c.max_iters = o.max_iters;
+    c.conv_eps = static_cast<float>(o.conv_eps);
+    c.div_eps = static_cast<float>(o.div_eps);
+    c.dedup_dist = static_cast<float>(o.dedup_dist);
+    c.flags = 0;
+    return c;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------ geometry
+RigidTransform RigidTransform::about_axis(const Vec3& pivot, const Vec3& axis, double angle) {
+    const double n = axis.norm();
+    if (n < 1e-12) throw std::invalid_argument("RigidTransform::about_axis: axis must be nonzero");
+    const Vec3 k = axis / n;
+    const double c = std::cos(angle), s = std::sin(angle), t = 1.0 - c;
+    Mat3 r;
+    r(0, 0) = c + t * k[0] * k[0];
+    r(0, 1) = t * k[0] * k[1] - s * k[2];
+    r(0, 2) = t * k[0] * k[2] + s * k[1];
+    r(1, 0) = t * k[1] * k[0] + s * k[2];
+    r(1, 1) = c + t * k[1] * k[1];
+    r(1, 2) = t * k[1] * k[2] - s * k[0];
+    r(2, 0) = t * k[2] * k[0] - s * k[1];
+    r(2, 1) = t * k[2] * k[1] + s * k[0];
+    r(2, 2) = c + t * k[2] * k[2];
+    return {r, pivot - r * pivot};
+}
+
+double point_segment_distance(const Vec3& p, const Vec3& a, const Vec3& b) {
+    const Vec3 ab = b - a;
+    const double len2 = ab.squaredNorm();
+    if (len2 < 1e-24) return (p - a).norm();
+    const double t = std::clamp((p - a).dot(ab) / len2, 0.0, 1.0);
+    return (p - (a + t * ab)).norm();
+}
+
+// ------------------------------------------------------------------------ skinning grid (host utilities)
+SkinningVoxelGrid::SkinningVoxelGrid(GridDims dims, Aabb bbox, int n_bones)
+    : dims_(dims), bbox_(bbox), n_bones_(n_bones) {
+    if (dims.nx < 2 || dims.ny < 2 || dims.nz < 2)
+        throw std::invalid_argument("SkinningVoxelGrid: dims must be >= 2 per axis");
+    if (n_bones < 1) throw std::invalid_argument("SkinningVoxelGrid: n_bones must be >= 1");
+    for (int a = 0; a < 3; ++a)
+        if (!(bbox.max[a] - bbox.min[a] > 0.0))
+            throw std::invalid_argument("SkinningVoxelGrid: bbox must have positive extent");
+    data_.assign(static_cast<size_t>(dims.vertex_count()) * n_bones, 0.0);
+}
+
+Vec3 SkinningVoxelGrid::cell_size() const {
+    const Vec3 e = bbox_.extent();
+    return {e.x() / (dims_.nx - 1), e.y() / (dims_.ny - 1), e.z() / (dims_.nz - 1)};
+}
+
+Vec3 SkinningVoxelGrid::vertex_position(int i, int j, int k) const {
+    const Vec3 h = cell_size();
+    return bbox_.min + Vec3(i * h.x(), j * h.y(), k * h.z());
+}
+
+void SkinningVoxelGrid::validate() const {
+    for (int a = 0; a < 3; ++a)
+        if (!(bbox_.max[a] - bbox_.min[a] > 0.0))
+            throw std::invalid_argument("SkinningVoxelGrid: bbox must have positive extent");
+    const std::int64_t n = dims_.vertex_count();
+    for (std::int64_t v = 0; v < n; ++v) {
+        const double* w = data_.data() + v * n_bones_;
+        double sum = 0.0;
+        for (int b = 0; b < n_bones_; ++b) {
+            if (w[b] < 0.0)
+                throw std::invalid_argument("SkinningVoxelGrid: negative weight at vertex " + std::to_string(v));
+            sum += w[b];
+        }
+        if (std::abs(sum - 1.0) > 1e-5)
+            throw std::invalid_argument("SkinningVoxelGrid: weights at vertex " + std::to_string(v) + " sum to " +
+                                        std::to_string(sum));
+    }
+}
+
+namespace {
+CellLocator locate(const GridDims& dims, const Aabb& bbox, const Vec3& x, bool lower) {
+    const Vec3 p = bbox.clamp(x);
+    const Vec3 ext = bbox.extent();
+    const int n[3] = {dims.nx, dims.ny, dims.nz};
+    int idx[3];
+    double t[3];
+    for (int a = 0; a < 3; ++a) {
+        const double u = (p[a] - bbox.min[a]) / ext[a] * (n[a] - 1);
+        int i = (u == u) ? static_cast<int>(std::floor(u)) : 0;
+        if (lower && i >= 1 && u == static_cast<double>(i)) i -= 1;
+        i = std::max(0, std::min(i, n[a] - 2));
+        idx[a] = i;
+        t[a] = std::clamp(u - i, 0.0, 1.0);
+    }
+    return {idx[0], idx[1], idx[2], t[0], t[1], t[2]};
+}
+}  // namespace
+
+CellLocator locate_cell(const GridDims& dims, const Aabb& bbox, const Vec3& x) { return locate(dims, bbox, x, false); }
+CellLocator locate_cell_lower(const GridDims& dims, const Aabb& bbox, const Vec3& x) {
+    return locate(dims, bbox, x, true);
+}
+
+void trilerp_weights_into(const SkinningVoxelGrid& grid, const Vec3& x, double* out) {
+    const CellLocator c = locate_cell(grid.dims(), grid.bbox(), x);
+    const int nb = grid.bone_count();
+    for (int b = 0; b < nb; ++b) out[b] = 0.0;
+    for (int dk = 0; dk < 2; ++dk) {
+        const double wz = dk ? c.tz : 1.0 - c.tz;
+        for (int dj = 0; dj < 2; ++dj) {
+            const double wyz = wz * (dj ? c.ty : 1.0 - c.ty);
+            for (int di = 0; di < 2; ++di) {
+                const double w = wyz * (di ? c.tx : 1.0 - c.tx);
+                const double* v = grid.vertex_weights(c.i0 + di, c.j0 + dj, c.k0 + dk);
+                for (int b = 0; b < nb; ++b) out[b] += w * v[b];
+            }
+        }
+    }
+}
+
+VectorXd trilerp_weights(const SkinningVoxelGrid& grid, const Vec3& x) {
+    VectorXd out(grid.bone_count());
+    trilerp_weights_into(grid, x, out.data());
+    return out;
+}
+
+MatrixXd weight_spatial_gradient(const SkinningVoxelGrid& grid, const Vec3& x) {
+    const CellLocator c = locate_cell_lower(grid.dims(), grid.bbox(), x);
+    const Vec3 h = grid.cell_size();
+    const int nb = grid.bone_count();
+    MatrixXd g(nb, 3);
+    const double f[3][2] = {{1.0 - c.tx, c.tx}, {1.0 - c.ty, c.ty}, {1.0 - c.tz, c.tz}};
+    const double s[3][2] = {{-1.0 / h.x(), 1.0 / h.x()}, {-1.0 / h.y(), 1.0 / h.y()}, {-1.0 / h.z(), 1.0 / h.z()}};
+    for (int dk = 0; dk < 2; ++dk)
+        for (int dj = 0; dj < 2; ++dj)
+            for (int di = 0; di < 2; ++di) {
+                const double* v = grid.vertex_weights(c.i0 + di, c.j0 + dj, c.k0 + dk);
+                const double gx = s[0][di] * f[1][dj] * f[2][dk];
+                const double gy = f[0][di] * s[1][dj] * f[2][dk];
+                const double gz = f[0][di] * f[1][dj] * s[2][dk];
+                for (int b = 0; b < nb; ++b) {
+                    g(b, 0) += gx * v[b];
+                    g(b, 1) += gy * v[b];
+                    g(b, 2) += gz * v[b];
+                }
+            }
+    return g;
+}
+
+void save_sknv(const SkinningVoxelGrid& grid, const std::string& path) {
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw std::runtime_error("cannot write grid file: " + path);
+    out.write("SKNV", 4);
+    const std::uint32_t hdr[5] = {1u, static_cast<std::uint32_t>(grid.dims().nx), static_cast<std::uint32_t>(grid.dims().ny),
+                                  static_cast<std::uint32_t>(grid.dims().nz), static_cast<std::uint32_t>(grid.bone_count())};
+    out.write(reinterpret_cast<const char*>(hdr), sizeof(hdr));
+    float bb[6];
+    for (int a = 0; a < 3; ++a) {
+        bb[a] = static_cast<float>(grid.bbox().min[a]);
+        bb[3 + a] = static_cast<float>(grid.bbox().max[a]);
+    }
+    out.write(reinterpret_cast<const char*>(bb), sizeof(bb));
+    std::vector<float> buf(grid.raw().begin(), grid.raw().end());
+    out.write(reinterpret_cast<const char*>(buf.data()), static_cast<std::streamsize>(buf.size() * sizeof(float)));
+    if (!out) throw std::runtime_error("short write to grid file: " + path);
+}
+
+SkinningVoxelGrid load_sknv(const std::string& path) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw std::runtime_error("cannot open grid file: " + path);
+    char magic[4];
+    in.read(magic, 4);
+    if (!in || std::memcmp(magic, "SKNV", 4) != 0) throw std::runtime_error(path + ": not a SKNV grid file");
+    std::uint32_t hdr[5];
+    in.read(reinterpret_cast<char*>(hdr), sizeof(hdr));
+    if (hdr[0] != 1u) throw std::runtime_error(path + ": unsupported SKNV version " + std::to_string(hdr[0]));
+    float bb[6];
+    in.read(reinterpret_cast<char*>(bb), sizeof(bb));
+    GridDims dims{static_cast<int>(hdr[1]), static_cast<int>(hdr[2]), static_cast<int>(hdr[3])};
+    SkinningVoxelGrid grid(dims, Aabb{{bb[0], bb[1], bb[2]}, {bb[3], bb[4], bb[5]}}, static_cast<int>(hdr[4]));
+    std::vector<float> buf(grid.raw().size());
+    in.read(reinterpret_cast<char*>(buf.data()), static_cast<std::streamsize>(buf.size() * sizeof(float)));
+    if (!in) throw std::runtime_error(path + ": truncated SKNV payload");
+    std::copy(buf.begin(), buf.end(), grid.raw().begin());
+    return grid;
+}
+
+// ------------------------------------------------------------------------ deformer
+Affine3 lbs_blend(std::span<const double> weights, std::span<const RigidTransform> bones) {
+    if (weights.size() != bones.size()) throw std::invalid_argument("lbs_blend: weight/bone count mismatch");
+    Affine3 out = Affine3::zero();
+    for (size_t i = 0; i < bones.size(); ++i) {
+        out.linear += bones[i].rotation * weights[i];
+        out.translation += bones[i].translation * weights[i];
+    }
+    return out;
+}
+
+Vec3 forward_deform(const Vec3& x, const SkinningVoxelGrid& grid, std::span<const RigidTransform> bones) {
+    const VectorXd w = trilerp_weights(grid, x);
+    return lbs_blend({w.data(), static_cast<size_t>(w.size())}, bones).apply(x);
+}
+
+TransformGrid::TransformGrid(GridDims dims, Aabb bbox) : dims_(dims), bbox_(bbox) {
+    data_.assign(static_cast<size_t>(dims.vertex_count()) * 12, 0.0);
+}
+
+Affine3 TransformGrid::vertex_affine(int i, int j, int k) const {
+    const double* m = vertex_transform(vertex_index(i, j, k));
+    Affine3 t;
+    for (int r = 0; r < 3; ++r) {
+        for (int c = 0; c < 3; ++c) t.linear(r, c) = m[r * 4 + c];
+        t.translation[r] = m[r * 4 + 3];
+    }
+    return t;
+}
+
+void TransformGrid::set_vertex(std::int64_t v, const Affine3& t) {
+    double* m = vertex_transform(v);
+    for (int r = 0; r < 3; ++r) {
+        for (int c = 0; c < 3; ++c) m[r * 4 + c] = t.linear(r, c);
+        m[r * 4 + 3] = t.translation[r];
+    }
+}
+
+const float* TransformGrid::device_data() const {
+    const size_t V = static_cast<size_t>(dims_.vertex_count());
+    if (!dev_) {
+        auto* b = new DevBuf(V * 12 * sizeof(float));
+        dev_ = std::shared_ptr<void>(b, [](void* p) { delete static_cast<DevBuf*>(p); });
+        host_dirty_ = true;
+    }
+    if (host_dirty_) {
+        std::vector<float> f(data_.begin(), data_.end());
+        h2d(static_cast<DevBuf*>(dev_.get())->p, f.data(), f.size() * sizeof(float));
+        host_dirty_ = false;
+    }
+    return static_cast<DevBuf*>(dev_.get())->as<float>();
+}
+
+TransformGrid precompute_transform_grid(const SkinningVoxelGrid& grid, std::span<const RigidTransform> bones, int) {
+    if (static_cast<int>(bones.size()) != grid.bone_count())
+        throw std::invalid_argument("precompute_transform_grid: bone count mismatch");
+    TransformGrid tg(grid.dims(), grid.bbox());
+    const std::int64_t V = grid.dims().vertex_count();
+    const int nb = grid.bone_count();
+    std::vector<float> w(grid.raw().begin(), grid.raw().end());
+    const std::vector<float> b = bones_f32(bones);
+    DevBuf dw(w.size() * sizeof(float)), db(b.size() * sizeof(float));
+    auto* dt = new DevBuf(static_cast<size_t>(V) * 12 * sizeof(float));
+    tg.dev_ = std::shared_ptr<void>(dt, [](void* p) { delete static_cast<DevBuf*>(p); });
+    h2d(dw.p, w.data(), w.size() * sizeof(float));
+    h2d(db.p, b.data(), b.size() * sizeof(float));
+    const fsk_grid_desc d = desc_of(grid.dims(), grid.bbox(), nb);
+    check(fsk_precompute_tgrid(ctx(), dw.as<float>(), &d, db.as<float>(), nb, dt->as<float>(), nullptr));
+    std::vector<float> out(static_cast<size_t>(V) * 12);
+    d2h(out.data(), dt->p, out.size() * sizeof(float));
+    std::copy(out.begin(), out.end(), tg.data_.begin());
+    tg.host_dirty_ = false;
+    return tg;
+}
+
+namespace {
+void eval_batch(const TransformGrid& tg, std::span<const Vec3> x, float* t12, float* d, float* jac) {
+    const size_t n = x.size();
+    const std::vector<float> p = points_f32(x);
+    DevBuf dx(p.size() * sizeof(float)), dt(n * 12 * sizeof(float)), dd(n * 3 * sizeof(float)), dj(n * 9 * sizeof(float));
+    h2d(dx.p, p.data(), p.size() * sizeof(float));
+    const fsk_grid_desc desc = desc_of(tg.dims(), tg.bbox(), 1);
+    check(fsk_eval_points(ctx(), tg.device_data(), &desc, dx.as<float>(), static_cast<std::int64_t>(n),
+                          t12 ? dt.as<float>() : nullptr, d ? dd.as<float>() : nullptr, jac ? dj.as<float>() : nullptr,
+                          nullptr));
+    if (t12) d2h(t12, dt.p, n * 12 * sizeof(float));
+    if (d) d2h(d, dd.p, n * 3 * sizeof(float));
+    if (jac) d2h(jac, dj.p, n * 9 * sizeof(float));
+}
+}  // namespace
+
+void trilerp_transform_into(const TransformGrid& tgrid, const Vec3& x, double* out12) {
+    float t[12];
+    eval_batch(tgrid, {&x, 1}, t, nullptr, nullptr);
+    for (int e = 0; e < 12; ++e) out12[e] = t[e];
+}
+
+Affine3 trilerp_transform(const TransformGrid& tgrid, const Vec3& x) {
+    double m[12];
+    trilerp_transform_into(tgrid, x, m);
+    Affine3 t;
+    for (int r = 0; r < 3; ++r) {
+        for (int c = 0; c < 3; ++c) t.linear(r, c) = m[r * 4 + c];
+        t.translation[r] = m[r * 4 + 3];
+    }
+    return t;
+}
+
+std::vector<Vec3> forward_deform_batch(std::span<const Vec3> x, const TransformGrid& tgrid) {
+    std::vector<float> d(x.size() * 3);
+    if (!x.empty()) eval_batch(tgrid, x, nullptr, d.data(), nullptr);
+    std::vector<Vec3> out(x.size());
+    for (size_t i = 0; i < x.size(); ++i) out[i] = Vec3(d[3 * i], d[3 * i + 1], d[3 * i + 2]);
+    return out;
+}
+
+Vec3 forward_deform(const Vec3& x, const TransformGrid& tgrid) { return forward_deform_batch({&x, 1}, tgrid)[0]; }
+
+std::vector<Mat3> deform_jacobian_batch(std::span<const Vec3> x, const TransformGrid& tgrid) {
+    std::vector<float> j(x.size() * 9);
+    if (!x.empty()) eval_batch(tgrid, x, nullptr, nullptr, j.data());
+    std::vector<Mat3> out(x.size());
+    for (size_t i = 0; i < x.size(); ++i)
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) out[i](r, c) = j[9 * i + 3 * r + c];
+    return out;
+}
+
+Mat3 deform_jacobian(const Vec3& x, const SkinningVoxelGrid& grid, std::span<const RigidTransform> bones) {
+    const TransformGrid tg = precompute_transform_grid(grid, bones);
+    return deform_jacobian_batch({&x, 1}, tg)[0];
+}
+
+// ------------------------------------------------------------------------ correspondence
+SearchOptions SearchOptions::defaults_for(const Aabb& bbox) {
+    const double diag = bbox.diagonal();
+    SearchOptions o;
+    o.conv_eps = 1e-5 * diag;
+    o.div_eps = 0.5 * diag;
+    o.dedup_dist = 1e-2 * diag;
+    return o;
+}
+
+void SearchOptions::validate() const {
+    if (max_iters < 1) throw std::invalid_argument("search: max_iters must be >= 1");
+    if (!(conv_eps > 0.0)) throw std::invalid_argument("search: conv_eps must be > 0");
+    if (!(div_eps > conv_eps)) throw std::invalid_argument("search: div_eps must exceed conv_eps");
+    if (!(dedup_dist >= 0.0)) throw std::invalid_argument("search: dedup_dist must be >= 0");
+    if (max_iters > 255) throw std::invalid_argument("fsk: max_iters must be <= 255 (uint8 iteration counts)");
+}
+
+std::vector<InitState> init_states(const Vec3& x_prime, const SearchContext& c, SearchVariant variant) {
+    check_context(c, variant);
+    const int nb = static_cast<int>(c.bones.size());
+    const std::vector<float> b = bones_f32(c.bones);
+    const std::vector<float> p = points_f32({&x_prime, 1});
+    DevBuf db(b.size() * 4), dp(12), dx(nb * 12), dj(nb * 36);
+    h2d(db.p, b.data(), b.size() * 4);
+    h2d(dp.p, p.data(), 12);
+    const fsk_grid_desc d = desc_of(c.tgrid->dims(), c.tgrid->bbox(), nb);
+    check(fsk_init_states(ctx(), c.tgrid->device_data(), &d, db.as<float>(), nb, dp.as<float>(), 1, dx.as<float>(),
+                          dj.as<float>(), nullptr));
+    std::vector<float> x0(nb * 3), j0(nb * 9);
+    d2h(x0.data(), dx.p, x0.size() * 4);
+    d2h(j0.data(), dj.p, j0.size() * 4);
+    std::vector<InitState> out(nb);
+    for (int i = 0; i < nb; ++i) {
+        out[i].x0 = Vec3(x0[3 * i], x0[3 * i + 1], x0[3 * i + 2]);
+        for (int r = 0; r < 3; ++r)
+            for (int q = 0; q < 3; ++q) out[i].inv_jacobian(r, q) = j0[9 * i + 3 * r + q];
+    }
+    return out;
+}
+
+std::vector<CorrespondenceSet> batch_search(std::span<const Vec3> queries, const SearchContext& c,
+                                            const SearchOptions& opts, int) {
+    check_context(c, opts.variant);
+    opts.validate();
+    const std::int64_t n = static_cast<std::int64_t>(queries.size());
+    std::vector<CorrespondenceSet> out(queries.size());
+    for (size_t q = 0; q < queries.size(); ++q) out[q].query = queries[q];
+    if (n == 0) return out;
+    const int nb = static_cast<int>(c.bones.size());
+    const std::vector<float> b = bones_f32(c.bones);
+    const std::vector<float> p = points_f32(queries);
+    const std::int64_t S = n * nb;
+    DevBuf db(b.size() * 4), dp(p.size() * 4), xc(S * 12), jv(S * 36), rs(S * 4), it(S), cv(S), kp(S), nr(n * 4),
+        offs((n + 1) * 8);
+    h2d(db.p, b.data(), b.size() * 4);
+    h2d(dp.p, p.data(), p.size() * 4);
+    fsk_search_out o{xc.as<float>(), jv.as<float>(), rs.as<float>(), it.as<uint8_t>(), cv.as<uint8_t>(),
+                     kp.as<uint8_t>(), nr.as<int32_t>()};
+    const fsk_grid_desc d = desc_of(c.tgrid->dims(), c.tgrid->bbox(), nb);
+    const fsk_search_opts so = c_opts(opts);
+    check(fsk_search_fwd(ctx(), c.tgrid->device_data(), &d, db.as<float>(), nb, dp.as<float>(), n, &so, &o, nullptr));
+    std::int64_t total = 0;
+    // first pass sizes the root buffer (cap 0 → FSK_EINVAL with total set unless empty)
+    const int rc = fsk_compact_roots(ctx(), &o, n, nb, offs.as<std::int64_t>(), nullptr, 0, &total, nullptr);
+    if (rc != FSK_OK && total == 0) check(rc);
+    std::vector<std::int64_t> h_offs(n + 1);
+    std::vector<fsk_root> roots(static_cast<size_t>(total));
+    if (total > 0) {
+        DevBuf dr(total * sizeof(fsk_root));
+        check(fsk_compact_roots(ctx(), &o, n, nb, offs.as<std::int64_t>(), dr.as<fsk_root>(), total, &total, nullptr));
+        d2h(roots.data(), dr.p, roots.size() * sizeof(fsk_root));
+    }
+    d2h(h_offs.data(), offs.p, h_offs.size() * 8);
+    for (std::int64_t q = 0; q < n; ++q) {
+        auto& set = out[static_cast<size_t>(q)];
+        for (std::int64_t k = h_offs[q]; k < h_offs[q + 1]; ++k) {
+            const fsk_root& r = roots[static_cast<size_t>(k)];
+            Root root;
+            root.x = Vec3(r.x[0], r.x[1], r.x[2]);
+            root.residual = r.residual;
+            for (int a = 0; a < 3; ++a)
+                for (int e = 0; e < 3; ++e) root.inv_jacobian(a, e) = r.inv_jacobian[3 * a + e];
+            root.source_bone = r.source_bone;
+            root.iterations = r.iterations;
+            set.roots.push_back(root);
+        }
+    }
+    return out;
+}
+
+CorrespondenceSet broyden_search(const Vec3& x_prime, const SearchContext& c, const SearchOptions& opts) {
+    return batch_search({&x_prime, 1}, c, opts)[0];
+}
+
+std::vector<Root> dedup_roots(std::vector<Root> roots, double dedup_dist) {
+    std::vector<Root> kept;
+    kept.reserve(roots.size());
+    for (Root& r : roots) {
+        bool dup = false;
+        for (const Root& k : kept)
+            if ((r.x - k.x).norm() < dedup_dist) {
+                dup = true;
+                break;
+            }
+        if (!dup) kept.push_back(std::move(r));
+    }
+    return kept;
+}
+
+}  // namespace fskin

@@ -1,0 +1,132 @@
+// Exercises the reference-facing C++ API (include/fskin/*.hpp) exactly as the reference's
+// callers do (cmd_deform / cmd_bench / train: precompute_transform_grid → batch_search,
+// fskin_cli.cpp:395-408, diff.cpp:278-289), on inputs written by tests/test_cpp_api.py.
+// Writes the CorrespondenceSets as text for the Python side to compare with the oracle,
+// and checks the API's own contracts (soundness, error messages, identity pose).
+#include <cstdio>
+#include <cstdlib>
+#include <fstream>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "fskin/correspondence.hpp"
+#include "fskin/deformer.hpp"
+
+using namespace fskin;
+
+static int fails = 0;
+#define CHECK(c)                                                          \
+    do {                                                                  \
+        if (!(c)) {                                                       \
+            std::fprintf(stderr, "CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #c); \
+            ++fails;                                                      \
+        }                                                                 \
+    } while (0)
+
+template <typename Fn>
+static void expect_invalid(Fn&& fn, const std::string& msg) {
+    try {
+        fn();
+        std::fprintf(stderr, "expected invalid_argument '%s'\n", msg.c_str());
+        ++fails;
+    } catch (const std::invalid_argument& e) {
+        if (std::string(e.what()).find(msg) == std::string::npos) {
+            std::fprintf(stderr, "wrong message '%s' (want '%s')\n", e.what(), msg.c_str());
+            ++fails;
+        }
+    }
+}
+
+int main(int argc, char** argv) {
+    if (argc < 3) return 2;
+    std::ifstream in(argv[1], std::ios::binary);
+    int hdr[5];  // nx ny nz nb n
+    in.read(reinterpret_cast<char*>(hdr), sizeof(hdr));
+    float bb[6];
+    in.read(reinterpret_cast<char*>(bb), sizeof(bb));
+    int max_iters;
+    in.read(reinterpret_cast<char*>(&max_iters), 4);
+    const GridDims dims{hdr[0], hdr[1], hdr[2]};
+    const int nb = hdr[3], n = hdr[4];
+    SkinningVoxelGrid grid(dims, Aabb{{bb[0], bb[1], bb[2]}, {bb[3], bb[4], bb[5]}}, nb);
+    std::vector<float> w(grid.raw().size()), b(nb * 12), x(3 * n);
+    in.read(reinterpret_cast<char*>(w.data()), w.size() * 4);
+    in.read(reinterpret_cast<char*>(b.data()), b.size() * 4);
+    in.read(reinterpret_cast<char*>(x.data()), x.size() * 4);
+    if (!in) return 3;
+    std::copy(w.begin(), w.end(), grid.raw().begin());
+    grid.validate();
+    std::vector<RigidTransform> bones(nb);
+    for (int i = 0; i < nb; ++i)
+        for (int r = 0; r < 3; ++r) {
+            for (int c = 0; c < 3; ++c) bones[i].rotation(r, c) = b[i * 12 + r * 4 + c];
+            bones[i].translation[r] = b[i * 12 + r * 4 + 3];
+        }
+    std::vector<Vec3> queries(n);
+    for (int p = 0; p < n; ++p) queries[p] = Vec3(x[3 * p], x[3 * p + 1], x[3 * p + 2]);
+
+    const TransformGrid tgrid = precompute_transform_grid(grid, bones, 4);
+    SearchContext ctx{bones, nullptr, &grid, &tgrid};
+    SearchOptions opts = SearchOptions::defaults_for(grid.bbox());
+    opts.max_iters = max_iters;
+    const std::vector<CorrespondenceSet> sets = batch_search(queries, ctx, opts, 8);
+    CHECK(sets.size() == static_cast<size_t>(n));
+
+    std::FILE* f = std::fopen(argv[2], "w");
+    for (const auto& s : sets) {
+        std::fprintf(f, "%zu", s.roots.size());
+        for (const Root& r : s.roots)
+            std::fprintf(f, " %d %.9g %.9g %.9g %.9g %d", r.source_bone, r.x.x(), r.x.y(), r.x.z(), r.residual,
+                         r.iterations);
+        std::fprintf(f, "\n");
+    }
+    std::fclose(f);
+
+    // soundness through the API's own evaluator
+    for (int p = 0; p < n && p < 500; ++p)
+        for (const Root& r : sets[p].roots) {
+            const Vec3 d = forward_deform(r.x, tgrid);
+            CHECK((d - queries[p]).norm() < opts.conv_eps * 1.01);
+            CHECK((r.x - queries[p]).norm() >= 0.0);
+        }
+    // broyden_search on one query equals the batch result
+    const CorrespondenceSet one = broyden_search(queries[0], ctx, opts);
+    CHECK(one.roots.size() == sets[0].roots.size());
+    for (size_t k = 0; k < one.roots.size(); ++k) CHECK(one.roots[k].x == sets[0].roots[k].x);
+    // init_states: x0 = B_i^-1 x'
+    const auto st = init_states(queries[1], ctx, SearchVariant::Voxel);
+    CHECK(st.size() == static_cast<size_t>(nb));
+    for (int i = 0; i < nb; ++i) CHECK((st[i].x0 - bones[i].inverse().apply(queries[1])).norm() < 1e-5);
+    // host evaluator agrees with the GPU evaluator (lossless precomputation, FP32)
+    for (int p = 0; p < 50; ++p) {
+        const Vec3 a = forward_deform(queries[p], grid, bones);
+        const Vec3 g = forward_deform(queries[p], tgrid);
+        CHECK((a - g).norm() < 1e-5);
+        const Mat3 J = deform_jacobian(queries[p], grid, bones);
+        CHECK(std::isfinite(J.determinant()));
+    }
+    // dedup_roots
+    std::vector<Root> rr(3);
+    rr[0].x = Vec3(0, 0, 0);
+    rr[1].x = Vec3(0, 0, 0);
+    rr[2].x = Vec3(1, 0, 0);
+    CHECK(dedup_roots(rr, 0.5).size() == 2);
+    // error contract (correspondence.cpp:19-41, deformer.cpp:64-66)
+    expect_invalid([&] { SearchOptions o = opts; o.max_iters = 0; batch_search(queries, ctx, o); },
+                   "search: max_iters must be >= 1");
+    expect_invalid([&] { SearchOptions o = opts; o.div_eps = o.conv_eps; batch_search(queries, ctx, o); },
+                   "search: div_eps must exceed conv_eps");
+    expect_invalid([&] { SearchContext c2 = ctx; c2.tgrid = nullptr; batch_search(queries, c2, opts); },
+                   "search: voxel variant needs skinning and transform grids");
+    expect_invalid([&] { SearchContext c2 = ctx; c2.bones = {}; batch_search(queries, c2, opts); },
+                   "search: no bone transforms");
+    expect_invalid([&] { precompute_transform_grid(grid, std::span<const RigidTransform>(bones).first(nb - 1)); },
+                   "precompute_transform_grid: bone count mismatch");
+    expect_invalid([&] { SearchOptions o = opts; o.variant = SearchVariant::Mlp; batch_search(queries, ctx, o); },
+                   "MLP variant");
+    // empty query list → empty result
+    CHECK(batch_search(std::span<const Vec3>(), ctx, opts).empty());
+    std::printf("fskin_api_check: %d failures\n", fails);
+    return fails ? 1 : 0;
+}

@@ -75,8 +75,11 @@ def test_init_states_match_oracle(deformer, c1):
     x0, j0 = (t.cpu().numpy() for t in deformer.init_states(tg, sc.dims, sc.bbox, B, x))
     rx0, rj0 = oracle.init_states(sc.weights, sc.dims, sc.bbox, sc.bones, sc.points)
     assert np.abs(x0 - rx0).max() < 5e-6
+    # J~0 = J^-1: the FP32 error of J (~1e-6 rel, test above) is amplified by cond(J)
     rel = np.abs(j0 - rj0).max(axis=(2, 3)) / np.maximum(1.0, np.abs(rj0).max(axis=(2, 3)))
-    assert np.quantile(rel, 0.9999) < 1e-3
+    cond = np.linalg.cond(np.linalg.inv(rj0.reshape(-1, 3, 3))).reshape(rel.shape)
+    assert np.median(rel) < 1e-5
+    assert (rel <= 2e-6 * cond + 1e-5).mean() >= 0.9999
 
 
 def _parity(g, r, conv_eps):
