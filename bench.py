@@ -193,12 +193,12 @@ def run_ours(args, rank, world, local_rank):
     opts = SearchOptions(args.max_iters, **{k: v for k, v in sc.search_options(args.max_iters).items()
                                            if k != "max_iters"})
     opts.sort = not args.no_sort
-    out = D.alloc_search_out(n, nb)
+    roots_buf = D.alloc_roots(n, nb)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
 
     def step():
-        D.precompute_transform_grid(w, sc.dims, sc.bbox, B, out=tg)
-        D.batch_search(tg, sc.dims, sc.bbox, B, x, opts, out=out)
+        # one frame: precompute_transform_grid + batch_search → CorrespondenceSets on device
+        D.deform(w, sc.dims, sc.bbox, B, x, opts, tgrid=tg, out=roots_buf)
 
     peak_fp32 = D.measure_fp32_peak()
     for _ in range(args.warmup):
@@ -237,8 +237,11 @@ def run_ours(args, rank, world, local_rank):
         total_ms = float(t.item())
 
     # algorithmic work of one K2 launch (deterministic: identical every step)
+    # per-solve iteration counts (deterministic: identical to the timed launches)
+    out = D.batch_search(tg, sc.dims, sc.bbox, B, x, opts)
     iters = out["iters"].to(torch.int64)
     conv = out["converged"].to(torch.bool)
+    total_roots = int(roots_buf[0][n].item())
     sum_iters = int(iters.sum().item())
     n_final = int((conv & (iters > 0)).sum().item())
     solves = n * nb
@@ -266,6 +269,7 @@ def run_ours(args, rank, world, local_rank):
                                     "MEASURED_PEAKS.json has no FP32 figure",
                      "algorithmic_flops_per_launch": flops, "avg_launch_ms": k2_avg,
                      "mean_iters_per_solve": sum_iters / solves, "converged_frac": float(conv.float().mean()),
+                     "kept_roots_per_query": total_roots / n,
                      "gather": {"requested_bytes_per_launch": gather,
                                 "achieved_GBps": gather / (k2_avg * 1e-3) / 1e9},
                      "k2_share_of_step": k2_ms / max(all_ms, 1e-9),

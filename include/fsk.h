@@ -116,6 +116,25 @@ int fsk_search_fwd(fsk_ctx* ctx, const float* tgrid, const fsk_grid_desc* desc,
                    const float* bones, int32_t n_bones_pose, const float* points, int64_t n,
                    const fsk_search_opts* opts, fsk_search_out* out, void* stream);
 
+/* batch_search straight to CorrespondenceSets on the device: K2 + dedup + compaction.
+ * offsets [N+1] int64 (dev): roots of query p are roots[offsets[p] .. offsets[p+1]), in bone
+ * order (Root::source_bone ascending); offsets[N] = total kept roots. roots (dev) has room for
+ * `cap` records; records beyond cap are dropped — check offsets[N] <= cap (N*n_b always
+ * suffices). Fully asynchronous (no host synchronization). */
+int fsk_batch_search(fsk_ctx* ctx, const float* tgrid, const fsk_grid_desc* desc,
+                     const float* bones, int32_t n_bones_pose, const float* points, int64_t n,
+                     const fsk_search_opts* opts, int64_t* offsets, fsk_root* roots, int64_t cap,
+                     void* stream);
+
+/* One frame of the deformer on device buffers — precompute_transform_grid followed by
+ * batch_search (what cmd_deform / cmd_bench / train do per pose: fskin_cli.cpp:395-408,
+ * :663-678, diff.cpp:278-289): K1 (fused with the gather relayout), K2, dedup, compaction.
+ * tgrid [V][12] (dev) receives the reference-layout transform grid, or NULL. Outputs as for
+ * fsk_batch_search. Fully asynchronous. */
+int fsk_deform(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* desc, const float* bones,
+               int32_t n_bones_pose, const float* points, int64_t n, const fsk_search_opts* opts,
+               float* tgrid, int64_t* offsets, fsk_root* roots, int64_t cap, void* stream);
+
 /* Stream-compaction of the kept roots into CorrespondenceSet form: offsets [N+1] int64
  * (dev), roots [total] fsk_root (dev, capacity `cap` records). *total_out (host) receives
  * the number of kept roots; this call synchronizes `stream` to read it. Returns FSK_EINVAL
@@ -156,6 +175,12 @@ int fsk_init_states(fsk_ctx* ctx, const float* tgrid, const fsk_grid_desc* desc,
 int fsk_search_bwd(fsk_ctx* ctx, const fsk_grid_desc* desc, const float* x_c, const float* jinv,
                    int32_t n_init, const float* grad_xc, const int32_t* root_sel, int64_t n,
                    float* grad_tgrid, int deterministic, void* stream);
+
+/* Same backward from compact roots (fsk_batch_search / fsk_deform output): root_index [N]
+ * int64 (dev) selects roots[root_index[p]] as x* / J~ of query p, or -1 for none. */
+int fsk_search_bwd_roots(fsk_ctx* ctx, const fsk_grid_desc* desc, const fsk_root* roots,
+                         const int64_t* root_index, const float* grad_xc, int64_t n,
+                         float* grad_tgrid, int deterministic, void* stream);
 
 /* dL/dw[v][i] = <dL/dT[v], B_i>_F  (chain rule through deformer.cpp:70-74). [V][n_b] dev. */
 int fsk_grad_weights(fsk_ctx* ctx, const fsk_grid_desc* desc, const float* grad_tgrid,

@@ -20,7 +20,8 @@ EXPORTS = [
     "fsk_ctx_create", "fsk_ctx_destroy", "fsk_last_error", "fsk_ctx_launch_count", "fsk_device_sm_count",
     "fsk_search_opts_defaults", "fsk_precompute_tgrid", "fsk_search_fwd", "fsk_compact_roots",
     "fsk_deform_host", "fsk_eval_points", "fsk_init_states", "fsk_search_bwd", "fsk_grad_weights",
-    "fsk_ctx_set_profiling", "fsk_ctx_prof_read", "fsk_measure_fp32_peak",
+    "fsk_ctx_set_profiling", "fsk_ctx_prof_read", "fsk_measure_fp32_peak", "fsk_batch_search", "fsk_deform",
+    "fsk_search_bwd_roots",
 ]
 
 
@@ -84,6 +85,9 @@ def load():
     L.fsk_init_states.argtypes = [_vp, _vp, G, _vp, _i32, _vp, _i64, _vp, _vp, _vp]
     L.fsk_search_bwd.argtypes = [_vp, G, _vp, _vp, _i32, _vp, _vp, _i64, _vp, ctypes.c_int, _vp]
     L.fsk_grad_weights.argtypes = [_vp, G, _vp, _vp, _i32, _vp, _vp]
+    L.fsk_batch_search.argtypes = [_vp, _vp, G, _vp, _i32, _vp, _i64, O, _vp, _vp, _i64, _vp]
+    L.fsk_deform.argtypes = [_vp, _vp, G, _vp, _i32, _vp, _i64, O, _vp, _vp, _vp, _i64, _vp]
+    L.fsk_search_bwd_roots.argtypes = [_vp, G, _vp, _vp, _vp, _i64, _vp, ctypes.c_int, _vp]
     L.fsk_ctx_set_profiling.argtypes = [_vp, ctypes.c_int]
     L.fsk_ctx_prof_read.argtypes = [_vp, ctypes.c_char_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64),
                                     ctypes.c_int]

@@ -17,8 +17,10 @@ LIB = os.path.join(HERE, "libfsk_b200.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC,-O2", "-I", INCLUDE, "-I", CSRC]
+# extra -D flags for tuning sweeps (e.g. FSK_NVCC_DEFS="-DFSK_SEARCH_MINB=2")
+NVCC_FLAGS += os.environ.get("FSK_NVCC_DEFS", "").split()
 
-CU_SOURCES = ["fsk.cu"]
+CU_SOURCES = ["fsk_ctx.cu", "fsk_search.cu", "fsk_bwd.cu"]
 CXX_SOURCES = ["fskin_api.cpp"]
 
 

@@ -1,0 +1,250 @@
+// fsk_bwd.cu — implicit-differentiation backward of the deformer on sm_100a (K3, GW).
+//
+// implicit_grad_approx (diff.cpp:43-51) and the training root-cotangent block
+// (diff.cpp:336-359): with v = dL/dx* and the converged Broyden estimate J~ ≈ (∂d/∂x)^-1,
+//   u = −J~ᵀ v                                        (diff.cpp:351)
+// The reference pushes uw_i = u·(B_i x̃*) (:354-356) through the skinning MLP at x*. Here the
+// skinning field is the voxel grid itself, so the cotangent is scattered to the grid:
+//   dL/dT_c += φ_c(x*) · u (x*, 1)ᵀ        (3×4, the 8 corners of locate_cell(x*))
+//   dL/dw_{c,i} = <dL/dT_c, B_i>_F          (k_grad_weights; T_c = Σ_i w_{c,i} B_i)
+// Fast mode: float4 vector reductions (REDG.E.ADD.F32x4). Deterministic mode: every term is
+// rounded to int64 fixed point with a data-derived power-of-two scale and accumulated with
+// integer reductions — associative, so bitwise reproducible for any order or GPU count.
+#include "fsk_ctx.h"
+
+namespace fsk {
+
+struct RootRef {  // where the selected root of each query lives
+    // dense form: x_c [N][n_init][3], jinv [N][n_init][9], sel [N] init index
+    const float* x_c;
+    const float* jinv;
+    const int32_t* sel;
+    int n_init;
+    // compact form: roots [M], ridx [N] root index (int64) or -1
+    const fsk_root* roots;
+    const int64_t* ridx;
+};
+
+__device__ __forceinline__ bool bwd_load(const RootRef& R, int64_t p, const float* __restrict__ gx, float xs[3],
+                                         float u[3]) {
+    const float* J;
+    if (R.roots) {
+        const int64_t k = R.ridx[p];
+        if (k < 0) return false;
+        const fsk_root& r = R.roots[k];
+        xs[0] = r.x[0];
+        xs[1] = r.x[1];
+        xs[2] = r.x[2];
+        J = r.inv_jacobian;
+    } else {
+        const int sidx = R.sel[p];
+        if (sidx < 0 || sidx >= R.n_init) return false;
+        const int64_t s = p * R.n_init + sidx;
+        J = R.jinv + 9 * s;
+        xs[0] = R.x_c[3 * s];
+        xs[1] = R.x_c[3 * s + 1];
+        xs[2] = R.x_c[3 * s + 2];
+    }
+    const float v0 = gx[3 * p], v1 = gx[3 * p + 1], v2 = gx[3 * p + 2];
+    u[0] = -(J[0] * v0 + J[3] * v1 + J[6] * v2);
+    u[1] = -(J[1] * v0 + J[4] * v1 + J[7] * v2);
+    u[2] = -(J[2] * v0 + J[5] * v1 + J[8] * v2);
+    return true;
+}
+
+__global__ void k_zero(float4* __restrict__ p, int64_t n4) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+__global__ void __launch_bounds__(256) k_bwd_scatter(GridP g, RootRef R, const float* __restrict__ gx, int64_t n,
+                                                     float4* __restrict__ gT) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    float xs[3], u[3];
+    if (!bwd_load(R, p, gx, xs, u)) return;
+    const Cell c = locate<false>(g, xs[0], xs[1], xs[2]);
+    const int nxy = g.nx * g.ny;
+#pragma unroll
+    for (int dk = 0; dk < 2; ++dk) {
+        const float wz = dk ? c.tz : 1.f - c.tz;
+#pragma unroll
+        for (int dj = 0; dj < 2; ++dj) {
+            const float wyz = wz * (dj ? c.ty : 1.f - c.ty);
+#pragma unroll
+            for (int di = 0; di < 2; ++di) {
+                const float phi = wyz * (di ? c.tx : 1.f - c.tx);
+                float4* dst = gT + 3 * (int64_t)(c.base + dk * nxy + dj * g.nx + di);
+#pragma unroll
+                for (int r = 0; r < 3; ++r) {
+                    const float a = phi * u[r];
+                    atomicAdd(dst + r, make_float4(a * xs[0], a * xs[1], a * xs[2], a));
+                }
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_bwd_maxterm(RootRef R, const float* __restrict__ gx, int64_t n,
+                                                     unsigned int* __restrict__ maxbits) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    float m = 0.f;
+    if (p < n) {
+        float xs[3], u[3];
+        if (bwd_load(R, p, gx, xs, u)) {
+            const float mu = fmaxf(fabsf(u[0]), fmaxf(fabsf(u[1]), fabsf(u[2])));
+            const float mx = fmaxf(1.f, fmaxf(fabsf(xs[0]), fmaxf(fabsf(xs[1]), fabsf(xs[2]))));
+            m = mu * mx;
+            if (!isfinite(m)) m = 3.0e38f;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffff, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(maxbits, __float_as_uint(m));  // m >= 0: bit order == value order
+}
+
+__device__ __forceinline__ double fixed_scale(unsigned int maxbits, int64_t n) {
+    const double m = (double)__uint_as_float(maxbits) * (double)(n > 0 ? n : 1);
+    if (!(m > 0.0)) return 1.0;
+    const int e = (int)floor(log2(m));
+    return ldexp(1.0, 61 - e);  // n·max|term|·scale < 2^62: no overflow in any sum
+}
+
+__global__ void __launch_bounds__(256) k_bwd_scatter_fixed(GridP g, RootRef R, const float* __restrict__ gx, int64_t n,
+                                                           const unsigned int* __restrict__ maxbits,
+                                                           unsigned long long* __restrict__ acc) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    float xs[3], u[3];
+    if (!bwd_load(R, p, gx, xs, u)) return;
+    const double scale = fixed_scale(*maxbits, n);
+    const Cell c = locate<false>(g, xs[0], xs[1], xs[2]);
+    const int nxy = g.nx * g.ny;
+    const double xt[4] = {xs[0], xs[1], xs[2], 1.0};
+    for (int q = 0; q < 8; ++q) {
+        const int di = q & 1, dj = (q >> 1) & 1, dk = q >> 2;
+        const float phi = ((dk ? c.tz : 1.f - c.tz) * (dj ? c.ty : 1.f - c.ty)) * (di ? c.tx : 1.f - c.tx);
+        unsigned long long* dst = acc + 12 * (int64_t)(c.base + dk * nxy + dj * g.nx + di);
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+            const double a = (double)phi * (double)u[r] * scale;
+#pragma unroll
+            for (int col = 0; col < 4; ++col)
+                atomicAdd(dst + 4 * r + col, (unsigned long long)__double2ll_rn(a * xt[col]));
+        }
+    }
+}
+
+__global__ void k_bwd_fixed_to_float(const long long* __restrict__ acc, int64_t m,
+                                     const unsigned int* __restrict__ maxbits, int64_t n, float* __restrict__ out) {
+    const double inv = 1.0 / fixed_scale(*maxbits, n);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (float)((double)acc[i] * inv);
+}
+
+// dL/dw[v][i] = Σ_e dL/dT[v][e]·B_i[e]. Tile of 128 vertices staged in shared memory so the
+// [V][n_b] store is coalesced. HBM-bound: V·(48 + 4·n_b) bytes.
+constexpr int kGwTile = 128;
+__global__ void __launch_bounds__(kGwTile) k_grad_weights(const float* __restrict__ gT, const float* __restrict__ bones,
+                                                          int nb, int64_t V, float* __restrict__ gw) {
+    extern __shared__ float sm[];
+    float* sB = sm;            // nb*12
+    float* sO = sm + nb * 12;  // kGwTile*nb
+    for (int e = threadIdx.x; e < nb * 12; e += blockDim.x) sB[e] = bones[e];
+    __syncthreads();
+    const int64_t v0 = blockIdx.x * (int64_t)kGwTile;
+    const int64_t v = v0 + threadIdx.x;
+    if (v < V) {
+        const float4* src = reinterpret_cast<const float4*>(gT) + 3 * v;
+        const float4 a = src[0], b = src[1], c = src[2];
+        const float G[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
+        for (int i = 0; i < nb; ++i) {
+            float s = 0.f;
+#pragma unroll
+            for (int e = 0; e < 12; ++e) s = fmaf(G[e], sB[i * 12 + e], s);
+            sO[threadIdx.x * nb + i] = s;
+        }
+    }
+    __syncthreads();
+    const int64_t cnt = min((int64_t)kGwTile, V - v0) * nb;
+    for (int64_t e = threadIdx.x; e < cnt; e += blockDim.x) gw[v0 * nb + e] = sO[e];
+}
+
+namespace {
+
+void run_bwd(fsk_ctx* ctx, const GridP& g, const RootRef& R, const float* grad_xc, int64_t n, float* grad_tgrid,
+             int deterministic, cudaStream_t st) {
+    const int64_t V = (int64_t)g.nx * g.ny * g.nz;
+    const unsigned cap_blocks = (unsigned)ctx->sm_count * 8;
+    if (!deterministic) {
+        FSK_LAUNCH(ctx, st, k_zero, std::min(blocks_for(V * 3, 256), cap_blocks), 256, 0,
+                   reinterpret_cast<float4*>(grad_tgrid), V * 3);
+        if (n > 0)
+            FSK_LAUNCH(ctx, st, k_bwd_scatter, blocks_for(n, 256), 256, 0, g, R, grad_xc, n,
+                       reinterpret_cast<float4*>(grad_tgrid));
+        return;
+    }
+    unsigned long long* acc = (unsigned long long*)scratch(ctx, kBwdAcc, V * 12 * sizeof(unsigned long long));
+    unsigned int* mx = (unsigned int*)scratch(ctx, kBwdMax, 16);
+    FSK_LAUNCH(ctx, st, k_zero, std::min(blocks_for(V * 6, 256), cap_blocks), 256, 0, reinterpret_cast<float4*>(acc),
+               V * 6);
+    FSK_LAUNCH(ctx, st, k_zero, 1, 32, 0, reinterpret_cast<float4*>(mx), (int64_t)1);
+    if (n > 0) {
+        FSK_LAUNCH(ctx, st, k_bwd_maxterm, blocks_for(n, 256), 256, 0, R, grad_xc, n, mx);
+        FSK_LAUNCH(ctx, st, k_bwd_scatter_fixed, blocks_for(n, 256), 256, 0, g, R, grad_xc, n, mx, acc);
+    }
+    FSK_LAUNCH(ctx, st, k_bwd_fixed_to_float, std::min(blocks_for(V * 12, 256), cap_blocks), 256, 0,
+               reinterpret_cast<const long long*>(acc), V * 12, mx, n, grad_tgrid);
+}
+
+}  // namespace
+}  // namespace fsk
+
+using namespace fsk;
+
+extern "C" {
+
+int fsk_search_bwd(fsk_ctx* ctx, const fsk_grid_desc* desc, const float* x_c, const float* jinv, int32_t n_init,
+                   const float* grad_xc, const int32_t* root_sel, int64_t n, float* grad_tgrid, int deterministic,
+                   void* stream) {
+    return guard([&] {
+        set_device(ctx);
+        const GridP g = make_grid(desc);
+        if (n < 0) fail(FSK_EINVAL, "fsk: negative point count");
+        if (n_init < 1) fail(FSK_EINVAL, "fsk: n_init must be >= 1");
+        if (!grad_tgrid || (n > 0 && (!x_c || !jinv || !grad_xc || !root_sel))) fail(FSK_EINVAL, "fsk: null buffer");
+        RootRef R{x_c, jinv, root_sel, n_init, nullptr, nullptr};
+        run_bwd(ctx, g, R, grad_xc, n, grad_tgrid, deterministic, (cudaStream_t)stream);
+    });
+}
+
+int fsk_search_bwd_roots(fsk_ctx* ctx, const fsk_grid_desc* desc, const fsk_root* roots, const int64_t* root_index,
+                         const float* grad_xc, int64_t n, float* grad_tgrid, int deterministic, void* stream) {
+    return guard([&] {
+        set_device(ctx);
+        const GridP g = make_grid(desc);
+        if (n < 0) fail(FSK_EINVAL, "fsk: negative point count");
+        if (!grad_tgrid || (n > 0 && (!roots || !root_index || !grad_xc))) fail(FSK_EINVAL, "fsk: null buffer");
+        RootRef R{nullptr, nullptr, nullptr, 0, roots, root_index};
+        run_bwd(ctx, g, R, grad_xc, n, grad_tgrid, deterministic, (cudaStream_t)stream);
+    });
+}
+
+int fsk_grad_weights(fsk_ctx* ctx, const fsk_grid_desc* desc, const float* grad_tgrid, const float* bones,
+                     int32_t n_bones_pose, float* grad_w, void* stream) {
+    return guard([&] {
+        set_device(ctx);
+        const GridP g = make_grid(desc);
+        if (n_bones_pose != g.nb) fail(FSK_EINVAL, "precompute_transform_grid: bone count mismatch");
+        if (!grad_tgrid || !bones || !grad_w) fail(FSK_EINVAL, "fsk: null buffer");
+        const int64_t V = (int64_t)g.nx * g.ny * g.nz;
+        const size_t smem = (size_t)(g.nb * 12 + kGwTile * g.nb) * sizeof(float);
+        if (smem > 200 * 1024) fail(FSK_EINVAL, "fsk: too many bones for grad_weights");
+        if (smem > 48 * 1024)
+            cuda_check(cudaFuncSetAttribute(k_grad_weights, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                       "cudaFuncSetAttribute");
+        cudaStream_t st = (cudaStream_t)stream;
+        FSK_LAUNCH(ctx, st, k_grad_weights, blocks_for(V, kGwTile), kGwTile, smem, grad_tgrid, bones, g.nb, V, grad_w);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,235 @@
+// fsk_ctx.cu — context lifecycle, scratch, errors, validation, profiling hooks and the
+// FP32 roofline microbenchmark of the C-ABI (include/fsk.h).
+#include <cstring>
+#include <stdexcept>
+
+#include "fsk_ctx.h"
+
+namespace fsk {
+
+namespace {
+thread_local std::string g_err;
+}
+
+void set_error(const std::string& m) { g_err = m; }
+
+void* scratch(fsk_ctx* ctx, int slot, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    if (ctx->cap[slot] < bytes) {
+        if (ctx->buf[slot]) cuda_check(cudaFree(ctx->buf[slot]), "cudaFree");
+        ctx->buf[slot] = nullptr;
+        ctx->cap[slot] = 0;
+        const size_t b = bytes + bytes / 8;
+        cuda_check(cudaMalloc(&ctx->buf[slot], b), "cudaMalloc");
+        ctx->cap[slot] = b;
+    }
+    return ctx->buf[slot];
+}
+
+void set_device(fsk_ctx* ctx) {
+    if (!ctx) fail(FSK_EINVAL, "fsk: null context");
+    cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+}
+
+namespace {
+cudaEvent_t pooled_event(fsk_ctx* ctx) {
+    if (!ctx->pool.empty()) {
+        cudaEvent_t e = ctx->pool.back();
+        ctx->pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+    return e;
+}
+}  // namespace
+
+void prof_begin(fsk_ctx* ctx, cudaStream_t st) {
+    if (!ctx->prof_on) return;
+    ctx->pending = pooled_event(ctx);
+    ctx->pending_stream = st;
+    cuda_check(cudaEventRecord(ctx->pending, st), "cudaEventRecord");
+}
+
+void after_launch(fsk_ctx* ctx, const char* name) {
+    ctx->launches++;
+    cuda_check(cudaGetLastError(), name);
+    if (ctx->prof_on && ctx->pending) {
+        cudaEvent_t b = pooled_event(ctx);
+        cuda_check(cudaEventRecord(b, ctx->pending_stream), "cudaEventRecord");
+        ctx->prof.push_back({name, ctx->pending, b});
+        ctx->pending = nullptr;
+    }
+}
+
+GridP make_grid(const fsk_grid_desc* d) {
+    if (!d) fail(FSK_EINVAL, "fsk: null grid descriptor");
+    // SkinningVoxelGrid ctor checks (skinning.cpp:60-70)
+    if (d->nx < 2 || d->ny < 2 || d->nz < 2) fail(FSK_EINVAL, "SkinningVoxelGrid: dims must be >= 2 per axis");
+    if (d->n_bones < 1) fail(FSK_EINVAL, "SkinningVoxelGrid: n_bones must be >= 1");
+    if ((int64_t)d->nx * d->ny * d->nz >= (int64_t(1) << 30)) fail(FSK_EINVAL, "fsk: grid too large (>= 2^30 vertices)");
+    GridP g;
+    g.nx = d->nx;
+    g.ny = d->ny;
+    g.nz = d->nz;
+    g.nb = d->n_bones;
+    const int n[3] = {d->nx, d->ny, d->nz};
+    for (int a = 0; a < 3; ++a) {
+        g.lo[a] = d->bbox_min[a];
+        g.hi[a] = d->bbox_max[a];
+        const float ext = g.hi[a] - g.lo[a];
+        if (!(ext > 0.f)) fail(FSK_EINVAL, "SkinningVoxelGrid: bbox must have positive extent");
+        g.scale[a] = (float)((double)(n[a] - 1) / (double)ext);
+    }
+    return g;
+}
+
+SearchP make_search(const fsk_search_opts* o) {
+    if (!o) fail(FSK_EINVAL, "fsk: null search options");
+    // SearchOptions::validate (correspondence.cpp:19-25)
+    if (o->max_iters < 1) fail(FSK_EINVAL, "search: max_iters must be >= 1");
+    if (!(o->conv_eps > 0.f)) fail(FSK_EINVAL, "search: conv_eps must be > 0");
+    if (!(o->div_eps > o->conv_eps)) fail(FSK_EINVAL, "search: div_eps must exceed conv_eps");
+    if (!(o->dedup_dist >= 0.f)) fail(FSK_EINVAL, "search: dedup_dist must be >= 0");
+    if (o->max_iters > 255) fail(FSK_EINVAL, "fsk: max_iters must be <= 255 (uint8 iteration counts)");
+    SearchP s;
+    s.max_iters = o->max_iters;
+    s.conv2 = (float)((double)o->conv_eps * (double)o->conv_eps);
+    s.div2 = (float)((double)o->div_eps * (double)o->div_eps);
+    s.dedup2 = (float)((double)o->dedup_dist * (double)o->dedup_dist);
+    return s;
+}
+
+// FFMA throughput microbenchmark: 8 independent dependency chains per thread over all SMs.
+__global__ void __launch_bounds__(256) k_peak_fp32(float* out, int iters, float a, float b) {
+    float x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = threadIdx.x * 1e-3f + i;
+    for (int k = 0; k < iters; ++k) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = fmaf(x[i], a, b);
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += x[i];
+    if (s == 12345.678f) out[0] = s;  // keep the chains alive
+}
+
+}  // namespace fsk
+
+using namespace fsk;
+
+extern "C" {
+
+const char* fsk_last_error(void) { return g_err.c_str(); }
+
+int fsk_ctx_create(int device, fsk_ctx** out) {
+    return guard([&] {
+        if (!out) fail(FSK_EINVAL, "fsk: null output pointer");
+        *out = nullptr;
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+            cudaGetLastError();
+            fail(FSK_ENODEV, "fsk: no CUDA device available (this library has no CPU fallback)");
+        }
+        if (device < 0 || device >= n) fail(FSK_EINVAL, "fsk: device ordinal out of range");
+        cudaDeviceProp prop;
+        cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+        if (prop.major != 10) fail(FSK_ENODEV, std::string("fsk: built for sm_100a, device is ") + prop.name);
+        auto* c = new fsk_ctx();
+        c->device = device;
+        c->sm_count = prop.multiProcessorCount;
+        *out = c;
+    });
+}
+
+int fsk_ctx_destroy(fsk_ctx* ctx) {
+    return guard([&] {
+        if (!ctx) return;
+        cudaSetDevice(ctx->device);
+        for (auto& b : ctx->buf)
+            if (b) cudaFree(b);
+        for (auto& r : ctx->prof) {
+            cudaEventDestroy(r.a);
+            cudaEventDestroy(r.b);
+        }
+        for (auto& e : ctx->pool) cudaEventDestroy(e);
+        delete ctx;
+    });
+}
+
+int64_t fsk_ctx_launch_count(const fsk_ctx* ctx) { return ctx ? ctx->launches : -1; }
+int fsk_device_sm_count(const fsk_ctx* ctx) { return ctx ? ctx->sm_count : -1; }
+
+int fsk_ctx_set_profiling(fsk_ctx* ctx, int on) {
+    return guard([&] {
+        set_device(ctx);
+        ctx->prof_on = on != 0;
+    });
+}
+
+int fsk_ctx_prof_read(fsk_ctx* ctx, const char* name, double* total_ms, int64_t* count, int reset) {
+    return guard([&] {
+        set_device(ctx);
+        if (!total_ms || !count) fail(FSK_EINVAL, "fsk: null output pointer");
+        double t = 0.0;
+        int64_t c = 0;
+        for (auto& r : ctx->prof) {
+            if (name && std::strcmp(name, r.name) != 0) continue;
+            cuda_check(cudaEventSynchronize(r.b), "cudaEventSynchronize");
+            float ms = 0.f;
+            cuda_check(cudaEventElapsedTime(&ms, r.a, r.b), "cudaEventElapsedTime");
+            t += ms;
+            ++c;
+        }
+        *total_ms = t;
+        *count = c;
+        if (reset) {
+            for (auto& r : ctx->prof) {
+                cuda_check(cudaEventSynchronize(r.b), "cudaEventSynchronize");
+                ctx->pool.push_back(r.a);
+                ctx->pool.push_back(r.b);
+            }
+            ctx->prof.clear();
+        }
+    });
+}
+
+int fsk_measure_fp32_peak(fsk_ctx* ctx, double* tflops) {
+    return guard([&] {
+        set_device(ctx);
+        if (!tflops) fail(FSK_EINVAL, "fsk: null output pointer");
+        float* o = (float*)scratch(ctx, kBwdMax, 16);
+        const int blocks = ctx->sm_count * 8, iters = 1 << 14;
+        cudaEvent_t a, b;
+        cuda_check(cudaEventCreate(&a), "cudaEventCreate");
+        cuda_check(cudaEventCreate(&b), "cudaEventCreate");
+        k_peak_fp32<<<blocks, 256>>>(o, 256, 0.999f, 1e-3f);  // warm-up
+        cuda_check(cudaEventRecord(a, 0), "cudaEventRecord");
+        k_peak_fp32<<<blocks, 256>>>(o, iters, 0.999f, 1e-3f);
+        cuda_check(cudaEventRecord(b, 0), "cudaEventRecord");
+        cuda_check(cudaEventSynchronize(b), "cudaEventSynchronize");
+        float ms = 0.f;
+        cuda_check(cudaEventElapsedTime(&ms, a, b), "cudaEventElapsedTime");
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        *tflops = 2.0 * 8.0 * iters * (double)blocks * 256.0 / (ms * 1e-3) / 1e12;
+    });
+}
+
+fsk_search_opts fsk_search_opts_defaults(const fsk_grid_desc* d) {
+    fsk_search_opts o{50, 1e-5f, 0.5f, 1e-2f, 0};
+    if (!d) return o;
+    double s = 0.0;
+    for (int a = 0; a < 3; ++a) {
+        const double e = (double)d->bbox_max[a] - (double)d->bbox_min[a];
+        s += e * e;
+    }
+    const double diag = std::sqrt(s);
+    o.conv_eps = (float)(1e-5 * diag);
+    o.div_eps = (float)(0.5 * diag);
+    o.dedup_dist = (float)(1e-2 * diag);
+    return o;
+}
+
+}  // extern "C"

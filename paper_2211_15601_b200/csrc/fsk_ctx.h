@@ -1,0 +1,94 @@
+// fsk_ctx.h — host-side internals shared by the C-ABI translation units: the context
+// (device, growable scratch, launch counter, optional per-launch event profiling), error
+// handling (no exception crosses the C-ABI), and argument validation with the
+// reference's messages.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "fsk.h"
+#include "fsk_device.cuh"
+
+struct fsk_ctx {
+    int device = 0;
+    int sm_count = 0;
+    int64_t launches = 0;
+    static constexpr int kSlots = 40;
+    void* buf[kSlots] = {};
+    size_t cap[kSlots] = {};
+    // optional per-launch CUDA-event profiling (bench.py reads per-kernel device time)
+    bool prof_on = false;
+    cudaEvent_t pending = nullptr;
+    cudaStream_t pending_stream = nullptr;
+    struct Rec {
+        const char* name;
+        cudaEvent_t a, b;
+    };
+    std::vector<Rec> prof;
+    std::vector<cudaEvent_t> pool;
+};
+
+namespace fsk {
+
+// Scratch slots (one growable device buffer each).
+enum Slot {
+    kHist, kBbox, kKeys, kPerm, kXs, kScanPart, kBwdAcc, kBwdMax, kPlanes,
+    kOXr, kOJa, kOJb, kOJc, kOMeta, kOKeep, kNRoots, kOffs, kRootsTmp,
+    kHW, kHB, kHP, kHT, kHOffs, kHRoots,
+    kSlotCount
+};
+static_assert(kSlotCount <= fsk_ctx::kSlots, "scratch slots");
+
+struct Error {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] inline void fail(int code, const std::string& m) { throw Error{code, m}; }
+
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(FSK_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void set_error(const std::string& m);  // thread-local fsk_last_error text (fsk_ctx.cu)
+
+template <typename Fn>
+int guard(Fn&& fn) {
+    try {
+        fn();
+        return FSK_OK;
+    } catch (const Error& e) {
+        set_error(e.msg);
+        return e.code;
+    } catch (const std::exception& e) {
+        set_error(e.what());
+        return FSK_ECUDA;
+    }
+}
+
+void* scratch(fsk_ctx* ctx, int slot, size_t bytes);
+void set_device(fsk_ctx* ctx);
+void prof_begin(fsk_ctx* ctx, cudaStream_t st);
+void after_launch(fsk_ctx* ctx, const char* name);
+
+GridP make_grid(const fsk_grid_desc* d);
+SearchP make_search(const fsk_search_opts* o);
+
+inline unsigned blocks_for(int64_t n, int t) { return (unsigned)std::max<int64_t>(1, (n + t - 1) / t); }
+
+}  // namespace fsk
+
+// Launch helper: optional profiling events around the launch, launch counting and error
+// check. Usage: FSK_LAUNCH(ctx, st, kernel, grid, block, smem, args...).
+#define FSK_LAUNCH(ctx, st, kern, grid, block, smem, ...)       \
+    do {                                                        \
+        ::fsk::prof_begin((ctx), (st));                         \
+        kern<<<(grid), (block), (smem), (st)>>>(__VA_ARGS__);   \
+        ::fsk::after_launch((ctx), #kern);                      \
+    } while (0)

@@ -1,0 +1,789 @@
+// fsk_search.cu — forward hot path of the deformer on sm_100a and its C-ABI entry points.
+//
+//   K1  k_precompute        precompute_transform_grid (deformer.cpp:61-77, lbs_blend :9-19)
+//                           fused with the x-pair gather-plane relayout (fsk_device.cuh)
+//   S*  k_sort_*            spatial (Morton) ordering of the queries — performance only
+//   K2  k_search            search_one per (point, bone-init) (correspondence.cpp:126-150)
+//                           with iterate (:97-124) in registers
+//   D   k_dedup             dedup_roots (correspondence.cpp:162-176)
+//   C*  k_scan_*, k_emit    compaction into CorrespondenceSets (correspondence.hpp:29-42)
+//   k_scatter_dense         the dense per-(point, init) form (fsk_search_out)
+//   E   k_eval_points, k_init_states
+//
+// K2 writes its per-solve state bone-major in sorted-query order ("search planes") so
+// every store of a warp is one contiguous, coalesced segment; dedup then reads the n_b
+// inits of a query with coalesced loads, and only kept roots are scattered to the
+// caller's query order (≈1 root per query instead of n_b dense records).
+#include <cstring>
+
+#include "fsk_ctx.h"
+
+namespace fsk {
+
+// ============================================================================ K1
+// T_v = Σ_i w_{v,i}·B_i, accumulated in bone order like lbs_blend. One thread per vertex,
+// bones staged in shared memory. Writes the reference-layout [V][12] grid (if tg != null)
+// and the gather planes: P[r][v].lo = row r of T_v, P[r][v-1].hi = row r of T_v.
+__global__ void __launch_bounds__(256) k_precompute(const float* __restrict__ w, const float* __restrict__ bones,
+                                                    int nb, int nx, int64_t V, float4* __restrict__ tg,
+                                                    float4* __restrict__ planes) {
+    extern __shared__ float sB[];
+    for (int e = threadIdx.x; e < nb * 12; e += blockDim.x) sB[e] = bones[e];
+    __syncthreads();
+    const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (v >= V) return;
+    const float* wv = w + v * nb;
+    float T[12];
+#pragma unroll
+    for (int e = 0; e < 12; ++e) T[e] = 0.f;
+    for (int i = 0; i < nb; ++i) {
+        const float wi = __ldg(wv + i);
+#pragma unroll
+        for (int e = 0; e < 12; ++e) T[e] = fmaf(wi, sB[i * 12 + e], T[e]);
+    }
+    const float4 r0 = make_float4(T[0], T[1], T[2], T[3]);
+    const float4 r1 = make_float4(T[4], T[5], T[6], T[7]);
+    const float4 r2 = make_float4(T[8], T[9], T[10], T[11]);
+    if (tg) {
+        tg[3 * v] = r0;
+        tg[3 * v + 1] = r1;
+        tg[3 * v + 2] = r2;
+    }
+    if (planes) {
+        const int64_t stride = 2 * V;  // float4 units per row plane
+        const bool has_left = (v % nx) != 0;
+        planes[2 * v] = r0;
+        planes[stride + 2 * v] = r1;
+        planes[2 * stride + 2 * v] = r2;
+        if (has_left) {
+            planes[2 * (v - 1) + 1] = r0;
+            planes[stride + 2 * (v - 1) + 1] = r1;
+            planes[2 * stride + 2 * (v - 1) + 1] = r2;
+        }
+    }
+}
+
+// Relayout of a caller-provided [V][12] grid into the gather planes.
+__global__ void __launch_bounds__(256) k_relayout(const float4* __restrict__ tg, int nx, int64_t V,
+                                                  float4* __restrict__ planes) {
+    const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (v >= V) return;
+    const int64_t stride = 2 * V;
+    const bool has_right = (v % nx) != nx - 1;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        planes[r * stride + 2 * v] = tg[3 * v + r];
+        planes[r * stride + 2 * v + 1] = has_right ? tg[3 * (v + 1) + r] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+}
+
+// ============================================================================ sort
+// Counting sort of the queries on a 15-bit Morton key of their posed position within
+// the queries' bounding box. Performance only: every solve runs the same instruction
+// sequence wherever it lands, so results are order-independent (and bitwise
+// deterministic); neighbouring lanes then gather neighbouring grid cells.
+constexpr int kSortBitsPerAxis = 5;
+constexpr int kSortBuckets = 1 << (3 * kSortBitsPerAxis);
+
+__device__ __forceinline__ int f2ord(float f) {
+    const int i = __float_as_int(f);
+    return i >= 0 ? i : i ^ 0x7fffffff;
+}
+__device__ __forceinline__ float ord2f(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7fffffff); }
+
+__global__ void k_sort_init(int* __restrict__ hist, int* __restrict__ bbox) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    for (int i = t; i < kSortBuckets; i += gridDim.x * blockDim.x) hist[i] = 0;
+    if (t < 3) {
+        bbox[t] = f2ord(INFINITY);
+        bbox[3 + t] = f2ord(-INFINITY);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_sort_bbox(const float* __restrict__ x, int64_t n, int* __restrict__ bbox) {
+    float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const float v = x[3 * p + a];
+            if (isfinite(v)) {
+                lo[a] = fminf(lo[a], v);
+                hi[a] = fmaxf(hi[a], v);
+            }
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        for (int o = 16; o > 0; o >>= 1) {
+            lo[a] = fminf(lo[a], __shfl_xor_sync(0xffffffff, lo[a], o));
+            hi[a] = fmaxf(hi[a], __shfl_xor_sync(0xffffffff, hi[a], o));
+        }
+    }
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            atomicMin(bbox + a, f2ord(lo[a]));
+            atomicMax(bbox + 3 + a, f2ord(hi[a]));
+        }
+    }
+}
+
+__device__ __forceinline__ uint32_t spread3(uint32_t v) {  // 5 bits -> every third bit
+    v &= 0x1f;
+    v = (v | (v << 8)) & 0x100f;
+    v = (v | (v << 4)) & 0x10c3;
+    v = (v | (v << 2)) & 0x1249;
+    return v;
+}
+
+__global__ void __launch_bounds__(256) k_sort_hist(const float* __restrict__ x, int64_t n, const int* __restrict__ bbox,
+                                                   uint16_t* __restrict__ keys, int* __restrict__ hist) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    uint32_t q[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const float lo = ord2f(bbox[a]), hi = ord2f(bbox[3 + a]);
+        const float s = (float)(1 << kSortBitsPerAxis) / fmaxf(hi - lo, 1e-30f);
+        const float u = (x[3 * p + a] - lo) * s;
+        const int qi = isfinite(u) ? __float2int_rd(u) : 0;
+        q[a] = (uint32_t)max(0, min(qi, (1 << kSortBitsPerAxis) - 1));
+    }
+    const uint32_t k = spread3(q[0]) | (spread3(q[1]) << 1) | (spread3(q[2]) << 2);
+    keys[p] = (uint16_t)k;
+    atomicAdd(hist + k, 1);
+}
+
+// Single-block exclusive scan of the 32768 bucket counts (1024 threads × 32).
+__global__ void __launch_bounds__(1024) k_sort_scan(int* __restrict__ hist) {
+    __shared__ int warp_tot[32];
+    constexpr int kPer = kSortBuckets / 1024;
+    const int t = threadIdx.x;
+    int v[kPer];
+    int s = 0;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+        v[i] = hist[t * kPer + i];
+        s += v[i];
+    }
+    int incl = s;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffff, incl, o);
+        if ((t & 31) >= o) incl += y;
+    }
+    if ((t & 31) == 31) warp_tot[t >> 5] = incl;
+    __syncthreads();
+    if (t < 32) {
+        const int w = warp_tot[t];
+        int wi = w;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffff, wi, o);
+            if (t >= o) wi += y;
+        }
+        warp_tot[t] = wi - w;
+    }
+    __syncthreads();
+    int run = warp_tot[t >> 5] + incl - s;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+        hist[t * kPer + i] = run;
+        run += v[i];
+    }
+}
+
+// Scatter into sorted order: perm[pos] = p, xs[pos] = (x_p, 0) as float4 (16-B loads in K2).
+__global__ void __launch_bounds__(256) k_sort_scatter(const float* __restrict__ x, const uint16_t* __restrict__ keys,
+                                                      int64_t n, int* __restrict__ offs, int* __restrict__ perm,
+                                                      float4* __restrict__ xs) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const int pos = atomicAdd(offs + keys[p], 1);
+    perm[pos] = (int)p;
+    xs[pos] = make_float4(x[3 * p], x[3 * p + 1], x[3 * p + 2], 0.f);
+}
+
+__global__ void __launch_bounds__(256) k_identity_order(const float* __restrict__ x, int64_t n, int* __restrict__ perm,
+                                                        float4* __restrict__ xs) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    perm[p] = (int)p;
+    xs[p] = make_float4(x[3 * p], x[3 * p + 1], x[3 * p + 2], 0.f);
+}
+
+// ============================================================================ K2
+// Per-solve state, bone-major in sorted order: q = bone*n + j.
+struct SearchPlanes {
+    float4* xr;      // {x, y, z, residual}
+    float4* ja;      // J~[0..3]
+    float4* jb;      // J~[4..7]
+    float* jc;       // J~[8]
+    uint16_t* meta;  // iterations | converged << 8
+    uint8_t* keep;   // dedup survivors
+};
+
+constexpr int kSearchBlock = 256;
+#ifndef FSK_SEARCH_MINB
+#define FSK_SEARCH_MINB 3  // resident blocks per SM the register budget is sized for
+#endif
+
+// One thread per (posed point, bone-init) solve. Blocks are bone-major (B_i^-1 is a
+// block-uniform broadcast load) over spatially sorted queries.
+__global__ void __launch_bounds__(kSearchBlock, FSK_SEARCH_MINB) k_search(Planes P, GridP g, const float* __restrict__ bones,
+                                                            const float4* __restrict__ xs, int64_t n,
+                                                            int blocks_per_bone, SearchP o, SearchPlanes out) {
+    const int bone = blockIdx.x / blocks_per_bone;
+    const int64_t j = (int64_t)(blockIdx.x - bone * blocks_per_bone) * kSearchBlock + threadIdx.x;
+    if (j >= n) return;
+    const float4 xq = __ldg(xs + j);
+    const float xp0 = xq.x, xp1 = xq.y, xp2 = xq.z;
+
+    float x0, x1, x2, Ji[9], T[12], d[3];
+    solve_init(P, g, bones + 12 * bone, xp0, xp1, xp2, x0, x1, x2, Ji, T);
+    apply_T(T, x0, x1, x2, d);  // g0 = d(x0) − x' from the init gather (correspondence.cpp:137)
+    float g0 = d[0] - xp0, g1 = d[1] - xp1, g2 = d[2] - xp2;
+    float err2 = g0 * g0 + g1 * g1 + g2 * g2;
+
+    int iters = 0;
+    bool conv = err2 < o.conv2;  // (:100-103)
+    if (!conv) {
+        for (int k = 0; k < o.max_iters; ++k) {
+            if (err2 > o.div2) break;  // divergence check at the top (:105)
+            // dx = −J~ g; x += dx (:106-107)
+            const float dx0 = -(Ji[0] * g0 + Ji[1] * g1 + Ji[2] * g2);
+            const float dx1 = -(Ji[3] * g0 + Ji[4] * g1 + Ji[5] * g2);
+            const float dx2 = -(Ji[6] * g0 + Ji[7] * g1 + Ji[8] * g2);
+            x0 += dx0;
+            x1 += dx1;
+            x2 += dx2;
+            // g' = d(x) − x'; dg = g' − g (:108-112)
+            const Cell c = locate<false>(g, x0, x1, x2);
+            trilerp_T(P, g, c, T);
+            apply_T(T, x0, x1, x2, d);
+            const float n0 = d[0] - xp0, n1 = d[1] - xp1, n2 = d[2] - xp2;
+            const float dg0 = n0 - g0, dg1 = n1 - g1, dg2 = n2 - g2;
+            g0 = n0;
+            g1 = n1;
+            g2 = n2;
+            iters = k + 1;
+            err2 = g0 * g0 + g1 * g1 + g2 * g2;
+            if (err2 < o.conv2) {  // (:113-116)
+                conv = true;
+                break;
+            }
+            // good Broyden: J~ += ((dx − J~dg)/(dx·J~dg)) (dxᵀJ~) if |den| > 1e-18 (:118-122)
+            const float j0 = Ji[0] * dg0 + Ji[1] * dg1 + Ji[2] * dg2;
+            const float j1 = Ji[3] * dg0 + Ji[4] * dg1 + Ji[5] * dg2;
+            const float j2 = Ji[6] * dg0 + Ji[7] * dg1 + Ji[8] * dg2;
+            const float den = dx0 * j0 + dx1 * j1 + dx2 * j2;
+            if (fabsf(den) > 1e-18f) {
+                const float inv = 1.f / den;
+                const float q0 = (dx0 - j0) * inv, q1 = (dx1 - j1) * inv, q2 = (dx2 - j2) * inv;
+                const float w0 = dx0 * Ji[0] + dx1 * Ji[3] + dx2 * Ji[6];
+                const float w1 = dx0 * Ji[1] + dx1 * Ji[4] + dx2 * Ji[7];
+                const float w2 = dx0 * Ji[2] + dx1 * Ji[5] + dx2 * Ji[8];
+                Ji[0] = fmaf(q0, w0, Ji[0]); Ji[1] = fmaf(q0, w1, Ji[1]); Ji[2] = fmaf(q0, w2, Ji[2]);
+                Ji[3] = fmaf(q1, w0, Ji[3]); Ji[4] = fmaf(q1, w1, Ji[4]); Ji[5] = fmaf(q1, w2, Ji[5]);
+                Ji[6] = fmaf(q2, w0, Ji[6]); Ji[7] = fmaf(q2, w1, Ji[7]); Ji[8] = fmaf(q2, w2, Ji[8]);
+            }
+        }
+    }
+    const int64_t q = (int64_t)bone * n + j;
+    out.xr[q] = make_float4(x0, x1, x2, sqrtf(err2));
+    out.ja[q] = make_float4(Ji[0], Ji[1], Ji[2], Ji[3]);
+    out.jb[q] = make_float4(Ji[4], Ji[5], Ji[6], Ji[7]);
+    out.jc[q] = Ji[8];
+    out.meta[q] = (uint16_t)(iters | (conv ? 0x100 : 0));
+}
+
+// ============================================================================ dedup
+// dedup_roots over each query's converged inits in bone order: a root is kept iff
+// ||x − k|| >= dedup_dist for every already-kept k (strict '<' drops; :162-176).
+// One thread per sorted query; all loads of a warp are coalesced rows of the planes.
+__global__ void __launch_bounds__(256) k_dedup(int64_t n, int nb, float dedup2, SearchPlanes sp,
+                                               const int* __restrict__ perm, int32_t* __restrict__ n_roots_p) {
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    int count = 0;
+    for (int b = 0; b < nb; ++b) {
+        const int64_t q = (int64_t)b * n + j;
+        int k = 0;
+        if (sp.meta[q] & 0x100) {
+            const float4 a = sp.xr[q];
+            k = 1;
+            for (int c = 0; c < b; ++c) {
+                const int64_t qc = (int64_t)c * n + j;
+                if (!sp.keep[qc]) continue;
+                const float4 e = sp.xr[qc];
+                const float e0 = a.x - e.x, e1 = a.y - e.y, e2 = a.z - e.z;
+                if (e0 * e0 + e1 * e1 + e2 * e2 < dedup2) {
+                    k = 0;
+                    break;
+                }
+            }
+        }
+        sp.keep[q] = (uint8_t)k;
+        count += k;
+    }
+    n_roots_p[perm[j]] = count;
+}
+
+// ============================================================================ scan (int32 -> int64 exclusive)
+constexpr int kScanThreads = 1024, kScanPer = 4, kScanTile = kScanThreads * kScanPer;
+
+__device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t* warp_tot, int64_t* total) {
+    const int t = threadIdx.x;
+    int64_t incl = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffff, incl, o);
+        if ((t & 31) >= o) incl += y;
+    }
+    if ((t & 31) == 31) warp_tot[t >> 5] = incl;
+    __syncthreads();
+    if (t < 32) {
+        const int64_t w = warp_tot[t];
+        int64_t wi = w;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t y = __shfl_up_sync(0xffffffff, wi, o);
+            if (t >= o) wi += y;
+        }
+        warp_tot[t] = wi - w;
+        if (t == 31) *total = wi;
+    }
+    __syncthreads();
+    const int64_t r = warp_tot[t >> 5] + incl - v;
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_partial(const int32_t* __restrict__ in, int64_t n,
+                                                               int64_t* __restrict__ part) {
+    __shared__ int64_t wt[32];
+    __shared__ int64_t tot;
+    const int64_t base = blockIdx.x * (int64_t)kScanTile + threadIdx.x * kScanPer;
+    int64_t s = 0;
+#pragma unroll
+    for (int i = 0; i < kScanPer; ++i)
+        if (base + i < n) s += in[base + i];
+    block_excl_scan(s, wt, &tot);
+    if (threadIdx.x == 0) part[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_top(int64_t* __restrict__ part, int64_t nparts) {
+    __shared__ int64_t wt[32];
+    __shared__ int64_t tot;
+    int64_t carry = 0;
+    for (int64_t b0 = 0; b0 < nparts; b0 += kScanThreads) {
+        const int64_t i = b0 + threadIdx.x;
+        const int64_t v = i < nparts ? part[i] : 0;
+        const int64_t e = block_excl_scan(v, wt, &tot);
+        if (i < nparts) part[i] = carry + e;
+        carry += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[nparts] = carry;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_apply(const int32_t* __restrict__ in, int64_t n,
+                                                             const int64_t* __restrict__ part,
+                                                             int64_t* __restrict__ out) {
+    __shared__ int64_t wt[32];
+    __shared__ int64_t tot;
+    const int64_t base = blockIdx.x * (int64_t)kScanTile + threadIdx.x * kScanPer;
+    int64_t v[kScanPer];
+    int64_t s = 0;
+#pragma unroll
+    for (int i = 0; i < kScanPer; ++i) {
+        v[i] = (base + i < n) ? in[base + i] : 0;
+        s += v[i];
+    }
+    int64_t run = part[blockIdx.x] + block_excl_scan(s, wt, &tot);
+#pragma unroll
+    for (int i = 0; i < kScanPer; ++i) {
+        if (base + i < n) out[base + i] = run;
+        run += v[i];
+    }
+    const int64_t nblocks = n > 0 ? (n + kScanTile - 1) / kScanTile : 1;
+    if (blockIdx.x == nblocks - 1 && threadIdx.x == 0) out[n] = part[nblocks];
+}
+
+// ============================================================================ compaction
+__device__ __forceinline__ void store_root(fsk_root* dst, float4 xr, float4 ja, float4 jb, float jc, int bone,
+                                           int iters) {
+    float4* d = reinterpret_cast<float4*>(dst);
+    d[0] = xr;  // x[3], residual
+    d[1] = ja;  // J~[0..3]
+    d[2] = jb;  // J~[4..7]
+    d[3] = make_float4(jc, __int_as_float(bone), __int_as_float(iters), 0.f);
+}
+
+// Kept roots of each query, in bone order, at offsets[p] (CorrespondenceSet::roots).
+// Records at index >= cap are dropped (the caller checks offsets[N] <= cap).
+__global__ void __launch_bounds__(256) k_emit(int64_t n, int nb, SearchPlanes sp, const int* __restrict__ perm,
+                                              const int64_t* __restrict__ offs, fsk_root* __restrict__ roots,
+                                              int64_t cap) {
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    int64_t o = offs[perm[j]];
+    for (int b = 0; b < nb; ++b) {
+        const int64_t q = (int64_t)b * n + j;
+        if (!sp.keep[q]) continue;
+        if (o < cap) store_root(roots + o, sp.xr[q], sp.ja[q], sp.jb[q], sp.jc[q], b, sp.meta[q] & 0xff);
+        ++o;
+    }
+}
+
+// Dense per-(point, init) form, point-major (fsk_search_out). One thread per solve.
+struct DenseOut {
+    float* x_c;
+    float* jinv;
+    float* resid;
+    uint8_t* iters;
+    uint8_t* converged;
+    uint8_t* keep;
+    int32_t* n_roots;
+};
+
+__global__ void __launch_bounds__(256) k_scatter_dense(int64_t n, int nb, SearchPlanes sp, const int* __restrict__ perm,
+                                                       DenseOut d) {
+    const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q >= n * nb) return;
+    const int b = (int)(q / n);
+    const int64_t j = q - (int64_t)b * n;
+    const int64_t s = (int64_t)perm[j] * nb + b;
+    const float4 xr = sp.xr[q];
+    if (d.x_c) {
+        d.x_c[3 * s] = xr.x;
+        d.x_c[3 * s + 1] = xr.y;
+        d.x_c[3 * s + 2] = xr.z;
+    }
+    if (d.resid) d.resid[s] = xr.w;
+    if (d.jinv) {
+        const float4 a = sp.ja[q], c = sp.jb[q];
+        float* J = d.jinv + 9 * s;
+        J[0] = a.x; J[1] = a.y; J[2] = a.z; J[3] = a.w;
+        J[4] = c.x; J[5] = c.y; J[6] = c.z; J[7] = c.w;
+        J[8] = sp.jc[q];
+    }
+    const uint16_t m = sp.meta[q];
+    if (d.iters) d.iters[s] = (uint8_t)(m & 0xff);
+    d.converged[s] = (uint8_t)(m >> 8);
+    if (d.keep) d.keep[s] = sp.keep[q];
+}
+
+// Compaction of a caller-held dense result (fsk_compact_roots).
+__global__ void __launch_bounds__(256) k_emit_dense(int64_t n, int nb, DenseOut d, const int64_t* __restrict__ offs,
+                                                    fsk_root* __restrict__ roots) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    int64_t o = offs[p];
+    for (int i = 0; i < nb; ++i) {
+        const int64_t s = p * nb + i;
+        if (!d.keep[s]) continue;
+        const float* J = d.jinv ? d.jinv + 9 * s : nullptr;
+        store_root(roots + o, make_float4(d.x_c[3 * s], d.x_c[3 * s + 1], d.x_c[3 * s + 2], d.resid ? d.resid[s] : 0.f),
+                   J ? make_float4(J[0], J[1], J[2], J[3]) : make_float4(0.f, 0.f, 0.f, 0.f),
+                   J ? make_float4(J[4], J[5], J[6], J[7]) : make_float4(0.f, 0.f, 0.f, 0.f), J ? J[8] : 0.f, i,
+                   d.iters ? d.iters[s] : 0);
+        ++o;
+    }
+}
+
+// ============================================================================ E
+__global__ void __launch_bounds__(256) k_eval_points(Planes P, GridP g, const float* __restrict__ x, int64_t n,
+                                                     float* __restrict__ t12, float* __restrict__ dout,
+                                                     float* __restrict__ jac) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const float x0 = x[3 * p], x1 = x[3 * p + 1], x2 = x[3 * p + 2];
+    float T[12], J[9], d[3];
+    jacobian_and_T(P, g, x0, x1, x2, T, J);
+    apply_T(T, x0, x1, x2, d);
+    if (t12)
+        for (int e = 0; e < 12; ++e) t12[12 * p + e] = T[e];
+    if (dout)
+        for (int e = 0; e < 3; ++e) dout[3 * p + e] = d[e];
+    if (jac)
+        for (int e = 0; e < 9; ++e) jac[9 * p + e] = J[e];
+}
+
+// init_states (correspondence.cpp:58-70): one thread per (point, bone), point-major output.
+__global__ void __launch_bounds__(256) k_init_states(Planes P, GridP g, const float* __restrict__ bones,
+                                                     const float* __restrict__ pts, int64_t n, float* __restrict__ x0o,
+                                                     float* __restrict__ jo) {
+    const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (s >= n * g.nb) return;
+    const int64_t p = s / g.nb;
+    const int bone = (int)(s - p * g.nb);
+    float x0, x1, x2, Ji[9], T[12];
+    solve_init(P, g, bones + 12 * bone, pts[3 * p], pts[3 * p + 1], pts[3 * p + 2], x0, x1, x2, Ji, T);
+    if (x0o) {
+        x0o[3 * s] = x0;
+        x0o[3 * s + 1] = x1;
+        x0o[3 * s + 2] = x2;
+    }
+    if (jo)
+        for (int e = 0; e < 9; ++e) jo[9 * s + e] = Ji[e];
+}
+
+// ============================================================================ host pipeline
+namespace {
+
+int64_t vertex_count(const GridP& g) { return (int64_t)g.nx * g.ny * g.nz; }
+
+Planes planes_scratch(fsk_ctx* ctx, const GridP& g) {
+    const int64_t V = vertex_count(g);
+    Planes P;
+    P.p = (const float*)scratch(ctx, kPlanes, 3 * V * 8 * sizeof(float));
+    P.stride = V * 8;
+    return P;
+}
+
+void run_precompute(fsk_ctx* ctx, const float* w, const GridP& g, const float* bones, float* tg, bool planes,
+                    cudaStream_t st) {
+    const int64_t V = vertex_count(g);
+    float4* pl = planes ? (float4*)planes_scratch(ctx, g).p : nullptr;
+    FSK_LAUNCH(ctx, st, k_precompute, blocks_for(V, 256), 256, g.nb * 12 * sizeof(float), w, bones, g.nb, g.nx, V,
+               reinterpret_cast<float4*>(tg), pl);
+}
+
+Planes run_relayout(fsk_ctx* ctx, const float* tg, const GridP& g, cudaStream_t st) {
+    const int64_t V = vertex_count(g);
+    Planes P = planes_scratch(ctx, g);
+    FSK_LAUNCH(ctx, st, k_relayout, blocks_for(V, 256), 256, 0, reinterpret_cast<const float4*>(tg), g.nx, V,
+               (float4*)P.p);
+    return P;
+}
+
+struct SearchState {
+    SearchPlanes sp;
+    int* perm;
+    int32_t* n_roots_p;
+};
+
+// sort + K2 + dedup into the ctx's search planes.
+SearchState run_search(fsk_ctx* ctx, const Planes& P, const GridP& g, const float* bones, const float* pts, int64_t n,
+                       const SearchP& sp, int flags, cudaStream_t st) {
+    if (n >= (int64_t(1) << 31) / std::max(1, g.nb)) fail(FSK_EINVAL, "fsk: too many points for one call (split the batch)");
+    const int64_t S = std::max<int64_t>(1, n * g.nb);
+    SearchState s;
+    s.sp.xr = (float4*)scratch(ctx, kOXr, S * sizeof(float4));
+    s.sp.ja = (float4*)scratch(ctx, kOJa, S * sizeof(float4));
+    s.sp.jb = (float4*)scratch(ctx, kOJb, S * sizeof(float4));
+    s.sp.jc = (float*)scratch(ctx, kOJc, S * sizeof(float));
+    s.sp.meta = (uint16_t*)scratch(ctx, kOMeta, S * sizeof(uint16_t));
+    s.sp.keep = (uint8_t*)scratch(ctx, kOKeep, S);
+    s.perm = (int*)scratch(ctx, kPerm, std::max<int64_t>(1, n) * sizeof(int));
+    s.n_roots_p = (int32_t*)scratch(ctx, kNRoots, std::max<int64_t>(1, n) * sizeof(int32_t));
+    if (n == 0) return s;
+    float4* xs = (float4*)scratch(ctx, kXs, n * sizeof(float4));
+    if (!(flags & FSK_SEARCH_NO_SORT)) {
+        int* hist = (int*)scratch(ctx, kHist, kSortBuckets * sizeof(int));
+        int* bbox = (int*)scratch(ctx, kBbox, 6 * sizeof(int));
+        uint16_t* keys = (uint16_t*)scratch(ctx, kKeys, n * sizeof(uint16_t));
+        FSK_LAUNCH(ctx, st, k_sort_init, 32, 1024, 0, hist, bbox);
+        const unsigned gb = (unsigned)std::min<int64_t>(blocks_for(n, 256), (int64_t)ctx->sm_count * 8);
+        FSK_LAUNCH(ctx, st, k_sort_bbox, gb, 256, 0, pts, n, bbox);
+        FSK_LAUNCH(ctx, st, k_sort_hist, blocks_for(n, 256), 256, 0, pts, n, bbox, keys, hist);
+        FSK_LAUNCH(ctx, st, k_sort_scan, 1, 1024, 0, hist);
+        FSK_LAUNCH(ctx, st, k_sort_scatter, blocks_for(n, 256), 256, 0, pts, keys, n, hist, s.perm, xs);
+    } else {
+        FSK_LAUNCH(ctx, st, k_identity_order, blocks_for(n, 256), 256, 0, pts, n, s.perm, xs);
+    }
+    const int bpb = (int)blocks_for(n, kSearchBlock);
+    const int64_t nblocks = (int64_t)bpb * g.nb;
+    if (nblocks >= (int64_t(1) << 31)) fail(FSK_EINVAL, "fsk: search grid too large");
+    FSK_LAUNCH(ctx, st, k_search, (unsigned)nblocks, kSearchBlock, 0, P, g, bones, xs, n, bpb, sp, s.sp);
+    FSK_LAUNCH(ctx, st, k_dedup, blocks_for(n, 256), 256, 0, n, g.nb, sp.dedup2, s.sp, s.perm, s.n_roots_p);
+    return s;
+}
+
+void run_scan(fsk_ctx* ctx, const int32_t* in, int64_t n, int64_t* out, cudaStream_t st) {
+    const int64_t nb = std::max<int64_t>(1, (n + kScanTile - 1) / kScanTile);
+    int64_t* part = (int64_t*)scratch(ctx, kScanPart, (nb + 1) * sizeof(int64_t));
+    FSK_LAUNCH(ctx, st, k_scan_partial, (unsigned)nb, kScanThreads, 0, in, n, part);
+    FSK_LAUNCH(ctx, st, k_scan_top, 1, kScanThreads, 0, part, nb);
+    FSK_LAUNCH(ctx, st, k_scan_apply, (unsigned)nb, kScanThreads, 0, in, n, part, out);
+}
+
+void compact(fsk_ctx* ctx, const SearchState& s, int64_t n, int nb, int64_t* offsets, fsk_root* roots, int64_t cap,
+             cudaStream_t st) {
+    run_scan(ctx, s.n_roots_p, n, offsets, st);
+    if (n > 0 && roots && cap > 0)
+        FSK_LAUNCH(ctx, st, k_emit, blocks_for(n, 256), 256, 0, n, nb, s.sp, s.perm, offsets, roots, cap);
+}
+
+void check_search_args(const GridP& g, int32_t n_bones_pose, const void* grid_ptr, const char* mismatch) {
+    if (n_bones_pose < 1) fail(FSK_EINVAL, "search: no bone transforms");
+    if (!grid_ptr) fail(FSK_EINVAL, "search: voxel variant needs skinning and transform grids");
+    if (n_bones_pose != g.nb) fail(FSK_EINVAL, mismatch);
+}
+
+}  // namespace
+}  // namespace fsk
+
+using namespace fsk;
+
+extern "C" {
+
+int fsk_precompute_tgrid(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* desc, const float* bones,
+                         int32_t n_bones_pose, float* tgrid, void* stream) {
+    return guard([&] {
+        set_device(ctx);
+        const GridP g = make_grid(desc);
+        if (n_bones_pose != g.nb) fail(FSK_EINVAL, "precompute_transform_grid: bone count mismatch");
+        if (!weights || !bones || !tgrid) fail(FSK_EINVAL, "fsk: null buffer");
+        run_precompute(ctx, weights, g, bones, tgrid, false, (cudaStream_t)stream);
+    });
+}
+
+int fsk_search_fwd(fsk_ctx* ctx, const float* tgrid, const fsk_grid_desc* desc, const float* bones,
+                   int32_t n_bones_pose, const float* points, int64_t n, const fsk_search_opts* opts,
+                   fsk_search_out* out, void* stream) {
+    return guard([&] {
+        set_device(ctx);
+        // check_context (correspondence.cpp:29-41), then validate (:19-25)
+        const GridP g = make_grid(desc);
+        check_search_args(g, n_bones_pose, tgrid, "search: grid bone count mismatch");
+        const SearchP sp = make_search(opts);
+        if (!out || !out->converged) fail(FSK_EINVAL, "fsk: search output needs a converged mask");
+        if (n < 0) fail(FSK_EINVAL, "fsk: negative point count");
+        if (n > 0 && (!points || !bones)) fail(FSK_EINVAL, "fsk: null buffer");
+        if (n == 0) return;
+        cudaStream_t st = (cudaStream_t)stream;
+        const Planes P = run_relayout(ctx, tgrid, g, st);
+        const SearchState s = run_search(ctx, P, g, bones, points, n, sp, opts->flags, st);
+        DenseOut d{out->x_c, out->jinv, out->resid, out->iters, out->converged, out->keep, out->n_roots};
+        FSK_LAUNCH(ctx, st, k_scatter_dense, blocks_for(n * g.nb, 256), 256, 0, n, g.nb, s.sp, s.perm, d);
+        if (out->n_roots)
+            cuda_check(cudaMemcpyAsync(out->n_roots, s.n_roots_p, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st),
+                       "cudaMemcpyAsync");
+    });
+}
+
+int fsk_batch_search(fsk_ctx* ctx, const float* tgrid, const fsk_grid_desc* desc, const float* bones,
+                     int32_t n_bones_pose, const float* points, int64_t n, const fsk_search_opts* opts,
+                     int64_t* offsets, fsk_root* roots, int64_t cap, void* stream) {
+    return guard([&] {
+        set_device(ctx);
+        const GridP g = make_grid(desc);
+        check_search_args(g, n_bones_pose, tgrid, "search: grid bone count mismatch");
+        const SearchP sp = make_search(opts);
+        if (n < 0) fail(FSK_EINVAL, "fsk: negative point count");
+        if (!offsets || (n > 0 && (!points || !bones))) fail(FSK_EINVAL, "fsk: null buffer");
+        cudaStream_t st = (cudaStream_t)stream;
+        const Planes P = run_relayout(ctx, tgrid, g, st);
+        const SearchState s = run_search(ctx, P, g, bones, points, n, sp, opts->flags, st);
+        compact(ctx, s, n, g.nb, offsets, roots, cap, st);
+    });
+}
+
+int fsk_deform(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* desc, const float* bones,
+               int32_t n_bones_pose, const float* points, int64_t n, const fsk_search_opts* opts, float* tgrid,
+               int64_t* offsets, fsk_root* roots, int64_t cap, void* stream) {
+    return guard([&] {
+        set_device(ctx);
+        const GridP g = make_grid(desc);
+        check_search_args(g, n_bones_pose, weights, "precompute_transform_grid: bone count mismatch");
+        const SearchP sp = make_search(opts);
+        if (n < 0) fail(FSK_EINVAL, "fsk: negative point count");
+        if (!offsets || !bones || (n > 0 && !points)) fail(FSK_EINVAL, "fsk: null buffer");
+        cudaStream_t st = (cudaStream_t)stream;
+        run_precompute(ctx, weights, g, bones, tgrid, true, st);
+        const SearchState s = run_search(ctx, planes_scratch(ctx, g), g, bones, points, n, sp, opts->flags, st);
+        compact(ctx, s, n, g.nb, offsets, roots, cap, st);
+    });
+}
+
+int fsk_compact_roots(fsk_ctx* ctx, const fsk_search_out* dense, int64_t n, int32_t n_init, int64_t* offsets,
+                      fsk_root* roots, int64_t cap, int64_t* total_out, void* stream) {
+    return guard([&] {
+        set_device(ctx);
+        if (!dense || !dense->keep || !dense->x_c || !dense->n_roots)
+            fail(FSK_EINVAL, "fsk: compaction needs x_c, keep and n_roots");
+        if (!offsets || !total_out) fail(FSK_EINVAL, "fsk: null buffer");
+        cudaStream_t st = (cudaStream_t)stream;
+        run_scan(ctx, dense->n_roots, n, offsets, st);
+        int64_t total = 0;
+        cuda_check(cudaMemcpyAsync(&total, offsets + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
+        cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+        *total_out = total;
+        if (total > cap) fail(FSK_EINVAL, "fsk: root buffer too small");
+        if (n > 0 && total > 0) {
+            if (!roots) fail(FSK_EINVAL, "fsk: null buffer");
+            DenseOut d{dense->x_c, dense->jinv, dense->resid, dense->iters, dense->converged, dense->keep,
+                       dense->n_roots};
+            FSK_LAUNCH(ctx, st, k_emit_dense, blocks_for(n, 256), 256, 0, n, n_init, d, offsets, roots);
+        }
+    });
+}
+
+int fsk_deform_host(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* desc, const float* bones,
+                    int32_t n_bones_pose, const float* points, int64_t n, const fsk_search_opts* opts,
+                    int64_t* offsets, fsk_root* roots, int64_t cap, int64_t* total_out, void* stream) {
+    return guard([&] {
+        set_device(ctx);
+        const GridP g = make_grid(desc);
+        check_search_args(g, n_bones_pose, weights, "precompute_transform_grid: bone count mismatch");
+        const SearchP sp = make_search(opts);
+        if (n < 0) fail(FSK_EINVAL, "fsk: negative point count");
+        if (!bones || !offsets || !total_out || (n > 0 && !points)) fail(FSK_EINVAL, "fsk: null buffer");
+        cudaStream_t st = (cudaStream_t)stream;
+        const int64_t V = vertex_count(g);
+        const int nb = g.nb;
+        float* dW = (float*)scratch(ctx, kHW, V * nb * sizeof(float));
+        float* dB = (float*)scratch(ctx, kHB, nb * 12 * sizeof(float));
+        float* dP = (float*)scratch(ctx, kHP, std::max<int64_t>(1, n) * 3 * sizeof(float));
+        int64_t* dOff = (int64_t*)scratch(ctx, kHOffs, (n + 1) * sizeof(int64_t));
+        // every root a query can have fits: no second pass after the count is known
+        const int64_t rcap = std::max<int64_t>(1, n * nb);
+        fsk_root* dR = (fsk_root*)scratch(ctx, kHRoots, rcap * sizeof(fsk_root));
+        cuda_check(cudaMemcpyAsync(dW, weights, V * nb * sizeof(float), cudaMemcpyHostToDevice, st), "H2D weights");
+        cuda_check(cudaMemcpyAsync(dB, bones, nb * 12 * sizeof(float), cudaMemcpyHostToDevice, st), "H2D bones");
+        if (n > 0)
+            cuda_check(cudaMemcpyAsync(dP, points, n * 3 * sizeof(float), cudaMemcpyHostToDevice, st), "H2D points");
+        run_precompute(ctx, dW, g, dB, nullptr, true, st);
+        const SearchState s = run_search(ctx, planes_scratch(ctx, g), g, dB, dP, n, sp, opts->flags, st);
+        compact(ctx, s, n, nb, dOff, dR, rcap, st);
+        cuda_check(cudaMemcpyAsync(offsets, dOff, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st), "D2H offsets");
+        cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+        const int64_t total = offsets[n];
+        *total_out = total;
+        if (total > cap) fail(FSK_EINVAL, "fsk: root buffer too small");
+        if (total > 0) {
+            if (!roots) fail(FSK_EINVAL, "fsk: null buffer");
+            cuda_check(cudaMemcpyAsync(roots, dR, total * sizeof(fsk_root), cudaMemcpyDeviceToHost, st), "D2H roots");
+            cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+        }
+    });
+}
+
+int fsk_init_states(fsk_ctx* ctx, const float* tgrid, const fsk_grid_desc* desc, const float* bones,
+                    int32_t n_bones_pose, const float* points, int64_t n, float* x0, float* jinv0, void* stream) {
+    return guard([&] {
+        set_device(ctx);
+        const GridP g = make_grid(desc);
+        check_search_args(g, n_bones_pose, tgrid, "search: grid bone count mismatch");
+        if (n < 0) fail(FSK_EINVAL, "fsk: negative point count");
+        if (n == 0) return;
+        if (!points || !bones) fail(FSK_EINVAL, "fsk: null buffer");
+        cudaStream_t st = (cudaStream_t)stream;
+        const Planes P = run_relayout(ctx, tgrid, g, st);
+        FSK_LAUNCH(ctx, st, k_init_states, blocks_for(n * g.nb, 256), 256, 0, P, g, bones, points, n, x0, jinv0);
+    });
+}
+
+int fsk_eval_points(fsk_ctx* ctx, const float* tgrid, const fsk_grid_desc* desc, const float* x, int64_t n,
+                    float* t12, float* d, float* jac, void* stream) {
+    return guard([&] {
+        set_device(ctx);
+        const GridP g = make_grid(desc);
+        if (n < 0) fail(FSK_EINVAL, "fsk: negative point count");
+        if (n == 0) return;
+        if (!tgrid || !x) fail(FSK_EINVAL, "fsk: null buffer");
+        cudaStream_t st = (cudaStream_t)stream;
+        const Planes P = run_relayout(ctx, tgrid, g, st);
+        FSK_LAUNCH(ctx, st, k_eval_points, blocks_for(n, 256), 256, 0, P, g, x, n, t12, d, jac);
+    });
+}
+
+}  // extern "C"

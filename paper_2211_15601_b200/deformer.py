@@ -180,6 +180,49 @@ class Deformer:
                                     ctypes.byref(opts.c()), ctypes.byref(co), _stream(self.device)))
         return out
 
+    def alloc_roots(self, n, nb, cap=None):
+        """Device CorrespondenceSet buffers: offsets [N+1] int64, roots [cap,16] float32
+        (fsk_root records: x(3), residual, J~(9), bone, iterations, pad)."""
+        cap = n * nb if cap is None else cap
+        return (torch.empty((n + 1,), dtype=torch.int64, device=self.device),
+                torch.empty((max(cap, 1), 16), dtype=torch.float32, device=self.device))
+
+    def batch_search_roots(self, tgrid, dims, bbox, bones, points, opts: SearchOptions, out=None):
+        """``batch_search`` straight to CorrespondenceSets on the device (fsk_batch_search):
+        returns (offsets, roots); roots of query p are roots[offsets[p]:offsets[p+1]]."""
+        nb, n = bones.numel() // 12, points.shape[0]
+        offsets, roots = out if out is not None else self.alloc_roots(n, nb)
+        desc = grid_desc(dims, bbox, nb)
+        check(self.L.fsk_batch_search(self._ctx, _ptr(_f32(tgrid, "tgrid", self.device)), ctypes.byref(desc),
+                                      _ptr(_f32(bones, "bones", self.device)), nb,
+                                      _ptr(_f32(points, "points", self.device)), n, ctypes.byref(opts.c()),
+                                      _ptr(offsets), _ptr(roots), roots.shape[0], _stream(self.device)))
+        return offsets, roots
+
+    def deform(self, weights, dims, bbox, bones, points, opts: SearchOptions, tgrid=None, out=None):
+        """One deformer frame on device buffers (fsk_deform): precompute_transform_grid +
+        batch_search → (offsets, roots). ``tgrid`` [V,12] receives the transform grid if given."""
+        nb, n = bones.numel() // 12, points.shape[0]
+        offsets, roots = out if out is not None else self.alloc_roots(n, nb)
+        desc = grid_desc(dims, bbox, nb)
+        check(self.L.fsk_deform(self._ctx, _ptr(_f32(weights, "weights", self.device)), ctypes.byref(desc),
+                                _ptr(_f32(bones, "bones", self.device)), nb, _ptr(_f32(points, "points", self.device)),
+                                n, ctypes.byref(opts.c()), _ptr(tgrid), _ptr(offsets), _ptr(roots), roots.shape[0],
+                                _stream(self.device)))
+        return offsets, roots
+
+    def search_bwd_roots(self, dims, bbox, n_bones, roots, root_index, grad_xc, deterministic=False, out=None):
+        """Backward from compact roots: root_index [N] int64 into ``roots`` (or -1)."""
+        desc = grid_desc(dims, bbox, n_bones)
+        V = desc.nx * desc.ny * desc.nz
+        if out is None:
+            out = torch.empty((V, 12), dtype=torch.float32, device=self.device)
+        ri = root_index.to(device=self.device, dtype=torch.int64).contiguous()
+        check(self.L.fsk_search_bwd_roots(self._ctx, ctypes.byref(desc), _ptr(roots), _ptr(ri),
+                                          _ptr(_f32(grad_xc, "grad_xc", self.device)), grad_xc.shape[0], _ptr(out),
+                                          1 if deterministic else 0, _stream(self.device)))
+        return out
+
     def compact_roots(self, dense, n, nb):
         """Kept roots in CorrespondenceSet form: (offsets [N+1] int64, roots [M,16] float32 view of
         fsk_root records: x(3), residual, J~(9), bone, iterations, pad)."""

@@ -1,0 +1,99 @@
+"""Multi-GPU plumbing: posed points shard across ranks (one process per GPU, NCCL).
+
+The correspondence search has no data-path exchange — every (point, init) solve reads
+only the immutable transform grid and bones — so the forward is pure
+data parallelism over contiguous point ranges, the partition of ``parallel_for``
+(``proj/include/fskin/parallel.hpp:28-29``). Collectives appear only at the edges:
+
+* before K1: ``broadcast`` of the weight grid and bones from the rank that owns the pose
+  (each rank then runs K1 locally — cheaper than broadcasting per-pose T grids);
+* after K2 (optional): ``all_gather`` of the per-rank dense results (unequal shard sizes
+  are padded to the largest shard);
+* backward: ``all_reduce(SUM)`` of dL/dT [V,12] before the local dL/dw contraction.
+
+The compute functions are injected so the same plumbing is exercised on CPU with the
+``gloo`` backend in tests (tests/test_dist_gloo.py) and on GPUs with NCCL.
+"""
+from __future__ import annotations
+
+from typing import Callable, Dict, Optional
+
+import torch
+import torch.distributed as dist
+
+
+def shard_range(n: int, rank: int, world: int):
+    """``parallel_for``'s static contiguous partition (parallel.hpp:28-29)."""
+    return n * rank // world, n * (rank + 1) // world
+
+
+def broadcast_inputs(tensors, src: int = 0, group=None):
+    """Broadcast the pose inputs (weight grid, bones) from ``src`` to every rank, in place."""
+    for t in tensors:
+        dist.broadcast(t, src, group=group)
+    return tensors
+
+
+def gather_dense(local: Dict[str, Optional[torch.Tensor]], n_total: int, group=None) -> Dict[str, torch.Tensor]:
+    """All-gather per-rank dense search results (leading dim = local points) into the
+    full [n_total, ...] arrays in global point order."""
+    world = dist.get_world_size(group)
+    sizes = [shard_range(n_total, r, world) for r in range(world)]
+    maxn = max(b - a for a, b in sizes)
+    out = {}
+    for k, t in local.items():
+        if t is None:
+            out[k] = None
+            continue
+        pad = torch.zeros((maxn, *t.shape[1:]), dtype=t.dtype, device=t.device)
+        pad[: t.shape[0]] = t
+        bufs = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(bufs, pad, group=group)
+        out[k] = torch.cat([bufs[r][: b - a] for r, (a, b) in enumerate(sizes)], 0)
+    return out
+
+
+def allreduce_grad(grad: torch.Tensor, group=None) -> torch.Tensor:
+    dist.all_reduce(grad, op=dist.ReduceOp.SUM, group=group)
+    return grad
+
+
+def sharded_forward(points_full: torch.Tensor, search_fn: Callable[[torch.Tensor], Dict[str, torch.Tensor]],
+                    gather: bool = True, group=None):
+    """Run ``search_fn`` on this rank's contiguous shard of ``points_full``; optionally
+    all-gather the dense results. Returns (results, (begin, end))."""
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    a, b = shard_range(points_full.shape[0], rank, world)
+    local = search_fn(points_full[a:b].contiguous())
+    if gather:
+        return gather_dense(local, points_full.shape[0], group=group), (a, b)
+    return local, (a, b)
+
+
+def sharded_backward(local_grad_fn: Callable[[], torch.Tensor],
+                     contract_fn: Optional[Callable[[torch.Tensor], torch.Tensor]] = None, group=None):
+    """Per-rank dL/dT from the local roots, summed over ranks, then (optionally) the local
+    dL/dw contraction — identical on every rank."""
+    g = allreduce_grad(local_grad_fn(), group=group)
+    return (g, contract_fn(g)) if contract_fn else (g, None)
+
+
+class MultiGPUDeformer:
+    """One rank of the sharded deformer over ``paper_2211_15601_b200.deformer.Deformer``."""
+
+    def __init__(self, deformer, group=None):
+        self.D, self.group = deformer, group
+
+    def forward(self, weights, dims, bbox, bones, points_full, opts, src=0, gather=True):
+        broadcast_inputs([weights, bones], src=src, group=self.group)
+        tg = self.D.precompute_transform_grid(weights, dims, bbox, bones)
+        res, rng = sharded_forward(points_full,
+                                   lambda x: self.D.batch_search(tg, dims, bbox, bones, x, opts),
+                                   gather=gather, group=self.group)
+        return tg, res, rng
+
+    def backward(self, dims, bbox, bones, local_dense, grad_xc_local, root_sel_local, deterministic=False):
+        nb = bones.numel() // 12
+        return sharded_backward(
+            lambda: self.D.search_bwd(dims, bbox, nb, local_dense, grad_xc_local, root_sel_local, deterministic),
+            lambda g: self.D.grad_weights(dims, bbox, g, bones), group=self.group)

@@ -283,3 +283,39 @@ def test_backward_end_to_end_against_oracle_forward(deformer, c3):
     print(f"\nselected-root agreement {same:.5f}  max|dT| {np.abs(gT - rT).max():.3e}")
     assert same >= MASK_AGREE - 1e-3
     assert np.abs(gT - rT).max() <= TOL_GRAD
+
+
+def test_device_correspondence_sets_match_dense_path(deformer, c1):
+    """fsk_batch_search and fsk_deform (device CorrespondenceSets, the bench path) equal the
+    dense per-(point, init) result compacted in bone order."""
+    w, B, x = dev(c1.weights), dev(c1.bones), dev(c1.points)
+    tg = deformer.precompute_transform_grid(w, c1.dims, c1.bbox, B)
+    o = opts_of(c1, 50)
+    d = {k: v.cpu().numpy() for k, v in deformer.batch_search(tg, c1.dims, c1.bbox, B, x, o).items()}
+    keep = np.argwhere(d["keep"] == 1)
+    offs1, roots1 = (t.cpu().numpy() for t in deformer.batch_search_roots(tg, c1.dims, c1.bbox, B, x, o))
+    tg2 = torch.empty_like(tg)
+    offs2, roots2 = (t.cpu().numpy() for t in deformer.deform(w, c1.dims, c1.bbox, B, x, o, tgrid=tg2))
+    np.testing.assert_array_equal(tg2.cpu().numpy(), tg.cpu().numpy())
+    total = int(offs1[-1])
+    assert total == keep.shape[0] == int(offs2[-1])
+    np.testing.assert_array_equal(offs1, offs2)
+    np.testing.assert_array_equal(roots1[:total], roots2[:total])
+    np.testing.assert_array_equal(np.diff(offs1), d["n_roots"])
+    r = roots1[:total]
+    np.testing.assert_array_equal(r[:, :3], d["x_c"][keep[:, 0], keep[:, 1]])
+    np.testing.assert_array_equal(r[:, 3], d["resid"][keep[:, 0], keep[:, 1]])
+    np.testing.assert_array_equal(r[:, 4:13], d["jinv"][keep[:, 0], keep[:, 1]].reshape(-1, 9))
+    np.testing.assert_array_equal(r[:, 13].view(np.int32), keep[:, 1])
+    np.testing.assert_array_equal(r[:, 14].view(np.int32), d["iters"][keep[:, 0], keep[:, 1]])
+
+
+def test_backward_from_compact_roots_matches_dense(deformer, c3):
+    sc, B, dense, sel, v = c3
+    w, x = dev(sc.weights), dev(sc.points)
+    offs, roots = deformer.deform(w, sc.dims, sc.bbox, B, x, opts_of(sc, 50))
+    offs_h = offs.cpu().numpy()
+    ridx = np.where(sel >= 0, offs_h[:-1], -1).astype(np.int64)  # first kept root = first record
+    a = deformer.search_bwd(sc.dims, sc.bbox, sc.n_bones, dense, dev(v), dev(sel), deterministic=True)
+    b = deformer.search_bwd_roots(sc.dims, sc.bbox, sc.n_bones, roots, dev(ridx), dev(v), deterministic=True)
+    np.testing.assert_array_equal(a.cpu().numpy(), b.cpu().numpy())
