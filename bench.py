@@ -213,6 +213,7 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    D.search_stats(reset=True)
     clocks.start()
     launches0 = D.launch_count
     for i in range(args.steps):
@@ -228,29 +229,33 @@ def run_ours(args, rank, world, local_rank):
     D.set_profiling(False)
     step_ms = [a.elapsed_time(b) for a, b in evs]
     total_ms = float(np.sum(step_ms))
-    k2_ms, k2_n = D.prof_read("k_search", reset=False)
-    k1_ms, k1_n = D.prof_read("k_precompute_tgrid", reset=False)
+    k2_ms, k2_n = D.prof_read("k_search_fast", reset=False)
+    k2e_ms, k2e_n = D.prof_read("k_search_escalated", reset=False)
+    k1_ms, k1_n = D.prof_read("k_precompute", reset=False)
     all_ms, _ = D.prof_read(None, reset=True)
     if world > 1:
         t = torch.tensor([total_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
 
-    # algorithmic work of one K2 launch (deterministic: identical every step)
-    # per-solve iteration counts (deterministic: identical to the timed launches)
-    out = D.batch_search(tg, sc.dims, sc.bbox, B, x, opts)
-    iters = out["iters"].to(torch.int64)
-    conv = out["converged"].to(torch.bool)
-    total_roots = int(roots_buf[0][n].item())
-    sum_iters = int(iters.sum().item())
-    n_final = int((conv & (iters > 0)).sum().item())
+    # algorithmic work per step, counted by the kernels themselves (identical every step):
+    # float32 pass (k_search_fast) and float64 escalation pass (k_search_escalated)
+    st = D.search_stats(reset=True)
+    per = max(args.steps, 1)
+    s32, it32, fin32, s64, it64, fin64 = (v / per for v in st)
     solves = n * nb
-    flops = solves * FLOPS_INIT + sum_iters * FLOPS_ITER - n_final * FLOPS_FINAL_SAVING
-    gather = (solves + sum_iters) * GATHER_BYTES
+    flops = s32 * FLOPS_INIT + it32 * FLOPS_ITER - fin32 * FLOPS_FINAL_SAVING
+    flops64 = s64 * FLOPS_INIT + it64 * FLOPS_ITER - fin64 * FLOPS_FINAL_SAVING
+    gather = (s32 + it32) * GATHER_BYTES
     k2_avg = k2_ms / max(k2_n, 1)
     achieved = flops / (k2_avg * 1e-3) / 1e12
     V = w.shape[0]
     k1_bytes = V * (4 * nb + 48)
+    total_roots = int(roots_buf[0][n].item())
+    dense = D.batch_search(tg, sc.dims, sc.bbox, B, x, opts)  # final (post-escalation) per-solve state
+    conv_frac = float(dense["converged"].float().mean())
+    mean_iters = float(dense["iters"].float().mean())
+    D.search_stats(reset=True)
 
     value = world * solves * args.steps / (total_ms * 1e-3)
     line = {
@@ -263,16 +268,21 @@ def run_ours(args, rank, world, local_rank):
                    "max_iters": args.max_iters, "sort": not args.no_sort,
                    "l2": "flushed between steps (256 MiB fill outside the per-step CUDA events)",
                    "parallelism": f"points sharded across {world} GPU(s), no data-path collective"},
-        "roofline": {"bound": "fp32", "kernel": "k_search", "achieved": achieved, "peak": peak_fp32,
+        "roofline": {"bound": "fp32", "kernel": "k_search_fast", "achieved": achieved, "peak": peak_fp32,
                      "unit": "TFLOP/s", "frac": achieved / peak_fp32, "traffic": None,
                      "peak_source": "measured live: FFMA-chain kernel over all SMs (fsk_measure_fp32_peak); "
                                     "MEASURED_PEAKS.json has no FP32 figure",
                      "algorithmic_flops_per_launch": flops, "avg_launch_ms": k2_avg,
-                     "mean_iters_per_solve": sum_iters / solves, "converged_frac": float(conv.float().mean()),
+                     "fp32_pass": {"solves": s32, "iterations": it32},
+                     "fp64_escalation": {"solves": s64, "frac_of_solves": s64 / solves, "iterations": it64,
+                                         "flops": flops64, "avg_launch_ms": k2e_ms / max(k2e_n, 1),
+                                         "achieved_TFLOPs_f64": flops64 / max(k2e_ms / max(k2e_n, 1), 1e-9) / 1e9},
+                     "mean_final_iters_per_solve": mean_iters, "converged_frac": conv_frac,
                      "kept_roots_per_query": total_roots / n,
                      "gather": {"requested_bytes_per_launch": gather,
                                 "achieved_GBps": gather / (k2_avg * 1e-3) / 1e9},
                      "k2_share_of_step": k2_ms / max(all_ms, 1e-9),
+                     "k2_escalated_share_of_step": k2e_ms / max(all_ms, 1e-9),
                      "k1": {"bytes_per_launch": k1_bytes, "avg_launch_ms": k1_ms / max(k1_n, 1),
                             "achieved_GBps": k1_bytes / (k1_ms / max(k1_n, 1) * 1e-3) / 1e9}},
         "gpu_launches": launches,

@@ -6,18 +6,22 @@
  *   FSK_OK (0)            success
  *   FSK_EINVAL (1)        invalid argument — fsk_last_error() holds the reference's
  *                         std::invalid_argument message text where one exists
- *   FSK_ECUDA (2)         CUDA / NCCL / allocation failure (std::runtime_error)
+ *   FSK_ECUDA (2)         CUDA / allocation failure (std::runtime_error)
  *   FSK_ENODEV (3)        no usable sm_100 device (the library has no CPU fallback)
  * Device pointers ("dev") must live on the context's device. Calls are stream-ordered
  * on `stream` (a cudaStream_t; NULL = legacy default stream) and asynchronous unless
  * stated otherwise. A context is not thread-safe; distinct (ctx, stream) pairs are.
  *
- * Layouts (identical to the reference's storage, in float32):
+ * Layouts (the reference's storage order; float32 unless noted):
  *   weights  [V][n_b]     x-fastest vertex order, bone innermost (skinning.hpp:54-77)
  *   tgrid    [V][12]      rows of the blended 3x4 [R|t], x-fastest (deformer.hpp:35-39)
  *   bones    [n_b][12]    rows of RigidTransform [R|t] (geometry.hpp:42-78)
  *   points   [N][3]
  *   per-(point, init) outputs are point-major: [N][n_init][...], init i = bone i.
+ *
+ * Precision: searches run a float32 pass and re-solve in float64 every (point, init)
+ * whose float32 outcome could differ from a float64 solve (long or late-diverging Broyden
+ * trajectories, threshold decisions within float32 noise); see DESIGN.md §precision.
  */
 #ifndef FSK_H_
 #define FSK_H_
@@ -49,13 +53,15 @@ typedef struct fsk_grid_desc {
  * = SearchOptions::defaults_for(bbox) (correspondence.cpp:10-17). */
 typedef struct fsk_search_opts {
     int32_t max_iters;    /* >= 1, <= 255 */
-    float conv_eps;       /* > 0 */
-    float div_eps;        /* > conv_eps */
-    float dedup_dist;     /* >= 0 */
     int32_t flags;        /* FSK_SEARCH_* */
+    double conv_eps;      /* > 0 */
+    double div_eps;       /* > conv_eps */
+    double dedup_dist;    /* >= 0 */
 } fsk_search_opts;
 
-#define FSK_SEARCH_NO_SORT 0x1   /* ablation: skip the spatial ordering of queries */
+#define FSK_SEARCH_NO_SORT 0x1    /* ablation: skip the spatial ordering of queries */
+#define FSK_SEARCH_FP32_ONLY 0x2  /* ablation: float32 only, no float64 escalation */
+#define FSK_SEARCH_FP64 0x4       /* parity mode: every solve in float64 */
 
 /* Dense per-(point, init) search result (the GPU form of Root / CorrespondenceSet,
  * correspondence.hpp:29-42). All pointers dev, [N][n_b] point-major; any may be NULL
@@ -68,8 +74,8 @@ typedef struct fsk_search_out {
     float* resid;         /* [N][n_b] ||d(x)-x'|| at termination (Root::residual) */
     uint8_t* iters;       /* [N][n_b] iterations executed (Root::iterations) */
     uint8_t* converged;   /* [N][n_b] 1 iff residual < conv_eps was reached */
-    uint8_t* keep;        /* [N][n_b] dedup survivors (NULL: dedup skipped) */
-    int32_t* n_roots;     /* [N] kept roots per point (NULL allowed) */
+    uint8_t* keep;        /* [N][n_b] dedup survivors */
+    int32_t* n_roots;     /* [N] kept roots per point */
 } fsk_search_out;
 
 /* Compact root record — one kept Root, in bone order per query (CorrespondenceSet). */
@@ -97,56 +103,65 @@ int fsk_device_sm_count(const fsk_ctx* ctx);
 int fsk_ctx_set_profiling(fsk_ctx* ctx, int on);
 int fsk_ctx_prof_read(fsk_ctx* ctx, const char* name, double* total_ms, int64_t* count, int reset);
 int fsk_measure_fp32_peak(fsk_ctx* ctx, double* tflops);
+/* Search work counters accumulated by the context's searches (synchronizes the device):
+ * out = {float32 solves, float32 Broyden iterations, float32 converged-terminating
+ * iterations, float64 solves, float64 iterations, float64 converged-terminating iterations}. */
+int fsk_ctx_search_stats(fsk_ctx* ctx, uint64_t out[6], int reset);
 
 /* SearchOptions::defaults_for (correspondence.cpp:10-17): conv 1e-5*diag,
  * div 0.5*diag, dedup 1e-2*diag, max_iters 50. */
 fsk_search_opts fsk_search_opts_defaults(const fsk_grid_desc* desc);
 
 /* ---- K1: precompute_transform_grid (deformer.hpp:53-55; deformer.cpp:61-77) -------
- * tgrid[v] = lbs_blend(weights[v], bones) (deformer.cpp:9-19). n_bones_pose must equal
- * desc->n_bones ("precompute_transform_grid: bone count mismatch"). All dev. */
+ * tgrid[v] = lbs_blend(weights[v], bones) (deformer.cpp:9-19) in float32 and/or, into
+ * tgrid64 (double [V][12], the reference's TransformGrid precision), in float64; either
+ * output may be NULL (not both). n_bones_pose must equal desc->n_bones
+ * ("precompute_transform_grid: bone count mismatch"). All dev. */
 int fsk_precompute_tgrid(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* desc,
-                         const float* bones, int32_t n_bones_pose, float* tgrid, void* stream);
+                         const float* bones, int32_t n_bones_pose, float* tgrid, double* tgrid64,
+                         void* stream);
 
 /* ---- K2: batch_search, voxel variant (correspondence.hpp:77-80; correspondence.cpp:178-192)
  * One Broyden solve per (point, bone-init): x0 = B_i^-1 x' (:135), J~0 from the analytic
- * grid Jacobian (:43-54), good-Broyden iterate (:97-124), converged mask, then dedup
- * (:162-176) when out->keep != NULL. points, tgrid, bones dev. N may be 0. */
-int fsk_search_fwd(fsk_ctx* ctx, const float* tgrid, const fsk_grid_desc* desc,
-                   const float* bones, int32_t n_bones_pose, const float* points, int64_t n,
-                   const fsk_search_opts* opts, fsk_search_out* out, void* stream);
+ * grid Jacobian (:43-54), good-Broyden iterate (:97-124), converged mask, dedup (:162-176).
+ * The transform grid is given as float32 `tgrid` and/or float64 `tgrid64` (either may be
+ * NULL, not both); the float64 re-solves read tgrid64 when given (exact parity with an f64
+ * TransformGrid), else the float32 grid widened. points, grids, bones dev. N may be 0. */
+int fsk_search_fwd(fsk_ctx* ctx, const float* tgrid, const double* tgrid64,
+                   const fsk_grid_desc* desc, const float* bones, int32_t n_bones_pose,
+                   const float* points, int64_t n, const fsk_search_opts* opts,
+                   fsk_search_out* out, void* stream);
 
 /* batch_search straight to CorrespondenceSets on the device: K2 + dedup + compaction.
  * offsets [N+1] int64 (dev): roots of query p are roots[offsets[p] .. offsets[p+1]), in bone
  * order (Root::source_bone ascending); offsets[N] = total kept roots. roots (dev) has room for
  * `cap` records; records beyond cap are dropped — check offsets[N] <= cap (N*n_b always
  * suffices). Fully asynchronous (no host synchronization). */
-int fsk_batch_search(fsk_ctx* ctx, const float* tgrid, const fsk_grid_desc* desc,
-                     const float* bones, int32_t n_bones_pose, const float* points, int64_t n,
-                     const fsk_search_opts* opts, int64_t* offsets, fsk_root* roots, int64_t cap,
-                     void* stream);
+int fsk_batch_search(fsk_ctx* ctx, const float* tgrid, const double* tgrid64,
+                     const fsk_grid_desc* desc, const float* bones, int32_t n_bones_pose,
+                     const float* points, int64_t n, const fsk_search_opts* opts,
+                     int64_t* offsets, fsk_root* roots, int64_t cap, void* stream);
 
 /* One frame of the deformer on device buffers — precompute_transform_grid followed by
  * batch_search (what cmd_deform / cmd_bench / train do per pose: fskin_cli.cpp:395-408,
- * :663-678, diff.cpp:278-289): K1 (fused with the gather relayout), K2, dedup, compaction.
- * tgrid [V][12] (dev) receives the reference-layout transform grid, or NULL. Outputs as for
- * fsk_batch_search. Fully asynchronous. */
+ * :663-678, diff.cpp:278-289): K1 (fused with the gather relayout, float32 + float64), K2,
+ * dedup, compaction. tgrid [V][12] (dev) receives the float32 transform grid, or NULL.
+ * Outputs as for fsk_batch_search. Fully asynchronous. */
 int fsk_deform(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* desc, const float* bones,
                int32_t n_bones_pose, const float* points, int64_t n, const fsk_search_opts* opts,
                float* tgrid, int64_t* offsets, fsk_root* roots, int64_t cap, void* stream);
 
-/* Stream-compaction of the kept roots into CorrespondenceSet form: offsets [N+1] int64
- * (dev), roots [total] fsk_root (dev, capacity `cap` records). *total_out (host) receives
- * the number of kept roots; this call synchronizes `stream` to read it. Returns FSK_EINVAL
- * if cap is too small (roots untouched, *total_out still set). */
+/* Stream-compaction of a dense result's kept roots into CorrespondenceSet form: offsets
+ * [N+1] int64 (dev), roots [total] (dev, capacity `cap`). *total_out (host) receives the
+ * number of kept roots; this call synchronizes `stream` to read it. Returns FSK_EINVAL if
+ * cap is too small (roots untouched, *total_out still set). */
 int fsk_compact_roots(fsk_ctx* ctx, const fsk_search_out* dense, int64_t n, int32_t n_init,
                       int64_t* offsets, fsk_root* roots, int64_t cap, int64_t* total_out,
                       void* stream);
 
-/* End-to-end host-buffer entry point (what cmd_deform / cmd_bench do per frame,
- * fskin_cli.cpp:395-408, :663-678): H2D of weights, bones and points, K1, K2, dedup,
- * compaction and D2H of the CorrespondenceSets. All pointers are HOST memory (pinned
- * recommended). offsets [N+1]; roots capacity `cap`. Synchronous. */
+/* End-to-end host-buffer entry point (one cmd_deform / cmd_bench frame): H2D of weights,
+ * bones and points, fsk_deform, D2H of the CorrespondenceSets. All pointers are HOST memory
+ * (pinned recommended). offsets [N+1]; roots capacity `cap`. Synchronous. */
 int fsk_deform_host(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* desc,
                     const float* bones, int32_t n_bones_pose, const float* points, int64_t n,
                     const fsk_search_opts* opts, int64_t* offsets, fsk_root* roots, int64_t cap,
@@ -155,13 +170,13 @@ int fsk_deform_host(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* des
 /* ---- point evaluators (batch forms of trilerp_transform / forward_deform /
  * deform_jacobian, deformer.hpp:59-68): at points x [N][3] (dev) write T(x) [N][12],
  * d(x) [N][3] and the analytic Jacobian dd/dx [N][9] (transform-grid form).
- * Any output may be NULL. */
+ * Any output may be NULL. float32. */
 int fsk_eval_points(fsk_ctx* ctx, const float* tgrid, const fsk_grid_desc* desc,
                     const float* x, int64_t n, float* t12, float* d, float* jac, void* stream);
 
 /* init_states (correspondence.hpp:62-63; correspondence.cpp:58-70): for every (point, bone)
  * x0 [N][n_b][3] = B_i^-1 x' and jinv0 [N][n_b][9] = J(x0)^-1, or I when |det J| < 1e-8.
- * Either output may be NULL. */
+ * Either output may be NULL. float32. */
 int fsk_init_states(fsk_ctx* ctx, const float* tgrid, const fsk_grid_desc* desc, const float* bones,
                     int32_t n_bones_pose, const float* points, int64_t n, float* x0, float* jinv0,
                     void* stream);

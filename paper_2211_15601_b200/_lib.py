@@ -14,6 +14,8 @@ LIB_PATH = os.path.join(HERE, "libfsk_b200.so")
 
 FSK_OK, FSK_EINVAL, FSK_ECUDA, FSK_ENODEV = 0, 1, 2, 3
 FSK_SEARCH_NO_SORT = 0x1
+FSK_SEARCH_FP32_ONLY = 0x2
+FSK_SEARCH_FP64 = 0x4
 
 # Every symbol include/fsk.h declares (checked by tests/test_lib_exports.py).
 EXPORTS = [
@@ -21,7 +23,7 @@ EXPORTS = [
     "fsk_search_opts_defaults", "fsk_precompute_tgrid", "fsk_search_fwd", "fsk_compact_roots",
     "fsk_deform_host", "fsk_eval_points", "fsk_init_states", "fsk_search_bwd", "fsk_grad_weights",
     "fsk_ctx_set_profiling", "fsk_ctx_prof_read", "fsk_measure_fp32_peak", "fsk_batch_search", "fsk_deform",
-    "fsk_search_bwd_roots",
+    "fsk_search_bwd_roots", "fsk_ctx_search_stats",
 ]
 
 
@@ -31,8 +33,8 @@ class GridDesc(ctypes.Structure):
 
 
 class SearchOpts(ctypes.Structure):
-    _fields_ = [("max_iters", ctypes.c_int32), ("conv_eps", ctypes.c_float), ("div_eps", ctypes.c_float),
-                ("dedup_dist", ctypes.c_float), ("flags", ctypes.c_int32)]
+    _fields_ = [("max_iters", ctypes.c_int32), ("flags", ctypes.c_int32), ("conv_eps", ctypes.c_double),
+                ("div_eps", ctypes.c_double), ("dedup_dist", ctypes.c_double)]
 
 
 class SearchOut(ctypes.Structure):
@@ -77,20 +79,21 @@ def load():
     L.fsk_search_opts_defaults.argtypes = [ctypes.POINTER(GridDesc)]
     L.fsk_search_opts_defaults.restype = SearchOpts
     G, O, S = ctypes.POINTER(GridDesc), ctypes.POINTER(SearchOpts), ctypes.POINTER(SearchOut)
-    L.fsk_precompute_tgrid.argtypes = [_vp, _vp, G, _vp, _i32, _vp, _vp]
-    L.fsk_search_fwd.argtypes = [_vp, _vp, G, _vp, _i32, _vp, _i64, O, S, _vp]
+    L.fsk_precompute_tgrid.argtypes = [_vp, _vp, G, _vp, _i32, _vp, _vp, _vp]
+    L.fsk_search_fwd.argtypes = [_vp, _vp, _vp, G, _vp, _i32, _vp, _i64, O, S, _vp]
     L.fsk_compact_roots.argtypes = [_vp, S, _i64, _i32, _vp, _vp, _i64, ctypes.POINTER(_i64), _vp]
     L.fsk_deform_host.argtypes = [_vp, _vp, G, _vp, _i32, _vp, _i64, O, _vp, _vp, _i64, ctypes.POINTER(_i64), _vp]
     L.fsk_eval_points.argtypes = [_vp, _vp, G, _vp, _i64, _vp, _vp, _vp, _vp]
     L.fsk_init_states.argtypes = [_vp, _vp, G, _vp, _i32, _vp, _i64, _vp, _vp, _vp]
     L.fsk_search_bwd.argtypes = [_vp, G, _vp, _vp, _i32, _vp, _vp, _i64, _vp, ctypes.c_int, _vp]
     L.fsk_grad_weights.argtypes = [_vp, G, _vp, _vp, _i32, _vp, _vp]
-    L.fsk_batch_search.argtypes = [_vp, _vp, G, _vp, _i32, _vp, _i64, O, _vp, _vp, _i64, _vp]
+    L.fsk_batch_search.argtypes = [_vp, _vp, _vp, G, _vp, _i32, _vp, _i64, O, _vp, _vp, _i64, _vp]
     L.fsk_deform.argtypes = [_vp, _vp, G, _vp, _i32, _vp, _i64, O, _vp, _vp, _vp, _i64, _vp]
     L.fsk_search_bwd_roots.argtypes = [_vp, G, _vp, _vp, _vp, _i64, _vp, ctypes.c_int, _vp]
     L.fsk_ctx_set_profiling.argtypes = [_vp, ctypes.c_int]
     L.fsk_ctx_prof_read.argtypes = [_vp, ctypes.c_char_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64),
                                     ctypes.c_int]
+    L.fsk_ctx_search_stats.argtypes = [_vp, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
     L.fsk_measure_fp32_peak.argtypes = [_vp, ctypes.POINTER(ctypes.c_double)]
     _lib = L
     return L

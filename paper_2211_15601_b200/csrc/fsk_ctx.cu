@@ -79,7 +79,10 @@ GridP make_grid(const fsk_grid_desc* d) {
         g.hi[a] = d->bbox_max[a];
         const float ext = g.hi[a] - g.lo[a];
         if (!(ext > 0.f)) fail(FSK_EINVAL, "SkinningVoxelGrid: bbox must have positive extent");
-        g.scale[a] = (float)((double)(n[a] - 1) / (double)ext);
+        g.lod[a] = d->bbox_min[a];
+        g.hid[a] = d->bbox_max[a];
+        g.scaled[a] = (double)(n[a] - 1) / (g.hid[a] - g.lod[a]);  // skinning.cpp:109 in f64
+        g.scale[a] = (float)g.scaled[a];
     }
     return g;
 }
@@ -88,15 +91,31 @@ SearchP make_search(const fsk_search_opts* o) {
     if (!o) fail(FSK_EINVAL, "fsk: null search options");
     // SearchOptions::validate (correspondence.cpp:19-25)
     if (o->max_iters < 1) fail(FSK_EINVAL, "search: max_iters must be >= 1");
-    if (!(o->conv_eps > 0.f)) fail(FSK_EINVAL, "search: conv_eps must be > 0");
+    if (!(o->conv_eps > 0.0)) fail(FSK_EINVAL, "search: conv_eps must be > 0");
     if (!(o->div_eps > o->conv_eps)) fail(FSK_EINVAL, "search: div_eps must exceed conv_eps");
-    if (!(o->dedup_dist >= 0.f)) fail(FSK_EINVAL, "search: dedup_dist must be >= 0");
+    if (!(o->dedup_dist >= 0.0)) fail(FSK_EINVAL, "search: dedup_dist must be >= 0");
     if (o->max_iters > 255) fail(FSK_EINVAL, "fsk: max_iters must be <= 255 (uint8 iteration counts)");
+    if ((o->flags & FSK_SEARCH_FP32_ONLY) && (o->flags & FSK_SEARCH_FP64))
+        fail(FSK_EINVAL, "fsk: FSK_SEARCH_FP32_ONLY and FSK_SEARCH_FP64 are exclusive");
     SearchP s;
     s.max_iters = o->max_iters;
-    s.conv2 = (float)((double)o->conv_eps * (double)o->conv_eps);
-    s.div2 = (float)((double)o->div_eps * (double)o->div_eps);
-    s.dedup2 = (float)((double)o->dedup_dist * (double)o->dedup_dist);
+    s.conv2 = o->conv_eps * o->conv_eps;
+    s.div2 = o->div_eps * o->div_eps;
+    s.dedup2 = o->dedup_dist * o->dedup_dist;
+    // Escalation rule of the float32 pass (validated on 1.5M solves
+    // against the f64 oracle with oracle/precision_emul.cpp): cap at 8 iterations, escalate
+    // unconverged runs of >= 3 iterations, and any threshold decision within float32 noise:
+    // err^2 within ±2% of conv^2 (f32 residuals near conv carry ~1e-7/3e-5 relative error),
+    // within ±2e-4 of div^2, |det J0| < 1e-5 (vs the 1e-8 singular cut), |den| < 1e-12
+    // (vs the 1e-18 Broyden guard).
+    s.esc_cap = 8;
+    s.esc_min_div = 3;
+    s.esc_conv_lo = 0.98f;
+    s.esc_conv_hi = 1.02f;
+    s.esc_div_lo = 0.9998f;
+    s.esc_div_hi = 1.0002f;
+    s.esc_det = 1e-5f;
+    s.esc_den = 1e-12f;
     return s;
 }
 
@@ -136,9 +155,15 @@ int fsk_ctx_create(int device, fsk_ctx** out) {
         cudaDeviceProp prop;
         cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
         if (prop.major != 10) fail(FSK_ENODEV, std::string("fsk: built for sm_100a, device is ") + prop.name);
+        cuda_check(cudaSetDevice(device), "cudaSetDevice");
         auto* c = new fsk_ctx();
         c->device = device;
         c->sm_count = prop.multiProcessorCount;
+        if (cudaMalloc(&c->stats, 8 * sizeof(unsigned long long)) != cudaSuccess ||
+            cudaMemset(c->stats, 0, 8 * sizeof(unsigned long long)) != cudaSuccess) {
+            delete c;
+            fail(FSK_ECUDA, "fsk: cannot allocate context state");
+        }
         *out = c;
     });
 }
@@ -154,6 +179,7 @@ int fsk_ctx_destroy(fsk_ctx* ctx) {
             cudaEventDestroy(r.b);
         }
         for (auto& e : ctx->pool) cudaEventDestroy(e);
+        if (ctx->stats) cudaFree(ctx->stats);
         delete ctx;
     });
 }
@@ -195,6 +221,18 @@ int fsk_ctx_prof_read(fsk_ctx* ctx, const char* name, double* total_ms, int64_t*
     });
 }
 
+int fsk_ctx_search_stats(fsk_ctx* ctx, uint64_t out[6], int reset) {
+    return guard([&] {
+        set_device(ctx);
+        if (!out) fail(FSK_EINVAL, "fsk: null output pointer");
+        cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+        unsigned long long h[8];
+        cuda_check(cudaMemcpy(h, ctx->stats, sizeof(h), cudaMemcpyDeviceToHost), "cudaMemcpy");
+        for (int i = 0; i < 6; ++i) out[i] = h[i];
+        if (reset) cuda_check(cudaMemset(ctx->stats, 0, sizeof(h)), "cudaMemset");
+    });
+}
+
 int fsk_measure_fp32_peak(fsk_ctx* ctx, double* tflops) {
     return guard([&] {
         set_device(ctx);
@@ -218,7 +256,7 @@ int fsk_measure_fp32_peak(fsk_ctx* ctx, double* tflops) {
 }
 
 fsk_search_opts fsk_search_opts_defaults(const fsk_grid_desc* d) {
-    fsk_search_opts o{50, 1e-5f, 0.5f, 1e-2f, 0};
+    fsk_search_opts o{50, 0, 1e-5, 0.5, 1e-2};
     if (!d) return o;
     double s = 0.0;
     for (int a = 0; a < 3; ++a) {
@@ -226,9 +264,9 @@ fsk_search_opts fsk_search_opts_defaults(const fsk_grid_desc* d) {
         s += e * e;
     }
     const double diag = std::sqrt(s);
-    o.conv_eps = (float)(1e-5 * diag);
-    o.div_eps = (float)(0.5 * diag);
-    o.dedup_dist = (float)(1e-2 * diag);
+    o.conv_eps = 1e-5 * diag;
+    o.div_eps = 0.5 * diag;
+    o.dedup_dist = 1e-2 * diag;
     return o;
 }
 

@@ -32,13 +32,15 @@ struct fsk_ctx {
     };
     std::vector<Rec> prof;
     std::vector<cudaEvent_t> pool;
+    // search work counters [solves32, iters32, final32, solves64, iters64, final64]
+    unsigned long long* stats = nullptr;
 };
 
 namespace fsk {
 
 // Scratch slots (one growable device buffer each).
 enum Slot {
-    kHist, kBbox, kKeys, kPerm, kXs, kScanPart, kBwdAcc, kBwdMax, kPlanes,
+    kHist, kBbox, kKeys, kPerm, kXs, kScanPart, kBwdAcc, kBwdMax, kPlanes, kPlanes64, kEscQ, kEscN,
     kOXr, kOJa, kOJb, kOJc, kOMeta, kOKeep, kNRoots, kOffs, kRootsTmp,
     kHW, kHB, kHP, kHT, kHOffs, kHRoots,
     kSlotCount

@@ -1,4 +1,6 @@
-// fsk_device.cuh — device-side building blocks of the Fast-SNARF deformer kernels (sm_100a).
+// fsk_device.cuh — device-side building blocks of the Fast-SNARF deformer kernels (sm_100a),
+// templated on the arithmetic type R (float for the fast pass, double for the escalation /
+// parity pass).
 //
 // Semantics follow SURVEY Appendix A: the cell lookup clamps x to the bbox while the
 // affine map is applied to the unclamped x (deformer.cpp:79-94,107-113); the initial
@@ -7,11 +9,12 @@
 // grid instead of the n_b-wide weight grid (equal in real arithmetic).
 //
 // Gather layout ("x-pair planes"): the reference's [V][12] transform grid is re-laid out
-// once per pose into three planes, one per matrix row r, whose element v is 32 bytes:
-//     P[r][v] = { row r of T_v , row r of T_{v+1} }      (8 floats)
-// so one 256-bit load (LDG.E.ENL2.256, new on sm_100) returns one row of BOTH x-corners of
-// a cell edge, and x-neighbouring vertices sit 32 B apart (4 per 128-B line). A trilinear
-// evaluation is 12 LDG.256 (4 (dj,dk) edges × 3 rows) instead of 24 LDG.128 in [V][12].
+// once per pose into three planes, one per matrix row r, whose element v is
+//     P[r][v] = { row r of T_v , row r of T_{v+1} }      (8 values)
+// so one 256-bit load (LDG.E.ENL2.256, new on sm_100) returns one row of BOTH x-corners
+// of a cell edge in float32 (two loads in float64), and x-neighbouring vertices sit 32 B
+// apart. A trilinear evaluation is 12 LDG.256 (4 (dj,dk) edges × 3 rows) instead of 24
+// LDG.128 in [V][12].
 #pragma once
 
 #include <cstdint>
@@ -23,38 +26,56 @@ struct GridP {
     int nx, ny, nz, nb;
     float lo[3], hi[3];
     float scale[3];  // (n-1)/ext: u = (p-lo)*scale; also 1/h for the gradient stencil
+    double lod[3], hid[3], scaled[3];
 };
 
+template <typename R> __device__ __forceinline__ R g_lo(const GridP& g, int a);
+template <> __device__ __forceinline__ float g_lo<float>(const GridP& g, int a) { return g.lo[a]; }
+template <> __device__ __forceinline__ double g_lo<double>(const GridP& g, int a) { return g.lod[a]; }
+template <typename R> __device__ __forceinline__ R g_hi(const GridP& g, int a);
+template <> __device__ __forceinline__ float g_hi<float>(const GridP& g, int a) { return g.hi[a]; }
+template <> __device__ __forceinline__ double g_hi<double>(const GridP& g, int a) { return g.hid[a]; }
+template <typename R> __device__ __forceinline__ R g_scale(const GridP& g, int a);
+template <> __device__ __forceinline__ float g_scale<float>(const GridP& g, int a) { return g.scale[a]; }
+template <> __device__ __forceinline__ double g_scale<double>(const GridP& g, int a) { return g.scaled[a]; }
+
+// Search thresholds (SearchOptions, correspondence.hpp:14-26) squared, plus the
+// precision-escalation rule of the float32 pass.
 struct SearchP {
     int max_iters;
-    float conv2;  // conv_eps^2
-    float div2;   // div_eps^2
-    float dedup2;
+    int esc_cap;        // fp32 pass stops after this many iterations and escalates
+    int esc_min_div;    // escalate unconverged solves with at least this many iterations
+    double conv2, div2, dedup2;
+    float esc_conv_lo, esc_conv_hi;  // err2 within [lo,hi]·conv2 → threshold too close to call in fp32
+    float esc_div_lo, esc_div_hi;
+    float esc_det;      // |det J0| below this → singular-fallback decision too close to call
+    float esc_den;      // |dx·J~dg| below this → Broyden-guard decision too close to call
 };
 
+template <typename R>
 struct Cell {
     int base;  // vertex index of corner (i0, j0, k0)
-    float tx, ty, tz;
+    R tx, ty, tz;
 };
 
-// locate_cell (skinning.cpp:104-120) / locate_cell_lower (:122-139) in float32.
-template <bool kLower>
-__device__ __forceinline__ Cell locate(const GridP& g, float x, float y, float z) {
-    const float xs[3] = {x, y, z};
+// locate_cell (skinning.cpp:104-120) / locate_cell_lower (:122-139).
+template <bool kLower, typename R>
+__device__ __forceinline__ Cell<R> locate(const GridP& g, R x, R y, R z) {
+    const R xs[3] = {x, y, z};
     const int n[3] = {g.nx, g.ny, g.nz};
     int idx[3];
-    float t[3];
+    R t[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        const float p = fminf(fmaxf(xs[a], g.lo[a]), g.hi[a]);  // Aabb::clamp
-        const float u = (p - g.lo[a]) * g.scale[a];
-        int i = __float2int_rd(u);  // floor; NaN -> 0
-        if (kLower && i >= 1 && u == (float)i) i -= 1;
+        const R p = fmin(fmax(xs[a], g_lo<R>(g, a)), g_hi<R>(g, a));  // Aabb::clamp
+        const R u = (p - g_lo<R>(g, a)) * g_scale<R>(g, a);
+        int i = (int)floor(u);  // NaN -> 0 (cvt.rzi of NaN)
+        if (kLower && i >= 1 && u == (R)i) i -= 1;
         i = max(0, min(i, n[a] - 2));
         idx[a] = i;
-        t[a] = fminf(fmaxf(u - (float)i, 0.f), 1.f);
+        t[a] = fmin(fmax(u - (R)i, (R)0), (R)1);
     }
-    Cell c;
+    Cell<R> c;
     c.base = (idx[2] * g.ny + idx[1]) * g.nx + idx[0];
     c.tx = t[0];
     c.ty = t[1];
@@ -62,50 +83,62 @@ __device__ __forceinline__ Cell locate(const GridP& g, float x, float y, float z
     return c;
 }
 
-// 256-bit read-only load (sm_100: LDG.E.ENL2.256.CONSTANT).
-__device__ __forceinline__ void ldg256(const float* p, float4& a, float4& b) {
-    asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-        : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
-        : "l"(p));
-}
-
-struct Planes {
-    const float* p;   // [3][V][8]
-    int64_t stride;   // V*8 floats between row planes
+template <typename R>
+struct V4 {
+    R x, y, z, w;
 };
 
-__device__ __forceinline__ void load_edge(const Planes& P, int v, int r, float4& a, float4& b) {
-    ldg256(P.p + r * P.stride + (int64_t)v * 8, a, b);
+// x-pair planes; stride = V * 8 elements between row planes.
+template <typename R>
+struct Planes {
+    const R* p;
+    int64_t stride;
+};
+
+__device__ __forceinline__ void load_edge(const Planes<float>& P, int v, int r, V4<float>& a, V4<float>& b) {
+    const float* q = P.p + r * P.stride + (int64_t)v * 8;
+    asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+        : "l"(q));
 }
 
-__device__ __forceinline__ void fma4(float* T, float w, const float4& a) {
-    T[0] = fmaf(w, a.x, T[0]);
-    T[1] = fmaf(w, a.y, T[1]);
-    T[2] = fmaf(w, a.z, T[2]);
-    T[3] = fmaf(w, a.w, T[3]);
+__device__ __forceinline__ void load_edge(const Planes<double>& P, int v, int r, V4<double>& a, V4<double>& b) {
+    const double* q = P.p + r * P.stride + (int64_t)v * 8;
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a.x), "=d"(a.y), "=d"(a.z), "=d"(a.w) : "l"(q));
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(b.x), "=d"(b.y), "=d"(b.z), "=d"(b.w) : "l"(q + 4));
 }
 
-__device__ __forceinline__ float row_dot(const float4& a, float x, float y, float z) {
+template <typename R>
+__device__ __forceinline__ void fma4(R* T, R w, const V4<R>& a) {
+    T[0] = fma(w, a.x, T[0]);
+    T[1] = fma(w, a.y, T[1]);
+    T[2] = fma(w, a.z, T[2]);
+    T[3] = fma(w, a.w, T[3]);
+}
+
+template <typename R>
+__device__ __forceinline__ R row_dot(const V4<R>& a, R x, R y, R z) {
     return a.x * x + a.y * y + a.z * z + a.w;
 }
 
 // trilerp_transform_into (deformer.cpp:79-94) on the x-pair planes. Corner weights are
 // formed as (wz*wy)*wx like the reference; accumulation is per (dk, dj) edge.
-__device__ __forceinline__ void trilerp_T(const Planes& P, const GridP& g, const Cell& c, float T[12]) {
+template <typename R>
+__device__ __forceinline__ void trilerp_T(const Planes<R>& P, const GridP& g, const Cell<R>& c, R T[12]) {
 #pragma unroll
-    for (int e = 0; e < 12; ++e) T[e] = 0.f;
+    for (int e = 0; e < 12; ++e) T[e] = 0;
     const int nxy = g.nx * g.ny;
 #pragma unroll
     for (int dk = 0; dk < 2; ++dk) {
-        const float wz = dk ? c.tz : 1.f - c.tz;
+        const R wz = dk ? c.tz : (R)1 - c.tz;
 #pragma unroll
         for (int dj = 0; dj < 2; ++dj) {
-            const float wyz = wz * (dj ? c.ty : 1.f - c.ty);
-            const float w0 = wyz * (1.f - c.tx), w1 = wyz * c.tx;
+            const R wyz = wz * (dj ? c.ty : (R)1 - c.ty);
+            const R w0 = wyz * ((R)1 - c.tx), w1 = wyz * c.tx;
             const int v = c.base + dk * nxy + dj * g.nx;
 #pragma unroll
             for (int r = 0; r < 3; ++r) {
-                float4 a, b;
+                V4<R> a, b;
                 load_edge(P, v, r, a, b);
                 fma4(T + 4 * r, w0, a);
                 fma4(T + 4 * r, w1, b);
@@ -115,54 +148,52 @@ __device__ __forceinline__ void trilerp_T(const Planes& P, const GridP& g, const
 }
 
 // d = T·[x;1] on the unclamped x (deformer.cpp:107-113).
-__device__ __forceinline__ void apply_T(const float T[12], float x, float y, float z, float d[3]) {
+template <typename R>
+__device__ __forceinline__ void apply_T(const R T[12], R x, R y, R z, R d[3]) {
     d[0] = T[0] * x + T[1] * y + T[2] * z + T[3];
     d[1] = T[4] * x + T[5] * y + T[6] * z + T[7];
     d[2] = T[8] * x + T[9] * y + T[10] * z + T[11];
 }
 
-// Gradient-stencil term of one corner: G += (T_c x̃) ∇φ_cᵀ, ∇φ from fractions (fx,fy,fz)
-// of the lower cell with ±1/h (skinning.cpp:164-193).
-__device__ __forceinline__ void grad_term(float G[9], float y0, float y1, float y2, float gx, float gy, float gz) {
-    G[0] = fmaf(y0, gx, G[0]); G[1] = fmaf(y0, gy, G[1]); G[2] = fmaf(y0, gz, G[2]);
-    G[3] = fmaf(y1, gx, G[3]); G[4] = fmaf(y1, gy, G[4]); G[5] = fmaf(y1, gz, G[5]);
-    G[6] = fmaf(y2, gx, G[6]); G[7] = fmaf(y2, gy, G[7]); G[8] = fmaf(y2, gz, G[8]);
+template <typename R>
+__device__ __forceinline__ void grad_term(R G[9], R y0, R y1, R y2, R gx, R gy, R gz) {
+    G[0] = fma(y0, gx, G[0]); G[1] = fma(y0, gy, G[1]); G[2] = fma(y0, gz, G[2]);
+    G[3] = fma(y1, gx, G[3]); G[4] = fma(y1, gy, G[4]); G[5] = fma(y1, gz, G[5]);
+    G[6] = fma(y2, gx, G[6]); G[7] = fma(y2, gy, G[7]); G[8] = fma(y2, gz, G[8]);
 }
 
 // Analytic Jacobian and T(p) at x:
 //   J = T_lin(p) + Σ_c (T_c x̃) ∇φ_c(p)ᵀ
-// T from the locate_cell cell, ∇φ from the locate_cell_lower cell; both from one gather
-// unless x lies exactly on an interior face (then the lower cell is gathered again).
-__device__ __forceinline__ void jacobian_and_T(const Planes& P, const GridP& g, float x, float y, float z,
-                                               float T[12], float J[9]) {
-    const Cell c = locate<false>(g, x, y, z);
-    const Cell cl = locate<true>(g, x, y, z);
+// T from the locate_cell cell, ∇φ from the locate_cell_lower cell (±1/h stencils); both
+// from one gather unless x lies exactly on an interior face (then the lower cell is
+// gathered again).
+template <typename R>
+__device__ __forceinline__ void jacobian_and_T(const Planes<R>& P, const GridP& g, R x, R y, R z, R T[12], R J[9]) {
+    const Cell<R> c = locate<false, R>(g, x, y, z);
+    const Cell<R> cl = locate<true, R>(g, x, y, z);
     const int nxy = g.nx * g.ny;
     const bool same = (c.base == cl.base);
 #pragma unroll
-    for (int e = 0; e < 12; ++e) T[e] = 0.f;
-    float G[9];
+    for (int e = 0; e < 12; ++e) T[e] = 0;
+    R G[9];
 #pragma unroll
-    for (int e = 0; e < 9; ++e) G[e] = 0.f;
-    const float sx = g.scale[0], sy = g.scale[1], sz = g.scale[2];
+    for (int e = 0; e < 9; ++e) G[e] = 0;
+    const R sx = g_scale<R>(g, 0), sy = g_scale<R>(g, 1), sz = g_scale<R>(g, 2);
 #pragma unroll
     for (int dk = 0; dk < 2; ++dk) {
-        const float wz = dk ? c.tz : 1.f - c.tz;
-        const float fz = dk ? cl.tz : 1.f - cl.tz, gz_s = dk ? sz : -sz;
+        const R wz = dk ? c.tz : (R)1 - c.tz;
+        const R fz = dk ? cl.tz : (R)1 - cl.tz, gz_s = dk ? sz : -sz;
 #pragma unroll
         for (int dj = 0; dj < 2; ++dj) {
-            const float wyz = wz * (dj ? c.ty : 1.f - c.ty);
-            const float w0 = wyz * (1.f - c.tx), w1 = wyz * c.tx;
-            const float fy = dj ? cl.ty : 1.f - cl.ty, gy_s = dj ? sy : -sy;
-            // ∇φ of the two x-corners of this edge
-            const float fx0 = 1.f - cl.tx, fx1 = cl.tx;
-            const float g0x = -sx * fy * fz, g0y = fx0 * gy_s * fz, g0z = fx0 * fy * gz_s;
-            const float g1x = sx * fy * fz, g1y = fx1 * gy_s * fz, g1z = fx1 * fy * gz_s;
+            const R wyz = wz * (dj ? c.ty : (R)1 - c.ty);
+            const R w0 = wyz * ((R)1 - c.tx), w1 = wyz * c.tx;
+            const R fy = dj ? cl.ty : (R)1 - cl.ty, gy_s = dj ? sy : -sy;
+            const R fx0 = (R)1 - cl.tx, fx1 = cl.tx;
             const int v = c.base + dk * nxy + dj * g.nx;
-            float y0[3], y1[3];
+            R y0[3], y1[3];
 #pragma unroll
             for (int r = 0; r < 3; ++r) {
-                float4 a, b;
+                V4<R> a, b;
                 load_edge(P, v, r, a, b);
                 fma4(T + 4 * r, w0, a);
                 fma4(T + 4 * r, w1, b);
@@ -170,8 +201,8 @@ __device__ __forceinline__ void jacobian_and_T(const Planes& P, const GridP& g, 
                 y1[r] = row_dot(b, x, y, z);
             }
             if (same) {
-                grad_term(G, y0[0], y0[1], y0[2], g0x, g0y, g0z);
-                grad_term(G, y1[0], y1[1], y1[2], g1x, g1y, g1z);
+                grad_term(G, y0[0], y0[1], y0[2], -sx * fy * fz, fx0 * gy_s * fz, fx0 * fy * gz_s);
+                grad_term(G, y1[0], y1[1], y1[2], sx * fy * fz, fx1 * gy_s * fz, fx1 * fy * gz_s);
             }
         }
     }
@@ -179,14 +210,14 @@ __device__ __forceinline__ void jacobian_and_T(const Planes& P, const GridP& g, 
 #pragma unroll 1
         for (int q = 0; q < 4; ++q) {
             const int dj = q & 1, dk = q >> 1;
-            const float fz = dk ? cl.tz : 1.f - cl.tz, gz_s = dk ? sz : -sz;
-            const float fy = dj ? cl.ty : 1.f - cl.ty, gy_s = dj ? sy : -sy;
-            const float fx0 = 1.f - cl.tx, fx1 = cl.tx;
+            const R fz = dk ? cl.tz : (R)1 - cl.tz, gz_s = dk ? sz : -sz;
+            const R fy = dj ? cl.ty : (R)1 - cl.ty, gy_s = dj ? sy : -sy;
+            const R fx0 = (R)1 - cl.tx, fx1 = cl.tx;
             const int v = cl.base + dk * nxy + dj * g.nx;
-            float y0[3], y1[3];
+            R y0[3], y1[3];
 #pragma unroll
             for (int r = 0; r < 3; ++r) {
-                float4 a, b;
+                V4<R> a, b;
                 load_edge(P, v, r, a, b);
                 y0[r] = row_dot(a, x, y, z);
                 y1[r] = row_dot(b, x, y, z);
@@ -200,47 +231,131 @@ __device__ __forceinline__ void jacobian_and_T(const Planes& P, const GridP& g, 
     J[6] = T[8] + G[6]; J[7] = T[9] + G[7]; J[8] = T[10] + G[8];
 }
 
-// initial_inverse_jacobian (correspondence.cpp:43-54): cofactor inverse, identity if |det|<1e-8.
-__device__ __forceinline__ void inverse_or_identity(const float J[9], float Ji[9]) {
-    const float c00 = J[4] * J[8] - J[5] * J[7];
-    const float c01 = J[2] * J[7] - J[1] * J[8];
-    const float c02 = J[1] * J[5] - J[2] * J[4];
-    const float c10 = J[5] * J[6] - J[3] * J[8];
-    const float c11 = J[0] * J[8] - J[2] * J[6];
-    const float c12 = J[2] * J[3] - J[0] * J[5];
-    const float c20 = J[3] * J[7] - J[4] * J[6];
-    const float c21 = J[1] * J[6] - J[0] * J[7];
-    const float c22 = J[0] * J[4] - J[1] * J[3];
-    const float det = J[0] * c00 + J[1] * c10 + J[2] * c20;
-    if (fabsf(det) < 1e-8f) {  // NaN det fails the test and propagates, as in the reference
-        Ji[0] = 1.f; Ji[1] = 0.f; Ji[2] = 0.f;
-        Ji[3] = 0.f; Ji[4] = 1.f; Ji[5] = 0.f;
-        Ji[6] = 0.f; Ji[7] = 0.f; Ji[8] = 1.f;
-        return;
+// initial_inverse_jacobian (correspondence.cpp:43-54): cofactor inverse, identity if
+// |det| < 1e-8. Returns det (for the escalation rule).
+template <typename R>
+__device__ __forceinline__ R inverse_or_identity(const R J[9], R Ji[9]) {
+    const R c00 = J[4] * J[8] - J[5] * J[7];
+    const R c01 = J[2] * J[7] - J[1] * J[8];
+    const R c02 = J[1] * J[5] - J[2] * J[4];
+    const R c10 = J[5] * J[6] - J[3] * J[8];
+    const R c11 = J[0] * J[8] - J[2] * J[6];
+    const R c12 = J[2] * J[3] - J[0] * J[5];
+    const R c20 = J[3] * J[7] - J[4] * J[6];
+    const R c21 = J[1] * J[6] - J[0] * J[7];
+    const R c22 = J[0] * J[4] - J[1] * J[3];
+    const R det = J[0] * c00 + J[1] * c10 + J[2] * c20;
+    if (fabs(det) < (R)1e-8) {  // NaN det fails the test and propagates, as in the reference
+        Ji[0] = 1; Ji[1] = 0; Ji[2] = 0;
+        Ji[3] = 0; Ji[4] = 1; Ji[5] = 0;
+        Ji[6] = 0; Ji[7] = 0; Ji[8] = 1;
+        return det;
     }
-    const float inv = 1.f / det;
+    const R inv = (R)1 / det;
     Ji[0] = c00 * inv; Ji[1] = c01 * inv; Ji[2] = c02 * inv;
     Ji[3] = c10 * inv; Ji[4] = c11 * inv; Ji[5] = c12 * inv;
     Ji[6] = c20 * inv; Ji[7] = c21 * inv; Ji[8] = c22 * inv;
+    return det;
 }
 
 // Per-init start of search_one (correspondence.cpp:135-137): x0 = B_i^-1 x' as
 // Rᵀx' + (−Rᵀt) (geometry.hpp:58-61), J~0 = J(x0)^-1 or I (:43-54), and T(x0) for g0.
-__device__ __forceinline__ void solve_init(const Planes& P, const GridP& g, const float* __restrict__ B,
-                                           float xp0, float xp1, float xp2, float& x0, float& x1, float& x2,
-                                           float Ji[9], float T[12]) {
-    const float r00 = __ldg(B + 0), r01 = __ldg(B + 1), r02 = __ldg(B + 2), t0 = __ldg(B + 3);
-    const float r10 = __ldg(B + 4), r11 = __ldg(B + 5), r12 = __ldg(B + 6), t1 = __ldg(B + 7);
-    const float r20 = __ldg(B + 8), r21 = __ldg(B + 9), r22 = __ldg(B + 10), t2 = __ldg(B + 11);
-    const float it0 = -(r00 * t0 + r10 * t1 + r20 * t2);
-    const float it1 = -(r01 * t0 + r11 * t1 + r21 * t2);
-    const float it2 = -(r02 * t0 + r12 * t1 + r22 * t2);
+// Returns det J(x0).
+template <typename R>
+__device__ __forceinline__ R solve_init(const Planes<R>& P, const GridP& g, const float* __restrict__ B, R xp0, R xp1,
+                                        R xp2, R& x0, R& x1, R& x2, R Ji[9], R T[12]) {
+    const R r00 = __ldg(B + 0), r01 = __ldg(B + 1), r02 = __ldg(B + 2), t0 = __ldg(B + 3);
+    const R r10 = __ldg(B + 4), r11 = __ldg(B + 5), r12 = __ldg(B + 6), t1 = __ldg(B + 7);
+    const R r20 = __ldg(B + 8), r21 = __ldg(B + 9), r22 = __ldg(B + 10), t2 = __ldg(B + 11);
+    const R it0 = -(r00 * t0 + r10 * t1 + r20 * t2);
+    const R it1 = -(r01 * t0 + r11 * t1 + r21 * t2);
+    const R it2 = -(r02 * t0 + r12 * t1 + r22 * t2);
     x0 = r00 * xp0 + r10 * xp1 + r20 * xp2 + it0;
     x1 = r01 * xp0 + r11 * xp1 + r21 * xp2 + it1;
     x2 = r02 * xp0 + r12 * xp1 + r22 * xp2 + it2;
-    float Jm[9];
+    R Jm[9];
     jacobian_and_T(P, g, x0, x1, x2, T, Jm);
-    inverse_or_identity(Jm, Ji);
+    return inverse_or_identity(Jm, Ji);
+}
+
+// One Broyden solve: search_one's per-init body (correspondence.cpp:132-146) with iterate
+// (:97-124). With kFast (the float32 pass) the solve stops after p.esc_cap iterations and
+// raises `esc` whenever its outcome could differ from a float64 solve: a long trajectory
+// (iters >= esc_cap), an unconverged run of >= esc_min_div iterations, or a threshold
+// decision (conv, div, |det|<1e-8, |den|>1e-18) taken within float32 noise of the threshold.
+struct SolveOut {
+    int iters;
+    bool conv;
+    bool esc;
+};
+
+template <typename R, bool kFast>
+__device__ __forceinline__ SolveOut solve_one(const Planes<R>& P, const GridP& g, const float* __restrict__ B, R xp0,
+                                              R xp1, R xp2, const SearchP& o, R& x0, R& x1, R& x2, R Ji[9], R& err2) {
+    R T[12], d[3];
+    const R det = solve_init<R>(P, g, B, xp0, xp1, xp2, x0, x1, x2, Ji, T);
+    apply_T(T, x0, x1, x2, d);  // g0 = d(x0) − x' from the init gather (:137)
+    R g0 = d[0] - xp0, g1 = d[1] - xp1, g2 = d[2] - xp2;
+    err2 = g0 * g0 + g1 * g1 + g2 * g2;
+    const R conv2 = (R)o.conv2, div2 = (R)o.div2;
+    bool esc = false;
+    auto near = [&](R e2) {
+        return (e2 >= (R)o.esc_conv_lo * conv2 && e2 <= (R)o.esc_conv_hi * conv2) ||
+               (e2 >= (R)o.esc_div_lo * div2 && e2 <= (R)o.esc_div_hi * div2);
+    };
+    if (kFast) esc = fabs(det) < (R)o.esc_det || near(err2);
+    int iters = 0;
+    bool conv = err2 < conv2;  // (:100-103)
+    if (!conv) {
+        const int limit = kFast ? min(o.max_iters, o.esc_cap) : o.max_iters;
+        int k = 0;
+        for (; k < limit; ++k) {
+            if (err2 > div2) break;  // divergence check at the top (:105)
+            // dx = −J~ g; x += dx (:106-107)
+            const R dx0 = -(Ji[0] * g0 + Ji[1] * g1 + Ji[2] * g2);
+            const R dx1 = -(Ji[3] * g0 + Ji[4] * g1 + Ji[5] * g2);
+            const R dx2 = -(Ji[6] * g0 + Ji[7] * g1 + Ji[8] * g2);
+            x0 += dx0;
+            x1 += dx1;
+            x2 += dx2;
+            // g' = d(x) − x'; dg = g' − g (:108-112)
+            const Cell<R> c = locate<false, R>(g, x0, x1, x2);
+            trilerp_T(P, g, c, T);
+            apply_T(T, x0, x1, x2, d);
+            const R n0 = d[0] - xp0, n1 = d[1] - xp1, n2 = d[2] - xp2;
+            const R dg0 = n0 - g0, dg1 = n1 - g1, dg2 = n2 - g2;
+            g0 = n0;
+            g1 = n1;
+            g2 = n2;
+            iters = k + 1;
+            err2 = g0 * g0 + g1 * g1 + g2 * g2;
+            if (kFast && near(err2)) esc = true;
+            if (err2 < conv2) {  // (:113-116)
+                conv = true;
+                break;
+            }
+            // good Broyden: J~ += ((dx − J~dg)/(dx·J~dg)) (dxᵀJ~) if |den| > 1e-18 (:118-122)
+            const R j0 = Ji[0] * dg0 + Ji[1] * dg1 + Ji[2] * dg2;
+            const R j1 = Ji[3] * dg0 + Ji[4] * dg1 + Ji[5] * dg2;
+            const R j2 = Ji[6] * dg0 + Ji[7] * dg1 + Ji[8] * dg2;
+            const R den = dx0 * j0 + dx1 * j1 + dx2 * j2;
+            if (kFast && fabs(den) < (R)o.esc_den) esc = true;
+            if (fabs(den) > (R)1e-18) {
+                const R inv = (R)1 / den;
+                const R q0 = (dx0 - j0) * inv, q1 = (dx1 - j1) * inv, q2 = (dx2 - j2) * inv;
+                const R w0 = dx0 * Ji[0] + dx1 * Ji[3] + dx2 * Ji[6];
+                const R w1 = dx0 * Ji[1] + dx1 * Ji[4] + dx2 * Ji[7];
+                const R w2 = dx0 * Ji[2] + dx1 * Ji[5] + dx2 * Ji[8];
+                Ji[0] = fma(q0, w0, Ji[0]); Ji[1] = fma(q0, w1, Ji[1]); Ji[2] = fma(q0, w2, Ji[2]);
+                Ji[3] = fma(q1, w0, Ji[3]); Ji[4] = fma(q1, w1, Ji[4]); Ji[5] = fma(q1, w2, Ji[5]);
+                Ji[6] = fma(q2, w0, Ji[6]); Ji[7] = fma(q2, w1, Ji[7]); Ji[8] = fma(q2, w2, Ji[8]);
+            }
+        }
+        // the float32 pass hit its iteration cap before max_iters: the f64 pass decides
+        if (kFast && !conv && k == limit && limit < o.max_iters && !(err2 > div2)) esc = true;
+        if (kFast && !conv && iters >= o.esc_min_div) esc = true;
+    }
+    return SolveOut{iters, conv, esc};
 }
 
 }  // namespace fsk

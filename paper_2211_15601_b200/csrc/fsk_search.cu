@@ -1,10 +1,13 @@
 // fsk_search.cu — forward hot path of the deformer on sm_100a and its C-ABI entry points.
 //
 //   K1  k_precompute        precompute_transform_grid (deformer.cpp:61-77, lbs_blend :9-19)
-//                           fused with the x-pair gather-plane relayout (fsk_device.cuh)
+//                           fused with the x-pair gather-plane relayout (fsk_device.cuh), in
+//                           float32 and (for the escalation pass) float64
 //   S*  k_sort_*            spatial (Morton) ordering of the queries — performance only
-//   K2  k_search            search_one per (point, bone-init) (correspondence.cpp:126-150)
-//                           with iterate (:97-124) in registers
+//   K2  k_search_fast       search_one per (point, bone-init) (correspondence.cpp:126-150)
+//                           with iterate (:97-124) in registers, float32, iteration-capped,
+//                           flags solves whose float32 outcome is not trustworthy
+//   K2b k_search_escalated  the flagged solves re-run from scratch in float64
 //   D   k_dedup             dedup_roots (correspondence.cpp:162-176)
 //   C*  k_scan_*, k_emit    compaction into CorrespondenceSets (correspondence.hpp:29-42)
 //   k_scatter_dense         the dense per-(point, init) form (fsk_search_out)
@@ -14,6 +17,13 @@
 // every store of a warp is one contiguous, coalesced segment; dedup then reads the n_b
 // inits of a query with coalesced loads, and only kept roots are scattered to the
 // caller's query order (≈1 root per query instead of n_b dense records).
+//
+// Precision: long Broyden trajectories are chaotic — a float32
+// rounding of the transform grid alone flips ~0.03 % of converged masks against the
+// float64 reference. The float32 pass therefore stops at esc_cap iterations and flags
+// every solve whose outcome float32 cannot settle (long or late-diverging trajectories,
+// threshold decisions within float32 noise); those (~5 %) are solved again in float64,
+// which B200 runs at half the float32 rate.
 #include <cstring>
 
 #include "fsk_ctx.h"
@@ -23,10 +33,28 @@ namespace fsk {
 // ============================================================================ K1
 // T_v = Σ_i w_{v,i}·B_i, accumulated in bone order like lbs_blend. One thread per vertex,
 // bones staged in shared memory. Writes the reference-layout [V][12] grid (if tg != null)
-// and the gather planes: P[r][v].lo = row r of T_v, P[r][v-1].hi = row r of T_v.
+// and the gather planes: P[r][v].lo = row r of T_v, P[r][v-1].hi = row r of T_v — in
+// float32 (p32) and, when p64 != null, float64 from the same float32 inputs.
+template <typename R>
+__device__ __forceinline__ void put_planes(R* planes, int64_t V, int64_t v, bool has_left, const R* T) {
+    const int64_t stride = 8 * V;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        R* lo = planes + r * stride + 8 * v;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) lo[e] = T[4 * r + e];
+        if (has_left) {
+            R* hi = planes + r * stride + 8 * (v - 1) + 4;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) hi[e] = T[4 * r + e];
+        }
+    }
+}
+
 __global__ void __launch_bounds__(256) k_precompute(const float* __restrict__ w, const float* __restrict__ bones,
                                                     int nb, int nx, int64_t V, float4* __restrict__ tg,
-                                                    float4* __restrict__ planes) {
+                                                    float* __restrict__ p32, double* __restrict__ p64,
+                                                    double* __restrict__ tg64) {
     extern __shared__ float sB[];
     for (int e = threadIdx.x; e < nb * 12; e += blockDim.x) sB[e] = bones[e];
     __syncthreads();
@@ -41,40 +69,44 @@ __global__ void __launch_bounds__(256) k_precompute(const float* __restrict__ w,
 #pragma unroll
         for (int e = 0; e < 12; ++e) T[e] = fmaf(wi, sB[i * 12 + e], T[e]);
     }
-    const float4 r0 = make_float4(T[0], T[1], T[2], T[3]);
-    const float4 r1 = make_float4(T[4], T[5], T[6], T[7]);
-    const float4 r2 = make_float4(T[8], T[9], T[10], T[11]);
+    const bool has_left = (v % nx) != 0;
     if (tg) {
-        tg[3 * v] = r0;
-        tg[3 * v + 1] = r1;
-        tg[3 * v + 2] = r2;
+        tg[3 * v] = make_float4(T[0], T[1], T[2], T[3]);
+        tg[3 * v + 1] = make_float4(T[4], T[5], T[6], T[7]);
+        tg[3 * v + 2] = make_float4(T[8], T[9], T[10], T[11]);
     }
-    if (planes) {
-        const int64_t stride = 2 * V;  // float4 units per row plane
-        const bool has_left = (v % nx) != 0;
-        planes[2 * v] = r0;
-        planes[stride + 2 * v] = r1;
-        planes[2 * stride + 2 * v] = r2;
-        if (has_left) {
-            planes[2 * (v - 1) + 1] = r0;
-            planes[stride + 2 * (v - 1) + 1] = r1;
-            planes[2 * stride + 2 * (v - 1) + 1] = r2;
+    if (p32) put_planes(p32, V, v, has_left, T);
+    if (p64 || tg64) {
+        double D[12];
+#pragma unroll
+        for (int e = 0; e < 12; ++e) D[e] = 0.0;
+        for (int i = 0; i < nb; ++i) {
+            const double wi = (double)__ldg(wv + i);
+#pragma unroll
+            for (int e = 0; e < 12; ++e) D[e] = fma(wi, (double)sB[i * 12 + e], D[e]);
         }
+        if (p64) put_planes(p64, V, v, has_left, D);
+        if (tg64)
+            for (int e = 0; e < 12; ++e) tg64[12 * v + e] = D[e];
     }
 }
 
-// Relayout of a caller-provided [V][12] grid into the gather planes.
-__global__ void __launch_bounds__(256) k_relayout(const float4* __restrict__ tg, int nx, int64_t V,
-                                                  float4* __restrict__ planes) {
+// Relayout of a caller-provided [V][12] grid (float32, or float64 when tg64 != null) into
+// the gather planes of both precisions.
+__global__ void __launch_bounds__(256) k_relayout(const float* __restrict__ tg, const double* __restrict__ tg64, int nx,
+                                                  int64_t V, float* __restrict__ p32, double* __restrict__ p64) {
     const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (v >= V) return;
-    const int64_t stride = 2 * V;
-    const bool has_right = (v % nx) != nx - 1;
+    const bool has_left = (v % nx) != 0;
+    float T[12];
+    double D[12];
 #pragma unroll
-    for (int r = 0; r < 3; ++r) {
-        planes[r * stride + 2 * v] = tg[3 * v + r];
-        planes[r * stride + 2 * v + 1] = has_right ? tg[3 * (v + 1) + r] : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int e = 0; e < 12; ++e) {
+        D[e] = tg64 ? tg64[12 * v + e] : (double)tg[12 * v + e];
+        T[e] = tg ? tg[12 * v + e] : (float)D[e];
     }
+    if (p32) put_planes(p32, V, v, has_left, T);
+    if (p64) put_planes(p64, V, v, has_left, D);
 }
 
 // ============================================================================ sort
@@ -91,8 +123,9 @@ __device__ __forceinline__ int f2ord(float f) {
 }
 __device__ __forceinline__ float ord2f(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7fffffff); }
 
-__global__ void k_sort_init(int* __restrict__ hist, int* __restrict__ bbox) {
+__global__ void k_sort_init(int* __restrict__ hist, int* __restrict__ bbox, int* __restrict__ esc_count) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t == 0) *esc_count = 0;
     for (int i = t; i < kSortBuckets; i += gridDim.x * blockDim.x) hist[i] = 0;
     if (t < 3) {
         bbox[t] = f2ord(INFINITY);
@@ -203,12 +236,14 @@ __global__ void __launch_bounds__(256) k_sort_scatter(const float* __restrict__ 
 }
 
 __global__ void __launch_bounds__(256) k_identity_order(const float* __restrict__ x, int64_t n, int* __restrict__ perm,
-                                                        float4* __restrict__ xs) {
+                                                        float4* __restrict__ xs, int* __restrict__ esc_count) {
     const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p == 0) *esc_count = 0;
     if (p >= n) return;
     perm[p] = (int)p;
     xs[p] = make_float4(x[3 * p], x[3 * p + 1], x[3 * p + 2], 0.f);
 }
+
 
 // ============================================================================ K2
 // Per-solve state, bone-major in sorted order: q = bone*n + j.
@@ -223,76 +258,95 @@ struct SearchPlanes {
 
 constexpr int kSearchBlock = 256;
 #ifndef FSK_SEARCH_MINB
-#define FSK_SEARCH_MINB 3  // resident blocks per SM the register budget is sized for
+#define FSK_SEARCH_MINB 3  // resident blocks per SM the fast pass's register budget is sized for
 #endif
 
-// One thread per (posed point, bone-init) solve. Blocks are bone-major (B_i^-1 is a
-// block-uniform broadcast load) over spatially sorted queries.
-__global__ void __launch_bounds__(kSearchBlock, FSK_SEARCH_MINB) k_search(Planes P, GridP g, const float* __restrict__ bones,
-                                                            const float4* __restrict__ xs, int64_t n,
-                                                            int blocks_per_bone, SearchP o, SearchPlanes out) {
+template <typename R>
+__device__ __forceinline__ void store_solve(const SearchPlanes& out, int64_t q, R x0, R x1, R x2, const R Ji[9], R err2,
+                                            const SolveOut& s) {
+    out.xr[q] = make_float4((float)x0, (float)x1, (float)x2, (float)sqrt(err2));
+    out.ja[q] = make_float4((float)Ji[0], (float)Ji[1], (float)Ji[2], (float)Ji[3]);
+    out.jb[q] = make_float4((float)Ji[4], (float)Ji[5], (float)Ji[6], (float)Ji[7]);
+    out.jc[q] = (float)Ji[8];
+    out.meta[q] = (uint16_t)(s.iters | (s.conv ? 0x100 : 0));
+}
+
+// Work counters for the roofline (bench.py): per pass, solves / Broyden iterations /
+// converged-terminating iterations, one warp-aggregated atomic per warp.
+__device__ __forceinline__ void count_work(unsigned long long* stats, const SolveOut& s) {
+    if (!stats) return;
+    const unsigned act = __activemask();
+    const unsigned it = __reduce_add_sync(act, (unsigned)s.iters);
+    const unsigned fin = __reduce_add_sync(act, (unsigned)(s.conv && s.iters > 0));
+    if ((threadIdx.x & 31) == __ffs(act) - 1) {
+        atomicAdd(stats + 0, (unsigned long long)__popc(act));
+        atomicAdd(stats + 1, (unsigned long long)it);
+        atomicAdd(stats + 2, (unsigned long long)fin);
+    }
+}
+
+// Fast pass: one thread per (posed point, bone-init) solve in float32. Blocks are
+// bone-major (B_i^-1 is a block-uniform broadcast load) over spatially sorted queries.
+// Solves flagged for escalation are appended (warp-aggregated) to esc_q.
+__global__ void __launch_bounds__(kSearchBlock, FSK_SEARCH_MINB)
+    k_search_fast(Planes<float> P, GridP g, const float* __restrict__ bones, const float4* __restrict__ xs, int64_t n,
+                  int blocks_per_bone, SearchP o, SearchPlanes out, int* __restrict__ esc_q,
+                  int* __restrict__ esc_count, unsigned long long* __restrict__ stats) {
     const int bone = blockIdx.x / blocks_per_bone;
     const int64_t j = (int64_t)(blockIdx.x - bone * blocks_per_bone) * kSearchBlock + threadIdx.x;
     if (j >= n) return;
     const float4 xq = __ldg(xs + j);
-    const float xp0 = xq.x, xp1 = xq.y, xp2 = xq.z;
-
-    float x0, x1, x2, Ji[9], T[12], d[3];
-    solve_init(P, g, bones + 12 * bone, xp0, xp1, xp2, x0, x1, x2, Ji, T);
-    apply_T(T, x0, x1, x2, d);  // g0 = d(x0) − x' from the init gather (correspondence.cpp:137)
-    float g0 = d[0] - xp0, g1 = d[1] - xp1, g2 = d[2] - xp2;
-    float err2 = g0 * g0 + g1 * g1 + g2 * g2;
-
-    int iters = 0;
-    bool conv = err2 < o.conv2;  // (:100-103)
-    if (!conv) {
-        for (int k = 0; k < o.max_iters; ++k) {
-            if (err2 > o.div2) break;  // divergence check at the top (:105)
-            // dx = −J~ g; x += dx (:106-107)
-            const float dx0 = -(Ji[0] * g0 + Ji[1] * g1 + Ji[2] * g2);
-            const float dx1 = -(Ji[3] * g0 + Ji[4] * g1 + Ji[5] * g2);
-            const float dx2 = -(Ji[6] * g0 + Ji[7] * g1 + Ji[8] * g2);
-            x0 += dx0;
-            x1 += dx1;
-            x2 += dx2;
-            // g' = d(x) − x'; dg = g' − g (:108-112)
-            const Cell c = locate<false>(g, x0, x1, x2);
-            trilerp_T(P, g, c, T);
-            apply_T(T, x0, x1, x2, d);
-            const float n0 = d[0] - xp0, n1 = d[1] - xp1, n2 = d[2] - xp2;
-            const float dg0 = n0 - g0, dg1 = n1 - g1, dg2 = n2 - g2;
-            g0 = n0;
-            g1 = n1;
-            g2 = n2;
-            iters = k + 1;
-            err2 = g0 * g0 + g1 * g1 + g2 * g2;
-            if (err2 < o.conv2) {  // (:113-116)
-                conv = true;
-                break;
-            }
-            // good Broyden: J~ += ((dx − J~dg)/(dx·J~dg)) (dxᵀJ~) if |den| > 1e-18 (:118-122)
-            const float j0 = Ji[0] * dg0 + Ji[1] * dg1 + Ji[2] * dg2;
-            const float j1 = Ji[3] * dg0 + Ji[4] * dg1 + Ji[5] * dg2;
-            const float j2 = Ji[6] * dg0 + Ji[7] * dg1 + Ji[8] * dg2;
-            const float den = dx0 * j0 + dx1 * j1 + dx2 * j2;
-            if (fabsf(den) > 1e-18f) {
-                const float inv = 1.f / den;
-                const float q0 = (dx0 - j0) * inv, q1 = (dx1 - j1) * inv, q2 = (dx2 - j2) * inv;
-                const float w0 = dx0 * Ji[0] + dx1 * Ji[3] + dx2 * Ji[6];
-                const float w1 = dx0 * Ji[1] + dx1 * Ji[4] + dx2 * Ji[7];
-                const float w2 = dx0 * Ji[2] + dx1 * Ji[5] + dx2 * Ji[8];
-                Ji[0] = fmaf(q0, w0, Ji[0]); Ji[1] = fmaf(q0, w1, Ji[1]); Ji[2] = fmaf(q0, w2, Ji[2]);
-                Ji[3] = fmaf(q1, w0, Ji[3]); Ji[4] = fmaf(q1, w1, Ji[4]); Ji[5] = fmaf(q1, w2, Ji[5]);
-                Ji[6] = fmaf(q2, w0, Ji[6]); Ji[7] = fmaf(q2, w1, Ji[7]); Ji[8] = fmaf(q2, w2, Ji[8]);
-            }
+    float x0, x1, x2, Ji[9], err2;
+    const SolveOut s = solve_one<float, true>(P, g, bones + 12 * bone, xq.x, xq.y, xq.z, o, x0, x1, x2, Ji, err2);
+    const int64_t q = (int64_t)bone * n + j;
+    store_solve(out, q, x0, x1, x2, Ji, err2, s);
+    count_work(stats, s);
+    if (esc_q) {
+        const unsigned act = __activemask();
+        const unsigned m = __ballot_sync(act, s.esc);
+        if (m) {
+            const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+            int base = 0;
+            if (lane == leader) base = atomicAdd(esc_count, __popc(m));
+            base = __shfl_sync(act, base, leader);
+            if (s.esc) esc_q[base + __popc(m & ((1u << lane) - 1))] = (int)q;
         }
     }
-    const int64_t q = (int64_t)bone * n + j;
-    out.xr[q] = make_float4(x0, x1, x2, sqrtf(err2));
-    out.ja[q] = make_float4(Ji[0], Ji[1], Ji[2], Ji[3]);
-    out.jb[q] = make_float4(Ji[4], Ji[5], Ji[6], Ji[7]);
-    out.jc[q] = Ji[8];
-    out.meta[q] = (uint16_t)(iters | (conv ? 0x100 : 0));
+}
+
+// Escalation pass: the flagged solves from scratch in float64 (persistent grid-stride over
+// the device-side queue), overwriting their float32 results.
+__global__ void __launch_bounds__(128) k_search_escalated(Planes<double> P, GridP g, const float* __restrict__ bones,
+                                                          const float4* __restrict__ xs, int64_t n, SearchP o,
+                                                          SearchPlanes out, const int* __restrict__ esc_q,
+                                                          const int* __restrict__ esc_count,
+                                                          unsigned long long* __restrict__ stats) {
+    const int cnt = *esc_count;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+        const int64_t q = esc_q[i];
+        const int bone = (int)(q / n);
+        const int64_t j = q - (int64_t)bone * n;
+        const float4 xq = __ldg(xs + j);
+        double x0, x1, x2, Ji[9], err2;
+        const SolveOut s =
+            solve_one<double, false>(P, g, bones + 12 * bone, xq.x, xq.y, xq.z, o, x0, x1, x2, Ji, err2);
+        store_solve(out, q, x0, x1, x2, Ji, err2, s);
+        count_work(stats ? stats + 3 : nullptr, s);
+    }
+}
+
+// Parity mode: every solve in float64.
+__global__ void __launch_bounds__(128) k_search_f64(Planes<double> P, GridP g, const float* __restrict__ bones,
+                                                    const float4* __restrict__ xs, int64_t n, int blocks_per_bone,
+                                                    SearchP o, SearchPlanes out, unsigned long long* __restrict__ stats) {
+    const int bone = blockIdx.x / blocks_per_bone;
+    const int64_t j = (int64_t)(blockIdx.x - bone * blocks_per_bone) * 128 + threadIdx.x;
+    if (j >= n) return;
+    const float4 xq = __ldg(xs + j);
+    double x0, x1, x2, Ji[9], err2;
+    const SolveOut s = solve_one<double, false>(P, g, bones + 12 * bone, xq.x, xq.y, xq.z, o, x0, x1, x2, Ji, err2);
+    store_solve(out, (int64_t)bone * n + j, x0, x1, x2, Ji, err2, s);
+    count_work(stats ? stats + 3 : nullptr, s);
 }
 
 // ============================================================================ dedup
@@ -488,16 +542,17 @@ __global__ void __launch_bounds__(256) k_emit_dense(int64_t n, int nb, DenseOut 
     }
 }
 
+
 // ============================================================================ E
-__global__ void __launch_bounds__(256) k_eval_points(Planes P, GridP g, const float* __restrict__ x, int64_t n,
+__global__ void __launch_bounds__(256) k_eval_points(Planes<float> P, GridP g, const float* __restrict__ x, int64_t n,
                                                      float* __restrict__ t12, float* __restrict__ dout,
                                                      float* __restrict__ jac) {
     const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (p >= n) return;
     const float x0 = x[3 * p], x1 = x[3 * p + 1], x2 = x[3 * p + 2];
     float T[12], J[9], d[3];
-    jacobian_and_T(P, g, x0, x1, x2, T, J);
-    apply_T(T, x0, x1, x2, d);
+    jacobian_and_T<float>(P, g, x0, x1, x2, T, J);
+    apply_T<float>(T, x0, x1, x2, d);
     if (t12)
         for (int e = 0; e < 12; ++e) t12[12 * p + e] = T[e];
     if (dout)
@@ -507,7 +562,7 @@ __global__ void __launch_bounds__(256) k_eval_points(Planes P, GridP g, const fl
 }
 
 // init_states (correspondence.cpp:58-70): one thread per (point, bone), point-major output.
-__global__ void __launch_bounds__(256) k_init_states(Planes P, GridP g, const float* __restrict__ bones,
+__global__ void __launch_bounds__(256) k_init_states(Planes<float> P, GridP g, const float* __restrict__ bones,
                                                      const float* __restrict__ pts, int64_t n, float* __restrict__ x0o,
                                                      float* __restrict__ jo) {
     const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -515,7 +570,7 @@ __global__ void __launch_bounds__(256) k_init_states(Planes P, GridP g, const fl
     const int64_t p = s / g.nb;
     const int bone = (int)(s - p * g.nb);
     float x0, x1, x2, Ji[9], T[12];
-    solve_init(P, g, bones + 12 * bone, pts[3 * p], pts[3 * p + 1], pts[3 * p + 2], x0, x1, x2, Ji, T);
+    solve_init<float>(P, g, bones + 12 * bone, pts[3 * p], pts[3 * p + 1], pts[3 * p + 2], x0, x1, x2, Ji, T);
     if (x0o) {
         x0o[3 * s] = x0;
         x0o[3 * s + 1] = x1;
@@ -530,27 +585,39 @@ namespace {
 
 int64_t vertex_count(const GridP& g) { return (int64_t)g.nx * g.ny * g.nz; }
 
-Planes planes_scratch(fsk_ctx* ctx, const GridP& g) {
+struct GridPlanes {
+    Planes<float> p32;
+    Planes<double> p64;
+};
+
+GridPlanes planes_scratch(fsk_ctx* ctx, const GridP& g) {
     const int64_t V = vertex_count(g);
-    Planes P;
-    P.p = (const float*)scratch(ctx, kPlanes, 3 * V * 8 * sizeof(float));
-    P.stride = V * 8;
+    GridPlanes P;
+    P.p32.p = (const float*)scratch(ctx, kPlanes, 3 * V * 8 * sizeof(float));
+    P.p32.stride = V * 8;
+    P.p64.p = (const double*)scratch(ctx, kPlanes64, 3 * V * 8 * sizeof(double));
+    P.p64.stride = V * 8;
     return P;
 }
 
-void run_precompute(fsk_ctx* ctx, const float* w, const GridP& g, const float* bones, float* tg, bool planes,
-                    cudaStream_t st) {
+bool needs_f64(int flags) { return !(flags & FSK_SEARCH_FP32_ONLY); }
+
+// K1: tg / tg64 outputs optional; planes in both precisions when `planes`.
+GridPlanes run_precompute(fsk_ctx* ctx, const float* w, const GridP& g, const float* bones, float* tg, double* tg64,
+                          bool planes, bool f64, cudaStream_t st) {
     const int64_t V = vertex_count(g);
-    float4* pl = planes ? (float4*)planes_scratch(ctx, g).p : nullptr;
+    GridPlanes P = planes_scratch(ctx, g);
     FSK_LAUNCH(ctx, st, k_precompute, blocks_for(V, 256), 256, g.nb * 12 * sizeof(float), w, bones, g.nb, g.nx, V,
-               reinterpret_cast<float4*>(tg), pl);
+               reinterpret_cast<float4*>(tg), planes ? (float*)P.p32.p : nullptr,
+               planes && f64 ? (double*)P.p64.p : nullptr, tg64);
+    return P;
 }
 
-Planes run_relayout(fsk_ctx* ctx, const float* tg, const GridP& g, cudaStream_t st) {
+GridPlanes run_relayout(fsk_ctx* ctx, const float* tg, const double* tg64, const GridP& g, bool f64, cudaStream_t st) {
     const int64_t V = vertex_count(g);
-    Planes P = planes_scratch(ctx, g);
-    FSK_LAUNCH(ctx, st, k_relayout, blocks_for(V, 256), 256, 0, reinterpret_cast<const float4*>(tg), g.nx, V,
-               (float4*)P.p);
+    GridPlanes P = planes_scratch(ctx, g);
+    FSK_LAUNCH(ctx, st, k_relayout, blocks_for(V, 256), 256, 0, tg, tg64, g.nx, V, (float*)P.p32.p,
+               f64 ? (double*)P.p64.p : nullptr);
     return P;
 }
 
@@ -560,9 +627,9 @@ struct SearchState {
     int32_t* n_roots_p;
 };
 
-// sort + K2 + dedup into the ctx's search planes.
-SearchState run_search(fsk_ctx* ctx, const Planes& P, const GridP& g, const float* bones, const float* pts, int64_t n,
-                       const SearchP& sp, int flags, cudaStream_t st) {
+// sort + K2 (+ K2b escalation) + dedup into the ctx's search planes.
+SearchState run_search(fsk_ctx* ctx, const GridPlanes& P, const GridP& g, const float* bones, const float* pts,
+                       int64_t n, const SearchP& sp, int flags, cudaStream_t st) {
     if (n >= (int64_t(1) << 31) / std::max(1, g.nb)) fail(FSK_EINVAL, "fsk: too many points for one call (split the batch)");
     const int64_t S = std::max<int64_t>(1, n * g.nb);
     SearchState s;
@@ -576,24 +643,42 @@ SearchState run_search(fsk_ctx* ctx, const Planes& P, const GridP& g, const floa
     s.n_roots_p = (int32_t*)scratch(ctx, kNRoots, std::max<int64_t>(1, n) * sizeof(int32_t));
     if (n == 0) return s;
     float4* xs = (float4*)scratch(ctx, kXs, n * sizeof(float4));
+    int* esc_n = (int*)scratch(ctx, kEscN, sizeof(int));
     if (!(flags & FSK_SEARCH_NO_SORT)) {
         int* hist = (int*)scratch(ctx, kHist, kSortBuckets * sizeof(int));
         int* bbox = (int*)scratch(ctx, kBbox, 6 * sizeof(int));
         uint16_t* keys = (uint16_t*)scratch(ctx, kKeys, n * sizeof(uint16_t));
-        FSK_LAUNCH(ctx, st, k_sort_init, 32, 1024, 0, hist, bbox);
+        FSK_LAUNCH(ctx, st, k_sort_init, 32, 1024, 0, hist, bbox, esc_n);
         const unsigned gb = (unsigned)std::min<int64_t>(blocks_for(n, 256), (int64_t)ctx->sm_count * 8);
         FSK_LAUNCH(ctx, st, k_sort_bbox, gb, 256, 0, pts, n, bbox);
         FSK_LAUNCH(ctx, st, k_sort_hist, blocks_for(n, 256), 256, 0, pts, n, bbox, keys, hist);
         FSK_LAUNCH(ctx, st, k_sort_scan, 1, 1024, 0, hist);
         FSK_LAUNCH(ctx, st, k_sort_scatter, blocks_for(n, 256), 256, 0, pts, keys, n, hist, s.perm, xs);
     } else {
-        FSK_LAUNCH(ctx, st, k_identity_order, blocks_for(n, 256), 256, 0, pts, n, s.perm, xs);
+        FSK_LAUNCH(ctx, st, k_identity_order, blocks_for(n, 256), 256, 0, pts, n, s.perm, xs, esc_n);
     }
-    const int bpb = (int)blocks_for(n, kSearchBlock);
-    const int64_t nblocks = (int64_t)bpb * g.nb;
-    if (nblocks >= (int64_t(1) << 31)) fail(FSK_EINVAL, "fsk: search grid too large");
-    FSK_LAUNCH(ctx, st, k_search, (unsigned)nblocks, kSearchBlock, 0, P, g, bones, xs, n, bpb, sp, s.sp);
-    FSK_LAUNCH(ctx, st, k_dedup, blocks_for(n, 256), 256, 0, n, g.nb, sp.dedup2, s.sp, s.perm, s.n_roots_p);
+    if (flags & FSK_SEARCH_FP64) {
+        const int bpb = (int)blocks_for(n, 128);
+        const int64_t nblocks = (int64_t)bpb * g.nb;
+        if (nblocks >= (int64_t(1) << 31)) fail(FSK_EINVAL, "fsk: search grid too large");
+        FSK_LAUNCH(ctx, st, k_search_f64, (unsigned)nblocks, 128, 0, P.p64, g, bones, xs, n, bpb, sp, s.sp, ctx->stats);
+    } else {
+        const bool esc = needs_f64(flags);
+        int* esc_q = esc ? (int*)scratch(ctx, kEscQ, S * sizeof(int)) : nullptr;
+        const int bpb = (int)blocks_for(n, kSearchBlock);
+        const int64_t nblocks = (int64_t)bpb * g.nb;
+        if (nblocks >= (int64_t(1) << 31)) fail(FSK_EINVAL, "fsk: search grid too large");
+        SearchP spf = sp;
+        if (!esc) {  // float32 only (ablation): no cap, no flags
+            spf.esc_cap = sp.max_iters;
+        }
+        FSK_LAUNCH(ctx, st, k_search_fast, (unsigned)nblocks, kSearchBlock, 0, P.p32, g, bones, xs, n, bpb, spf, s.sp,
+                   esc_q, esc_n, ctx->stats);
+        if (esc)
+            FSK_LAUNCH(ctx, st, k_search_escalated, (unsigned)ctx->sm_count * 8, 128, 0, P.p64, g, bones, xs, n, sp, s.sp,
+                       esc_q, esc_n, ctx->stats);
+    }
+    FSK_LAUNCH(ctx, st, k_dedup, blocks_for(n, 256), 256, 0, n, g.nb, (float)sp.dedup2, s.sp, s.perm, s.n_roots_p);
     return s;
 }
 
@@ -626,31 +711,32 @@ using namespace fsk;
 extern "C" {
 
 int fsk_precompute_tgrid(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* desc, const float* bones,
-                         int32_t n_bones_pose, float* tgrid, void* stream) {
+                         int32_t n_bones_pose, float* tgrid, double* tgrid64, void* stream) {
     return guard([&] {
         set_device(ctx);
         const GridP g = make_grid(desc);
         if (n_bones_pose != g.nb) fail(FSK_EINVAL, "precompute_transform_grid: bone count mismatch");
-        if (!weights || !bones || !tgrid) fail(FSK_EINVAL, "fsk: null buffer");
-        run_precompute(ctx, weights, g, bones, tgrid, false, (cudaStream_t)stream);
+        if (!weights || !bones || (!tgrid && !tgrid64)) fail(FSK_EINVAL, "fsk: null buffer");
+        run_precompute(ctx, weights, g, bones, tgrid, tgrid64, false, false, (cudaStream_t)stream);
     });
 }
 
-int fsk_search_fwd(fsk_ctx* ctx, const float* tgrid, const fsk_grid_desc* desc, const float* bones,
-                   int32_t n_bones_pose, const float* points, int64_t n, const fsk_search_opts* opts,
-                   fsk_search_out* out, void* stream) {
+int fsk_search_fwd(fsk_ctx* ctx, const float* tgrid, const double* tgrid64, const fsk_grid_desc* desc,
+                   const float* bones, int32_t n_bones_pose, const float* points, int64_t n,
+                   const fsk_search_opts* opts, fsk_search_out* out, void* stream) {
     return guard([&] {
         set_device(ctx);
         // check_context (correspondence.cpp:29-41), then validate (:19-25)
         const GridP g = make_grid(desc);
-        check_search_args(g, n_bones_pose, tgrid, "search: grid bone count mismatch");
+        check_search_args(g, n_bones_pose, tgrid ? (const void*)tgrid : (const void*)tgrid64,
+                          "search: grid bone count mismatch");
         const SearchP sp = make_search(opts);
-        if (!out || !out->converged) fail(FSK_EINVAL, "fsk: search output needs a converged mask");
+        if (!out || (n > 0 && !out->converged)) fail(FSK_EINVAL, "fsk: search output needs a converged mask");
         if (n < 0) fail(FSK_EINVAL, "fsk: negative point count");
         if (n > 0 && (!points || !bones)) fail(FSK_EINVAL, "fsk: null buffer");
         if (n == 0) return;
         cudaStream_t st = (cudaStream_t)stream;
-        const Planes P = run_relayout(ctx, tgrid, g, st);
+        const GridPlanes P = run_relayout(ctx, tgrid, tgrid64, g, needs_f64(opts->flags), st);
         const SearchState s = run_search(ctx, P, g, bones, points, n, sp, opts->flags, st);
         DenseOut d{out->x_c, out->jinv, out->resid, out->iters, out->converged, out->keep, out->n_roots};
         FSK_LAUNCH(ctx, st, k_scatter_dense, blocks_for(n * g.nb, 256), 256, 0, n, g.nb, s.sp, s.perm, d);
@@ -660,18 +746,19 @@ int fsk_search_fwd(fsk_ctx* ctx, const float* tgrid, const fsk_grid_desc* desc, 
     });
 }
 
-int fsk_batch_search(fsk_ctx* ctx, const float* tgrid, const fsk_grid_desc* desc, const float* bones,
-                     int32_t n_bones_pose, const float* points, int64_t n, const fsk_search_opts* opts,
-                     int64_t* offsets, fsk_root* roots, int64_t cap, void* stream) {
+int fsk_batch_search(fsk_ctx* ctx, const float* tgrid, const double* tgrid64, const fsk_grid_desc* desc,
+                     const float* bones, int32_t n_bones_pose, const float* points, int64_t n,
+                     const fsk_search_opts* opts, int64_t* offsets, fsk_root* roots, int64_t cap, void* stream) {
     return guard([&] {
         set_device(ctx);
         const GridP g = make_grid(desc);
-        check_search_args(g, n_bones_pose, tgrid, "search: grid bone count mismatch");
+        check_search_args(g, n_bones_pose, tgrid ? (const void*)tgrid : (const void*)tgrid64,
+                          "search: grid bone count mismatch");
         const SearchP sp = make_search(opts);
         if (n < 0) fail(FSK_EINVAL, "fsk: negative point count");
         if (!offsets || (n > 0 && (!points || !bones))) fail(FSK_EINVAL, "fsk: null buffer");
         cudaStream_t st = (cudaStream_t)stream;
-        const Planes P = run_relayout(ctx, tgrid, g, st);
+        const GridPlanes P = run_relayout(ctx, tgrid, tgrid64, g, needs_f64(opts->flags), st);
         const SearchState s = run_search(ctx, P, g, bones, points, n, sp, opts->flags, st);
         compact(ctx, s, n, g.nb, offsets, roots, cap, st);
     });
@@ -688,8 +775,8 @@ int fsk_deform(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* desc, co
         if (n < 0) fail(FSK_EINVAL, "fsk: negative point count");
         if (!offsets || !bones || (n > 0 && !points)) fail(FSK_EINVAL, "fsk: null buffer");
         cudaStream_t st = (cudaStream_t)stream;
-        run_precompute(ctx, weights, g, bones, tgrid, true, st);
-        const SearchState s = run_search(ctx, planes_scratch(ctx, g), g, bones, points, n, sp, opts->flags, st);
+        const GridPlanes P = run_precompute(ctx, weights, g, bones, tgrid, nullptr, true, needs_f64(opts->flags), st);
+        const SearchState s = run_search(ctx, P, g, bones, points, n, sp, opts->flags, st);
         compact(ctx, s, n, g.nb, offsets, roots, cap, st);
     });
 }
@@ -741,8 +828,8 @@ int fsk_deform_host(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* des
         cuda_check(cudaMemcpyAsync(dB, bones, nb * 12 * sizeof(float), cudaMemcpyHostToDevice, st), "H2D bones");
         if (n > 0)
             cuda_check(cudaMemcpyAsync(dP, points, n * 3 * sizeof(float), cudaMemcpyHostToDevice, st), "H2D points");
-        run_precompute(ctx, dW, g, dB, nullptr, true, st);
-        const SearchState s = run_search(ctx, planes_scratch(ctx, g), g, dB, dP, n, sp, opts->flags, st);
+        const GridPlanes P = run_precompute(ctx, dW, g, dB, nullptr, nullptr, true, needs_f64(opts->flags), st);
+        const SearchState s = run_search(ctx, P, g, dB, dP, n, sp, opts->flags, st);
         compact(ctx, s, n, nb, dOff, dR, rcap, st);
         cuda_check(cudaMemcpyAsync(offsets, dOff, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st), "D2H offsets");
         cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
@@ -767,8 +854,8 @@ int fsk_init_states(fsk_ctx* ctx, const float* tgrid, const fsk_grid_desc* desc,
         if (n == 0) return;
         if (!points || !bones) fail(FSK_EINVAL, "fsk: null buffer");
         cudaStream_t st = (cudaStream_t)stream;
-        const Planes P = run_relayout(ctx, tgrid, g, st);
-        FSK_LAUNCH(ctx, st, k_init_states, blocks_for(n * g.nb, 256), 256, 0, P, g, bones, points, n, x0, jinv0);
+        const GridPlanes P = run_relayout(ctx, tgrid, nullptr, g, false, st);
+        FSK_LAUNCH(ctx, st, k_init_states, blocks_for(n * g.nb, 256), 256, 0, P.p32, g, bones, points, n, x0, jinv0);
     });
 }
 
@@ -781,8 +868,8 @@ int fsk_eval_points(fsk_ctx* ctx, const float* tgrid, const fsk_grid_desc* desc,
         if (n == 0) return;
         if (!tgrid || !x) fail(FSK_EINVAL, "fsk: null buffer");
         cudaStream_t st = (cudaStream_t)stream;
-        const Planes P = run_relayout(ctx, tgrid, g, st);
-        FSK_LAUNCH(ctx, st, k_eval_points, blocks_for(n, 256), 256, 0, P, g, x, n, t12, d, jac);
+        const GridPlanes P = run_relayout(ctx, tgrid, nullptr, g, false, st);
+        FSK_LAUNCH(ctx, st, k_eval_points, blocks_for(n, 256), 256, 0, P.p32, g, x, n, t12, d, jac);
     });
 }
 

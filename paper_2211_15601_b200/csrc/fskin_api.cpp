@@ -118,9 +118,9 @@ void check_context(const SearchContext& c, SearchVariant variant) {
 fsk_search_opts c_opts(const SearchOptions& o) {
     fsk_search_opts c;
     c.max_iters = o.max_iters;
-    c.conv_eps = static_cast<float>(o.conv_eps);
-    c.div_eps = static_cast<float>(o.div_eps);
-    c.dedup_dist = static_cast<float>(o.dedup_dist);
+    c.conv_eps = o.conv_eps;
+    c.div_eps = o.div_eps;
+    c.dedup_dist = o.dedup_dist;
     c.flags = 0;
     return c;
 }
@@ -341,21 +341,39 @@ void TransformGrid::set_vertex(std::int64_t v, const Affine3& t) {
     }
 }
 
-const float* TransformGrid::device_data() const {
+namespace {
+std::shared_ptr<void> dev_buffer(size_t bytes) {
+    return std::shared_ptr<void>(new DevBuf(bytes), [](void* p) { delete static_cast<DevBuf*>(p); });
+}
+}  // namespace
+
+void TransformGrid::sync_device() const {
     const size_t V = static_cast<size_t>(dims_.vertex_count());
-    if (!dev_) {
-        auto* b = new DevBuf(V * 12 * sizeof(float));
-        dev_ = std::shared_ptr<void>(b, [](void* p) { delete static_cast<DevBuf*>(p); });
+    if (!dev_ || !dev64_) {
+        dev_ = dev_buffer(V * 12 * sizeof(float));
+        dev64_ = dev_buffer(V * 12 * sizeof(double));
         host_dirty_ = true;
     }
     if (host_dirty_) {
         std::vector<float> f(data_.begin(), data_.end());
         h2d(static_cast<DevBuf*>(dev_.get())->p, f.data(), f.size() * sizeof(float));
+        h2d(static_cast<DevBuf*>(dev64_.get())->p, data_.data(), data_.size() * sizeof(double));
         host_dirty_ = false;
     }
+}
+
+const float* TransformGrid::device_data() const {
+    sync_device();
     return static_cast<DevBuf*>(dev_.get())->as<float>();
 }
 
+const double* TransformGrid::device_data64() const {
+    sync_device();
+    return static_cast<DevBuf*>(dev64_.get())->as<double>();
+}
+
+// K1 on the GPU in float32 (the fast search's grid) and float64 (the reference's
+// TransformGrid precision: the host copy and the float64 re-solves read it).
 TransformGrid precompute_transform_grid(const SkinningVoxelGrid& grid, std::span<const RigidTransform> bones, int) {
     if (static_cast<int>(bones.size()) != grid.bone_count())
         throw std::invalid_argument("precompute_transform_grid: bone count mismatch");
@@ -365,15 +383,14 @@ TransformGrid precompute_transform_grid(const SkinningVoxelGrid& grid, std::span
     std::vector<float> w(grid.raw().begin(), grid.raw().end());
     const std::vector<float> b = bones_f32(bones);
     DevBuf dw(w.size() * sizeof(float)), db(b.size() * sizeof(float));
-    auto* dt = new DevBuf(static_cast<size_t>(V) * 12 * sizeof(float));
-    tg.dev_ = std::shared_ptr<void>(dt, [](void* p) { delete static_cast<DevBuf*>(p); });
+    tg.dev_ = dev_buffer(static_cast<size_t>(V) * 12 * sizeof(float));
+    tg.dev64_ = dev_buffer(static_cast<size_t>(V) * 12 * sizeof(double));
     h2d(dw.p, w.data(), w.size() * sizeof(float));
     h2d(db.p, b.data(), b.size() * sizeof(float));
     const fsk_grid_desc d = desc_of(grid.dims(), grid.bbox(), nb);
-    check(fsk_precompute_tgrid(ctx(), dw.as<float>(), &d, db.as<float>(), nb, dt->as<float>(), nullptr));
-    std::vector<float> out(static_cast<size_t>(V) * 12);
-    d2h(out.data(), dt->p, out.size() * sizeof(float));
-    std::copy(out.begin(), out.end(), tg.data_.begin());
+    check(fsk_precompute_tgrid(ctx(), dw.as<float>(), &d, db.as<float>(), nb, static_cast<DevBuf*>(tg.dev_.get())->as<float>(),
+                               static_cast<DevBuf*>(tg.dev64_.get())->as<double>(), nullptr));
+    d2h(tg.data_.data(), static_cast<DevBuf*>(tg.dev64_.get())->p, tg.data_.size() * sizeof(double));
     tg.host_dirty_ = false;
     return tg;
 }
@@ -488,28 +505,19 @@ std::vector<CorrespondenceSet> batch_search(std::span<const Vec3> queries, const
     const int nb = static_cast<int>(c.bones.size());
     const std::vector<float> b = bones_f32(c.bones);
     const std::vector<float> p = points_f32(queries);
-    const std::int64_t S = n * nb;
-    DevBuf db(b.size() * 4), dp(p.size() * 4), xc(S * 12), jv(S * 36), rs(S * 4), it(S), cv(S), kp(S), nr(n * 4),
-        offs((n + 1) * 8);
+    const std::int64_t cap = n * nb;  // every init of every query: no overflow possible
+    DevBuf db(b.size() * 4), dp(p.size() * 4), offs((n + 1) * 8), dr(cap * sizeof(fsk_root));
     h2d(db.p, b.data(), b.size() * 4);
     h2d(dp.p, p.data(), p.size() * 4);
-    fsk_search_out o{xc.as<float>(), jv.as<float>(), rs.as<float>(), it.as<uint8_t>(), cv.as<uint8_t>(),
-                     kp.as<uint8_t>(), nr.as<int32_t>()};
     const fsk_grid_desc d = desc_of(c.tgrid->dims(), c.tgrid->bbox(), nb);
     const fsk_search_opts so = c_opts(opts);
-    check(fsk_search_fwd(ctx(), c.tgrid->device_data(), &d, db.as<float>(), nb, dp.as<float>(), n, &so, &o, nullptr));
-    std::int64_t total = 0;
-    // first pass sizes the root buffer (cap 0 → FSK_EINVAL with total set unless empty)
-    const int rc = fsk_compact_roots(ctx(), &o, n, nb, offs.as<std::int64_t>(), nullptr, 0, &total, nullptr);
-    if (rc != FSK_OK && total == 0) check(rc);
+    check(fsk_batch_search(ctx(), c.tgrid->device_data(), c.tgrid->device_data64(), &d, db.as<float>(), nb,
+                           dp.as<float>(), n, &so, offs.as<std::int64_t>(), dr.as<fsk_root>(), cap, nullptr));
     std::vector<std::int64_t> h_offs(n + 1);
-    std::vector<fsk_root> roots(static_cast<size_t>(total));
-    if (total > 0) {
-        DevBuf dr(total * sizeof(fsk_root));
-        check(fsk_compact_roots(ctx(), &o, n, nb, offs.as<std::int64_t>(), dr.as<fsk_root>(), total, &total, nullptr));
-        d2h(roots.data(), dr.p, roots.size() * sizeof(fsk_root));
-    }
     d2h(h_offs.data(), offs.p, h_offs.size() * 8);
+    const std::int64_t total = h_offs[n];
+    std::vector<fsk_root> roots(static_cast<size_t>(total));
+    if (total > 0) d2h(roots.data(), dr.p, roots.size() * sizeof(fsk_root));
     for (std::int64_t q = 0; q < n; ++q) {
         auto& set = out[static_cast<size_t>(q)];
         for (std::int64_t k = h_offs[q]; k < h_offs[q + 1]; ++k) {

@@ -45,6 +45,7 @@ class SearchOptions:
     div_eps: float = 0.5
     dedup_dist: float = 1e-2
     sort: bool = True  # spatial ordering of queries (performance only)
+    precision: str = "mixed"  # "mixed" (fp32 + fp64 escalation), "fp32" (ablation), "fp64" (parity mode)
 
     @staticmethod
     def defaults_for(bbox) -> "SearchOptions":
@@ -65,8 +66,10 @@ class SearchOptions:
             raise FskInvalidArgument("search: dedup_dist must be >= 0")
 
     def c(self) -> SearchOpts:
-        return SearchOpts(int(self.max_iters), float(self.conv_eps), float(self.div_eps), float(self.dedup_dist),
-                          0 if self.sort else _lib.FSK_SEARCH_NO_SORT)
+        flags = 0 if self.sort else _lib.FSK_SEARCH_NO_SORT
+        flags |= {"mixed": 0, "fp32": _lib.FSK_SEARCH_FP32_ONLY, "fp64": _lib.FSK_SEARCH_FP64}[self.precision]
+        return SearchOpts(int(self.max_iters), flags, float(self.conv_eps), float(self.div_eps),
+                          float(self.dedup_dist))
 
 
 def grid_desc(dims, bbox, n_bones) -> GridDesc:
@@ -127,14 +130,22 @@ class Deformer:
                                        ctypes.byref(cnt), 1 if reset else 0))
         return ms.value, cnt.value
 
+    def search_stats(self, reset=True):
+        """(f32 solves, f32 iterations, f32 converged-terminating iterations, f64 solves,
+        f64 iterations, f64 converged-terminating iterations) accumulated by searches."""
+        buf = (ctypes.c_uint64 * 6)()
+        check(self.L.fsk_ctx_search_stats(self._ctx, buf, 1 if reset else 0))
+        return tuple(int(v) for v in buf)
+
     def measure_fp32_peak(self) -> float:
         t = ctypes.c_double()
         check(self.L.fsk_measure_fp32_peak(self._ctx, ctypes.byref(t)))
         return t.value
 
     # ---------------------------------------------------------------- K1
-    def precompute_transform_grid(self, weights, dims, bbox, bones, out=None):
-        """``precompute_transform_grid`` (deformer.hpp:53-55) → tgrid [V,12] float32."""
+    def precompute_transform_grid(self, weights, dims, bbox, bones, out=None, out64=None):
+        """``precompute_transform_grid`` (deformer.hpp:53-55) → tgrid [V,12] float32 (and the
+        float64 grid into ``out64`` [V,12] when given)."""
         weights = _f32(weights, "weights", self.device)
         bones = _f32(bones, "bones", self.device)
         nb = weights.shape[1] if weights.dim() == 2 else bones.shape[0]
@@ -143,7 +154,7 @@ class Deformer:
         if out is None:
             out = torch.empty((V, 12), dtype=torch.float32, device=self.device)
         check(self.L.fsk_precompute_tgrid(self._ctx, _ptr(weights), ctypes.byref(desc), _ptr(bones),
-                                          bones.numel() // 12, _ptr(out), _stream(self.device)))
+                                          bones.numel() // 12, _ptr(out), _ptr(out64), _stream(self.device)))
         return out
 
     # ---------------------------------------------------------------- K2 + dedup
@@ -164,7 +175,7 @@ class Deformer:
         return SearchOut(*[o[k].data_ptr() if o.get(k) is not None else None
                            for k in ("x_c", "jinv", "resid", "iters", "converged", "keep", "n_roots")])
 
-    def batch_search(self, tgrid, dims, bbox, bones, points, opts: SearchOptions, out=None):
+    def batch_search(self, tgrid, dims, bbox, bones, points, opts: SearchOptions, out=None, tgrid64=None):
         """``batch_search`` voxel variant (correspondence.hpp:77-80) → dense per-(point, init)
         results: x_c, jinv, resid, iters, converged, keep (dedup), n_roots."""
         tgrid = _f32(tgrid, "tgrid", self.device)
@@ -176,7 +187,8 @@ class Deformer:
         if out is None:
             out = self.alloc_search_out(n, nb)
         co = self._c_out(out)
-        check(self.L.fsk_search_fwd(self._ctx, _ptr(tgrid), ctypes.byref(desc), _ptr(bones), nb, _ptr(points), n,
+        check(self.L.fsk_search_fwd(self._ctx, _ptr(tgrid), _ptr(tgrid64), ctypes.byref(desc), _ptr(bones), nb,
+                                    _ptr(points), n,
                                     ctypes.byref(opts.c()), ctypes.byref(co), _stream(self.device)))
         return out
 
@@ -187,13 +199,14 @@ class Deformer:
         return (torch.empty((n + 1,), dtype=torch.int64, device=self.device),
                 torch.empty((max(cap, 1), 16), dtype=torch.float32, device=self.device))
 
-    def batch_search_roots(self, tgrid, dims, bbox, bones, points, opts: SearchOptions, out=None):
+    def batch_search_roots(self, tgrid, dims, bbox, bones, points, opts: SearchOptions, out=None, tgrid64=None):
         """``batch_search`` straight to CorrespondenceSets on the device (fsk_batch_search):
         returns (offsets, roots); roots of query p are roots[offsets[p]:offsets[p+1]]."""
         nb, n = bones.numel() // 12, points.shape[0]
         offsets, roots = out if out is not None else self.alloc_roots(n, nb)
         desc = grid_desc(dims, bbox, nb)
-        check(self.L.fsk_batch_search(self._ctx, _ptr(_f32(tgrid, "tgrid", self.device)), ctypes.byref(desc),
+        check(self.L.fsk_batch_search(self._ctx, _ptr(_f32(tgrid, "tgrid", self.device)), _ptr(tgrid64),
+                                      ctypes.byref(desc),
                                       _ptr(_f32(bones, "bones", self.device)), nb,
                                       _ptr(_f32(points, "points", self.device)), n, ctypes.byref(opts.c()),
                                       _ptr(offsets), _ptr(roots), roots.shape[0], _stream(self.device)))

@@ -26,12 +26,16 @@ def opts_of(sc, max_iters):
     return SearchOptions(max_iters=max_iters, **{k: v for k, v in sc.search_options(max_iters).items() if k != "max_iters"})
 
 
-def run_gpu(deformer, sc, max_iters, sort=True):
+def run_gpu(deformer, sc, max_iters, sort=True, precision="mixed"):
+    """K1 (float32 + float64 transform grids from the float32 weights, like the oracle's
+    f64 TransformGrid) then batch_search with the float64 grid for the escalation pass."""
     w, B, x = dev(sc.weights), dev(sc.bones), dev(sc.points)
-    tg = deformer.precompute_transform_grid(w, sc.dims, sc.bbox, B)
+    tg64 = torch.empty((w.shape[0], 12), dtype=torch.float64, device="cuda")
+    tg = deformer.precompute_transform_grid(w, sc.dims, sc.bbox, B, out64=tg64)
     o = opts_of(sc, max_iters)
     o.sort = sort
-    out = deformer.batch_search(tg, sc.dims, sc.bbox, B, x, o)
+    o.precision = precision
+    out = deformer.batch_search(tg, sc.dims, sc.bbox, B, x, o, tgrid64=tg64)
     torch.cuda.synchronize()
     return tg, {k: (v.cpu().numpy() if v is not None else None) for k, v in out.items()}
 
@@ -319,3 +323,29 @@ def test_backward_from_compact_roots_matches_dense(deformer, c3):
     a = deformer.search_bwd(sc.dims, sc.bbox, sc.n_bones, dense, dev(v), dev(sel), deterministic=True)
     b = deformer.search_bwd_roots(sc.dims, sc.bbox, sc.n_bones, roots, dev(ridx), dev(v), deterministic=True)
     np.testing.assert_array_equal(a.cpu().numpy(), b.cpu().numpy())
+
+
+def test_precompute_f64_grid_matches_oracle(deformer, c1):
+    w, B = dev(c1.weights), dev(c1.bones)
+    tg64 = torch.empty((w.shape[0], 12), dtype=torch.float64, device="cuda")
+    deformer.precompute_transform_grid(w, c1.dims, c1.bbox, B, out64=tg64)
+    ref = oracle.precompute_transform_grid(c1.weights, c1.dims, c1.bbox, c1.bones)
+    assert np.abs(tg64.cpu().numpy() - ref).max() < 1e-14
+
+
+def test_precision_modes(deformer):
+    """fp32-only (ablation) misses the bar on chaotic long trajectories; the default mixed
+    mode (fp32 pass + fp64 re-solve of the flagged tail) and fp64 parity mode meet it."""
+    sc = S.make_scene((32, 32, 32), 8000, seed=3)
+    r = run_oracle(sc, 50)
+    res = {}
+    for prec in ("fp32", "mixed", "fp64"):
+        deformer.search_stats(reset=True)
+        _, g = run_gpu(deformer, sc, 50, precision=prec)
+        st = deformer.search_stats(reset=True)
+        agree, dx, _, keep, _ = _parity(g, r, sc.search_options(50)["conv_eps"])
+        res[prec] = (agree, dx, keep, st[3] / max(st[0] + (st[3] if prec == "fp64" else 0), 1))
+        print(f"\n{prec}: mask agreement {agree:.6f} keep {keep:.6f} max|dx| {dx:.2e} fp64 share {res[prec][3]:.4f}")
+    assert res["mixed"][0] >= MASK_AGREE and res["mixed"][1] <= TOL_X
+    assert res["fp64"][0] >= 0.99999 and res["fp64"][1] <= TOL_X
+    assert res["mixed"][3] < 0.15  # the fp64 tail stays a small share of the solves
