@@ -208,8 +208,6 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.current_stream(dev)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     clocks = ClockSampler(local_rank)
-    D.prof_read(reset=True)
-    D.set_profiling(True)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -226,12 +224,28 @@ def run_ours(args, rank, world, local_rank):
         dist.barrier()
     clk = clocks.stop()
     launches = D.launch_count - launches0
-    D.set_profiling(False)
     step_ms = [a.elapsed_time(b) for a, b in evs]
     total_ms = float(np.sum(step_ms))
+    st = D.search_stats(reset=True)
+    # per-kernel device time: a second, profiled pass (events around every launch perturb
+    # the launch gaps, so it is kept out of the timed region above)
+    D.prof_read(reset=True)
+    D.set_profiling(True)
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        step()
+    torch.cuda.synchronize()
+    D.set_profiling(False)
     k2_ms, k2_n = D.prof_read("k_search_fast", reset=False)
     k2e_ms, k2e_n = D.prof_read("k_search_escalated", reset=False)
     k1_ms, k1_n = D.prof_read("k_precompute", reset=False)
+    breakdown = {}
+    for kname in ("k_precompute", "k_sort_init", "k_sort_bbox", "k_sort_hist", "k_sort_scan", "k_sort_scatter",
+                  "k_search_fast", "k_search_escalated", "k_dedup", "k_scan_partial", "k_scan_top", "k_scan_apply",
+                  "k_emit"):
+        ms_, n_ = D.prof_read(kname, reset=False)
+        if n_:
+            breakdown[kname] = round(ms_ / args.steps, 5)
     all_ms, _ = D.prof_read(None, reset=True)
     if world > 1:
         t = torch.tensor([total_ms], device=dev)
@@ -240,7 +254,6 @@ def run_ours(args, rank, world, local_rank):
 
     # algorithmic work per step, counted by the kernels themselves (identical every step):
     # float32 pass (k_search_fast) and float64 escalation pass (k_search_escalated)
-    st = D.search_stats(reset=True)
     per = max(args.steps, 1)
     s32, it32, fin32, s64, it64, fin64 = (v / per for v in st)
     solves = n * nb
@@ -283,6 +296,7 @@ def run_ours(args, rank, world, local_rank):
                                 "achieved_GBps": gather / (k2_avg * 1e-3) / 1e9},
                      "k2_share_of_step": k2_ms / max(all_ms, 1e-9),
                      "k2_escalated_share_of_step": k2e_ms / max(all_ms, 1e-9),
+                     "kernel_ms_per_step": breakdown,
                      "k1": {"bytes_per_launch": k1_bytes, "avg_launch_ms": k1_ms / max(k1_n, 1),
                             "achieved_GBps": k1_bytes / (k1_ms / max(k1_n, 1) * 1e-3) / 1e9}},
         "gpu_launches": launches,
