@@ -97,9 +97,15 @@ struct Planes {
 
 __device__ __forceinline__ void load_edge(const Planes<float>& P, int v, int r, V4<float>& a, V4<float>& b) {
     const float* q = P.p + r * P.stride + (int64_t)v * 8;
+#ifdef FSK_LDG128  // tuning ablation: two 128-bit loads instead of one 256-bit load
+    const float4 lo = __ldg(reinterpret_cast<const float4*>(q)), hi = __ldg(reinterpret_cast<const float4*>(q) + 1);
+    a = V4<float>{lo.x, lo.y, lo.z, lo.w};
+    b = V4<float>{hi.x, hi.y, hi.z, hi.w};
+#else
     asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
         : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
         : "l"(q));
+#endif
 }
 
 __device__ __forceinline__ void load_edge(const Planes<double>& P, int v, int r, V4<double>& a, V4<double>& b) {
@@ -289,14 +295,70 @@ struct SolveOut {
     bool esc;
 };
 
+// One Broyden iteration after the divergence check (correspondence.cpp:106-122): step,
+// re-evaluate, and — unless the new residual converged — the good-Broyden rank-one update.
+// Returns true iff converged; `den` receives dx·J~dg (0 when converged).
+template <typename R>
+__device__ __forceinline__ bool broyden_step(const Planes<R>& P, const GridP& g, R xp0, R xp1, R xp2, R conv2, R& x0,
+                                             R& x1, R& x2, R Ji[9], R& g0, R& g1, R& g2, R& err2, R& den) {
+    // dx = −J~ g; x += dx (:106-107)
+    const R dx0 = -(Ji[0] * g0 + Ji[1] * g1 + Ji[2] * g2);
+    const R dx1 = -(Ji[3] * g0 + Ji[4] * g1 + Ji[5] * g2);
+    const R dx2 = -(Ji[6] * g0 + Ji[7] * g1 + Ji[8] * g2);
+    x0 += dx0;
+    x1 += dx1;
+    x2 += dx2;
+    // g' = d(x) − x'; dg = g' − g (:108-112)
+    R T[12], d[3];
+    const Cell<R> c = locate<false, R>(g, x0, x1, x2);
+    trilerp_T(P, g, c, T);
+    apply_T(T, x0, x1, x2, d);
+    const R n0 = d[0] - xp0, n1 = d[1] - xp1, n2 = d[2] - xp2;
+    const R dg0 = n0 - g0, dg1 = n1 - g1, dg2 = n2 - g2;
+    g0 = n0;
+    g1 = n1;
+    g2 = n2;
+    err2 = g0 * g0 + g1 * g1 + g2 * g2;
+    den = 0;
+    if (err2 < conv2) return true;  // (:113-116)
+    // good Broyden: J~ += ((dx − J~dg)/(dx·J~dg)) (dxᵀJ~) if |den| > 1e-18 (:118-122)
+    const R j0 = Ji[0] * dg0 + Ji[1] * dg1 + Ji[2] * dg2;
+    const R j1 = Ji[3] * dg0 + Ji[4] * dg1 + Ji[5] * dg2;
+    const R j2 = Ji[6] * dg0 + Ji[7] * dg1 + Ji[8] * dg2;
+    den = dx0 * j0 + dx1 * j1 + dx2 * j2;
+    if (fabs(den) > (R)1e-18) {
+        const R inv = (R)1 / den;
+        const R q0 = (dx0 - j0) * inv, q1 = (dx1 - j1) * inv, q2 = (dx2 - j2) * inv;
+        const R w0 = dx0 * Ji[0] + dx1 * Ji[3] + dx2 * Ji[6];
+        const R w1 = dx0 * Ji[1] + dx1 * Ji[4] + dx2 * Ji[7];
+        const R w2 = dx0 * Ji[2] + dx1 * Ji[5] + dx2 * Ji[8];
+        Ji[0] = fma(q0, w0, Ji[0]); Ji[1] = fma(q0, w1, Ji[1]); Ji[2] = fma(q0, w2, Ji[2]);
+        Ji[3] = fma(q1, w0, Ji[3]); Ji[4] = fma(q1, w1, Ji[4]); Ji[5] = fma(q1, w2, Ji[5]);
+        Ji[6] = fma(q2, w0, Ji[6]); Ji[7] = fma(q2, w1, Ji[7]); Ji[8] = fma(q2, w2, Ji[8]);
+    }
+    return false;
+}
+
+// Start of a solve (correspondence.cpp:135-137): x0, J~0 and g0 = d(x0) − x' from one
+// gather. Returns det J(x0).
+template <typename R>
+__device__ __forceinline__ R solve_start(const Planes<R>& P, const GridP& g, const float* __restrict__ B, R xp0, R xp1,
+                                         R xp2, R& x0, R& x1, R& x2, R Ji[9], R& g0, R& g1, R& g2, R& err2) {
+    R T[12], d[3];
+    const R det = solve_init<R>(P, g, B, xp0, xp1, xp2, x0, x1, x2, Ji, T);
+    apply_T(T, x0, x1, x2, d);
+    g0 = d[0] - xp0;
+    g1 = d[1] - xp1;
+    g2 = d[2] - xp2;
+    err2 = g0 * g0 + g1 * g1 + g2 * g2;
+    return det;
+}
+
 template <typename R, bool kFast>
 __device__ __forceinline__ SolveOut solve_one(const Planes<R>& P, const GridP& g, const float* __restrict__ B, R xp0,
                                               R xp1, R xp2, const SearchP& o, R& x0, R& x1, R& x2, R Ji[9], R& err2) {
-    R T[12], d[3];
-    const R det = solve_init<R>(P, g, B, xp0, xp1, xp2, x0, x1, x2, Ji, T);
-    apply_T(T, x0, x1, x2, d);  // g0 = d(x0) − x' from the init gather (:137)
-    R g0 = d[0] - xp0, g1 = d[1] - xp1, g2 = d[2] - xp2;
-    err2 = g0 * g0 + g1 * g1 + g2 * g2;
+    R g0, g1, g2;
+    const R det = solve_start<R>(P, g, B, xp0, xp1, xp2, x0, x1, x2, Ji, g0, g1, g2, err2);
     const R conv2 = (R)o.conv2, div2 = (R)o.div2;
     bool esc = false;
     auto near = [&](R e2) {
@@ -311,45 +373,15 @@ __device__ __forceinline__ SolveOut solve_one(const Planes<R>& P, const GridP& g
         int k = 0;
         for (; k < limit; ++k) {
             if (err2 > div2) break;  // divergence check at the top (:105)
-            // dx = −J~ g; x += dx (:106-107)
-            const R dx0 = -(Ji[0] * g0 + Ji[1] * g1 + Ji[2] * g2);
-            const R dx1 = -(Ji[3] * g0 + Ji[4] * g1 + Ji[5] * g2);
-            const R dx2 = -(Ji[6] * g0 + Ji[7] * g1 + Ji[8] * g2);
-            x0 += dx0;
-            x1 += dx1;
-            x2 += dx2;
-            // g' = d(x) − x'; dg = g' − g (:108-112)
-            const Cell<R> c = locate<false, R>(g, x0, x1, x2);
-            trilerp_T(P, g, c, T);
-            apply_T(T, x0, x1, x2, d);
-            const R n0 = d[0] - xp0, n1 = d[1] - xp1, n2 = d[2] - xp2;
-            const R dg0 = n0 - g0, dg1 = n1 - g1, dg2 = n2 - g2;
-            g0 = n0;
-            g1 = n1;
-            g2 = n2;
+            R den;
+            const bool c = broyden_step<R>(P, g, xp0, xp1, xp2, conv2, x0, x1, x2, Ji, g0, g1, g2, err2, den);
             iters = k + 1;
-            err2 = g0 * g0 + g1 * g1 + g2 * g2;
             if (kFast && near(err2)) esc = true;
-            if (err2 < conv2) {  // (:113-116)
+            if (c) {
                 conv = true;
                 break;
             }
-            // good Broyden: J~ += ((dx − J~dg)/(dx·J~dg)) (dxᵀJ~) if |den| > 1e-18 (:118-122)
-            const R j0 = Ji[0] * dg0 + Ji[1] * dg1 + Ji[2] * dg2;
-            const R j1 = Ji[3] * dg0 + Ji[4] * dg1 + Ji[5] * dg2;
-            const R j2 = Ji[6] * dg0 + Ji[7] * dg1 + Ji[8] * dg2;
-            const R den = dx0 * j0 + dx1 * j1 + dx2 * j2;
             if (kFast && fabs(den) < (R)o.esc_den) esc = true;
-            if (fabs(den) > (R)1e-18) {
-                const R inv = (R)1 / den;
-                const R q0 = (dx0 - j0) * inv, q1 = (dx1 - j1) * inv, q2 = (dx2 - j2) * inv;
-                const R w0 = dx0 * Ji[0] + dx1 * Ji[3] + dx2 * Ji[6];
-                const R w1 = dx0 * Ji[1] + dx1 * Ji[4] + dx2 * Ji[7];
-                const R w2 = dx0 * Ji[2] + dx1 * Ji[5] + dx2 * Ji[8];
-                Ji[0] = fma(q0, w0, Ji[0]); Ji[1] = fma(q0, w1, Ji[1]); Ji[2] = fma(q0, w2, Ji[2]);
-                Ji[3] = fma(q1, w0, Ji[3]); Ji[4] = fma(q1, w1, Ji[4]); Ji[5] = fma(q1, w2, Ji[5]);
-                Ji[6] = fma(q2, w0, Ji[6]); Ji[7] = fma(q2, w1, Ji[7]); Ji[8] = fma(q2, w2, Ji[8]);
-            }
         }
         // the float32 pass hit its iteration cap before max_iters: the f64 pass decides
         if (kFast && !conv && k == limit && limit < o.max_iters && !(err2 > div2)) esc = true;

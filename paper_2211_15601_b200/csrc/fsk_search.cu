@@ -125,7 +125,7 @@ __device__ __forceinline__ float ord2f(int i) { return __int_as_float(i >= 0 ? i
 
 __global__ void k_sort_init(int* __restrict__ hist, int* __restrict__ bbox, int* __restrict__ esc_count) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t == 0) *esc_count = 0;
+    if (t == 0) esc_count[0] = esc_count[1] = 0;
     for (int i = t; i < kSortBuckets; i += gridDim.x * blockDim.x) hist[i] = 0;
     if (t < 3) {
         bbox[t] = f2ord(INFINITY);
@@ -145,19 +145,31 @@ __global__ void __launch_bounds__(256) k_sort_bbox(const float* __restrict__ x, 
             }
         }
     }
+    // warp, then block reduction: 6 atomics per block (per-warp atomics on 6 addresses
+    // serialized in the L2 atomic unit)
+    __shared__ float s_lo[3][8], s_hi[3][8];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
         for (int o = 16; o > 0; o >>= 1) {
             lo[a] = fminf(lo[a], __shfl_xor_sync(0xffffffff, lo[a], o));
             hi[a] = fmaxf(hi[a], __shfl_xor_sync(0xffffffff, hi[a], o));
         }
-    }
-    if ((threadIdx.x & 31) == 0) {
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            atomicMin(bbox + a, f2ord(lo[a]));
-            atomicMax(bbox + 3 + a, f2ord(hi[a]));
+        if (lane == 0) {
+            s_lo[a][warp] = lo[a];
+            s_hi[a][warp] = hi[a];
         }
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        const int a = threadIdx.x;
+        float l = s_lo[a][0], h = s_hi[a][0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+            l = fminf(l, s_lo[a][w]);
+            h = fmaxf(h, s_hi[a][w]);
+        }
+        atomicMin(bbox + a, f2ord(l));
+        atomicMax(bbox + 3 + a, f2ord(h));
     }
 }
 
@@ -187,40 +199,56 @@ __global__ void __launch_bounds__(256) k_sort_hist(const float* __restrict__ x, 
     atomicAdd(hist + k, 1);
 }
 
-// Single-block exclusive scan of the 32768 bucket counts (1024 threads × 32).
+// Single-block exclusive scan of the 32768 bucket counts in 4 chunks of 8192 (1024 threads
+// × 8 contiguous), staged through shared memory so global loads and stores are coalesced.
 __global__ void __launch_bounds__(1024) k_sort_scan(int* __restrict__ hist) {
+    constexpr int kChunk = 8192, kPer = kChunk / 1024;
     __shared__ int warp_tot[32];
-    constexpr int kPer = kSortBuckets / 1024;
+    __shared__ int block_tot;
+    __shared__ int sh[kChunk + kChunk / 32];  // +1 pad per 32 words against bank conflicts
     const int t = threadIdx.x;
-    int v[kPer];
-    int s = 0;
+    auto pad = [](int i) { return i + (i >> 5); };
+    int carry = 0;
+    for (int c0 = 0; c0 < kSortBuckets; c0 += kChunk) {
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) {
-        v[i] = hist[t * kPer + i];
-        s += v[i];
-    }
-    int incl = s;
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffff, incl, o);
-        if ((t & 31) >= o) incl += y;
-    }
-    if ((t & 31) == 31) warp_tot[t >> 5] = incl;
-    __syncthreads();
-    if (t < 32) {
-        const int w = warp_tot[t];
-        int wi = w;
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffff, wi, o);
-            if (t >= o) wi += y;
+        for (int i = t; i < kChunk; i += 1024) sh[pad(i)] = hist[c0 + i];
+        __syncthreads();
+        int v[kPer];
+        int s = 0;
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+            v[i] = sh[pad(t * kPer + i)];
+            s += v[i];
         }
-        warp_tot[t] = wi - w;
-    }
-    __syncthreads();
-    int run = warp_tot[t >> 5] + incl - s;
+        int incl = s;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffff, incl, o);
+            if ((t & 31) >= o) incl += y;
+        }
+        if ((t & 31) == 31) warp_tot[t >> 5] = incl;
+        __syncthreads();
+        if (t < 32) {
+            const int w = warp_tot[t];
+            int wi = w;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffff, wi, o);
+                if (t >= o) wi += y;
+            }
+            warp_tot[t] = wi - w;
+            if (t == 31) block_tot = wi;
+        }
+        __syncthreads();
+        int run = carry + warp_tot[t >> 5] + incl - s;
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) {
-        hist[t * kPer + i] = run;
-        run += v[i];
+        for (int i = 0; i < kPer; ++i) {
+            sh[pad(t * kPer + i)] = run;
+            run += v[i];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = t; i < kChunk; i += 1024) hist[c0 + i] = sh[pad(i)];
+        carry += block_tot;
+        __syncthreads();
     }
 }
 
@@ -238,7 +266,7 @@ __global__ void __launch_bounds__(256) k_sort_scatter(const float* __restrict__ 
 __global__ void __launch_bounds__(256) k_identity_order(const float* __restrict__ x, int64_t n, int* __restrict__ perm,
                                                         float4* __restrict__ xs, int* __restrict__ esc_count) {
     const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (p == 0) *esc_count = 0;
+    if (p == 0) esc_count[0] = esc_count[1] = 0;
     if (p >= n) return;
     perm[p] = (int)p;
     xs[p] = make_float4(x[3 * p], x[3 * p + 1], x[3 * p + 2], 0.f);
@@ -321,17 +349,74 @@ __global__ void __launch_bounds__(128) k_search_escalated(Planes<double> P, Grid
                                                           SearchPlanes out, const int* __restrict__ esc_q,
                                                           const int* __restrict__ esc_count,
                                                           unsigned long long* __restrict__ stats) {
+    // Persistent lanes with refill: a lane whose solve finished takes the next queue entry
+    // (one warp-aggregated atomic per refill round), so long float64 trajectories do not hold
+    // a whole warp idle. Each solve runs exactly solve_one<double>'s arithmetic (solve_start +
+    // broyden_step), so results are identical to the one-thread-per-solve kernel.
     const int cnt = *esc_count;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
-        const int64_t q = esc_q[i];
-        const int bone = (int)(q / n);
-        const int64_t j = q - (int64_t)bone * n;
-        const float4 xq = __ldg(xs + j);
-        double x0, x1, x2, Ji[9], err2;
-        const SolveOut s =
-            solve_one<double, false>(P, g, bones + 12 * bone, xq.x, xq.y, xq.z, o, x0, x1, x2, Ji, err2);
-        store_solve(out, q, x0, x1, x2, Ji, err2, s);
-        count_work(stats ? stats + 3 : nullptr, s);
+    int* work = const_cast<int*>(esc_count) + 1;
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const double conv2 = o.conv2, div2 = o.div2;
+    bool active = false, started = false;
+    unsigned n_solves = 0, n_iters = 0, n_final = 0;
+    int64_t q = 0;
+    int k = 0;
+    float4 xq = make_float4(0.f, 0.f, 0.f, 0.f);
+    double x0 = 0, x1 = 0, x2 = 0, Ji[9], g0 = 0, g1 = 0, g2 = 0, err2 = 0;
+#pragma unroll
+    for (int e = 0; e < 9; ++e) Ji[e] = 0;
+    while (true) {
+        const unsigned need = __ballot_sync(full, !active);
+        if (need) {
+            int base = 0;
+            if (lane == __ffs(need) - 1) base = atomicAdd(work, __popc(need));
+            base = __shfl_sync(full, base, __ffs(need) - 1);
+            if (!active) {
+                const int idx = base + __popc(need & ((1u << lane) - 1));
+                if (idx < cnt) {
+                    q = esc_q[idx];
+                    active = true;
+                    started = false;
+                }
+            }
+        }
+        if (!__any_sync(full, active)) break;
+        if (active) {
+            const int bone = (int)(q / n);
+            bool done = false, conv = false;
+            if (!started) {
+                xq = __ldg(xs + (q - (int64_t)bone * n));
+                solve_start<double>(P, g, bones + 12 * bone, xq.x, xq.y, xq.z, x0, x1, x2, Ji, g0, g1, g2, err2);
+                started = true;
+                k = 0;
+                if (err2 < conv2) done = conv = true;              // (:100-103)
+                else if (err2 > div2 || o.max_iters < 1) done = true;  // top-of-loop divergence (:105)
+            } else {
+                double den;
+                conv = broyden_step<double>(P, g, xq.x, xq.y, xq.z, conv2, x0, x1, x2, Ji, g0, g1, g2, err2, den);
+                ++k;
+                if (conv || k >= o.max_iters || err2 > div2) done = true;
+            }
+            if (done) {
+                const SolveOut s{k, conv, false};
+                store_solve(out, q, x0, x1, x2, Ji, err2, s);
+                n_solves += 1;
+                n_iters += k;
+                n_final += (conv && k > 0);
+                active = false;
+            }
+        }
+    }
+    if (stats) {
+        n_solves = __reduce_add_sync(full, n_solves);
+        n_iters = __reduce_add_sync(full, n_iters);
+        n_final = __reduce_add_sync(full, n_final);
+        if (lane == 0 && n_solves) {
+            atomicAdd(stats + 3, (unsigned long long)n_solves);
+            atomicAdd(stats + 4, (unsigned long long)n_iters);
+            atomicAdd(stats + 5, (unsigned long long)n_final);
+        }
     }
 }
 
@@ -357,26 +442,61 @@ __global__ void __launch_bounds__(256) k_dedup(int64_t n, int nb, float dedup2, 
                                                const int* __restrict__ perm, int32_t* __restrict__ n_roots_p) {
     const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (j >= n) return;
+    // The first kRegKept kept roots stay in registers (a query has ~1 root); later kept roots
+    // are re-read from the planes. Loads are issued 8 bones at a time (independent).
+    constexpr int kRegKept = 4, kBatch = 8;
+    float kx[kRegKept], ky[kRegKept], kz[kRegKept];
+#pragma unroll
+    for (int c = 0; c < kRegKept; ++c) kx[c] = ky[c] = kz[c] = 0.f;
     int count = 0;
-    for (int b = 0; b < nb; ++b) {
-        const int64_t q = (int64_t)b * n + j;
-        int k = 0;
-        if (sp.meta[q] & 0x100) {
-            const float4 a = sp.xr[q];
-            k = 1;
-            for (int c = 0; c < b; ++c) {
-                const int64_t qc = (int64_t)c * n + j;
-                if (!sp.keep[qc]) continue;
-                const float4 e = sp.xr[qc];
-                const float e0 = a.x - e.x, e1 = a.y - e.y, e2 = a.z - e.z;
-                if (e0 * e0 + e1 * e1 + e2 * e2 < dedup2) {
-                    k = 0;
-                    break;
-                }
+    for (int b0 = 0; b0 < nb; b0 += kBatch) {
+        float4 xv[kBatch];
+        uint16_t mv[kBatch];
+#pragma unroll
+        for (int i = 0; i < kBatch; ++i) {
+            mv[i] = 0;
+            if (b0 + i < nb) {
+                const int64_t q = (int64_t)(b0 + i) * n + j;
+                mv[i] = sp.meta[q];
+                xv[i] = sp.xr[q];
             }
         }
-        sp.keep[q] = (uint8_t)k;
-        count += k;
+#pragma unroll
+        for (int i = 0; i < kBatch; ++i) {
+            const int b = b0 + i;
+            if (b >= nb) break;
+            int k = 0;
+            if (mv[i] & 0x100) {
+                k = 1;
+#pragma unroll
+                for (int c = 0; c < kRegKept; ++c) {
+                    const float e0 = xv[i].x - kx[c], e1 = xv[i].y - ky[c], e2 = xv[i].z - kz[c];
+                    if (c < count && e0 * e0 + e1 * e1 + e2 * e2 < dedup2) k = 0;
+                }
+                if (k && count > kRegKept) {  // rare: compare with the kept roots beyond the registers
+                    int seen = 0;
+                    for (int c = 0; c < b && k; ++c) {
+                        const int64_t qc = (int64_t)c * n + j;
+                        if (!sp.keep[qc]) continue;
+                        if (seen++ < kRegKept) continue;
+                        const float4 e = sp.xr[qc];
+                        const float e0 = xv[i].x - e.x, e1 = xv[i].y - e.y, e2 = xv[i].z - e.z;
+                        if (e0 * e0 + e1 * e1 + e2 * e2 < dedup2) k = 0;
+                    }
+                }
+                if (k) {
+#pragma unroll
+                    for (int c = 0; c < kRegKept; ++c)
+                        if (c == count) {
+                            kx[c] = xv[i].x;
+                            ky[c] = xv[i].y;
+                            kz[c] = xv[i].z;
+                        }
+                }
+            }
+            sp.keep[(int64_t)b * n + j] = (uint8_t)k;
+            count += k;
+        }
     }
     n_roots_p[perm[j]] = count;
 }
@@ -643,7 +763,7 @@ SearchState run_search(fsk_ctx* ctx, const GridPlanes& P, const GridP& g, const 
     s.n_roots_p = (int32_t*)scratch(ctx, kNRoots, std::max<int64_t>(1, n) * sizeof(int32_t));
     if (n == 0) return s;
     float4* xs = (float4*)scratch(ctx, kXs, n * sizeof(float4));
-    int* esc_n = (int*)scratch(ctx, kEscN, sizeof(int));
+    int* esc_n = (int*)scratch(ctx, kEscN, 2 * sizeof(int));
     if (!(flags & FSK_SEARCH_NO_SORT)) {
         int* hist = (int*)scratch(ctx, kHist, kSortBuckets * sizeof(int));
         int* bbox = (int*)scratch(ctx, kBbox, 6 * sizeof(int));
@@ -674,8 +794,11 @@ SearchState run_search(fsk_ctx* ctx, const GridPlanes& P, const GridP& g, const 
         }
         FSK_LAUNCH(ctx, st, k_search_fast, (unsigned)nblocks, kSearchBlock, 0, P.p32, g, bones, xs, n, bpb, spf, s.sp,
                    esc_q, esc_n, ctx->stats);
+        int per_sm = 0;  // persistent kernel: exactly the resident capacity
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search_escalated, 128, 0), "occupancy");
         if (esc)
-            FSK_LAUNCH(ctx, st, k_search_escalated, (unsigned)ctx->sm_count * 8, 128, 0, P.p64, g, bones, xs, n, sp, s.sp,
+            FSK_LAUNCH(ctx, st, k_search_escalated, (unsigned)(ctx->sm_count * std::max(per_sm, 1)), 128, 0, P.p64, g,
+                       bones, xs, n, sp, s.sp,
                        esc_q, esc_n, ctx->stats);
     }
     FSK_LAUNCH(ctx, st, k_dedup, blocks_for(n, 256), 256, 0, n, g.nb, (float)sp.dedup2, s.sp, s.perm, s.n_roots_p);
