@@ -201,6 +201,7 @@ def run_ours(args, rank, world, local_rank):
         D.deform(w, sc.dims, sc.bbox, B, x, opts, tgrid=tg, out=roots_buf)
 
     peak_fp32 = D.measure_fp32_peak()
+    peak_fp64 = D.measure_fp64_peak()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -289,7 +290,8 @@ def run_ours(args, rank, world, local_rank):
                      "fp32_pass": {"solves": s32, "iterations": it32},
                      "fp64_escalation": {"solves": s64, "frac_of_solves": s64 / solves, "iterations": it64,
                                          "flops": flops64, "avg_launch_ms": k2e_ms / max(k2e_n, 1),
-                                         "achieved_TFLOPs_f64": flops64 / max(k2e_ms / max(k2e_n, 1), 1e-9) / 1e9},
+                                         "achieved_TFLOPs_f64": flops64 / max(k2e_ms / max(k2e_n, 1), 1e-9) / 1e9,
+                                         "peak_TFLOPs_f64_measured": peak_fp64},
                      "mean_final_iters_per_solve": mean_iters, "converged_frac": conv_frac,
                      "kept_roots_per_query": total_roots / n,
                      "gather": {"requested_bytes_per_launch": gather,

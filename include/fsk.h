@@ -103,6 +103,7 @@ int fsk_device_sm_count(const fsk_ctx* ctx);
 int fsk_ctx_set_profiling(fsk_ctx* ctx, int on);
 int fsk_ctx_prof_read(fsk_ctx* ctx, const char* name, double* total_ms, int64_t* count, int reset);
 int fsk_measure_fp32_peak(fsk_ctx* ctx, double* tflops);
+int fsk_measure_fp64_peak(fsk_ctx* ctx, double* tflops);  /* same with DFMA chains */
 /* Search work counters accumulated by the context's searches (synchronizes the device):
  * out = {float32 solves, float32 Broyden iterations, float32 converged-terminating
  * iterations, float64 solves, float64 iterations, float64 converged-terminating iterations}. */

@@ -119,19 +119,39 @@ SearchP make_search(const fsk_search_opts* o) {
     return s;
 }
 
-// FFMA throughput microbenchmark: 8 independent dependency chains per thread over all SMs.
-__global__ void __launch_bounds__(256) k_peak_fp32(float* out, int iters, float a, float b) {
-    float x[8];
+// FMA throughput microbenchmark: 8 independent dependency chains per thread over all SMs.
+template <typename R>
+__global__ void __launch_bounds__(256) k_peak_fma(R* out, int iters, R a, R b) {
+    R x[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) x[i] = threadIdx.x * 1e-3f + i;
+    for (int i = 0; i < 8; ++i) x[i] = threadIdx.x * (R)1e-3 + i;
     for (int k = 0; k < iters; ++k) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) x[i] = fmaf(x[i], a, b);
+        for (int i = 0; i < 8; ++i) x[i] = fma(x[i], a, b);
     }
-    float s = 0.f;
+    R s = 0;
 #pragma unroll
     for (int i = 0; i < 8; ++i) s += x[i];
-    if (s == 12345.678f) out[0] = s;  // keep the chains alive
+    if (s == (R)12345.678) out[0] = s;  // keep the chains alive
+}
+
+template <typename R>
+double measure_peak(fsk_ctx* ctx, int iters) {
+    R* o = (R*)scratch(ctx, kBwdMax, 16);
+    const int blocks = ctx->sm_count * 8;
+    cudaEvent_t a, b;
+    cuda_check(cudaEventCreate(&a), "cudaEventCreate");
+    cuda_check(cudaEventCreate(&b), "cudaEventCreate");
+    k_peak_fma<R><<<blocks, 256>>>(o, 256, (R)0.999, (R)1e-3);  // warm-up
+    cuda_check(cudaEventRecord(a, 0), "cudaEventRecord");
+    k_peak_fma<R><<<blocks, 256>>>(o, iters, (R)0.999, (R)1e-3);
+    cuda_check(cudaEventRecord(b, 0), "cudaEventRecord");
+    cuda_check(cudaEventSynchronize(b), "cudaEventSynchronize");
+    float ms = 0.f;
+    cuda_check(cudaEventElapsedTime(&ms, a, b), "cudaEventElapsedTime");
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return 2.0 * 8.0 * iters * (double)blocks * 256.0 / (ms * 1e-3) / 1e12;
 }
 
 }  // namespace fsk
@@ -237,21 +257,15 @@ int fsk_measure_fp32_peak(fsk_ctx* ctx, double* tflops) {
     return guard([&] {
         set_device(ctx);
         if (!tflops) fail(FSK_EINVAL, "fsk: null output pointer");
-        float* o = (float*)scratch(ctx, kBwdMax, 16);
-        const int blocks = ctx->sm_count * 8, iters = 1 << 14;
-        cudaEvent_t a, b;
-        cuda_check(cudaEventCreate(&a), "cudaEventCreate");
-        cuda_check(cudaEventCreate(&b), "cudaEventCreate");
-        k_peak_fp32<<<blocks, 256>>>(o, 256, 0.999f, 1e-3f);  // warm-up
-        cuda_check(cudaEventRecord(a, 0), "cudaEventRecord");
-        k_peak_fp32<<<blocks, 256>>>(o, iters, 0.999f, 1e-3f);
-        cuda_check(cudaEventRecord(b, 0), "cudaEventRecord");
-        cuda_check(cudaEventSynchronize(b), "cudaEventSynchronize");
-        float ms = 0.f;
-        cuda_check(cudaEventElapsedTime(&ms, a, b), "cudaEventElapsedTime");
-        cudaEventDestroy(a);
-        cudaEventDestroy(b);
-        *tflops = 2.0 * 8.0 * iters * (double)blocks * 256.0 / (ms * 1e-3) / 1e12;
+        *tflops = measure_peak<float>(ctx, 1 << 14);
+    });
+}
+
+int fsk_measure_fp64_peak(fsk_ctx* ctx, double* tflops) {
+    return guard([&] {
+        set_device(ctx);
+        if (!tflops) fail(FSK_EINVAL, "fsk: null output pointer");
+        *tflops = measure_peak<double>(ctx, 1 << 12);
     });
 }
 

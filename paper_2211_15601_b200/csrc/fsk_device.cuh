@@ -174,7 +174,8 @@ __device__ __forceinline__ void grad_term(R G[9], R y0, R y1, R y2, R gx, R gy, 
 // from one gather unless x lies exactly on an interior face (then the lower cell is
 // gathered again).
 template <typename R>
-__device__ __forceinline__ void jacobian_and_T(const Planes<R>& P, const GridP& g, R x, R y, R z, R T[12], R J[9]) {
+__device__ __forceinline__ void jacobian_and_T(const Planes<R>& P, const GridP& g, R x, R y, R z, R T[12], R J[9],
+                                               bool grad = true) {
     const Cell<R> c = locate<false, R>(g, x, y, z);
     const Cell<R> cl = locate<true, R>(g, x, y, z);
     const int nxy = g.nx * g.ny;
@@ -206,13 +207,13 @@ __device__ __forceinline__ void jacobian_and_T(const Planes<R>& P, const GridP& 
                 y0[r] = row_dot(a, x, y, z);
                 y1[r] = row_dot(b, x, y, z);
             }
-            if (same) {
+            if (grad && same) {
                 grad_term(G, y0[0], y0[1], y0[2], -sx * fy * fz, fx0 * gy_s * fz, fx0 * fy * gz_s);
                 grad_term(G, y1[0], y1[1], y1[2], sx * fy * fz, fx1 * gy_s * fz, fx1 * fy * gz_s);
             }
         }
     }
-    if (!same) {  // x on an interior cell face: gradient from the lower-index cell
+    if (grad && !same) {  // x on an interior cell face: gradient from the lower-index cell
 #pragma unroll 1
         for (int q = 0; q < 4; ++q) {
             const int dj = q & 1, dk = q >> 1;

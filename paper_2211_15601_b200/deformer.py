@@ -142,6 +142,11 @@ class Deformer:
         check(self.L.fsk_measure_fp32_peak(self._ctx, ctypes.byref(t)))
         return t.value
 
+    def measure_fp64_peak(self) -> float:
+        t = ctypes.c_double()
+        check(self.L.fsk_measure_fp64_peak(self._ctx, ctypes.byref(t)))
+        return t.value
+
     # ---------------------------------------------------------------- K1
     def precompute_transform_grid(self, weights, dims, bbox, bones, out=None, out64=None):
         """``precompute_transform_grid`` (deformer.hpp:53-55) → tgrid [V,12] float32 (and the
