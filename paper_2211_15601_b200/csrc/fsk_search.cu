@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(kSearchBlock, FSK_SEARCH_MINB)
 // Escalation pass: the flagged solves from scratch in float64 (persistent grid-stride over
 // the device-side queue), overwriting their float32 results.
 #ifndef FSK_ESC_MINB
-#define FSK_ESC_MINB 1
+#define FSK_ESC_MINB 3  // caps registers at 168 (12 warps/SM); without it ptxas takes 254
 #endif
 __global__ void __launch_bounds__(128, FSK_ESC_MINB) k_search_escalated(Planes<double> P, GridP g, const float* __restrict__ bones,
                                                           const float4* __restrict__ xs, int64_t n, SearchP o,
@@ -369,22 +369,34 @@ __global__ void __launch_bounds__(128, FSK_ESC_MINB) k_search_escalated(Planes<d
     double x0 = 0, x1 = 0, x2 = 0, Ji[9], g0 = 0, g1 = 0, g2 = 0, err2 = 0;
 #pragma unroll
     for (int e = 0; e < 9; ++e) Ji[e] = 0;
+    // Warp-local buffer of 32 queue slots (lane i holds slot base+i): one atomic per 32 solves.
+    int buf_idx = 0, bused = 32;
+    bool dry = false;
     while (true) {
+        // one refill round per trip; lanes left idle by a short buffer wait one trip
         const unsigned need = __ballot_sync(full, !active);
-        if (need) {
-            int base = 0;
-            if (lane == __ffs(need) - 1) base = atomicAdd(work, __popc(need));
-            base = __shfl_sync(full, base, __ffs(need) - 1);
-            if (!active) {
-                const int idx = base + __popc(need & ((1u << lane) - 1));
-                if (idx < cnt) {
-                    q = esc_q[idx];
-                    active = true;
-                    started = false;
-                }
+        if (need && !dry) {
+            if (bused == 32) {
+                int base = 0;
+                if (lane == 0) base = atomicAdd(work, 32);
+                base = __shfl_sync(full, base, 0);
+                buf_idx = base + lane;
+                bused = 0;
+                dry = base >= cnt;
             }
+            const int rank = __popc(need & ((1u << lane) - 1));
+            const bool take = !dry && ((need >> lane) & 1u) && rank < 32 - bused;
+            const int idx = __shfl_sync(full, buf_idx, min(bused + rank, 31));
+            const bool got = take && idx < cnt;
+            if (got) {
+                q = esc_q[idx];
+                active = true;
+                started = false;
+            }
+            bused += __popc(__ballot_sync(full, take));
+            if (__any_sync(full, take && !got)) dry = true;  // queue exhausted
         }
-        if (!__any_sync(full, active)) break;
+        if (!__any_sync(full, active) && dry) break;
         // One trip = one gather for every active lane, whether it starts a solve (x0, with
         // the Jacobian stencil) or continues one (x + dx): init and iteration lanes of a warp
         // share the loads instead of running two divergent gather paths.
