@@ -50,6 +50,11 @@ def parse():
     ap.add_argument("--no-sort", action="store_true", help="ablation: no spatial ordering")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--poses", type=int, default=1, help="poses per step (C4: 16 poses x 1M points, 64^3 grid)")
+    ap.add_argument("--backward", action="store_true", help="C3: add the implicit-diff backward to each frame")
+    ap.add_argument("--deterministic", action="store_true", help="backward with int64 fixed-point accumulation")
+    ap.add_argument("--precision", default="mixed", choices=["mixed", "fp32", "fp64"])
+    ap.add_argument("--no-graph", dest="graph", action="store_false", help="launch eagerly instead of a CUDA graph")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-baseline sample duration")
     return ap.parse_args()
 
@@ -66,8 +71,13 @@ def scene_for_rank(args, rank):
 
 
 def workload_name(args):
-    return (f"C2: {args.points // 1000}k posed points x 24 bone inits per GPU, {args.grid.replace(',', 'x')} grid, "
-            f"max_iters {args.max_iters}; step = precompute + sort + search + dedup")
+    name = "C3" if args.backward else ("C4" if args.poses > 1 else "C2")
+    s = (f"{name}: {args.poses} pose(s) x {args.points // 1000}k posed points x 24 bone inits per GPU, "
+         f"{args.grid.replace(',', 'x')} grid, max_iters {args.max_iters}; step = per pose: precompute + sort + "
+         f"search (fp32 pass + fp64 escalation) + dedup + compaction to CorrespondenceSets")
+    if args.backward:
+        s += " + implicit-diff backward (dL/dT scatter + dL/dw)"
+    return s
 
 
 # ------------------------------------------------------------------------------ clocks
@@ -187,24 +197,66 @@ def run_ours(args, rank, world, local_rank):
     sc = scene_for_rank(args, rank)
     nb, n = sc.n_bones, sc.points.shape[0]
     w = torch.from_numpy(sc.weights).to(dev)
-    B = torch.from_numpy(sc.bones).to(dev)
-    x = torch.from_numpy(sc.points).to(dev)
+    # frames: one pose (C2/C3) or `--poses` poses (C4), each with its own posed points
+    frames = [(torch.from_numpy(sc.bones).to(dev), torch.from_numpy(sc.points).to(dev))]
+    skel = S.smpl_like_skeleton()
+    for fi in range(1, args.poses):
+        rng = np.random.default_rng(args.seed * 7919 + 104729 * rank + fi)
+        ang = rng.uniform(-0.5, 0.5, nb)
+        bones = S.forward_kinematics(skel, ang)
+        lo, hi = S.posed_sampling_box(skel, bones, 0.1)
+        frames.append((torch.from_numpy(bones.reshape(nb, 12).astype(np.float32)).to(dev),
+                       torch.from_numpy(S.uniform_points(lo, hi, n, rng).astype(np.float32)).to(dev)))
+    B, x = frames[0]
     tg = torch.empty((w.shape[0], 12), dtype=torch.float32, device=dev)
     opts = SearchOptions(args.max_iters, **{k: v for k, v in sc.search_options(args.max_iters).items()
                                            if k != "max_iters"})
     opts.sort = not args.no_sort
+    opts.precision = args.precision
     roots_buf = D.alloc_roots(n, nb)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+    if args.backward:  # C3: cotangent dL/dx* ~ N(0,1)/N per query (loss mean, diff.cpp:331)
+        gx = torch.randn((n, 3), generator=torch.Generator(device=dev).manual_seed(rank + 1), device=dev) / n
+        gT = torch.empty((w.shape[0], 12), dtype=torch.float32, device=dev)
+        gW = torch.empty_like(w)
 
     def step():
-        # one frame: precompute_transform_grid + batch_search → CorrespondenceSets on device
-        D.deform(w, sc.dims, sc.bbox, B, x, opts, tgrid=tg, out=roots_buf)
+        for Bf, xf in frames:
+            # one frame: precompute_transform_grid + batch_search → CorrespondenceSets on device
+            offs, roots = D.deform(w, sc.dims, sc.bbox, Bf, xf, opts, tgrid=tg, out=roots_buf)
+            if args.backward:
+                # the training step's root choice (occupancy argmax, diff.cpp:292) is out of scope:
+                # take each query's first kept root; then the implicit-diff backward (K3) and dL/dw
+                ridx = torch.where(offs[1:] > offs[:-1], offs[:-1], torch.full_like(offs[:-1], -1))
+                D.search_bwd_roots(sc.dims, sc.bbox, nb, roots, ridx, gx, deterministic=args.deterministic, out=gT)
+                D.grad_weights(sc.dims, sc.bbox, gT, Bf, out=gW)
 
     peak_fp32 = D.measure_fp32_peak()
     peak_fp64 = D.measure_fp64_peak()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+
+    # CUDA graph of one step (all scratch is sized by the warm-up, the C-ABI calls are fully
+    # asynchronous): replays remove the host launch path and the inter-kernel gaps
+    launches_per_step = None
+    run_step = step
+    if args.graph:
+        l0 = D.launch_count
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            step()
+        torch.cuda.current_stream(dev).wait_stream(side)
+        torch.cuda.synchronize()
+        launches_per_step = D.launch_count - l0
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        torch.cuda.synchronize()
+        graph.replay()
+        torch.cuda.synchronize()
+        run_step = graph.replay
 
     stream = torch.cuda.current_stream(dev)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -218,13 +270,15 @@ def run_ours(args, rank, world, local_rank):
     for i in range(args.steps):
         flush.fill_(float(i))  # L2 flush between steps, outside the per-step events
         evs[i][0].record(stream)
-        step()
+        run_step()
         evs[i][1].record(stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
     launches = D.launch_count - launches0
+    if args.graph:  # graph replays do not pass through the host launch counter
+        launches = launches_per_step * args.steps
     step_ms = [a.elapsed_time(b) for a, b in evs]
     total_ms = float(np.sum(step_ms))
     st = D.search_stats(reset=True)
@@ -255,9 +309,9 @@ def run_ours(args, rank, world, local_rank):
 
     # algorithmic work per step, counted by the kernels themselves (identical every step):
     # float32 pass (k_search_fast) and float64 escalation pass (k_search_escalated)
-    per = max(args.steps, 1)
+    per = max(args.steps, 1) * args.poses  # counters per search launch (one launch per pose)
     s32, it32, fin32, s64, it64, fin64 = (v / per for v in st)
-    solves = n * nb
+    solves = n * nb * args.poses
     flops = s32 * FLOPS_INIT + it32 * FLOPS_ITER - fin32 * FLOPS_FINAL_SAVING
     flops64 = s64 * FLOPS_INIT + it64 * FLOPS_ITER - fin64 * FLOPS_FINAL_SAVING
     gather = (s32 + it32) * GATHER_BYTES
@@ -279,7 +333,8 @@ def run_ours(args, rank, world, local_rank):
         "data": "synthetic: SMPL-like 24-bone skeleton, random pose U(-0.5,0.5) rad, analytic capsule weight grid, "
                 "uniform posed points (seeded; same inputs the oracle parity tests use)",
         "config": {"workload": workload_name(args), "points_per_gpu": n, "n_init": nb, "grid": list(sc.dims),
-                   "max_iters": args.max_iters, "sort": not args.no_sort,
+                   "max_iters": args.max_iters, "sort": not args.no_sort, "poses": args.poses,
+                   "precision": args.precision, "cuda_graph": bool(args.graph),
                    "l2": "flushed between steps (256 MiB fill outside the per-step CUDA events)",
                    "parallelism": f"points sharded across {world} GPU(s), no data-path collective"},
         "roofline": {"bound": "fp32", "kernel": "k_search_fast", "achieved": achieved, "peak": peak_fp32,
@@ -288,7 +343,7 @@ def run_ours(args, rank, world, local_rank):
                                     "MEASURED_PEAKS.json has no FP32 figure",
                      "algorithmic_flops_per_launch": flops, "avg_launch_ms": k2_avg,
                      "fp32_pass": {"solves": s32, "iterations": it32},
-                     "fp64_escalation": {"solves": s64, "frac_of_solves": s64 / solves, "iterations": it64,
+                     "fp64_escalation": {"solves": s64, "frac_of_solves": s64 / (n * nb), "iterations": it64,
                                          "flops": flops64, "avg_launch_ms": k2e_ms / max(k2e_n, 1),
                                          "achieved_TFLOPs_f64": flops64 / max(k2e_ms / max(k2e_n, 1), 1e-9) / 1e9,
                                          "peak_TFLOPs_f64_measured": peak_fp64},

@@ -370,12 +370,16 @@ __global__ void __launch_bounds__(128, FSK_ESC_MINB) k_search_escalated(Planes<d
 #pragma unroll
     for (int e = 0; e < 9; ++e) Ji[e] = 0;
     // Warp-local buffer of 32 queue slots (lane i holds slot base+i): one atomic per 32 solves.
+    // Idle lanes are refilled in batches (>= kRefillIdle idle, or the whole warp), so the
+    // divergent init path (x0, Jacobian stencil, inverse) runs for many lanes at once and the
+    // iteration trips — the bulk of the work — run with most lanes active.
+    constexpr int kRefillIdle = 12;
     int buf_idx = 0, bused = 32;
     bool dry = false;
+    (void)started;
     while (true) {
-        // one refill round per trip; lanes left idle by a short buffer wait one trip
-        const unsigned need = __ballot_sync(full, !active);
-        if (need && !dry) {
+        const unsigned idle = __ballot_sync(full, !active);
+        if (!dry && (__popc(idle) >= kRefillIdle || idle == full)) {
             if (bused == 32) {
                 int base = 0;
                 if (lane == 0) base = atomicAdd(work, 32);
@@ -384,94 +388,37 @@ __global__ void __launch_bounds__(128, FSK_ESC_MINB) k_search_escalated(Planes<d
                 bused = 0;
                 dry = base >= cnt;
             }
-            const int rank = __popc(need & ((1u << lane) - 1));
-            const bool take = !dry && ((need >> lane) & 1u) && rank < 32 - bused;
+            const int rank = __popc(idle & ((1u << lane) - 1));
+            const bool take = !dry && ((idle >> lane) & 1u) && rank < 32 - bused;
             const int idx = __shfl_sync(full, buf_idx, min(bused + rank, 31));
             const bool got = take && idx < cnt;
-            if (got) {
-                q = esc_q[idx];
-                active = true;
-                started = false;
-            }
             bused += __popc(__ballot_sync(full, take));
             if (__any_sync(full, take && !got)) dry = true;  // queue exhausted
-        }
-        if (!__any_sync(full, active) && dry) break;
-        // One trip = one gather for every active lane, whether it starts a solve (x0, with
-        // the Jacobian stencil) or continues one (x + dx): init and iteration lanes of a warp
-        // share the loads instead of running two divergent gather paths.
-        double dx0 = 0, dx1 = 0, dx2 = 0, T[12], Jm[9];
-        const bool init = active && !started;
-        if (active) {
-            const int bone = (int)(q / n);
-            if (init) {
+            if (got) {  // start of the solve (correspondence.cpp:135-137, :43-54)
+                q = esc_q[idx];
+                const int bone = (int)(q / n);
                 xq = __ldg(xs + (q - (int64_t)bone * n));
-                const float* B = bones + 12 * bone;  // x0 = Rᵀx' + (−Rᵀt) (geometry.hpp:58-61)
-                const double r00 = __ldg(B + 0), r01 = __ldg(B + 1), r02 = __ldg(B + 2), t0 = __ldg(B + 3);
-                const double r10 = __ldg(B + 4), r11 = __ldg(B + 5), r12 = __ldg(B + 6), t1 = __ldg(B + 7);
-                const double r20 = __ldg(B + 8), r21 = __ldg(B + 9), r22 = __ldg(B + 10), t2 = __ldg(B + 11);
-                const double it0 = -(r00 * t0 + r10 * t1 + r20 * t2);
-                const double it1 = -(r01 * t0 + r11 * t1 + r21 * t2);
-                const double it2 = -(r02 * t0 + r12 * t1 + r22 * t2);
-                const double xp0 = xq.x, xp1 = xq.y, xp2 = xq.z;
-                x0 = r00 * xp0 + r10 * xp1 + r20 * xp2 + it0;
-                x1 = r01 * xp0 + r11 * xp1 + r21 * xp2 + it1;
-                x2 = r02 * xp0 + r12 * xp1 + r22 * xp2 + it2;
-            } else {  // dx = −J~ g; x += dx (:106-107)
-                dx0 = -(Ji[0] * g0 + Ji[1] * g1 + Ji[2] * g2);
-                dx1 = -(Ji[3] * g0 + Ji[4] * g1 + Ji[5] * g2);
-                dx2 = -(Ji[6] * g0 + Ji[7] * g1 + Ji[8] * g2);
-                x0 += dx0;
-                x1 += dx1;
-                x2 += dx2;
-            }
-            jacobian_and_T<double>(P, g, x0, x1, x2, T, Jm, init);
-        }
-        if (active) {
-            bool done = false, conv = false;
-            double d[3];
-            apply_T(T, x0, x1, x2, d);
-            const double n0 = d[0] - xq.x, n1 = d[1] - xq.y, n2 = d[2] - xq.z;
-            if (init) {  // J~0 and g0 (correspondence.cpp:43-54, :137)
-                inverse_or_identity<double>(Jm, Ji);
-                g0 = n0;
-                g1 = n1;
-                g2 = n2;
-                err2 = g0 * g0 + g1 * g1 + g2 * g2;
-                started = true;
+                solve_start<double>(P, g, bones + 12 * bone, xq.x, xq.y, xq.z, x0, x1, x2, Ji, g0, g1, g2, err2);
                 k = 0;
-                if (err2 < conv2) done = conv = true;  // (:100-103)
-                else if (err2 > div2) done = true;     // divergence check at the top (:105)
-            } else {  // g' = d(x) − x'; dg (:108-112), converge (:113-116), Broyden update (:118-122)
-                const double dg0 = n0 - g0, dg1 = n1 - g1, dg2 = n2 - g2;
-                g0 = n0;
-                g1 = n1;
-                g2 = n2;
-                err2 = g0 * g0 + g1 * g1 + g2 * g2;
-                ++k;
-                if (err2 < conv2) {
-                    conv = true;
-                } else {
-                    const double j0 = Ji[0] * dg0 + Ji[1] * dg1 + Ji[2] * dg2;
-                    const double j1 = Ji[3] * dg0 + Ji[4] * dg1 + Ji[5] * dg2;
-                    const double j2 = Ji[6] * dg0 + Ji[7] * dg1 + Ji[8] * dg2;
-                    const double den = dx0 * j0 + dx1 * j1 + dx2 * j2;
-                    if (fabs(den) > 1e-18) {
-                        const double inv = 1.0 / den;
-                        const double q0 = (dx0 - j0) * inv, q1 = (dx1 - j1) * inv, q2 = (dx2 - j2) * inv;
-                        const double w0 = dx0 * Ji[0] + dx1 * Ji[3] + dx2 * Ji[6];
-                        const double w1 = dx0 * Ji[1] + dx1 * Ji[4] + dx2 * Ji[7];
-                        const double w2 = dx0 * Ji[2] + dx1 * Ji[5] + dx2 * Ji[8];
-                        Ji[0] = fma(q0, w0, Ji[0]); Ji[1] = fma(q0, w1, Ji[1]); Ji[2] = fma(q0, w2, Ji[2]);
-                        Ji[3] = fma(q1, w0, Ji[3]); Ji[4] = fma(q1, w1, Ji[4]); Ji[5] = fma(q1, w2, Ji[5]);
-                        Ji[6] = fma(q2, w0, Ji[6]); Ji[7] = fma(q2, w1, Ji[7]); Ji[8] = fma(q2, w2, Ji[8]);
-                    }
+                active = true;
+                const bool conv = err2 < conv2;  // (:100-103)
+                if (conv || err2 > div2) {       // divergence check at the top (:105)
+                    store_solve(out, q, x0, x1, x2, Ji, err2, SolveOut{0, conv, false});
+                    n_solves += 1;
+                    active = false;
                 }
-                if (conv || k >= o.max_iters || err2 > div2) done = true;
             }
-            if (done) {
-                const SolveOut s{k, conv, false};
-                store_solve(out, q, x0, x1, x2, Ji, err2, s);
+        }
+        if (!__any_sync(full, active)) {
+            if (dry) break;
+            continue;
+        }
+        if (active) {  // one Broyden iteration (:106-122)
+            double den;
+            const bool conv = broyden_step<double>(P, g, xq.x, xq.y, xq.z, conv2, x0, x1, x2, Ji, g0, g1, g2, err2, den);
+            ++k;
+            if (conv || k >= o.max_iters || err2 > div2) {
+                store_solve(out, q, x0, x1, x2, Ji, err2, SolveOut{k, conv, false});
                 n_solves += 1;
                 n_iters += k;
                 n_final += (conv && k > 0);
