@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(kSearchBlock, FSK_SEARCH_MINB)
 // Escalation pass: the flagged solves from scratch in float64 (persistent grid-stride over
 // the device-side queue), overwriting their float32 results.
 #ifndef FSK_ESC_MINB
-#define FSK_ESC_MINB 3  // caps registers at 168 (12 warps/SM); without it ptxas takes 254
+#define FSK_ESC_MINB 2  // measured: 254 regs / 8 warps per SM beats 168 regs / 12 warps (0.263 vs 0.277 ms)
 #endif
 __global__ void __launch_bounds__(128, FSK_ESC_MINB) k_search_escalated(Planes<double> P, GridP g, const float* __restrict__ bones,
                                                           const float4* __restrict__ xs, int64_t n, SearchP o,
