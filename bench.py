@@ -35,13 +35,19 @@ UNIT = "solves/s"
 # terminating (converged) iteration that skips the rank-one update.
 FLOPS_INIT, FLOPS_ITER, FLOPS_FINAL_SAVING = 674, 332, 66
 GATHER_BYTES = 384  # 8 corners x 48 B of transform grid per d(x) evaluation
+# dram__bytes_read.sum + dram__bytes_write.sum of one k_search_fast launch (C2), from the
+# ncu --set full capture profiles/r01_search_kernels.ncu-rep (6.9 MB read + 204.1 MB written:
+# the bone-major search planes; the gather itself is L1/L2-resident)
+NCU_TRAFFIC_K2 = 211.0e6
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    # ~1 ms steps: 300 timed steps keep the nvidia-smi clock sampler (100 ms period) inside
+    # the timed region for several samples
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--points", type=int, default=200_000, help="posed points per GPU")
     ap.add_argument("--grid", default="32,32,32")
@@ -338,7 +344,9 @@ def run_ours(args, rank, world, local_rank):
                    "l2": "flushed between steps (256 MiB fill outside the per-step CUDA events)",
                    "parallelism": f"points sharded across {world} GPU(s), no data-path collective"},
         "roofline": {"bound": "fp32", "kernel": "k_search_fast", "achieved": achieved, "peak": peak_fp32,
-                     "unit": "TFLOP/s", "frac": achieved / peak_fp32, "traffic": None,
+                     "unit": "TFLOP/s", "frac": achieved / peak_fp32,
+                     "traffic": NCU_TRAFFIC_K2 if (args.grid == "32,32,32" and args.points == 200_000) else None,
+                     "traffic_source": "ncu --set full, profiles/r01_search_kernels.ncu-rep (C2 only)",
                      "peak_source": "measured live: FFMA-chain kernel over all SMs (fsk_measure_fp32_peak); "
                                     "MEASURED_PEAKS.json has no FP32 figure",
                      "algorithmic_flops_per_launch": flops, "avg_launch_ms": k2_avg,
