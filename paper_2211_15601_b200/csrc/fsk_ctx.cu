@@ -200,6 +200,8 @@ int fsk_ctx_destroy(fsk_ctx* ctx) {
         }
         for (auto& e : ctx->pool) cudaEventDestroy(e);
         if (ctx->stats) cudaFree(ctx->stats);
+        if (ctx->copy) cudaStreamDestroy(ctx->copy);
+        if (ctx->hcount) cudaFreeHost(ctx->hcount);
         delete ctx;
     });
 }

@@ -34,6 +34,9 @@ struct fsk_ctx {
     std::vector<cudaEvent_t> pool;
     // search work counters [solves32, iters32, final32, solves64, iters64, final64]
     unsigned long long* stats = nullptr;
+    // device→host copy stream of the host-buffer entry point (created on first use)
+    cudaStream_t copy = nullptr;
+    int64_t* hcount = nullptr;  // pinned per-chunk root counts
 };
 
 namespace fsk {

@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(128, FSK_ESC_MINB) k_search_escalated(Planes<d
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const double conv2 = o.conv2, div2 = o.div2;
-    bool active = false, started = false;
+    bool active = false;
     unsigned n_solves = 0, n_iters = 0, n_final = 0;
     int64_t q = 0;
     int k = 0;
@@ -376,7 +376,6 @@ __global__ void __launch_bounds__(128, FSK_ESC_MINB) k_search_escalated(Planes<d
     constexpr int kRefillIdle = 12;
     int buf_idx = 0, bused = 32;
     bool dry = false;
-    (void)started;
     while (true) {
         const unsigned idle = __ballot_sync(full, !active);
         if (!dry && (__popc(idle) >= kRefillIdle || idle == full)) {
@@ -958,30 +957,70 @@ int fsk_deform_host(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* des
         cudaStream_t st = (cudaStream_t)stream;
         const int64_t V = vertex_count(g);
         const int nb = g.nb;
+        // Pipelined over point chunks: the searches run back to back on `st` while the
+        // CorrespondenceSets of finished chunks stream to the host on the copy stream.
+        const int64_t nchunks = std::max<int64_t>(1, std::min<int64_t>(4, n / 32768));
+        const int64_t csz = (n + nchunks - 1) / nchunks;
         float* dW = (float*)scratch(ctx, kHW, V * nb * sizeof(float));
         float* dB = (float*)scratch(ctx, kHB, nb * 12 * sizeof(float));
         float* dP = (float*)scratch(ctx, kHP, std::max<int64_t>(1, n) * 3 * sizeof(float));
-        int64_t* dOff = (int64_t*)scratch(ctx, kHOffs, (n + 1) * sizeof(int64_t));
+        int64_t* dOff = (int64_t*)scratch(ctx, kHOffs, (n + nchunks) * sizeof(int64_t));
         // every root a query can have fits: no second pass after the count is known
-        const int64_t rcap = std::max<int64_t>(1, n * nb);
-        fsk_root* dR = (fsk_root*)scratch(ctx, kHRoots, rcap * sizeof(fsk_root));
+        fsk_root* dR = (fsk_root*)scratch(ctx, kHRoots, std::max<int64_t>(1, n * nb) * sizeof(fsk_root));
+        if (!ctx->copy) cuda_check(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking), "cudaStreamCreate");
+        if (!ctx->hcount) cuda_check(cudaMallocHost(&ctx->hcount, 64 * sizeof(int64_t)), "cudaMallocHost");
         cuda_check(cudaMemcpyAsync(dW, weights, V * nb * sizeof(float), cudaMemcpyHostToDevice, st), "H2D weights");
         cuda_check(cudaMemcpyAsync(dB, bones, nb * 12 * sizeof(float), cudaMemcpyHostToDevice, st), "H2D bones");
         if (n > 0)
             cuda_check(cudaMemcpyAsync(dP, points, n * 3 * sizeof(float), cudaMemcpyHostToDevice, st), "H2D points");
         const GridPlanes P = run_precompute(ctx, dW, g, dB, nullptr, nullptr, true, needs_f64(opts->flags), st);
-        const SearchState s = run_search(ctx, P, g, dB, dP, n, sp, opts->flags, st);
-        compact(ctx, s, n, nb, dOff, dR, rcap, st);
-        cuda_check(cudaMemcpyAsync(offsets, dOff, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st), "D2H offsets");
-        cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
-        const int64_t total = offsets[n];
-        *total_out = total;
-        if (total > cap) fail(FSK_EINVAL, "fsk: root buffer too small");
-        if (total > 0) {
-            if (!roots) fail(FSK_EINVAL, "fsk: null buffer");
-            cuda_check(cudaMemcpyAsync(roots, dR, total * sizeof(fsk_root), cudaMemcpyDeviceToHost, st), "D2H roots");
-            cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+        std::vector<cudaEvent_t> done(nchunks), offs_ready(nchunks);
+        for (int64_t c = 0; c < nchunks; ++c) {
+            cuda_check(cudaEventCreateWithFlags(&done[c], cudaEventDisableTiming), "cudaEventCreate");
+            cuda_check(cudaEventCreateWithFlags(&offs_ready[c], cudaEventDisableTiming), "cudaEventCreate");
         }
+        struct Events {
+            std::vector<cudaEvent_t>* a;
+            std::vector<cudaEvent_t>* b;
+            ~Events() {
+                for (auto e : *a) cudaEventDestroy(e);
+                for (auto e : *b) cudaEventDestroy(e);
+            }
+        } cleanup{&done, &offs_ready};
+        for (int64_t c = 0; c < nchunks; ++c) {
+            const int64_t p0 = c * csz, m = std::max<int64_t>(0, std::min(csz, n - p0));
+            const SearchState s = run_search(ctx, P, g, dB, dP + 3 * p0, m, sp, opts->flags, st);
+            compact(ctx, s, m, nb, dOff + p0 + c, dR + p0 * nb, m * nb, st);
+            cuda_check(cudaEventRecord(done[c], st), "cudaEventRecord");
+            cuda_check(cudaStreamWaitEvent(ctx->copy, done[c], 0), "cudaStreamWaitEvent");
+            if (m > 0)
+                cuda_check(cudaMemcpyAsync(offsets + p0, dOff + p0 + c, m * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                           ctx->copy),
+                           "D2H offsets");
+            cuda_check(cudaMemcpyAsync(ctx->hcount + c, dOff + p0 + c + m, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                       ctx->copy),
+                       "D2H count");
+            cuda_check(cudaEventRecord(offs_ready[c], ctx->copy), "cudaEventRecord");
+        }
+        int64_t base = 0;
+        for (int64_t c = 0; c < nchunks; ++c) {  // chunk c's roots stream out while later chunks compute
+            const int64_t p0 = c * csz, m = std::max<int64_t>(0, std::min(csz, n - p0));
+            cuda_check(cudaEventSynchronize(offs_ready[c]), "cudaEventSynchronize");
+            const int64_t cnt = ctx->hcount[c];  // chunk-local total
+            if (base + cnt > cap) fail(FSK_EINVAL, "fsk: root buffer too small");
+            if (cnt > 0) {
+                if (!roots) fail(FSK_EINVAL, "fsk: null buffer");
+                cuda_check(cudaMemcpyAsync(roots + base, dR + p0 * nb, cnt * sizeof(fsk_root), cudaMemcpyDeviceToHost,
+                                           ctx->copy),
+                           "D2H roots");
+            }
+            for (int64_t i = 0; i < m; ++i) offsets[p0 + i] += base;
+            base += cnt;
+        }
+        offsets[n] = base;
+        *total_out = base;
+        cuda_check(cudaStreamSynchronize(ctx->copy), "cudaStreamSynchronize");
+        cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
     });
 }
 
