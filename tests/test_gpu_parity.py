@@ -358,3 +358,76 @@ def test_precision_modes(deformer):
     assert res["mixed"][0] >= MASK_AGREE and res["mixed"][1] <= TOL_X
     assert res["fp64"][0] >= 0.99999 and res["fp64"][1] <= TOL_X
     assert res["mixed"][3] < 0.15  # the fp64 tail stays a small share of the solves
+
+
+# ------------------------------------------------------------------ full-size (C2) properties
+@pytest.fixture(scope="module")
+def c2_full(deformer):
+    """BASELINE.json configs[1] at full size: 200k posed points x 24 inits, 32^3, max_iters 50."""
+    sc = S.make_scene((32, 32, 32), 200_000, seed=1)
+    w, B, x = dev(sc.weights), dev(sc.bones), dev(sc.points)
+    o = opts_of(sc, 50)
+    offs, roots = deformer.deform(w, sc.dims, sc.bbox, B, x, o)
+    torch.cuda.synchronize()
+    return sc, w, B, x, o, offs, roots
+
+
+def test_full_size_soundness_and_dedup_invariants(deformer, c2_full):
+    """Size-independent checks at 200k x 24 (SPEC.md:566 soundness, :248 dedup spacing):
+    every kept root re-evaluates to ||d(x*) - x'|| < conv_eps (float32 evaluation noise
+    allowed), roots of a query are in bone order and pairwise >= dedup_dist apart."""
+    sc, w, B, x, o, offs, roots = c2_full
+    tg = deformer.precompute_transform_grid(w, sc.dims, sc.bbox, B)
+    offs_h = offs.cpu().numpy()
+    total = int(offs_h[-1])
+    r = roots[:total]
+    _, d, _ = deformer.eval_points(tg, sc.dims, sc.bbox, sc.n_bones, r[:, :3].contiguous())
+    qidx = np.repeat(np.arange(sc.points.shape[0]), np.diff(offs_h))
+    res = np.linalg.norm(d.cpu().numpy() - sc.points[qidx], axis=1)
+    assert (res < o.conv_eps * 1.05).all(), res.max() / o.conv_eps
+    rh = r.cpu().numpy()
+    bone = rh[:, 13].view(np.int32)
+    same_q = qidx[1:] == qidx[:-1]
+    assert (bone[1:][same_q] > bone[:-1][same_q]).all()  # bone order within a query
+    # pairwise spacing of consecutive kept roots of a query (greedy dedup keeps all pairs apart)
+    gap = np.linalg.norm(rh[1:, :3] - rh[:-1, :3], axis=1)[same_q]
+    assert (gap >= o.dedup_dist * (1 - 1e-5)).all()
+    assert 1.0 <= total / sc.points.shape[0] <= 3.0
+
+
+def test_full_size_sharding_invariance(deformer, c2_full):
+    """The multi-GPU partition (contiguous point ranges, parallel.hpp:28-29) cannot change a
+    solve: searching the two halves separately gives the whole batch's records bitwise."""
+    sc, w, B, x, o, offs, roots = c2_full
+    n = sc.points.shape[0]
+    parts = []
+    for a, b in ((0, n // 2), (n // 2, n)):
+        po, pr = deformer.deform(w, sc.dims, sc.bbox, B, x[a:b].contiguous(), o)
+        parts.append(pr[: int(po[-1].item())].cpu())
+    whole = roots[: int(offs[-1].item())].cpu()
+    assert torch.equal(torch.cat(parts), whole)
+
+
+def test_full_size_mask_agreement_on_sample(deformer, c2_full):
+    """Oracle parity on a 12k-point sample of the full-size batch (the oracle would take
+    minutes on all 4.8M solves): the same points searched inside the full batch."""
+    sc, w, B, x, o, offs, roots = c2_full
+    idx = np.random.default_rng(0).choice(sc.points.shape[0], 12_000, replace=False)
+    idx.sort()
+    sub = S.Scene(sc.dims, sc.bbox, sc.weights, sc.bones, sc.points[idx], sc.angles, sc.diag)
+    r = run_oracle(sub, 50)
+    offs_h = offs.cpu().numpy()
+    rh = roots.cpu().numpy()
+    agree = 0
+    maxdx = 0.0
+    for k, p in enumerate(idx):
+        recs = rh[offs_h[p]:offs_h[p + 1]]
+        bones_gpu = recs[:, 13].view(np.int32).tolist()
+        bones_ref = np.where(r["keep"][k] == 1)[0].tolist()
+        agree += bones_gpu == bones_ref
+        for rec, b in zip(recs, bones_gpu):
+            if r["keep"][k, b]:
+                maxdx = max(maxdx, float(np.abs(rec[:3] - r["x_c"][k, b]).max()))
+    print(f"\nfull-size sample: identical root sets {agree}/{len(idx)}, max|dx| {maxdx:.2e}")
+    assert agree / len(idx) >= MASK_AGREE
+    assert maxdx <= TOL_X
