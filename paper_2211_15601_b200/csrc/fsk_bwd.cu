@@ -134,6 +134,91 @@ __global__ void __launch_bounds__(256) k_bwd_scatter_fixed(GridP g, RootRef R, c
     }
 }
 
+// ---- deterministic mode, gather formulation (no atomics on the gradient) ------------------
+// 1. k_bwd_bucket_count: per root, its cell (the locate_cell base vertex) → count per cell;
+//    also the fixed-point scale's max term.
+// 2. exclusive scan of the counts → bucket starts.
+// 3. k_bwd_bucket_fill: roots written into their cell's bucket as {x*, u} (order inside a
+//    bucket is arbitrary — the sums below are integer and therefore order-independent).
+// 4. k_bwd_gather_fixed: one thread per grid vertex sums, over the ≤ 8 cells it is a corner
+//    of, every bucketed root's fixed-point term φ_c·u_r·x̃_col·scale in int64 registers, and
+//    writes dL/dT[v] once. Bitwise reproducible, identical to the scattered fixed-point sum.
+struct BwdRec {
+    float x[3];
+    float u[3];
+};
+
+__global__ void __launch_bounds__(256) k_bwd_bucket_count(GridP g, RootRef R, const float* __restrict__ gx, int64_t n,
+                                                          int32_t* __restrict__ cnt, int32_t* __restrict__ cell_of,
+                                                          unsigned int* __restrict__ maxbits) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    float m = 0.f;
+    if (p < n) {
+        float xs[3], u[3];
+        int cell = -1;
+        if (bwd_load(R, p, gx, xs, u)) {
+            cell = locate<false>(g, xs[0], xs[1], xs[2]).base;
+            atomicAdd(cnt + cell, 1);
+            const float mu = fmaxf(fabsf(u[0]), fmaxf(fabsf(u[1]), fabsf(u[2])));
+            const float mx = fmaxf(1.f, fmaxf(fabsf(xs[0]), fmaxf(fabsf(xs[1]), fabsf(xs[2]))));
+            m = mu * mx;
+            if (!isfinite(m)) m = 3.0e38f;
+        }
+        cell_of[p] = cell;
+    }
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffff, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(maxbits, __float_as_uint(m));
+}
+
+__global__ void __launch_bounds__(256) k_bwd_bucket_fill(RootRef R, const float* __restrict__ gx, int64_t n,
+                                                         const int32_t* __restrict__ cell_of,
+                                                         const int64_t* __restrict__ start, int32_t* __restrict__ fill,
+                                                         BwdRec* __restrict__ rec) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const int cell = cell_of[p];
+    if (cell < 0) return;
+    float xs[3], u[3];
+    bwd_load(R, p, gx, xs, u);
+    const int64_t pos = start[cell] + atomicAdd(fill + cell, 1);
+    rec[pos] = BwdRec{{xs[0], xs[1], xs[2]}, {u[0], u[1], u[2]}};
+}
+
+__global__ void __launch_bounds__(128) k_bwd_gather_fixed(GridP g, const int64_t* __restrict__ start,
+                                                          const BwdRec* __restrict__ rec,
+                                                          const unsigned int* __restrict__ maxbits, int64_t n,
+                                                          float* __restrict__ out) {
+    const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t V = (int64_t)g.nx * g.ny * g.nz;
+    if (v >= V) return;
+    const int i = (int)(v % g.nx), j = (int)((v / g.nx) % g.ny), k = (int)(v / ((int64_t)g.nx * g.ny));
+    const double scale = fixed_scale(*maxbits, n);
+    long long acc[12];
+#pragma unroll
+    for (int e = 0; e < 12; ++e) acc[e] = 0;
+    for (int q = 0; q < 8; ++q) {
+        const int di = q & 1, dj = (q >> 1) & 1, dk = q >> 2;  // v is corner (di,dj,dk) of this cell
+        const int ci = i - di, cj = j - dj, ck = k - dk;
+        if (ci < 0 || cj < 0 || ck < 0 || ci > g.nx - 2 || cj > g.ny - 2 || ck > g.nz - 2) continue;
+        const int cell = (ck * g.ny + cj) * g.nx + ci;
+        for (int64_t r = start[cell]; r < start[cell + 1]; ++r) {
+            const BwdRec b = rec[r];
+            const Cell c = locate<false>(g, b.x[0], b.x[1], b.x[2]);  // same φ as the scatter
+            const float phi = ((dk ? c.tz : 1.f - c.tz) * (dj ? c.ty : 1.f - c.ty)) * (di ? c.tx : 1.f - c.tx);
+            const double xt[4] = {b.x[0], b.x[1], b.x[2], 1.0};
+#pragma unroll
+            for (int rr = 0; rr < 3; ++rr) {
+                const double a = (double)phi * (double)b.u[rr] * scale;
+#pragma unroll
+                for (int col = 0; col < 4; ++col) acc[4 * rr + col] += __double2ll_rn(a * xt[col]);
+            }
+        }
+    }
+    const double inv = 1.0 / scale;
+#pragma unroll
+    for (int e = 0; e < 12; ++e) out[12 * v + e] = (float)((double)acc[e] * inv);
+}
+
 __global__ void k_bwd_fixed_to_float(const long long* __restrict__ acc, int64_t m,
                                      const unsigned int* __restrict__ maxbits, int64_t n, float* __restrict__ out) {
     const double inv = 1.0 / fixed_scale(*maxbits, n);
@@ -183,17 +268,21 @@ void run_bwd(fsk_ctx* ctx, const GridP& g, const RootRef& R, const float* grad_x
                        reinterpret_cast<float4*>(grad_tgrid));
         return;
     }
-    unsigned long long* acc = (unsigned long long*)scratch(ctx, kBwdAcc, V * 12 * sizeof(unsigned long long));
-    unsigned int* mx = (unsigned int*)scratch(ctx, kBwdMax, 16);
-    FSK_LAUNCH(ctx, st, k_zero, std::min(blocks_for(V * 6, 256), cap_blocks), 256, 0, reinterpret_cast<float4*>(acc),
-               V * 6);
-    FSK_LAUNCH(ctx, st, k_zero, 1, 32, 0, reinterpret_cast<float4*>(mx), (int64_t)1);
-    if (n > 0) {
-        FSK_LAUNCH(ctx, st, k_bwd_maxterm, blocks_for(n, 256), 256, 0, R, grad_xc, n, mx);
-        FSK_LAUNCH(ctx, st, k_bwd_scatter_fixed, blocks_for(n, 256), 256, 0, g, R, grad_xc, n, mx, acc);
-    }
-    FSK_LAUNCH(ctx, st, k_bwd_fixed_to_float, std::min(blocks_for(V * 12, 256), cap_blocks), 256, 0,
-               reinterpret_cast<const long long*>(acc), V * 12, mx, n, grad_tgrid);
+    // deterministic: bucket the roots by cell, then gather per vertex (see k_bwd_gather_fixed)
+    const int64_t V4 = (V + 3) / 4 * 4;  // counts and fill cursors, zeroed together
+    int32_t* cnt = (int32_t*)scratch(ctx, kBwdAcc, (2 * V4 + 8) * sizeof(int32_t));
+    int32_t* fill = cnt + V4;
+    unsigned int* mx = (unsigned int*)(fill + V4);
+    int64_t* start = (int64_t*)scratch(ctx, kBwdStart, (V + 1) * sizeof(int64_t));
+    int32_t* cell_of = (int32_t*)scratch(ctx, kBwdCell, std::max<int64_t>(1, n) * sizeof(int32_t));
+    BwdRec* rec = (BwdRec*)scratch(ctx, kBwdRec, std::max<int64_t>(1, n) * sizeof(BwdRec));
+    FSK_LAUNCH(ctx, st, k_zero, std::min(blocks_for((2 * V4 + 8) / 4, 256), cap_blocks), 256, 0,
+               reinterpret_cast<float4*>(cnt), (2 * V4 + 8) / 4);
+    if (n > 0) FSK_LAUNCH(ctx, st, k_bwd_bucket_count, blocks_for(n, 256), 256, 0, g, R, grad_xc, n, cnt, cell_of, mx);
+    scan_i32_to_i64(ctx, cnt, V, start, st);
+    if (n > 0)
+        FSK_LAUNCH(ctx, st, k_bwd_bucket_fill, blocks_for(n, 256), 256, 0, R, grad_xc, n, cell_of, start, fill, rec);
+    FSK_LAUNCH(ctx, st, k_bwd_gather_fixed, blocks_for(V, 128), 128, 0, g, start, rec, mx, n, grad_tgrid);
 }
 
 }  // namespace

@@ -44,6 +44,7 @@ namespace fsk {
 // Scratch slots (one growable device buffer each).
 enum Slot {
     kHist, kBbox, kKeys, kPerm, kXs, kScanPart, kBwdAcc, kBwdMax, kPlanes, kPlanes64, kEscQ, kEscN,
+    kBwdStart, kBwdCell, kBwdRec,
     kOXr, kOJa, kOJb, kOJc, kOMeta, kOKeep, kNRoots, kOffs, kRootsTmp,
     kHW, kHB, kHP, kHT, kHOffs, kHRoots,
     kSlotCount
@@ -84,6 +85,8 @@ void after_launch(fsk_ctx* ctx, const char* name);
 
 GridP make_grid(const fsk_grid_desc* d);
 SearchP make_search(const fsk_search_opts* o);
+// exclusive scan of n int32 into n+1 int64 (out[n] = total); fsk_search.cu
+void scan_i32_to_i64(fsk_ctx* ctx, const int32_t* in, int64_t n, int64_t* out, cudaStream_t st);
 
 inline unsigned blocks_for(int64_t n, int t) { return (unsigned)std::max<int64_t>(1, (n + t - 1) / t); }
 

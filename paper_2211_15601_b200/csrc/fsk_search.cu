@@ -844,6 +844,12 @@ void check_search_args(const GridP& g, int32_t n_bones_pose, const void* grid_pt
 }
 
 }  // namespace
+
+// Exclusive int32 → int64 scan for other translation units (fsk_ctx.h).
+void scan_i32_to_i64(fsk_ctx* ctx, const int32_t* in, int64_t n, int64_t* out, cudaStream_t st) {
+    run_scan(ctx, in, n, out, st);
+}
+
 }  // namespace fsk
 
 using namespace fsk;

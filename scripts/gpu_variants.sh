@@ -1,5 +1,4 @@
 set -x
-python -m pytest tests -m gpu -q -rf > gpurun_out/pytest11.log 2>&1
-python bench.py > gpurun_out/bench11_full.log 2>&1
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke11.log 2>&1
-python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench11_ref.log 2>&1
+python -m pytest tests -m gpu -q -rf -s > gpurun_out/pytest12.log 2>&1
+python bench.py --steps 50 --warmup 5 --cpu-seconds 3 > gpurun_out/bench12.log 2>&1
+python bench.py --steps 5 --warmup 2 --no-cpu-baseline --grid 128,128,32 --points 8000000 > gpurun_out/bench12_c5.log 2>&1
