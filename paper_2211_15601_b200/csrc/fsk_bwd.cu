@@ -85,53 +85,13 @@ __global__ void __launch_bounds__(256) k_bwd_scatter(GridP g, RootRef R, const f
     }
 }
 
-__global__ void __launch_bounds__(256) k_bwd_maxterm(RootRef R, const float* __restrict__ gx, int64_t n,
-                                                     unsigned int* __restrict__ maxbits) {
-    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    float m = 0.f;
-    if (p < n) {
-        float xs[3], u[3];
-        if (bwd_load(R, p, gx, xs, u)) {
-            const float mu = fmaxf(fabsf(u[0]), fmaxf(fabsf(u[1]), fabsf(u[2])));
-            const float mx = fmaxf(1.f, fmaxf(fabsf(xs[0]), fmaxf(fabsf(xs[1]), fabsf(xs[2]))));
-            m = mu * mx;
-            if (!isfinite(m)) m = 3.0e38f;
-        }
-    }
-    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffff, m, o));
-    if ((threadIdx.x & 31) == 0) atomicMax(maxbits, __float_as_uint(m));  // m >= 0: bit order == value order
-}
-
+// Fixed-point scale of the deterministic mode: a power of two with n·max|term|·scale < 2^62,
+// so no int64 sum over at most n roots can overflow; max|term| ≤ max|u|·max(1, |x*|).
 __device__ __forceinline__ double fixed_scale(unsigned int maxbits, int64_t n) {
     const double m = (double)__uint_as_float(maxbits) * (double)(n > 0 ? n : 1);
     if (!(m > 0.0)) return 1.0;
     const int e = (int)floor(log2(m));
-    return ldexp(1.0, 61 - e);  // n·max|term|·scale < 2^62: no overflow in any sum
-}
-
-__global__ void __launch_bounds__(256) k_bwd_scatter_fixed(GridP g, RootRef R, const float* __restrict__ gx, int64_t n,
-                                                           const unsigned int* __restrict__ maxbits,
-                                                           unsigned long long* __restrict__ acc) {
-    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (p >= n) return;
-    float xs[3], u[3];
-    if (!bwd_load(R, p, gx, xs, u)) return;
-    const double scale = fixed_scale(*maxbits, n);
-    const Cell c = locate<false>(g, xs[0], xs[1], xs[2]);
-    const int nxy = g.nx * g.ny;
-    const double xt[4] = {xs[0], xs[1], xs[2], 1.0};
-    for (int q = 0; q < 8; ++q) {
-        const int di = q & 1, dj = (q >> 1) & 1, dk = q >> 2;
-        const float phi = ((dk ? c.tz : 1.f - c.tz) * (dj ? c.ty : 1.f - c.ty)) * (di ? c.tx : 1.f - c.tx);
-        unsigned long long* dst = acc + 12 * (int64_t)(c.base + dk * nxy + dj * g.nx + di);
-#pragma unroll
-        for (int r = 0; r < 3; ++r) {
-            const double a = (double)phi * (double)u[r] * scale;
-#pragma unroll
-            for (int col = 0; col < 4; ++col)
-                atomicAdd(dst + 4 * r + col, (unsigned long long)__double2ll_rn(a * xt[col]));
-        }
-    }
+    return ldexp(1.0, 61 - e);
 }
 
 // ---- deterministic mode, gather formulation (no atomics on the gradient) ------------------
@@ -188,20 +148,25 @@ __global__ void __launch_bounds__(128) k_bwd_gather_fixed(GridP g, const int64_t
                                                           const BwdRec* __restrict__ rec,
                                                           const unsigned int* __restrict__ maxbits, int64_t n,
                                                           float* __restrict__ out) {
-    const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    // 8 lanes per vertex, lane q handles the cell for which v is corner q; the 8 partial
+    // int64 sums are combined with shuffles (integer: order-independent).
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t V = (int64_t)g.nx * g.ny * g.nz;
-    if (v >= V) return;
+    const int64_t v = t >> 3;
+    const int q = (int)(t & 7);
+    const bool live = v < V;
     const int i = (int)(v % g.nx), j = (int)((v / g.nx) % g.ny), k = (int)(v / ((int64_t)g.nx * g.ny));
     const double scale = fixed_scale(*maxbits, n);
     long long acc[12];
 #pragma unroll
     for (int e = 0; e < 12; ++e) acc[e] = 0;
-    for (int q = 0; q < 8; ++q) {
+    {
         const int di = q & 1, dj = (q >> 1) & 1, dk = q >> 2;  // v is corner (di,dj,dk) of this cell
         const int ci = i - di, cj = j - dj, ck = k - dk;
-        if (ci < 0 || cj < 0 || ck < 0 || ci > g.nx - 2 || cj > g.ny - 2 || ck > g.nz - 2) continue;
-        const int cell = (ck * g.ny + cj) * g.nx + ci;
-        for (int64_t r = start[cell]; r < start[cell + 1]; ++r) {
+        const bool ok = live && ci >= 0 && cj >= 0 && ck >= 0 && ci <= g.nx - 2 && cj <= g.ny - 2 && ck <= g.nz - 2;
+        const int cell = ok ? (ck * g.ny + cj) * g.nx + ci : 0;
+        const int64_t r0 = ok ? start[cell] : 0, r1 = ok ? start[cell + 1] : 0;
+        for (int64_t r = r0; r < r1; ++r) {
             const BwdRec b = rec[r];
             const Cell c = locate<false>(g, b.x[0], b.x[1], b.x[2]);  // same φ as the scatter
             const float phi = ((dk ? c.tz : 1.f - c.tz) * (dj ? c.ty : 1.f - c.ty)) * (di ? c.tx : 1.f - c.tx);
@@ -214,17 +179,15 @@ __global__ void __launch_bounds__(128) k_bwd_gather_fixed(GridP g, const int64_t
             }
         }
     }
-    const double inv = 1.0 / scale;
 #pragma unroll
-    for (int e = 0; e < 12; ++e) out[12 * v + e] = (float)((double)acc[e] * inv);
+    for (int e = 0; e < 12; ++e)
+        for (int o = 4; o > 0; o >>= 1) acc[e] += __shfl_down_sync(0xffffffff, acc[e], o, 8);
+    const double inv = 1.0 / scale;
+    if (live && q == 0)
+#pragma unroll
+        for (int e = 0; e < 12; ++e) out[12 * v + e] = (float)((double)acc[e] * inv);
 }
 
-__global__ void k_bwd_fixed_to_float(const long long* __restrict__ acc, int64_t m,
-                                     const unsigned int* __restrict__ maxbits, int64_t n, float* __restrict__ out) {
-    const double inv = 1.0 / fixed_scale(*maxbits, n);
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
-        out[i] = (float)((double)acc[i] * inv);
-}
 
 // dL/dw[v][i] = Σ_e dL/dT[v][e]·B_i[e]. Tile of 128 vertices staged in shared memory so the
 // [V][n_b] store is coalesced. HBM-bound: V·(48 + 4·n_b) bytes.
@@ -282,7 +245,7 @@ void run_bwd(fsk_ctx* ctx, const GridP& g, const RootRef& R, const float* grad_x
     scan_i32_to_i64(ctx, cnt, V, start, st);
     if (n > 0)
         FSK_LAUNCH(ctx, st, k_bwd_bucket_fill, blocks_for(n, 256), 256, 0, R, grad_xc, n, cell_of, start, fill, rec);
-    FSK_LAUNCH(ctx, st, k_bwd_gather_fixed, blocks_for(V, 128), 128, 0, g, start, rec, mx, n, grad_tgrid);
+    FSK_LAUNCH(ctx, st, k_bwd_gather_fixed, blocks_for(8 * V, 128), 128, 0, g, start, rec, mx, n, grad_tgrid);
 }
 
 }  // namespace
