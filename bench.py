@@ -239,6 +239,7 @@ def run_ours(args, rank, world, local_rank):
 
     peak_fp32 = D.measure_fp32_peak()
     peak_fp64 = D.measure_fp64_peak()
+    peak_l1 = D.measure_l1_gather_peak()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -303,7 +304,8 @@ def run_ours(args, rank, world, local_rank):
     breakdown = {}
     for kname in ("k_precompute", "k_sort_init", "k_sort_bbox", "k_sort_hist", "k_sort_scan", "k_sort_scatter",
                   "k_search_fast", "k_search_escalated", "k_dedup", "k_scan_partial", "k_scan_top", "k_scan_apply",
-                  "k_emit"):
+                  "k_emit", "k_zero", "k_bwd_scatter", "k_bwd_bucket_count", "k_bwd_bucket_fill", "k_bwd_gather_fixed",
+                  "k_grad_weights"):
         ms_, n_ = D.prof_read(kname, reset=False)
         if n_:
             breakdown[kname] = round(ms_ / args.steps, 5)
@@ -358,7 +360,12 @@ def run_ours(args, rank, world, local_rank):
                      "mean_final_iters_per_solve": mean_iters, "converged_frac": conv_frac,
                      "kept_roots_per_query": total_roots / n,
                      "gather": {"requested_bytes_per_launch": gather,
-                                "achieved_GBps": gather / (k2_avg * 1e-3) / 1e9},
+                                "achieved_GBps": gather / (k2_avg * 1e-3) / 1e9,
+                                "peak_GBps_measured": peak_l1,
+                                "frac": gather / (k2_avg * 1e-3) / 1e9 / peak_l1,
+                                "peak_source": "fsk_measure_l1_gather_peak: independent LDG.256 at random "
+                                               "32-B slots of an L1-resident table, all SMs",
+                                "note": "the binding resource of k_search_fast per ncu (L1 data pipe 92 %)"},
                      "k2_share_of_step": k2_ms / max(all_ms, 1e-9),
                      "k2_escalated_share_of_step": k2e_ms / max(all_ms, 1e-9),
                      "kernel_ms_per_step": breakdown,

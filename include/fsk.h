@@ -104,6 +104,9 @@ int fsk_ctx_set_profiling(fsk_ctx* ctx, int on);
 int fsk_ctx_prof_read(fsk_ctx* ctx, const char* name, double* total_ms, int64_t* count, int reset);
 int fsk_measure_fp32_peak(fsk_ctx* ctx, double* tflops);
 int fsk_measure_fp64_peak(fsk_ctx* ctx, double* tflops);  /* same with DFMA chains */
+/* L1 gather delivery rate (GB/s): independent 256-bit loads at random 32-B slots of an
+ * L1-resident table, the access pattern of the search's gathers (roofline denominator). */
+int fsk_measure_l1_gather_peak(fsk_ctx* ctx, double* gbps);
 /* Search work counters accumulated by the context's searches (synchronizes the device):
  * out = {float32 solves, float32 Broyden iterations, float32 converged-terminating
  * iterations, float64 solves, float64 iterations, float64 converged-terminating iterations}. */

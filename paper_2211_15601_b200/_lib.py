@@ -23,7 +23,7 @@ EXPORTS = [
     "fsk_search_opts_defaults", "fsk_precompute_tgrid", "fsk_search_fwd", "fsk_compact_roots",
     "fsk_deform_host", "fsk_eval_points", "fsk_init_states", "fsk_search_bwd", "fsk_grad_weights",
     "fsk_ctx_set_profiling", "fsk_ctx_prof_read", "fsk_measure_fp32_peak", "fsk_batch_search", "fsk_deform",
-    "fsk_search_bwd_roots", "fsk_ctx_search_stats", "fsk_measure_fp64_peak",
+    "fsk_search_bwd_roots", "fsk_ctx_search_stats", "fsk_measure_fp64_peak", "fsk_measure_l1_gather_peak",
 ]
 
 
@@ -96,6 +96,7 @@ def load():
     L.fsk_ctx_search_stats.argtypes = [_vp, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
     L.fsk_measure_fp32_peak.argtypes = [_vp, ctypes.POINTER(ctypes.c_double)]
     L.fsk_measure_fp64_peak.argtypes = [_vp, ctypes.POINTER(ctypes.c_double)]
+    L.fsk_measure_l1_gather_peak.argtypes = [_vp, ctypes.POINTER(ctypes.c_double)]
     _lib = L
     return L
 

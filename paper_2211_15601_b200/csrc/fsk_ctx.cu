@@ -135,6 +135,28 @@ __global__ void __launch_bounds__(256) k_peak_fma(R* out, int iters, R a, R b) {
     if (s == (R)12345.678) out[0] = s;  // keep the chains alive
 }
 
+// L1 gather microbenchmark: every lane issues independent 256-bit loads at pseudo-random
+// 32-byte-aligned offsets of a 64 KiB table (L1-resident after the first touch) — the access
+// pattern of the search's x-pair gathers with no reuse between lanes. Returns the bytes
+// delivered to registers per second: the roofline denominator of the gather-bound kernels.
+__global__ void __launch_bounds__(256) k_peak_l1_gather(const float* __restrict__ table, float* out, int iters) {
+    uint32_t s = (blockIdx.x * 256u + threadIdx.x) * 2654435761u + 12345u;
+    float acc = 0.f;
+    for (int k = 0; k < iters; ++k) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            s = s * 1664525u + 1013904223u;
+            const float* q = table + ((s >> 8) & 2047u) * 8;  // 2048 slots × 32 B
+            float a0, a1, a2, a3, a4, a5, a6, a7;
+            asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                         : "=f"(a0), "=f"(a1), "=f"(a2), "=f"(a3), "=f"(a4), "=f"(a5), "=f"(a6), "=f"(a7)
+                         : "l"(q));
+            acc += ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
+        }
+    }
+    if (acc == 12345.678f) out[0] = acc;
+}
+
 template <typename R>
 double measure_peak(fsk_ctx* ctx, int iters) {
     R* o = (R*)scratch(ctx, kBwdMax, 16);
@@ -260,6 +282,29 @@ int fsk_measure_fp32_peak(fsk_ctx* ctx, double* tflops) {
         set_device(ctx);
         if (!tflops) fail(FSK_EINVAL, "fsk: null output pointer");
         *tflops = measure_peak<float>(ctx, 1 << 14);
+    });
+}
+
+int fsk_measure_l1_gather_peak(fsk_ctx* ctx, double* gbps) {
+    return guard([&] {
+        set_device(ctx);
+        if (!gbps) fail(FSK_EINVAL, "fsk: null output pointer");
+        float* table = (float*)scratch(ctx, kPeakTable, 2048 * 8 * sizeof(float) + 64);
+        cuda_check(cudaMemset(table, 0, 2048 * 8 * sizeof(float) + 64), "cudaMemset");
+        const int blocks = ctx->sm_count * 8, iters = 1 << 10;
+        cudaEvent_t a, b;
+        cuda_check(cudaEventCreate(&a), "cudaEventCreate");
+        cuda_check(cudaEventCreate(&b), "cudaEventCreate");
+        k_peak_l1_gather<<<blocks, 256>>>(table, table + 2048 * 8, 16);  // warm-up
+        cuda_check(cudaEventRecord(a, 0), "cudaEventRecord");
+        k_peak_l1_gather<<<blocks, 256>>>(table, table + 2048 * 8, iters);
+        cuda_check(cudaEventRecord(b, 0), "cudaEventRecord");
+        cuda_check(cudaEventSynchronize(b), "cudaEventSynchronize");
+        float ms = 0.f;
+        cuda_check(cudaEventElapsedTime(&ms, a, b), "cudaEventElapsedTime");
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        *gbps = 32.0 * 8.0 * iters * (double)blocks * 256.0 / (ms * 1e-3) / 1e9;
     });
 }
 

@@ -44,7 +44,7 @@ namespace fsk {
 // Scratch slots (one growable device buffer each).
 enum Slot {
     kHist, kBbox, kKeys, kPerm, kXs, kScanPart, kBwdAcc, kBwdMax, kPlanes, kPlanes64, kEscQ, kEscN,
-    kBwdStart, kBwdCell, kBwdRec,
+    kBwdStart, kBwdCell, kBwdRec, kPeakTable,
     kOXr, kOJa, kOJb, kOJc, kOMeta, kOKeep, kNRoots, kOffs, kRootsTmp,
     kHW, kHB, kHP, kHT, kHOffs, kHRoots,
     kSlotCount

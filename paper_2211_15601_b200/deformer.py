@@ -142,6 +142,11 @@ class Deformer:
         check(self.L.fsk_measure_fp32_peak(self._ctx, ctypes.byref(t)))
         return t.value
 
+    def measure_l1_gather_peak(self) -> float:
+        t = ctypes.c_double()
+        check(self.L.fsk_measure_l1_gather_peak(self._ctx, ctypes.byref(t)))
+        return t.value
+
     def measure_fp64_peak(self) -> float:
         t = ctypes.c_double()
         check(self.L.fsk_measure_fp64_peak(self._ctx, ctypes.byref(t)))
