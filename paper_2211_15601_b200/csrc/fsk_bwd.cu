@@ -144,48 +144,52 @@ __global__ void __launch_bounds__(256) k_bwd_bucket_fill(RootRef R, const float*
     rec[pos] = BwdRec{{xs[0], xs[1], xs[2]}, {u[0], u[1], u[2]}};
 }
 
-__global__ void __launch_bounds__(128) k_bwd_gather_fixed(GridP g, const int64_t* __restrict__ start,
-                                                          const BwdRec* __restrict__ rec,
-                                                          const unsigned int* __restrict__ maxbits, int64_t n,
-                                                          float* __restrict__ out) {
-    // 8 lanes per vertex, lane q handles the cell for which v is corner q; the 8 partial
-    // int64 sums are combined with shuffles (integer: order-independent).
-    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+// One warp per non-empty cell: lane L owns the outputs o = L, L+32, L+64 of the cell's
+// 8 corners × 12 entries (o = 12·corner + entry) and sums their fixed-point terms over every
+// root in the cell's bucket (broadcast loads; no imbalance from dense cells beyond the warp);
+// the per-cell sums then go to the corner vertices with integer atomics — 96 per cell instead
+// of 96 per root, and integer addition keeps the result bitwise order-independent.
+__global__ void __launch_bounds__(256) k_bwd_cell_reduce(GridP g, const int64_t* __restrict__ start,
+                                                         const BwdRec* __restrict__ rec,
+                                                         const unsigned int* __restrict__ maxbits, int64_t n,
+                                                         unsigned long long* __restrict__ acc) {
     const int64_t V = (int64_t)g.nx * g.ny * g.nz;
-    const int64_t v = t >> 3;
-    const int q = (int)(t & 7);
-    const bool live = v < V;
-    const int i = (int)(v % g.nx), j = (int)((v / g.nx) % g.ny), k = (int)(v / ((int64_t)g.nx * g.ny));
+    const int lane = threadIdx.x & 31;
+    const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const double scale = fixed_scale(*maxbits, n);
-    long long acc[12];
-#pragma unroll
-    for (int e = 0; e < 12; ++e) acc[e] = 0;
-    {
-        const int di = q & 1, dj = (q >> 1) & 1, dk = q >> 2;  // v is corner (di,dj,dk) of this cell
-        const int ci = i - di, cj = j - dj, ck = k - dk;
-        const bool ok = live && ci >= 0 && cj >= 0 && ck >= 0 && ci <= g.nx - 2 && cj <= g.ny - 2 && ck <= g.nz - 2;
-        const int cell = ok ? (ck * g.ny + cj) * g.nx + ci : 0;
-        const int64_t r0 = ok ? start[cell] : 0, r1 = ok ? start[cell + 1] : 0;
+    const int nxy = g.nx * g.ny;
+    for (int64_t cell = warp0; cell < V; cell += nwarps) {
+        const int64_t r0 = start[cell], r1 = start[cell + 1];
+        if (r0 == r1) continue;
+        long long s[3] = {0, 0, 0};
         for (int64_t r = r0; r < r1; ++r) {
             const BwdRec b = rec[r];
-            const Cell c = locate<false>(g, b.x[0], b.x[1], b.x[2]);  // same φ as the scatter
-            const float phi = ((dk ? c.tz : 1.f - c.tz) * (dj ? c.ty : 1.f - c.ty)) * (di ? c.tx : 1.f - c.tx);
-            const double xt[4] = {b.x[0], b.x[1], b.x[2], 1.0};
+            const Cell c = locate<false>(g, b.x[0], b.x[1], b.x[2]);  // c.base == cell
 #pragma unroll
-            for (int rr = 0; rr < 3; ++rr) {
-                const double a = (double)phi * (double)b.u[rr] * scale;
-#pragma unroll
-                for (int col = 0; col < 4; ++col) acc[4 * rr + col] += __double2ll_rn(a * xt[col]);
+            for (int t = 0; t < 3; ++t) {
+                const int o = lane + 32 * t, q = o / 12, e = o - 12 * q;
+                const int di = q & 1, dj = (q >> 1) & 1, dk = q >> 2, row = e >> 2, col = e & 3;
+                const float phi = ((dk ? c.tz : 1.f - c.tz) * (dj ? c.ty : 1.f - c.ty)) * (di ? c.tx : 1.f - c.tx);
+                const double a = (double)phi * (double)b.u[row] * scale;
+                const double xc = col == 3 ? 1.0 : (double)b.x[col];
+                s[t] += __double2ll_rn(a * xc);
             }
         }
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+            const int o = lane + 32 * t, q = o / 12, e = o - 12 * q;
+            const int64_t v = cell + (q >> 2) * nxy + ((q >> 1) & 1) * g.nx + (q & 1);
+            if (s[t]) atomicAdd(acc + 12 * v + e, (unsigned long long)s[t]);
+        }
     }
-#pragma unroll
-    for (int e = 0; e < 12; ++e)
-        for (int o = 4; o > 0; o >>= 1) acc[e] += __shfl_down_sync(0xffffffff, acc[e], o, 8);
-    const double inv = 1.0 / scale;
-    if (live && q == 0)
-#pragma unroll
-        for (int e = 0; e < 12; ++e) out[12 * v + e] = (float)((double)acc[e] * inv);
+}
+
+__global__ void k_bwd_fixed_to_float(const long long* __restrict__ acc, int64_t m,
+                                     const unsigned int* __restrict__ maxbits, int64_t n, float* __restrict__ out) {
+    const double inv = 1.0 / fixed_scale(*maxbits, n);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (float)((double)acc[i] * inv);
 }
 
 
@@ -231,21 +235,28 @@ void run_bwd(fsk_ctx* ctx, const GridP& g, const RootRef& R, const float* grad_x
                        reinterpret_cast<float4*>(grad_tgrid));
         return;
     }
-    // deterministic: bucket the roots by cell, then gather per vertex (see k_bwd_gather_fixed)
-    const int64_t V4 = (V + 3) / 4 * 4;  // counts and fill cursors, zeroed together
-    int32_t* cnt = (int32_t*)scratch(ctx, kBwdAcc, (2 * V4 + 8) * sizeof(int32_t));
+    // deterministic: bucket the roots by cell, reduce per cell, integer atomics to vertices
+    const int64_t V4 = (V + 3) / 4 * 4;  // fixed-point accumulators, counts, fill cursors: zeroed together
+    const int64_t words = 2 * (12 * V4) + 2 * V4 + 8;  // int32 words
+    int32_t* base = (int32_t*)scratch(ctx, kBwdAcc, words * sizeof(int32_t));
+    unsigned long long* acc = reinterpret_cast<unsigned long long*>(base);
+    int32_t* cnt = base + 2 * (12 * V4);
     int32_t* fill = cnt + V4;
     unsigned int* mx = (unsigned int*)(fill + V4);
     int64_t* start = (int64_t*)scratch(ctx, kBwdStart, (V + 1) * sizeof(int64_t));
     int32_t* cell_of = (int32_t*)scratch(ctx, kBwdCell, std::max<int64_t>(1, n) * sizeof(int32_t));
     BwdRec* rec = (BwdRec*)scratch(ctx, kBwdRec, std::max<int64_t>(1, n) * sizeof(BwdRec));
-    FSK_LAUNCH(ctx, st, k_zero, std::min(blocks_for((2 * V4 + 8) / 4, 256), cap_blocks), 256, 0,
-               reinterpret_cast<float4*>(cnt), (2 * V4 + 8) / 4);
+    FSK_LAUNCH(ctx, st, k_zero, std::min(blocks_for(words / 4, 256), cap_blocks), 256, 0,
+               reinterpret_cast<float4*>(base), words / 4);
     if (n > 0) FSK_LAUNCH(ctx, st, k_bwd_bucket_count, blocks_for(n, 256), 256, 0, g, R, grad_xc, n, cnt, cell_of, mx);
     scan_i32_to_i64(ctx, cnt, V, start, st);
-    if (n > 0)
+    if (n > 0) {
         FSK_LAUNCH(ctx, st, k_bwd_bucket_fill, blocks_for(n, 256), 256, 0, R, grad_xc, n, cell_of, start, fill, rec);
-    FSK_LAUNCH(ctx, st, k_bwd_gather_fixed, blocks_for(8 * V, 128), 128, 0, g, start, rec, mx, n, grad_tgrid);
+        FSK_LAUNCH(ctx, st, k_bwd_cell_reduce, std::min(blocks_for(32 * V, 256), cap_blocks * 2), 256, 0, g, start, rec,
+                   mx, n, acc);
+    }
+    FSK_LAUNCH(ctx, st, k_bwd_fixed_to_float, std::min(blocks_for(12 * V, 256), cap_blocks), 256, 0,
+               reinterpret_cast<const long long*>(acc), 12 * V, mx, n, grad_tgrid);
 }
 
 }  // namespace
