@@ -99,32 +99,47 @@ struct EscRule {
     double conv_band = 0, div_band = 0, det_guard = 0, den_guard = 0;
 };
 
-template <typename R, typename G>
-void solve(const Emu<R, G>& E, const double* B12, const double* xpd, int max_iters, R conv, R div, double* xo,
-           uint8_t* cv, int32_t* it, const EscRule* rule = nullptr, uint8_t* esc = nullptr) {
+// R: Broyden algebra and trilerp (J~, dx, dg, T); X: position x, residual g = T·[x;1] − x'
+// and the threshold tests; G: grid storage. (R, X, G) = (f32, f64, f32) is the "f64 state"
+// variant of the FP32 pass.
+template <typename R, typename G, typename X = R>
+void solve(const Emu<R, G>& E, const double* B12, const double* xpd, int max_iters, X conv, X div, double* xo,
+           uint8_t* cv, int32_t* it, const EscRule* rule = nullptr, uint8_t* esc = nullptr, double* jn = nullptr) {
     bool e = false;
-    auto near = [&](R v, R thr, double band) { return band > 0 && std::fabs((double)v / (double)thr - 1.0) < band; };
-    const R xp[3] = {(R)xpd[0], (R)xpd[1], (R)xpd[2]};
-    R Rm[9], t[3];
+    auto near = [&](X v, X thr, double band) { return band > 0 && std::fabs((double)v / (double)thr - 1.0) < band; };
+    const X xp[3] = {(X)xpd[0], (X)xpd[1], (X)xpd[2]};
+    X Rm[9], t[3];
     for (int r = 0; r < 3; ++r) {
-        for (int c = 0; c < 3; ++c) Rm[3 * r + c] = (R)B12[4 * r + c];
-        t[r] = (R)B12[4 * r + 3];
+        for (int c = 0; c < 3; ++c) Rm[3 * r + c] = (X)B12[4 * r + c];
+        t[r] = (X)B12[4 * r + 3];
     }
-    R x[3];
+    X x[3];
     for (int a = 0; a < 3; ++a) {
-        const R rt = Rm[a] * t[0] + Rm[3 + a] * t[1] + Rm[6 + a] * t[2];
+        const X rt = Rm[a] * t[0] + Rm[3 + a] * t[1] + Rm[6 + a] * t[2];
         x[a] = Rm[a] * xp[0] + Rm[3 + a] * xp[1] + Rm[6 + a] * xp[2] + (-rt);
     }
-    R J[9], Ji[9], d[3], g[3];
-    E.jacobian(x, J);
+    auto deform = [&](const X xx[3], X d[3]) {
+        const R xr[3] = {(R)xx[0], (R)xx[1], (R)xx[2]};
+        R T[12];
+        E.trilerp(xr, T);
+        for (int r = 0; r < 3; ++r)
+            d[r] = (X)T[4 * r] * xx[0] + (X)T[4 * r + 1] * xx[1] + (X)T[4 * r + 2] * xx[2] + (X)T[4 * r + 3];
+    };
+    R J[9], Ji[9];
+    X d[3], g[3];
+    double amp = 0, cosmin = 1;  // sensitivity diagnostics: largest relative rank-1 update, smallest |cos(dx, J~dg)|
+    {
+        const R xr[3] = {(R)x[0], (R)x[1], (R)x[2]};
+        E.jacobian(xr, J);
+    }
     if (rule) {
         const R det = J[0] * (J[4] * J[8] - J[5] * J[7]) - J[1] * (J[3] * J[8] - J[5] * J[6]) + J[2] * (J[3] * J[7] - J[4] * J[6]);
         if (std::fabs((double)det) < rule->det_guard) e = true;
     }
     inv_or_id(J, Ji);
-    E.deform(x, d);
+    deform(x, d);
     for (int a = 0; a < 3; ++a) g[a] = d[a] - xp[a];
-    R err = std::sqrt(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
+    X err = std::sqrt(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
     int iters = 0;
     bool conv_ok = err < conv;
     if (rule && (near(err, conv, rule->conv_band) || near(err, div, rule->div_band))) e = true;
@@ -133,13 +148,15 @@ void solve(const Emu<R, G>& E, const double* B12, const double* xpd, int max_ite
             if (rule && k >= rule->cap) { e = true; break; }
             if (err > div) break;
             R dx[3];
-            for (int r = 0; r < 3; ++r) dx[r] = -(Ji[3 * r] * g[0] + Ji[3 * r + 1] * g[1] + Ji[3 * r + 2] * g[2]);
-            for (int a = 0; a < 3; ++a) x[a] += dx[a];
-            E.deform(x, d);
-            R gn[3], dg[3];
+            const R gr[3] = {(R)g[0], (R)g[1], (R)g[2]};
+            for (int r = 0; r < 3; ++r) dx[r] = -(Ji[3 * r] * gr[0] + Ji[3 * r + 1] * gr[1] + Ji[3 * r + 2] * gr[2]);
+            for (int a = 0; a < 3; ++a) x[a] += (X)dx[a];
+            deform(x, d);
+            X gn[3];
+            R dg[3];
             for (int a = 0; a < 3; ++a) {
                 gn[a] = d[a] - xp[a];
-                dg[a] = gn[a] - g[a];
+                dg[a] = (R)(gn[a] - g[a]);
                 g[a] = gn[a];
             }
             iters = k + 1;
@@ -153,10 +170,22 @@ void solve(const Emu<R, G>& E, const double* B12, const double* xpd, int max_ite
             for (int r = 0; r < 3; ++r) jdg[r] = Ji[3 * r] * dg[0] + Ji[3 * r + 1] * dg[1] + Ji[3 * r + 2] * dg[2];
             const R den = dx[0] * jdg[0] + dx[1] * jdg[1] + dx[2] * jdg[2];
             if (rule && std::fabs((double)den) < rule->den_guard) e = true;
+            {
+                const double nd = std::sqrt((double)dx[0] * dx[0] + (double)dx[1] * dx[1] + (double)dx[2] * dx[2]);
+                const double nj = std::sqrt((double)jdg[0] * jdg[0] + (double)jdg[1] * jdg[1] + (double)jdg[2] * jdg[2]);
+                if (nd > 0 && nj > 0) cosmin = std::fmin(cosmin, std::fabs((double)den) / (nd * nj));
+            }
             if (std::fabs(den) > (R)1e-18) {
                 R q[3], w[3];
                 for (int r = 0; r < 3; ++r) q[r] = (dx[r] - jdg[r]) / den;
                 for (int c = 0; c < 3; ++c) w[c] = dx[0] * Ji[c] + dx[1] * Ji[3 + c] + dx[2] * Ji[6 + c];
+                double um = 0, jm = 0;
+                for (int r = 0; r < 3; ++r)
+                    for (int c = 0; c < 3; ++c) {
+                        um = std::fmax(um, std::fabs((double)(q[r] * w[c])));
+                        jm = std::fmax(jm, std::fabs((double)Ji[3 * r + c]));
+                    }
+                if (jm > 0) amp = std::fmax(amp, um / jm);
                 for (int r = 0; r < 3; ++r)
                     for (int c = 0; c < 3; ++c) Ji[3 * r + c] += q[r] * w[c];
             }
@@ -167,12 +196,19 @@ void solve(const Emu<R, G>& E, const double* B12, const double* xpd, int max_ite
     *cv = conv_ok;
     *it = iters;
     if (esc) *esc = e;
+    if (jn) {
+        double m = 0;
+        for (int q = 0; q < 9; ++q) m = std::fmax(m, std::fabs((double)Ji[q]));
+        jn[0] = m;
+        jn[1] = amp;
+        jn[2] = cosmin;
+    }
 }
 
-template <typename R, typename G>
+template <typename R, typename G, typename X = R>
 void run(const double* tg64, int nx, int ny, int nz, const double* bbox, const double* bones, int nb, const double* x,
          int64_t n, int max_iters, double conv, double div, int workers, double* xo, uint8_t* cv, int32_t* it,
-         const EscRule* rule = nullptr, uint8_t* esc = nullptr) {
+         const EscRule* rule = nullptr, uint8_t* esc = nullptr, double* jn = nullptr) {
     const int64_t V = int64_t(nx) * ny * nz;
     std::vector<G> tg(V * 12);
     for (int64_t e = 0; e < V * 12; ++e) tg[e] = (G)tg64[e];
@@ -190,8 +226,8 @@ void run(const double* tg64, int nx, int ny, int nz, const double* bbox, const d
             for (int64_t p = n * w / workers; p < n * (w + 1) / workers; ++p)
                 for (int i = 0; i < nb; ++i) {
                     const int64_t s = p * nb + i;
-                    solve<R, G>(E, bones + 12 * i, x + 3 * p, max_iters, (R)conv, (R)div, xo + 3 * s, cv + s, it + s,
-                                rule, esc ? esc + s : nullptr);
+                    solve<R, G, X>(E, bones + 12 * i, x + 3 * p, max_iters, (X)conv, (X)div, xo + 3 * s, cv + s, it + s,
+                                rule, esc ? esc + s : nullptr, jn ? jn + 3 * s : nullptr);
                 }
         });
     for (auto& t : pool) t.join();
@@ -202,11 +238,13 @@ void run(const double* tg64, int nx, int ny, int nz, const double* bbox, const d
 extern "C" int orc_emul_search(int mode, const double* tgrid, int nx, int ny, int nz, const double* bbox6,
                                const double* bones, int nb, const double* x, int64_t n, int max_iters, double conv,
                                double div, int workers, double* x_c, uint8_t* converged, int32_t* iters) {
-    // mode 0: f64 state, f64 grid; 1: f32 state, f32 grid (the GPU kernel); 2: f64 state, f32 grid
+    // mode 0: f64 state, f64 grid; 1: f32 state, f32 grid (the GPU kernel); 2: f64 state, f32 grid;
+    // 3: f32 trilerp and Broyden algebra, f64 position and residual, f32 grid
     switch (mode) {
         case 0: run<double, double>(tgrid, nx, ny, nz, bbox6, bones, nb, x, n, max_iters, conv, div, workers, x_c, converged, iters); break;
         case 1: run<float, float>(tgrid, nx, ny, nz, bbox6, bones, nb, x, n, max_iters, conv, div, workers, x_c, converged, iters); break;
         case 2: run<double, float>(tgrid, nx, ny, nz, bbox6, bones, nb, x, n, max_iters, conv, div, workers, x_c, converged, iters); break;
+        case 3: run<float, float, double>(tgrid, nx, ny, nz, bbox6, bones, nb, x, n, max_iters, conv, div, workers, x_c, converged, iters); break;
         default: return 1;
     }
     return 0;
@@ -217,7 +255,8 @@ extern "C" int orc_emul_search(int mode, const double* tgrid, int nx, int ny, in
 extern "C" int orc_emul_hybrid(const double* tgrid, int nx, int ny, int nz, const double* bbox6, const double* bones,
                                int nb, const double* x, int64_t n, int max_iters, double conv, double div, int workers,
                                int cap, int min_div_iters, double conv_band, double div_band, double det_guard,
-                               double den_guard, double* x_c, uint8_t* converged, int32_t* iters, uint8_t* esc) {
+                               double den_guard, double* x_c, uint8_t* converged, int32_t* iters, uint8_t* esc,
+                               double* jinv_maxabs, int mixed_state) {
     EscRule r;
     r.cap = cap;
     r.min_div_iters = min_div_iters;
@@ -225,6 +264,9 @@ extern "C" int orc_emul_hybrid(const double* tgrid, int nx, int ny, int nz, cons
     r.div_band = div_band;
     r.det_guard = det_guard;
     r.den_guard = den_guard;
-    run<float, float>(tgrid, nx, ny, nz, bbox6, bones, nb, x, n, max_iters, conv, div, workers, x_c, converged, iters, &r, esc);
+    if (mixed_state)
+        run<float, float, double>(tgrid, nx, ny, nz, bbox6, bones, nb, x, n, max_iters, conv, div, workers, x_c, converged, iters, &r, esc, jinv_maxabs);
+    else
+        run<float, float>(tgrid, nx, ny, nz, bbox6, bones, nb, x, n, max_iters, conv, div, workers, x_c, converged, iters, &r, esc, jinv_maxabs);
     return 0;
 }
