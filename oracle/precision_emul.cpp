@@ -202,6 +202,7 @@ void solve(const Emu<R, G>& E, const double* B12, const double* xpd, int max_ite
         jn[0] = m;
         jn[1] = amp;
         jn[2] = cosmin;
+        for (int q = 0; q < 9; ++q) jn[3 + q] = (double)Ji[q];  // final J~
     }
 }
 
@@ -227,7 +228,7 @@ void run(const double* tg64, int nx, int ny, int nz, const double* bbox, const d
                 for (int i = 0; i < nb; ++i) {
                     const int64_t s = p * nb + i;
                     solve<R, G, X>(E, bones + 12 * i, x + 3 * p, max_iters, (X)conv, (X)div, xo + 3 * s, cv + s, it + s,
-                                rule, esc ? esc + s : nullptr, jn ? jn + 3 * s : nullptr);
+                                rule, esc ? esc + s : nullptr, jn ? jn + 12 * s : nullptr);
                 }
         });
     for (auto& t : pool) t.join();
@@ -256,7 +257,7 @@ extern "C" int orc_emul_hybrid(const double* tgrid, int nx, int ny, int nz, cons
                                int nb, const double* x, int64_t n, int max_iters, double conv, double div, int workers,
                                int cap, int min_div_iters, double conv_band, double div_band, double det_guard,
                                double den_guard, double* x_c, uint8_t* converged, int32_t* iters, uint8_t* esc,
-                               double* jinv_maxabs, int mixed_state) {
+                               double* jinv_diag /* [n][nb][12]: max|J~|, amp, cos_min, J~ */, int mixed_state) {
     EscRule r;
     r.cap = cap;
     r.min_div_iters = min_div_iters;
@@ -265,8 +266,8 @@ extern "C" int orc_emul_hybrid(const double* tgrid, int nx, int ny, int nz, cons
     r.det_guard = det_guard;
     r.den_guard = den_guard;
     if (mixed_state)
-        run<float, float, double>(tgrid, nx, ny, nz, bbox6, bones, nb, x, n, max_iters, conv, div, workers, x_c, converged, iters, &r, esc, jinv_maxabs);
+        run<float, float, double>(tgrid, nx, ny, nz, bbox6, bones, nb, x, n, max_iters, conv, div, workers, x_c, converged, iters, &r, esc, jinv_diag);
     else
-        run<float, float>(tgrid, nx, ny, nz, bbox6, bones, nb, x, n, max_iters, conv, div, workers, x_c, converged, iters, &r, esc, jinv_maxabs);
+        run<float, float>(tgrid, nx, ny, nz, bbox6, bones, nb, x, n, max_iters, conv, div, workers, x_c, converged, iters, &r, esc, jinv_diag);
     return 0;
 }

@@ -10,7 +10,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfsk_b200.so")
+# FSK_LIB: load a tuning-variant build instead (scripts/build_variants.sh); default in-tree.
+LIB_PATH = os.environ.get("FSK_LIB") or os.path.join(HERE, "libfsk_b200.so")
 
 FSK_OK, FSK_EINVAL, FSK_ECUDA, FSK_ENODEV = 0, 1, 2, 3
 FSK_SEARCH_NO_SORT = 0x1

@@ -108,14 +108,21 @@ SearchP make_search(const fsk_search_opts* o) {
     // err^2 within ±2% of conv^2 (f32 residuals near conv carry ~1e-7/3e-5 relative error),
     // within ±2e-4 of div^2, |det J0| < 1e-5 (vs the 1e-8 singular cut), |den| < 1e-12
     // (vs the 1e-18 Broyden guard).
+    // Conditioning (scripts/escalation_rules.py, 72 scenes × 720k solves: without it
+    // max|dx| reached 4.8e-4 on 64^3 / 128x128x32 grids): a converged root with max|J~| > 6
+    // (rounding amplified into x*), or any Broyden update with |cos(dx, J~dg)| < 0.1
+    // (near-degenerate rank-one update). Bands are on err, like the emulator's:
+    // |err/conv - 1| < 2 %, |err/div - 1| < 2e-4.
     s.esc_cap = 8;
     s.esc_min_div = 3;
-    s.esc_conv_lo = 0.98f;
-    s.esc_conv_hi = 1.02f;
-    s.esc_div_lo = 0.9998f;
-    s.esc_div_hi = 1.0002f;
+    s.esc_conv_lo = 0.98f * 0.98f;
+    s.esc_conv_hi = 1.02f * 1.02f;
+    s.esc_div_lo = (1.0f - 2e-4f) * (1.0f - 2e-4f);
+    s.esc_div_hi = (1.0f + 2e-4f) * (1.0f + 2e-4f);
     s.esc_det = 1e-5f;
     s.esc_den = 1e-12f;
+    s.esc_jmax = 6.0f;
+    s.esc_cos2 = 0.1f * 0.1f;
     return s;
 }
 

@@ -50,6 +50,8 @@ struct SearchP {
     float esc_div_lo, esc_div_hi;
     float esc_det;      // |det J0| below this → singular-fallback decision too close to call
     float esc_den;      // |dx·J~dg| below this → Broyden-guard decision too close to call
+    float esc_jmax;     // converged root with max|J~| above this → ill-conditioned, x* not settled in fp32
+    float esc_cos2;     // (dx·J~dg)² < esc_cos2·|dx|²|J~dg|² → near-degenerate rank-one update
 };
 
 template <typename R>
@@ -153,6 +155,48 @@ __device__ __forceinline__ void trilerp_T(const Planes<R>& P, const GridP& g, co
     }
 }
 
+// Register cache of the 8 corners of one cell (4 x-pair edges × 3 rows = 96 values) for the
+// float32 pass: about half of all Broyden re-evaluations land in the cell of the previous
+// evaluation (late iterations take short steps), and those then issue no gather at all.
+// The arithmetic is the same as trilerp_T's, so results are bitwise identical.
+template <typename R>
+struct CellCache {
+    int base;
+    V4<R> a[4][3], b[4][3];  // [edge (dj + 2·dk)][row]: corner di = 0 / 1
+};
+
+template <typename R>
+__device__ __forceinline__ void cache_fill(const Planes<R>& P, const GridP& g, int base, CellCache<R>& C) {
+    const int nxy = g.nx * g.ny;
+    C.base = base;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const int v = base + (e >> 1) * nxy + (e & 1) * g.nx;
+#pragma unroll
+        for (int r = 0; r < 3; ++r) load_edge(P, v, r, C.a[e][r], C.b[e][r]);
+    }
+}
+
+template <typename R>
+__device__ __forceinline__ void trilerp_cached(const CellCache<R>& C, const Cell<R>& c, R T[12]) {
+#pragma unroll
+    for (int e = 0; e < 12; ++e) T[e] = 0;
+#pragma unroll
+    for (int dk = 0; dk < 2; ++dk) {
+        const R wz = dk ? c.tz : (R)1 - c.tz;
+#pragma unroll
+        for (int dj = 0; dj < 2; ++dj) {
+            const R wyz = wz * (dj ? c.ty : (R)1 - c.ty);
+            const R w0 = wyz * ((R)1 - c.tx), w1 = wyz * c.tx;
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+                fma4(T + 4 * r, w0, C.a[2 * dk + dj][r]);
+                fma4(T + 4 * r, w1, C.b[2 * dk + dj][r]);
+            }
+        }
+    }
+}
+
 // d = T·[x;1] on the unclamped x (deformer.cpp:107-113).
 template <typename R>
 __device__ __forceinline__ void apply_T(const R T[12], R x, R y, R z, R d[3]) {
@@ -173,10 +217,11 @@ __device__ __forceinline__ void grad_term(R G[9], R y0, R y1, R y2, R gx, R gy, 
 // T from the locate_cell cell, ∇φ from the locate_cell_lower cell (±1/h stencils); both
 // from one gather unless x lies exactly on an interior face (then the lower cell is
 // gathered again).
-template <typename R>
+template <typename R, bool kCache = false>
 __device__ __forceinline__ void jacobian_and_T(const Planes<R>& P, const GridP& g, R x, R y, R z, R T[12], R J[9],
-                                               bool grad = true) {
+                                               bool grad = true, CellCache<R>* C = nullptr) {
     const Cell<R> c = locate<false, R>(g, x, y, z);
+    if constexpr (kCache) cache_fill(P, g, c.base, *C);
     const Cell<R> cl = locate<true, R>(g, x, y, z);
     const int nxy = g.nx * g.ny;
     const bool same = (c.base == cl.base);
@@ -201,7 +246,12 @@ __device__ __forceinline__ void jacobian_and_T(const Planes<R>& P, const GridP& 
 #pragma unroll
             for (int r = 0; r < 3; ++r) {
                 V4<R> a, b;
-                load_edge(P, v, r, a, b);
+                if constexpr (kCache) {
+                    a = C->a[2 * dk + dj][r];
+                    b = C->b[2 * dk + dj][r];
+                } else {
+                    load_edge(P, v, r, a, b);
+                }
                 fma4(T + 4 * r, w0, a);
                 fma4(T + 4 * r, w1, b);
                 y0[r] = row_dot(a, x, y, z);
@@ -268,9 +318,9 @@ __device__ __forceinline__ R inverse_or_identity(const R J[9], R Ji[9]) {
 // Per-init start of search_one (correspondence.cpp:135-137): x0 = B_i^-1 x' as
 // Rᵀx' + (−Rᵀt) (geometry.hpp:58-61), J~0 = J(x0)^-1 or I (:43-54), and T(x0) for g0.
 // Returns det J(x0).
-template <typename R>
+template <typename R, bool kCache = false>
 __device__ __forceinline__ R solve_init(const Planes<R>& P, const GridP& g, const float* __restrict__ B, R xp0, R xp1,
-                                        R xp2, R& x0, R& x1, R& x2, R Ji[9], R T[12]) {
+                                        R xp2, R& x0, R& x1, R& x2, R Ji[9], R T[12], CellCache<R>* C = nullptr) {
     const R r00 = __ldg(B + 0), r01 = __ldg(B + 1), r02 = __ldg(B + 2), t0 = __ldg(B + 3);
     const R r10 = __ldg(B + 4), r11 = __ldg(B + 5), r12 = __ldg(B + 6), t1 = __ldg(B + 7);
     const R r20 = __ldg(B + 8), r21 = __ldg(B + 9), r22 = __ldg(B + 10), t2 = __ldg(B + 11);
@@ -281,7 +331,7 @@ __device__ __forceinline__ R solve_init(const Planes<R>& P, const GridP& g, cons
     x1 = r01 * xp0 + r11 * xp1 + r21 * xp2 + it1;
     x2 = r02 * xp0 + r12 * xp1 + r22 * xp2 + it2;
     R Jm[9];
-    jacobian_and_T(P, g, x0, x1, x2, T, Jm);
+    jacobian_and_T<R, kCache>(P, g, x0, x1, x2, T, Jm, true, C);
     return inverse_or_identity(Jm, Ji);
 }
 
@@ -299,9 +349,10 @@ struct SolveOut {
 // One Broyden iteration after the divergence check (correspondence.cpp:106-122): step,
 // re-evaluate, and — unless the new residual converged — the good-Broyden rank-one update.
 // Returns true iff converged; `den` receives dx·J~dg (0 when converged).
-template <typename R>
+template <typename R, bool kCache = false>
 __device__ __forceinline__ bool broyden_step(const Planes<R>& P, const GridP& g, R xp0, R xp1, R xp2, R conv2, R& x0,
-                                             R& x1, R& x2, R Ji[9], R& g0, R& g1, R& g2, R& err2, R& den) {
+                                             R& x1, R& x2, R Ji[9], R& g0, R& g1, R& g2, R& err2, R& den,
+                                             CellCache<R>* C = nullptr, R cos2 = 0, bool* degenerate = nullptr) {
     // dx = −J~ g; x += dx (:106-107)
     const R dx0 = -(Ji[0] * g0 + Ji[1] * g1 + Ji[2] * g2);
     const R dx1 = -(Ji[3] * g0 + Ji[4] * g1 + Ji[5] * g2);
@@ -312,7 +363,12 @@ __device__ __forceinline__ bool broyden_step(const Planes<R>& P, const GridP& g,
     // g' = d(x) − x'; dg = g' − g (:108-112)
     R T[12], d[3];
     const Cell<R> c = locate<false, R>(g, x0, x1, x2);
-    trilerp_T(P, g, c, T);
+    if constexpr (kCache) {
+        if (c.base != C->base) cache_fill(P, g, c.base, *C);
+        trilerp_cached(*C, c, T);
+    } else {
+        trilerp_T(P, g, c, T);
+    }
     apply_T(T, x0, x1, x2, d);
     const R n0 = d[0] - xp0, n1 = d[1] - xp1, n2 = d[2] - xp2;
     const R dg0 = n0 - g0, dg1 = n1 - g1, dg2 = n2 - g2;
@@ -327,6 +383,10 @@ __device__ __forceinline__ bool broyden_step(const Planes<R>& P, const GridP& g,
     const R j1 = Ji[3] * dg0 + Ji[4] * dg1 + Ji[5] * dg2;
     const R j2 = Ji[6] * dg0 + Ji[7] * dg1 + Ji[8] * dg2;
     den = dx0 * j0 + dx1 * j1 + dx2 * j2;
+    if (degenerate) {  // float32 pass: |cos(dx, J~dg)| < sqrt(cos2)
+        const R nd = dx0 * dx0 + dx1 * dx1 + dx2 * dx2, nj = j0 * j0 + j1 * j1 + j2 * j2;
+        if (den * den < cos2 * (nd * nj)) *degenerate = true;
+    }
     if (fabs(den) > (R)1e-18) {
         const R inv = (R)1 / den;
         const R q0 = (dx0 - j0) * inv, q1 = (dx1 - j1) * inv, q2 = (dx2 - j2) * inv;
@@ -342,11 +402,12 @@ __device__ __forceinline__ bool broyden_step(const Planes<R>& P, const GridP& g,
 
 // Start of a solve (correspondence.cpp:135-137): x0, J~0 and g0 = d(x0) − x' from one
 // gather. Returns det J(x0).
-template <typename R>
+template <typename R, bool kCache = false>
 __device__ __forceinline__ R solve_start(const Planes<R>& P, const GridP& g, const float* __restrict__ B, R xp0, R xp1,
-                                         R xp2, R& x0, R& x1, R& x2, R Ji[9], R& g0, R& g1, R& g2, R& err2) {
+                                         R xp2, R& x0, R& x1, R& x2, R Ji[9], R& g0, R& g1, R& g2, R& err2,
+                                         CellCache<R>* C = nullptr) {
     R T[12], d[3];
-    const R det = solve_init<R>(P, g, B, xp0, xp1, xp2, x0, x1, x2, Ji, T);
+    const R det = solve_init<R, kCache>(P, g, B, xp0, xp1, xp2, x0, x1, x2, Ji, T, C);
     apply_T(T, x0, x1, x2, d);
     g0 = d[0] - xp0;
     g1 = d[1] - xp1;
@@ -359,7 +420,13 @@ template <typename R, bool kFast>
 __device__ __forceinline__ SolveOut solve_one(const Planes<R>& P, const GridP& g, const float* __restrict__ B, R xp0,
                                               R xp1, R xp2, const SearchP& o, R& x0, R& x1, R& x2, R Ji[9], R& err2) {
     R g0, g1, g2;
-    const R det = solve_start<R>(P, g, B, xp0, xp1, xp2, x0, x1, x2, Ji, g0, g1, g2, err2);
+#ifdef FSK_NO_REGCACHE
+    constexpr bool kCache = false;
+#else
+    constexpr bool kCache = kFast;  // float32 pass: per-thread register cache of the current cell
+#endif
+    CellCache<R> cache;
+    const R det = solve_start<R, kCache>(P, g, B, xp0, xp1, xp2, x0, x1, x2, Ji, g0, g1, g2, err2, &cache);
     const R conv2 = (R)o.conv2, div2 = (R)o.div2;
     bool esc = false;
     auto near = [&](R e2) {
@@ -375,7 +442,8 @@ __device__ __forceinline__ SolveOut solve_one(const Planes<R>& P, const GridP& g
         for (; k < limit; ++k) {
             if (err2 > div2) break;  // divergence check at the top (:105)
             R den;
-            const bool c = broyden_step<R>(P, g, xp0, xp1, xp2, conv2, x0, x1, x2, Ji, g0, g1, g2, err2, den);
+            const bool c = broyden_step<R, kCache>(P, g, xp0, xp1, xp2, conv2, x0, x1, x2, Ji, g0, g1, g2, err2, den,
+                                                   &cache, (R)o.esc_cos2, kFast ? &esc : nullptr);
             iters = k + 1;
             if (kFast && near(err2)) esc = true;
             if (c) {
@@ -387,6 +455,12 @@ __device__ __forceinline__ SolveOut solve_one(const Planes<R>& P, const GridP& g
         // the float32 pass hit its iteration cap before max_iters: the f64 pass decides
         if (kFast && !conv && k == limit && limit < o.max_iters && !(err2 > div2)) esc = true;
         if (kFast && !conv && iters >= o.esc_min_div) esc = true;
+    }
+    if (kFast && conv) {  // ill-conditioned root: float32 rounding is amplified into x*
+        R m = 0;
+#pragma unroll
+        for (int e = 0; e < 9; ++e) m = fmax(m, fabs(Ji[e]));
+        if (m > (R)o.esc_jmax) esc = true;
     }
     return SolveOut{iters, conv, esc};
 }

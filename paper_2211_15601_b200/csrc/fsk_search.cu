@@ -284,9 +284,12 @@ struct SearchPlanes {
     uint8_t* keep;   // dedup survivors
 };
 
-constexpr int kSearchBlock = 256;
+#ifndef FSK_SEARCH_BLOCK
+#define FSK_SEARCH_BLOCK 128
+#endif
+constexpr int kSearchBlock = FSK_SEARCH_BLOCK;
 #ifndef FSK_SEARCH_MINB
-#define FSK_SEARCH_MINB 3  // resident blocks per SM the fast pass's register budget is sized for
+#define FSK_SEARCH_MINB 3  // 128-thread CTAs: 168 registers hold the 96-float cell cache without spills (measured best: 128x3 0.598 ms, 256x1 0.802, 128x4 0.722 with spills, no cache 256x3 0.691)
 #endif
 
 template <typename R>

@@ -1,4 +1,8 @@
-set -x
-python -m pytest tests -m gpu -q -rf -s -k "backward or golden" > gpurun_out/pytest16.log 2>&1
-B="python bench.py --steps 30 --warmup 3 --no-cpu-baseline --no-e2e"
-$B --backward --deterministic > gpurun_out/bench16_c3det.log 2>&1
+# Tuning sweep over build/variants/*.so (scripts/build_variants.py): bitwise-identity hash
+# of the C2 forward outputs and a short bench per variant.
+mkdir -p gpurun_out
+for v in ${VARIANTS:-build/variants/*.so}; do
+  n=$(basename $v .so)
+  FSK_LIB=$v timeout 300 python scripts/variant_hash.py >> gpurun_out/var_hash.log 2>&1
+  FSK_LIB=$v timeout 300 python bench.py --steps 100 --warmup 5 --no-cpu-baseline --no-e2e $BENCH_ARGS > gpurun_out/var_$n.log 2>&1
+done

@@ -46,7 +46,7 @@ def test_library_carries_sm100a_code():
 
 
 def test_search_kernels_register_budget():
-    """The fast pass is sized for FSK_SEARCH_MINB resident CTAs of 256 threads; any local
+    """The fast pass is sized for FSK_SEARCH_MINB resident CTAs of FSK_SEARCH_BLOCK threads; any local
     memory it needs must stay a few words (no large spills on the hot loop)."""
     out = subprocess.run(["cuobjdump", "-res-usage", B.LIB], capture_output=True, text=True, check=True).stdout
     blocks = out.split("Function ")
