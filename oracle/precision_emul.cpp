@@ -128,6 +128,7 @@ void solve(const Emu<R, G>& E, const double* B12, const double* xpd, int max_ite
     R J[9], Ji[9];
     X d[3], g[3];
     double amp = 0, cosmin = 1;  // sensitivity diagnostics: largest relative rank-1 update, smallest |cos(dx, J~dg)|
+    double err_prev = 0, step_last = 0;  // residual before the last step, length of the last step
     {
         const R xr[3] = {(R)x[0], (R)x[1], (R)x[2]};
         E.jacobian(xr, J);
@@ -151,6 +152,8 @@ void solve(const Emu<R, G>& E, const double* B12, const double* xpd, int max_ite
             const R gr[3] = {(R)g[0], (R)g[1], (R)g[2]};
             for (int r = 0; r < 3; ++r) dx[r] = -(Ji[3 * r] * gr[0] + Ji[3 * r + 1] * gr[1] + Ji[3 * r + 2] * gr[2]);
             for (int a = 0; a < 3; ++a) x[a] += (X)dx[a];
+            err_prev = (double)err;
+            step_last = std::sqrt((double)dx[0] * dx[0] + (double)dx[1] * dx[1] + (double)dx[2] * dx[2]);
             deform(x, d);
             X gn[3];
             R dg[3];
@@ -203,6 +206,16 @@ void solve(const Emu<R, G>& E, const double* B12, const double* xpd, int max_ite
         jn[1] = amp;
         jn[2] = cosmin;
         for (int q = 0; q < 9; ++q) jn[3 + q] = (double)Ji[q];  // final J~
+        double nx = 0;  // |J~ g| at the end: the step a further iteration would take
+        for (int r = 0; r < 3; ++r) {
+            const double v = (double)Ji[3 * r] * (double)g[0] + (double)Ji[3 * r + 1] * (double)g[1] +
+                             (double)Ji[3 * r + 2] * (double)g[2];
+            nx += v * v;
+        }
+        jn[12] = (double)err / (double)conv;
+        jn[13] = std::sqrt(nx) / (double)conv;
+        jn[14] = err_prev / (double)conv;
+        jn[15] = step_last / (double)conv;
     }
 }
 
@@ -228,7 +241,7 @@ void run(const double* tg64, int nx, int ny, int nz, const double* bbox, const d
                 for (int i = 0; i < nb; ++i) {
                     const int64_t s = p * nb + i;
                     solve<R, G, X>(E, bones + 12 * i, x + 3 * p, max_iters, (X)conv, (X)div, xo + 3 * s, cv + s, it + s,
-                                rule, esc ? esc + s : nullptr, jn ? jn + 12 * s : nullptr);
+                                rule, esc ? esc + s : nullptr, jn ? jn + 16 * s : nullptr);
                 }
         });
     for (auto& t : pool) t.join();
@@ -257,7 +270,7 @@ extern "C" int orc_emul_hybrid(const double* tgrid, int nx, int ny, int nz, cons
                                int nb, const double* x, int64_t n, int max_iters, double conv, double div, int workers,
                                int cap, int min_div_iters, double conv_band, double div_band, double det_guard,
                                double den_guard, double* x_c, uint8_t* converged, int32_t* iters, uint8_t* esc,
-                               double* jinv_diag /* [n][nb][12]: max|J~|, amp, cos_min, J~ */, int mixed_state) {
+                               double* jinv_diag /* [n][nb][16]: max|J~|, amp, cos_min, J~, err/conv, |J~g|/conv, err_prev/conv, |dx_last|/conv */, int mixed_state) {
     EscRule r;
     r.cap = cap;
     r.min_div_iters = min_div_iters;

@@ -123,6 +123,12 @@ SearchP make_search(const fsk_search_opts* o) {
     s.esc_den = 1e-12f;
     s.esc_jmax = 6.0f;
     s.esc_cos2 = 0.1f * 0.1f;
+    // Step rule (scripts/band_study.py on the GPU, 30 scenes × 720k solves: converged solves
+    // whose iteration count differed from the oracle's by one had the float32 err/conv as low
+    // as 0.84 on one side and the oracle's as high as 0.93 on the other; the roots then differ
+    // by one step, up to 4·conv): rho = 0.7, tau = 2 (a one-step difference stays < 2·conv).
+    s.esc_rho2 = 0.7f * 0.7f;
+    s.esc_tau2 = 2.0f * 2.0f;
     return s;
 }
 

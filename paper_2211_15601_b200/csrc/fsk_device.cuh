@@ -52,6 +52,8 @@ struct SearchP {
     float esc_den;      // |dx·J~dg| below this → Broyden-guard decision too close to call
     float esc_jmax;     // converged root with max|J~| above this → ill-conditioned, x* not settled in fp32
     float esc_cos2;     // (dx·J~dg)² < esc_cos2·|dx|²|J~dg|² → near-degenerate rank-one update
+    float esc_rho2;     // step rule: the stop decision is "near" when err² ∈ [rho², 1/rho²]·conv² ...
+    float esc_tau2;     // ... and the step it decides (taken or not) is longer than tau·conv
 };
 
 template <typename R>
@@ -435,12 +437,19 @@ __device__ __forceinline__ SolveOut solve_one(const Planes<R>& P, const GridP& g
     };
     if (kFast) esc = fabs(det) < (R)o.esc_det || near(err2);
     int iters = 0;
+    R xl0 = x0, xl1 = x1, xl2 = x2, e2l = 0;  // float32 pass: position and err² before the last step
     bool conv = err2 < conv2;  // (:100-103)
     if (!conv) {
         const int limit = kFast ? min(o.max_iters, o.esc_cap) : o.max_iters;
         int k = 0;
         for (; k < limit; ++k) {
             if (err2 > div2) break;  // divergence check at the top (:105)
+            if (kFast) {
+                xl0 = x0;
+                xl1 = x1;
+                xl2 = x2;
+                e2l = err2;
+            }
             R den;
             const bool c = broyden_step<R, kCache>(P, g, xp0, xp1, xp2, conv2, x0, x1, x2, Ji, g0, g1, g2, err2, den,
                                                    &cache, (R)o.esc_cos2, kFast ? &esc : nullptr);
@@ -461,6 +470,21 @@ __device__ __forceinline__ SolveOut solve_one(const Planes<R>& P, const GridP& g
 #pragma unroll
         for (int e = 0; e < 9; ++e) m = fmax(m, fabs(Ji[e]));
         if (m > (R)o.esc_jmax) esc = true;
+        // Step rule: a float64 solve may stop one Broyden step earlier or later than this one
+        // when a stop decision sat near conv; the roots then differ by that step. Escalate if
+        // the step in question is long: |J~g| (the next step) when err ≥ rho·conv, or the last
+        // step when the previous err ≤ conv/rho.
+        const R tau2 = (R)o.esc_tau2 * conv2;
+        if (err2 >= (R)o.esc_rho2 * conv2) {
+            const R s0 = Ji[0] * g0 + Ji[1] * g1 + Ji[2] * g2;
+            const R s1 = Ji[3] * g0 + Ji[4] * g1 + Ji[5] * g2;
+            const R s2 = Ji[6] * g0 + Ji[7] * g1 + Ji[8] * g2;
+            if (s0 * s0 + s1 * s1 + s2 * s2 > tau2) esc = true;
+        }
+        if (iters > 0 && e2l * (R)o.esc_rho2 <= conv2) {
+            const R d0 = x0 - xl0, d1 = x1 - xl1, d2 = x2 - xl2;
+            if (d0 * d0 + d1 * d1 + d2 * d2 > tau2) esc = true;
+        }
     }
     return SolveOut{iters, conv, esc};
 }

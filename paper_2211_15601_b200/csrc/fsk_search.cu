@@ -376,7 +376,10 @@ __global__ void __launch_bounds__(128, FSK_ESC_MINB) k_search_escalated(Planes<d
     // Idle lanes are refilled in batches (>= kRefillIdle idle, or the whole warp), so the
     // divergent init path (x0, Jacobian stencil, inverse) runs for many lanes at once and the
     // iteration trips — the bulk of the work — run with most lanes active.
-    constexpr int kRefillIdle = 12;
+#ifndef FSK_REFILL_IDLE
+#define FSK_REFILL_IDLE 12
+#endif
+    constexpr int kRefillIdle = FSK_REFILL_IDLE;
     int buf_idx = 0, bused = 32;
     bool dry = false;
     while (true) {

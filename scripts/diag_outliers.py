@@ -9,7 +9,8 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from precision_study import S, hybrid, oracle  # noqa: E402
-from tests.test_gpu_parity import run_gpu  # noqa: E402
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
+from test_gpu_parity import run_gpu  # noqa: E402
 from paper_2211_15601_b200.deformer import Deformer  # noqa: E402
 
 dims = tuple(int(a) for a in sys.argv[1:4])

@@ -29,10 +29,11 @@ def collect(cap, seeds, n):
             xo, cv, it, esc, jn = hybrid(sc, tg, o, cap)
             nb = sc.n_bones
             dx = np.abs(xo - ref["x_c"]).max(-1).ravel()
-            dj = np.abs(jn[..., 3:] - ref["jinv"].reshape(n, nb, 9)).max(-1).ravel()
+            dj = np.abs(jn[..., 3:12] - ref["jinv"].reshape(n, nb, 9)).max(-1).ravel()
             rows.append(dict(dims=dims, pts=pts, seed=seed, esc=esc.ravel() != 0, cv=cv.ravel(),
                              rc=ref["converged"].ravel(), dx=dx, dj=dj, jmax=jn[..., 0].ravel(),
-                             cos=jn[..., 2].ravel()))
+                             cos=jn[..., 2].ravel(), e=jn[..., 12].ravel(), s_next=jn[..., 13].ravel(),
+                             e_prev=jn[..., 14].ravel(), s_last=jn[..., 15].ravel()))
             r = rows[-1]
             both = ~r["esc"] & (r["cv"] == 1) & (r["rc"] == 1)
             print(f"{dims} {pts:8s} seed {seed}: esc {r['esc'].mean()*100:.2f}%  flips "

@@ -29,7 +29,7 @@ def hybrid(sc, tg, o, cap, min_div=3, mixed=0, workers=8):
     B = np.ascontiguousarray(sc.bones, np.float64)
     bb = np.ascontiguousarray(sc.bbox, np.float64)
     xo, cv = np.zeros((n, nb, 3)), np.zeros((n, nb), np.uint8)
-    it, esc, jn = np.zeros((n, nb), np.int32), np.zeros((n, nb), np.uint8), np.zeros((n, nb, 12))
+    it, esc, jn = np.zeros((n, nb), np.int32), np.zeros((n, nb), np.uint8), np.zeros((n, nb, 16))
     L.orc_emul_hybrid(P(tg), *sc.dims, P(bb), P(B), nb, P(x), n, o["max_iters"], o["conv_eps"], o["div_eps"], workers,
                       cap, min_div, 0.02, 2e-4, 1e-5, 1e-12, P(xo), P(cv, _u8), P(it, _i32), P(esc, _u8), P(jn), mixed)
     return xo, cv, it, esc, jn
