@@ -346,6 +346,7 @@ struct SolveOut {
     int iters;
     bool conv;
     bool esc;
+    bool capped;  // escalated because the float32 pass hit its iteration cap (a long trajectory)
 };
 
 // One Broyden iteration after the divergence check (correspondence.cpp:106-122): step,
@@ -430,7 +431,7 @@ __device__ __forceinline__ SolveOut solve_one(const Planes<R>& P, const GridP& g
     CellCache<R> cache;
     const R det = solve_start<R, kCache>(P, g, B, xp0, xp1, xp2, x0, x1, x2, Ji, g0, g1, g2, err2, &cache);
     const R conv2 = (R)o.conv2, div2 = (R)o.div2;
-    bool esc = false;
+    bool esc = false, capped = false;
     auto near = [&](R e2) {
         return (e2 >= (R)o.esc_conv_lo * conv2 && e2 <= (R)o.esc_conv_hi * conv2) ||
                (e2 >= (R)o.esc_div_lo * div2 && e2 <= (R)o.esc_div_hi * div2);
@@ -462,7 +463,7 @@ __device__ __forceinline__ SolveOut solve_one(const Planes<R>& P, const GridP& g
             if (kFast && fabs(den) < (R)o.esc_den) esc = true;
         }
         // the float32 pass hit its iteration cap before max_iters: the f64 pass decides
-        if (kFast && !conv && k == limit && limit < o.max_iters && !(err2 > div2)) esc = true;
+        if (kFast && !conv && k == limit && limit < o.max_iters && !(err2 > div2)) esc = capped = true;
         if (kFast && !conv && iters >= o.esc_min_div) esc = true;
     }
     if (kFast && conv) {  // ill-conditioned root: float32 rounding is amplified into x*
@@ -486,7 +487,7 @@ __device__ __forceinline__ SolveOut solve_one(const Planes<R>& P, const GridP& g
             if (d0 * d0 + d1 * d1 + d2 * d2 > tau2) esc = true;
         }
     }
-    return SolveOut{iters, conv, esc};
+    return SolveOut{iters, conv, esc, capped};
 }
 
 }  // namespace fsk
