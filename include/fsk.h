@@ -205,6 +205,30 @@ int fsk_search_bwd_roots(fsk_ctx* ctx, const fsk_grid_desc* desc, const fsk_root
 int fsk_grad_weights(fsk_ctx* ctx, const fsk_grid_desc* desc, const float* grad_tgrid,
                      const float* bones, int32_t n_bones_pose, float* grad_w, void* stream);
 
+/* ---- MLP stages next to the search, tcgen05 tensor cores, 3xTF32 (FP32-faithful).
+ * theta: the network's flat parameter vector in Mlp::parameters() order (mlp.cpp:207-219: per
+ * layer W column-major [out x in], then b), float32, device. widths: host array {in, H, ..., out}
+ * with every hidden width equal to H in {64, 128}; softplus hidden units, linear head
+ * (Mlp::forward, mlp.cpp:115-138). */
+
+/* distill (skinning.cpp:195-221): weights [V][n_b] (dev, float32) = softmax(net(vertex_position(v)))
+ * over the grid of desc (vertex_position, skinning.cpp:77-80). widths = {3, H.., n_b}, n_b <= 64
+ * and == desc->n_bones. Replaces fskin::distill(const SkinningMlp&, GridDims, const Aabb&). */
+int fsk_distill(fsk_ctx* ctx, const float* theta, const int32_t* widths, int32_t n_widths,
+                const fsk_grid_desc* desc, float* weights, void* stream);
+
+/* posed_occupancy_batch (shape.cpp:242-269) over CorrespondenceSets on the device: for query q,
+ * pred[q] = max over roots r in [offsets[q], offsets[q+1]) of sigmoid(net(roots[r].x, pose))
+ * (OccupancyMlp::occupancy_batch, shape.cpp:218-228) and argmax[q] = r - offsets[q] of the first
+ * maximum, -1 (pred 0) for an empty set. widths = {3 + n_pose, H.., 1}. n_roots = offsets[n].
+ * argmax and occ_per_root ([n_roots], per-root occupancy) may be NULL. All device buffers.
+ * Replaces fskin::posed_occupancy_batch(std::span<const CorrespondenceSet>, const OccupancyMlp&,
+ * const VectorXd&, std::vector<int>*). */
+int fsk_posed_occupancy(fsk_ctx* ctx, const float* theta, const int32_t* widths, int32_t n_widths,
+                        const float* pose, int32_t n_pose, const int64_t* offsets, const fsk_root* roots,
+                        int64_t n, int64_t n_roots, float* pred, int32_t* argmax, float* occ_per_root,
+                        void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -26,8 +26,8 @@ _int = ctypes.c_int
 
 
 def build(force: bool = False) -> str:
-    src = os.path.join(_HERE, "fskin_oracle.cpp")
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(src):
+    srcs = [os.path.join(_HERE, f) for f in ("fskin_oracle.cpp", "precision_emul.cpp", "mlp_oracle.cpp", "Makefile")]
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(os.path.getmtime(s) for s in srcs):
         subprocess.run(["make", "-s", "-C", _HERE], check=True)
     return _LIB
 
@@ -48,6 +48,13 @@ def lib():
         L.orc_dedup_roots.argtypes = [_d, _int, ctypes.c_double, _u8]
         L.orc_grid_vjp.argtypes = [_int, _int, _int, _int, _d, _d, _d, _d, _d, _i32, _i64, _d, _d]
         L.orc_implicit_u_exact.argtypes = [_d, _int, _int, _int, _int, _d, _d, _d, _d, _i64, _d, _u8]
+        L.orc_mlp_last_error.restype = ctypes.c_char_p
+        _pi = ctypes.POINTER(ctypes.c_int)
+        _pi64 = ctypes.POINTER(ctypes.c_int64)
+        L.orc_mlp_forward.argtypes = [_d, _pi, _int, _d, _i64, _d, _int]
+        L.orc_distill.argtypes = [_d, _pi, _int, _int, _int, _int, _d, _d, _int]
+        L.orc_distill_vjp.argtypes = [_d, _pi, _int, _int, _int, _int, _d, _d, _d, _int]
+        L.orc_posed_occupancy.argtypes = [_d, _pi, _int, _d, _int, _pi64, _d, _i64, _d, _i32, _int]
         _lib = L
     return _lib
 
@@ -153,3 +160,69 @@ def implicit_u_exact(weights, dims, bbox, bones, x_star, v):
     u, ok = np.zeros((n, 3)), np.zeros(n, np.uint8)
     _check(lib().orc_implicit_u_exact(_p(w), *dims, w.shape[1], _p(bb), _p(B), _p(xs), _p(v), n, _p(u), _p(ok, _u8)))
     return u, ok
+
+
+# ---------------------------------------------------------------- MLP stages
+def _mlp_check(rc):
+    if rc != 0:
+        msg = lib().orc_mlp_last_error().decode()
+        raise (OracleInvalidArgument if rc == 1 else OracleError)(msg)
+
+
+def _widths(widths):
+    return (ctypes.c_int * len(widths))(*widths)
+
+
+def mlp_param_count(widths):
+    return sum(widths[l + 1] * widths[l] + widths[l + 1] for l in range(len(widths) - 1))
+
+
+def mlp_init(widths, seed=0, head_scale=1.0):
+    """Seeded fan-in-scaled normal init (mlp.cpp:97-110 recipe; numpy stream, not mt19937),
+    flattened in Mlp::parameters() order: per layer W column-major, then b (mlp.cpp:207-219).
+    Biases get a small random value so the bias path is exercised."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for l in range(len(widths) - 1):
+        W = rng.normal(0.0, np.sqrt(2.0 / widths[l]), (widths[l + 1], widths[l]))
+        b = rng.normal(0.0, 0.05, widths[l + 1])
+        if l == len(widths) - 2:
+            W, b = W * head_scale, b * head_scale
+        out += [W.reshape(-1, order="F"), b]
+    return np.concatenate(out)
+
+
+def mlp_forward(theta, widths, X, workers=8):
+    X = _f64(X).reshape(-1, widths[0])
+    out = np.zeros((X.shape[0], widths[-1]))
+    _mlp_check(lib().orc_mlp_forward(_p(_f64(theta)), _widths(widths), len(widths), _p(X), X.shape[0], _p(out), workers))
+    return out
+
+
+def distill(theta, widths, dims, bbox, workers=8):
+    """distill (skinning.cpp:195-221) -> weights [V, nb] float64."""
+    nx, ny, nz = dims
+    out = np.zeros((nx * ny * nz, widths[-1]))
+    _mlp_check(lib().orc_distill(_p(_f64(theta)), _widths(widths), len(widths), nx, ny, nz, _p(_f64(bbox)),
+                                 _p(out), workers))
+    return out
+
+
+def distill_vjp(theta, widths, dims, bbox, dw, workers=8):
+    nx, ny, nz = dims
+    out = np.zeros(mlp_param_count(widths))
+    _mlp_check(lib().orc_distill_vjp(_p(_f64(theta)), _widths(widths), len(widths), nx, ny, nz, _p(_f64(bbox)),
+                                     _p(_f64(dw)), _p(out), workers))
+    return out
+
+
+def posed_occupancy(theta, widths, pose, offsets, roots_x, workers=8):
+    """posed_occupancy_batch (shape.cpp:242-269) -> (pred [n], argmax [n] int32)."""
+    offs = np.ascontiguousarray(offsets, dtype=np.int64)
+    n = offs.shape[0] - 1
+    pose = _f64(pose if pose is not None else np.zeros(0))
+    pred, am = np.zeros(n), np.zeros(n, np.int32)
+    _mlp_check(lib().orc_posed_occupancy(_p(_f64(theta)), _widths(widths), len(widths), _p(pose), pose.shape[0],
+                                         offs.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                         _p(_f64(roots_x).reshape(-1, 3)), n, _p(pred), _p(am, _i32), workers))
+    return pred, am

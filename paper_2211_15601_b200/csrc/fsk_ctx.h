@@ -47,6 +47,7 @@ enum Slot {
     kBwdStart, kBwdCell, kBwdRec, kPeakTable,
     kOXr, kOJa, kOJb, kOJc, kOMeta, kOKeep, kNRoots, kOffs, kRootsTmp,
     kHW, kHB, kHP, kHT, kHOffs, kHRoots,
+    kMlpPack, kMlpWidths, kMlpOcc,
     kSlotCount
 };
 static_assert(kSlotCount <= fsk_ctx::kSlots, "scratch slots");

@@ -310,6 +310,39 @@ class Deformer:
                                       _ptr(_f32(bones, "bones", self.device)), nb, _ptr(out), _stream(self.device)))
         return out
 
+    # ---------------------------------------------------------------- MLP stages
+    @staticmethod
+    def _widths(widths):
+        return (ctypes.c_int32 * len(widths))(*[int(w) for w in widths])
+
+    def distill(self, theta, widths, dims, bbox, out=None):
+        """``distill`` (skinning.cpp:195-221): skinning-network softmax weights [V, n_b] at the
+        grid vertices. ``theta``: the flat Mlp::parameters() vector (mlp.cpp:207-219)."""
+        nb = int(widths[-1])
+        desc = grid_desc(dims, bbox, nb)
+        V = desc.nx * desc.ny * desc.nz
+        if out is None:
+            out = torch.empty((V, nb), dtype=torch.float32, device=self.device)
+        check(self.L.fsk_distill(self._ctx, _ptr(_f32(theta, "theta", self.device)), self._widths(widths), len(widths),
+                                 ctypes.byref(desc), _ptr(out), _stream(self.device)))
+        return out
+
+    def posed_occupancy(self, theta, widths, pose, offsets, roots, occ_per_root=None):
+        """``posed_occupancy_batch`` (shape.cpp:242-269) over device CorrespondenceSets
+        (offsets [N+1] int64, roots [M,16] fsk_root records): returns (pred [N], argmax [N])."""
+        n = offsets.shape[0] - 1
+        n_roots = int(offsets[-1].item()) if n >= 0 else 0
+        pose_t = None
+        if pose is not None and len(pose) > 0:
+            pose_t = torch.as_tensor(pose, dtype=torch.float32).to(self.device).contiguous()
+        n_pose = 0 if pose_t is None else pose_t.numel()
+        pred = torch.empty((max(n, 0),), dtype=torch.float32, device=self.device)
+        am = torch.empty((max(n, 0),), dtype=torch.int32, device=self.device)
+        check(self.L.fsk_posed_occupancy(self._ctx, _ptr(_f32(theta, "theta", self.device)), self._widths(widths),
+                                         len(widths), _ptr(pose_t), n_pose, _ptr(offsets), _ptr(roots), n, n_roots,
+                                         _ptr(pred), _ptr(am), _ptr(occ_per_root), _stream(self.device)))
+        return pred, am
+
     # ---------------------------------------------------------------- end to end (host buffers)
     def deform_host(self, weights, dims, bbox, bones, points, opts: SearchOptions, offsets, roots):
         """``fsk_deform_host``: host (pinned) buffers in, CorrespondenceSets out. Returns the

@@ -1,1 +1,1 @@
-timeout 900 python -m pytest tests -m gpu -q -rf -x > gpurun_out/pytest_esc.log 2>&1; python scripts/variant_hash.py > gpurun_out/hash.log 2>&1; timeout 300 python bench.py --steps 100 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/bench_esc.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_mlp.py -q -rf -s -x > gpurun_out/pytest_mlp.log 2>&1

@@ -372,3 +372,65 @@ def test_implicit_grad_approx_cosine_and_one_hot_exact():
     ue, _ = oracle.implicit_u_exact(w, DIMS, BBOX, B, rr["x_c"][:, 0], vv)
     ua = -np.einsum("nij,ni->nj", rr["jinv"][:, 0], vv)
     np.testing.assert_allclose(ua, ue, atol=1e-10)
+
+
+# ---------------------------------------------------------------- MLP stages
+def _np_mlp(theta, widths, X):
+    """numpy f64 Mlp::forward (mlp.cpp:115-138) on Mlp::parameters() order (mlp.cpp:207-219)."""
+    off, h = 0, np.asarray(X, np.float64)
+    for l in range(len(widths) - 1):
+        n_in, n_out = widths[l], widths[l + 1]
+        W = theta[off:off + n_in * n_out].reshape(n_in, n_out).T  # column-major storage
+        off += n_in * n_out
+        b = theta[off:off + n_out]
+        off += n_out
+        z = h @ W.T + b
+        h = (np.maximum(z, 0) + np.log1p(np.exp(-np.abs(z)))) if l + 2 < len(widths) else z
+    return h
+
+
+def test_oracle_mlp_forward_and_distill_match_numpy():
+    widths = [3, 64, 64, 64, 24]
+    th = oracle.mlp_init(widths, 4, 0.05)
+    X = np.random.default_rng(0).uniform(-1, 1, (50, 3))
+    assert np.allclose(oracle.mlp_forward(th, widths, X), _np_mlp(th, widths, X), rtol=0, atol=1e-12)
+    bbox = np.array([-1.0, -0.5, -0.25, 1.0, 2.0, 0.25])
+    dims = (5, 4, 3)
+    W = oracle.distill(th, widths, dims, bbox)
+    g = np.stack(np.meshgrid(*[np.linspace(bbox[a], bbox[3 + a], dims[a]) for a in range(3)], indexing="ij"), -1)
+    V = g.transpose(2, 1, 0, 3).reshape(-1, 3)  # x fastest (skinning.cpp:72-80 vertex order)
+    z = _np_mlp(th, widths, V)
+    e = np.exp(z - z.max(1, keepdims=True))
+    assert np.allclose(W, e / e.sum(1, keepdims=True), rtol=0, atol=1e-12)
+
+
+def test_oracle_distill_vjp_matches_finite_differences():
+    widths = [3, 8, 8, 5]
+    th = oracle.mlp_init(widths, 2)
+    dims, bbox = (3, 3, 2), np.array([0.0, 0.0, 0.0, 1.0, 1.0, 1.0])
+    dw = np.random.default_rng(1).normal(size=(18, 5))
+    g = oracle.distill_vjp(th, widths, dims, bbox, dw)
+    rng = np.random.default_rng(3)
+    for i in rng.choice(len(th), 12, replace=False):
+        e = np.zeros_like(th)
+        e[i] = 1e-6
+        fd = ((oracle.distill(th + e, widths, dims, bbox) - oracle.distill(th - e, widths, dims, bbox)) * dw).sum() / 2e-6
+        assert abs(fd - g[i]) <= 1e-6 * max(1.0, abs(fd))
+
+
+def test_oracle_posed_occupancy_semantics():
+    """max over each set's roots, first root wins ties, empty set -> (0, -1) (shape.cpp:242-269)."""
+    widths = [3, 16, 16, 1]
+    th = oracle.mlp_init(widths, 7)
+    x = np.random.default_rng(5).uniform(-1, 1, (6, 3))
+    x[4] = x[3]  # a tie inside set 2
+    offs = np.array([0, 2, 2, 5, 6])
+    pred, am = oracle.posed_occupancy(th, widths, None, offs, x)
+    occ = 1 / (1 + np.exp(-_np_mlp(th, widths, x)[:, 0]))
+    assert am[1] == -1 and pred[1] == 0.0
+    for q, (a, b) in enumerate(zip(offs[:-1], offs[1:])):
+        if b > a:
+            assert pred[q] == pytest.approx(occ[a:b].max(), abs=1e-14)
+            assert am[q] == int(np.argmax(occ[a:b]))  # numpy argmax = first maximum
+    with pytest.raises(oracle.OracleInvalidArgument, match="pose vector length 1, field conditioned on 0"):
+        oracle.posed_occupancy(th, widths, np.zeros(1), offs, x)
