@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--no-sort", action="store_true", help="ablation: no spatial ordering")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-mlp", action="store_true", help="skip the MLP-stage measurements (SURVEY 8(f))")
     ap.add_argument("--poses", type=int, default=1, help="poses per step (C4: 16 poses x 1M points, 64^3 grid)")
     ap.add_argument("--backward", action="store_true", help="C3: add the implicit-diff backward to each frame")
     ap.add_argument("--deterministic", action="store_true", help="backward with int64 fixed-point accumulation")
@@ -376,6 +377,8 @@ def run_ours(args, rank, world, local_rank):
         "clocks": clk,
     }
 
+    if rank == 0 and not args.no_mlp:
+        line["mlp_stages"] = mlp_stages(D, sc, roots_buf, n, dev)
     if rank == 0 and not args.no_e2e:
         line["e2e"] = e2e_ours(D, sc, opts, args)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -387,6 +390,71 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0:
         print(json.dumps(line), flush=True)
     D.close()
+
+
+SKIN_WIDTHS = [3, 64, 64, 64, 24]   # SkinningMlp (skinning.cpp:10-17)
+OCC_WIDTHS = [3, 128, 128, 128, 1]   # OccupancyMlp (shape.cpp:181-184)
+
+
+def mlp_stages(D, sc, roots_buf, n, dev, reps=20):
+    """SURVEY §8(f) rows 1-2 on the tensor cores: distill (skinning net at every grid vertex,
+    C2 grid and the training loop's 32x32x8 grid, diff.hpp:106) and the occupancy query over
+    this step's CorrespondenceSets (posed_occupancy_batch). Random-init float32 parameters.
+    Flops are algorithmic (2·Σ w_l·w_l+1 per row, one pass; the 3xTF32 split issues 3x)."""
+    import torch
+
+    import oracle
+    peak_bf16 = None
+    try:
+        peak_bf16 = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"]
+    except Exception:
+        pass
+    peak_tf32 = (peak_bf16 / 2) if peak_bf16 else 1125.0  # dense TF32 = half the BF16 rate
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    def flops_per_row(w):
+        return 2 * sum(w[i] * w[i + 1] for i in range(len(w) - 1))
+
+    out = {"precision": "3xTF32 split on tcgen05 (FP32-faithful, max err vs f64 ~1e-6)",
+           "tensor_peak_TFLOPs": peak_tf32,
+           "peak_source": "MEASURED_PEAKS.json bf16_tflops / 2 (dense TF32 rate)" if peak_bf16 else
+                          "nominal B200 dense TF32"}
+    th_s = torch.from_numpy(oracle.mlp_init(SKIN_WIDTHS, 1, 0.05).astype(np.float32)).to(dev)
+    for dims in ((32, 32, 32), (32, 32, 8), (64, 64, 64)):
+        V = dims[0] * dims[1] * dims[2]
+        wout = torch.empty((V, SKIN_WIDTHS[-1]), dtype=torch.float32, device=dev)
+        ms = timed(lambda: D.distill(th_s, SKIN_WIDTHS, dims, sc.bbox, out=wout))
+        f = flops_per_row(SKIN_WIDTHS) * V
+        out[f"distill_{dims[0]}x{dims[1]}x{dims[2]}"] = {
+            "ms": ms, "vertices_per_s": V / (ms * 1e-3), "achieved_TFLOPs": f / (ms * 1e-3) / 1e12,
+            "frac_of_3xTF32_peak": 3 * f / (ms * 1e-3) / 1e12 / peak_tf32}
+    offs, roots = roots_buf[0][: n + 1], roots_buf[1]
+    n_roots = int(offs[-1].item())
+    th_o = torch.from_numpy(oracle.mlp_init(OCC_WIDTHS, 2).astype(np.float32)).to(dev)
+    ms = timed(lambda: D.posed_occupancy(th_o, OCC_WIDTHS, None, offs, roots))
+    f = flops_per_row(OCC_WIDTHS) * n_roots
+    out["posed_occupancy"] = {"queries": n, "roots": n_roots, "ms": ms, "roots_per_s": n_roots / (ms * 1e-3),
+                              "achieved_TFLOPs": f / (ms * 1e-3) / 1e12,
+                              "frac_of_3xTF32_peak": 3 * f / (ms * 1e-3) / 1e12 / peak_tf32}
+    # the reference path on the host cores (oracle f64 restatement), bounded sample
+    m = min(n_roots, 20000)
+    rx = roots[:m, :3].cpu().numpy().astype(np.float64)
+    t0 = time.perf_counter()
+    oracle.mlp_forward(oracle.mlp_init(OCC_WIDTHS, 2), OCC_WIDTHS, rx, workers=os.cpu_count() or 1)
+    dt = time.perf_counter() - t0
+    out["posed_occupancy"]["cpu_baseline_roots_per_s"] = m / dt
+    out["posed_occupancy"]["cpu_sample"] = f"{m} roots, f64 oracle Mlp::forward, {os.cpu_count()} threads"
+    return out
 
 
 def e2e_ours(D, sc, opts, args, steps=None):

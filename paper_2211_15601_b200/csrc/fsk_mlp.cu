@@ -92,7 +92,9 @@ __device__ __forceinline__ float tf32_hi(float x) {
 }
 
 // softplus (mlp.cpp:10-13) and sigmoid (:15-21) in FP32
-__device__ __forceinline__ float softplus_f(float x) { return fmaxf(x, 0.f) + log1pf(__expf(-fabsf(x))); }
+// MUFU ex2/lg2 forms: abs error ~5e-7 (log of an argument in [1, 2]); for large |x| the
+// log term underflows to 0 where the exact value is < 6e-8.
+__device__ __forceinline__ float softplus_f(float x) { return fmaxf(x, 0.f) + __logf(1.f + __expf(-fabsf(x))); }
 __device__ __forceinline__ float sigmoid_f(float x) {
     if (x >= 0.f) return 1.f / (1.f + __expf(-x));
     const float e = __expf(x);
@@ -160,25 +162,32 @@ MlpShape mlp_shape(const int32_t* widths, int nw, bool softmax_head) {
     return s;
 }
 
+constexpr int kMaxWidths = 32;
+
 struct MlpDev {
     int K0, H, n_out, NP, n_hidden, softmax;
     int64_t off_W0, off_b0, off_hidden, off_head, hidden_stride_al;
+    int nw;
+    int widths[kMaxWidths];  // by value: no host→device copy per call
 };
 
-MlpDev to_dev(const MlpShape& s) {
-    return MlpDev{s.K0, s.H, s.n_out, s.NP, s.n_hidden, s.softmax_head ? 1 : 0, s.off_W0, s.off_b0, s.off_hidden,
-                  s.off_head, (s.hidden_stride() + 31) / 32 * 32};
+MlpDev to_dev(const MlpShape& s, const int32_t* widths, int nw) {
+    MlpDev d{s.K0, s.H, s.n_out, s.NP, s.n_hidden, s.softmax_head ? 1 : 0, s.off_W0, s.off_b0, s.off_hidden,
+             s.off_head, (s.hidden_stride() + 31) / 32 * 32, nw, {}};
+    for (int i = 0; i < nw; ++i) d.widths[i] = widths[i];
+    return d;
 }
 
 // theta offsets of layer l in Mlp::parameters() order
-__device__ inline int64_t theta_off(const int32_t* w, int l) {
+__device__ inline int64_t theta_off(const int* w, int l) {
     int64_t o = 0;
     for (int i = 0; i < l; ++i) o += (int64_t)w[i + 1] * w[i] + w[i + 1];
     return o;
 }
 
-__global__ void k_mlp_pack(const float* __restrict__ theta, const int32_t* __restrict__ widths, int nw, MlpDev m,
-                           float* __restrict__ pk) {
+__global__ void k_mlp_pack(const float* __restrict__ theta, MlpDev m, float* __restrict__ pk) {
+    const int* widths = m.widths;
+    const int nw = m.nw;
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int H = m.H;
@@ -241,6 +250,8 @@ struct MlpRows {
 };
 
 constexpr int kTile = 128;
+constexpr int kThreads = 256;            // two warps per TMEM lane quarter: each owns half the columns
+constexpr int kSplit = kThreads / kTile;
 
 __device__ __forceinline__ void row_input(const MlpRows& R, int64_t r, float* x) {
     if (R.source == kRowsGrid) {
@@ -259,7 +270,7 @@ __device__ __forceinline__ void row_input(const MlpRows& R, int64_t r, float* x)
 // One 128-row tile per iteration of a persistent CTA (128 threads; thread t owns TMEM lane t =
 // tile row t). TMEM columns: D [0, H), A_hi [H, 2H), A_lo [2H, 3H).
 template <int H, bool kStream>
-__global__ void __launch_bounds__(kTile, 1)
+__global__ void __launch_bounds__(kThreads, H == 64 ? 2 : 1)  // H = 64: two CTAs per SM (256 TMEM columns each)
     k_mlp_fwd(MlpDev m, const float* __restrict__ pk, MlpRows R, float* __restrict__ out) {
     extern __shared__ __align__(128) float smem[];
     // smem: [weights (hidden layers resident, or one streamed layer) | head image | W0, b0 | pose]
@@ -277,23 +288,30 @@ __global__ void __launch_bounds__(kTile, 1)
     __shared__ uint32_t s_tmem;
 
     const int tid = threadIdx.x, warp = tid >> 5;
+    // warp w reads/writes TMEM lanes [32 (w % 4), +32) (tcgen05 lane-quarter rule) and the
+    // column half w / 4 of every layer; tile row = its TMEM lane
+    const int quarter = warp & 3, half = warp >> 2;
+    const int trow = quarter * 32 + (tid & 31);
+    constexpr int HC = H / kSplit;  // columns per thread
+    __shared__ float s_logit[kTile];
     const uint32_t b_mma = smem_u32(&bar_mma), b_w = smem_u32(&bar_w);
 
-    for (int i = tid; i < H * m.K0; i += kTile) s_w0[i] = pk[m.off_W0 + i];
-    for (int i = tid; i < H; i += kTile) s_b0[i] = pk[m.off_b0 + i];
+    for (int i = tid; i < H * m.K0; i += kThreads) s_w0[i] = pk[m.off_W0 + i];
+    for (int i = tid; i < H; i += kThreads) s_b0[i] = pk[m.off_b0 + i];
     for (int l = 0; l < m.n_hidden; ++l)
-        for (int i = tid; i < H; i += kTile) s_bias[l * H + i] = pk[m.off_hidden + l * m.hidden_stride_al + kHidImg + i];
+        for (int i = tid; i < H; i += kThreads)
+            s_bias[l * H + i] = pk[m.off_hidden + l * m.hidden_stride_al + kHidImg + i];
     if (m.softmax) {
-        for (int i = tid; i < m.NP; i += kTile) s_headv[i] = pk[m.off_head + 2 * m.NP * H + i];
+        for (int i = tid; i < m.NP; i += kThreads) s_headv[i] = pk[m.off_head + 2 * m.NP * H + i];
     } else {
-        for (int i = tid; i <= H; i += kTile) s_headv[i] = pk[m.off_head + i];
+        for (int i = tid; i <= H; i += kThreads) s_headv[i] = pk[m.off_head + i];
     }
     if (R.source == kRowsRoots)
-        for (int i = tid; i < R.n_pose; i += kTile) s_pose[i] = R.pose[i];
+        for (int i = tid; i < R.n_pose; i += kThreads) s_pose[i] = R.pose[i];
     __syncthreads();
     // the pose inputs are the same for every row: fold W0[:, 3:]·pose into the input bias
     if (m.K0 > 3)
-        for (int j = tid; j < H; j += kTile) {
+        for (int j = tid; j < H; j += kThreads) {
             float z = s_b0[j];
             for (int p = 3; p < m.K0; ++p) z = fmaf(s_w0[j * m.K0 + p], s_pose[p - 3], z);
             s_b0[j] = z;
@@ -312,7 +330,7 @@ __global__ void __launch_bounds__(kTile, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = s_tmem;
-    const uint32_t t_row = tmem + ((uint32_t)(warp * 32) << 16);  // this warp's lane quarter
+    const uint32_t t_row = tmem + ((uint32_t)(quarter * 32) << 16);  // this warp's lane quarter
     const uint32_t tD = 0, tAh = H, tAl = 2 * H;
 
     // weights: bulk copies (TMA) of the pre-laid-out images
@@ -337,13 +355,13 @@ __global__ void __launch_bounds__(kTile, 1)
 
     const int64_t n_tiles = (R.n + kTile - 1) / kTile;
     for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const int64_t row = tile * kTile + tid;
+        const int64_t row = tile * kTile + trow;
         const int64_t rr = row < R.n ? row : R.n - 1;
         // ---- layer 0 (K0 inputs) on the FP32 pipe → A (hi/lo) in TMEM
         float x[3];
         row_input(R, rr, x);
 #pragma unroll 1
-        for (int c0 = 0; c0 < H; c0 += 16) {
+        for (int c0 = half * HC; c0 < (half + 1) * HC; c0 += 16) {
             float hv[16], lv[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
@@ -394,7 +412,7 @@ __global__ void __launch_bounds__(kTile, 1)
                 if (tid == 0) load_hidden(l + 1 < m.n_hidden ? l + 1 : 0, 0);
                 w_ready = false;
             }
-            if (head) {  // softmax head (SkinningMlp::weights_batch, skinning.cpp:47-51)
+            if (head && half == 0) {  // softmax head (SkinningMlp::weights_batch, skinning.cpp:47-51)
                 float z[64];
 #pragma unroll
                 for (int c0 = 0; c0 < 64; c0 += 16)
@@ -413,33 +431,39 @@ __global__ void __launch_bounds__(kTile, 1)
                 const float inv = 1.f / sum;
                 if (row < R.n)
                     for (int i = 0; i < m.n_out; ++i) out[row * m.n_out + i] = z[i] * inv;
-            } else {  // hidden epilogue: bias, softplus, split → next layer's A (and scalar head)
+            } else if (!head) {  // hidden epilogue: bias, softplus, split → next layer's A (and scalar head)
                 const float* b = s_bias + l * H;
                 const bool last_hidden = l + 1 == m.n_hidden;
-#pragma unroll 1
-                for (int c0 = 0; c0 < H; c0 += 16) {
+                // all of the row's accumulators in flight at once, one wait (64 or 128 registers)
+                float acc[HC];
+                const int cb = half * HC;
+#pragma unroll
+                for (int c0 = 0; c0 < HC; c0 += 16) tmem_ld16(t_row + tD + cb + c0, acc + c0);
+                tmem_wait_ld();
+#pragma unroll
+                for (int c0 = 0; c0 < HC; c0 += 16) {
                     float v[16], lv[16];
-                    tmem_ld16(t_row + tD + c0, v);
-                    tmem_wait_ld();
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
-                        const float h = softplus_f(v[j] + b[c0 + j]);
-                        if (!m.softmax && last_hidden) logit = fmaf(s_headv[c0 + j], h, logit);
+                        const float h = softplus_f(acc[c0 + j] + b[cb + c0 + j]);
+                        if (!m.softmax && last_hidden) logit = fmaf(s_headv[cb + c0 + j], h, logit);
                         v[j] = tf32_hi(h);
                         lv[j] = h - v[j];
                     }
                     if (!(last_hidden && !m.softmax)) {
-                        tmem_st16(t_row + tAh + c0, v);
-                        tmem_st16(t_row + tAl + c0, lv);
+                        tmem_st16(t_row + tAh + cb + c0, v);
+                        tmem_st16(t_row + tAl + cb + c0, lv);
                     }
                 }
             }
         }
-        if (!m.softmax && row < R.n) out[row] = sigmoid_f(logit + s_headv[H]);  // OccupancyMlp (shape.cpp:208-228)
+        if (!m.softmax && half == 1) s_logit[trow] = logit;  // partial over the upper columns
         tmem_wait_st();
         tc_fence_before();
         __syncthreads();  // TMEM A/D reuse by the next tile
         tc_fence_after();
+        if (!m.softmax && half == 0 && row < R.n)  // OccupancyMlp (shape.cpp:208-228)
+            out[row] = sigmoid_f(logit + s_logit[trow] + s_headv[H]);
     }
     if (kStream && tid == 0 && !w_ready) mbar_wait(b_w, ph_w);  // drain the last prefetch
     tc_fence_before();
@@ -476,37 +500,46 @@ size_t fwd_smem_bytes(const MlpShape& s, bool stream) {
 }
 
 template <int H, bool kStream>
-void launch_fwd(fsk_ctx* ctx, const MlpShape& s, const float* pk, const MlpRows& R, float* out, cudaStream_t st) {
+void launch_fwd(fsk_ctx* ctx, const MlpShape& s, const int32_t* widths, int nw, const float* pk, const MlpRows& R,
+                float* out, cudaStream_t st) {
     const size_t sm = fwd_smem_bytes(s, kStream);
-    cuda_check(cudaFuncSetAttribute(k_mlp_fwd<H, kStream>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
-               "cudaFuncSetAttribute");
+    // the dynamic-smem opt-in and the residency query once per (instantiation, size)
+    static thread_local size_t set_for = 0;
+    static thread_local int per_sm = 1;
+    if (set_for != sm) {
+        cuda_check(cudaFuncSetAttribute(k_mlp_fwd<H, kStream>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
+                   "cudaFuncSetAttribute");
+        // persistent grid = resident capacity (two CTAs per SM for H = 64: one's MMAs overlap the other's epilogue)
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mlp_fwd<H, kStream>, kThreads, sm),
+                   "occupancy");
+        set_for = sm;
+    }
     const int64_t tiles = (R.n + kTile - 1) / kTile;
-    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, ctx->sm_count));
-    FSK_LAUNCH(ctx, st, (k_mlp_fwd<H, kStream>), grid, kTile, sm, to_dev(s), pk, R, out);
+    const unsigned grid =
+        (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)ctx->sm_count * std::max(per_sm, 1)));
+    FSK_LAUNCH(ctx, st, (k_mlp_fwd<H, kStream>), grid, kThreads, sm, to_dev(s, widths, nw), pk, R, out);
 }
 
-void run_fwd(fsk_ctx* ctx, const MlpShape& s, const float* pk, const MlpRows& R, float* out, cudaStream_t st) {
+void run_fwd(fsk_ctx* ctx, const MlpShape& s, const int32_t* widths, int nw, const float* pk, const MlpRows& R,
+             float* out, cudaStream_t st) {
     if (R.n == 0) return;
     // weights resident when they fit next to the head image (227 KB per CTA), else streamed per layer
     const bool stream = fwd_smem_bytes(s, false) > 200 * 1024;
     if (fwd_smem_bytes(s, stream) > 227 * 1024) fail(FSK_EINVAL, "fsk mlp: network too large for one CTA");
     if (s.H == 64) {
-        if (stream) launch_fwd<64, true>(ctx, s, pk, R, out, st);
-        else launch_fwd<64, false>(ctx, s, pk, R, out, st);
+        if (stream) launch_fwd<64, true>(ctx, s, widths, nw, pk, R, out, st);
+        else launch_fwd<64, false>(ctx, s, widths, nw, pk, R, out, st);
     } else {
-        if (stream) launch_fwd<128, true>(ctx, s, pk, R, out, st);
-        else launch_fwd<128, false>(ctx, s, pk, R, out, st);
+        if (stream) launch_fwd<128, true>(ctx, s, widths, nw, pk, R, out, st);
+        else launch_fwd<128, false>(ctx, s, widths, nw, pk, R, out, st);
     }
 }
 
 const float* pack(fsk_ctx* ctx, const MlpShape& s, const float* theta, const int32_t* widths, int nw,
                   cudaStream_t st) {
+    if (nw > kMaxWidths) fail(FSK_EINVAL, "fsk mlp: too many layers");
     float* pk = (float*)scratch(ctx, kMlpPack, (size_t)s.total * sizeof(float));
-    int32_t* dw = (int32_t*)scratch(ctx, kMlpWidths, 64 * sizeof(int32_t));
-    if (nw > 64) fail(FSK_EINVAL, "fsk mlp: too many layers");
-    cuda_check(cudaMemcpyAsync(dw, widths, nw * sizeof(int32_t), cudaMemcpyHostToDevice, st), "cudaMemcpyAsync");
-    cuda_check(cudaMemsetAsync(pk, 0, (size_t)s.total * sizeof(float), st), "cudaMemsetAsync");
-    FSK_LAUNCH(ctx, st, k_mlp_pack, 148, 256, 0, theta, dw, nw, to_dev(s), pk);
+    FSK_LAUNCH(ctx, st, k_mlp_pack, (unsigned)ctx->sm_count, 256, 0, theta, to_dev(s, widths, nw), pk);
     return pk;
 }
 
@@ -538,7 +571,7 @@ int fsk_distill(fsk_ctx* ctx, const float* theta, const int32_t* widths, int32_t
             R.lo[a] = desc->bbox_min[a];
             R.h[a] = (float)(((double)desc->bbox_max[a] - (double)desc->bbox_min[a]) / (n3[a] - 1));
         }
-        run_fwd(ctx, s, pk, R, weights, st);
+        run_fwd(ctx, s, widths, n_widths, pk, R, weights, st);
     });
 }
 
@@ -568,7 +601,7 @@ int fsk_posed_occupancy(fsk_ctx* ctx, const float* theta, const int32_t* widths,
         R.roots = roots;
         R.pose = pose;
         R.n_pose = n_pose;
-        run_fwd(ctx, s, pk, R, occ, st);
+        run_fwd(ctx, s, widths, n_widths, pk, R, occ, st);
         if (n > 0) FSK_LAUNCH(ctx, st, k_occ_reduce, blocks_for(n, 256), 256, 0, occ, offsets, n, pred, argmax);
     });
 }
