@@ -438,6 +438,14 @@ def mlp_stages(D, sc, roots_buf, n, dev, reps=20):
         out[f"distill_{dims[0]}x{dims[1]}x{dims[2]}"] = {
             "ms": ms, "vertices_per_s": V / (ms * 1e-3), "achieved_TFLOPs": f / (ms * 1e-3) / 1e12,
             "frac_of_3xTF32_peak": 3 * f / (ms * 1e-3) / 1e12 / peak_tf32}
+    dims = (32, 32, 8)  # training loop's distill grid (diff.hpp:106)
+    V = dims[0] * dims[1] * dims[2]
+    gw = torch.randn((V, SKIN_WIDTHS[-1]), generator=torch.Generator(device=dev).manual_seed(0), device=dev) / V
+    gth = torch.empty((sum(SKIN_WIDTHS[i] * SKIN_WIDTHS[i + 1] + SKIN_WIDTHS[i + 1] for i in range(4)),),
+                      dtype=torch.float32, device=dev)
+    ms = timed(lambda: D.distill_bwd(th_s, SKIN_WIDTHS, dims, sc.bbox, gw, out=gth))
+    out["distill_bwd_32x32x8"] = {"ms": ms, "vertices_per_s": V / (ms * 1e-3),
+                                  "note": "forward recomputed on tcgen05 + FP32 cuBLAS GEMMs for Mlp::backward"}
     offs, roots = roots_buf[0][: n + 1], roots_buf[1]
     n_roots = int(offs[-1].item())
     th_o = torch.from_numpy(oracle.mlp_init(OCC_WIDTHS, 2).astype(np.float32)).to(dev)

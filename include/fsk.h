@@ -217,6 +217,14 @@ int fsk_grad_weights(fsk_ctx* ctx, const fsk_grid_desc* desc, const float* grad_
 int fsk_distill(fsk_ctx* ctx, const float* theta, const int32_t* widths, int32_t n_widths,
                 const fsk_grid_desc* desc, float* weights, void* stream);
 
+/* VJP of distill (the chain the training step takes through the skinning network,
+ * diff.cpp:348-359, with the grid vertices in place of the roots): given dL/dw [V][n_b] (dev,
+ * e.g. fsk_grad_weights' output), writes dL/dtheta [P] (dev, Mlp::parameters() order) =
+ * sum_v Mlp::backward(softmax_vjp(w_v, dL/dw_v)) (mlp.cpp:38-41, :140-163). FP32: the forward
+ * is recomputed on the tensor cores, the backward runs as FP32 GEMMs (cuBLAS, pedantic math). */
+int fsk_distill_bwd(fsk_ctx* ctx, const float* theta, const int32_t* widths, int32_t n_widths,
+                    const fsk_grid_desc* desc, const float* grad_w, float* grad_theta, void* stream);
+
 /* posed_occupancy_batch (shape.cpp:242-269) over CorrespondenceSets on the device: for query q,
  * pred[q] = max over roots r in [offsets[q], offsets[q+1]) of sigmoid(net(roots[r].x, pose))
  * (OccupancyMlp::occupancy_batch, shape.cpp:218-228) and argmax[q] = r - offsets[q] of the first

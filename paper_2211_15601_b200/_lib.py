@@ -25,7 +25,7 @@ EXPORTS = [
     "fsk_deform_host", "fsk_eval_points", "fsk_init_states", "fsk_search_bwd", "fsk_grad_weights",
     "fsk_ctx_set_profiling", "fsk_ctx_prof_read", "fsk_measure_fp32_peak", "fsk_batch_search", "fsk_deform",
     "fsk_search_bwd_roots", "fsk_ctx_search_stats", "fsk_measure_fp64_peak", "fsk_measure_l1_gather_peak",
-    "fsk_distill", "fsk_posed_occupancy",
+    "fsk_distill", "fsk_posed_occupancy", "fsk_distill_bwd",
 ]
 
 
@@ -100,6 +100,7 @@ def load():
     L.fsk_measure_fp64_peak.argtypes = [_vp, ctypes.POINTER(ctypes.c_double)]
     L.fsk_measure_l1_gather_peak.argtypes = [_vp, ctypes.POINTER(ctypes.c_double)]
     L.fsk_distill.argtypes = [_vp, _vp, _vp, _i32, G, _vp, _vp]
+    L.fsk_distill_bwd.argtypes = [_vp, _vp, _vp, _i32, G, _vp, _vp, _vp]
     L.fsk_posed_occupancy.argtypes = [_vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp]
     _lib = L
     return L

@@ -20,6 +20,7 @@ NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC,-O2"
 # extra -D flags for tuning sweeps (e.g. FSK_NVCC_DEFS="-DFSK_SEARCH_MINB=2")
 NVCC_FLAGS += os.environ.get("FSK_NVCC_DEFS", "").split()
 
+LIBS = ["-lcudart", "-lcublas"]
 CU_SOURCES = ["fsk_ctx.cu", "fsk_search.cu", "fsk_bwd.cu", "fsk_mlp.cu"]
 CXX_SOURCES = ["fskin_api.cpp"]
 
@@ -40,7 +41,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         t = os.path.getmtime(LIB)
         if all(os.path.getmtime(d) <= t for d in deps):
             return LIB
-    cmd = ["nvcc", *NVCC_FLAGS, "-shared", "-o", LIB, *srcs, "-lcudart"]
+    cmd = ["nvcc", *NVCC_FLAGS, "-shared", "-o", LIB, *srcs, *LIBS]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

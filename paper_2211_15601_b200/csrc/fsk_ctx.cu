@@ -3,6 +3,8 @@
 #include <cstring>
 #include <stdexcept>
 
+#include <cublas_v2.h>
+
 #include "fsk_ctx.h"
 
 namespace fsk {
@@ -236,6 +238,7 @@ int fsk_ctx_destroy(fsk_ctx* ctx) {
         for (auto& e : ctx->pool) cudaEventDestroy(e);
         if (ctx->stats) cudaFree(ctx->stats);
         if (ctx->copy) cudaStreamDestroy(ctx->copy);
+        if (ctx->blas) cublasDestroy(ctx->blas);
         if (ctx->hcount) cudaFreeHost(ctx->hcount);
         delete ctx;
     });

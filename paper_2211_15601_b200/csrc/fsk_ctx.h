@@ -6,6 +6,8 @@
 
 #include <cuda_runtime.h>
 
+struct cublasContext;
+
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
@@ -19,7 +21,7 @@ struct fsk_ctx {
     int device = 0;
     int sm_count = 0;
     int64_t launches = 0;
-    static constexpr int kSlots = 40;
+    static constexpr int kSlots = 48;
     void* buf[kSlots] = {};
     size_t cap[kSlots] = {};
     // optional per-launch CUDA-event profiling (bench.py reads per-kernel device time)
@@ -37,6 +39,7 @@ struct fsk_ctx {
     // device→host copy stream of the host-buffer entry point (created on first use)
     cudaStream_t copy = nullptr;
     int64_t* hcount = nullptr;  // pinned per-chunk root counts
+    cublasContext* blas = nullptr;  // FP32 GEMMs of the distill backward (created on first use)
 };
 
 namespace fsk {
@@ -47,7 +50,7 @@ enum Slot {
     kBwdStart, kBwdCell, kBwdRec, kPeakTable,
     kOXr, kOJa, kOJb, kOJc, kOMeta, kOKeep, kNRoots, kOffs, kRootsTmp,
     kHW, kHB, kHP, kHT, kHOffs, kHRoots,
-    kMlpPack, kMlpWidths, kMlpOcc,
+    kMlpPack, kMlpWidths, kMlpOcc, kMlpAct, kMlpD0, kMlpD1, kMlpOnes,
     kSlotCount
 };
 static_assert(kSlotCount <= fsk_ctx::kSlots, "scratch slots");

@@ -21,6 +21,8 @@
 //
 // Parameters are the reference's flat vector (Mlp::parameters(), mlp.cpp:207-219: per layer
 // W column-major then b), in float32 on the device; k_mlp_pack re-lays them out once per call.
+#include <cublas_v2.h>
+
 #include <cstring>
 
 #include "fsk_ctx.h"
@@ -269,9 +271,10 @@ __device__ __forceinline__ void row_input(const MlpRows& R, int64_t r, float* x)
 
 // One 128-row tile per iteration of a persistent CTA (128 threads; thread t owns TMEM lane t =
 // tile row t). TMEM columns: D [0, H), A_hi [H, 2H), A_lo [2H, 3H).
+// act (optional, for the backward): x [n][4] then the softplus outputs h_l [(n_hidden+1)][n][H].
 template <int H, bool kStream>
 __global__ void __launch_bounds__(kThreads, H == 64 ? 2 : 1)  // H = 64: two CTAs per SM (256 TMEM columns each)
-    k_mlp_fwd(MlpDev m, const float* __restrict__ pk, MlpRows R, float* __restrict__ out) {
+    k_mlp_fwd(MlpDev m, const float* __restrict__ pk, MlpRows R, float* __restrict__ out, float* __restrict__ act) {
     extern __shared__ __align__(128) float smem[];
     // smem: [weights (hidden layers resident, or one streamed layer) | head image | W0, b0 | pose]
     constexpr int kHidImg = 2 * H * H;  // floats (hi + lo)
@@ -360,6 +363,9 @@ __global__ void __launch_bounds__(kThreads, H == 64 ? 2 : 1)  // H = 64: two CTA
         // ---- layer 0 (K0 inputs) on the FP32 pipe → A (hi/lo) in TMEM
         float x[3];
         row_input(R, rr, x);
+        float* act_h = act ? act + 4 * R.n : nullptr;
+        if (act && half == 0 && row < R.n)
+            reinterpret_cast<float4*>(act)[row] = make_float4(x[0], x[1], x[2], 0.f);
 #pragma unroll 1
         for (int c0 = half * HC; c0 < (half + 1) * HC; c0 += 16) {
             float hv[16], lv[16];
@@ -374,6 +380,9 @@ __global__ void __launch_bounds__(kThreads, H == 64 ? 2 : 1)  // H = 64: two CTA
                 hv[j] = tf32_hi(h);
                 lv[j] = h - hv[j];
             }
+            if (act_h && row < R.n)
+#pragma unroll
+                for (int j = 0; j < 16; ++j) act_h[row * H + c0 + j] = hv[j] + lv[j];
             tmem_st16(t_row + tAh + c0, hv);
             tmem_st16(t_row + tAl + c0, lv);
         }
@@ -450,6 +459,10 @@ __global__ void __launch_bounds__(kThreads, H == 64 ? 2 : 1)  // H = 64: two CTA
                         v[j] = tf32_hi(h);
                         lv[j] = h - v[j];
                     }
+                    if (act_h && row < R.n)
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            act_h[((int64_t)(l + 1) * R.n + row) * H + cb + c0 + j] = v[j] + lv[j];
                     if (!(last_hidden && !m.softmax)) {
                         tmem_st16(t_row + tAh + cb + c0, v);
                         tmem_st16(t_row + tAl + cb + c0, lv);
@@ -501,7 +514,7 @@ size_t fwd_smem_bytes(const MlpShape& s, bool stream) {
 
 template <int H, bool kStream>
 void launch_fwd(fsk_ctx* ctx, const MlpShape& s, const int32_t* widths, int nw, const float* pk, const MlpRows& R,
-                float* out, cudaStream_t st) {
+                float* out, float* act, cudaStream_t st) {
     const size_t sm = fwd_smem_bytes(s, kStream);
     // the dynamic-smem opt-in and the residency query once per (instantiation, size)
     static thread_local size_t set_for = 0;
@@ -517,21 +530,21 @@ void launch_fwd(fsk_ctx* ctx, const MlpShape& s, const int32_t* widths, int nw, 
     const int64_t tiles = (R.n + kTile - 1) / kTile;
     const unsigned grid =
         (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)ctx->sm_count * std::max(per_sm, 1)));
-    FSK_LAUNCH(ctx, st, (k_mlp_fwd<H, kStream>), grid, kThreads, sm, to_dev(s, widths, nw), pk, R, out);
+    FSK_LAUNCH(ctx, st, (k_mlp_fwd<H, kStream>), grid, kThreads, sm, to_dev(s, widths, nw), pk, R, out, act);
 }
 
 void run_fwd(fsk_ctx* ctx, const MlpShape& s, const int32_t* widths, int nw, const float* pk, const MlpRows& R,
-             float* out, cudaStream_t st) {
+             float* out, cudaStream_t st, float* act = nullptr) {
     if (R.n == 0) return;
     // weights resident when they fit next to the head image (227 KB per CTA), else streamed per layer
     const bool stream = fwd_smem_bytes(s, false) > 200 * 1024;
     if (fwd_smem_bytes(s, stream) > 227 * 1024) fail(FSK_EINVAL, "fsk mlp: network too large for one CTA");
     if (s.H == 64) {
-        if (stream) launch_fwd<64, true>(ctx, s, widths, nw, pk, R, out, st);
-        else launch_fwd<64, false>(ctx, s, widths, nw, pk, R, out, st);
+        if (stream) launch_fwd<64, true>(ctx, s, widths, nw, pk, R, out, act, st);
+        else launch_fwd<64, false>(ctx, s, widths, nw, pk, R, out, act, st);
     } else {
-        if (stream) launch_fwd<128, true>(ctx, s, widths, nw, pk, R, out, st);
-        else launch_fwd<128, false>(ctx, s, widths, nw, pk, R, out, st);
+        if (stream) launch_fwd<128, true>(ctx, s, widths, nw, pk, R, out, act, st);
+        else launch_fwd<128, false>(ctx, s, widths, nw, pk, R, out, act, st);
     }
 }
 
@@ -541,6 +554,33 @@ const float* pack(fsk_ctx* ctx, const MlpShape& s, const float* theta, const int
     float* pk = (float*)scratch(ctx, kMlpPack, (size_t)s.total * sizeof(float));
     FSK_LAUNCH(ctx, st, k_mlp_pack, (unsigned)ctx->sm_count, 256, 0, theta, to_dev(s, widths, nw), pk);
     return pk;
+}
+
+// ------------------------------------------------------------------ distill backward
+// dz = softmax_vjp(w, dw) = w ⊙ (dw − <w, dw>) (mlp.cpp:38-41), one thread per vertex
+__global__ void k_softmax_vjp(const float* __restrict__ w, const float* __restrict__ dw, int64_t n, int nb,
+                              float* __restrict__ dz) {
+    const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    float dot = 0.f;
+    for (int i = 0; i < nb; ++i) dot = fmaf(w[v * nb + i], dw[v * nb + i], dot);
+    for (int i = 0; i < nb; ++i) dz[v * nb + i] = w[v * nb + i] * (dw[v * nb + i] - dot);
+}
+
+// delta = (delta_{l+1} W_{l+1}) ⊙ softplus'(z_l), softplus'(z) = sigmoid(z) = 1 − exp(−softplus(z))
+// taken from the stored activation h_l (mlp.cpp:157-160)
+__global__ void k_softplus_bwd(float* __restrict__ d, const float* __restrict__ h, int64_t count) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < count) d[i] *= -expm1f(-h[i]);
+}
+
+__global__ void k_fill(float* __restrict__ p, int64_t n, float v) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+void blas_check(cublasStatus_t e, const char* what) {
+    if (e != CUBLAS_STATUS_SUCCESS) fail(FSK_ECUDA, std::string(what) + ": cuBLAS status " + std::to_string((int)e));
 }
 
 }  // namespace
@@ -603,6 +643,77 @@ int fsk_posed_occupancy(fsk_ctx* ctx, const float* theta, const int32_t* widths,
         R.n_pose = n_pose;
         run_fwd(ctx, s, widths, n_widths, pk, R, occ, st);
         if (n > 0) FSK_LAUNCH(ctx, st, k_occ_reduce, blocks_for(n, 256), 256, 0, occ, offsets, n, pred, argmax);
+    });
+}
+
+int fsk_distill_bwd(fsk_ctx* ctx, const float* theta, const int32_t* widths, int32_t n_widths,
+                    const fsk_grid_desc* desc, const float* grad_w, float* grad_theta, void* stream) {
+    return guard([&] {
+        set_device(ctx);
+        if (!desc || !widths || !theta || !grad_w || !grad_theta) fail(FSK_EINVAL, "fsk: null buffer");
+        if (desc->nx < 2 || desc->ny < 2 || desc->nz < 2) fail(FSK_EINVAL, "distill: dims must be >= 2 per axis");
+        if (n_widths < 2 || widths[0] != 3) fail(FSK_EINVAL, "SkinningMlp: network input width must be 3");
+        if (widths[n_widths - 1] != desc->n_bones) fail(FSK_EINVAL, "distill: bone count mismatch");
+        const MlpShape s = mlp_shape(widths, n_widths, true);
+        cudaStream_t st = (cudaStream_t)stream;
+        const int64_t V = (int64_t)desc->nx * desc->ny * desc->nz;
+        if (V >= (int64_t(1) << 31)) fail(FSK_EINVAL, "fsk: grid too large");
+        const int H = s.H, nb = s.n_out, L = n_widths - 1;  // weight layers
+        // forward with the activations kept: x [V][4], h_l [L-1][V][H], w [V][nb]
+        const float* pk = pack(ctx, s, theta, widths, n_widths, st);
+        float* act = (float*)scratch(ctx, kMlpAct, (size_t)(4 * V + (int64_t)(L - 1) * V * H) * sizeof(float));
+        float* w = (float*)scratch(ctx, kMlpOcc, (size_t)V * nb * sizeof(float));
+        MlpRows R{};
+        R.source = kRowsGrid;
+        R.n = V;
+        R.nx = desc->nx;
+        R.ny = desc->ny;
+        const int n3[3] = {desc->nx, desc->ny, desc->nz};
+        for (int a = 0; a < 3; ++a) {
+            R.lo[a] = desc->bbox_min[a];
+            R.h[a] = (float)(((double)desc->bbox_max[a] - (double)desc->bbox_min[a]) / (n3[a] - 1));
+        }
+        run_fwd(ctx, s, widths, n_widths, pk, R, w, st, act);
+        // backward (Mlp::backward, mlp.cpp:140-163) as FP32 GEMMs over all vertices
+        if (!ctx->blas) blas_check(cublasCreate(&ctx->blas), "cublasCreate");
+        blas_check(cublasSetStream(ctx->blas, st), "cublasSetStream");
+        blas_check(cublasSetMathMode(ctx->blas, CUBLAS_PEDANTIC_MATH), "cublasSetMathMode");  // true FP32
+        const int64_t wmax = std::max(H, nb);
+        float* dA = (float*)scratch(ctx, kMlpD0, (size_t)V * wmax * sizeof(float));
+        float* dB = (float*)scratch(ctx, kMlpD1, (size_t)V * wmax * sizeof(float));
+        float* ones = (float*)scratch(ctx, kMlpOnes, (size_t)V * sizeof(float));
+        FSK_LAUNCH(ctx, st, k_fill, blocks_for(V, 256), 256, 0, ones, V, 1.f);
+        FSK_LAUNCH(ctx, st, k_softmax_vjp, blocks_for(V, 256), 256, 0, w, grad_w, V, nb, dA);
+        std::vector<int64_t> off(L);
+        int64_t o = 0;
+        for (int l = 0; l < L; ++l) {
+            off[l] = o;
+            o += (int64_t)widths[l + 1] * widths[l] + widths[l + 1];
+        }
+        const float one = 1.f, zero = 0.f;
+        const float* act_h = act + 4 * V;
+        for (int l = L - 1; l >= 0; --l) {
+            const int n_out = widths[l + 1], n_in = widths[l];
+            // input of layer l: x (row stride 4) or h_{l-1} (row stride H)
+            const float* in = l == 0 ? act : act_h + (int64_t)(l - 1) * V * H;
+            const int ld_in = l == 0 ? 4 : H;
+            float* dW = grad_theta + off[l];
+            float* db = dW + (int64_t)n_out * n_in;
+            // dW_l (column-major n_out x n_in, the Mlp::parameters() layout) = delta_l^T · in
+            blas_check(cublasSgemm(ctx->blas, CUBLAS_OP_N, CUBLAS_OP_T, n_out, n_in, (int)V, &one, dA, n_out, in, ld_in,
+                                   &zero, dW, n_out),
+                       "cublasSgemm dW");
+            blas_check(cublasSgemv(ctx->blas, CUBLAS_OP_N, n_out, (int)V, &one, dA, n_out, ones, 1, &zero, db, 1),
+                       "cublasSgemv db");
+            if (l == 0) break;
+            // delta_{l-1} = (delta_l · W_l) ⊙ softplus'(z_{l-1})
+            blas_check(cublasSgemm(ctx->blas, CUBLAS_OP_T, CUBLAS_OP_N, n_in, (int)V, n_out, &one, theta + off[l], n_out,
+                                   dA, n_out, &zero, dB, n_in),
+                       "cublasSgemm delta");
+            FSK_LAUNCH(ctx, st, k_softplus_bwd, blocks_for(V * n_in, 256), 256, 0, dB,
+                       act_h + (int64_t)(l - 1) * V * H, V * n_in);
+            std::swap(dA, dB);
+        }
     });
 }
 

@@ -327,6 +327,19 @@ class Deformer:
                                  ctypes.byref(desc), _ptr(out), _stream(self.device)))
         return out
 
+    def distill_bwd(self, theta, widths, dims, bbox, grad_w, out=None):
+        """VJP of ``distill``: dL/dtheta [P] from dL/dw [V, n_b] (Mlp::backward through the
+        softmax head, mlp.cpp:38-41,140-163)."""
+        nb = int(widths[-1])
+        desc = grid_desc(dims, bbox, nb)
+        if out is None:
+            P = sum(int(widths[i + 1]) * int(widths[i]) + int(widths[i + 1]) for i in range(len(widths) - 1))
+            out = torch.empty((P,), dtype=torch.float32, device=self.device)
+        check(self.L.fsk_distill_bwd(self._ctx, _ptr(_f32(theta, "theta", self.device)), self._widths(widths),
+                                     len(widths), ctypes.byref(desc), _ptr(_f32(grad_w, "grad_w", self.device)),
+                                     _ptr(out), _stream(self.device)))
+        return out
+
     def posed_occupancy(self, theta, widths, pose, offsets, roots, occ_per_root=None):
         """``posed_occupancy_batch`` (shape.cpp:242-269) over device CorrespondenceSets
         (offsets [N+1] int64, roots [M,16] fsk_root records): returns (pred [N], argmax [N])."""

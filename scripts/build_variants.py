@@ -16,7 +16,7 @@ def one(name, defs):
     srcs, _ = B._sources()
     out = os.path.join(ROOT, "build", "variants", name + ".so")
     os.makedirs(os.path.dirname(out), exist_ok=True)
-    cmd = ["nvcc", *B.NVCC_FLAGS, *defs.split(), "-shared", "-o", out, *srcs, "-lcudart"]
+    cmd = ["nvcc", *B.NVCC_FLAGS, *defs.split(), "-shared", "-o", out, *srcs, *B.LIBS]
     r = subprocess.run(cmd, capture_output=True, text=True)
     return name, r.returncode, r.stderr[-2000:]
 

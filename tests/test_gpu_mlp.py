@@ -118,3 +118,47 @@ def test_distill_feeds_the_search(deformer):
     n_roots = int(offs[-1].item())
     assert n_roots > 0
     assert (roots[:n_roots, 3] < o["conv_eps"]).all()  # every emitted root converged
+
+
+@pytest.mark.parametrize("dims,widths", [((32, 32, 8), SKIN), ((16, 16, 16), [3, 64, 64, 7]),
+                                         ((9, 8, 7), [3, 128, 128, 128, 30])])
+def test_distill_backward_matches_oracle_vjp(deformer, dims, widths):
+    """dL/dtheta of distill (Mlp::backward through the softmax head) vs the f64 oracle VJP."""
+    sc = S.make_scene((4, 4, 4), 10, seed=1)
+    th = theta32(widths, 13, 0.05)
+    V = dims[0] * dims[1] * dims[2]
+    dw = (np.random.default_rng(4).normal(size=(V, widths[-1])) / V).astype(np.float32)
+    g = deformer.distill_bwd(torch.from_numpy(th).cuda(), widths, dims, sc.bbox, torch.from_numpy(dw).cuda())
+    g = g.cpu().numpy()
+    r = oracle.distill_vjp(th, widths, dims, sc.bbox, dw)
+    err = np.abs(g - r).max()
+    print(f"\ndistill bwd {dims} {widths}: max|dg| {err:.2e} (max|g| {np.abs(r).max():.2e})")
+    assert err <= 1e-4 * np.abs(r).max() + 1e-7
+
+
+def test_training_chain_grid_to_skinning_params(deformer):
+    """K3 (implicit-diff backward to the transform grid) -> dL/dw -> dL/dtheta: the GPU chain
+    against the oracle chain on the same roots (diff.cpp:336-359 with the grid in the loop)."""
+    sc = S.make_scene((32, 32, 8), 3000, seed=12, points="training")
+    th = theta32(SKIN, 21, 0.05)
+    tht = torch.from_numpy(th).cuda()
+    w = deformer.distill(tht, SKIN, sc.dims, sc.bbox)
+    B, x = torch.from_numpy(sc.bones).cuda(), torch.from_numpy(sc.points).cuda()
+    o = sc.search_options(50)
+    offs, roots = deformer.deform(w, sc.dims, sc.bbox, B, x, SearchOptions(50, o["conv_eps"], o["div_eps"],
+                                                                          o["dedup_dist"]))
+    n = x.shape[0]
+    ridx = torch.where(offs[1:] > offs[:-1], offs[:-1], torch.full_like(offs[:-1], -1))
+    gx = torch.randn((n, 3), generator=torch.Generator(device="cuda").manual_seed(3), device="cuda") / n
+    gT = deformer.search_bwd_roots(sc.dims, sc.bbox, 24, roots, ridx, gx)
+    gW = deformer.grad_weights(sc.dims, sc.bbox, gT, B)
+    gth = deformer.distill_bwd(tht, SKIN, sc.dims, sc.bbox, gW).cpu().numpy()
+    # oracle chain from the same roots (x*, J~) and cotangents
+    ri = ridx.cpu().numpy()
+    sel = ri >= 0
+    R = roots.cpu().numpy()
+    _, rw = oracle.grid_vjp(sc.dims, sc.bbox, sc.bones, R[ri[sel], :3], R[ri[sel], 4:13], gx.cpu().numpy()[sel])
+    rth = oracle.distill_vjp(th, SKIN, sc.dims, sc.bbox, rw)
+    err = np.abs(gth - rth).max()
+    print(f"\nchain dL/dtheta: max|d| {err:.2e} (max|g| {np.abs(rth).max():.2e})")
+    assert err <= 1e-4 * np.abs(rth).max() + 1e-7
