@@ -55,40 +55,46 @@ __global__ void __launch_bounds__(256) k_precompute(const float* __restrict__ w,
                                                     int nb, int nx, int64_t V, float4* __restrict__ tg,
                                                     float* __restrict__ p32, double* __restrict__ p64,
                                                     double* __restrict__ tg64) {
+    // one thread per (vertex, matrix row r): three threads share a vertex's weights (L1 broadcast)
     extern __shared__ float sB[];
     for (int e = threadIdx.x; e < nb * 12; e += blockDim.x) sB[e] = bones[e];
     __syncthreads();
-    const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (v >= V) return;
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= 3 * V) return;
+    const int64_t v = t / 3;
+    const int r = (int)(t - 3 * v);
     const float* wv = w + v * nb;
-    float T[12];
-#pragma unroll
-    for (int e = 0; e < 12; ++e) T[e] = 0.f;
+    float T[4] = {0.f, 0.f, 0.f, 0.f};
+    double D[4] = {0.0, 0.0, 0.0, 0.0};
+    const bool f64 = p64 || tg64;
     for (int i = 0; i < nb; ++i) {
         const float wi = __ldg(wv + i);
+        const float* Bi = sB + i * 12 + 4 * r;
 #pragma unroll
-        for (int e = 0; e < 12; ++e) T[e] = fmaf(wi, sB[i * 12 + e], T[e]);
+        for (int e = 0; e < 4; ++e) T[e] = fmaf(wi, Bi[e], T[e]);  // lbs_blend bone order (deformer.cpp:9-19)
+        if (f64)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) D[e] = fma((double)wi, (double)Bi[e], D[e]);
     }
     const bool has_left = (v % nx) != 0;
-    if (tg) {
-        tg[3 * v] = make_float4(T[0], T[1], T[2], T[3]);
-        tg[3 * v + 1] = make_float4(T[4], T[5], T[6], T[7]);
-        tg[3 * v + 2] = make_float4(T[8], T[9], T[10], T[11]);
+    if (tg) tg[3 * v + r] = make_float4(T[0], T[1], T[2], T[3]);
+    const int64_t stride = 8 * V;
+    if (p32) {
+        float* lo = p32 + r * stride + 8 * v;
+        *reinterpret_cast<float4*>(lo) = make_float4(T[0], T[1], T[2], T[3]);
+        if (has_left) *reinterpret_cast<float4*>(lo - 4) = make_float4(T[0], T[1], T[2], T[3]);
     }
-    if (p32) put_planes(p32, V, v, has_left, T);
-    if (p64 || tg64) {
-        double D[12];
+    if (p64) {
+        double* lo = p64 + r * stride + 8 * v;
 #pragma unroll
-        for (int e = 0; e < 12; ++e) D[e] = 0.0;
-        for (int i = 0; i < nb; ++i) {
-            const double wi = (double)__ldg(wv + i);
+        for (int e = 0; e < 4; ++e) lo[e] = D[e];
+        if (has_left)
 #pragma unroll
-            for (int e = 0; e < 12; ++e) D[e] = fma(wi, (double)sB[i * 12 + e], D[e]);
-        }
-        if (p64) put_planes(p64, V, v, has_left, D);
-        if (tg64)
-            for (int e = 0; e < 12; ++e) tg64[12 * v + e] = D[e];
+            for (int e = 0; e < 4; ++e) lo[e - 4] = D[e];
     }
+    if (tg64)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) tg64[12 * v + 4 * r + e] = D[e];
 }
 
 // Relayout of a caller-provided [V][12] grid (float32, or float64 when tg64 != null) into
@@ -295,7 +301,8 @@ constexpr int kSearchBlock = FSK_SEARCH_BLOCK;
 template <typename R>
 __device__ __forceinline__ void store_solve(const SearchPlanes& out, int64_t q, R x0, R x1, R x2, const R Ji[9], R err2,
                                             const SolveOut& s) {
-    out.xr[q] = make_float4((float)x0, (float)x1, (float)x2, (float)sqrt(err2));
+    // the residual's sign bit carries the converged flag (dedup reads one float4 per solve)
+    out.xr[q] = make_float4((float)x0, (float)x1, (float)x2, copysignf((float)sqrt(err2), s.conv ? 1.f : -1.f));
     out.ja[q] = make_float4((float)Ji[0], (float)Ji[1], (float)Ji[2], (float)Ji[3]);
     out.jb[q] = make_float4((float)Ji[4], (float)Ji[5], (float)Ji[6], (float)Ji[7]);
     out.jc[q] = (float)Ji[8];
@@ -476,30 +483,24 @@ __global__ void __launch_bounds__(256) k_dedup(int64_t n, int nb, float dedup2, 
     const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (j >= n) return;
     // The first kRegKept kept roots stay in registers (a query has ~1 root); later kept roots
-    // are re-read from the planes. Loads are issued 8 bones at a time (independent).
-    constexpr int kRegKept = 4, kBatch = 8;
+    // are re-read from the planes. Loads are issued kBatch bones at a time (independent
+    // coalesced rows of the bone-major planes); converged = sign bit of the residual clear.
+    constexpr int kRegKept = 4, kBatch = 24;
     float kx[kRegKept], ky[kRegKept], kz[kRegKept];
 #pragma unroll
     for (int c = 0; c < kRegKept; ++c) kx[c] = ky[c] = kz[c] = 0.f;
     int count = 0;
     for (int b0 = 0; b0 < nb; b0 += kBatch) {
         float4 xv[kBatch];
-        uint16_t mv[kBatch];
 #pragma unroll
-        for (int i = 0; i < kBatch; ++i) {
-            mv[i] = 0;
-            if (b0 + i < nb) {
-                const int64_t q = (int64_t)(b0 + i) * n + j;
-                mv[i] = sp.meta[q];
-                xv[i] = sp.xr[q];
-            }
-        }
+        for (int i = 0; i < kBatch; ++i)
+            if (b0 + i < nb) xv[i] = __ldcs(sp.xr + (int64_t)(b0 + i) * n + j);
 #pragma unroll
         for (int i = 0; i < kBatch; ++i) {
             const int b = b0 + i;
-            if (b >= nb) break;
+            if (b >= nb) continue;
             int k = 0;
-            if (mv[i] & 0x100) {
+            if (!signbit(xv[i].w)) {
                 k = 1;
 #pragma unroll
                 for (int c = 0; c < kRegKept; ++c) {
@@ -634,7 +635,11 @@ __global__ void __launch_bounds__(256) k_emit(int64_t n, int nb, SearchPlanes sp
     for (int b = 0; b < nb; ++b) {
         const int64_t q = (int64_t)b * n + j;
         if (!sp.keep[q]) continue;
-        if (o < cap) store_root(roots + o, sp.xr[q], sp.ja[q], sp.jb[q], sp.jc[q], b, sp.meta[q] & 0xff);
+        if (o < cap) {
+            float4 xr = sp.xr[q];
+            xr.w = fabsf(xr.w);
+            store_root(roots + o, xr, sp.ja[q], sp.jb[q], sp.jc[q], b, sp.meta[q] & 0xff);
+        }
         ++o;
     }
 }
@@ -663,7 +668,7 @@ __global__ void __launch_bounds__(256) k_scatter_dense(int64_t n, int nb, Search
         d.x_c[3 * s + 1] = xr.y;
         d.x_c[3 * s + 2] = xr.z;
     }
-    if (d.resid) d.resid[s] = xr.w;
+    if (d.resid) d.resid[s] = fabsf(xr.w);
     if (d.jinv) {
         const float4 a = sp.ja[q], c = sp.jb[q];
         float* J = d.jinv + 9 * s;
@@ -760,7 +765,7 @@ GridPlanes run_precompute(fsk_ctx* ctx, const float* w, const GridP& g, const fl
                           bool planes, bool f64, cudaStream_t st) {
     const int64_t V = vertex_count(g);
     GridPlanes P = planes_scratch(ctx, g);
-    FSK_LAUNCH(ctx, st, k_precompute, blocks_for(V, 256), 256, g.nb * 12 * sizeof(float), w, bones, g.nb, g.nx, V,
+    FSK_LAUNCH(ctx, st, k_precompute, blocks_for(3 * V, 256), 256, g.nb * 12 * sizeof(float), w, bones, g.nb, g.nx, V,
                reinterpret_cast<float4*>(tg), planes ? (float*)P.p32.p : nullptr,
                planes && f64 ? (double*)P.p64.p : nullptr, tg64);
     return P;

@@ -1,2 +1,2 @@
-timeout 600 python -m pytest tests/test_gpu_mlp.py -q -rf -s -x > gpurun_out/pytest_mlp.log 2>&1
-timeout 600 python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_mlp.log 2>&1
+BENCH_ARGS="--no-mlp" bash scripts/gpu_variants.sh
+timeout 900 python -m pytest tests -m gpu -q -rf -x > gpurun_out/pytest_all.log 2>&1
