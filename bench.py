@@ -79,6 +79,8 @@ def scene_for_rank(args, rank):
 
 def workload_name(args):
     name = "C3" if args.backward else ("C4" if args.poses > 1 else "C2")
+    if args.grid == "128,128,32" and not args.backward and args.poses == 1:
+        name = "C5 (per-GPU shard of the 64M-point ray-sample workload)"
     s = (f"{name}: {args.poses} pose(s) x {args.points // 1000}k posed points x 24 bone inits per GPU, "
          f"{args.grid.replace(',', 'x')} grid, max_iters {args.max_iters}; step = per pose: precompute + sort + "
          f"search (fp32 pass + fp64 escalation) + dedup + compaction to CorrespondenceSets")
@@ -303,7 +305,7 @@ def run_ours(args, rank, world, local_rank):
     k2e_ms, k2e_n = D.prof_read("k_search_escalated", reset=False)
     k1_ms, k1_n = D.prof_read("k_precompute", reset=False)
     breakdown = {}
-    for kname in ("k_precompute", "k_sort_init", "k_sort_bbox", "k_sort_hist", "k_sort_scan", "k_sort_scatter",
+    for kname in ("k_precompute", "k_sort_bbox", "k_sort_hist", "k_sort_scan", "k_sort_scatter",
                   "k_search_fast", "k_search_escalated", "k_dedup", "k_scan_partial", "k_scan_top", "k_scan_apply",
                   "k_emit", "k_zero", "k_bwd_scatter", "k_bwd_bucket_count", "k_bwd_bucket_fill", "k_bwd_cell_reduce",
                   "k_bwd_fixed_to_float",

@@ -129,17 +129,16 @@ __device__ __forceinline__ int f2ord(float f) {
 }
 __device__ __forceinline__ float ord2f(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7fffffff); }
 
-__global__ void k_sort_init(int* __restrict__ hist, int* __restrict__ bbox, int* __restrict__ esc_count) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t == 0) esc_count[0] = esc_count[1] = esc_count[2] = esc_count[3] = 0;
-    for (int i = t; i < kSortBuckets; i += gridDim.x * blockDim.x) hist[i] = 0;
-    if (t < 3) {
-        bbox[t] = f2ord(INFINITY);
-        bbox[3 + t] = f2ord(-INFINITY);
-    }
-}
+// Sort state, one contiguous int block zeroed by a single memset per call:
+//   [0, kSortBuckets) histogram, then bbox (6 words), escalation counters (4), scan barrier (2).
+// The bbox is kept in a zero-identity encoding: u = f2ord(f) ^ 0x80000000 (unsigned order);
+// max stored as u, min stored as ~u, both reduced with atomicMax.
+constexpr int kSortStateInts = kSortBuckets + 64;  // + bbox, counters, barrier + 32 block sums
+constexpr int kBboxOff = kSortBuckets, kEscOff = kSortBuckets + 8, kScanBarOff = kSortBuckets + 16;
+__device__ __forceinline__ unsigned bb_enc(float f) { return (unsigned)f2ord(f) ^ 0x80000000u; }
+__device__ __forceinline__ float bb_dec(unsigned u) { return ord2f((int)(u ^ 0x80000000u)); }
 
-__global__ void __launch_bounds__(256) k_sort_bbox(const float* __restrict__ x, int64_t n, int* __restrict__ bbox) {
+__global__ void __launch_bounds__(256) k_sort_bbox(const float* __restrict__ x, int64_t n, unsigned* __restrict__ bbox) {
     float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
 #pragma unroll
@@ -174,8 +173,8 @@ __global__ void __launch_bounds__(256) k_sort_bbox(const float* __restrict__ x, 
             l = fminf(l, s_lo[a][w]);
             h = fmaxf(h, s_hi[a][w]);
         }
-        atomicMin(bbox + a, f2ord(l));
-        atomicMax(bbox + 3 + a, f2ord(h));
+        atomicMax(bbox + a, ~bb_enc(l));
+        atomicMax(bbox + 3 + a, bb_enc(h));
     }
 }
 
@@ -187,14 +186,14 @@ __device__ __forceinline__ uint32_t spread3(uint32_t v) {  // 5 bits -> every th
     return v;
 }
 
-__global__ void __launch_bounds__(256) k_sort_hist(const float* __restrict__ x, int64_t n, const int* __restrict__ bbox,
+__global__ void __launch_bounds__(256) k_sort_hist(const float* __restrict__ x, int64_t n, const unsigned* __restrict__ bbox,
                                                    uint16_t* __restrict__ keys, int* __restrict__ hist) {
     const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (p >= n) return;
     uint32_t q[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        const float lo = ord2f(bbox[a]), hi = ord2f(bbox[3 + a]);
+        const float lo = bb_dec(~bbox[a]), hi = bb_dec(bbox[3 + a]);
         const float s = (float)(1 << kSortBitsPerAxis) / fmaxf(hi - lo, 1e-30f);
         const float u = (x[3 * p + a] - lo) * s;
         const int qi = isfinite(u) ? __float2int_rd(u) : 0;
@@ -205,57 +204,44 @@ __global__ void __launch_bounds__(256) k_sort_hist(const float* __restrict__ x, 
     atomicAdd(hist + k, 1);
 }
 
-// Single-block exclusive scan of the 32768 bucket counts in 4 chunks of 8192 (1024 threads
-// × 8 contiguous), staged through shared memory so global loads and stores are coalesced.
-__global__ void __launch_bounds__(1024) k_sort_scan(int* __restrict__ hist) {
-    constexpr int kChunk = 8192, kPer = kChunk / 1024;
+// Exclusive scan of the 32768 bucket counts by 32 co-resident blocks of 1024 (one bucket per
+// thread): block sums, a grid barrier on a counter, then each block adds the sums before it.
+constexpr int kScanBlocks = kSortBuckets / 1024;
+__global__ void __launch_bounds__(1024) k_sort_scan(int* __restrict__ hist, int* __restrict__ bar) {
     __shared__ int warp_tot[32];
-    __shared__ int block_tot;
-    __shared__ int sh[kChunk + kChunk / 32];  // +1 pad per 32 words against bank conflicts
-    const int t = threadIdx.x;
-    auto pad = [](int i) { return i + (i >> 5); };
-    int carry = 0;
-    for (int c0 = 0; c0 < kSortBuckets; c0 += kChunk) {
-#pragma unroll
-        for (int i = t; i < kChunk; i += 1024) sh[pad(i)] = hist[c0 + i];
-        __syncthreads();
-        int v[kPer];
-        int s = 0;
-#pragma unroll
-        for (int i = 0; i < kPer; ++i) {
-            v[i] = sh[pad(t * kPer + i)];
-            s += v[i];
-        }
-        int incl = s;
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffff, incl, o);
-            if ((t & 31) >= o) incl += y;
-        }
-        if ((t & 31) == 31) warp_tot[t >> 5] = incl;
-        __syncthreads();
-        if (t < 32) {
-            const int w = warp_tot[t];
-            int wi = w;
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffff, wi, o);
-                if (t >= o) wi += y;
-            }
-            warp_tot[t] = wi - w;
-            if (t == 31) block_tot = wi;
-        }
-        __syncthreads();
-        int run = carry + warp_tot[t >> 5] + incl - s;
-#pragma unroll
-        for (int i = 0; i < kPer; ++i) {
-            sh[pad(t * kPer + i)] = run;
-            run += v[i];
-        }
-        __syncthreads();
-#pragma unroll
-        for (int i = t; i < kChunk; i += 1024) hist[c0 + i] = sh[pad(i)];
-        carry += block_tot;
-        __syncthreads();
+    __shared__ int prefix;
+    const int t = threadIdx.x, b = blockIdx.x;
+    const int v = hist[b * 1024 + t];
+    int incl = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffff, incl, o);
+        if ((t & 31) >= o) incl += y;
     }
+    if ((t & 31) == 31) warp_tot[t >> 5] = incl;
+    __syncthreads();
+    if (t < 32) {
+        const int w = warp_tot[t];
+        int wi = w;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffff, wi, o);
+            if (t >= o) wi += y;
+        }
+        warp_tot[t] = wi - w;
+        if (t == 31) {
+            volatile int* sums = bar + 2;
+            sums[b] = wi;  // block total
+            __threadfence();
+            atomicAdd(bar, 1);
+            while (*(volatile int*)bar < (int)gridDim.x) {
+            }
+            __threadfence();
+            int p = 0;
+            for (int i = 0; i < b; ++i) p += sums[i];
+            prefix = p;
+        }
+    }
+    __syncthreads();
+    hist[b * 1024 + t] = prefix + warp_tot[t >> 5] + incl - v;
 }
 
 // Scatter into sorted order: perm[pos] = p, xs[pos] = (x_p, 0) as float4 (16-B loads in K2).
@@ -802,15 +788,17 @@ SearchState run_search(fsk_ctx* ctx, const GridPlanes& P, const GridP& g, const 
     if (n == 0) return s;
     float4* xs = (float4*)scratch(ctx, kXs, n * sizeof(float4));
     int* esc_n = (int*)scratch(ctx, kEscN, 4 * sizeof(int));  // {-, work cursor, short count, long count}
+    // (with the spatial sort, the counters live in the sort state and are zeroed with it)
     if (!(flags & FSK_SEARCH_NO_SORT)) {
-        int* hist = (int*)scratch(ctx, kHist, kSortBuckets * sizeof(int));
-        int* bbox = (int*)scratch(ctx, kBbox, 6 * sizeof(int));
+        int* hist = (int*)scratch(ctx, kHist, kSortStateInts * sizeof(int));
+        unsigned* bbox = (unsigned*)(hist + kBboxOff);
+        esc_n = hist + kEscOff;  // zeroed with the histogram
         uint16_t* keys = (uint16_t*)scratch(ctx, kKeys, n * sizeof(uint16_t));
-        FSK_LAUNCH(ctx, st, k_sort_init, 32, 1024, 0, hist, bbox, esc_n);
+        cuda_check(cudaMemsetAsync(hist, 0, kSortStateInts * sizeof(int), st), "cudaMemsetAsync");
         const unsigned gb = (unsigned)std::min<int64_t>(blocks_for(n, 256), (int64_t)ctx->sm_count * 8);
         FSK_LAUNCH(ctx, st, k_sort_bbox, gb, 256, 0, pts, n, bbox);
         FSK_LAUNCH(ctx, st, k_sort_hist, blocks_for(n, 256), 256, 0, pts, n, bbox, keys, hist);
-        FSK_LAUNCH(ctx, st, k_sort_scan, 1, 1024, 0, hist);
+        FSK_LAUNCH(ctx, st, k_sort_scan, kScanBlocks, 1024, 0, hist, hist + kScanBarOff);
         FSK_LAUNCH(ctx, st, k_sort_scatter, blocks_for(n, 256), 256, 0, pts, keys, n, hist, s.perm, xs);
     } else {
         FSK_LAUNCH(ctx, st, k_identity_order, blocks_for(n, 256), 256, 0, pts, n, s.perm, xs, esc_n);
