@@ -36,9 +36,9 @@ UNIT = "solves/s"
 FLOPS_INIT, FLOPS_ITER, FLOPS_FINAL_SAVING = 674, 332, 66
 GATHER_BYTES = 384  # 8 corners x 48 B of transform grid per d(x) evaluation
 # dram__bytes_read.sum + dram__bytes_write.sum of one k_search_fast launch (C2), from the
-# ncu --set full capture profiles/r01_search_kernels.ncu-rep (6.9 MB read + 204.1 MB written:
+# ncu --set full capture profiles/r01_final_search.ncu-rep (6.8 MB read + 205.0 MB written:
 # the bone-major search planes; the gather itself is L1/L2-resident)
-NCU_TRAFFIC_K2 = 211.0e6
+NCU_TRAFFIC_K2 = 211.8e6
 
 
 def parse():
@@ -352,7 +352,7 @@ def run_ours(args, rank, world, local_rank):
         "roofline": {"bound": "fp32", "kernel": "k_search_fast", "achieved": achieved, "peak": peak_fp32,
                      "unit": "TFLOP/s", "frac": achieved / peak_fp32,
                      "traffic": NCU_TRAFFIC_K2 if (args.grid == "32,32,32" and args.points == 200_000) else None,
-                     "traffic_source": "ncu --set full, profiles/r01_search_kernels.ncu-rep (C2 only)",
+                     "traffic_source": "ncu --set full, profiles/r01_final_search.ncu-rep (C2 only)",
                      "peak_source": "measured live: FFMA-chain kernel over all SMs (fsk_measure_fp32_peak); "
                                     "MEASURED_PEAKS.json has no FP32 figure",
                      "algorithmic_flops_per_launch": flops, "avg_launch_ms": k2_avg,
