@@ -205,6 +205,30 @@ int fsk_search_bwd_roots(fsk_ctx* ctx, const fsk_grid_desc* desc, const fsk_root
 int fsk_grad_weights(fsk_ctx* ctx, const fsk_grid_desc* desc, const float* grad_tgrid,
                      const float* bones, int32_t n_bones_pose, float* grad_w, void* stream);
 
+/* ---- single-process multi-GPU: one context, stream and host thread per
+ * device; points shard in contiguous ranges [n*r/R, n*(r+1)/R) (the parallel_for partition,
+ * parallel.hpp:28-29); no collective on the forward; the backward sums dL/dT over the devices
+ * with one NCCL all-reduce (ncclCommInitAll communicator, created on first use). */
+typedef struct fsk_multi fsk_multi;
+int fsk_multi_create(int32_t n_devices, const int32_t* devices, fsk_multi** out);
+int fsk_multi_destroy(fsk_multi* m);
+int32_t fsk_multi_device_count(const fsk_multi* m);
+
+/* fsk_deform_host over all devices: HOST buffers in/out, results identical to the one-device
+ * call (CorrespondenceSets in query order; offsets [N+1], roots [cap], *total_out). */
+int fsk_multi_deform_host(fsk_multi* m, const float* weights, const fsk_grid_desc* desc, const float* bones,
+                          int32_t n_bones_pose, const float* points, int64_t n, const fsk_search_opts* opts,
+                          int64_t* offsets, fsk_root* roots, int64_t cap, int64_t* total_out);
+
+/* Training-step backward over all devices from HOST buffers: root_index [N] selects
+ * roots[root_index[p]] (or -1) as x*, J~ of query p; grad_xc [N][3] = dL/dx*. Each device runs
+ * K3 on its query shard into dL/dT, NCCL sums dL/dT, device 0 contracts to grad_w [V][n_b]
+ * (host). Equal to fsk_search_bwd_roots + fsk_grad_weights on one device up to the order of
+ * the float sums (bitwise for one device). */
+int fsk_multi_grad_weights_host(fsk_multi* m, const fsk_grid_desc* desc, const float* bones, int32_t n_bones_pose,
+                                const fsk_root* roots, const int64_t* root_index, const float* grad_xc, int64_t n,
+                                float* grad_w, int deterministic);
+
 /* ---- MLP stages next to the search, tcgen05 tensor cores, 3xTF32 (FP32-faithful).
  * theta: the network's flat parameter vector in Mlp::parameters() order (mlp.cpp:207-219: per
  * layer W column-major [out x in], then b), float32, device. widths: host array {in, H, ..., out}

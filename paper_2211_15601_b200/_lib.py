@@ -26,6 +26,8 @@ EXPORTS = [
     "fsk_ctx_set_profiling", "fsk_ctx_prof_read", "fsk_measure_fp32_peak", "fsk_batch_search", "fsk_deform",
     "fsk_search_bwd_roots", "fsk_ctx_search_stats", "fsk_measure_fp64_peak", "fsk_measure_l1_gather_peak",
     "fsk_distill", "fsk_posed_occupancy", "fsk_distill_bwd",
+    "fsk_multi_create", "fsk_multi_destroy", "fsk_multi_device_count", "fsk_multi_deform_host",
+    "fsk_multi_grad_weights_host",
 ]
 
 
@@ -101,6 +103,12 @@ def load():
     L.fsk_measure_l1_gather_peak.argtypes = [_vp, ctypes.POINTER(ctypes.c_double)]
     L.fsk_distill.argtypes = [_vp, _vp, _vp, _i32, G, _vp, _vp]
     L.fsk_distill_bwd.argtypes = [_vp, _vp, _vp, _i32, G, _vp, _vp, _vp]
+    L.fsk_multi_create.argtypes = [_i32, _vp, ctypes.POINTER(_vp)]
+    L.fsk_multi_destroy.argtypes = [_vp]
+    L.fsk_multi_device_count.argtypes = [_vp]
+    L.fsk_multi_device_count.restype = _i32
+    L.fsk_multi_deform_host.argtypes = [_vp, _vp, G, _vp, _i32, _vp, _i64, O, _vp, _vp, _i64, ctypes.POINTER(_i64)]
+    L.fsk_multi_grad_weights_host.argtypes = [_vp, G, _vp, _i32, _vp, _vp, _vp, _i64, _vp, ctypes.c_int]
     L.fsk_posed_occupancy.argtypes = [_vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp]
     _lib = L
     return L

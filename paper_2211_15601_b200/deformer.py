@@ -367,3 +367,49 @@ class Deformer:
                                      points.shape[0], ctypes.byref(opts.c()), _ptr(offsets), _ptr(roots),
                                      roots.shape[0], ctypes.byref(total), _stream(self.device)))
         return total.value
+
+
+class MultiDeformer:
+    """Single-process multi-GPU C-ABI (``fsk_multi_*``): one context, stream and host thread
+    per device, points sharded in contiguous ranges (parallel.hpp:28-29), NCCL all-reduce of
+    dL/dT in the backward. Host (pinned or pageable) buffers in and out."""
+
+    def __init__(self, devices):
+        self.L = _lib.load()
+        self._m = ctypes.c_void_p()
+        devs = (ctypes.c_int32 * len(devices))(*devices)
+        check(self.L.fsk_multi_create(len(devices), devs, ctypes.byref(self._m)))
+
+    @property
+    def device_count(self) -> int:
+        return int(self.L.fsk_multi_device_count(self._m))
+
+    def close(self):
+        if self._m:
+            self.L.fsk_multi_destroy(self._m)
+            self._m = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def deform_host(self, weights, dims, bbox, bones, points, opts: SearchOptions, offsets, roots):
+        nb = bones.numel() // 12
+        desc = grid_desc(dims, bbox, nb)
+        total = ctypes.c_int64()
+        check(self.L.fsk_multi_deform_host(self._m, _ptr(weights), ctypes.byref(desc), _ptr(bones), nb, _ptr(points),
+                                           points.shape[0], ctypes.byref(opts.c()), _ptr(offsets), _ptr(roots),
+                                           roots.shape[0], ctypes.byref(total)))
+        return total.value
+
+    def grad_weights_host(self, dims, bbox, bones, roots, root_index, grad_xc, deterministic=False):
+        nb = bones.numel() // 12
+        desc = grid_desc(dims, bbox, nb)
+        V = desc.nx * desc.ny * desc.nz
+        out = torch.empty((V, nb), dtype=torch.float32)
+        check(self.L.fsk_multi_grad_weights_host(self._m, ctypes.byref(desc), _ptr(bones), nb, _ptr(roots),
+                                                 _ptr(root_index), _ptr(grad_xc), grad_xc.shape[0], _ptr(out),
+                                                 1 if deterministic else 0))
+        return out
