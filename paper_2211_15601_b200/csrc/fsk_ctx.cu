@@ -238,6 +238,7 @@ int fsk_ctx_destroy(fsk_ctx* ctx) {
         for (auto& e : ctx->pool) cudaEventDestroy(e);
         if (ctx->stats) cudaFree(ctx->stats);
         if (ctx->copy) cudaStreamDestroy(ctx->copy);
+        if (ctx->upload) cudaStreamDestroy(ctx->upload);
         if (ctx->blas) cublasDestroy(ctx->blas);
         if (ctx->hcount) cudaFreeHost(ctx->hcount);
         delete ctx;

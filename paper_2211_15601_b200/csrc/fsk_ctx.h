@@ -38,6 +38,7 @@ struct fsk_ctx {
     unsigned long long* stats = nullptr;
     // device→host copy stream of the host-buffer entry point (created on first use)
     cudaStream_t copy = nullptr;
+    cudaStream_t upload = nullptr;  // host→device stream of the host-buffer entry point
     int64_t* hcount = nullptr;  // pinned per-chunk root counts
     cublasContext* blas = nullptr;  // FP32 GEMMs of the distill backward (created on first use)
 };

@@ -976,7 +976,10 @@ int fsk_deform_host(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* des
         // while the CorrespondenceSets of finished chunks stream to the host on the copy stream.
         // Each chunk pays its own launches and float64-tail, so batches below 2M queries stay
         // whole (measured on C2, 200k queries: 4 chunks 1.99 ms vs 1 chunk 1.63 ms).
-        const int64_t nchunks = std::max<int64_t>(1, std::min<int64_t>(8, n / (1 << 21)));
+        int64_t nchunks = std::max<int64_t>(1, std::min<int64_t>(8, n / (1 << 21)));
+        if (const char* e = getenv("FSK_HOST_CHUNKS"))  // tuning override
+            nchunks = std::max<int64_t>(1, std::min<int64_t>(64, atoll(e)));
+        if (n < nchunks) nchunks = std::max<int64_t>(1, n);
         const int64_t csz = (n + nchunks - 1) / nchunks;
         float* dW = (float*)scratch(ctx, kHW, V * nb * sizeof(float));
         float* dB = (float*)scratch(ctx, kHB, nb * 12 * sizeof(float));
@@ -985,27 +988,43 @@ int fsk_deform_host(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* des
         // every root a query can have fits: no second pass after the count is known
         fsk_root* dR = (fsk_root*)scratch(ctx, kHRoots, std::max<int64_t>(1, n * nb) * sizeof(fsk_root));
         if (!ctx->copy) cuda_check(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking), "cudaStreamCreate");
+        if (!ctx->upload)
+            cuda_check(cudaStreamCreateWithFlags(&ctx->upload, cudaStreamNonBlocking), "cudaStreamCreate");
         if (!ctx->hcount) cuda_check(cudaMallocHost(&ctx->hcount, 64 * sizeof(int64_t)), "cudaMallocHost");
         cuda_check(cudaMemcpyAsync(dW, weights, V * nb * sizeof(float), cudaMemcpyHostToDevice, st), "H2D weights");
         cuda_check(cudaMemcpyAsync(dB, bones, nb * 12 * sizeof(float), cudaMemcpyHostToDevice, st), "H2D bones");
-        if (n > 0)
-            cuda_check(cudaMemcpyAsync(dP, points, n * 3 * sizeof(float), cudaMemcpyHostToDevice, st), "H2D points");
-        const GridPlanes P = run_precompute(ctx, dW, g, dB, nullptr, nullptr, true, needs_f64(opts->flags), st);
-        std::vector<cudaEvent_t> done(nchunks), offs_ready(nchunks);
+        std::vector<cudaEvent_t> done(nchunks), offs_ready(nchunks), up(nchunks);
         for (int64_t c = 0; c < nchunks; ++c) {
             cuda_check(cudaEventCreateWithFlags(&done[c], cudaEventDisableTiming), "cudaEventCreate");
             cuda_check(cudaEventCreateWithFlags(&offs_ready[c], cudaEventDisableTiming), "cudaEventCreate");
+            cuda_check(cudaEventCreateWithFlags(&up[c], cudaEventDisableTiming), "cudaEventCreate");
         }
         struct Events {
             std::vector<cudaEvent_t>* a;
             std::vector<cudaEvent_t>* b;
+            std::vector<cudaEvent_t>* c;
             ~Events() {
                 for (auto e : *a) cudaEventDestroy(e);
                 for (auto e : *b) cudaEventDestroy(e);
+                for (auto e : *c) cudaEventDestroy(e);
             }
-        } cleanup{&done, &offs_ready};
+        } cleanup{&done, &offs_ready, &up};
+        // each chunk's points upload on their own stream, ahead of (and overlapping) the
+        // previous chunks' searches
+        cuda_check(cudaEventRecord(up[0], st), "cudaEventRecord");
+        cuda_check(cudaStreamWaitEvent(ctx->upload, up[0], 0), "cudaStreamWaitEvent");  // order after prior use
         for (int64_t c = 0; c < nchunks; ++c) {
             const int64_t p0 = c * csz, m = std::max<int64_t>(0, std::min(csz, n - p0));
+            if (m > 0)
+                cuda_check(cudaMemcpyAsync(dP + 3 * p0, points + 3 * p0, m * 3 * sizeof(float), cudaMemcpyHostToDevice,
+                                           ctx->upload),
+                           "H2D points");
+            cuda_check(cudaEventRecord(up[c], ctx->upload), "cudaEventRecord");
+        }
+        const GridPlanes P = run_precompute(ctx, dW, g, dB, nullptr, nullptr, true, needs_f64(opts->flags), st);
+        for (int64_t c = 0; c < nchunks; ++c) {
+            const int64_t p0 = c * csz, m = std::max<int64_t>(0, std::min(csz, n - p0));
+            cuda_check(cudaStreamWaitEvent(st, up[c], 0), "cudaStreamWaitEvent");
             const SearchState s = run_search(ctx, P, g, dB, dP + 3 * p0, m, sp, opts->flags, st);
             compact(ctx, s, m, nb, dOff + p0 + c, dR + p0 * nb, m * nb, st);
             cuda_check(cudaEventRecord(done[c], st), "cudaEventRecord");
@@ -1031,7 +1050,8 @@ int fsk_deform_host(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* des
                                            ctx->copy),
                            "D2H roots");
             }
-            for (int64_t i = 0; i < m; ++i) offsets[p0 + i] += base;
+            if (base)
+                for (int64_t i = 0; i < m; ++i) offsets[p0 + i] += base;
             base += cnt;
         }
         offsets[n] = base;
