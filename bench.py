@@ -322,11 +322,11 @@ def run_ours(args, rank, world, local_rank):
     # algorithmic work per step, counted by the kernels themselves (identical every step):
     # float32 pass (k_search_fast) and float64 escalation pass (k_search_escalated)
     per = max(args.steps, 1) * args.poses  # counters per search launch (one launch per pose)
-    s32, it32, fin32, s64, it64, fin64 = (v / per for v in st)
+    s32, it32, fin32, s64, it64, fin64, fills32 = (v / per for v in st)
     solves = n * nb * args.poses
     flops = s32 * FLOPS_INIT + it32 * FLOPS_ITER - fin32 * FLOPS_FINAL_SAVING
     flops64 = s64 * FLOPS_INIT + it64 * FLOPS_ITER - fin64 * FLOPS_FINAL_SAVING
-    gather = (s32 + it32) * GATHER_BYTES
+    gather = (s32 + fills32) * GATHER_BYTES  # inits + iteration gathers (cache misses)
     k2_avg = k2_ms / max(k2_n, 1)
     achieved = flops / (k2_avg * 1e-3) / 1e12
     V = w.shape[0]
@@ -369,7 +369,9 @@ def run_ours(args, rank, world, local_rank):
                                 "frac": gather / (k2_avg * 1e-3) / 1e9 / peak_l1,
                                 "peak_source": "fsk_measure_l1_gather_peak: independent LDG.256 at random "
                                                "32-B slots of an L1-resident table, all SMs",
-                                "note": "the binding resource of k_search_fast per ncu (L1 data pipe 92 %)"},
+                                "cell_cache_hit_frac": 1 - fills32 / max(it32, 1),
+                                "note": "bytes actually gathered (init + iterations that left the register-cached "
+                                        "cell); ncu: L1 data pipe 68 %, issue slots 47 % (profiles/r01_final_summary.md)"},
                      "k2_share_of_step": k2_ms / max(all_ms, 1e-9),
                      "k2_escalated_share_of_step": k2e_ms / max(all_ms, 1e-9),
                      "kernel_ms_per_step": breakdown,

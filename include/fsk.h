@@ -109,8 +109,9 @@ int fsk_measure_fp64_peak(fsk_ctx* ctx, double* tflops);  /* same with DFMA chai
 int fsk_measure_l1_gather_peak(fsk_ctx* ctx, double* gbps);
 /* Search work counters accumulated by the context's searches (synchronizes the device):
  * out = {float32 solves, float32 Broyden iterations, float32 converged-terminating
- * iterations, float64 solves, float64 iterations, float64 converged-terminating iterations}. */
-int fsk_ctx_search_stats(fsk_ctx* ctx, uint64_t out[6], int reset);
+ * iterations, float64 solves, float64 iterations, float64 converged-terminating iterations,
+ * float32 iteration gathers (re-evaluations that left the cell cached in registers)}. */
+int fsk_ctx_search_stats(fsk_ctx* ctx, uint64_t out[7], int reset);
 
 /* SearchOptions::defaults_for (correspondence.cpp:10-17): conv 1e-5*diag,
  * div 0.5*diag, dedup 1e-2*diag, max_iters 50. */

@@ -282,14 +282,14 @@ int fsk_ctx_prof_read(fsk_ctx* ctx, const char* name, double* total_ms, int64_t*
     });
 }
 
-int fsk_ctx_search_stats(fsk_ctx* ctx, uint64_t out[6], int reset) {
+int fsk_ctx_search_stats(fsk_ctx* ctx, uint64_t out[7], int reset) {
     return guard([&] {
         set_device(ctx);
         if (!out) fail(FSK_EINVAL, "fsk: null output pointer");
         cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
         unsigned long long h[8];
         cuda_check(cudaMemcpy(h, ctx->stats, sizeof(h), cudaMemcpyDeviceToHost), "cudaMemcpy");
-        for (int i = 0; i < 6; ++i) out[i] = h[i];
+        for (int i = 0; i < 7; ++i) out[i] = h[i];
         if (reset) cuda_check(cudaMemset(ctx->stats, 0, sizeof(h)), "cudaMemset");
     });
 }

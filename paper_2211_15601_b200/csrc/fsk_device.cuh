@@ -347,6 +347,7 @@ struct SolveOut {
     bool conv;
     bool esc;
     bool capped;  // escalated because the float32 pass hit its iteration cap (a long trajectory)
+    int fills = 0;  // iteration gathers (cell-cache misses) of the float32 pass
 };
 
 // One Broyden iteration after the divergence check (correspondence.cpp:106-122): step,
@@ -355,7 +356,8 @@ struct SolveOut {
 template <typename R, bool kCache = false>
 __device__ __forceinline__ bool broyden_step(const Planes<R>& P, const GridP& g, R xp0, R xp1, R xp2, R conv2, R& x0,
                                              R& x1, R& x2, R Ji[9], R& g0, R& g1, R& g2, R& err2, R& den,
-                                             CellCache<R>* C = nullptr, R cos2 = 0, bool* degenerate = nullptr) {
+                                             CellCache<R>* C = nullptr, R cos2 = 0, bool* degenerate = nullptr,
+                                             int* fills = nullptr) {
     // dx = −J~ g; x += dx (:106-107)
     const R dx0 = -(Ji[0] * g0 + Ji[1] * g1 + Ji[2] * g2);
     const R dx1 = -(Ji[3] * g0 + Ji[4] * g1 + Ji[5] * g2);
@@ -367,7 +369,10 @@ __device__ __forceinline__ bool broyden_step(const Planes<R>& P, const GridP& g,
     R T[12], d[3];
     const Cell<R> c = locate<false, R>(g, x0, x1, x2);
     if constexpr (kCache) {
-        if (c.base != C->base) cache_fill(P, g, c.base, *C);
+        if (c.base != C->base) {
+            cache_fill(P, g, c.base, *C);
+            if (fills) ++*fills;
+        }
         trilerp_cached(*C, c, T);
     } else {
         trilerp_T(P, g, c, T);
@@ -432,6 +437,7 @@ __device__ __forceinline__ SolveOut solve_one(const Planes<R>& P, const GridP& g
     const R det = solve_start<R, kCache>(P, g, B, xp0, xp1, xp2, x0, x1, x2, Ji, g0, g1, g2, err2, &cache);
     const R conv2 = (R)o.conv2, div2 = (R)o.div2;
     bool esc = false, capped = false;
+    int fills = 0;
     auto near = [&](R e2) {
         return (e2 >= (R)o.esc_conv_lo * conv2 && e2 <= (R)o.esc_conv_hi * conv2) ||
                (e2 >= (R)o.esc_div_lo * div2 && e2 <= (R)o.esc_div_hi * div2);
@@ -453,7 +459,7 @@ __device__ __forceinline__ SolveOut solve_one(const Planes<R>& P, const GridP& g
             }
             R den;
             const bool c = broyden_step<R, kCache>(P, g, xp0, xp1, xp2, conv2, x0, x1, x2, Ji, g0, g1, g2, err2, den,
-                                                   &cache, (R)o.esc_cos2, kFast ? &esc : nullptr);
+                                                   &cache, (R)o.esc_cos2, kFast ? &esc : nullptr, &fills);
             iters = k + 1;
             if (kFast && near(err2)) esc = true;
             if (c) {
@@ -487,7 +493,7 @@ __device__ __forceinline__ SolveOut solve_one(const Planes<R>& P, const GridP& g
             if (d0 * d0 + d1 * d1 + d2 * d2 > tau2) esc = true;
         }
     }
-    return SolveOut{iters, conv, esc, capped};
+    return SolveOut{iters, conv, esc, capped, fills};
 }
 
 }  // namespace fsk

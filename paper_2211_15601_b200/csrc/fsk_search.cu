@@ -302,10 +302,12 @@ __device__ __forceinline__ void count_work(unsigned long long* stats, const Solv
     const unsigned act = __activemask();
     const unsigned it = __reduce_add_sync(act, (unsigned)s.iters);
     const unsigned fin = __reduce_add_sync(act, (unsigned)(s.conv && s.iters > 0));
+    const unsigned fl = __reduce_add_sync(act, (unsigned)s.fills);
     if ((threadIdx.x & 31) == __ffs(act) - 1) {
         atomicAdd(stats + 0, (unsigned long long)__popc(act));
         atomicAdd(stats + 1, (unsigned long long)it);
         atomicAdd(stats + 2, (unsigned long long)fin);
+        if (fl) atomicAdd(stats + 6, (unsigned long long)fl);
     }
 }
 

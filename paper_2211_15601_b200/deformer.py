@@ -132,8 +132,9 @@ class Deformer:
 
     def search_stats(self, reset=True):
         """(f32 solves, f32 iterations, f32 converged-terminating iterations, f64 solves,
-        f64 iterations, f64 converged-terminating iterations) accumulated by searches."""
-        buf = (ctypes.c_uint64 * 6)()
+        f64 iterations, f64 converged-terminating iterations, f32 iteration gathers)
+        accumulated by searches."""
+        buf = (ctypes.c_uint64 * 7)()
         check(self.L.fsk_ctx_search_stats(self._ctx, buf, 1 if reset else 0))
         return tuple(int(v) for v in buf)
 
