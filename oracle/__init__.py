@@ -55,6 +55,9 @@ def lib():
         L.orc_distill.argtypes = [_d, _pi, _int, _int, _int, _int, _d, _d, _int]
         L.orc_distill_vjp.argtypes = [_d, _pi, _int, _int, _int, _int, _d, _d, _d, _int]
         L.orc_posed_occupancy.argtypes = [_d, _pi, _int, _d, _int, _pi64, _d, _i64, _d, _i32, _int]
+        L.orc_mlp_weights_jacobian.argtypes = [_d, _pi, _int, _d, _i64, _d, _d, _int]
+        L.orc_batch_search_mlp.argtypes = [_d, _pi, _int, _d, _int, _d, _i64, _int, ctypes.c_double,
+                                           ctypes.c_double, ctypes.c_double, _int, _d, _d, _d, _i32, _u8, _u8]
         _lib = L
     return _lib
 
@@ -226,3 +229,27 @@ def posed_occupancy(theta, widths, pose, offsets, roots_x, workers=8):
                                          offs.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
                                          _p(_f64(roots_x).reshape(-1, 3)), n, _p(pred), _p(am, _i32), workers))
     return pred, am
+
+
+def mlp_weights_jacobian(theta, widths, x, workers=8):
+    """SkinningMlp::weights and weight_jacobian (skinning.cpp:41-64) at x [n,3]."""
+    x = _f64(x).reshape(-1, 3)
+    n, nb = x.shape[0], widths[-1]
+    w, dw = np.zeros((n, nb)), np.zeros((n, nb, 3))
+    _mlp_check(lib().orc_mlp_weights_jacobian(_p(_f64(theta)), _widths(widths), len(widths), _p(x), n, _p(w), _p(dw),
+                                              workers))
+    return w, dw
+
+
+def batch_search_mlp(theta, widths, bones, x_prime, max_iters, conv_eps, div_eps, dedup_dist, workers=8):
+    """batch_search with SearchVariant::Mlp (correspondence.cpp:126-192), dense outputs."""
+    B, x = _f64(bones).reshape(-1, 12), _f64(x_prime).reshape(-1, 3)
+    n, nb = x.shape[0], B.shape[0]
+    out = dict(x_c=np.zeros((n, nb, 3)), jinv=np.zeros((n, nb, 3, 3)), resid=np.zeros((n, nb)),
+               iters=np.zeros((n, nb), np.int32), converged=np.zeros((n, nb), np.uint8),
+               keep=np.zeros((n, nb), np.uint8))
+    _mlp_check(lib().orc_batch_search_mlp(_p(_f64(theta)), _widths(widths), len(widths), _p(B), nb, _p(x), n,
+                                          int(max_iters), conv_eps, div_eps, dedup_dist, workers, _p(out["x_c"]),
+                                          _p(out["jinv"]), _p(out["resid"]), _p(out["iters"], _i32),
+                                          _p(out["converged"], _u8), _p(out["keep"], _u8)))
+    return out

@@ -12,6 +12,11 @@
 //     vertices in place of the roots);
 //   * OccupancyMlp::occupancy_batch (proj/src/shape.cpp:218-228) and posed_occupancy_batch
 //     (:242-269): max over each query's roots, first root wins ties, argmax -1 when empty.
+//   * the MLP variant of the search (SearchVariant::Mlp): eval_deform via
+//     forward_deform(x, mlp, bones) (deformer.cpp:22-26, correspondence.cpp:77-79), the initial
+//     Jacobian deform_jacobian(x, mlp, bones) (deformer.cpp:117-141) with
+//     SkinningMlp::weight_jacobian (skinning.cpp:53-64, Mlp::input_tangent mlp.cpp:142-155),
+//     iterate (correspondence.cpp:97-124), search_one / dedup_roots (:126-176).
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
@@ -102,6 +107,35 @@ struct Net {
             delta = std::move(d);
         }
     }
+    // weights w = softmax(net(x)) and dw/dx [nb][3] (SkinningMlp::weight_jacobian,
+    // skinning.cpp:53-64: Mlp::input_tangent then the softmax Jacobian)
+    void weights_and_jacobian(const double* x, std::vector<double>& w, std::vector<double>& dw) const {
+        std::vector<std::vector<double>> pre, act;
+        forward(x, pre, act);
+        const int nb = w_out();
+        w = pre.back();
+        softmax_inplace(w.data(), nb);
+        dw.assign((size_t)nb * 3, 0.0);
+        for (int c = 0; c < 3; ++c) {
+            std::vector<double> t(this->w[0], 0.0);
+            t[c] = 1.0;
+            for (int l = 0; l < layers(); ++l) {
+                std::vector<double> u(this->w[l + 1]);
+                for (int r = 0; r < this->w[l + 1]; ++r) {
+                    double acc = 0.0;
+                    for (int k = 0; k < this->w[l]; ++k) acc += Wat(l, r, k) * t[k];
+                    u[r] = acc;
+                }
+                if (l + 1 < layers())
+                    for (int r = 0; r < this->w[l + 1]; ++r) u[r] *= sigmoid(pre[l][r]);
+                t = std::move(u);
+            }
+            double dot = 0.0;
+            for (int i = 0; i < nb; ++i) dot += w[i] * t[i];
+            for (int i = 0; i < nb; ++i) dw[(size_t)i * 3 + c] = w[i] * (t[i] - dot);
+        }
+    }
+    int w_out() const { return w.back(); }
     int64_t n_params() const {
         int64_t n = 0;
         for (int l = 0; l < layers(); ++l) n += (int64_t)w[l + 1] * w[l] + w[l + 1];
@@ -244,6 +278,174 @@ int orc_posed_occupancy(const double* theta, const int* widths, int nw, const do
                         argmax[q] = (int32_t)(r - offsets[q]);
                         first = false;
                     }
+                }
+            }
+        });
+    });
+}
+
+// ---------------------------------------------------------------- MLP-variant search
+namespace {
+struct MB {  // rigid bone [R|t] (row-major 3x4)
+    double R[9], t[3];
+};
+// forward_deform(x, mlp, bones) = lbs_blend(w(x), B)·x (deformer.cpp:9-19, :22-26)
+void mlp_deform(const Net& net, const std::vector<MB>& B, const double* x, double* d, std::vector<double>& w,
+                std::vector<double>* dw) {
+    if (dw) {
+        net.weights_and_jacobian(x, w, *dw);
+    } else {
+        std::vector<std::vector<double>> pre, act;
+        net.forward(x, pre, act);
+        w = pre.back();
+        softmax_inplace(w.data(), (int)w.size());
+    }
+    double M[9] = {0}, T[3] = {0};
+    for (size_t i = 0; i < B.size(); ++i) {
+        for (int e = 0; e < 9; ++e) M[e] += w[i] * B[i].R[e];
+        for (int e = 0; e < 3; ++e) T[e] += w[i] * B[i].t[e];
+    }
+    for (int r = 0; r < 3; ++r) d[r] = M[3 * r] * x[0] + M[3 * r + 1] * x[1] + M[3 * r + 2] * x[2] + T[r];
+}
+}  // namespace
+
+// SkinningMlp::weights / weight_jacobian at points x [n][3]: w [n][nb], dw [n][nb][3]
+int orc_mlp_weights_jacobian(const double* theta, const int* widths, int nw, const double* x, int64_t n, double* w_out,
+                             double* dw_out, int workers) {
+    return guard([&] {
+        const Net net(theta, widths, nw);
+        const int nb = widths[nw - 1];
+        parallel_for(n, workers, [&](int64_t p0, int64_t p1, int) {
+            std::vector<double> w, dw;
+            for (int64_t p = p0; p < p1; ++p) {
+                net.weights_and_jacobian(x + 3 * p, w, dw);
+                std::copy(w.begin(), w.end(), w_out + p * nb);
+                std::copy(dw.begin(), dw.end(), dw_out + p * nb * 3);
+            }
+        });
+    });
+}
+
+// batch_search with SearchVariant::Mlp (correspondence.cpp:126-192), dense per-(point, init)
+// outputs like orc_batch_search.
+int orc_batch_search_mlp(const double* theta, const int* widths, int nw, const double* bones, int n_bones,
+                         const double* x_prime, int64_t n, int max_iters, double conv_eps, double div_eps,
+                         double dedup_dist, int workers, double* x_c, double* jinv, double* resid, int32_t* iters,
+                         uint8_t* converged, uint8_t* keep) {
+    return guard([&] {
+        if (n_bones < 1) throw std::invalid_argument("search: no bone transforms");
+        if (widths[0] != 3) throw std::invalid_argument("SkinningMlp: network input width must be 3");
+        if (widths[nw - 1] != n_bones) throw std::invalid_argument("search: mlp bone count mismatch");
+        if (max_iters < 1) throw std::invalid_argument("search: max_iters must be >= 1");
+        if (!(conv_eps > 0.0)) throw std::invalid_argument("search: conv_eps must be > 0");
+        if (!(div_eps > conv_eps)) throw std::invalid_argument("search: div_eps must exceed conv_eps");
+        if (!(dedup_dist >= 0.0)) throw std::invalid_argument("search: dedup_dist must be >= 0");
+        const Net net(theta, widths, nw);
+        std::vector<MB> B(n_bones);
+        for (int i = 0; i < n_bones; ++i)
+            for (int r = 0; r < 3; ++r) {
+                for (int c = 0; c < 3; ++c) B[i].R[3 * r + c] = bones[12 * i + 4 * r + c];
+                B[i].t[r] = bones[12 * i + 4 * r + 3];
+            }
+        const int nb = n_bones;
+        parallel_for(n, workers, [&](int64_t p0, int64_t p1, int) {
+            std::vector<double> w, dw;
+            for (int64_t p = p0; p < p1; ++p) {
+                const double* xp = x_prime + 3 * p;
+                std::vector<double> xs(3 * nb);
+                std::vector<uint8_t> cv(nb);
+                for (int i = 0; i < nb; ++i) {
+                    const MB& b = B[i];
+                    // x0 = B_i^-1 x' = Rᵀ x' + (−Rᵀ t) (geometry.hpp:58-61)
+                    double x[3], it[3];
+                    for (int a = 0; a < 3; ++a) it[a] = -(b.R[a] * b.t[0] + b.R[3 + a] * b.t[1] + b.R[6 + a] * b.t[2]);
+                    for (int a = 0; a < 3; ++a) x[a] = b.R[a] * xp[0] + b.R[3 + a] * xp[1] + b.R[6 + a] * xp[2] + it[a];
+                    // J = Σ w_i R_i + Σ (B_i x)(∇w_i)ᵀ (deformer.cpp:117-128), inverse or I (:43-54)
+                    double d[3];
+                    mlp_deform(net, B, x, d, w, &dw);
+                    double J[9] = {0};
+                    for (int k = 0; k < nb; ++k)
+                        for (int e = 0; e < 9; ++e) J[e] += w[k] * B[k].R[e];
+                    for (int k = 0; k < nb; ++k) {
+                        double bx[3];
+                        for (int r = 0; r < 3; ++r)
+                            bx[r] = B[k].R[3 * r] * x[0] + B[k].R[3 * r + 1] * x[1] + B[k].R[3 * r + 2] * x[2] + B[k].t[r];
+                        for (int r = 0; r < 3; ++r)
+                            for (int c = 0; c < 3; ++c) J[3 * r + c] += bx[r] * dw[(size_t)k * 3 + c];
+                    }
+                    double Ji[9];
+                    const double c00 = J[4] * J[8] - J[5] * J[7], c01 = J[2] * J[7] - J[1] * J[8],
+                                 c02 = J[1] * J[5] - J[2] * J[4], c10 = J[5] * J[6] - J[3] * J[8],
+                                 c11 = J[0] * J[8] - J[2] * J[6], c12 = J[2] * J[3] - J[0] * J[5],
+                                 c20 = J[3] * J[7] - J[4] * J[6], c21 = J[1] * J[6] - J[0] * J[7],
+                                 c22 = J[0] * J[4] - J[1] * J[3];
+                    const double det = J[0] * c00 + J[1] * c10 + J[2] * c20;
+                    if (std::abs(det) < 1e-8) {
+                        for (int e = 0; e < 9; ++e) Ji[e] = (e % 4 == 0) ? 1.0 : 0.0;
+                    } else {
+                        const double cc[9] = {c00, c01, c02, c10, c11, c12, c20, c21, c22};
+                        for (int e = 0; e < 9; ++e) Ji[e] = cc[e] / det;
+                    }
+                    double g[3] = {d[0] - xp[0], d[1] - xp[1], d[2] - xp[2]};
+                    // iterate (correspondence.cpp:97-124)
+                    int k_it = 0;
+                    bool conv = false;
+                    double err = std::sqrt(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
+                    if (err < conv_eps) conv = true;
+                    for (int k = 0; !conv && k < max_iters; ++k) {
+                        if (err > div_eps) break;
+                        double dx[3];
+                        for (int r = 0; r < 3; ++r) dx[r] = -(Ji[3 * r] * g[0] + Ji[3 * r + 1] * g[1] + Ji[3 * r + 2] * g[2]);
+                        for (int a = 0; a < 3; ++a) x[a] += dx[a];
+                        mlp_deform(net, B, x, d, w, nullptr);
+                        double dg[3];
+                        for (int a = 0; a < 3; ++a) {
+                            const double gn = d[a] - xp[a];
+                            dg[a] = gn - g[a];
+                            g[a] = gn;
+                        }
+                        k_it = k + 1;
+                        err = std::sqrt(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
+                        if (err < conv_eps) {
+                            conv = true;
+                            break;
+                        }
+                        double jdg[3];
+                        for (int r = 0; r < 3; ++r) jdg[r] = Ji[3 * r] * dg[0] + Ji[3 * r + 1] * dg[1] + Ji[3 * r + 2] * dg[2];
+                        const double den = dx[0] * jdg[0] + dx[1] * jdg[1] + dx[2] * jdg[2];
+                        if (std::abs(den) > 1e-18) {
+                            double q[3], wr[3];
+                            for (int r = 0; r < 3; ++r) q[r] = (dx[r] - jdg[r]) / den;
+                            for (int c = 0; c < 3; ++c) wr[c] = dx[0] * Ji[c] + dx[1] * Ji[3 + c] + dx[2] * Ji[6 + c];
+                            for (int r = 0; r < 3; ++r)
+                                for (int c = 0; c < 3; ++c) Ji[3 * r + c] += q[r] * wr[c];
+                        }
+                    }
+                    const int64_t s = p * nb + i;
+                    for (int a = 0; a < 3; ++a) x_c[3 * s + a] = xs[3 * i + a] = x[a];
+                    if (jinv)
+                        for (int e = 0; e < 9; ++e) jinv[9 * s + e] = Ji[e];
+                    if (resid) resid[s] = err;
+                    if (iters) iters[s] = k_it;
+                    converged[s] = cv[i] = conv ? 1 : 0;
+                }
+                // dedup_roots (correspondence.cpp:162-176) over the converged inits in bone order
+                std::vector<int> kept;
+                for (int i = 0; i < nb; ++i) {
+                    uint8_t kk = 0;
+                    if (cv[i]) {
+                        kk = 1;
+                        for (int j : kept) {
+                            const double e0 = xs[3 * i] - xs[3 * j], e1 = xs[3 * i + 1] - xs[3 * j + 1],
+                                         e2 = xs[3 * i + 2] - xs[3 * j + 2];
+                            if (std::sqrt(e0 * e0 + e1 * e1 + e2 * e2) < dedup_dist) {
+                                kk = 0;
+                                break;
+                            }
+                        }
+                        if (kk) kept.push_back(i);
+                    }
+                    if (keep) keep[p * nb + i] = kk;
                 }
             }
         });

@@ -434,3 +434,34 @@ def test_oracle_posed_occupancy_semantics():
             assert am[q] == int(np.argmax(occ[a:b]))  # numpy argmax = first maximum
     with pytest.raises(oracle.OracleInvalidArgument, match="pose vector length 1, field conditioned on 0"):
         oracle.posed_occupancy(th, widths, np.zeros(1), offs, x)
+
+
+def test_oracle_mlp_weight_jacobian_matches_finite_differences():
+    widths = [3, 64, 64, 64, 24]
+    th = oracle.mlp_init(widths, 6, 0.5)
+    x = np.random.default_rng(2).uniform(-1, 1, (20, 3))
+    w, dw = oracle.mlp_weights_jacobian(th, widths, x)
+    sm = lambda z: np.exp(z - z.max(1, keepdims=True)) / np.exp(z - z.max(1, keepdims=True)).sum(1, keepdims=True)  # noqa: E731
+    assert np.allclose(w, sm(oracle.mlp_forward(th, widths, x)), atol=1e-14)
+    for c in range(3):
+        e = np.zeros(3)
+        e[c] = 1e-6
+        fd = (sm(oracle.mlp_forward(th, widths, x + e)) - sm(oracle.mlp_forward(th, widths, x - e))) / 2e-6
+        assert np.abs(fd - dw[:, :, c]).max() <= 1e-7
+
+
+def test_oracle_mlp_variant_known_answers():
+    """SPEC.md:273-274 for the MLP variant: identity pose -> one root = the query; a single
+    rigid bone -> the exact inverse (w = 1 whatever the network)."""
+    widths = [3, 16, 16, 3]
+    th = oracle.mlp_init(widths, 1)
+    rng = np.random.default_rng(3)
+    x = rng.uniform(-1, 1, (50, 3))
+    ident = np.tile(np.array([1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0.0]), (3, 1))
+    r = oracle.batch_search_mlp(th, widths, ident, x, 50, 1e-5, 1.0, 1e-2)
+    assert (r["keep"].sum(1) == 1).all() and r["converged"].all()
+    np.testing.assert_allclose(r["x_c"][:, 0], x, atol=1e-12)
+    T = S.about_axis(np.array([0.1, 0.2, 0.3]), np.array([0.3, 1.0, 0.2]), 0.7)
+    r = oracle.batch_search_mlp(oracle.mlp_init([3, 8, 8, 1], 2), [3, 8, 8, 1], T.reshape(1, 12), S.apply(T, x),
+                                50, 1e-9, 10.0, 1e-2)
+    np.testing.assert_allclose(r["x_c"][:, 0], x, atol=1e-9)
