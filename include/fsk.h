@@ -230,6 +230,17 @@ int fsk_multi_grad_weights_host(fsk_multi* m, const fsk_grid_desc* desc, const f
                                 const fsk_root* roots, const int64_t* root_index, const float* grad_xc, int64_t n,
                                 float* grad_w, int deterministic);
 
+/* ---- MLP-variant search (SearchVariant::Mlp): batch_search with
+ * d(x) = lbs_blend(softmax(net(x)), B)·x (deformer.cpp:22-26, correspondence.cpp:77-79) and the
+ * initial Jacobian from the network's input tangents (deform_jacobian(x, mlp, bones),
+ * deformer.cpp:117-141). theta/widths as for fsk_distill (widths = {3, H.., n_b}); outputs as
+ * fsk_search_fwd (dense per (point, init), dedup'd). Rounds of one batched network evaluation
+ * (tcgen05, 3xTF32) + one Broyden step per active solve, float32 state; synchronizes `stream`
+ * once per round. The ablation the paper's voxel search is measured against. */
+int fsk_search_fwd_mlp(fsk_ctx* ctx, const float* theta, const int32_t* widths, int32_t n_widths,
+                       const float* bones, int32_t n_bones_pose, const float* points, int64_t n,
+                       const fsk_search_opts* opts, fsk_search_out* out, void* stream);
+
 /* ---- MLP stages next to the search, tcgen05 tensor cores, 3xTF32 (FP32-faithful).
  * theta: the network's flat parameter vector in Mlp::parameters() order (mlp.cpp:207-219: per
  * layer W column-major [out x in], then b), float32, device. widths: host array {in, H, ..., out}

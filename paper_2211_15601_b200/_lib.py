@@ -27,7 +27,7 @@ EXPORTS = [
     "fsk_search_bwd_roots", "fsk_ctx_search_stats", "fsk_measure_fp64_peak", "fsk_measure_l1_gather_peak",
     "fsk_distill", "fsk_posed_occupancy", "fsk_distill_bwd",
     "fsk_multi_create", "fsk_multi_destroy", "fsk_multi_device_count", "fsk_multi_deform_host",
-    "fsk_multi_grad_weights_host",
+    "fsk_multi_grad_weights_host", "fsk_search_fwd_mlp",
 ]
 
 
@@ -103,6 +103,7 @@ def load():
     L.fsk_measure_l1_gather_peak.argtypes = [_vp, ctypes.POINTER(ctypes.c_double)]
     L.fsk_distill.argtypes = [_vp, _vp, _vp, _i32, G, _vp, _vp]
     L.fsk_distill_bwd.argtypes = [_vp, _vp, _vp, _i32, G, _vp, _vp, _vp]
+    L.fsk_search_fwd_mlp.argtypes = [_vp, _vp, _vp, _i32, _vp, _i32, _vp, _i64, O, S, _vp]
     L.fsk_multi_create.argtypes = [_i32, _vp, ctypes.POINTER(_vp)]
     L.fsk_multi_destroy.argtypes = [_vp]
     L.fsk_multi_device_count.argtypes = [_vp]

@@ -21,7 +21,7 @@ struct fsk_ctx {
     int device = 0;
     int sm_count = 0;
     int64_t launches = 0;
-    static constexpr int kSlots = 48;
+    static constexpr int kSlots = 64;
     void* buf[kSlots] = {};
     size_t cap[kSlots] = {};
     // optional per-launch CUDA-event profiling (bench.py reads per-kernel device time)
@@ -52,6 +52,7 @@ enum Slot {
     kOXr, kOJa, kOJb, kOJc, kOMeta, kOKeep, kNRoots, kOffs, kRootsTmp,
     kHW, kHB, kHP, kHT, kHOffs, kHRoots,
     kMlpPack, kMlpWidths, kMlpOcc, kMlpAct, kMlpD0, kMlpD1, kMlpOnes,
+    kMvPos, kMvPosNext, kMvW, kMvX, kMvG, kMvJ, kMvDx, kMvK, kMvAct, kMvActNext, kMvCnt,
     kSlotCount
 };
 static_assert(kSlotCount <= fsk_ctx::kSlots, "scratch slots");
@@ -92,6 +93,11 @@ GridP make_grid(const fsk_grid_desc* d);
 SearchP make_search(const fsk_search_opts* o);
 // exclusive scan of n int32 into n+1 int64 (out[n] = total); fsk_search.cu
 void scan_i32_to_i64(fsk_ctx* ctx, const int32_t* in, int64_t n, int64_t* out, cudaStream_t st);
+
+// fsk_mlp.cu: the skinning network for the MLP-variant search
+const float* mlp_skinning_pack(fsk_ctx* ctx, const float* theta, const int32_t* widths, int nw, cudaStream_t st);
+void mlp_skinning_eval(fsk_ctx* ctx, const float* pk, const int32_t* widths, int nw, const float4* pos, int64_t n_rows,
+                       bool tangent, float* out, cudaStream_t st);
 
 inline unsigned blocks_for(int64_t n, int t) { return (unsigned)std::max<int64_t>(1, (n + t - 1) / t); }
 

@@ -237,7 +237,7 @@ __global__ void k_mlp_pack(const float* __restrict__ theta, MlpDev m, float* __r
 }
 
 // ------------------------------------------------------------------ fused MLP kernel
-enum RowSource { kRowsGrid = 0, kRowsRoots = 1 };
+enum RowSource { kRowsGrid = 0, kRowsRoots = 1, kRowsPositions = 2 };
 
 struct MlpRows {
     int source;
@@ -249,6 +249,11 @@ struct MlpRows {
     const fsk_root* roots;
     const float* pose;
     int n_pose;
+    // positions (MLP-variant search): float4 {x, y, z, -} per point; with `tangent` every point
+    // owns 4 consecutive rows {value, d/dx, d/dy, d/dz} (forward-mode input tangents,
+    // Mlp::input_tangent mlp.cpp:142-155) and n counts rows
+    const float4* pos;
+    int tangent;
 };
 
 constexpr int kTile = 128;
@@ -261,12 +266,30 @@ __device__ __forceinline__ void row_input(const MlpRows& R, int64_t r, float* x)
         x[0] = R.lo[0] + (float)i * R.h[0];
         x[1] = R.lo[1] + (float)j * R.h[1];
         x[2] = R.lo[2] + (float)k * R.h[2];
-    } else {
+    } else if (R.source == kRowsRoots) {
         const float4 a = __ldg(reinterpret_cast<const float4*>(R.roots + r));
         x[0] = a.x;
         x[1] = a.y;
         x[2] = a.z;
+    } else {
+        const float4 a = __ldg(R.pos + (R.tangent ? r >> 2 : r));
+        x[0] = a.x;
+        x[1] = a.y;
+        x[2] = a.z;
     }
+}
+
+// softplus and its slope in one: e = exp(−|z|), softplus = max(z, 0) + log(1 + e), sigmoid
+// from the same e. With input tangents the value row of a 4-row group gives the slope to its
+// tangent rows (lanes 4m..4m+3 of one warp): h = softplus(z) for the value row, σ(z_value)·ż
+// for a tangent row (the chain rule of Mlp::input_tangent, mlp.cpp:148-152).
+__device__ __forceinline__ float act_fwd(float z, bool tangent, int role) {
+    const float e = __expf(-fabsf(z));
+    const float sp = fmaxf(z, 0.f) + __logf(1.f + e);
+    if (!tangent) return sp;
+    const float sig = z >= 0.f ? 1.f / (1.f + e) : e / (1.f + e);
+    const float sv = __shfl_sync(0xffffffffu, sig, (threadIdx.x & 31) & ~3);
+    return role == 0 ? sp : sv * z;
 }
 
 // One 128-row tile per iteration of a persistent CTA (128 threads; thread t owns TMEM lane t =
@@ -363,6 +386,8 @@ __global__ void __launch_bounds__(kThreads, H == 64 ? 2 : 1)  // H = 64: two CTA
         // ---- layer 0 (K0 inputs) on the FP32 pipe → A (hi/lo) in TMEM
         float x[3];
         row_input(R, rr, x);
+        const bool tan = R.source == kRowsPositions && R.tangent;
+        const int role = tan ? (int)(row & 3) : 0;  // 0: value row, 1..3: d/dx_{role-1}
         float* act_h = act ? act + 4 * R.n : nullptr;
         if (act && half == 0 && row < R.n)
             reinterpret_cast<float4*>(act)[row] = make_float4(x[0], x[1], x[2], 0.f);
@@ -371,12 +396,17 @@ __global__ void __launch_bounds__(kThreads, H == 64 ? 2 : 1)  // H = 64: two CTA
             float hv[16], lv[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-                float z = s_b0[c0 + j];
                 const float* w = s_w0 + (c0 + j) * m.K0;
-                z = fmaf(w[0], x[0], z);
-                z = fmaf(w[1], x[1], z);
-                z = fmaf(w[2], x[2], z);
-                const float h = softplus_f(z);
+                float z;
+                if (role == 0) {
+                    z = s_b0[c0 + j];
+                    z = fmaf(w[0], x[0], z);
+                    z = fmaf(w[1], x[1], z);
+                    z = fmaf(w[2], x[2], z);
+                } else {
+                    z = w[role - 1];  // W0 · e_k
+                }
+                const float h = act_fwd(z, tan, role);
                 hv[j] = tf32_hi(h);
                 lv[j] = h - hv[j];
             }
@@ -429,17 +459,29 @@ __global__ void __launch_bounds__(kThreads, H == 64 ? 2 : 1)  // H = 64: two CTA
                 tmem_wait_ld();
                 float mx = -INFINITY;
                 for (int i = 0; i < m.n_out; ++i) {
-                    z[i] += s_headv[i];
+                    if (role == 0) z[i] += s_headv[i];
                     mx = fmaxf(mx, z[i]);
                 }
-                float sum = 0.f;
+                float sum = 0.f, zt[64];
                 for (int i = 0; i < m.n_out; ++i) {
+                    zt[i] = z[i];
                     z[i] = __expf(z[i] - mx);
                     sum += z[i];
                 }
                 const float inv = 1.f / sum;
+                for (int i = 0; i < m.n_out; ++i) z[i] *= inv;
+                if (tan) {  // softmax Jacobian on the tangent rows: ẇ = w ⊙ (ż − <w, ż>) (skinning.cpp:57-63)
+                    float dot = 0.f;
+                    for (int i = 0; i < m.n_out; ++i) {
+                        const float wv = __shfl_sync(0xffffffffu, z[i], (threadIdx.x & 31) & ~3);
+                        z[i] = wv;
+                        dot = fmaf(wv, zt[i], dot);
+                    }
+                    if (role != 0)
+                        for (int i = 0; i < m.n_out; ++i) z[i] = z[i] * (zt[i] - dot);
+                }
                 if (row < R.n)
-                    for (int i = 0; i < m.n_out; ++i) out[row * m.n_out + i] = z[i] * inv;
+                    for (int i = 0; i < m.n_out; ++i) out[row * m.n_out + i] = z[i];
             } else if (!head) {  // hidden epilogue: bias, softplus, split → next layer's A (and scalar head)
                 const float* b = s_bias + l * H;
                 const bool last_hidden = l + 1 == m.n_hidden;
@@ -454,7 +496,7 @@ __global__ void __launch_bounds__(kThreads, H == 64 ? 2 : 1)  // H = 64: two CTA
                     float v[16], lv[16];
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
-                        const float h = softplus_f(acc[c0 + j] + b[cb + c0 + j]);
+                        const float h = act_fwd(role == 0 ? acc[c0 + j] + b[cb + c0 + j] : acc[c0 + j], tan, role);
                         if (!m.softmax && last_hidden) logit = fmaf(s_headv[cb + c0 + j], h, logit);
                         v[j] = tf32_hi(h);
                         lv[j] = h - v[j];
@@ -584,6 +626,26 @@ void blas_check(cublasStatus_t e, const char* what) {
 }
 
 }  // namespace
+
+// For the MLP-variant search (fsk_search.cu): pack once, then evaluate the skinning network
+// (softmax head) at float4 positions, optionally with the 3 forward-mode input tangents per
+// point (rows = 4 × points).
+const float* mlp_skinning_pack(fsk_ctx* ctx, const float* theta, const int32_t* widths, int nw, cudaStream_t st) {
+    const MlpShape s = mlp_shape(widths, nw, true);
+    return pack(ctx, s, theta, widths, nw, st);
+}
+
+void mlp_skinning_eval(fsk_ctx* ctx, const float* pk, const int32_t* widths, int nw, const float4* pos, int64_t n_rows,
+                       bool tangent, float* out, cudaStream_t st) {
+    const MlpShape s = mlp_shape(widths, nw, true);
+    MlpRows R{};
+    R.source = kRowsPositions;
+    R.n = n_rows;
+    R.pos = pos;
+    R.tangent = tangent ? 1 : 0;
+    run_fwd(ctx, s, widths, nw, pk, R, out, st);
+}
+
 }  // namespace fsk
 
 using namespace fsk;

@@ -854,6 +854,199 @@ void check_search_args(const GridP& g, int32_t n_bones_pose, const void* grid_pt
     if (n_bones_pose != g.nb) fail(FSK_EINVAL, mismatch);
 }
 
+// ============================================================================ MLP-variant search
+// SearchVariant::Mlp (correspondence.cpp:77-79, deformer.cpp:22-26,
+// :117-141): d(x) = lbs_blend(softmax(net(x)), B)·x, the initial Jacobian from the network's
+// input tangents. Batched in rounds: every round evaluates the skinning network on the tensor
+// cores (fsk_mlp.cu, 3xTF32) at the positions of all still-active solves, then one thread per
+// solve takes the Broyden step (the same iterate() arithmetic as K2, float32). Solves are
+// bone-major (q = bone·n + j) so dedup and compaction are K2's.
+struct MvState {
+    float4* x;   // x, -
+    float4* g;   // g, err2
+    float* ji;   // J~ [9]
+    float4* dx;  // last step
+    int* k;
+};
+
+__device__ __forceinline__ void mv_deform(const float* sB, int nb, const float* w, float x0, float x1, float x2,
+                                          float d[3]) {
+    float M[12];
+#pragma unroll
+    for (int e = 0; e < 12; ++e) M[e] = 0.f;
+    for (int i = 0; i < nb; ++i) {  // lbs_blend (deformer.cpp:9-19), bone order
+        const float wi = w[i];
+#pragma unroll
+        for (int e = 0; e < 12; ++e) M[e] = fmaf(wi, sB[12 * i + e], M[e]);
+    }
+    d[0] = M[0] * x0 + M[1] * x1 + M[2] * x2 + M[3];
+    d[1] = M[4] * x0 + M[5] * x1 + M[6] * x2 + M[7];
+    d[2] = M[8] * x0 + M[9] * x1 + M[10] * x2 + M[11];
+}
+
+__device__ __forceinline__ void mv_append(int* cnt, int* act, float4* pos, int s, float x0, float x1, float x2,
+                                          bool on) {
+    const unsigned m = __ballot_sync(__activemask(), on);
+    if (!on) return;
+    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(cnt, __popc(m));
+    base = __shfl_sync(m, base, leader);
+    const int slot = base + __popc(m & ((1u << lane) - 1));
+    act[slot] = s;
+    pos[slot] = make_float4(x0, x1, x2, 0.f);
+}
+
+__global__ void __launch_bounds__(256) k_mv_init(const float* __restrict__ bones, const float* __restrict__ pts,
+                                                 int64_t n, int nb, float4* __restrict__ pos) {
+    const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (s >= n * nb) return;
+    const int b = (int)(s / n);
+    const int64_t j = s - (int64_t)b * n;
+    const float* B = bones + 12 * b;
+    const float xp0 = pts[3 * j], xp1 = pts[3 * j + 1], xp2 = pts[3 * j + 2];
+    const float it0 = -(B[0] * B[3] + B[4] * B[7] + B[8] * B[11]);
+    const float it1 = -(B[1] * B[3] + B[5] * B[7] + B[9] * B[11]);
+    const float it2 = -(B[2] * B[3] + B[6] * B[7] + B[10] * B[11]);
+    pos[s] = make_float4(B[0] * xp0 + B[4] * xp1 + B[8] * xp2 + it0, B[1] * xp0 + B[5] * xp1 + B[9] * xp2 + it1,
+                         B[2] * xp0 + B[6] * xp1 + B[10] * xp2 + it2, 0.f);  // x0 = B_i^-1 x' (geometry.hpp:58-61)
+}
+
+// solve start (correspondence.cpp:135-137): J = Σ w_i R_i + Σ (B_i x)(∇w_i)ᵀ (deformer.cpp:117-128)
+// from the tangent rows, J~0 = J^-1 or I, g0; then the divergence check and the first step.
+__global__ void __launch_bounds__(256) k_mv_start(const float* __restrict__ bones, const float* __restrict__ pts,
+                                                  int64_t n, int nb, SearchP o, const float4* __restrict__ pos,
+                                                  const float* __restrict__ wt, SearchPlanes out, MvState st,
+                                                  int* __restrict__ cnt_next, int* __restrict__ act_next,
+                                                  float4* __restrict__ pos_next) {
+    extern __shared__ float sB[];
+    for (int e = threadIdx.x; e < nb * 12; e += blockDim.x) sB[e] = bones[e];
+    __syncthreads();
+    const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool live = s < n * nb;
+    bool go = false;
+    float x0 = 0, x1 = 0, x2 = 0;
+    if (live) {
+        const int64_t j = s - (s / n) * n;
+        const float4 xv = pos[s];
+        x0 = xv.x;
+        x1 = xv.y;
+        x2 = xv.z;
+        const float* w = wt + (4 * s) * nb;
+        float J[9];
+#pragma unroll
+        for (int e = 0; e < 9; ++e) J[e] = 0.f;
+        for (int i = 0; i < nb; ++i) {
+            const float* B = sB + 12 * i;
+            const float wi = w[i];
+            J[0] = fmaf(wi, B[0], J[0]); J[1] = fmaf(wi, B[1], J[1]); J[2] = fmaf(wi, B[2], J[2]);
+            J[3] = fmaf(wi, B[4], J[3]); J[4] = fmaf(wi, B[5], J[4]); J[5] = fmaf(wi, B[6], J[5]);
+            J[6] = fmaf(wi, B[8], J[6]); J[7] = fmaf(wi, B[9], J[7]); J[8] = fmaf(wi, B[10], J[8]);
+        }
+        for (int i = 0; i < nb; ++i) {
+            const float* B = sB + 12 * i;
+            const float bx[3] = {B[0] * x0 + B[1] * x1 + B[2] * x2 + B[3], B[4] * x0 + B[5] * x1 + B[6] * x2 + B[7],
+                                 B[8] * x0 + B[9] * x1 + B[10] * x2 + B[11]};
+            const float gw[3] = {w[nb + i], w[2 * nb + i], w[3 * nb + i]};  // ∂w_i/∂x_c from tangent row c
+#pragma unroll
+            for (int r = 0; r < 3; ++r)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) J[3 * r + c] = fmaf(bx[r], gw[c], J[3 * r + c]);
+        }
+        float Ji[9];
+        inverse_or_identity(J, Ji);
+        float d[3];
+        mv_deform(sB, nb, w, x0, x1, x2, d);
+        const float g0 = d[0] - pts[3 * j], g1 = d[1] - pts[3 * j + 1], g2 = d[2] - pts[3 * j + 2];
+        const float err2 = g0 * g0 + g1 * g1 + g2 * g2;
+        const bool conv = err2 < (float)o.conv2;  // (:100-103)
+        if (conv || err2 > (float)o.div2 || o.max_iters <= 0) {
+            store_solve(out, s, x0, x1, x2, Ji, err2, SolveOut{0, conv, false, false});
+        } else {
+            const float dx0 = -(Ji[0] * g0 + Ji[1] * g1 + Ji[2] * g2);
+            const float dx1 = -(Ji[3] * g0 + Ji[4] * g1 + Ji[5] * g2);
+            const float dx2 = -(Ji[6] * g0 + Ji[7] * g1 + Ji[8] * g2);
+            st.g[s] = make_float4(g0, g1, g2, err2);
+            for (int e = 0; e < 9; ++e) st.ji[9 * s + e] = Ji[e];
+            st.dx[s] = make_float4(dx0, dx1, dx2, 0.f);
+            st.k[s] = 0;
+            x0 += dx0;
+            x1 += dx1;
+            x2 += dx2;
+            st.x[s] = make_float4(x0, x1, x2, 0.f);
+            go = true;
+        }
+    }
+    mv_append(cnt_next, act_next, pos_next, (int)s, x0, x1, x2, go);
+}
+
+// one Broyden iteration after the network evaluation at x (correspondence.cpp:108-122)
+__global__ void __launch_bounds__(256) k_mv_step(const float* __restrict__ bones, const float* __restrict__ pts,
+                                                 int64_t n, int nb, SearchP o, const int* __restrict__ cnt,
+                                                 const int* __restrict__ act, const float* __restrict__ wv,
+                                                 SearchPlanes out, MvState st, int* __restrict__ cnt_next,
+                                                 int* __restrict__ act_next, float4* __restrict__ pos_next) {
+    extern __shared__ float sB[];
+    for (int e = threadIdx.x; e < nb * 12; e += blockDim.x) sB[e] = bones[e];
+    __syncthreads();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int c = *cnt;
+    bool go = false;
+    int s = 0;
+    float x0 = 0, x1 = 0, x2 = 0;
+    if (i < c) {
+        s = act[i];
+        const int64_t j = (int64_t)s - ((int64_t)s / n) * n;
+        const float4 xv = st.x[s], gv = st.g[s], dv = st.dx[s];
+        x0 = xv.x;
+        x1 = xv.y;
+        x2 = xv.z;
+        float Ji[9];
+        for (int e = 0; e < 9; ++e) Ji[e] = st.ji[9 * s + e];
+        float d[3];
+        mv_deform(sB, nb, wv + (int64_t)i * nb, x0, x1, x2, d);
+        const float n0 = d[0] - pts[3 * j], n1 = d[1] - pts[3 * j + 1], n2 = d[2] - pts[3 * j + 2];
+        const float dg0 = n0 - gv.x, dg1 = n1 - gv.y, dg2 = n2 - gv.z;
+        const float err2 = n0 * n0 + n1 * n1 + n2 * n2;
+        const int k = st.k[s] + 1;
+        const bool conv = err2 < (float)o.conv2;  // (:113-116)
+        if (!conv) {
+            const float dx0 = dv.x, dx1 = dv.y, dx2 = dv.z;
+            const float j0 = Ji[0] * dg0 + Ji[1] * dg1 + Ji[2] * dg2;
+            const float j1 = Ji[3] * dg0 + Ji[4] * dg1 + Ji[5] * dg2;
+            const float j2 = Ji[6] * dg0 + Ji[7] * dg1 + Ji[8] * dg2;
+            const float den = dx0 * j0 + dx1 * j1 + dx2 * j2;
+            if (fabsf(den) > 1e-18f) {
+                const float inv = 1.f / den;
+                const float q0 = (dx0 - j0) * inv, q1 = (dx1 - j1) * inv, q2 = (dx2 - j2) * inv;
+                const float w0 = dx0 * Ji[0] + dx1 * Ji[3] + dx2 * Ji[6];
+                const float w1 = dx0 * Ji[1] + dx1 * Ji[4] + dx2 * Ji[7];
+                const float w2 = dx0 * Ji[2] + dx1 * Ji[5] + dx2 * Ji[8];
+                Ji[0] = fmaf(q0, w0, Ji[0]); Ji[1] = fmaf(q0, w1, Ji[1]); Ji[2] = fmaf(q0, w2, Ji[2]);
+                Ji[3] = fmaf(q1, w0, Ji[3]); Ji[4] = fmaf(q1, w1, Ji[4]); Ji[5] = fmaf(q1, w2, Ji[5]);
+                Ji[6] = fmaf(q2, w0, Ji[6]); Ji[7] = fmaf(q2, w1, Ji[7]); Ji[8] = fmaf(q2, w2, Ji[8]);
+            }
+        }
+        if (conv || k >= o.max_iters || err2 > (float)o.div2) {
+            store_solve(out, s, x0, x1, x2, Ji, err2, SolveOut{k, conv, false, false});
+        } else {  // divergence check passed: the next step (:105-107)
+            const float dx0 = -(Ji[0] * n0 + Ji[1] * n1 + Ji[2] * n2);
+            const float dx1 = -(Ji[3] * n0 + Ji[4] * n1 + Ji[5] * n2);
+            const float dx2 = -(Ji[6] * n0 + Ji[7] * n1 + Ji[8] * n2);
+            st.g[s] = make_float4(n0, n1, n2, err2);
+            for (int e = 0; e < 9; ++e) st.ji[9 * s + e] = Ji[e];
+            st.dx[s] = make_float4(dx0, dx1, dx2, 0.f);
+            st.k[s] = k;
+            x0 += dx0;
+            x1 += dx1;
+            x2 += dx2;
+            st.x[s] = make_float4(x0, x1, x2, 0.f);
+            go = true;
+        }
+    }
+    mv_append(cnt_next, act_next, pos_next, s, x0, x1, x2, go);
+}
+
 }  // namespace
 
 // Exclusive int32 → int64 scan for other translation units (fsk_ctx.h).
@@ -899,6 +1092,80 @@ int fsk_search_fwd(fsk_ctx* ctx, const float* tgrid, const double* tgrid64, cons
         FSK_LAUNCH(ctx, st, k_scatter_dense, blocks_for(n * g.nb, 256), 256, 0, n, g.nb, s.sp, s.perm, d);
         if (out->n_roots)
             cuda_check(cudaMemcpyAsync(out->n_roots, s.n_roots_p, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st),
+                       "cudaMemcpyAsync");
+    });
+}
+
+int fsk_search_fwd_mlp(fsk_ctx* ctx, const float* theta, const int32_t* widths, int32_t n_widths,
+                       const float* bones, int32_t n_bones_pose, const float* points, int64_t n,
+                       const fsk_search_opts* opts, fsk_search_out* out, void* stream) {
+    return guard([&] {
+        set_device(ctx);
+        if (n_bones_pose < 1) fail(FSK_EINVAL, "search: no bone transforms");
+        if (!theta || !widths) fail(FSK_EINVAL, "search: mlp variant needs a skinning network");
+        if (n_widths < 2 || widths[0] != 3) fail(FSK_EINVAL, "SkinningMlp: network input width must be 3");
+        if (widths[n_widths - 1] != n_bones_pose) fail(FSK_EINVAL, "search: mlp bone count mismatch");
+        const SearchP sp = make_search(opts);
+        if (!out || (n > 0 && !out->converged)) fail(FSK_EINVAL, "fsk: search output needs a converged mask");
+        if (n < 0) fail(FSK_EINVAL, "fsk: negative point count");
+        if (n > 0 && (!points || !bones)) fail(FSK_EINVAL, "fsk: null buffer");
+        if (n == 0) return;
+        const int nb = n_bones_pose;
+        const int64_t S = n * nb;
+        if (4 * S >= (int64_t(1) << 31)) fail(FSK_EINVAL, "fsk: too many points for one call (split the batch)");
+        cudaStream_t st = (cudaStream_t)stream;
+        // search planes, identity order (dedup + dense scatter are K2's)
+        SearchState ss;
+        ss.sp.xr = (float4*)scratch(ctx, kOXr, S * sizeof(float4));
+        ss.sp.ja = (float4*)scratch(ctx, kOJa, S * sizeof(float4));
+        ss.sp.jb = (float4*)scratch(ctx, kOJb, S * sizeof(float4));
+        ss.sp.jc = (float*)scratch(ctx, kOJc, S * sizeof(float));
+        ss.sp.meta = (uint16_t*)scratch(ctx, kOMeta, S * sizeof(uint16_t));
+        ss.sp.keep = (uint8_t*)scratch(ctx, kOKeep, S);
+        ss.perm = (int*)scratch(ctx, kPerm, n * sizeof(int));
+        ss.n_roots_p = (int32_t*)scratch(ctx, kNRoots, n * sizeof(int32_t));
+        float4* xs = (float4*)scratch(ctx, kXs, n * sizeof(float4));
+        int* esc_n = (int*)scratch(ctx, kEscN, 4 * sizeof(int));
+        FSK_LAUNCH(ctx, st, k_identity_order, blocks_for(n, 256), 256, 0, points, n, ss.perm, xs, esc_n);
+        MvState mv;
+        mv.x = (float4*)scratch(ctx, kMvX, S * sizeof(float4));
+        mv.g = (float4*)scratch(ctx, kMvG, S * sizeof(float4));
+        mv.ji = (float*)scratch(ctx, kMvJ, S * 9 * sizeof(float));
+        mv.dx = (float4*)scratch(ctx, kMvDx, S * sizeof(float4));
+        mv.k = (int*)scratch(ctx, kMvK, S * sizeof(int));
+        float4* pos[2] = {(float4*)scratch(ctx, kMvPos, S * sizeof(float4)),
+                          (float4*)scratch(ctx, kMvPosNext, S * sizeof(float4))};
+        int* act[2] = {(int*)scratch(ctx, kMvAct, S * sizeof(int)), (int*)scratch(ctx, kMvActNext, S * sizeof(int))};
+        int* cnt = (int*)scratch(ctx, kMvCnt, 2 * sizeof(int));
+        float* w = (float*)scratch(ctx, kMvW, 4 * S * nb * sizeof(float));
+        if (!ctx->hcount) cuda_check(cudaMallocHost(&ctx->hcount, 64 * sizeof(int64_t)), "cudaMallocHost");
+        const size_t smb = nb * 12 * sizeof(float);
+        const float* pk = mlp_skinning_pack(ctx, theta, widths, n_widths, st);
+        // starts: x0 for every solve, the network with input tangents (4 rows per solve)
+        FSK_LAUNCH(ctx, st, k_mv_init, blocks_for(S, 256), 256, 0, bones, points, n, nb, pos[0]);
+        mlp_skinning_eval(ctx, pk, widths, n_widths, pos[0], 4 * S, true, w, st);
+        cuda_check(cudaMemsetAsync(cnt, 0, 2 * sizeof(int), st), "cudaMemsetAsync");
+        FSK_LAUNCH(ctx, st, k_mv_start, blocks_for(S, 256), 256, smb, bones, points, n, nb, sp, pos[0], w, ss.sp, mv,
+                   cnt + 1, act[1], pos[1]);
+        int cur = 1;
+        for (int it = 0; it < sp.max_iters; ++it) {
+            int32_t* hc = reinterpret_cast<int32_t*>(ctx->hcount);
+            cuda_check(cudaMemcpyAsync(hc, cnt + cur, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H count");
+            cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+            const int c = hc[0];
+            if (c == 0) break;
+            const int nxt = cur ^ 1;
+            cuda_check(cudaMemsetAsync(cnt + nxt, 0, sizeof(int), st), "cudaMemsetAsync");
+            mlp_skinning_eval(ctx, pk, widths, n_widths, pos[cur], c, false, w, st);
+            FSK_LAUNCH(ctx, st, k_mv_step, blocks_for(c, 256), 256, smb, bones, points, n, nb, sp, cnt + cur, act[cur],
+                       w, ss.sp, mv, cnt + nxt, act[nxt], pos[nxt]);
+            cur = nxt;
+        }
+        FSK_LAUNCH(ctx, st, k_dedup, blocks_for(n, 256), 256, 0, n, nb, (float)sp.dedup2, ss.sp, ss.perm, ss.n_roots_p);
+        DenseOut d{out->x_c, out->jinv, out->resid, out->iters, out->converged, out->keep, out->n_roots};
+        FSK_LAUNCH(ctx, st, k_scatter_dense, blocks_for(S, 256), 256, 0, n, nb, ss.sp, ss.perm, d);
+        if (out->n_roots)
+            cuda_check(cudaMemcpyAsync(out->n_roots, ss.n_roots_p, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st),
                        "cudaMemcpyAsync");
     });
 }

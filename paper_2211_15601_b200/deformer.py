@@ -328,6 +328,20 @@ class Deformer:
                                  ctypes.byref(desc), _ptr(out), _stream(self.device)))
         return out
 
+    def batch_search_mlp(self, theta, widths, bones, points, opts: SearchOptions, out=None):
+        """``batch_search`` with ``SearchVariant::Mlp`` (correspondence.cpp:77-79): the skinning
+        network evaluated at every Broyden iterate (tensor cores) instead of the grid."""
+        bones = _f32(bones, "bones", self.device)
+        points = _f32(points, "points", self.device)
+        nb, n = bones.numel() // 12, points.shape[0]
+        if out is None:
+            out = self.alloc_search_out(n, nb)
+        co = self._c_out(out)
+        check(self.L.fsk_search_fwd_mlp(self._ctx, _ptr(_f32(theta, "theta", self.device)), self._widths(widths),
+                                        len(widths), _ptr(bones), nb, _ptr(points), n, ctypes.byref(opts.c()),
+                                        ctypes.byref(co), _stream(self.device)))
+        return out
+
     def distill_bwd(self, theta, widths, dims, bbox, grad_w, out=None):
         """VJP of ``distill``: dL/dtheta [P] from dL/dw [V, n_b] (Mlp::backward through the
         softmax head, mlp.cpp:38-41,140-163)."""
