@@ -8,6 +8,8 @@
  *                         std::invalid_argument message text where one exists
  *   FSK_ECUDA (2)         CUDA / allocation failure (std::runtime_error)
  *   FSK_ENODEV (3)        no usable sm_100 device (the library has no CPU fallback)
+ *   FSK_EIO (4)           file I/O failure of the wire-format helpers (std::runtime_error;
+ *                         text in fsk_io_last_error())
  * Device pointers ("dev") must live on the context's device. Calls are stream-ordered
  * on `stream` (a cudaStream_t; NULL = legacy default stream) and asynchronous unless
  * stated otherwise. A context is not thread-safe; distinct (ctx, stream) pairs are.
@@ -37,6 +39,7 @@ extern "C" {
 #define FSK_EINVAL 1
 #define FSK_ECUDA 2
 #define FSK_ENODEV 3
+#define FSK_EIO 4
 
 typedef struct fsk_ctx fsk_ctx;
 
@@ -229,6 +232,24 @@ int fsk_multi_deform_host(fsk_multi* m, const float* weights, const fsk_grid_des
 int fsk_multi_grad_weights_host(fsk_multi* m, const fsk_grid_desc* desc, const float* bones, int32_t n_bones_pose,
                                 const fsk_root* roots, const int64_t* root_index, const float* grad_xc, int64_t n,
                                 float* grad_w, int deterministic);
+
+/* ---- wire and disk formats, host functions; errors in fsk_io_last_error().
+ * SKNV grids (skinning.cpp:239-288), .bin points (pointio.cpp:43-62), correspondence dumps
+ * (pointio.cpp:97-117, "%.17g" text, formatted by `threads` host threads, 0 = all cores). */
+const char* fsk_io_last_error(void);
+int fsk_sknv_read(const char* path, fsk_grid_desc* desc, float* weights /* [V][n_b] host, NULL = header */,
+                  int64_t cap);
+int fsk_sknv_write(const char* path, const fsk_grid_desc* desc, const float* weights);
+int fsk_points_bin_read(const char* path, float* points /* [n][3] host, NULL = count */, int64_t cap,
+                        int64_t* n_out);
+int fsk_points_bin_write(const char* path, const float* points, int64_t n);
+int fsk_write_correspondence_dump(const char* path, const float* queries, int64_t n, const int64_t* offsets,
+                                  const fsk_root* roots, int32_t threads);
+/* one cmd_deform frame from files to file (fskin_cli.cpp:395-429, correspondences only):
+ * SKNV + .bin in, fsk_deform_host, dump out. */
+int fsk_deform_files(fsk_ctx* ctx, const char* grid_path, const float* bones, int32_t n_bones,
+                     const char* points_path, const fsk_search_opts* opts, const char* dump_path,
+                     int64_t* n_queries, int64_t* n_roots);
 
 /* ---- MLP-variant search (SearchVariant::Mlp): batch_search with
  * d(x) = lbs_blend(softmax(net(x)), B)·x (deformer.cpp:22-26, correspondence.cpp:77-79) and the

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # FSK_LIB: load a tuning-variant build instead (scripts/build_variants.sh); default in-tree.
 LIB_PATH = os.environ.get("FSK_LIB") or os.path.join(HERE, "libfsk_b200.so")
 
-FSK_OK, FSK_EINVAL, FSK_ECUDA, FSK_ENODEV = 0, 1, 2, 3
+FSK_OK, FSK_EINVAL, FSK_ECUDA, FSK_ENODEV, FSK_EIO = 0, 1, 2, 3, 4
 FSK_SEARCH_NO_SORT = 0x1
 FSK_SEARCH_FP32_ONLY = 0x2
 FSK_SEARCH_FP64 = 0x4
@@ -28,6 +28,8 @@ EXPORTS = [
     "fsk_distill", "fsk_posed_occupancy", "fsk_distill_bwd",
     "fsk_multi_create", "fsk_multi_destroy", "fsk_multi_device_count", "fsk_multi_deform_host",
     "fsk_multi_grad_weights_host", "fsk_search_fwd_mlp",
+    "fsk_io_last_error", "fsk_sknv_read", "fsk_sknv_write", "fsk_points_bin_read", "fsk_points_bin_write",
+    "fsk_write_correspondence_dump", "fsk_deform_files",
 ]
 
 
@@ -104,6 +106,14 @@ def load():
     L.fsk_distill.argtypes = [_vp, _vp, _vp, _i32, G, _vp, _vp]
     L.fsk_distill_bwd.argtypes = [_vp, _vp, _vp, _i32, G, _vp, _vp, _vp]
     L.fsk_search_fwd_mlp.argtypes = [_vp, _vp, _vp, _i32, _vp, _i32, _vp, _i64, O, S, _vp]
+    _cp = ctypes.c_char_p
+    L.fsk_io_last_error.restype = _cp
+    L.fsk_sknv_read.argtypes = [_cp, G, _vp, _i64]
+    L.fsk_sknv_write.argtypes = [_cp, G, _vp]
+    L.fsk_points_bin_read.argtypes = [_cp, _vp, _i64, ctypes.POINTER(_i64)]
+    L.fsk_points_bin_write.argtypes = [_cp, _vp, _i64]
+    L.fsk_write_correspondence_dump.argtypes = [_cp, _vp, _i64, _vp, _vp, _i32]
+    L.fsk_deform_files.argtypes = [_vp, _cp, _vp, _i32, _cp, O, _cp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]
     L.fsk_multi_create.argtypes = [_i32, _vp, ctypes.POINTER(_vp)]
     L.fsk_multi_destroy.argtypes = [_vp]
     L.fsk_multi_device_count.argtypes = [_vp]

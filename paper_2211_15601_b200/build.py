@@ -22,7 +22,7 @@ NVCC_FLAGS += os.environ.get("FSK_NVCC_DEFS", "").split()
 
 LIBS = ["-lcudart", "-lcublas", "-lnccl"]
 CU_SOURCES = ["fsk_ctx.cu", "fsk_search.cu", "fsk_bwd.cu", "fsk_mlp.cu", "fsk_multi.cu"]
-CXX_SOURCES = ["fskin_api.cpp"]
+CXX_SOURCES = ["fskin_api.cpp", "fsk_io.cpp"]
 
 
 def _sources():

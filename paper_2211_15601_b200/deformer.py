@@ -428,3 +428,60 @@ class MultiDeformer:
                                                  _ptr(root_index), _ptr(grad_xc), grad_xc.shape[0], _ptr(out),
                                                  1 if deterministic else 0))
         return out
+
+
+# ---------------------------------------------------------------- wire and disk formats
+def _io_check(rc):
+    if rc != _lib.FSK_OK:
+        L = _lib.load()
+        msg = (L.fsk_io_last_error() or L.fsk_last_error()).decode()
+        raise (FskInvalidArgument if rc == _lib.FSK_EINVAL else FskError)(msg)
+
+
+def read_sknv(path):
+    """load_sknv (skinning.cpp:264-288) -> (dims, bbox [6] float32, weights [V, n_b] float32)."""
+    L = _lib.load()
+    d = GridDesc()
+    _io_check(L.fsk_sknv_read(path.encode(), ctypes.byref(d), None, 0))
+    w = torch.empty((d.nx * d.ny * d.nz, d.n_bones), dtype=torch.float32)
+    _io_check(L.fsk_sknv_read(path.encode(), ctypes.byref(d), _ptr(w), w.numel()))
+    bbox = torch.tensor(list(d.bbox_min) + list(d.bbox_max), dtype=torch.float32)
+    return (d.nx, d.ny, d.nz), bbox.numpy(), w
+
+
+def write_sknv(path, dims, bbox, weights):
+    L = _lib.load()
+    w = weights.contiguous().float().cpu()
+    _io_check(L.fsk_sknv_write(path.encode(), ctypes.byref(grid_desc(dims, bbox, w.shape[1])), _ptr(w)))
+
+
+def read_points_bin(path):
+    L = _lib.load()
+    n = ctypes.c_int64()
+    _io_check(L.fsk_points_bin_read(path.encode(), None, 0, ctypes.byref(n)))
+    p = torch.empty((n.value, 3), dtype=torch.float32)
+    _io_check(L.fsk_points_bin_read(path.encode(), _ptr(p), n.value, ctypes.byref(n)))
+    return p
+
+
+def write_points_bin(path, points):
+    L = _lib.load()
+    p = points.contiguous().float().cpu()
+    _io_check(L.fsk_points_bin_write(path.encode(), _ptr(p), p.shape[0]))
+
+
+def write_correspondence_dump(path, queries, offsets, roots, threads=0):
+    """save_correspondence_dump (pointio.cpp:97-117) from host CorrespondenceSets."""
+    L = _lib.load()
+    q, o, r = (t.contiguous().cpu() for t in (queries.float(), offsets.long(), roots.float()))
+    _io_check(L.fsk_write_correspondence_dump(path.encode(), _ptr(q), q.shape[0], _ptr(o), _ptr(r), threads))
+
+
+def deform_files(deformer, grid_path, bones, points_path, opts: SearchOptions, dump_path):
+    """One cmd_deform frame from files to file (fskin_cli.cpp:395-429): returns (queries, roots)."""
+    b = bones.contiguous().float().cpu()
+    nq, nr = ctypes.c_int64(), ctypes.c_int64()
+    _io_check(deformer.L.fsk_deform_files(deformer._ctx, grid_path.encode(), _ptr(b), b.numel() // 12,
+                                          points_path.encode(), ctypes.byref(opts.c()), dump_path.encode(),
+                                          ctypes.byref(nq), ctypes.byref(nr)))
+    return nq.value, nr.value
