@@ -449,7 +449,7 @@ def mlp_stages(D, sc, roots_buf, n, dev, reps=20):
                       dtype=torch.float32, device=dev)
     ms = timed(lambda: D.distill_bwd(th_s, SKIN_WIDTHS, dims, sc.bbox, gw, out=gth))
     out["distill_bwd_32x32x8"] = {"ms": ms, "vertices_per_s": V / (ms * 1e-3),
-                                  "note": "forward recomputed on tcgen05 + FP32 cuBLAS GEMMs for Mlp::backward"}
+                                  "note": "forward recomputed on tcgen05 (activations kept) + fused FP32 Mlp::backward tiles"}
     # SPEC.md:572 (acceptance 7): voxel-variant search vs the MLP variant on the same queries,
     # grid distilled at 64x64x16 from the same network (SkinningMlp init, box-conditioned)
     from paper_2211_15601_b200.deformer import SearchOptions

@@ -278,7 +278,8 @@ int fsk_distill(fsk_ctx* ctx, const float* theta, const int32_t* widths, int32_t
  * diff.cpp:348-359, with the grid vertices in place of the roots): given dL/dw [V][n_b] (dev,
  * e.g. fsk_grad_weights' output), writes dL/dtheta [P] (dev, Mlp::parameters() order) =
  * sum_v Mlp::backward(softmax_vjp(w_v, dL/dw_v)) (mlp.cpp:38-41, :140-163). FP32: the forward
- * is recomputed on the tensor cores, the backward runs as FP32 GEMMs (cuBLAS, pedantic math). */
+ * is recomputed on the tensor cores (activations kept), the backward runs fused per 64-row
+ * tile on the CUDA cores with per-CTA partial sums reduced in a fixed order (deterministic). */
 int fsk_distill_bwd(fsk_ctx* ctx, const float* theta, const int32_t* widths, int32_t n_widths,
                     const fsk_grid_desc* desc, const float* grad_w, float* grad_theta, void* stream);
 

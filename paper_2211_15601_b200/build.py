@@ -20,7 +20,7 @@ NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC,-O2"
 # extra -D flags for tuning sweeps (e.g. FSK_NVCC_DEFS="-DFSK_SEARCH_MINB=2")
 NVCC_FLAGS += os.environ.get("FSK_NVCC_DEFS", "").split()
 
-LIBS = ["-lcudart", "-lcublas", "-lnccl"]
+LIBS = ["-lcudart", "-lnccl"]
 CU_SOURCES = ["fsk_ctx.cu", "fsk_search.cu", "fsk_bwd.cu", "fsk_mlp.cu", "fsk_multi.cu"]
 CXX_SOURCES = ["fskin_api.cpp", "fsk_io.cpp"]
 

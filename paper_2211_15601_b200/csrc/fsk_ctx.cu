@@ -3,8 +3,6 @@
 #include <cstring>
 #include <stdexcept>
 
-#include <cublas_v2.h>
-
 #include "fsk_ctx.h"
 
 namespace fsk {
@@ -239,7 +237,6 @@ int fsk_ctx_destroy(fsk_ctx* ctx) {
         if (ctx->stats) cudaFree(ctx->stats);
         if (ctx->copy) cudaStreamDestroy(ctx->copy);
         if (ctx->upload) cudaStreamDestroy(ctx->upload);
-        if (ctx->blas) cublasDestroy(ctx->blas);
         if (ctx->hcount) cudaFreeHost(ctx->hcount);
         delete ctx;
     });

@@ -6,7 +6,6 @@
 
 #include <cuda_runtime.h>
 
-struct cublasContext;
 
 #include <algorithm>
 #include <cmath>
@@ -40,7 +39,6 @@ struct fsk_ctx {
     cudaStream_t copy = nullptr;
     cudaStream_t upload = nullptr;  // host→device stream of the host-buffer entry point
     int64_t* hcount = nullptr;  // pinned per-chunk root counts
-    cublasContext* blas = nullptr;  // FP32 GEMMs of the distill backward (created on first use)
 };
 
 namespace fsk {

@@ -21,8 +21,6 @@
 //
 // Parameters are the reference's flat vector (Mlp::parameters(), mlp.cpp:207-219: per layer
 // W column-major then b), in float32 on the device; k_mlp_pack re-lays them out once per call.
-#include <cublas_v2.h>
-
 #include <cstring>
 
 #include "fsk_ctx.h"
@@ -93,10 +91,7 @@ __device__ __forceinline__ float tf32_hi(float x) {
     return __uint_as_float(r);
 }
 
-// softplus (mlp.cpp:10-13) and sigmoid (:15-21) in FP32
-// MUFU ex2/lg2 forms: abs error ~5e-7 (log of an argument in [1, 2]); for large |x| the
-// log term underflows to 0 where the exact value is < 6e-8.
-__device__ __forceinline__ float softplus_f(float x) { return fmaxf(x, 0.f) + __logf(1.f + __expf(-fabsf(x))); }
+// sigmoid (mlp.cpp:15-21) in FP32 (softplus: act_fwd below)
 __device__ __forceinline__ float sigmoid_f(float x) {
     if (x >= 0.f) return 1.f / (1.f + __expf(-x));
     const float e = __expf(x);
@@ -599,31 +594,134 @@ const float* pack(fsk_ctx* ctx, const MlpShape& s, const float* theta, const int
 }
 
 // ------------------------------------------------------------------ distill backward
-// dz = softmax_vjp(w, dw) = w ⊙ (dw − <w, dw>) (mlp.cpp:38-41), one thread per vertex
-__global__ void k_softmax_vjp(const float* __restrict__ w, const float* __restrict__ dw, int64_t n, int nb,
-                              float* __restrict__ dz) {
-    const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (v >= n) return;
-    float dot = 0.f;
-    for (int i = 0; i < nb; ++i) dot = fmaf(w[v * nb + i], dw[v * nb + i], dot);
-    for (int i = 0; i < nb; ++i) dz[v * nb + i] = w[v * nb + i] * (dw[v * nb + i] - dot);
+// Fused Mlp::backward over tiles of 64 rows (mlp.cpp:140-163), FP32 on the CUDA cores: per
+// tile the softmax VJP, then per layer (last to first) dW_l += δ_lᵀ·in_l, db_l += Σ δ_l and
+// δ_{l-1} = (δ_l·W_l) ⊙ softplus'(z_{l-1}) with softplus' = 1 − e^{−h} from the stored
+// activation. 4×4 register blocks over shared-memory tiles; each CTA accumulates into its own
+// slot of `part` ([grid][P], no atomics) and k_bwd_reduce sums the slots in a fixed order.
+constexpr int kBT = 64;  // rows per tile
+struct BwdNet {
+    int L, nw;
+    int w[kMaxWidths];
+    int64_t off[kMaxWidths];  // layer offsets in theta
+    int64_t P;
+    int maxw;
+};
+
+__device__ __forceinline__ void bwd_outer(const float* D, int ldd, const float* IN, int ldi, int n_out, int n_in,
+                                          float* dst_W, float* dst_b, int tid, int nthreads) {
+    // dW[o][i] += Σ_r D[r][o] IN[r][i] (column-major dst: i*n_out + o); db[o] += Σ_r D[r][o]
+    const int bo = (n_out + 3) / 4, bi = (n_in + 3) / 4;
+    for (int blk = tid; blk < bo * bi; blk += nthreads) {
+        const int o0 = (blk / bi) * 4, i0 = (blk % bi) * 4;
+        float acc[4][4] = {};
+        for (int r = 0; r < kBT; ++r) {
+            float d[4], v[4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                d[a] = o0 + a < n_out ? D[r * ldd + o0 + a] : 0.f;
+                v[a] = i0 + a < n_in ? IN[r * ldi + i0 + a] : 0.f;
+            }
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) acc[a][b] = fmaf(d[a], v[b], acc[a][b]);
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+                if (o0 + a < n_out && i0 + b < n_in) dst_W[(int64_t)(i0 + b) * n_out + o0 + a] += acc[a][b];
+    }
+    for (int o = tid; o < n_out; o += nthreads) {
+        float sacc = 0.f;
+        for (int r = 0; r < kBT; ++r) sacc += D[r * ldd + o];
+        dst_b[o] += sacc;
+    }
 }
 
-// delta = (delta_{l+1} W_{l+1}) ⊙ softplus'(z_l), softplus'(z) = sigmoid(z) = 1 − exp(−softplus(z))
-// taken from the stored activation h_l (mlp.cpp:157-160)
-__global__ void k_softplus_bwd(float* __restrict__ d, const float* __restrict__ h, int64_t count) {
+__global__ void __launch_bounds__(256) k_mlp_bwd(BwdNet net, const float* __restrict__ theta,
+                                                 const float* __restrict__ act, const float* __restrict__ w,
+                                                 const float* __restrict__ gw, int64_t n, int H,
+                                                 float* __restrict__ part) {
+    extern __shared__ float sm[];
+    const int M = net.maxw;
+    float* D0 = sm;                 // [kBT][M]
+    float* D1 = D0 + kBT * M;       // [kBT][M]
+    float* IN = D1 + kBT * M;       // [kBT][M]
+    float* Wl = IN + kBT * M;       // [M][M] row-major (n_out x n_in)
+    const int tid = threadIdx.x, nt = blockDim.x;
+    float* my = part + (int64_t)blockIdx.x * net.P;
+    for (int64_t i = tid; i < net.P; i += nt) my[i] = 0.f;
+    const int nb = net.w[net.nw - 1];
+    const int64_t n_tiles = (n + kBT - 1) / kBT;
+    const float* act_h = act + 4 * n;
+    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const int64_t r0 = t * kBT;
+        // δ_L = softmax_vjp(w, dw) (mlp.cpp:38-41); rows beyond n contribute 0
+        for (int r = tid; r < kBT; r += nt) {
+            const int64_t v = r0 + r;
+            float dot = 0.f;
+            if (v < n)
+                for (int i = 0; i < nb; ++i) dot = fmaf(w[v * nb + i], gw[v * nb + i], dot);
+            for (int i = 0; i < nb; ++i) D0[r * M + i] = v < n ? w[v * nb + i] * (gw[v * nb + i] - dot) : 0.f;
+        }
+        float *Dc = D0, *Dn = D1;
+        for (int l = net.L - 1; l >= 0; --l) {
+            const int n_out = net.w[l + 1], n_in = net.w[l];
+            __syncthreads();
+            // this layer's input rows: x (layer 0) or h_{l-1}
+            for (int e = tid; e < kBT * n_in; e += nt) {
+                const int r = e / n_in, c = e - r * n_in;
+                const int64_t v = r0 + r;
+                IN[r * M + c] = v < n ? (l == 0 ? act[4 * v + c] : act_h[((int64_t)(l - 1) * n + v) * H + c]) : 0.f;
+            }
+            if (l > 0)  // W_l row-major [n_out][n_in] from the column-major parameters
+                for (int e = tid; e < n_out * n_in; e += nt) {
+                    const int o = e / n_in, c = e - o * n_in;
+                    Wl[o * M + c] = theta[net.off[l] + (int64_t)c * n_out + o];
+                }
+            __syncthreads();
+            bwd_outer(Dc, M, IN, M, n_out, n_in, my + net.off[l], my + net.off[l] + (int64_t)n_out * n_in, tid, nt);
+            if (l == 0) break;
+            // δ_{l-1}[r][c] = (Σ_k δ_l[r][k] W_l[k][c]) · (1 − e^{−h_{l-1}[r][c]})
+            const int br = kBT / 4, bc = (n_in + 3) / 4;
+            for (int blk = tid; blk < br * bc; blk += nt) {
+                const int rr = (blk / bc) * 4, c0 = (blk % bc) * 4;
+                float acc[4][4] = {};
+                for (int k = 0; k < n_out; ++k) {
+                    float d[4], wv[4];
+#pragma unroll
+                    for (int a = 0; a < 4; ++a) {
+                        d[a] = Dc[(rr + a) * M + k];
+                        wv[a] = c0 + a < n_in ? Wl[k * M + c0 + a] : 0.f;
+                    }
+#pragma unroll
+                    for (int a = 0; a < 4; ++a)
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) acc[a][b] = fmaf(d[a], wv[b], acc[a][b]);
+                }
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b)
+                        if (c0 + b < n_in) Dn[(rr + a) * M + c0 + b] = acc[a][b] * -expm1f(-IN[(rr + a) * M + c0 + b]);
+            }
+            float* tmp = Dc;
+            Dc = Dn;
+            Dn = tmp;
+        }
+    }
+}
+
+__global__ void k_bwd_reduce(const float* __restrict__ part, int parts, int64_t P, float* __restrict__ out) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < count) d[i] *= -expm1f(-h[i]);
+    if (i >= P) return;
+    float s = 0.f;
+    for (int c = 0; c < parts; ++c) s += part[(int64_t)c * P + i];  // fixed order: deterministic
+    out[i] = s;
 }
 
-__global__ void k_fill(float* __restrict__ p, int64_t n, float v) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < n) p[i] = v;
-}
-
-void blas_check(cublasStatus_t e, const char* what) {
-    if (e != CUBLAS_STATUS_SUCCESS) fail(FSK_ECUDA, std::string(what) + ": cuBLAS status " + std::to_string((int)e));
-}
 
 }  // namespace
 
@@ -736,46 +834,30 @@ int fsk_distill_bwd(fsk_ctx* ctx, const float* theta, const int32_t* widths, int
             R.h[a] = (float)(((double)desc->bbox_max[a] - (double)desc->bbox_min[a]) / (n3[a] - 1));
         }
         run_fwd(ctx, s, widths, n_widths, pk, R, w, st, act);
-        // backward (Mlp::backward, mlp.cpp:140-163) as FP32 GEMMs over all vertices
-        if (!ctx->blas) blas_check(cublasCreate(&ctx->blas), "cublasCreate");
-        blas_check(cublasSetStream(ctx->blas, st), "cublasSetStream");
-        blas_check(cublasSetMathMode(ctx->blas, CUBLAS_PEDANTIC_MATH), "cublasSetMathMode");  // true FP32
-        const int64_t wmax = std::max(H, nb);
-        float* dA = (float*)scratch(ctx, kMlpD0, (size_t)V * wmax * sizeof(float));
-        float* dB = (float*)scratch(ctx, kMlpD1, (size_t)V * wmax * sizeof(float));
-        float* ones = (float*)scratch(ctx, kMlpOnes, (size_t)V * sizeof(float));
-        FSK_LAUNCH(ctx, st, k_fill, blocks_for(V, 256), 256, 0, ones, V, 1.f);
-        FSK_LAUNCH(ctx, st, k_softmax_vjp, blocks_for(V, 256), 256, 0, w, grad_w, V, nb, dA);
-        std::vector<int64_t> off(L);
+        // backward (Mlp::backward, mlp.cpp:140-163): fused tiles on the CUDA cores, FP32
+        BwdNet net{};
+        net.L = L;
+        net.nw = n_widths;
         int64_t o = 0;
+        net.maxw = 0;
+        for (int l = 0; l < n_widths; ++l) {
+            net.w[l] = widths[l];
+            net.maxw = std::max(net.maxw, (int)widths[l]);
+        }
+        net.maxw = (net.maxw + 3) / 4 * 4;
         for (int l = 0; l < L; ++l) {
-            off[l] = o;
+            net.off[l] = o;
             o += (int64_t)widths[l + 1] * widths[l] + widths[l + 1];
         }
-        const float one = 1.f, zero = 0.f;
-        const float* act_h = act + 4 * V;
-        for (int l = L - 1; l >= 0; --l) {
-            const int n_out = widths[l + 1], n_in = widths[l];
-            // input of layer l: x (row stride 4) or h_{l-1} (row stride H)
-            const float* in = l == 0 ? act : act_h + (int64_t)(l - 1) * V * H;
-            const int ld_in = l == 0 ? 4 : H;
-            float* dW = grad_theta + off[l];
-            float* db = dW + (int64_t)n_out * n_in;
-            // dW_l (column-major n_out x n_in, the Mlp::parameters() layout) = delta_l^T · in
-            blas_check(cublasSgemm(ctx->blas, CUBLAS_OP_N, CUBLAS_OP_T, n_out, n_in, (int)V, &one, dA, n_out, in, ld_in,
-                                   &zero, dW, n_out),
-                       "cublasSgemm dW");
-            blas_check(cublasSgemv(ctx->blas, CUBLAS_OP_N, n_out, (int)V, &one, dA, n_out, ones, 1, &zero, db, 1),
-                       "cublasSgemv db");
-            if (l == 0) break;
-            // delta_{l-1} = (delta_l · W_l) ⊙ softplus'(z_{l-1})
-            blas_check(cublasSgemm(ctx->blas, CUBLAS_OP_T, CUBLAS_OP_N, n_in, (int)V, n_out, &one, theta + off[l], n_out,
-                                   dA, n_out, &zero, dB, n_in),
-                       "cublasSgemm delta");
-            FSK_LAUNCH(ctx, st, k_softplus_bwd, blocks_for(V * n_in, 256), 256, 0, dB,
-                       act_h + (int64_t)(l - 1) * V * H, V * n_in);
-            std::swap(dA, dB);
-        }
+        net.P = o;
+        const size_t smb = (size_t)(3 * kBT * net.maxw + net.maxw * net.maxw) * sizeof(float);
+        cuda_check(cudaFuncSetAttribute(k_mlp_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb),
+                   "cudaFuncSetAttribute");
+        const int64_t tiles = (V + kBT - 1) / kBT;
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, ctx->sm_count));
+        float* part = (float*)scratch(ctx, kMlpD0, (size_t)grid * net.P * sizeof(float));
+        FSK_LAUNCH(ctx, st, k_mlp_bwd, grid, 256, smb, net, theta, act, w, grad_w, V, H, part);
+        FSK_LAUNCH(ctx, st, k_bwd_reduce, blocks_for(net.P, 256), 256, 0, part, grid, net.P, grad_theta);
     });
 }
 
