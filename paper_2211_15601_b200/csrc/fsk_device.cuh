@@ -161,10 +161,15 @@ __device__ __forceinline__ void trilerp_T(const Planes<R>& P, const GridP& g, co
 // float32 pass: about half of all Broyden re-evaluations land in the cell of the previous
 // evaluation (late iterations take short steps), and those then issue no gather at all.
 // The arithmetic is the same as trilerp_T's, so results are bitwise identical.
+#ifndef FSK_CACHE_ROWS
+#define FSK_CACHE_ROWS 3  // matrix rows of the current cell held in registers (the rest re-read from L1)
+#endif
+constexpr int kCacheRows = FSK_CACHE_ROWS;
+
 template <typename R>
 struct CellCache {
     int base;
-    V4<R> a[4][3], b[4][3];  // [edge (dj + 2·dk)][row]: corner di = 0 / 1
+    V4<R> a[4][3], b[4][3];  // [edge (dj + 2·dk)][row]: corner di = 0 / 1 (rows < kCacheRows used)
 };
 
 template <typename R>
@@ -175,14 +180,16 @@ __device__ __forceinline__ void cache_fill(const Planes<R>& P, const GridP& g, i
     for (int e = 0; e < 4; ++e) {
         const int v = base + (e >> 1) * nxy + (e & 1) * g.nx;
 #pragma unroll
-        for (int r = 0; r < 3; ++r) load_edge(P, v, r, C.a[e][r], C.b[e][r]);
+        for (int r = 0; r < kCacheRows; ++r) load_edge(P, v, r, C.a[e][r], C.b[e][r]);
     }
 }
 
 template <typename R>
-__device__ __forceinline__ void trilerp_cached(const CellCache<R>& C, const Cell<R>& c, R T[12]) {
+__device__ __forceinline__ void trilerp_cached(const Planes<R>& P, const GridP& g, const CellCache<R>& C,
+                                               const Cell<R>& c, R T[12]) {
 #pragma unroll
     for (int e = 0; e < 12; ++e) T[e] = 0;
+    const int nxy = g.nx * g.ny;
 #pragma unroll
     for (int dk = 0; dk < 2; ++dk) {
         const R wz = dk ? c.tz : (R)1 - c.tz;
@@ -192,8 +199,15 @@ __device__ __forceinline__ void trilerp_cached(const CellCache<R>& C, const Cell
             const R w0 = wyz * ((R)1 - c.tx), w1 = wyz * c.tx;
 #pragma unroll
             for (int r = 0; r < 3; ++r) {
-                fma4(T + 4 * r, w0, C.a[2 * dk + dj][r]);
-                fma4(T + 4 * r, w1, C.b[2 * dk + dj][r]);
+                V4<R> a, b;
+                if (r < kCacheRows) {
+                    a = C.a[2 * dk + dj][r];
+                    b = C.b[2 * dk + dj][r];
+                } else {
+                    load_edge(P, c.base + dk * nxy + dj * g.nx, r, a, b);
+                }
+                fma4(T + 4 * r, w0, a);
+                fma4(T + 4 * r, w1, b);
             }
         }
     }
@@ -248,7 +262,7 @@ __device__ __forceinline__ void jacobian_and_T(const Planes<R>& P, const GridP& 
 #pragma unroll
             for (int r = 0; r < 3; ++r) {
                 V4<R> a, b;
-                if constexpr (kCache) {
+                if (kCache && r < kCacheRows) {
                     a = C->a[2 * dk + dj][r];
                     b = C->b[2 * dk + dj][r];
                 } else {
@@ -373,7 +387,7 @@ __device__ __forceinline__ bool broyden_step(const Planes<R>& P, const GridP& g,
             cache_fill(P, g, c.base, *C);
             if (fills) ++*fills;
         }
-        trilerp_cached(*C, c, T);
+        trilerp_cached(P, g, *C, c, T);
     } else {
         trilerp_T(P, g, c, T);
     }
