@@ -536,6 +536,7 @@ def main():
     run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist
+        dist.barrier()  # rank 0 ran the untimed extras (MLP stages, e2e) after the timed region
         dist.destroy_process_group()
 
 
