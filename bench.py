@@ -383,8 +383,10 @@ def run_ours(args, rank, world, local_rank):
 
     if rank == 0 and not args.no_mlp:
         line["mlp_stages"] = mlp_stages(D, sc, roots_buf, n, dev)
-    if rank == 0 and not args.no_e2e:
-        line["e2e"] = e2e_ours(D, sc, opts, args)
+    if not args.no_e2e:  # every rank its own shard through the host API; whole-job rate, max over ranks
+        e2e = e2e_ours(D, sc, opts, args, world=world)
+        if rank == 0:
+            line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         workers = os.cpu_count() or 1
         rate, m, dt = cpu_rate(sc, args, args.cpu_seconds, workers)
@@ -496,7 +498,7 @@ def mlp_stages(D, sc, roots_buf, n, dev, reps=20):
     return out
 
 
-def e2e_ours(D, sc, opts, args, steps=None):
+def e2e_ours(D, sc, opts, args, steps=None, world=1):
     """Same metric through the C-ABI host-buffer entry point (fsk_deform_host): pinned host
     weights/bones/points in, CorrespondenceSets (offsets + kept roots) out, copies inside."""
     import torch
@@ -510,11 +512,18 @@ def e2e_ours(D, sc, opts, args, steps=None):
     for _ in range(2):
         total = D.deform_host(hw, sc.dims, sc.bbox, hb, hx, opts, hoffs, hroots)
     torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
     t0 = time.perf_counter()
     for _ in range(steps):
         total = D.deform_host(hw, sc.dims, sc.bbox, hb, hx, opts, hoffs, hroots)
     dt = (time.perf_counter() - t0) / steps
-    return {"value": n * nb / dt, "unit": UNIT, "ms_per_step": 1e3 * dt,
+    if world > 1:
+        t = torch.tensor([dt], dtype=torch.float64, device=torch.cuda.current_device())
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    return {"value": world * n * nb / dt, "unit": UNIT, "ms_per_step": 1e3 * dt,
             "h2d_bytes_per_step": int(hw.numel() * 4 + hb.numel() * 4 + hx.numel() * 4),
             "d2h_bytes_per_step": int((n + 1) * 8 + total * 64),
             "api": "fsk_deform_host (C-ABI, pinned host buffers; synchronous call timed on the host clock)"}
