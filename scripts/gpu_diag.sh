@@ -1,1 +1,1 @@
-BENCH_ARGS="--no-mlp" bash scripts/gpu_variants.sh
+timeout 900 python bench.py > gpurun_out/final_c2.json 2> gpurun_out/final_c2.err
