@@ -290,7 +290,7 @@ __device__ __forceinline__ float act_fwd(float z, bool tangent, int role) {
 // One 128-row tile per iteration of a persistent CTA (128 threads; thread t owns TMEM lane t =
 // tile row t). TMEM columns: D [0, H), A_hi [H, 2H), A_lo [2H, 3H).
 // act (optional, for the backward): x [n][4] then the softplus outputs h_l [(n_hidden+1)][n][H].
-template <int H, bool kStream>
+template <int H, bool kStream, bool kTangent>
 __global__ void __launch_bounds__(kThreads, H == 64 ? 2 : 1)  // H = 64: two CTAs per SM (256 TMEM columns each)
     k_mlp_fwd(MlpDev m, const float* __restrict__ pk, MlpRows R, float* __restrict__ out, float* __restrict__ act) {
     extern __shared__ __align__(128) float smem[];
@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(kThreads, H == 64 ? 2 : 1)  // H = 64: two CTA
         // ---- layer 0 (K0 inputs) on the FP32 pipe → A (hi/lo) in TMEM
         float x[3];
         row_input(R, rr, x);
-        const bool tan = R.source == kRowsPositions && R.tangent;
+        constexpr bool tan = kTangent;  // 4-row groups {value, d/dx, d/dy, d/dz} (MLP-variant starts)
         const int role = tan ? (int)(row & 3) : 0;  // 0: value row, 1..3: d/dx_{role-1}
         float* act_h = act ? act + 4 * R.n : nullptr;
         if (act && half == 0 && row < R.n)
@@ -457,15 +457,15 @@ __global__ void __launch_bounds__(kThreads, H == 64 ? 2 : 1)  // H = 64: two CTA
                     if (role == 0) z[i] += s_headv[i];
                     mx = fmaxf(mx, z[i]);
                 }
-                float sum = 0.f, zt[64];
+                float sum = 0.f, zt[kTangent ? 64 : 1];
                 for (int i = 0; i < m.n_out; ++i) {
-                    zt[i] = z[i];
+                    if constexpr (kTangent) zt[i] = z[i];
                     z[i] = __expf(z[i] - mx);
                     sum += z[i];
                 }
                 const float inv = 1.f / sum;
                 for (int i = 0; i < m.n_out; ++i) z[i] *= inv;
-                if (tan) {  // softmax Jacobian on the tangent rows: ẇ = w ⊙ (ż − <w, ż>) (skinning.cpp:57-63)
+                if constexpr (kTangent) {  // softmax Jacobian on the tangent rows: ẇ = w ⊙ (ż − <w, ż>) (skinning.cpp:57-63)
                     float dot = 0.f;
                     for (int i = 0; i < m.n_out; ++i) {
                         const float wv = __shfl_sync(0xffffffffu, z[i], (threadIdx.x & 31) & ~3);
@@ -549,7 +549,7 @@ size_t fwd_smem_bytes(const MlpShape& s, bool stream) {
     return (size_t)f * 4;
 }
 
-template <int H, bool kStream>
+template <int H, bool kStream, bool kTangent>
 void launch_fwd(fsk_ctx* ctx, const MlpShape& s, const int32_t* widths, int nw, const float* pk, const MlpRows& R,
                 float* out, float* act, cudaStream_t st) {
     const size_t sm = fwd_smem_bytes(s, kStream);
@@ -557,17 +557,17 @@ void launch_fwd(fsk_ctx* ctx, const MlpShape& s, const int32_t* widths, int nw, 
     static thread_local size_t set_for = 0;
     static thread_local int per_sm = 1;
     if (set_for != sm) {
-        cuda_check(cudaFuncSetAttribute(k_mlp_fwd<H, kStream>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
+        cuda_check(cudaFuncSetAttribute(k_mlp_fwd<H, kStream, kTangent>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
                    "cudaFuncSetAttribute");
         // persistent grid = resident capacity (two CTAs per SM for H = 64: one's MMAs overlap the other's epilogue)
-        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mlp_fwd<H, kStream>, kThreads, sm),
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mlp_fwd<H, kStream, kTangent>, kThreads, sm),
                    "occupancy");
         set_for = sm;
     }
     const int64_t tiles = (R.n + kTile - 1) / kTile;
     const unsigned grid =
         (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)ctx->sm_count * std::max(per_sm, 1)));
-    FSK_LAUNCH(ctx, st, (k_mlp_fwd<H, kStream>), grid, kThreads, sm, to_dev(s, widths, nw), pk, R, out, act);
+    FSK_LAUNCH(ctx, st, (k_mlp_fwd<H, kStream, kTangent>), grid, kThreads, sm, to_dev(s, widths, nw), pk, R, out, act);
 }
 
 void run_fwd(fsk_ctx* ctx, const MlpShape& s, const int32_t* widths, int nw, const float* pk, const MlpRows& R,
@@ -576,12 +576,17 @@ void run_fwd(fsk_ctx* ctx, const MlpShape& s, const int32_t* widths, int nw, con
     // weights resident when they fit next to the head image (227 KB per CTA), else streamed per layer
     const bool stream = fwd_smem_bytes(s, false) > 200 * 1024;
     if (fwd_smem_bytes(s, stream) > 227 * 1024) fail(FSK_EINVAL, "fsk mlp: network too large for one CTA");
+    const bool tan = R.source == kRowsPositions && R.tangent;
     if (s.H == 64) {
-        if (stream) launch_fwd<64, true>(ctx, s, widths, nw, pk, R, out, act, st);
-        else launch_fwd<64, false>(ctx, s, widths, nw, pk, R, out, act, st);
+        if (tan && stream) launch_fwd<64, true, true>(ctx, s, widths, nw, pk, R, out, act, st);
+        else if (tan) launch_fwd<64, false, true>(ctx, s, widths, nw, pk, R, out, act, st);
+        else if (stream) launch_fwd<64, true, false>(ctx, s, widths, nw, pk, R, out, act, st);
+        else launch_fwd<64, false, false>(ctx, s, widths, nw, pk, R, out, act, st);
     } else {
-        if (stream) launch_fwd<128, true>(ctx, s, widths, nw, pk, R, out, act, st);
-        else launch_fwd<128, false>(ctx, s, widths, nw, pk, R, out, act, st);
+        if (tan && stream) launch_fwd<128, true, true>(ctx, s, widths, nw, pk, R, out, act, st);
+        else if (tan) launch_fwd<128, false, true>(ctx, s, widths, nw, pk, R, out, act, st);
+        else if (stream) launch_fwd<128, true, false>(ctx, s, widths, nw, pk, R, out, act, st);
+        else launch_fwd<128, false, false>(ctx, s, widths, nw, pk, R, out, act, st);
     }
 }
 
