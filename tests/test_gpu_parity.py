@@ -453,3 +453,28 @@ def test_full_size_mask_agreement_on_sample(deformer, c2_full):
     print(f"\nfull-size sample: identical root sets {agree}/{len(idx)}, max|dx| {maxdx:.2e}")
     assert agree / len(idx) >= MASK_AGREE
     assert maxdx <= TOL_X
+
+
+@pytest.mark.parametrize("dims,n,points", [((64, 64, 64), 1_000_000, "training"), ((128, 128, 32), 2_000_000, "uniform")])
+def test_large_batch_sampled_parity(deformer, dims, n, points):
+    """BASELINE configs 4 and 5 grid shapes at large batch sizes (1M / 2M posed points in one
+    call): root sets of an 8k-query sample against the oracle run on just those queries."""
+    sc = S.make_scene(dims, n, seed=61, points=points)
+    w, B, x = dev(sc.weights), dev(sc.bones), dev(sc.points)
+    offs, roots = deformer.deform(w, sc.dims, sc.bbox, B, x, opts_of(sc, 50))
+    torch.cuda.synchronize()
+    idx = np.sort(np.random.default_rng(1).choice(n, 8000, replace=False))
+    sub = S.Scene(sc.dims, sc.bbox, sc.weights, sc.bones, sc.points[idx], sc.angles, sc.diag)
+    r = run_oracle(sub, 50)
+    offs_h, rh = offs.cpu().numpy(), roots.cpu().numpy()
+    agree, maxdx = 0, 0.0
+    for k, p in enumerate(idx):
+        recs = rh[offs_h[p]:offs_h[p + 1]]
+        bg = recs[:, 13].view(np.int32).tolist()
+        agree += bg == np.where(r["keep"][k] == 1)[0].tolist()
+        for rec, b in zip(recs, bg):
+            if r["keep"][k, b]:
+                maxdx = max(maxdx, float(np.abs(rec[:3] - r["x_c"][k, b]).max()))
+    print(f"\n{dims} x {n}: identical root sets {agree}/{len(idx)}, max|dx| {maxdx:.2e}")
+    assert agree / len(idx) >= 0.999  # root-set identity per query (24 solves each)
+    assert maxdx <= TOL_X
