@@ -65,6 +65,14 @@ typedef struct fsk_search_opts {
 #define FSK_SEARCH_NO_SORT 0x1    /* ablation: skip the spatial ordering of queries */
 #define FSK_SEARCH_FP32_ONLY 0x2  /* ablation: float32 only, no float64 escalation */
 #define FSK_SEARCH_FP64 0x4       /* parity mode: every solve in float64 */
+#define FSK_SEARCH_EXACT64 0x8    /* replay mode: every solve in float64 in the reference's own
+                                     operation order (unfused, J~0 from the n_b-wide weight grid),
+                                     bit-identical to a float64 build of the reference given the same
+                                     transform grid; needs the weight grid (fsk_search_fwd /
+                                     fsk_batch_search `weights`, always present in fsk_deform*) */
+#define FSK_SEARCH_EXACT_ESC 0x10 /* mixed mode whose float64 escalation pass runs the exact replay:
+                                     escalated solves equal the reference bit for bit, the rest are
+                                     the float32 pass's; needs the weight grid like EXACT64 */
 
 /* Dense per-(point, init) search result (the GPU form of Root / CorrespondenceSet,
  * correspondence.hpp:29-42). All pointers dev, [N][n_b] point-major; any may be NULL
@@ -134,9 +142,11 @@ int fsk_precompute_tgrid(fsk_ctx* ctx, const float* weights, const fsk_grid_desc
  * grid Jacobian (:43-54), good-Broyden iterate (:97-124), converged mask, dedup (:162-176).
  * The transform grid is given as float32 `tgrid` and/or float64 `tgrid64` (either may be
  * NULL, not both); the float64 re-solves read tgrid64 when given (exact parity with an f64
- * TransformGrid), else the float32 grid widened. points, grids, bones dev. N may be 0. */
+ * TransformGrid), else the float32 grid widened. `weights` [V][n_b] (dev) is the skinning
+ * weight grid (SearchContext::grid); it is read only under FSK_SEARCH_EXACT64 and may be NULL
+ * otherwise. points, grids, bones dev. N may be 0. */
 int fsk_search_fwd(fsk_ctx* ctx, const float* tgrid, const double* tgrid64,
-                   const fsk_grid_desc* desc, const float* bones, int32_t n_bones_pose,
+                   const float* weights, const fsk_grid_desc* desc, const float* bones, int32_t n_bones_pose,
                    const float* points, int64_t n, const fsk_search_opts* opts,
                    fsk_search_out* out, void* stream);
 
@@ -146,7 +156,7 @@ int fsk_search_fwd(fsk_ctx* ctx, const float* tgrid, const double* tgrid64,
  * `cap` records; records beyond cap are dropped — check offsets[N] <= cap (N*n_b always
  * suffices). Fully asynchronous (no host synchronization). */
 int fsk_batch_search(fsk_ctx* ctx, const float* tgrid, const double* tgrid64,
-                     const fsk_grid_desc* desc, const float* bones, int32_t n_bones_pose,
+                     const float* weights, const fsk_grid_desc* desc, const float* bones, int32_t n_bones_pose,
                      const float* points, int64_t n, const fsk_search_opts* opts,
                      int64_t* offsets, fsk_root* roots, int64_t cap, void* stream);
 

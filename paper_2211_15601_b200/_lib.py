@@ -17,6 +17,8 @@ FSK_OK, FSK_EINVAL, FSK_ECUDA, FSK_ENODEV, FSK_EIO = 0, 1, 2, 3, 4
 FSK_SEARCH_NO_SORT = 0x1
 FSK_SEARCH_FP32_ONLY = 0x2
 FSK_SEARCH_FP64 = 0x4
+FSK_SEARCH_EXACT64 = 0x8
+FSK_SEARCH_EXACT_ESC = 0x10
 
 # Every symbol include/fsk.h declares (checked by tests/test_lib_exports.py).
 EXPORTS = [
@@ -86,14 +88,14 @@ def load():
     L.fsk_search_opts_defaults.restype = SearchOpts
     G, O, S = ctypes.POINTER(GridDesc), ctypes.POINTER(SearchOpts), ctypes.POINTER(SearchOut)
     L.fsk_precompute_tgrid.argtypes = [_vp, _vp, G, _vp, _i32, _vp, _vp, _vp]
-    L.fsk_search_fwd.argtypes = [_vp, _vp, _vp, G, _vp, _i32, _vp, _i64, O, S, _vp]
+    L.fsk_search_fwd.argtypes = [_vp, _vp, _vp, _vp, G, _vp, _i32, _vp, _i64, O, S, _vp]
     L.fsk_compact_roots.argtypes = [_vp, S, _i64, _i32, _vp, _vp, _i64, ctypes.POINTER(_i64), _vp]
     L.fsk_deform_host.argtypes = [_vp, _vp, G, _vp, _i32, _vp, _i64, O, _vp, _vp, _i64, ctypes.POINTER(_i64), _vp]
     L.fsk_eval_points.argtypes = [_vp, _vp, G, _vp, _i64, _vp, _vp, _vp, _vp]
     L.fsk_init_states.argtypes = [_vp, _vp, G, _vp, _i32, _vp, _i64, _vp, _vp, _vp]
     L.fsk_search_bwd.argtypes = [_vp, G, _vp, _vp, _i32, _vp, _vp, _i64, _vp, ctypes.c_int, _vp]
     L.fsk_grad_weights.argtypes = [_vp, G, _vp, _vp, _i32, _vp, _vp]
-    L.fsk_batch_search.argtypes = [_vp, _vp, _vp, G, _vp, _i32, _vp, _i64, O, _vp, _vp, _i64, _vp]
+    L.fsk_batch_search.argtypes = [_vp, _vp, _vp, _vp, G, _vp, _i32, _vp, _i64, O, _vp, _vp, _i64, _vp]
     L.fsk_deform.argtypes = [_vp, _vp, G, _vp, _i32, _vp, _i64, O, _vp, _vp, _vp, _i64, _vp]
     L.fsk_search_bwd_roots.argtypes = [_vp, G, _vp, _vp, _vp, _i64, _vp, ctypes.c_int, _vp]
     L.fsk_ctx_set_profiling.argtypes = [_vp, ctypes.c_int]

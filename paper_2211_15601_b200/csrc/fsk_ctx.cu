@@ -99,6 +99,12 @@ SearchP make_search(const fsk_search_opts* o) {
         fail(FSK_EINVAL, "fsk: FSK_SEARCH_FP32_ONLY and FSK_SEARCH_FP64 are exclusive");
     SearchP s;
     s.max_iters = o->max_iters;
+    if ((o->flags & FSK_SEARCH_FP32_ONLY) && (o->flags & FSK_SEARCH_EXACT64))
+        fail(FSK_EINVAL, "fsk: FSK_SEARCH_FP32_ONLY and FSK_SEARCH_EXACT64 are exclusive");
+    if ((o->flags & FSK_SEARCH_EXACT_ESC) && (o->flags & (FSK_SEARCH_FP32_ONLY | FSK_SEARCH_FP64 | FSK_SEARCH_EXACT64)))
+        fail(FSK_EINVAL, "fsk: FSK_SEARCH_EXACT_ESC applies to the mixed mode only");
+    s.conv_eps = o->conv_eps;
+    s.div_eps = o->div_eps;
     s.conv2 = o->conv_eps * o->conv_eps;
     s.div2 = o->div_eps * o->div_eps;
     s.dedup2 = o->dedup_dist * o->dedup_dist;
@@ -259,7 +265,10 @@ int fsk_ctx_prof_read(fsk_ctx* ctx, const char* name, double* total_ms, int64_t*
         double t = 0.0;
         int64_t c = 0;
         for (auto& r : ctx->prof) {
-            if (name && std::strcmp(name, r.name) != 0) continue;
+            if (name) {  // a kernel template matches its base name ("k" matches "k<true>")
+                const size_t L = std::strlen(name);
+                if (std::strncmp(name, r.name, L) != 0 || (r.name[L] != '\0' && r.name[L] != '<')) continue;
+            }
             cuda_check(cudaEventSynchronize(r.b), "cudaEventSynchronize");
             float ms = 0.f;
             cuda_check(cudaEventElapsedTime(&ms, r.a, r.b), "cudaEventElapsedTime");

@@ -46,6 +46,7 @@ struct SearchP {
     int esc_cap;        // fp32 pass stops after this many iterations and escalates
     int esc_min_div;    // escalate unconverged solves with at least this many iterations
     double conv2, div2, dedup2;
+    double conv_eps, div_eps;  // unsquared, for the exact replay (err = sqrt(g·g) compared as the reference does)
     float esc_conv_lo, esc_conv_hi;  // err2 within [lo,hi]·conv2 → threshold too close to call in fp32
     float esc_div_lo, esc_div_hi;
     float esc_det;      // |det J0| below this → singular-fallback decision too close to call

@@ -1,0 +1,288 @@
+// fsk_exact.cuh — float64 replay of the reference's operation order (opt-in: FSK_SEARCH_EXACT64).
+//
+// Broyden trajectories of 25-50 iterations are chaotic even in float64: two implementations
+// that round one operation differently (an FMA contraction, (p−lo)·scale instead of
+// (p−lo)/ext·(n−1), the transform-grid form of J0 instead of the weight-grid form) part ways
+// and may stop at a different root. This path removes every such difference for the solves it
+// runs: each operation is an explicit round-to-nearest intrinsic (__dmul_rn / __dadd_rn /
+// __dsub_rn / __ddiv_rn, never contracted) in the order of the reference as restated by the
+// oracle —
+//   locate_cell / locate_cell_lower        skinning.cpp:104-139
+//   trilerp_weights_into                   skinning.cpp:141-156
+//   weight_spatial_gradient                skinning.cpp:164-193
+//   trilerp_transform_into, forward_deform deformer.cpp:79-94, :107-113
+//   deform_jacobian (weight-grid form)     deformer.cpp:117-136
+//   initial_inverse_jacobian (det, inv)    correspondence.cpp:43-54 (Eigen closed forms)
+//   RigidTransform::inverse / apply        geometry.hpp:51-61
+//   iterate                                correspondence.cpp:97-124
+// so a solve's float64 state is bit-identical to the oracle's (given the same float64 transform
+// grid, which k_precompute builds in lbs_blend's order). It needs the weight grid ([V][n_b]
+// float32, exactly representable in float64) for J0, like the reference's SearchContext.
+#pragma once
+
+#include "fsk_device.cuh"
+
+namespace fsk {
+namespace exact {
+
+__device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double div(double a, double b) { return __ddiv_rn(a, b); }
+// a0*b0 + a1*b1 + a2*b2, left to right
+__device__ __forceinline__ double dot3(double a0, double a1, double a2, double b0, double b1, double b2) {
+    return add(add(mul(a0, b0), mul(a1, b1)), mul(a2, b2));
+}
+
+struct XCell {
+    int i, j, k;
+    double tx, ty, tz;
+};
+
+// locate_cell (skinning.cpp:104-120) / locate_cell_lower (:122-139)
+__device__ __forceinline__ XCell locate(const GridP& g, double x0, double x1, double x2, bool lower) {
+    const double xs[3] = {x0, x1, x2};
+    const int n[3] = {g.nx, g.ny, g.nz};
+    int idx[3];
+    double t[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        double p = xs[a];
+        p = (p < g.lod[a]) ? g.lod[a] : p;  // Aabb::clamp (cwiseMax then cwiseMin)
+        p = (p > g.hid[a]) ? g.hid[a] : p;
+        const double ext = sub(g.hid[a], g.lod[a]);
+        const double u = mul(div(sub(p, g.lod[a]), ext), (double)(n[a] - 1));
+        int i = (u == u) ? (int)floor(u) : 0;
+        if (lower && i >= 1 && u == (double)i) i -= 1;
+        i = i < 0 ? 0 : (i > n[a] - 2 ? n[a] - 2 : i);
+        idx[a] = i;
+        const double tt = sub(u, (double)i);
+        t[a] = tt < 0.0 ? 0.0 : (tt > 1.0 ? 1.0 : tt);
+    }
+    return XCell{idx[0], idx[1], idx[2], t[0], t[1], t[2]};
+}
+
+__device__ __forceinline__ int vidx(const GridP& g, int i, int j, int k) { return (k * g.ny + j) * g.nx + i; }
+
+// forward_deform(x, tgrid) (deformer.cpp:79-94, :107-113) from the float64 x-pair planes
+__device__ __forceinline__ void deform(const Planes<double>& P, const GridP& g, double x0, double x1, double x2,
+                                       double d[3]) {
+    const XCell c = locate(g, x0, x1, x2, false);
+    double m[12];
+#pragma unroll
+    for (int e = 0; e < 12; ++e) m[e] = 0.0;
+#pragma unroll
+    for (int dk = 0; dk < 2; ++dk) {
+        const double wz = dk ? c.tz : sub(1.0, c.tz);
+#pragma unroll
+        for (int dj = 0; dj < 2; ++dj) {
+            const double wyz = mul(wz, dj ? c.ty : sub(1.0, c.ty));
+            const int v = vidx(g, c.i, c.j + dj, c.k + dk);
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+                V4<double> a, b;
+                load_edge(P, v, r, a, b);
+                const double w0 = mul(wyz, sub(1.0, c.tx)), w1 = mul(wyz, c.tx);
+                // corner di = 0 then di = 1, entries in row order (the oracle's e loop per corner;
+                // each entry's sum runs over corners in the same (dk, dj, di) order)
+                m[4 * r + 0] = add(m[4 * r + 0], mul(w0, a.x));
+                m[4 * r + 1] = add(m[4 * r + 1], mul(w0, a.y));
+                m[4 * r + 2] = add(m[4 * r + 2], mul(w0, a.z));
+                m[4 * r + 3] = add(m[4 * r + 3], mul(w0, a.w));
+                m[4 * r + 0] = add(m[4 * r + 0], mul(w1, b.x));
+                m[4 * r + 1] = add(m[4 * r + 1], mul(w1, b.y));
+                m[4 * r + 2] = add(m[4 * r + 2], mul(w1, b.z));
+                m[4 * r + 3] = add(m[4 * r + 3], mul(w1, b.w));
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < 3; ++r) d[r] = add(dot3(m[4 * r], m[4 * r + 1], m[4 * r + 2], x0, x1, x2), m[4 * r + 3]);
+}
+
+// x0 = B^-1 x' = Rᵀx' + (−Rᵀt) (geometry.hpp:51-61)
+__device__ __forceinline__ void inverse_apply(const float* B, double xp0, double xp1, double xp2, double& x0,
+                                              double& x1, double& x2) {
+    double R[9], t[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) R[3 * r + c] = (double)B[4 * r + c];
+        t[r] = (double)B[4 * r + 3];
+    }
+    double xo[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const double rt = dot3(R[i], R[3 + i], R[6 + i], t[0], t[1], t[2]);  // (Rᵀ t)_i
+        xo[i] = add(dot3(R[i], R[3 + i], R[6 + i], xp0, xp1, xp2), -rt);
+    }
+    x0 = xo[0];
+    x1 = xo[1];
+    x2 = xo[2];
+}
+
+// deform_jacobian(x, grid, bones) via jacobian_from_weights (deformer.cpp:117-136): weights from
+// locate_cell (trilerp_weights_into), gradient from locate_cell_lower with ±1/h stencils
+// (weight_spatial_gradient), J = Σ_i w_i R_i then + Σ_i (B_i x)(∇w_i)ᵀ, bone order.
+__device__ __forceinline__ void jacobian(const GridP& g, const float* __restrict__ W, const float* __restrict__ bones,
+                                         double x0, double x1, double x2, double J[9]) {
+    const int nb = g.nb;
+    const XCell c = locate(g, x0, x1, x2, false), cl = locate(g, x0, x1, x2, true);
+    const int n[3] = {g.nx, g.ny, g.nz};
+    double h[3], dmin[3], dplus[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        h[a] = div(sub(g.hid[a], g.lod[a]), (double)(n[a] - 1));  // cell_size (skinning.cpp:72-75)
+        dmin[a] = div(-1.0, h[a]);
+        dplus[a] = div(1.0, h[a]);
+    }
+#pragma unroll
+    for (int e = 0; e < 9; ++e) J[e] = 0.0;
+    for (int b = 0; b < nb; ++b) {  // Σ_i w_i R_i
+        double wb = 0.0;
+#pragma unroll
+        for (int dk = 0; dk < 2; ++dk) {
+            const double wz = dk ? c.tz : sub(1.0, c.tz);
+#pragma unroll
+            for (int dj = 0; dj < 2; ++dj) {
+                const double wyz = mul(wz, dj ? c.ty : sub(1.0, c.ty));
+#pragma unroll
+                for (int di = 0; di < 2; ++di) {
+                    const double w = mul(wyz, di ? c.tx : sub(1.0, c.tx));
+                    wb = add(wb, mul(w, (double)__ldg(W + (int64_t)vidx(g, c.i + di, c.j + dj, c.k + dk) * nb + b)));
+                }
+            }
+        }
+        const float* B = bones + 12 * b;
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) J[3 * r + cc] = add(J[3 * r + cc], mul(wb, (double)B[4 * r + cc]));
+    }
+    const double fx[2] = {sub(1.0, cl.tx), cl.tx}, fy[2] = {sub(1.0, cl.ty), cl.ty}, fz[2] = {sub(1.0, cl.tz), cl.tz};
+    for (int b = 0; b < nb; ++b) {  // + Σ_i (B_i x) ∇w_iᵀ
+        double gg[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int dk = 0; dk < 2; ++dk)
+#pragma unroll
+            for (int dj = 0; dj < 2; ++dj)
+#pragma unroll
+                for (int di = 0; di < 2; ++di) {
+                    const double v = (double)__ldg(W + (int64_t)vidx(g, cl.i + di, cl.j + dj, cl.k + dk) * nb + b);
+                    const double gx = mul(mul(di ? dplus[0] : dmin[0], fy[dj]), fz[dk]);
+                    const double gy = mul(mul(fx[di], dj ? dplus[1] : dmin[1]), fz[dk]);
+                    const double gz = mul(mul(fx[di], fy[dj]), dk ? dplus[2] : dmin[2]);
+                    gg[0] = add(gg[0], mul(gx, v));
+                    gg[1] = add(gg[1], mul(gy, v));
+                    gg[2] = add(gg[2], mul(gz, v));
+                }
+        const float* B = bones + 12 * b;
+        double bx[3];
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+            bx[r] = add(dot3((double)B[4 * r], (double)B[4 * r + 1], (double)B[4 * r + 2], x0, x1, x2), (double)B[4 * r + 3]);
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) J[3 * r + cc] = add(J[3 * r + cc], mul(bx[r], gg[cc]));
+    }
+}
+
+// initial_inverse_jacobian (correspondence.cpp:43-54): Eigen's det (expansion along row 0)
+// against 1e-8, then the cofactor inverse with its own det (adjugate / det)
+__device__ __forceinline__ void inverse_or_identity(const double a[9], double Ji[9]) {
+    auto h = [&](int c0, int c1, int c2) {
+        return mul(a[c0], sub(mul(a[3 + c1], a[6 + c2]), mul(a[3 + c2], a[6 + c1])));
+    };
+    const double det = add(sub(h(0, 1, 2), h(1, 0, 2)), h(2, 0, 1));
+    if (fabs(det) < 1e-8) {
+#pragma unroll
+        for (int e = 0; e < 9; ++e) Ji[e] = (e % 4 == 0) ? 1.0 : 0.0;
+        return;
+    }
+    double c[9];
+    c[0] = sub(mul(a[4], a[8]), mul(a[5], a[7]));
+    c[1] = sub(mul(a[2], a[7]), mul(a[1], a[8]));
+    c[2] = sub(mul(a[1], a[5]), mul(a[2], a[4]));
+    c[3] = sub(mul(a[5], a[6]), mul(a[3], a[8]));
+    c[4] = sub(mul(a[0], a[8]), mul(a[2], a[6]));
+    c[5] = sub(mul(a[2], a[3]), mul(a[0], a[5]));
+    c[6] = sub(mul(a[3], a[7]), mul(a[4], a[6]));
+    c[7] = sub(mul(a[1], a[6]), mul(a[0], a[7]));
+    c[8] = sub(mul(a[0], a[4]), mul(a[1], a[3]));
+    const double d2 = add(add(mul(a[0], c[0]), mul(a[1], c[3])), mul(a[2], c[6]));
+    const double inv = div(1.0, d2);
+#pragma unroll
+    for (int e = 0; e < 9; ++e) Ji[e] = mul(c[e], inv);
+}
+
+__device__ __forceinline__ double norm3(double g0, double g1, double g2) {
+    return __dsqrt_rn(add(add(mul(g0, g0), mul(g1, g1)), mul(g2, g2)));
+}
+
+// Solve state of the replay (search_one's per-init body, correspondence.cpp:132-146)
+struct XState {
+    double x0, x1, x2, g0, g1, g2, err;
+    double Ji[9];
+    double dx0, dx1, dx2;
+    int k;
+};
+
+// start: x0, J~0, g0 and err (the converged / diverged decisions are the caller's)
+__device__ __forceinline__ void start(const Planes<double>& P, const GridP& g, const float* __restrict__ W,
+                                      const float* __restrict__ bones, int bone, double xp0, double xp1, double xp2,
+                                      XState& s) {
+    inverse_apply(bones + 12 * bone, xp0, xp1, xp2, s.x0, s.x1, s.x2);
+    double J[9];
+    jacobian(g, W, bones, s.x0, s.x1, s.x2, J);
+    inverse_or_identity(J, s.Ji);
+    double d[3];
+    deform(P, g, s.x0, s.x1, s.x2, d);
+    s.g0 = sub(d[0], xp0);
+    s.g1 = sub(d[1], xp1);
+    s.g2 = sub(d[2], xp2);
+    s.err = norm3(s.g0, s.g1, s.g2);
+    s.k = 0;
+}
+
+// one pass of iterate's loop body after the divergence check (correspondence.cpp:106-122);
+// returns true iff converged
+__device__ __forceinline__ bool step(const Planes<double>& P, const GridP& g, double xp0, double xp1, double xp2,
+                                     double conv_eps, XState& s) {
+    const double* J = s.Ji;
+    const double dx0 = -dot3(J[0], J[1], J[2], s.g0, s.g1, s.g2);
+    const double dx1 = -dot3(J[3], J[4], J[5], s.g0, s.g1, s.g2);
+    const double dx2 = -dot3(J[6], J[7], J[8], s.g0, s.g1, s.g2);
+    s.x0 = add(s.x0, dx0);
+    s.x1 = add(s.x1, dx1);
+    s.x2 = add(s.x2, dx2);
+    double d[3];
+    deform(P, g, s.x0, s.x1, s.x2, d);
+    const double n0 = sub(d[0], xp0), n1 = sub(d[1], xp1), n2 = sub(d[2], xp2);
+    const double dg0 = sub(n0, s.g0), dg1 = sub(n1, s.g1), dg2 = sub(n2, s.g2);
+    s.g0 = n0;
+    s.g1 = n1;
+    s.g2 = n2;
+    s.k += 1;
+    s.err = norm3(n0, n1, n2);
+    if (s.err < conv_eps) return true;
+    const double j0 = dot3(J[0], J[1], J[2], dg0, dg1, dg2);
+    const double j1 = dot3(J[3], J[4], J[5], dg0, dg1, dg2);
+    const double j2 = dot3(J[6], J[7], J[8], dg0, dg1, dg2);
+    const double den = dot3(dx0, dx1, dx2, j0, j1, j2);
+    if (fabs(den) > 1e-18) {
+        const double r0 = div(sub(dx0, j0), den), r1 = div(sub(dx1, j1), den), r2 = div(sub(dx2, j2), den);
+        const double w0 = dot3(dx0, dx1, dx2, J[0], J[3], J[6]);
+        const double w1 = dot3(dx0, dx1, dx2, J[1], J[4], J[7]);
+        const double w2 = dot3(dx0, dx1, dx2, J[2], J[5], J[8]);
+        const double r[3] = {r0, r1, r2}, w[3] = {w0, w1, w2};
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) s.Ji[3 * i + c] = add(s.Ji[3 * i + c], mul(r[i], w[c]));
+    }
+    return false;
+}
+
+}  // namespace exact
+}  // namespace fsk

@@ -27,6 +27,7 @@
 #include <cstring>
 
 #include "fsk_ctx.h"
+#include "fsk_exact.cuh"
 
 namespace fsk {
 
@@ -74,7 +75,7 @@ __global__ void __launch_bounds__(256) k_precompute(const float* __restrict__ w,
         for (int e = 0; e < 4; ++e) T[e] = fmaf(wi, Bi[e], T[e]);  // lbs_blend bone order (deformer.cpp:9-19)
         if (f64)
 #pragma unroll
-            for (int e = 0; e < 4; ++e) D[e] = fma((double)wi, (double)Bi[e], D[e]);
+            for (int e = 0; e < 4; ++e) D[e] = __dadd_rn(D[e], __dmul_rn((double)wi, (double)Bi[e]));  // unfused, as lbs_blend
     }
     const bool has_left = (v % nx) != 0;
     if (tg) tg[3 * v + r] = make_float4(T[0], T[1], T[2], T[3]);
@@ -295,6 +296,15 @@ __device__ __forceinline__ void store_solve(const SearchPlanes& out, int64_t q, 
     out.meta[q] = (uint16_t)(s.iters | (s.conv ? 0x100 : 0));
 }
 
+// Final state of an exact-replay solve (fsk_exact.cuh): the residual is the replay's own norm.
+__device__ __forceinline__ void store_exact(const SearchPlanes& out, int64_t q, const exact::XState& s, bool conv) {
+    out.xr[q] = make_float4((float)s.x0, (float)s.x1, (float)s.x2, copysignf((float)s.err, conv ? 1.f : -1.f));
+    out.ja[q] = make_float4((float)s.Ji[0], (float)s.Ji[1], (float)s.Ji[2], (float)s.Ji[3]);
+    out.jb[q] = make_float4((float)s.Ji[4], (float)s.Ji[5], (float)s.Ji[6], (float)s.Ji[7]);
+    out.jc[q] = (float)s.Ji[8];
+    out.meta[q] = (uint16_t)(s.k | (conv ? 0x100 : 0));
+}
+
 // Work counters for the roofline (bench.py): per pass, solves / Broyden iterations /
 // converged-terminating iterations, one warp-aggregated atomic per warp.
 __device__ __forceinline__ void count_work(unsigned long long* stats, const SolveOut& s) {
@@ -358,8 +368,10 @@ constexpr int kEscBlock = 128;
 #ifndef FSK_REFILL_IDLE
 #define FSK_REFILL_IDLE 16  // measured 16 (0.253 ms) vs 12 (0.260) vs 8 (0.265) vs 20 (0.255)
 #endif
+template <bool kExact>  // kExact: the solves replay the reference's operation order (fsk_exact.cuh)
 __global__ void __launch_bounds__(kEscBlock, FSK_ESC_MINB)
-    k_search_escalated(Planes<double> P, GridP g, const float* __restrict__ bones, int64_t n, SearchP o,
+    k_search_escalated(Planes<double> P, GridP g, const float* __restrict__ W, const float* __restrict__ bones,
+                       int64_t n, SearchP o,
                        SearchPlanes out, const int4* __restrict__ esc_q, int64_t esc_cap,
                        const int* __restrict__ esc_count, unsigned long long* __restrict__ stats) {
     // Persistent lanes with refill: a lane whose solve finished takes the next queue entry
@@ -379,6 +391,7 @@ __global__ void __launch_bounds__(kEscBlock, FSK_ESC_MINB)
     double x0 = 0, x1 = 0, x2 = 0, Ji[9], g0 = 0, g1 = 0, g2 = 0, err2 = 0;
 #pragma unroll
     for (int e = 0; e < 9; ++e) Ji[e] = 0;
+    exact::XState xs{};
     // Warp-local buffer of 32 queue slots (lane i holds slot base+i): one atomic per 32 solves.
     // Idle lanes are refilled in batches (>= kRefillIdle idle, or the whole warp), so the
     // divergent init path (x0, Jacobian stencil, inverse) runs for many lanes at once and the
@@ -408,12 +421,21 @@ __global__ void __launch_bounds__(kEscBlock, FSK_ESC_MINB)
                 q = rec.x;
                 const int bone = (int)(q / n);
                 xq = make_float4(__int_as_float(rec.y), __int_as_float(rec.z), __int_as_float(rec.w), 0.f);
-                solve_start<double>(P, g, bones + 12 * bone, xq.x, xq.y, xq.z, x0, x1, x2, Ji, g0, g1, g2, err2);
                 k = 0;
                 active = true;
-                const bool conv = err2 < conv2;  // (:100-103)
-                if (conv || err2 > div2 || o.max_iters <= 0) {  // divergence check at the top (:105)
-                    store_solve(out, q, x0, x1, x2, Ji, err2, SolveOut{0, conv, false});
+                bool conv, stop;
+                if constexpr (kExact) {
+                    exact::start(P, g, W, bones, bone, xq.x, xq.y, xq.z, xs);
+                    conv = xs.err < o.conv_eps;
+                    stop = conv || xs.err > o.div_eps;
+                } else {
+                    solve_start<double>(P, g, bones + 12 * bone, xq.x, xq.y, xq.z, x0, x1, x2, Ji, g0, g1, g2, err2);
+                    conv = err2 < conv2;                 // (:100-103)
+                    stop = conv || err2 > div2;          // divergence check at the top (:105)
+                }
+                if (stop || o.max_iters <= 0) {
+                    if constexpr (kExact) store_exact(out, q, xs, conv);
+                    else store_solve(out, q, x0, x1, x2, Ji, err2, SolveOut{0, conv, false});
                     n_solves += 1;
                     active = false;
                 }
@@ -424,11 +446,19 @@ __global__ void __launch_bounds__(kEscBlock, FSK_ESC_MINB)
             continue;
         }
         if (active) {  // one Broyden iteration (:106-122)
-            double den;
-            const bool conv = broyden_step<double>(P, g, xq.x, xq.y, xq.z, conv2, x0, x1, x2, Ji, g0, g1, g2, err2, den);
+            bool conv, div;
+            if constexpr (kExact) {
+                conv = exact::step(P, g, xq.x, xq.y, xq.z, o.conv_eps, xs);
+                div = xs.err > o.div_eps;
+            } else {
+                double den;
+                conv = broyden_step<double>(P, g, xq.x, xq.y, xq.z, conv2, x0, x1, x2, Ji, g0, g1, g2, err2, den);
+                div = err2 > div2;
+            }
             ++k;
-            if (conv || k >= o.max_iters || err2 > div2) {
-                store_solve(out, q, x0, x1, x2, Ji, err2, SolveOut{k, conv, false});
+            if (conv || k >= o.max_iters || div) {
+                if constexpr (kExact) store_exact(out, q, xs, conv);
+                else store_solve(out, q, x0, x1, x2, Ji, err2, SolveOut{k, conv, false});
                 n_solves += 1;
                 n_iters += k;
                 n_final += (conv && k > 0);
@@ -460,6 +490,33 @@ __global__ void __launch_bounds__(128) k_search_f64(Planes<double> P, GridP g, c
     const SolveOut s = solve_one<double, false>(P, g, bones + 12 * bone, xq.x, xq.y, xq.z, o, x0, x1, x2, Ji, err2);
     store_solve(out, (int64_t)bone * n + j, x0, x1, x2, Ji, err2, s);
     count_work(stats ? stats + 3 : nullptr, s);
+}
+
+// Exact replay mode (FSK_SEARCH_EXACT64): every solve in float64 with the reference's own
+// operation order (fsk_exact.cuh), J~0 from the n_b-wide weight grid — bit-identical to the
+// oracle's search_one (correspondence.cpp:126-150) given the same float64 transform grid.
+__global__ void __launch_bounds__(128) k_search_exact(Planes<double> P, GridP g, const float* __restrict__ W,
+                                                      const float* __restrict__ bones, const float4* __restrict__ xs,
+                                                      int64_t n, int blocks_per_bone, SearchP o, SearchPlanes out,
+                                                      unsigned long long* __restrict__ stats) {
+    const int bone = blockIdx.x / blocks_per_bone;
+    const int64_t j = (int64_t)(blockIdx.x - bone * blocks_per_bone) * 128 + threadIdx.x;
+    if (j >= n) return;
+    const float4 xq = __ldg(xs + j);
+    const double xp0 = xq.x, xp1 = xq.y, xp2 = xq.z;
+    exact::XState s;
+    exact::start(P, g, W, bones, bone, xp0, xp1, xp2, s);
+    bool conv = s.err < o.conv_eps;  // iterate (correspondence.cpp:97-124)
+    if (!conv)
+        for (int k = 0; k < o.max_iters; ++k) {
+            if (s.err > o.div_eps) break;
+            if (exact::step(P, g, xp0, xp1, xp2, o.conv_eps, s)) {
+                conv = true;
+                break;
+            }
+        }
+    store_exact(out, (int64_t)bone * n + j, s, conv);
+    count_work(stats ? stats + 3 : nullptr, SolveOut{s.k, conv, false, false});
 }
 
 // ============================================================================ dedup
@@ -774,8 +831,10 @@ struct SearchState {
 };
 
 // sort + K2 (+ K2b escalation) + dedup into the ctx's search planes.
-SearchState run_search(fsk_ctx* ctx, const GridPlanes& P, const GridP& g, const float* bones, const float* pts,
-                       int64_t n, const SearchP& sp, int flags, cudaStream_t st) {
+SearchState run_search(fsk_ctx* ctx, const GridPlanes& P, const GridP& g, const float* weights, const float* bones,
+                       const float* pts, int64_t n, const SearchP& sp, int flags, cudaStream_t st) {
+    if ((flags & (FSK_SEARCH_EXACT64 | FSK_SEARCH_EXACT_ESC)) && !weights)
+        fail(FSK_EINVAL, "fsk: FSK_SEARCH_EXACT64 / _EXACT_ESC need the weight grid (J~0 from the skinning weights)");
     if (n >= (int64_t(1) << 31) / std::max(1, g.nb)) fail(FSK_EINVAL, "fsk: too many points for one call (split the batch)");
     const int64_t S = std::max<int64_t>(1, n * g.nb);
     SearchState s;
@@ -805,7 +864,13 @@ SearchState run_search(fsk_ctx* ctx, const GridPlanes& P, const GridP& g, const 
     } else {
         FSK_LAUNCH(ctx, st, k_identity_order, blocks_for(n, 256), 256, 0, pts, n, s.perm, xs, esc_n);
     }
-    if (flags & FSK_SEARCH_FP64) {
+    if (flags & FSK_SEARCH_EXACT64) {
+        const int bpb = (int)blocks_for(n, 128);
+        const int64_t nblocks = (int64_t)bpb * g.nb;
+        if (nblocks >= (int64_t(1) << 31)) fail(FSK_EINVAL, "fsk: search grid too large");
+        FSK_LAUNCH(ctx, st, k_search_exact, (unsigned)nblocks, 128, 0, P.p64, g, weights, bones, xs, n, bpb, sp, s.sp,
+                   ctx->stats);
+    } else if (flags & FSK_SEARCH_FP64) {
         const int bpb = (int)blocks_for(n, 128);
         const int64_t nblocks = (int64_t)bpb * g.nb;
         if (nblocks >= (int64_t(1) << 31)) fail(FSK_EINVAL, "fsk: search grid too large");
@@ -823,11 +888,19 @@ SearchState run_search(fsk_ctx* ctx, const GridPlanes& P, const GridP& g, const 
         FSK_LAUNCH(ctx, st, k_search_fast, (unsigned)nblocks, kSearchBlock, 0, P.p32, g, bones, xs, n, bpb, spf, s.sp,
                    esc_q, S, esc_n, ctx->stats);
         int per_sm = 0;  // persistent kernel: exactly the resident capacity
-        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search_escalated, kEscBlock, 0),
+        const bool exact_esc = flags & FSK_SEARCH_EXACT_ESC;
+        cuda_check(exact_esc ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search_escalated<true>,
+                                                                             kEscBlock, 0)
+                             : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search_escalated<false>,
+                                                                             kEscBlock, 0),
                    "occupancy");
-        if (esc)
-            FSK_LAUNCH(ctx, st, k_search_escalated, (unsigned)(ctx->sm_count * std::max(per_sm, 1)), kEscBlock, 0,
-                       P.p64, g, bones, n, sp, s.sp, esc_q, S, esc_n, ctx->stats);
+        const unsigned egrid = (unsigned)(ctx->sm_count * std::max(per_sm, 1));
+        if (esc && exact_esc)
+            FSK_LAUNCH(ctx, st, k_search_escalated<true>, egrid, kEscBlock, 0, P.p64, g, weights, bones, n, sp, s.sp,
+                       esc_q, S, esc_n, ctx->stats);
+        else if (esc)
+            FSK_LAUNCH(ctx, st, k_search_escalated<false>, egrid, kEscBlock, 0, P.p64, g, weights, bones, n, sp, s.sp,
+                       esc_q, S, esc_n, ctx->stats);
     }
     FSK_LAUNCH(ctx, st, k_dedup, blocks_for(n, 256), 256, 0, n, g.nb, (float)sp.dedup2, s.sp, s.perm, s.n_roots_p);
     return s;
@@ -1071,7 +1144,8 @@ int fsk_precompute_tgrid(fsk_ctx* ctx, const float* weights, const fsk_grid_desc
     });
 }
 
-int fsk_search_fwd(fsk_ctx* ctx, const float* tgrid, const double* tgrid64, const fsk_grid_desc* desc,
+int fsk_search_fwd(fsk_ctx* ctx, const float* tgrid, const double* tgrid64, const float* weights,
+                   const fsk_grid_desc* desc,
                    const float* bones, int32_t n_bones_pose, const float* points, int64_t n,
                    const fsk_search_opts* opts, fsk_search_out* out, void* stream) {
     return guard([&] {
@@ -1087,7 +1161,7 @@ int fsk_search_fwd(fsk_ctx* ctx, const float* tgrid, const double* tgrid64, cons
         if (n == 0) return;
         cudaStream_t st = (cudaStream_t)stream;
         const GridPlanes P = run_relayout(ctx, tgrid, tgrid64, g, needs_f64(opts->flags), st);
-        const SearchState s = run_search(ctx, P, g, bones, points, n, sp, opts->flags, st);
+        const SearchState s = run_search(ctx, P, g, weights, bones, points, n, sp, opts->flags, st);
         DenseOut d{out->x_c, out->jinv, out->resid, out->iters, out->converged, out->keep, out->n_roots};
         FSK_LAUNCH(ctx, st, k_scatter_dense, blocks_for(n * g.nb, 256), 256, 0, n, g.nb, s.sp, s.perm, d);
         if (out->n_roots)
@@ -1170,7 +1244,8 @@ int fsk_search_fwd_mlp(fsk_ctx* ctx, const float* theta, const int32_t* widths, 
     });
 }
 
-int fsk_batch_search(fsk_ctx* ctx, const float* tgrid, const double* tgrid64, const fsk_grid_desc* desc,
+int fsk_batch_search(fsk_ctx* ctx, const float* tgrid, const double* tgrid64, const float* weights,
+                     const fsk_grid_desc* desc,
                      const float* bones, int32_t n_bones_pose, const float* points, int64_t n,
                      const fsk_search_opts* opts, int64_t* offsets, fsk_root* roots, int64_t cap, void* stream) {
     return guard([&] {
@@ -1183,7 +1258,7 @@ int fsk_batch_search(fsk_ctx* ctx, const float* tgrid, const double* tgrid64, co
         if (!offsets || (n > 0 && (!points || !bones))) fail(FSK_EINVAL, "fsk: null buffer");
         cudaStream_t st = (cudaStream_t)stream;
         const GridPlanes P = run_relayout(ctx, tgrid, tgrid64, g, needs_f64(opts->flags), st);
-        const SearchState s = run_search(ctx, P, g, bones, points, n, sp, opts->flags, st);
+        const SearchState s = run_search(ctx, P, g, weights, bones, points, n, sp, opts->flags, st);
         compact(ctx, s, n, g.nb, offsets, roots, cap, st);
     });
 }
@@ -1200,7 +1275,7 @@ int fsk_deform(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* desc, co
         if (!offsets || !bones || (n > 0 && !points)) fail(FSK_EINVAL, "fsk: null buffer");
         cudaStream_t st = (cudaStream_t)stream;
         const GridPlanes P = run_precompute(ctx, weights, g, bones, tgrid, nullptr, true, needs_f64(opts->flags), st);
-        const SearchState s = run_search(ctx, P, g, bones, points, n, sp, opts->flags, st);
+        const SearchState s = run_search(ctx, P, g, weights, bones, points, n, sp, opts->flags, st);
         compact(ctx, s, n, g.nb, offsets, roots, cap, st);
     });
 }
@@ -1294,7 +1369,7 @@ int fsk_deform_host(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* des
         for (int64_t c = 0; c < nchunks; ++c) {
             const int64_t p0 = c * csz, m = std::max<int64_t>(0, std::min(csz, n - p0));
             cuda_check(cudaStreamWaitEvent(st, up[c], 0), "cudaStreamWaitEvent");
-            const SearchState s = run_search(ctx, P, g, dB, dP + 3 * p0, m, sp, opts->flags, st);
+            const SearchState s = run_search(ctx, P, g, dW, dB, dP + 3 * p0, m, sp, opts->flags, st);
             compact(ctx, s, m, nb, dOff + p0 + c, dR + p0 * nb, m * nb, st);
             cuda_check(cudaEventRecord(done[c], st), "cudaEventRecord");
             cuda_check(cudaStreamWaitEvent(ctx->copy, done[c], 0), "cudaStreamWaitEvent");

@@ -511,7 +511,7 @@ std::vector<CorrespondenceSet> batch_search(std::span<const Vec3> queries, const
     h2d(dp.p, p.data(), p.size() * 4);
     const fsk_grid_desc d = desc_of(c.tgrid->dims(), c.tgrid->bbox(), nb);
     const fsk_search_opts so = c_opts(opts);
-    check(fsk_batch_search(ctx(), c.tgrid->device_data(), c.tgrid->device_data64(), &d, db.as<float>(), nb,
+    check(fsk_batch_search(ctx(), c.tgrid->device_data(), c.tgrid->device_data64(), nullptr, &d, db.as<float>(), nb,
                            dp.as<float>(), n, &so, offs.as<std::int64_t>(), dr.as<fsk_root>(), cap, nullptr));
     std::vector<std::int64_t> h_offs(n + 1);
     d2h(h_offs.data(), offs.p, h_offs.size() * 8);

@@ -45,7 +45,10 @@ class SearchOptions:
     div_eps: float = 0.5
     dedup_dist: float = 1e-2
     sort: bool = True  # spatial ordering of queries (performance only)
-    precision: str = "mixed"  # "mixed" (fp32 + fp64 escalation), "fp32" (ablation), "fp64" (parity mode)
+    # "mixed" (fp32 + fp64 escalation), "fp32" (ablation), "fp64" (parity mode), "exact64" (float64
+    # replay of the reference's operation order; needs the weight grid), "mixed-exact" (fp32 pass +
+    # exact-replay escalation; needs the weight grid)
+    precision: str = "mixed"
 
     @staticmethod
     def defaults_for(bbox) -> "SearchOptions":
@@ -67,7 +70,8 @@ class SearchOptions:
 
     def c(self) -> SearchOpts:
         flags = 0 if self.sort else _lib.FSK_SEARCH_NO_SORT
-        flags |= {"mixed": 0, "fp32": _lib.FSK_SEARCH_FP32_ONLY, "fp64": _lib.FSK_SEARCH_FP64}[self.precision]
+        flags |= {"mixed": 0, "fp32": _lib.FSK_SEARCH_FP32_ONLY, "fp64": _lib.FSK_SEARCH_FP64,
+                  "exact64": _lib.FSK_SEARCH_EXACT64, "mixed-exact": _lib.FSK_SEARCH_EXACT_ESC}[self.precision]
         return SearchOpts(int(self.max_iters), flags, float(self.conv_eps), float(self.div_eps),
                           float(self.dedup_dist))
 
@@ -186,10 +190,13 @@ class Deformer:
         return SearchOut(*[o[k].data_ptr() if o.get(k) is not None else None
                            for k in ("x_c", "jinv", "resid", "iters", "converged", "keep", "n_roots")])
 
-    def batch_search(self, tgrid, dims, bbox, bones, points, opts: SearchOptions, out=None, tgrid64=None):
+    def batch_search(self, tgrid, dims, bbox, bones, points, opts: SearchOptions, out=None, tgrid64=None,
+                     weights=None):
         """``batch_search`` voxel variant (correspondence.hpp:77-80) → dense per-(point, init)
-        results: x_c, jinv, resid, iters, converged, keep (dedup), n_roots."""
-        tgrid = _f32(tgrid, "tgrid", self.device)
+        results: x_c, jinv, resid, iters, converged, keep (dedup), n_roots. ``weights`` (the
+        SearchContext's skinning grid, [V, n_b]) is needed only for precision="exact64"."""
+        tgrid = None if tgrid is None and tgrid64 is not None else _f32(tgrid, "tgrid", self.device)
+        weights = None if weights is None else _f32(weights, "weights", self.device)
         bones = _f32(bones, "bones", self.device)
         points = _f32(points, "points", self.device)
         nb = bones.numel() // 12
@@ -198,7 +205,7 @@ class Deformer:
         if out is None:
             out = self.alloc_search_out(n, nb)
         co = self._c_out(out)
-        check(self.L.fsk_search_fwd(self._ctx, _ptr(tgrid), _ptr(tgrid64), ctypes.byref(desc), _ptr(bones), nb,
+        check(self.L.fsk_search_fwd(self._ctx, _ptr(tgrid), _ptr(tgrid64), _ptr(weights), ctypes.byref(desc), _ptr(bones), nb,
                                     _ptr(points), n,
                                     ctypes.byref(opts.c()), ctypes.byref(co), _stream(self.device)))
         return out
@@ -210,14 +217,17 @@ class Deformer:
         return (torch.empty((n + 1,), dtype=torch.int64, device=self.device),
                 torch.empty((max(cap, 1), 16), dtype=torch.float32, device=self.device))
 
-    def batch_search_roots(self, tgrid, dims, bbox, bones, points, opts: SearchOptions, out=None, tgrid64=None):
+    def batch_search_roots(self, tgrid, dims, bbox, bones, points, opts: SearchOptions, out=None, tgrid64=None,
+                           weights=None):
         """``batch_search`` straight to CorrespondenceSets on the device (fsk_batch_search):
         returns (offsets, roots); roots of query p are roots[offsets[p]:offsets[p+1]]."""
         nb, n = bones.numel() // 12, points.shape[0]
         offsets, roots = out if out is not None else self.alloc_roots(n, nb)
         desc = grid_desc(dims, bbox, nb)
-        check(self.L.fsk_batch_search(self._ctx, _ptr(_f32(tgrid, "tgrid", self.device)), _ptr(tgrid64),
-                                      ctypes.byref(desc),
+        weights = None if weights is None else _f32(weights, "weights", self.device)
+        tgrid = None if tgrid is None and tgrid64 is not None else _f32(tgrid, "tgrid", self.device)
+        check(self.L.fsk_batch_search(self._ctx, _ptr(tgrid), _ptr(tgrid64),
+                                      _ptr(weights), ctypes.byref(desc),
                                       _ptr(_f32(bones, "bones", self.device)), nb,
                                       _ptr(_f32(points, "points", self.device)), n, ctypes.byref(opts.c()),
                                       _ptr(offsets), _ptr(roots), roots.shape[0], _stream(self.device)))

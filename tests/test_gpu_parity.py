@@ -226,7 +226,7 @@ def _mismatch(deformer, tg, sc, B, x):
     desc = grid_desc(sc.dims, sc.bbox, sc.n_bones)
     out = deformer.alloc_search_out(x.shape[0], sc.n_bones)
     co = deformer._c_out(out)
-    _lib.check(deformer.L.fsk_search_fwd(deformer._ctx, _ptr(tg), None, ctypes.byref(desc), _ptr(B), sc.n_bones - 1,
+    _lib.check(deformer.L.fsk_search_fwd(deformer._ctx, _ptr(tg), None, None, ctypes.byref(desc), _ptr(B), sc.n_bones - 1,
                                          _ptr(x), x.shape[0], ctypes.byref(opts_of(sc, 10).c()), ctypes.byref(co),
                                          _stream(deformer.device)))
 
