@@ -185,6 +185,17 @@ int fsk_deform_host(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* des
                     const fsk_search_opts* opts, int64_t* offsets, fsk_root* roots, int64_t cap,
                     int64_t* total_out, void* stream);
 
+/* A sequence of frames of one subject (the pose loop of cmd_bench, fskin_cli.cpp:663-678, each
+ * frame with cmd_deform's host copies, :395-429): weights [V][n_b] uploaded once; frame f has
+ * its own bones[f] [n_b][12], points[f] [n_points[f]][3] and outputs offsets[f] [n_points[f]+1],
+ * roots[f] (capacity caps[f]) and totals[f] — exactly what fsk_deform_host returns for that
+ * frame. Double-buffered on the device: frame f+1's upload and search overlap frame f's
+ * download. All pointers HOST memory (pinned for the overlap). Synchronous. */
+int fsk_deform_host_frames(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* desc, int32_t n_frames,
+                           const float* const* bones, int32_t n_bones_pose, const float* const* points,
+                           const int64_t* n_points, const fsk_search_opts* opts, int64_t* const* offsets,
+                           fsk_root* const* roots, const int64_t* caps, int64_t* totals, void* stream);
+
 /* ---- point evaluators (batch forms of trilerp_transform / forward_deform /
  * deform_jacobian, deformer.hpp:59-68): at points x [N][3] (dev) write T(x) [N][12],
  * d(x) [N][3] and the analytic Jacobian dd/dx [N][9] (transform-grid form).

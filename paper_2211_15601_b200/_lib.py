@@ -24,7 +24,7 @@ FSK_SEARCH_EXACT_ESC = 0x10
 EXPORTS = [
     "fsk_ctx_create", "fsk_ctx_destroy", "fsk_last_error", "fsk_ctx_launch_count", "fsk_device_sm_count",
     "fsk_search_opts_defaults", "fsk_precompute_tgrid", "fsk_search_fwd", "fsk_compact_roots",
-    "fsk_deform_host", "fsk_eval_points", "fsk_init_states", "fsk_search_bwd", "fsk_grad_weights",
+    "fsk_deform_host", "fsk_deform_host_frames", "fsk_eval_points", "fsk_init_states", "fsk_search_bwd", "fsk_grad_weights",
     "fsk_ctx_set_profiling", "fsk_ctx_prof_read", "fsk_measure_fp32_peak", "fsk_batch_search", "fsk_deform",
     "fsk_search_bwd_roots", "fsk_ctx_search_stats", "fsk_measure_fp64_peak", "fsk_measure_l1_gather_peak",
     "fsk_distill", "fsk_posed_occupancy", "fsk_distill_bwd",
@@ -91,6 +91,7 @@ def load():
     L.fsk_search_fwd.argtypes = [_vp, _vp, _vp, _vp, G, _vp, _i32, _vp, _i64, O, S, _vp]
     L.fsk_compact_roots.argtypes = [_vp, S, _i64, _i32, _vp, _vp, _i64, ctypes.POINTER(_i64), _vp]
     L.fsk_deform_host.argtypes = [_vp, _vp, G, _vp, _i32, _vp, _i64, O, _vp, _vp, _i64, ctypes.POINTER(_i64), _vp]
+    L.fsk_deform_host_frames.argtypes = [_vp, _vp, G, _i32, _vp, _i32, _vp, _vp, O, _vp, _vp, _vp, _vp, _vp]
     L.fsk_eval_points.argtypes = [_vp, _vp, G, _vp, _i64, _vp, _vp, _vp, _vp]
     L.fsk_init_states.argtypes = [_vp, _vp, G, _vp, _i32, _vp, _i64, _vp, _vp, _vp]
     L.fsk_search_bwd.argtypes = [_vp, G, _vp, _vp, _i32, _vp, _vp, _i64, _vp, ctypes.c_int, _vp]

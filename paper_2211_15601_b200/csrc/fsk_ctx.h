@@ -48,7 +48,7 @@ enum Slot {
     kHist, kBbox, kKeys, kPerm, kXs, kScanPart, kBwdAcc, kBwdMax, kPlanes, kPlanes64, kEscQ, kEscN,
     kBwdStart, kBwdCell, kBwdRec, kPeakTable,
     kOXr, kOJa, kOJb, kOJc, kOMeta, kOKeep, kNRoots, kOffs, kRootsTmp,
-    kHW, kHB, kHP, kHT, kHOffs, kHRoots,
+    kHW, kHB, kHP, kHT, kHOffs, kHRoots, kFB, kFP, kFOffs, kFRoots,
     kMlpPack, kMlpWidths, kMlpOcc, kMlpAct, kMlpD0, kMlpD1, kMlpOnes,
     kMvPos, kMvPosNext, kMvW, kMvX, kMvG, kMvJ, kMvDx, kMvK, kMvAct, kMvActNext, kMvCnt,
     kSlotCount

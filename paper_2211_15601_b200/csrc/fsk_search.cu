@@ -1405,6 +1405,116 @@ int fsk_deform_host(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* des
     });
 }
 
+// A sequence of frames of one subject (cmd_bench's pose loop, fskin_cli.cpp:663-678, with the
+// host copies of cmd_deform, :395-429): the weights are uploaded once, then every frame is
+// fsk_deform_host's H2D → K1 + search + compaction → D2H, double-buffered over two device
+// slots so frame f+1's upload and search run while frame f's CorrespondenceSets download.
+// Per frame the results are identical to a fsk_deform_host call.
+int fsk_deform_host_frames(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* desc, int32_t n_frames,
+                           const float* const* bones, int32_t n_bones_pose, const float* const* points,
+                           const int64_t* n_points, const fsk_search_opts* opts, int64_t* const* offsets,
+                           fsk_root* const* roots, const int64_t* caps, int64_t* totals, void* stream) {
+    return guard([&] {
+        set_device(ctx);
+        const GridP g = make_grid(desc);
+        check_search_args(g, n_bones_pose, weights, "precompute_transform_grid: bone count mismatch");
+        const SearchP sp = make_search(opts);
+        if (n_frames < 0) fail(FSK_EINVAL, "fsk: negative frame count");
+        if (n_frames == 0) return;
+        if (!bones || !points || !n_points || !offsets || !roots || !caps || !totals)
+            fail(FSK_EINVAL, "fsk: null buffer");
+        int64_t nmax = 1;
+        for (int f = 0; f < n_frames; ++f) {
+            if (n_points[f] < 0) fail(FSK_EINVAL, "fsk: negative point count");
+            if (!bones[f] || !offsets[f] || (n_points[f] > 0 && !points[f])) fail(FSK_EINVAL, "fsk: null buffer");
+            nmax = std::max(nmax, n_points[f]);
+        }
+        cudaStream_t st = (cudaStream_t)stream;
+        const int64_t V = vertex_count(g);
+        const int nb = g.nb;
+        float* dW = (float*)scratch(ctx, kHW, V * nb * sizeof(float));
+        float* dB = (float*)scratch(ctx, kFB, 2 * nb * 12 * sizeof(float));
+        float* dP = (float*)scratch(ctx, kFP, 2 * nmax * 3 * sizeof(float));
+        int64_t* dOff = (int64_t*)scratch(ctx, kFOffs, 2 * (nmax + 1) * sizeof(int64_t));
+        fsk_root* dR = (fsk_root*)scratch(ctx, kFRoots, 2 * nmax * nb * sizeof(fsk_root));
+        if (!ctx->copy) cuda_check(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking), "cudaStreamCreate");
+        if (!ctx->upload)
+            cuda_check(cudaStreamCreateWithFlags(&ctx->upload, cudaStreamNonBlocking), "cudaStreamCreate");
+        // per frame: points/bones uploaded, search done, offsets downloaded, roots downloaded
+        std::vector<cudaEvent_t> ev(4 * (size_t)n_frames + 1, nullptr);
+        struct Cleanup {  // on every exit: drain the three streams, then free the events
+            fsk_ctx* ctx;
+            cudaStream_t st;
+            std::vector<cudaEvent_t>* ev;
+            ~Cleanup() {
+                cudaStreamSynchronize(ctx->upload);
+                cudaStreamSynchronize(st);
+                cudaStreamSynchronize(ctx->copy);
+                for (auto e : *ev)
+                    if (e) cudaEventDestroy(e);
+            }
+        } cleanup{ctx, st, &ev};
+        for (auto& e : ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+        cudaEvent_t* up = ev.data();
+        cudaEvent_t* done = up + n_frames;
+        cudaEvent_t* offs_ready = done + n_frames;
+        cudaEvent_t* fetched = offs_ready + n_frames;
+        cudaEvent_t start = ev.back();
+        cuda_check(cudaEventRecord(start, st), "cudaEventRecord");  // order after prior use of the buffers
+        cuda_check(cudaStreamWaitEvent(ctx->upload, start, 0), "cudaStreamWaitEvent");
+        cuda_check(cudaStreamWaitEvent(ctx->copy, start, 0), "cudaStreamWaitEvent");
+        cuda_check(cudaMemcpyAsync(dW, weights, V * nb * sizeof(float), cudaMemcpyHostToDevice, st), "H2D weights");
+        auto slot_b = [&](int f) { return dB + (f & 1) * nb * 12; };
+        auto slot_p = [&](int f) { return dP + (f & 1) * nmax * 3; };
+        auto slot_o = [&](int f) { return dOff + (f & 1) * (nmax + 1); };
+        auto slot_r = [&](int f) { return dR + (f & 1) * nmax * nb; };
+        auto enqueue_frame = [&](int f) {
+            const int64_t n = n_points[f];
+            if (f >= 2) cuda_check(cudaStreamWaitEvent(ctx->upload, done[f - 2], 0), "cudaStreamWaitEvent");
+            cuda_check(cudaMemcpyAsync(slot_b(f), bones[f], nb * 12 * sizeof(float), cudaMemcpyHostToDevice,
+                                       ctx->upload),
+                       "H2D bones");
+            if (n > 0)
+                cuda_check(cudaMemcpyAsync(slot_p(f), points[f], n * 3 * sizeof(float), cudaMemcpyHostToDevice,
+                                           ctx->upload),
+                           "H2D points");
+            cuda_check(cudaEventRecord(up[f], ctx->upload), "cudaEventRecord");
+            cuda_check(cudaStreamWaitEvent(st, up[f], 0), "cudaStreamWaitEvent");
+            if (f >= 2) cuda_check(cudaStreamWaitEvent(st, fetched[f - 2], 0), "cudaStreamWaitEvent");
+            const GridPlanes P = run_precompute(ctx, dW, g, slot_b(f), nullptr, nullptr, true, needs_f64(opts->flags), st);
+            const SearchState s = run_search(ctx, P, g, dW, slot_b(f), slot_p(f), n, sp, opts->flags, st);
+            compact(ctx, s, n, nb, slot_o(f), slot_r(f), n * nb, st);
+            cuda_check(cudaEventRecord(done[f], st), "cudaEventRecord");
+        };
+        auto enqueue_offsets = [&](int f) {
+            cuda_check(cudaStreamWaitEvent(ctx->copy, done[f], 0), "cudaStreamWaitEvent");
+            cuda_check(cudaMemcpyAsync(offsets[f], slot_o(f), (n_points[f] + 1) * sizeof(int64_t),
+                                       cudaMemcpyDeviceToHost, ctx->copy),
+                       "D2H offsets");
+            cuda_check(cudaEventRecord(offs_ready[f], ctx->copy), "cudaEventRecord");
+        };
+        enqueue_frame(0);
+        enqueue_offsets(0);
+        for (int f = 0; f < n_frames; ++f) {
+            if (f + 1 < n_frames) enqueue_frame(f + 1);  // the device runs ahead while we wait
+            cuda_check(cudaEventSynchronize(offs_ready[f]), "cudaEventSynchronize");
+            const int64_t cnt = offsets[f][n_points[f]];
+            totals[f] = cnt;
+            if (cnt > caps[f]) fail(FSK_EINVAL, "fsk: root buffer too small");
+            if (cnt > 0) {
+                if (!roots[f]) fail(FSK_EINVAL, "fsk: null buffer");
+                cuda_check(cudaMemcpyAsync(roots[f], slot_r(f), cnt * sizeof(fsk_root), cudaMemcpyDeviceToHost,
+                                           ctx->copy),
+                           "D2H roots");
+            }
+            cuda_check(cudaEventRecord(fetched[f], ctx->copy), "cudaEventRecord");
+            if (f + 1 < n_frames) enqueue_offsets(f + 1);
+        }
+        cuda_check(cudaStreamSynchronize(ctx->copy), "cudaStreamSynchronize");
+        cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    });
+}
+
 int fsk_init_states(fsk_ctx* ctx, const float* tgrid, const fsk_grid_desc* desc, const float* bones,
                     int32_t n_bones_pose, const float* points, int64_t n, float* x0, float* jinv0, void* stream) {
     return guard([&] {

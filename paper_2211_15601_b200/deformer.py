@@ -393,6 +393,25 @@ class Deformer:
                                      roots.shape[0], ctypes.byref(total), _stream(self.device)))
         return total.value
 
+    def deform_host_frames(self, weights, dims, bbox, bones, points, opts: SearchOptions, offsets, roots):
+        """``fsk_deform_host_frames``: one subject, F frames (lists of host tensors: bones [n_b,12],
+        points [N_f,3], offsets [N_f+1] int64, roots [cap_f,16] float32), double-buffered so frame
+        f+1's upload and search overlap frame f's download. Returns the kept-root count per frame."""
+        F = len(points)
+        if not (len(bones) == len(offsets) == len(roots) == F):
+            raise FskInvalidArgument("fsk: one bones/points/offsets/roots entry per frame")
+        nb = bones[0].numel() // 12 if F else 1
+        desc = grid_desc(dims, bbox, nb)
+        vp = ctypes.c_void_p
+        arr = lambda ts: (vp * max(F, 1))(*[t.data_ptr() for t in ts])  # noqa: E731
+        n = (ctypes.c_int64 * max(F, 1))(*[p.shape[0] for p in points])
+        caps = (ctypes.c_int64 * max(F, 1))(*[r.shape[0] for r in roots])
+        totals = (ctypes.c_int64 * max(F, 1))()
+        check(self.L.fsk_deform_host_frames(self._ctx, _ptr(weights), ctypes.byref(desc), F, arr(bones), nb,
+                                            arr(points), n, ctypes.byref(opts.c()), arr(offsets), arr(roots), caps,
+                                            totals, _stream(self.device)))
+        return [int(totals[i]) for i in range(F)]
+
 
 class MultiDeformer:
     """Single-process multi-GPU C-ABI (``fsk_multi_*``): one context, stream and host thread

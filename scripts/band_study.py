@@ -24,7 +24,7 @@ for seed in seeds:
         pts = ["uniform", "training"][seed % 2]
         sc = S.make_scene(dims, n, seed=seed, points=pts)
         o = sc.search_options(50)
-        _, g = run_gpu(D, sc, 50)
+        _, g = run_gpu(D, sc, 50, precision=os.environ.get("BAND_PRECISION", "mixed"))
         r = oracle.batch_search(sc.weights, sc.dims, sc.bbox, sc.bones, sc.points, workers=os.cpu_count(), **o)
         both = (g["converged"] == 1) & (r["converged"] == 1)
         rg = g["resid"] / o["conv_eps"]

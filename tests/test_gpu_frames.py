@@ -1,0 +1,59 @@
+"""fsk_deform_host_frames (one subject, a sequence of poses, double-buffered host copies):
+every frame's CorrespondenceSets equal a separate fsk_deform_host call bit for bit, whatever
+the frame sizes (including empty frames), and a too-small root buffer fails loudly."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2211_15601_b200 import synthetic as S
+from paper_2211_15601_b200.deformer import FskInvalidArgument, SearchOptions
+
+pytestmark = pytest.mark.gpu
+
+
+def _opts(sc):
+    return SearchOptions(50, **{k: v for k, v in sc.search_options(50).items() if k != "max_iters"})
+
+
+def _frames(sizes, dims=(32, 32, 32)):
+    """One subject (weight grid of seed 0) in len(sizes) poses with their own point sets."""
+    base = S.make_scene(dims, 10, seed=0)
+    out = []
+    for i, n in enumerate(sizes):
+        sc = S.make_scene(dims, max(n, 1), seed=100 + i)
+        out.append((torch.from_numpy(sc.bones).pin_memory(), torch.from_numpy(sc.points[:n].copy()).pin_memory()))
+    return base, out
+
+
+@pytest.mark.parametrize("sizes", [[5000], [4000, 7000, 0, 3000, 6000], [20000, 20000, 20000, 20000]])
+def test_frames_equal_single_frame_calls(deformer, sizes):
+    base, frames = _frames(sizes)
+    hw = torch.from_numpy(base.weights).pin_memory()
+    nb = base.n_bones
+    o = _opts(base)
+    offs = [torch.empty(p.shape[0] + 1, dtype=torch.int64).pin_memory() for _, p in frames]
+    roots = [torch.zeros((max(p.shape[0] * nb, 1), 16), dtype=torch.float32).pin_memory() for _, p in frames]
+    totals = deformer.deform_host_frames(hw, base.dims, base.bbox, [b for b, _ in frames], [p for _, p in frames], o,
+                                         offs, roots)
+    for f, (b, p) in enumerate(frames):
+        o1 = torch.empty(p.shape[0] + 1, dtype=torch.int64).pin_memory()
+        r1 = torch.zeros((max(p.shape[0] * nb, 1), 16), dtype=torch.float32).pin_memory()
+        t1 = deformer.deform_host(hw, base.dims, base.bbox, b, p, o, o1, r1)
+        assert totals[f] == t1
+        np.testing.assert_array_equal(offs[f].numpy(), o1.numpy())
+        np.testing.assert_array_equal(roots[f][:t1].numpy().view(np.uint32), r1[:t1].numpy().view(np.uint32))
+
+
+def test_frames_root_buffer_too_small(deformer):
+    base, frames = _frames([3000, 3000])
+    hw = torch.from_numpy(base.weights).pin_memory()
+    offs = [torch.empty(p.shape[0] + 1, dtype=torch.int64).pin_memory() for _, p in frames]
+    roots = [torch.zeros((p.shape[0] * base.n_bones, 16)).pin_memory() for _, p in frames]
+    roots[1] = torch.zeros((10, 16)).pin_memory()
+    with pytest.raises(FskInvalidArgument, match="root buffer too small"):
+        deformer.deform_host_frames(hw, base.dims, base.bbox, [b for b, _ in frames], [p for _, p in frames],
+                                    _opts(base), offs, roots)
+    # the context stays usable
+    totals = deformer.deform_host_frames(hw, base.dims, base.bbox, [frames[0][0]], [frames[0][1]], _opts(base),
+                                         offs[:1], roots[:1])
+    assert totals[0] > 0

@@ -35,7 +35,7 @@ def run_gpu(deformer, sc, max_iters, sort=True, precision="mixed"):
     o = opts_of(sc, max_iters)
     o.sort = sort
     o.precision = precision
-    out = deformer.batch_search(tg, sc.dims, sc.bbox, B, x, o, tgrid64=tg64)
+    out = deformer.batch_search(tg, sc.dims, sc.bbox, B, x, o, tgrid64=tg64, weights=w)
     torch.cuda.synchronize()
     return tg, {k: (v.cpu().numpy() if v is not None else None) for k, v in out.items()}
 
