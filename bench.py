@@ -60,7 +60,7 @@ def parse():
     ap.add_argument("--poses", type=int, default=1, help="poses per step (C4: 16 poses x 1M points, 64^3 grid)")
     ap.add_argument("--backward", action="store_true", help="C3: add the implicit-diff backward to each frame")
     ap.add_argument("--deterministic", action="store_true", help="backward with int64 fixed-point accumulation")
-    ap.add_argument("--precision", default="mixed", choices=["mixed", "mixed-exact", "fp32", "fp64", "exact64"])
+    ap.add_argument("--precision", default="mixed", choices=["mixed", "mixed-fast", "fp32", "fp64", "exact64"])
     ap.add_argument("--no-graph", dest="graph", action="store_false", help="launch eagerly instead of a CUDA graph")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-baseline sample duration")
     return ap.parse_args()
@@ -83,7 +83,7 @@ def workload_name(args):
         name = "C5 (per-GPU shard of the 64M-point ray-sample workload)"
     s = (f"{name}: {args.poses} pose(s) x {args.points // 1000}k posed points x 24 bone inits per GPU, "
          f"{args.grid.replace(',', 'x')} grid, max_iters {args.max_iters}; step = per pose: precompute + sort + "
-         f"search (fp32 pass + fp64 escalation) + dedup + compaction to CorrespondenceSets")
+         f"search (fp32 pass + fp64 escalation replaying the reference exactly) + dedup + compaction to CorrespondenceSets")
     if args.backward:
         s += " + implicit-diff backward (dL/dT scatter + dL/dw)"
     return s

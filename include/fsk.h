@@ -70,9 +70,12 @@ typedef struct fsk_search_opts {
                                      bit-identical to a float64 build of the reference given the same
                                      transform grid; needs the weight grid (fsk_search_fwd /
                                      fsk_batch_search `weights`, always present in fsk_deform*) */
-#define FSK_SEARCH_EXACT_ESC 0x10 /* mixed mode whose float64 escalation pass runs the exact replay:
-                                     escalated solves equal the reference bit for bit, the rest are
-                                     the float32 pass's; needs the weight grid like EXACT64 */
+#define FSK_SEARCH_FAST_ESC 0x10  /* mixed mode, ablation: escalate to the fused float64 solver
+                                     (transform-grid J~0) even when the weight grid is given. By
+                                     default the escalation pass replays the reference exactly
+                                     whenever the weight grid is available (always in fsk_deform*;
+                                     fsk_search_fwd / fsk_batch_search when `weights` != NULL), so
+                                     escalated solves equal the reference bit for bit */
 
 /* Dense per-(point, init) search result (the GPU form of Root / CorrespondenceSet,
  * correspondence.hpp:29-42). All pointers dev, [N][n_b] point-major; any may be NULL

@@ -18,7 +18,7 @@ FSK_SEARCH_NO_SORT = 0x1
 FSK_SEARCH_FP32_ONLY = 0x2
 FSK_SEARCH_FP64 = 0x4
 FSK_SEARCH_EXACT64 = 0x8
-FSK_SEARCH_EXACT_ESC = 0x10
+FSK_SEARCH_FAST_ESC = 0x10
 
 # Every symbol include/fsk.h declares (checked by tests/test_lib_exports.py).
 EXPORTS = [

@@ -101,8 +101,8 @@ SearchP make_search(const fsk_search_opts* o) {
     s.max_iters = o->max_iters;
     if ((o->flags & FSK_SEARCH_FP32_ONLY) && (o->flags & FSK_SEARCH_EXACT64))
         fail(FSK_EINVAL, "fsk: FSK_SEARCH_FP32_ONLY and FSK_SEARCH_EXACT64 are exclusive");
-    if ((o->flags & FSK_SEARCH_EXACT_ESC) && (o->flags & (FSK_SEARCH_FP32_ONLY | FSK_SEARCH_FP64 | FSK_SEARCH_EXACT64)))
-        fail(FSK_EINVAL, "fsk: FSK_SEARCH_EXACT_ESC applies to the mixed mode only");
+    if ((o->flags & FSK_SEARCH_FAST_ESC) && (o->flags & (FSK_SEARCH_FP32_ONLY | FSK_SEARCH_FP64 | FSK_SEARCH_EXACT64)))
+        fail(FSK_EINVAL, "fsk: FSK_SEARCH_FAST_ESC applies to the mixed mode only");
     s.conv_eps = o->conv_eps;
     s.div_eps = o->div_eps;
     s.conv2 = o->conv_eps * o->conv_eps;

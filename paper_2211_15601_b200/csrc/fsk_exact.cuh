@@ -28,7 +28,11 @@ namespace exact {
 __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+#ifdef FSK_EXACT_TIMING_NODIV  // timing probe only (not bit-exact): division as a*(1/b)
+__device__ __forceinline__ double div(double a, double b) { return a * __drcp_rn(b); }
+#else
 __device__ __forceinline__ double div(double a, double b) { return __ddiv_rn(a, b); }
+#endif
 // a0*b0 + a1*b1 + a2*b2, left to right
 __device__ __forceinline__ double dot3(double a0, double a1, double a2, double b0, double b1, double b2) {
     return add(add(mul(a0, b0), mul(a1, b1)), mul(a2, b2));
@@ -123,9 +127,25 @@ __device__ __forceinline__ void inverse_apply(const float* B, double xp0, double
 
 // deform_jacobian(x, grid, bones) via jacobian_from_weights (deformer.cpp:117-136): weights from
 // locate_cell (trilerp_weights_into), gradient from locate_cell_lower with ±1/h stencils
-// (weight_spatial_gradient), J = Σ_i w_i R_i then + Σ_i (B_i x)(∇w_i)ᵀ, bone order.
-__device__ __forceinline__ void jacobian(const GridP& g, const float* __restrict__ W, const float* __restrict__ bones,
-                                         double x0, double x1, double x2, double J[9]) {
+// (weight_spatial_gradient), J = Σ_i w_i R_i then + Σ_i (B_i x)(∇w_i)ᵀ, bone order. The
+// per-corner factors are bone-independent and computed once (same operations, same bits);
+// the weights of 4 consecutive bones come in one 16-byte load when n_b % 4 == 0.
+template <int kVec>
+__device__ __forceinline__ void corner_weights(const float* __restrict__ W, int64_t v, int nb, int b, float out[kVec]) {
+    if constexpr (kVec == 4) {
+        const float4 q = __ldg(reinterpret_cast<const float4*>(W + v * nb + b));
+        out[0] = q.x;
+        out[1] = q.y;
+        out[2] = q.z;
+        out[3] = q.w;
+    } else {
+        out[0] = __ldg(W + v * nb + b);
+    }
+}
+
+template <int kVec>
+__device__ __forceinline__ void jacobian_vec(const GridP& g, const float* __restrict__ W, const float* __restrict__ bones,
+                                             double x0, double x1, double x2, double J[9]) {
     const int nb = g.nb;
     const XCell c = locate(g, x0, x1, x2, false), cl = locate(g, x0, x1, x2, true);
     const int n[3] = {g.nx, g.ny, g.nz};
@@ -136,56 +156,94 @@ __device__ __forceinline__ void jacobian(const GridP& g, const float* __restrict
         dmin[a] = div(-1.0, h[a]);
         dplus[a] = div(1.0, h[a]);
     }
+    int64_t vc[8], vl[8];
+    double w8[8];
 #pragma unroll
-    for (int e = 0; e < 9; ++e) J[e] = 0.0;
-    for (int b = 0; b < nb; ++b) {  // Σ_i w_i R_i
-        double wb = 0.0;
+    for (int dk = 0; dk < 2; ++dk) {
+        const double wz = dk ? c.tz : sub(1.0, c.tz);
 #pragma unroll
-        for (int dk = 0; dk < 2; ++dk) {
-            const double wz = dk ? c.tz : sub(1.0, c.tz);
+        for (int dj = 0; dj < 2; ++dj) {
+            const double wyz = mul(wz, dj ? c.ty : sub(1.0, c.ty));
 #pragma unroll
-            for (int dj = 0; dj < 2; ++dj) {
-                const double wyz = mul(wz, dj ? c.ty : sub(1.0, c.ty));
-#pragma unroll
-                for (int di = 0; di < 2; ++di) {
-                    const double w = mul(wyz, di ? c.tx : sub(1.0, c.tx));
-                    wb = add(wb, mul(w, (double)__ldg(W + (int64_t)vidx(g, c.i + di, c.j + dj, c.k + dk) * nb + b)));
-                }
+            for (int di = 0; di < 2; ++di) {
+                const int k8 = 4 * dk + 2 * dj + di;
+                w8[k8] = mul(wyz, di ? c.tx : sub(1.0, c.tx));
+                vc[k8] = vidx(g, c.i + di, c.j + dj, c.k + dk);
+                vl[k8] = vidx(g, cl.i + di, cl.j + dj, cl.k + dk);
             }
         }
-        const float* B = bones + 12 * b;
+    }
 #pragma unroll
-        for (int r = 0; r < 3; ++r)
+    for (int e = 0; e < 9; ++e) J[e] = 0.0;
+    for (int b0 = 0; b0 < nb; b0 += kVec) {  // Σ_i w_i R_i
+        double wb[kVec];
 #pragma unroll
-            for (int cc = 0; cc < 3; ++cc) J[3 * r + cc] = add(J[3 * r + cc], mul(wb, (double)B[4 * r + cc]));
+        for (int u = 0; u < kVec; ++u) wb[u] = 0.0;
+#pragma unroll
+        for (int k8 = 0; k8 < 8; ++k8) {
+            float q[kVec];
+            corner_weights<kVec>(W, vc[k8], nb, b0, q);
+#pragma unroll
+            for (int u = 0; u < kVec; ++u) wb[u] = add(wb[u], mul(w8[k8], (double)q[u]));
+        }
+#pragma unroll
+        for (int u = 0; u < kVec; ++u) {
+            const float* B = bones + 12 * (b0 + u);
+#pragma unroll
+            for (int r = 0; r < 3; ++r)
+#pragma unroll
+                for (int cc = 0; cc < 3; ++cc) J[3 * r + cc] = add(J[3 * r + cc], mul(wb[u], (double)B[4 * r + cc]));
+        }
     }
     const double fx[2] = {sub(1.0, cl.tx), cl.tx}, fy[2] = {sub(1.0, cl.ty), cl.ty}, fz[2] = {sub(1.0, cl.tz), cl.tz};
-    for (int b = 0; b < nb; ++b) {  // + Σ_i (B_i x) ∇w_iᵀ
-        double gg[3] = {0.0, 0.0, 0.0};
+    double gx8[8], gy8[8], gz8[8];
 #pragma unroll
-        for (int dk = 0; dk < 2; ++dk)
+    for (int dk = 0; dk < 2; ++dk)
 #pragma unroll
-            for (int dj = 0; dj < 2; ++dj)
+        for (int dj = 0; dj < 2; ++dj)
 #pragma unroll
-                for (int di = 0; di < 2; ++di) {
-                    const double v = (double)__ldg(W + (int64_t)vidx(g, cl.i + di, cl.j + dj, cl.k + dk) * nb + b);
-                    const double gx = mul(mul(di ? dplus[0] : dmin[0], fy[dj]), fz[dk]);
-                    const double gy = mul(mul(fx[di], dj ? dplus[1] : dmin[1]), fz[dk]);
-                    const double gz = mul(mul(fx[di], fy[dj]), dk ? dplus[2] : dmin[2]);
-                    gg[0] = add(gg[0], mul(gx, v));
-                    gg[1] = add(gg[1], mul(gy, v));
-                    gg[2] = add(gg[2], mul(gz, v));
-                }
-        const float* B = bones + 12 * b;
-        double bx[3];
+            for (int di = 0; di < 2; ++di) {
+                const int k8 = 4 * dk + 2 * dj + di;
+                gx8[k8] = mul(mul(di ? dplus[0] : dmin[0], fy[dj]), fz[dk]);
+                gy8[k8] = mul(mul(fx[di], dj ? dplus[1] : dmin[1]), fz[dk]);
+                gz8[k8] = mul(mul(fx[di], fy[dj]), dk ? dplus[2] : dmin[2]);
+            }
+    for (int b0 = 0; b0 < nb; b0 += kVec) {  // + Σ_i (B_i x) ∇w_iᵀ
+        double gg[kVec][3];
 #pragma unroll
-        for (int r = 0; r < 3; ++r)
-            bx[r] = add(dot3((double)B[4 * r], (double)B[4 * r + 1], (double)B[4 * r + 2], x0, x1, x2), (double)B[4 * r + 3]);
+        for (int u = 0; u < kVec; ++u) gg[u][0] = gg[u][1] = gg[u][2] = 0.0;
 #pragma unroll
-        for (int r = 0; r < 3; ++r)
+        for (int k8 = 0; k8 < 8; ++k8) {
+            float q[kVec];
+            corner_weights<kVec>(W, vl[k8], nb, b0, q);
 #pragma unroll
-            for (int cc = 0; cc < 3; ++cc) J[3 * r + cc] = add(J[3 * r + cc], mul(bx[r], gg[cc]));
+            for (int u = 0; u < kVec; ++u) {
+                const double v = (double)q[u];
+                gg[u][0] = add(gg[u][0], mul(gx8[k8], v));
+                gg[u][1] = add(gg[u][1], mul(gy8[k8], v));
+                gg[u][2] = add(gg[u][2], mul(gz8[k8], v));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kVec; ++u) {
+            const float* B = bones + 12 * (b0 + u);
+            double bx[3];
+#pragma unroll
+            for (int r = 0; r < 3; ++r)
+                bx[r] = add(dot3((double)B[4 * r], (double)B[4 * r + 1], (double)B[4 * r + 2], x0, x1, x2),
+                            (double)B[4 * r + 3]);
+#pragma unroll
+            for (int r = 0; r < 3; ++r)
+#pragma unroll
+                for (int cc = 0; cc < 3; ++cc) J[3 * r + cc] = add(J[3 * r + cc], mul(bx[r], gg[u][cc]));
+        }
     }
+}
+
+__device__ __forceinline__ void jacobian(const GridP& g, const float* __restrict__ W, const float* __restrict__ bones,
+                                         double x0, double x1, double x2, double J[9]) {
+    if (g.nb % 4 == 0) jacobian_vec<4>(g, W, bones, x0, x1, x2, J);
+    else jacobian_vec<1>(g, W, bones, x0, x1, x2, J);
 }
 
 // initial_inverse_jacobian (correspondence.cpp:43-54): Eigen's det (expansion along row 0)

@@ -364,12 +364,15 @@ __global__ void __launch_bounds__(kSearchBlock, FSK_SEARCH_MINB)
 #ifndef FSK_ESC_MINB
 #define FSK_ESC_MINB 2  // measured: 254 regs / 8 warps per SM beats 168 regs / 12 warps (0.263 vs 0.277 ms)
 #endif
+#ifndef FSK_ESC_EXACT_MINB
+#define FSK_ESC_EXACT_MINB 3
+#endif
 constexpr int kEscBlock = 128;
 #ifndef FSK_REFILL_IDLE
 #define FSK_REFILL_IDLE 16  // measured 16 (0.253 ms) vs 12 (0.260) vs 8 (0.265) vs 20 (0.255)
 #endif
 template <bool kExact>  // kExact: the solves replay the reference's operation order (fsk_exact.cuh)
-__global__ void __launch_bounds__(kEscBlock, FSK_ESC_MINB)
+__global__ void __launch_bounds__(kEscBlock, kExact ? FSK_ESC_EXACT_MINB : FSK_ESC_MINB)
     k_search_escalated(Planes<double> P, GridP g, const float* __restrict__ W, const float* __restrict__ bones,
                        int64_t n, SearchP o,
                        SearchPlanes out, const int4* __restrict__ esc_q, int64_t esc_cap,
@@ -833,8 +836,8 @@ struct SearchState {
 // sort + K2 (+ K2b escalation) + dedup into the ctx's search planes.
 SearchState run_search(fsk_ctx* ctx, const GridPlanes& P, const GridP& g, const float* weights, const float* bones,
                        const float* pts, int64_t n, const SearchP& sp, int flags, cudaStream_t st) {
-    if ((flags & (FSK_SEARCH_EXACT64 | FSK_SEARCH_EXACT_ESC)) && !weights)
-        fail(FSK_EINVAL, "fsk: FSK_SEARCH_EXACT64 / _EXACT_ESC need the weight grid (J~0 from the skinning weights)");
+    if ((flags & FSK_SEARCH_EXACT64) && !weights)
+        fail(FSK_EINVAL, "fsk: FSK_SEARCH_EXACT64 needs the weight grid (J~0 from the skinning weights)");
     if (n >= (int64_t(1) << 31) / std::max(1, g.nb)) fail(FSK_EINVAL, "fsk: too many points for one call (split the batch)");
     const int64_t S = std::max<int64_t>(1, n * g.nb);
     SearchState s;
@@ -888,7 +891,8 @@ SearchState run_search(fsk_ctx* ctx, const GridPlanes& P, const GridP& g, const 
         FSK_LAUNCH(ctx, st, k_search_fast, (unsigned)nblocks, kSearchBlock, 0, P.p32, g, bones, xs, n, bpb, spf, s.sp,
                    esc_q, S, esc_n, ctx->stats);
         int per_sm = 0;  // persistent kernel: exactly the resident capacity
-        const bool exact_esc = flags & FSK_SEARCH_EXACT_ESC;
+        // exact replay of the reference whenever the weight grid is at hand
+        const bool exact_esc = weights && !(flags & FSK_SEARCH_FAST_ESC);
         cuda_check(exact_esc ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search_escalated<true>,
                                                                              kEscBlock, 0)
                              : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search_escalated<false>,

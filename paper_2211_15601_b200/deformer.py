@@ -45,9 +45,9 @@ class SearchOptions:
     div_eps: float = 0.5
     dedup_dist: float = 1e-2
     sort: bool = True  # spatial ordering of queries (performance only)
-    # "mixed" (fp32 + fp64 escalation), "fp32" (ablation), "fp64" (parity mode), "exact64" (float64
-    # replay of the reference's operation order; needs the weight grid), "mixed-exact" (fp32 pass +
-    # exact-replay escalation; needs the weight grid)
+    # "mixed" (fp32 pass + fp64 escalation, the escalation an exact replay of the reference when the
+    # weight grid is given), "mixed-fast" (ablation: fused fp64 escalation), "fp32" (ablation),
+    # "fp64" (every solve in fp64), "exact64" (every solve an exact fp64 replay; needs the weights)
     precision: str = "mixed"
 
     @staticmethod
@@ -71,7 +71,7 @@ class SearchOptions:
     def c(self) -> SearchOpts:
         flags = 0 if self.sort else _lib.FSK_SEARCH_NO_SORT
         flags |= {"mixed": 0, "fp32": _lib.FSK_SEARCH_FP32_ONLY, "fp64": _lib.FSK_SEARCH_FP64,
-                  "exact64": _lib.FSK_SEARCH_EXACT64, "mixed-exact": _lib.FSK_SEARCH_EXACT_ESC}[self.precision]
+                  "exact64": _lib.FSK_SEARCH_EXACT64, "mixed-fast": _lib.FSK_SEARCH_FAST_ESC}[self.precision]
         return SearchOpts(int(self.max_iters), flags, float(self.conv_eps), float(self.div_eps),
                           float(self.dedup_dist))
 

@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Cost of the search precision modes on one frame (fsk_deform, device-resident inputs).
 
-mixed (default: fp32 pass + fp64 escalation), mixed-exact (escalation by exact replay), fp32 (ablation), fp64 (every solve in float64,
+mixed (default: fp32 pass + exact-replay fp64 escalation), mixed-fast (fused fp64 escalation), fp32 (ablation), fp64 (every solve in float64,
 transform-grid J0, fused arithmetic) and exact64 (every solve in float64 replaying the
 reference's operation order, weight-grid J0 — bit-identical to the oracle). Prints one JSON
 line per mode: solves/s, ms per frame, and (exact64 against fp64/mixed) the converged-mask
@@ -39,7 +39,7 @@ def main():
     buf = D.alloc_roots(n, nb)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     dense = {}
-    for mode in ("mixed", "mixed-exact", "fp32", "fp64", "exact64"):
+    for mode in ("mixed", "mixed-fast", "fp32", "fp64", "exact64"):
         o = SearchOptions(a.max_iters, **{k: v for k, v in sc.search_options(a.max_iters).items() if k != "max_iters"})
         o.precision = mode
         for _ in range(3):
@@ -64,7 +64,7 @@ def main():
                 "converged_frac": float(dense[mode]["converged"].mean())}
         print(json.dumps(line), flush=True)
     ex = dense["exact64"]
-    for mode in ("mixed", "mixed-exact", "fp32", "fp64"):
+    for mode in ("mixed", "mixed-fast", "fp32", "fp64"):
         d = dense[mode]
         both = (d["converged"] == 1) & (ex["converged"] == 1)
         print(json.dumps({"vs_exact64": mode, "mask_agreement": float((d["converged"] == ex["converged"]).mean()),

@@ -25,7 +25,7 @@ def _check(deformer, sc, max_iters, dedup=None, tol=TOL_X):
     tg64 = torch.empty((w.shape[0], 12), dtype=torch.float64, device="cuda")
     tg = deformer.precompute_transform_grid(w, sc.dims, sc.bbox, B, out64=tg64)
     out = deformer.batch_search(tg, sc.dims, sc.bbox, B, x, SearchOptions(max_iters, o["conv_eps"], o["div_eps"],
-                                                                         o["dedup_dist"]), tgrid64=tg64)
+                                                                         o["dedup_dist"]), tgrid64=tg64, weights=w)
     g = {k: (v.cpu().numpy() if v is not None else None) for k, v in out.items()}
     r = oracle.batch_search(sc.weights, sc.dims, sc.bbox, sc.bones, sc.points, workers=8, **o)
     agree, dx, _, keep_agree, _ = _parity(g, r, o["conv_eps"])

@@ -104,7 +104,7 @@ def test_exact64_needs_weights(deformer):
     w, B, x = dev(sc.weights), dev(sc.bones), dev(sc.points)
     tg64 = torch.empty((w.shape[0], 12), dtype=torch.float64, device="cuda")
     deformer.precompute_transform_grid(w, sc.dims, sc.bbox, B, out64=tg64)
-    with pytest.raises(FskInvalidArgument, match="need the weight grid"):
+    with pytest.raises(FskInvalidArgument, match="needs the weight grid"):
         deformer.batch_search(None, sc.dims, sc.bbox, B, x, opts_of(sc, 10), tgrid64=tg64)
     o = opts_of(sc, 10)
     o.precision = "exact64"
@@ -118,8 +118,8 @@ def test_exact64_needs_weights(deformer):
 
 @pytest.mark.parametrize("dims,seed,points", [((32, 32, 32), 1, "uniform"), ((64, 64, 16), 11, "training"),
                                               ((64, 64, 64), 25, "training")])
-def test_mixed_exact_escalations_are_the_oracle_bitwise(deformer, dims, seed, points):
-    """precision="mixed-exact": the float64 escalation pass runs the exact replay, so every
+def test_mixed_escalations_are_the_oracle_bitwise(deformer, dims, seed, points):
+    """Default mixed mode with the weight grid: the float64 escalation pass runs the exact replay, so every
     escalated solve equals the oracle bit for bit (at least as many bit-equal solves as were
     escalated), and the whole result keeps the north-star bar."""
     sc = S.make_scene(dims, 20_000, seed=seed, points=points)
@@ -127,7 +127,7 @@ def test_mixed_exact_escalations_are_the_oracle_bitwise(deformer, dims, seed, po
     tg64 = torch.empty((w.shape[0], 12), dtype=torch.float64, device="cuda")
     tg = deformer.precompute_transform_grid(w, sc.dims, sc.bbox, B, out64=tg64)
     deformer.search_stats(reset=True)
-    out = deformer.batch_search(tg, sc.dims, sc.bbox, B, x, opts_of(sc, 50, "mixed-exact"), tgrid64=tg64, weights=w)
+    out = deformer.batch_search(tg, sc.dims, sc.bbox, B, x, opts_of(sc, 50, "mixed"), tgrid64=tg64, weights=w)
     torch.cuda.synchronize()
     n_esc = deformer.search_stats(reset=True)[3]
     g = {k: (v.cpu().numpy() if v is not None else None) for k, v in out.items()}

@@ -235,7 +235,7 @@ def test_compaction_and_host_entry_point(deformer, c1):
     w, B, x = dev(c1.weights), dev(c1.bones), dev(c1.points)
     tg, tg64 = grids(deformer, w, c1, B)
     o = opts_of(c1, 50)
-    dense = deformer.batch_search(tg, c1.dims, c1.bbox, B, x, o, tgrid64=tg64)
+    dense = deformer.batch_search(tg, c1.dims, c1.bbox, B, x, o, tgrid64=tg64, weights=w)
     offs, roots = deformer.compact_roots(dense, x.shape[0], c1.n_bones)
     offs, roots = offs.cpu().numpy(), roots.cpu().numpy()
     d = {k: v.cpu().numpy() for k, v in dense.items()}
@@ -263,7 +263,7 @@ def c3(deformer):
     sc = S.make_scene((32, 32, 32), 20_000, seed=8, points="training")
     w, B, x = dev(sc.weights), dev(sc.bones), dev(sc.points)
     tg, tg64 = grids(deformer, w, sc, B)
-    dense = deformer.batch_search(tg, sc.dims, sc.bbox, B, x, opts_of(sc, 50), tgrid64=tg64)
+    dense = deformer.batch_search(tg, sc.dims, sc.bbox, B, x, opts_of(sc, 50), tgrid64=tg64, weights=w)
     keep = dense["keep"].cpu().numpy()
     sel = np.where(keep.any(1), np.argmax(keep, 1), -1).astype(np.int32)
     n = sc.points.shape[0]
@@ -326,9 +326,9 @@ def test_device_correspondence_sets_match_dense_path(deformer, c1):
     w, B, x = dev(c1.weights), dev(c1.bones), dev(c1.points)
     tg, tg64 = grids(deformer, w, c1, B)
     o = opts_of(c1, 50)
-    d = {k: v.cpu().numpy() for k, v in deformer.batch_search(tg, c1.dims, c1.bbox, B, x, o, tgrid64=tg64).items()}
+    d = {k: v.cpu().numpy() for k, v in deformer.batch_search(tg, c1.dims, c1.bbox, B, x, o, tgrid64=tg64, weights=w).items()}
     keep = np.argwhere(d["keep"] == 1)
-    offs1, roots1 = (t.cpu().numpy() for t in deformer.batch_search_roots(tg, c1.dims, c1.bbox, B, x, o, tgrid64=tg64))
+    offs1, roots1 = (t.cpu().numpy() for t in deformer.batch_search_roots(tg, c1.dims, c1.bbox, B, x, o, tgrid64=tg64, weights=w))
     tg2 = torch.empty_like(tg)
     offs2, roots2 = (t.cpu().numpy() for t in deformer.deform(w, c1.dims, c1.bbox, B, x, o, tgrid=tg2))
     np.testing.assert_array_equal(tg2.cpu().numpy(), tg.cpu().numpy())
@@ -370,7 +370,7 @@ def test_precision_modes(deformer):
     sc = S.make_scene((32, 32, 32), 8000, seed=3)
     r = run_oracle(sc, 50)
     res = {}
-    for prec in ("fp32", "mixed", "fp64"):
+    for prec in ("fp32", "mixed", "mixed-fast", "fp64"):
         deformer.search_stats(reset=True)
         _, g = run_gpu(deformer, sc, 50, precision=prec)
         st = deformer.search_stats(reset=True)
@@ -378,6 +378,7 @@ def test_precision_modes(deformer):
         res[prec] = (agree, dx, keep, st[3] / max(st[0] + (st[3] if prec == "fp64" else 0), 1))
         print(f"\n{prec}: mask agreement {agree:.6f} keep {keep:.6f} max|dx| {dx:.2e} fp64 share {res[prec][3]:.4f}")
     assert res["mixed"][0] >= MASK_AGREE and res["mixed"][1] <= TOL_X
+    assert res["mixed-fast"][0] >= MASK_AGREE and res["mixed-fast"][1] <= TOL_X
     assert res["fp64"][0] >= 0.99999 and res["fp64"][1] <= TOL_X
     assert res["mixed"][3] < 0.15  # the fp64 tail stays a small share of the solves
 
