@@ -45,7 +45,7 @@ namespace fsk {
 
 // Scratch slots (one growable device buffer each).
 enum Slot {
-    kHist, kBbox, kKeys, kPerm, kXs, kScanPart, kBwdAcc, kBwdMax, kPlanes, kPlanes64, kEscQ, kEscN,
+    kHist, kBbox, kKeys, kPerm, kXs, kScanPart, kBwdAcc, kBwdMax, kPlanes, kPlanes64, kEscQ, kEscN, kEscState,
     kBwdStart, kBwdCell, kBwdRec, kPeakTable,
     kOXr, kOJa, kOJb, kOJc, kOMeta, kOKeep, kNRoots, kOffs, kRootsTmp,
     kHW, kHB, kHP, kHT, kHOffs, kHRoots, kFB, kFP, kFOffs, kFRoots,

@@ -105,14 +105,14 @@ __device__ __forceinline__ void deform(const Planes<double>& P, const GridP& g, 
 }
 
 // x0 = B^-1 x' = Rᵀx' + (−Rᵀt) (geometry.hpp:51-61)
-__device__ __forceinline__ void inverse_apply(const float* B, double xp0, double xp1, double xp2, double& x0,
+__device__ __forceinline__ void inverse_apply(const double* B, double xp0, double xp1, double xp2, double& x0,
                                               double& x1, double& x2) {
     double R[9], t[3];
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
 #pragma unroll
-        for (int c = 0; c < 3; ++c) R[3 * r + c] = (double)B[4 * r + c];
-        t[r] = (double)B[4 * r + 3];
+        for (int c = 0; c < 3; ++c) R[3 * r + c] = B[4 * r + c];
+        t[r] = B[4 * r + 3];
     }
     double xo[3];
 #pragma unroll
@@ -129,22 +129,25 @@ __device__ __forceinline__ void inverse_apply(const float* B, double xp0, double
 // locate_cell (trilerp_weights_into), gradient from locate_cell_lower with ±1/h stencils
 // (weight_spatial_gradient), J = Σ_i w_i R_i then + Σ_i (B_i x)(∇w_i)ᵀ, bone order. The
 // per-corner factors are bone-independent and computed once (same operations, same bits);
-// the weights of 4 consecutive bones come in one 16-byte load when n_b % 4 == 0.
+// the weights of 4 consecutive bones come in one 16-byte load when n_b % 4 == 0 (a float64 copy
+// of the grid measured slower: the J~0 gathers are L1-bound); the bone transforms are float64
+// copies in shared memory.
 template <int kVec>
-__device__ __forceinline__ void corner_weights(const float* __restrict__ W, int64_t v, int nb, int b, float out[kVec]) {
+__device__ __forceinline__ void corner_weights(const float* __restrict__ W, int v, int nb, int b, double out[kVec]) {
+    const float* q = W + (int64_t)v * nb + b;
     if constexpr (kVec == 4) {
-        const float4 q = __ldg(reinterpret_cast<const float4*>(W + v * nb + b));
-        out[0] = q.x;
-        out[1] = q.y;
-        out[2] = q.z;
-        out[3] = q.w;
+        const float4 w = __ldg(reinterpret_cast<const float4*>(q));
+        out[0] = w.x;
+        out[1] = w.y;
+        out[2] = w.z;
+        out[3] = w.w;
     } else {
-        out[0] = __ldg(W + v * nb + b);
+        out[0] = __ldg(q);
     }
 }
 
 template <int kVec>
-__device__ __forceinline__ void jacobian_vec(const GridP& g, const float* __restrict__ W, const float* __restrict__ bones,
+__device__ __forceinline__ void jacobian_vec(const GridP& g, const float* __restrict__ W, const double* bones,
                                              double x0, double x1, double x2, double J[9]) {
     const int nb = g.nb;
     const XCell c = locate(g, x0, x1, x2, false), cl = locate(g, x0, x1, x2, true);
@@ -156,7 +159,7 @@ __device__ __forceinline__ void jacobian_vec(const GridP& g, const float* __rest
         dmin[a] = div(-1.0, h[a]);
         dplus[a] = div(1.0, h[a]);
     }
-    int64_t vc[8], vl[8];
+    int vc[8], vl[8];  // vertex indices (< 2^30)
     double w8[8];
 #pragma unroll
     for (int dk = 0; dk < 2; ++dk) {
@@ -181,57 +184,49 @@ __device__ __forceinline__ void jacobian_vec(const GridP& g, const float* __rest
         for (int u = 0; u < kVec; ++u) wb[u] = 0.0;
 #pragma unroll
         for (int k8 = 0; k8 < 8; ++k8) {
-            float q[kVec];
+            double q[kVec];
             corner_weights<kVec>(W, vc[k8], nb, b0, q);
 #pragma unroll
-            for (int u = 0; u < kVec; ++u) wb[u] = add(wb[u], mul(w8[k8], (double)q[u]));
+            for (int u = 0; u < kVec; ++u) wb[u] = add(wb[u], mul(w8[k8], q[u]));
         }
 #pragma unroll
         for (int u = 0; u < kVec; ++u) {
-            const float* B = bones + 12 * (b0 + u);
+            const double* B = bones + 12 * (b0 + u);
 #pragma unroll
             for (int r = 0; r < 3; ++r)
 #pragma unroll
-                for (int cc = 0; cc < 3; ++cc) J[3 * r + cc] = add(J[3 * r + cc], mul(wb[u], (double)B[4 * r + cc]));
+                for (int cc = 0; cc < 3; ++cc) J[3 * r + cc] = add(J[3 * r + cc], mul(wb[u], B[4 * r + cc]));
         }
     }
     const double fx[2] = {sub(1.0, cl.tx), cl.tx}, fy[2] = {sub(1.0, cl.ty), cl.ty}, fz[2] = {sub(1.0, cl.tz), cl.tz};
-    double gx8[8], gy8[8], gz8[8];
-#pragma unroll
-    for (int dk = 0; dk < 2; ++dk)
-#pragma unroll
-        for (int dj = 0; dj < 2; ++dj)
-#pragma unroll
-            for (int di = 0; di < 2; ++di) {
-                const int k8 = 4 * dk + 2 * dj + di;
-                gx8[k8] = mul(mul(di ? dplus[0] : dmin[0], fy[dj]), fz[dk]);
-                gy8[k8] = mul(mul(fx[di], dj ? dplus[1] : dmin[1]), fz[dk]);
-                gz8[k8] = mul(mul(fx[di], fy[dj]), dk ? dplus[2] : dmin[2]);
-            }
     for (int b0 = 0; b0 < nb; b0 += kVec) {  // + Σ_i (B_i x) ∇w_iᵀ
         double gg[kVec][3];
 #pragma unroll
         for (int u = 0; u < kVec; ++u) gg[u][0] = gg[u][1] = gg[u][2] = 0.0;
 #pragma unroll
         for (int k8 = 0; k8 < 8; ++k8) {
-            float q[kVec];
+            const int di = k8 & 1, dj = (k8 >> 1) & 1, dk = k8 >> 2;
+            // stencil factors recomputed per bone group (the same operations, fewer live registers)
+            const double gx = mul(mul(di ? dplus[0] : dmin[0], fy[dj]), fz[dk]);
+            const double gy = mul(mul(fx[di], dj ? dplus[1] : dmin[1]), fz[dk]);
+            const double gz = mul(mul(fx[di], fy[dj]), dk ? dplus[2] : dmin[2]);
+            double q[kVec];
             corner_weights<kVec>(W, vl[k8], nb, b0, q);
 #pragma unroll
             for (int u = 0; u < kVec; ++u) {
-                const double v = (double)q[u];
-                gg[u][0] = add(gg[u][0], mul(gx8[k8], v));
-                gg[u][1] = add(gg[u][1], mul(gy8[k8], v));
-                gg[u][2] = add(gg[u][2], mul(gz8[k8], v));
+                const double v = q[u];
+                gg[u][0] = add(gg[u][0], mul(gx, v));
+                gg[u][1] = add(gg[u][1], mul(gy, v));
+                gg[u][2] = add(gg[u][2], mul(gz, v));
             }
         }
 #pragma unroll
         for (int u = 0; u < kVec; ++u) {
-            const float* B = bones + 12 * (b0 + u);
+            const double* B = bones + 12 * (b0 + u);
             double bx[3];
 #pragma unroll
             for (int r = 0; r < 3; ++r)
-                bx[r] = add(dot3((double)B[4 * r], (double)B[4 * r + 1], (double)B[4 * r + 2], x0, x1, x2),
-                            (double)B[4 * r + 3]);
+                bx[r] = add(dot3(B[4 * r], B[4 * r + 1], B[4 * r + 2], x0, x1, x2), B[4 * r + 3]);
 #pragma unroll
             for (int r = 0; r < 3; ++r)
 #pragma unroll
@@ -240,7 +235,7 @@ __device__ __forceinline__ void jacobian_vec(const GridP& g, const float* __rest
     }
 }
 
-__device__ __forceinline__ void jacobian(const GridP& g, const float* __restrict__ W, const float* __restrict__ bones,
+__device__ __forceinline__ void jacobian(const GridP& g, const float* __restrict__ W, const double* bones,
                                          double x0, double x1, double x2, double J[9]) {
     if (g.nb % 4 == 0) jacobian_vec<4>(g, W, bones, x0, x1, x2, J);
     else jacobian_vec<1>(g, W, bones, x0, x1, x2, J);
@@ -287,9 +282,9 @@ struct XState {
 };
 
 // start: x0, J~0, g0 and err (the converged / diverged decisions are the caller's)
+// W: the weight grid; bones: float64 copies of the transforms (shared memory)
 __device__ __forceinline__ void start(const Planes<double>& P, const GridP& g, const float* __restrict__ W,
-                                      const float* __restrict__ bones, int bone, double xp0, double xp1, double xp2,
-                                      XState& s) {
+                                      const double* bones, int bone, double xp0, double xp1, double xp2, XState& s) {
     inverse_apply(bones + 12 * bone, xp0, xp1, xp2, s.x0, s.x1, s.x2);
     double J[9];
     jacobian(g, W, bones, s.x0, s.x1, s.x2, J);

@@ -371,17 +371,98 @@ constexpr int kEscBlock = 128;
 #ifndef FSK_REFILL_IDLE
 #define FSK_REFILL_IDLE 16  // measured 16 (0.253 ms) vs 12 (0.260) vs 8 (0.265) vs 20 (0.255)
 #endif
+// float64 copies of the bone transforms in shared memory for the exact replay (dynamic smem of
+// n_b·12 doubles; widening is exact)
+__device__ __forceinline__ const double* stage_bones64(const float* __restrict__ bones, int nb) {
+    extern __shared__ double s_bones64[];
+    for (int e = threadIdx.x; e < 12 * nb; e += blockDim.x) s_bones64[e] = (double)__ldg(bones + e);
+    __syncthreads();
+    return s_bones64;
+}
+
+// Start states of the escalated solves, one thread per queue entry (no refill divergence):
+// x0 = B^-1 x', J~0, g0 and the residual e (err for the exact replay, err² otherwise), packed
+// as 8 double2 [x0 x1 | x2 g0 | g1 g2 | e J0 | J1 J2 | J3 J4 | J5 J6 | J7 J8]. A solve that stops
+// at its start (converged or diverged, correspondence.cpp:100-105) is stored here and marked
+// e = -1. Entries at or beyond st_cap are started by the refill kernel itself.
+template <bool kExact>
+__device__ __forceinline__ void esc_start_one(const Planes<double>& P, const GridP& g, const float* __restrict__ W,
+                                              const float* __restrict__ bones, const double* bones64, int64_t n,
+                                              const SearchP& o, const int4& rec, double s[16], bool& stop,
+                                              bool& conv) {
+    const int64_t q = rec.x;
+    const int bone = (int)(q / n);
+    const float xp0 = __int_as_float(rec.y), xp1 = __int_as_float(rec.z), xp2 = __int_as_float(rec.w);
+    if constexpr (kExact) {
+        exact::XState xs;
+        exact::start(P, g, W, bones64, bone, xp0, xp1, xp2, xs);
+        conv = xs.err < o.conv_eps;
+        stop = conv || xs.err > o.div_eps;
+        s[0] = xs.x0, s[1] = xs.x1, s[2] = xs.x2, s[3] = xs.g0, s[4] = xs.g1, s[5] = xs.g2, s[6] = xs.err;
+#pragma unroll
+        for (int e = 0; e < 9; ++e) s[7 + e] = xs.Ji[e];
+    } else {
+        solve_start<double>(P, g, bones + 12 * bone, xp0, xp1, xp2, s[0], s[1], s[2], s + 7, s[3], s[4], s[5], s[6]);
+        conv = s[6] < o.conv2;                // (:100-103)
+        stop = conv || s[6] > o.div2;         // divergence check at the top (:105)
+    }
+    stop = stop || o.max_iters <= 0;
+}
+
+#ifndef FSK_ESC_START_MINB
+#define FSK_ESC_START_MINB 3
+#endif
+template <bool kExact>
+__global__ void __launch_bounds__(128, FSK_ESC_START_MINB)
+    k_esc_start(Planes<double> P, GridP g, const float* __restrict__ W, const float* __restrict__ bones, int64_t n,
+                SearchP o, SearchPlanes out, const int4* __restrict__ esc_q, int64_t esc_cap,
+                const int* __restrict__ esc_count, double2* __restrict__ st, int st_cap,
+                unsigned long long* __restrict__ stats) {
+    const int cnt_long = esc_count[3], cnt = min(esc_count[3] + esc_count[2], st_cap);
+    const double* bones64 = kExact ? stage_bones64(bones, g.nb) : nullptr;
+    unsigned n_solves = 0;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < cnt; idx += gridDim.x * blockDim.x) {
+        const int4 rec = esc_q[idx < cnt_long ? idx : esc_cap - 1 - (idx - cnt_long)];
+        double s[16];
+        bool stop, conv;
+        esc_start_one<kExact>(P, g, W, bones, bones64, n, o, rec, s, stop, conv);
+        if (stop) {
+            if constexpr (kExact) {
+                exact::XState xs;
+                xs.x0 = s[0], xs.x1 = s[1], xs.x2 = s[2], xs.err = s[6], xs.k = 0;
+#pragma unroll
+                for (int e = 0; e < 9; ++e) xs.Ji[e] = s[7 + e];
+                store_exact(out, rec.x, xs, conv);
+            } else {
+                store_solve(out, rec.x, s[0], s[1], s[2], s + 7, s[6], SolveOut{0, conv, false});
+            }
+            s[6] = -1.0;
+            n_solves += 1;
+        }
+        double2* d = st + 8 * (int64_t)idx;
+#pragma unroll
+        for (int h = 0; h < 8; ++h) d[h] = make_double2(s[2 * h], s[2 * h + 1]);
+    }
+    if (stats) {
+        const unsigned full = __activemask();
+        n_solves = __reduce_add_sync(full, n_solves);
+        if ((threadIdx.x & 31) == __ffs(full) - 1 && n_solves) atomicAdd(stats + 3, (unsigned long long)n_solves);
+    }
+}
+
 template <bool kExact>  // kExact: the solves replay the reference's operation order (fsk_exact.cuh)
 __global__ void __launch_bounds__(kEscBlock, kExact ? FSK_ESC_EXACT_MINB : FSK_ESC_MINB)
     k_search_escalated(Planes<double> P, GridP g, const float* __restrict__ W, const float* __restrict__ bones,
                        int64_t n, SearchP o,
                        SearchPlanes out, const int4* __restrict__ esc_q, int64_t esc_cap,
-                       const int* __restrict__ esc_count, unsigned long long* __restrict__ stats) {
+                       const int* __restrict__ esc_count, const double2* __restrict__ st, int st_cap,
+                       unsigned long long* __restrict__ stats) {
     // Persistent lanes with refill: a lane whose solve finished takes the next queue entry
     // (one warp-aggregated atomic per refill round), so long float64 trajectories do not hold
     // a whole warp idle. Each solve runs exactly solve_one<double>'s arithmetic (solve_start +
     // broyden_step), so results are identical to the one-thread-per-solve kernel.
     const int cnt_long = esc_count[3], cnt = esc_count[3] + esc_count[2];
+    const double* bones64 = kExact ? stage_bones64(bones, g.nb) : nullptr;
     int* work = const_cast<int*>(esc_count) + 1;
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;
@@ -422,21 +503,35 @@ __global__ void __launch_bounds__(kEscBlock, kExact ? FSK_ESC_EXACT_MINB : FSK_E
             if (got) {  // start of the solve (correspondence.cpp:135-137, :43-54)
                 const int4 rec = esc_q[idx < cnt_long ? idx : esc_cap - 1 - (idx - cnt_long)];
                 q = rec.x;
-                const int bone = (int)(q / n);
                 xq = make_float4(__int_as_float(rec.y), __int_as_float(rec.z), __int_as_float(rec.w), 0.f);
                 k = 0;
-                active = true;
-                bool conv, stop;
-                if constexpr (kExact) {
-                    exact::start(P, g, W, bones, bone, xq.x, xq.y, xq.z, xs);
-                    conv = xs.err < o.conv_eps;
-                    stop = conv || xs.err > o.div_eps;
+                double s[16];
+                bool conv = false, stop;
+                if (idx < st_cap) {  // started by k_esc_start (stopped ones are already stored)
+                    const double2* d = st + 8 * (int64_t)idx;
+#pragma unroll
+                    for (int h = 0; h < 8; ++h) {
+                        const double2 v = d[h];
+                        s[2 * h] = v.x;
+                        s[2 * h + 1] = v.y;
+                    }
+                    stop = s[6] < 0.0;
+                    active = !stop;
                 } else {
-                    solve_start<double>(P, g, bones + 12 * bone, xq.x, xq.y, xq.z, x0, x1, x2, Ji, g0, g1, g2, err2);
-                    conv = err2 < conv2;                 // (:100-103)
-                    stop = conv || err2 > div2;          // divergence check at the top (:105)
+                    esc_start_one<kExact>(P, g, W, bones, bones64, n, o, rec, s, stop, conv);
+                    active = true;
                 }
-                if (stop || o.max_iters <= 0) {
+                if constexpr (kExact) {
+                    xs.x0 = s[0], xs.x1 = s[1], xs.x2 = s[2], xs.g0 = s[3], xs.g1 = s[4], xs.g2 = s[5];
+                    xs.err = s[6], xs.k = 0;
+#pragma unroll
+                    for (int e = 0; e < 9; ++e) xs.Ji[e] = s[7 + e];
+                } else {
+                    x0 = s[0], x1 = s[1], x2 = s[2], g0 = s[3], g1 = s[4], g2 = s[5], err2 = s[6];
+#pragma unroll
+                    for (int e = 0; e < 9; ++e) Ji[e] = s[7 + e];
+                }
+                if (active && stop) {
                     if constexpr (kExact) store_exact(out, q, xs, conv);
                     else store_solve(out, q, x0, x1, x2, Ji, err2, SolveOut{0, conv, false});
                     n_solves += 1;
@@ -504,11 +599,12 @@ __global__ void __launch_bounds__(128) k_search_exact(Planes<double> P, GridP g,
                                                       unsigned long long* __restrict__ stats) {
     const int bone = blockIdx.x / blocks_per_bone;
     const int64_t j = (int64_t)(blockIdx.x - bone * blocks_per_bone) * 128 + threadIdx.x;
+    const double* bones64 = stage_bones64(bones, g.nb);
     if (j >= n) return;
     const float4 xq = __ldg(xs + j);
     const double xp0 = xq.x, xp1 = xq.y, xp2 = xq.z;
     exact::XState s;
-    exact::start(P, g, W, bones, bone, xp0, xp1, xp2, s);
+    exact::start(P, g, W, bones64, bone, xp0, xp1, xp2, s);
     bool conv = s.err < o.conv_eps;  // iterate (correspondence.cpp:97-124)
     if (!conv)
         for (int k = 0; k < o.max_iters; ++k) {
@@ -838,6 +934,11 @@ SearchState run_search(fsk_ctx* ctx, const GridPlanes& P, const GridP& g, const 
                        const float* pts, int64_t n, const SearchP& sp, int flags, cudaStream_t st) {
     if ((flags & FSK_SEARCH_EXACT64) && !weights)
         fail(FSK_EINVAL, "fsk: FSK_SEARCH_EXACT64 needs the weight grid (J~0 from the skinning weights)");
+    // the exact replay reads the weight grid and float64 copies of the bones (shared memory)
+    const bool exact_any = weights && ((flags & FSK_SEARCH_EXACT64) ||
+                                       !(flags & (FSK_SEARCH_FAST_ESC | FSK_SEARCH_FP32_ONLY | FSK_SEARCH_FP64)));
+    const size_t smem64 = (size_t)g.nb * 12 * sizeof(double);
+    const float* Wx = exact_any ? weights : nullptr;
     if (n >= (int64_t(1) << 31) / std::max(1, g.nb)) fail(FSK_EINVAL, "fsk: too many points for one call (split the batch)");
     const int64_t S = std::max<int64_t>(1, n * g.nb);
     SearchState s;
@@ -871,7 +972,7 @@ SearchState run_search(fsk_ctx* ctx, const GridPlanes& P, const GridP& g, const 
         const int bpb = (int)blocks_for(n, 128);
         const int64_t nblocks = (int64_t)bpb * g.nb;
         if (nblocks >= (int64_t(1) << 31)) fail(FSK_EINVAL, "fsk: search grid too large");
-        FSK_LAUNCH(ctx, st, k_search_exact, (unsigned)nblocks, 128, 0, P.p64, g, weights, bones, xs, n, bpb, sp, s.sp,
+        FSK_LAUNCH(ctx, st, k_search_exact, (unsigned)nblocks, 128, smem64, P.p64, g, Wx, bones, xs, n, bpb, sp, s.sp,
                    ctx->stats);
     } else if (flags & FSK_SEARCH_FP64) {
         const int bpb = (int)blocks_for(n, 128);
@@ -894,17 +995,25 @@ SearchState run_search(fsk_ctx* ctx, const GridPlanes& P, const GridP& g, const 
         // exact replay of the reference whenever the weight grid is at hand
         const bool exact_esc = weights && !(flags & FSK_SEARCH_FAST_ESC);
         cuda_check(exact_esc ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search_escalated<true>,
-                                                                             kEscBlock, 0)
+                                                                             kEscBlock, smem64)
                              : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search_escalated<false>,
                                                                              kEscBlock, 0),
                    "occupancy");
         const unsigned egrid = (unsigned)(ctx->sm_count * std::max(per_sm, 1));
-        if (esc && exact_esc)
-            FSK_LAUNCH(ctx, st, k_search_escalated<true>, egrid, kEscBlock, 0, P.p64, g, weights, bones, n, sp, s.sp,
-                       esc_q, S, esc_n, ctx->stats);
-        else if (esc)
-            FSK_LAUNCH(ctx, st, k_search_escalated<false>, egrid, kEscBlock, 0, P.p64, g, weights, bones, n, sp, s.sp,
-                       esc_q, S, esc_n, ctx->stats);
+        // start states of up to st_cap escalated solves (~5 % escalate; the rest start in-kernel)
+        const int st_cap = (int)std::min<int64_t>(S, std::max<int64_t>(1 << 16, S / 8));
+        double2* est = esc && exact_esc ? (double2*)scratch(ctx, kEscState, (size_t)st_cap * 8 * sizeof(double2))
+                                        : nullptr;
+        const unsigned sgrid = (unsigned)(ctx->sm_count * FSK_ESC_START_MINB);
+        if (esc && exact_esc) {
+            FSK_LAUNCH(ctx, st, k_esc_start<true>, sgrid, 128, smem64, P.p64, g, Wx, bones, n, sp, s.sp, esc_q, S,
+                       esc_n, est, st_cap, ctx->stats);
+            FSK_LAUNCH(ctx, st, k_search_escalated<true>, egrid, kEscBlock, smem64, P.p64, g, Wx, bones, n, sp, s.sp,
+                       esc_q, S, esc_n, est, st_cap, ctx->stats);
+        } else if (esc) {  // cheap starts (transform-grid J~0): measured faster inside the refill kernel
+            FSK_LAUNCH(ctx, st, k_search_escalated<false>, egrid, kEscBlock, 0, P.p64, g, nullptr, bones, n, sp, s.sp,
+                       esc_q, S, esc_n, nullptr, 0, ctx->stats);
+        }
     }
     FSK_LAUNCH(ctx, st, k_dedup, blocks_for(n, 256), 256, 0, n, g.nb, (float)sp.dedup2, s.sp, s.perm, s.n_roots_p);
     return s;
