@@ -384,7 +384,7 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0 and not args.no_mlp:
         line["mlp_stages"] = mlp_stages(D, sc, roots_buf, n, dev)
     if not args.no_e2e:  # every rank its own shard through the host API; whole-job rate, max over ranks
-        e2e = e2e_ours(D, sc, opts, args, world=world)
+        e2e = e2e_ours(D, sc, opts, args, world=world, roots_hint=total_roots)
         if rank == 0:
             line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -498,7 +498,7 @@ def mlp_stages(D, sc, roots_buf, n, dev, reps=20):
     return out
 
 
-def e2e_ours(D, sc, opts, args, steps=None, world=1):
+def e2e_ours(D, sc, opts, args, steps=None, world=1, roots_hint=None):
     """Same metric through the C-ABI host-buffer entry points: pinned host weights/bones/points
     in, CorrespondenceSets (offsets + kept roots) out, every copy inside the timed region.
     Headline: fsk_deform_host_frames over `steps` frames of the subject (one frame = one step;
@@ -512,7 +512,10 @@ def e2e_ours(D, sc, opts, args, steps=None, world=1):
     hx = torch.from_numpy(sc.points).pin_memory()
     # two output sets, alternated across frames (a consumer reads frame f while f+1 downloads)
     hoffs = [torch.empty(n + 1, dtype=torch.int64).pin_memory() for _ in range(2)]
-    hroots = [torch.empty((n * nb, 16), dtype=torch.float32).pin_memory() for _ in range(2)]
+    # root capacity: every (query, init) when that is small, else twice this frame's kept-root
+    # count measured on the device (a frame needing more fails loudly: "root buffer too small")
+    cap = n * nb if roots_hint is None or n * nb <= 8 << 20 else min(n * nb, 2 * roots_hint + 4096)
+    hroots = [torch.empty((cap, 16), dtype=torch.float32).pin_memory() for _ in range(2)]
 
     def frames_call():
         return D.deform_host_frames(hw, sc.dims, sc.bbox, [hb] * steps, [hx] * steps, opts,
