@@ -75,6 +75,31 @@ __device__ __forceinline__ void deform(const Planes<double>& P, const GridP& g, 
     double m[12];
 #pragma unroll
     for (int e = 0; e < 12; ++e) m[e] = 0.0;
+#ifdef FSK_EXACT_ROW_OUTER
+    // row-outer: the entries of row r only read row r of the corners, so processing one row's
+    // 4 edges at a time keeps fewer float64 loads in flight (same operations, same bits)
+    const double w1x = c.tx, w0x = sub(1.0, c.tx);
+    double wyz[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) wyz[e] = mul((e >> 1) ? c.tz : sub(1.0, c.tz), (e & 1) ? c.ty : sub(1.0, c.ty));
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            V4<double> a, b;
+            load_edge(P, vidx(g, c.i, c.j + (e & 1), c.k + (e >> 1)), r, a, b);
+            const double w0 = mul(wyz[e], w0x), w1 = mul(wyz[e], w1x);
+            m[4 * r + 0] = add(m[4 * r + 0], mul(w0, a.x));
+            m[4 * r + 1] = add(m[4 * r + 1], mul(w0, a.y));
+            m[4 * r + 2] = add(m[4 * r + 2], mul(w0, a.z));
+            m[4 * r + 3] = add(m[4 * r + 3], mul(w0, a.w));
+            m[4 * r + 0] = add(m[4 * r + 0], mul(w1, b.x));
+            m[4 * r + 1] = add(m[4 * r + 1], mul(w1, b.y));
+            m[4 * r + 2] = add(m[4 * r + 2], mul(w1, b.z));
+            m[4 * r + 3] = add(m[4 * r + 3], mul(w1, b.w));
+        }
+    }
+#else
 #pragma unroll
     for (int dk = 0; dk < 2; ++dk) {
         const double wz = dk ? c.tz : sub(1.0, c.tz);
@@ -100,6 +125,7 @@ __device__ __forceinline__ void deform(const Planes<double>& P, const GridP& g, 
             }
         }
     }
+#endif
 #pragma unroll
     for (int r = 0; r < 3; ++r) d[r] = add(dot3(m[4 * r], m[4 * r + 1], m[4 * r + 2], x0, x1, x2), m[4 * r + 3]);
 }
@@ -241,6 +267,101 @@ __device__ __forceinline__ void jacobian(const GridP& g, const float* __restrict
     else jacobian_vec<1>(g, W, bones, x0, x1, x2, J);
 }
 
+// jacobian() with one pass over the weight grid when both lookups pick the same cell (always,
+// unless x lies exactly on an interior cell face): each corner's weights are loaded and widened
+// once, feeding both Σ_i w_i R_i (accumulated into J in bone order) and ∇w_i, which is parked in
+// shared memory (stash: n_b·3 doubles per thread, strided by blockDim) until the second sum,
+// so J is added up in exactly jacobian_vec's order (same operations, same bits).
+template <int kVec>
+__device__ __noinline__ void jacobian_cold(const GridP& g, const float* __restrict__ W, const double* bones, double x0,
+                                           double x1, double x2, double J[9]) {
+    jacobian_vec<kVec>(g, W, bones, x0, x1, x2, J);
+}
+
+template <int kVec>
+__device__ __forceinline__ void jacobian_stash_vec(const GridP& g, const float* __restrict__ W, const double* bones,
+                                                   double x0, double x1, double x2, double J[9], double* stash) {
+    const int nb = g.nb;
+    const XCell c = locate(g, x0, x1, x2, false), cl = locate(g, x0, x1, x2, true);
+    if (c.i != cl.i || c.j != cl.j || c.k != cl.k) {
+        jacobian_cold<kVec>(g, W, bones, x0, x1, x2, J);  // x on an interior cell face (rare)
+        return;
+    }
+    const int n[3] = {g.nx, g.ny, g.nz};
+    double dmin[3], dplus[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double h = div(sub(g.hid[a], g.lod[a]), (double)(n[a] - 1));  // cell_size (skinning.cpp:72-75)
+        dmin[a] = div(-1.0, h);
+        dplus[a] = div(1.0, h);
+    }
+    const double fx[2] = {sub(1.0, cl.tx), cl.tx}, fy[2] = {sub(1.0, cl.ty), cl.ty}, fz[2] = {sub(1.0, cl.tz), cl.tz};
+    int vc[8];
+    double w8[8];
+#pragma unroll
+    for (int dk = 0; dk < 2; ++dk) {
+        const double wz = dk ? c.tz : sub(1.0, c.tz);
+#pragma unroll
+        for (int dj = 0; dj < 2; ++dj) {
+            const double wyz = mul(wz, dj ? c.ty : sub(1.0, c.ty));
+#pragma unroll
+            for (int di = 0; di < 2; ++di) {
+                const int k8 = 4 * dk + 2 * dj + di;
+                w8[k8] = mul(wyz, di ? c.tx : sub(1.0, c.tx));
+                vc[k8] = vidx(g, c.i + di, c.j + dj, c.k + dk);
+            }
+        }
+    }
+    const int ld = blockDim.x;
+#pragma unroll
+    for (int e = 0; e < 9; ++e) J[e] = 0.0;
+    for (int b0 = 0; b0 < nb; b0 += kVec) {
+        double wb[kVec], gg[kVec][3];
+#pragma unroll
+        for (int u = 0; u < kVec; ++u) wb[u] = gg[u][0] = gg[u][1] = gg[u][2] = 0.0;
+#pragma unroll
+        for (int k8 = 0; k8 < 8; ++k8) {
+            const int di = k8 & 1, dj = (k8 >> 1) & 1, dk = k8 >> 2;
+            // stencil factors recomputed per bone group (the same operations, fewer live registers)
+            const double gx = mul(mul(di ? dplus[0] : dmin[0], fy[dj]), fz[dk]);
+            const double gy = mul(mul(fx[di], dj ? dplus[1] : dmin[1]), fz[dk]);
+            const double gz = mul(mul(fx[di], fy[dj]), dk ? dplus[2] : dmin[2]);
+            double q[kVec];
+            corner_weights<kVec>(W, vc[k8], nb, b0, q);
+#pragma unroll
+            for (int u = 0; u < kVec; ++u) {
+                wb[u] = add(wb[u], mul(w8[k8], q[u]));
+                gg[u][0] = add(gg[u][0], mul(gx, q[u]));
+                gg[u][1] = add(gg[u][1], mul(gy, q[u]));
+                gg[u][2] = add(gg[u][2], mul(gz, q[u]));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kVec; ++u) {
+            const double* B = bones + 12 * (b0 + u);
+#pragma unroll
+            for (int r = 0; r < 3; ++r)
+#pragma unroll
+                for (int cc = 0; cc < 3; ++cc) J[3 * r + cc] = add(J[3 * r + cc], mul(wb[u], B[4 * r + cc]));
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) stash[(3 * (b0 + u) + cc) * ld] = gg[u][cc];
+        }
+    }
+    for (int b = 0; b < nb; ++b) {  // + Σ_i (B_i x) ∇w_iᵀ
+        const double* B = bones + 12 * b;
+        const double gg0 = stash[(3 * b) * ld], gg1 = stash[(3 * b + 1) * ld], gg2 = stash[(3 * b + 2) * ld];
+        double bx[3];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) bx[r] = add(dot3(B[4 * r], B[4 * r + 1], B[4 * r + 2], x0, x1, x2), B[4 * r + 3]);
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+            J[3 * r + 0] = add(J[3 * r + 0], mul(bx[r], gg0));
+            J[3 * r + 1] = add(J[3 * r + 1], mul(bx[r], gg1));
+            J[3 * r + 2] = add(J[3 * r + 2], mul(bx[r], gg2));
+        }
+    }
+}
+
 // initial_inverse_jacobian (correspondence.cpp:43-54): Eigen's det (expansion along row 0)
 // against 1e-8, then the cofactor inverse with its own det (adjugate / det)
 __device__ __forceinline__ void inverse_or_identity(const double a[9], double Ji[9]) {
@@ -284,10 +405,16 @@ struct XState {
 // start: x0, J~0, g0 and err (the converged / diverged decisions are the caller's)
 // W: the weight grid; bones: float64 copies of the transforms (shared memory)
 __device__ __forceinline__ void start(const Planes<double>& P, const GridP& g, const float* __restrict__ W,
-                                      const double* bones, int bone, double xp0, double xp1, double xp2, XState& s) {
+                                      const double* bones, int bone, double xp0, double xp1, double xp2, XState& s,
+                                      double* stash = nullptr) {
     inverse_apply(bones + 12 * bone, xp0, xp1, xp2, s.x0, s.x1, s.x2);
     double J[9];
-    jacobian(g, W, bones, s.x0, s.x1, s.x2, J);
+    if (stash) {
+        if (g.nb % 4 == 0) jacobian_stash_vec<4>(g, W, bones, s.x0, s.x1, s.x2, J, stash);
+        else jacobian_stash_vec<1>(g, W, bones, s.x0, s.x1, s.x2, J, stash);
+    } else {
+        jacobian(g, W, bones, s.x0, s.x1, s.x2, J);
+    }
     inverse_or_identity(J, s.Ji);
     double d[3];
     deform(P, g, s.x0, s.x1, s.x2, d);

@@ -365,11 +365,14 @@ __global__ void __launch_bounds__(kSearchBlock, FSK_SEARCH_MINB)
 #define FSK_ESC_MINB 2  // measured: 254 regs / 8 warps per SM beats 168 regs / 12 warps (0.263 vs 0.277 ms)
 #endif
 #ifndef FSK_ESC_EXACT_MINB
-#define FSK_ESC_EXACT_MINB 3
+#define FSK_ESC_EXACT_MINB 2  // 254 regs, no spills: 0.271 ms vs 0.302 at 3 (168 regs, loop-carried spills); refill threshold 16 vs 1/4/8 measured best too
 #endif
 constexpr int kEscBlock = 128;
 #ifndef FSK_REFILL_IDLE
 #define FSK_REFILL_IDLE 16  // measured 16 (0.253 ms) vs 12 (0.260) vs 8 (0.265) vs 20 (0.255)
+#endif
+#ifndef FSK_REFILL_IDLE_EXACT  // exact replay: starts come precomputed from k_esc_start, so a refill is one 128-B load
+#define FSK_REFILL_IDLE_EXACT 16
 #endif
 // float64 copies of the bone transforms in shared memory for the exact replay (dynamic smem of
 // n_b·12 doubles; widening is exact)
@@ -389,13 +392,13 @@ template <bool kExact>
 __device__ __forceinline__ void esc_start_one(const Planes<double>& P, const GridP& g, const float* __restrict__ W,
                                               const float* __restrict__ bones, const double* bones64, int64_t n,
                                               const SearchP& o, const int4& rec, double s[16], bool& stop,
-                                              bool& conv) {
+                                              bool& conv, double* stash = nullptr) {
     const int64_t q = rec.x;
     const int bone = (int)(q / n);
     const float xp0 = __int_as_float(rec.y), xp1 = __int_as_float(rec.z), xp2 = __int_as_float(rec.w);
     if constexpr (kExact) {
         exact::XState xs;
-        exact::start(P, g, W, bones64, bone, xp0, xp1, xp2, xs);
+        exact::start(P, g, W, bones64, bone, xp0, xp1, xp2, xs, stash);
         conv = xs.err < o.conv_eps;
         stop = conv || xs.err > o.div_eps;
         s[0] = xs.x0, s[1] = xs.x1, s[2] = xs.x2, s[3] = xs.g0, s[4] = xs.g1, s[5] = xs.g2, s[6] = xs.err;
@@ -410,22 +413,24 @@ __device__ __forceinline__ void esc_start_one(const Planes<double>& P, const Gri
 }
 
 #ifndef FSK_ESC_START_MINB
-#define FSK_ESC_START_MINB 3
+#define FSK_ESC_START_MINB 2  // with the ∇w stash (72 KB per CTA at 24 bones): 0.099 ms vs 0.124 at 3 (spills) and 0.106 without the stash
 #endif
 template <bool kExact>
 __global__ void __launch_bounds__(128, FSK_ESC_START_MINB)
     k_esc_start(Planes<double> P, GridP g, const float* __restrict__ W, const float* __restrict__ bones, int64_t n,
                 SearchP o, SearchPlanes out, const int4* __restrict__ esc_q, int64_t esc_cap,
                 const int* __restrict__ esc_count, double2* __restrict__ st, int st_cap,
-                unsigned long long* __restrict__ stats) {
+                unsigned long long* __restrict__ stats, bool stash_on) {
     const int cnt_long = esc_count[3], cnt = min(esc_count[3] + esc_count[2], st_cap);
     const double* bones64 = kExact ? stage_bones64(bones, g.nb) : nullptr;
+    // exact replay: per-thread stash of ∇w (n_b·3 doubles, strided) behind the bone copies, when sized in
+    double* stash = (kExact && stash_on) ? const_cast<double*>(bones64) + 12 * g.nb + threadIdx.x : nullptr;
     unsigned n_solves = 0;
     for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < cnt; idx += gridDim.x * blockDim.x) {
         const int4 rec = esc_q[idx < cnt_long ? idx : esc_cap - 1 - (idx - cnt_long)];
         double s[16];
         bool stop, conv;
-        esc_start_one<kExact>(P, g, W, bones, bones64, n, o, rec, s, stop, conv);
+        esc_start_one<kExact>(P, g, W, bones, bones64, n, o, rec, s, stop, conv, stash);
         if (stop) {
             if constexpr (kExact) {
                 exact::XState xs;
@@ -480,7 +485,7 @@ __global__ void __launch_bounds__(kEscBlock, kExact ? FSK_ESC_EXACT_MINB : FSK_E
     // Idle lanes are refilled in batches (>= kRefillIdle idle, or the whole warp), so the
     // divergent init path (x0, Jacobian stencil, inverse) runs for many lanes at once and the
     // iteration trips — the bulk of the work — run with most lanes active.
-    constexpr int kRefillIdle = FSK_REFILL_IDLE;
+    constexpr int kRefillIdle = kExact ? FSK_REFILL_IDLE_EXACT : FSK_REFILL_IDLE;
     int buf_idx = 0, bused = 32;
     bool dry = false;
     while (true) {
@@ -1004,10 +1009,25 @@ SearchState run_search(fsk_ctx* ctx, const GridPlanes& P, const GridP& g, const 
         const int st_cap = (int)std::min<int64_t>(S, std::max<int64_t>(1 << 16, S / 8));
         double2* est = esc && exact_esc ? (double2*)scratch(ctx, kEscState, (size_t)st_cap * 8 * sizeof(double2))
                                         : nullptr;
-        const unsigned sgrid = (unsigned)(ctx->sm_count * FSK_ESC_START_MINB);
         if (esc && exact_esc) {
-            FSK_LAUNCH(ctx, st, k_esc_start<true>, sgrid, 128, smem64, P.p64, g, Wx, bones, n, sp, s.sp, esc_q, S,
-                       esc_n, est, st_cap, ctx->stats);
+            // ∇w stash for the one-pass initial Jacobian: n_b·3 doubles per thread, if it fits
+            // (up to 73 bones at 128 threads; larger skeletons take the two-pass form)
+            const size_t stash_b = (size_t)g.nb * 3 * sizeof(double) * 128;
+#ifdef FSK_NO_STASH
+            const bool stash_on = false;
+#else
+            const bool stash_on = smem64 + stash_b <= 227 * 1024;
+#endif
+            const size_t smem_s = smem64 + (stash_on ? stash_b : 0);
+            int per_sm_s = 0;
+            if (smem_s > 48 * 1024)
+                cuda_check(cudaFuncSetAttribute(k_esc_start<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)smem_s), "cudaFuncSetAttribute");
+            cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_s, k_esc_start<true>, 128, smem_s),
+                       "occupancy");
+            const unsigned sgrid = (unsigned)(ctx->sm_count * std::max(1, std::min(per_sm_s, FSK_ESC_START_MINB)));
+            FSK_LAUNCH(ctx, st, k_esc_start<true>, sgrid, 128, smem_s, P.p64, g, Wx, bones, n, sp, s.sp, esc_q, S,
+                       esc_n, est, st_cap, ctx->stats, stash_on);
             FSK_LAUNCH(ctx, st, k_search_escalated<true>, egrid, kEscBlock, smem64, P.p64, g, Wx, bones, n, sp, s.sp,
                        esc_q, S, esc_n, est, st_cap, ctx->stats);
         } else if (esc) {  // cheap starts (transform-grid J~0): measured faster inside the refill kernel

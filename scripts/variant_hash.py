@@ -16,9 +16,12 @@ sc = S.make_scene((32, 32, 32), n, seed=1)
 o = sc.search_options(50)
 w, B, x = (torch.from_numpy(a).cuda() for a in (sc.weights, sc.bones, sc.points))
 tg = D.precompute_transform_grid(w, sc.dims, sc.bbox, B)
-out = D.batch_search(tg, sc.dims, sc.bbox, B, x, SearchOptions(50, o["conv_eps"], o["div_eps"], o["dedup_dist"]))
-h = hashlib.sha256()
-for k in sorted(out):
-    h.update(k.encode())
-    h.update(out[k].cpu().numpy().tobytes())
-print("HASH", os.environ.get("FSK_LIB", "default"), h.hexdigest()[:16])
+so = SearchOptions(50, o["conv_eps"], o["div_eps"], o["dedup_dist"])
+# without the weight grid: fused float64 escalation; with it (the default of fsk_deform*): exact replay
+for tag, wt in (("fused", None), ("exact", w)):
+    out = D.batch_search(tg, sc.dims, sc.bbox, B, x, so, weights=wt)
+    h = hashlib.sha256()
+    for k in sorted(out):
+        h.update(k.encode())
+        h.update(out[k].cpu().numpy().tobytes())
+    print("HASH", tag, os.environ.get("FSK_LIB", "default"), h.hexdigest()[:16])
