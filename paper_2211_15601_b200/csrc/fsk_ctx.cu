@@ -221,7 +221,10 @@ int fsk_ctx_create(int device, fsk_ctx** out) {
         c->device = device;
         c->sm_count = prop.multiProcessorCount;
         if (cudaMalloc(&c->stats, 8 * sizeof(unsigned long long)) != cudaSuccess ||
-            cudaMemset(c->stats, 0, 8 * sizeof(unsigned long long)) != cudaSuccess) {
+            cudaMemset(c->stats, 0, 8 * sizeof(unsigned long long)) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
             delete c;
             fail(FSK_ECUDA, "fsk: cannot allocate context state");
         }
@@ -243,6 +246,9 @@ int fsk_ctx_destroy(fsk_ctx* ctx) {
         if (ctx->stats) cudaFree(ctx->stats);
         if (ctx->copy) cudaStreamDestroy(ctx->copy);
         if (ctx->upload) cudaStreamDestroy(ctx->upload);
+        if (ctx->side) cudaStreamDestroy(ctx->side);
+        if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+        if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
         if (ctx->hcount) cudaFreeHost(ctx->hcount);
         delete ctx;
     });

@@ -38,6 +38,9 @@ struct fsk_ctx {
     // device→host copy stream of the host-buffer entry point (created on first use)
     cudaStream_t copy = nullptr;
     cudaStream_t upload = nullptr;  // host→device stream of the host-buffer entry point
+    // side stream + fork/join events: the spatial sort of a search runs beside K1 (precompute)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int64_t* hcount = nullptr;  // pinned per-chunk root counts
 };
 

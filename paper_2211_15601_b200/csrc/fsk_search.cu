@@ -321,39 +321,49 @@ __device__ __forceinline__ void count_work(unsigned long long* stats, const Solv
     }
 }
 
-// Fast pass: one thread per (posed point, bone-init) solve in float32. Blocks are
-// bone-major (B_i^-1 is a block-uniform broadcast load) over spatially sorted queries.
-// Solves flagged for escalation are appended (warp-aggregated) to esc_q.
+// Fast pass: one thread per posed point, looping over a group of `bpg` bone inits (one float32
+// solve each) over spatially sorted queries. Blocks are tile-major: block = (query tile, bone
+// group), so one SM solves several inits of the same queries back to back — they converge to the
+// same few canonical roots, and the iterations' gathers hit the cells the previous init left in
+// L1. B_i^-1 stays a block-uniform broadcast load. Solves flagged for escalation are appended
+// (warp-aggregated) to esc_q.
+#ifndef FSK_FAST_BPG
+#define FSK_FAST_BPG 8  // bone inits per block (0: all). C2 fast pass: 1 0.638 ms, 2 0.594, 4 0.575, 8 0.572, 12 0.581, 24 0.601 (bone-major blocks: 0.633)
+#endif
 __global__ void __launch_bounds__(kSearchBlock, FSK_SEARCH_MINB)
     k_search_fast(Planes<float> P, GridP g, const float* __restrict__ bones, const float4* __restrict__ xs, int64_t n,
-                  int blocks_per_bone, SearchP o, SearchPlanes out, int4* __restrict__ esc_q, int64_t esc_cap,
+                  int bpg, SearchP o, SearchPlanes out, int4* __restrict__ esc_q, int64_t esc_cap,
                   int* __restrict__ esc_count, unsigned long long* __restrict__ stats) {
-    const int bone = blockIdx.x / blocks_per_bone;
-    const int64_t j = (int64_t)(blockIdx.x - bone * blocks_per_bone) * kSearchBlock + threadIdx.x;
+    const int ngroups = (g.nb + bpg - 1) / bpg;
+    const int tile = blockIdx.x / ngroups, grp = blockIdx.x - tile * ngroups;
+    const int64_t j = (int64_t)tile * kSearchBlock + threadIdx.x;
     if (j >= n) return;
     const float4 xq = __ldg(xs + j);
-    float x0, x1, x2, Ji[9], err2;
-    const SolveOut s = solve_one<float, true>(P, g, bones + 12 * bone, xq.x, xq.y, xq.z, o, x0, x1, x2, Ji, err2);
-    const int64_t q = (int64_t)bone * n + j;
-    store_solve(out, q, x0, x1, x2, Ji, err2, s);
-    count_work(stats, s);
-    if (esc_q) {
-        // Capped (long) trajectories are queued from the front, the rest from the back, so
-        // the escalation pass starts the long float64 solves first and the short ones fill
-        // its tail (the pass reads front entries [0, A) then back entries [S-B, S)).
-        const unsigned act = __activemask();
-        const unsigned ml = __ballot_sync(act, s.esc && s.capped), ms = __ballot_sync(act, s.esc && !s.capped);
-        const int lane = threadIdx.x & 31, leader = __ffs(act) - 1;
-        const unsigned lt = (1u << lane) - 1;
-        unsigned long long b = 0;  // one atomic for both counters: {short (low word), long (high word)}
-        if (lane == leader && (ml | ms))
-            b = atomicAdd(reinterpret_cast<unsigned long long*>(esc_count + 2),
-                          ((unsigned long long)__popc(ml) << 32) | (unsigned long long)__popc(ms));
-        b = __shfl_sync(act, b, leader);
-        const int bl = (int)(b >> 32), bs = (int)(b & 0xffffffffu);
-        const int4 rec = make_int4((int)q, __float_as_int(xq.x), __float_as_int(xq.y), __float_as_int(xq.z));
-        if (s.esc && s.capped) esc_q[bl + __popc(ml & lt)] = rec;
-        else if (s.esc) esc_q[esc_cap - 1 - (bs + __popc(ms & lt))] = rec;
+    const int b_end = min(g.nb, (grp + 1) * bpg);
+    for (int bone = grp * bpg; bone < b_end; ++bone) {
+        float x0, x1, x2, Ji[9], err2;
+        const SolveOut s = solve_one<float, true>(P, g, bones + 12 * bone, xq.x, xq.y, xq.z, o, x0, x1, x2, Ji, err2);
+        const int64_t q = (int64_t)bone * n + j;
+        store_solve(out, q, x0, x1, x2, Ji, err2, s);
+        count_work(stats, s);
+        if (esc_q) {
+            // Capped (long) trajectories are queued from the front, the rest from the back, so
+            // the escalation pass starts the long float64 solves first and the short ones fill
+            // its tail (the pass reads front entries [0, A) then back entries [S-B, S)).
+            const unsigned act = __activemask();
+            const unsigned ml = __ballot_sync(act, s.esc && s.capped), ms = __ballot_sync(act, s.esc && !s.capped);
+            const int lane = threadIdx.x & 31, leader = __ffs(act) - 1;
+            const unsigned lt = (1u << lane) - 1;
+            unsigned long long b = 0;  // one atomic for both counters: {short (low word), long (high word)}
+            if (lane == leader && (ml | ms))
+                b = atomicAdd(reinterpret_cast<unsigned long long*>(esc_count + 2),
+                              ((unsigned long long)__popc(ml) << 32) | (unsigned long long)__popc(ms));
+            b = __shfl_sync(act, b, leader);
+            const int bl = (int)(b >> 32), bs = (int)(b & 0xffffffffu);
+            const int4 rec = make_int4((int)q, __float_as_int(xq.x), __float_as_int(xq.y), __float_as_int(xq.z));
+            if (s.esc && s.capped) esc_q[bl + __popc(ml & lt)] = rec;
+            else if (s.esc) esc_q[esc_cap - 1 - (bs + __popc(ms & lt))] = rec;
+        }
     }
 }
 
@@ -934,9 +944,20 @@ struct SearchState {
     int32_t* n_roots_p;
 };
 
-// sort + K2 (+ K2b escalation) + dedup into the ctx's search planes.
-SearchState run_search(fsk_ctx* ctx, const GridPlanes& P, const GridP& g, const float* weights, const float* bones,
-                       const float* pts, int64_t n, const SearchP& sp, int flags, cudaStream_t st) {
+// K1 issued by run_search itself, concurrently with the spatial sort (which only reads the points)
+struct PrecomputeReq {
+    const float* w;
+    const float* bones;
+    float* tg;
+    bool f64;
+};
+
+// sort + K2 (+ K2b escalation) + dedup into the ctx's search planes. With `pre`, K1 runs on `st`
+// while the sort runs on the ctx's side stream (fork/join by events, capturable in a graph), and
+// P is filled in here.
+SearchState run_search(fsk_ctx* ctx, GridPlanes& P, const GridP& g, const float* weights, const float* bones,
+                       const float* pts, int64_t n, const SearchP& sp, int flags, cudaStream_t st,
+                       const PrecomputeReq* pre = nullptr) {
     if ((flags & FSK_SEARCH_EXACT64) && !weights)
         fail(FSK_EINVAL, "fsk: FSK_SEARCH_EXACT64 needs the weight grid (J~0 from the skinning weights)");
     // the exact replay reads the weight grid and float64 copies of the bones (shared memory)
@@ -947,6 +968,9 @@ SearchState run_search(fsk_ctx* ctx, const GridPlanes& P, const GridP& g, const 
     if (n >= (int64_t(1) << 31) / std::max(1, g.nb)) fail(FSK_EINVAL, "fsk: too many points for one call (split the batch)");
     const int64_t S = std::max<int64_t>(1, n * g.nb);
     SearchState s;
+    auto precompute = [&] {
+        if (pre) P = run_precompute(ctx, pre->w, g, pre->bones, pre->tg, nullptr, true, pre->f64, st);
+    };
     s.sp.xr = (float4*)scratch(ctx, kOXr, S * sizeof(float4));
     s.sp.ja = (float4*)scratch(ctx, kOJa, S * sizeof(float4));
     s.sp.jb = (float4*)scratch(ctx, kOJb, S * sizeof(float4));
@@ -955,7 +979,10 @@ SearchState run_search(fsk_ctx* ctx, const GridPlanes& P, const GridP& g, const 
     s.sp.keep = (uint8_t*)scratch(ctx, kOKeep, S);
     s.perm = (int*)scratch(ctx, kPerm, std::max<int64_t>(1, n) * sizeof(int));
     s.n_roots_p = (int32_t*)scratch(ctx, kNRoots, std::max<int64_t>(1, n) * sizeof(int32_t));
-    if (n == 0) return s;
+    if (n == 0) {
+        precompute();
+        return s;
+    }
     float4* xs = (float4*)scratch(ctx, kXs, n * sizeof(float4));
     int* esc_n = (int*)scratch(ctx, kEscN, 4 * sizeof(int));  // {-, work cursor, short count, long count}
     // (with the spatial sort, the counters live in the sort state and are zeroed with it)
@@ -964,13 +991,25 @@ SearchState run_search(fsk_ctx* ctx, const GridPlanes& P, const GridP& g, const 
         unsigned* bbox = (unsigned*)(hist + kBboxOff);
         esc_n = hist + kEscOff;  // zeroed with the histogram
         uint16_t* keys = (uint16_t*)scratch(ctx, kKeys, n * sizeof(uint16_t));
-        cuda_check(cudaMemsetAsync(hist, 0, kSortStateInts * sizeof(int), st), "cudaMemsetAsync");
+        cudaStream_t ss = st;
+        if (pre) {  // fork: the sort on the side stream, K1 on st
+            cuda_check(cudaEventRecord(ctx->ev_fork, st), "cudaEventRecord");
+            cuda_check(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0), "cudaStreamWaitEvent");
+            ss = ctx->side;
+        }
+        cuda_check(cudaMemsetAsync(hist, 0, kSortStateInts * sizeof(int), ss), "cudaMemsetAsync");
         const unsigned gb = (unsigned)std::min<int64_t>(blocks_for(n, 256), (int64_t)ctx->sm_count * 8);
-        FSK_LAUNCH(ctx, st, k_sort_bbox, gb, 256, 0, pts, n, bbox);
-        FSK_LAUNCH(ctx, st, k_sort_hist, blocks_for(n, 256), 256, 0, pts, n, bbox, keys, hist);
-        FSK_LAUNCH(ctx, st, k_sort_scan, kScanBlocks, 1024, 0, hist, hist + kScanBarOff);
-        FSK_LAUNCH(ctx, st, k_sort_scatter, blocks_for(n, 256), 256, 0, pts, keys, n, hist, s.perm, xs);
+        FSK_LAUNCH(ctx, ss, k_sort_bbox, gb, 256, 0, pts, n, bbox);
+        FSK_LAUNCH(ctx, ss, k_sort_hist, blocks_for(n, 256), 256, 0, pts, n, bbox, keys, hist);
+        FSK_LAUNCH(ctx, ss, k_sort_scan, kScanBlocks, 1024, 0, hist, hist + kScanBarOff);
+        FSK_LAUNCH(ctx, ss, k_sort_scatter, blocks_for(n, 256), 256, 0, pts, keys, n, hist, s.perm, xs);
+        if (pre) {  // join
+            cuda_check(cudaEventRecord(ctx->ev_join, ss), "cudaEventRecord");
+            precompute();
+            cuda_check(cudaStreamWaitEvent(st, ctx->ev_join, 0), "cudaStreamWaitEvent");
+        }
     } else {
+        precompute();
         FSK_LAUNCH(ctx, st, k_identity_order, blocks_for(n, 256), 256, 0, pts, n, s.perm, xs, esc_n);
     }
     if (flags & FSK_SEARCH_EXACT64) {
@@ -987,14 +1026,14 @@ SearchState run_search(fsk_ctx* ctx, const GridPlanes& P, const GridP& g, const 
     } else {
         const bool esc = needs_f64(flags);
         int4* esc_q = esc ? (int4*)scratch(ctx, kEscQ, S * sizeof(int4)) : nullptr;
-        const int bpb = (int)blocks_for(n, kSearchBlock);
-        const int64_t nblocks = (int64_t)bpb * g.nb;
+        const int bpg = (FSK_FAST_BPG > 0) ? std::min(FSK_FAST_BPG, g.nb) : g.nb;
+        const int64_t nblocks = (int64_t)blocks_for(n, kSearchBlock) * ((g.nb + bpg - 1) / bpg);
         if (nblocks >= (int64_t(1) << 31)) fail(FSK_EINVAL, "fsk: search grid too large");
         SearchP spf = sp;
         if (!esc) {  // float32 only (ablation): no cap, no flags
             spf.esc_cap = sp.max_iters;
         }
-        FSK_LAUNCH(ctx, st, k_search_fast, (unsigned)nblocks, kSearchBlock, 0, P.p32, g, bones, xs, n, bpb, spf, s.sp,
+        FSK_LAUNCH(ctx, st, k_search_fast, (unsigned)nblocks, kSearchBlock, 0, P.p32, g, bones, xs, n, bpg, spf, s.sp,
                    esc_q, S, esc_n, ctx->stats);
         int per_sm = 0;  // persistent kernel: exactly the resident capacity
         // exact replay of the reference whenever the weight grid is at hand
@@ -1293,7 +1332,7 @@ int fsk_search_fwd(fsk_ctx* ctx, const float* tgrid, const double* tgrid64, cons
         if (n > 0 && (!points || !bones)) fail(FSK_EINVAL, "fsk: null buffer");
         if (n == 0) return;
         cudaStream_t st = (cudaStream_t)stream;
-        const GridPlanes P = run_relayout(ctx, tgrid, tgrid64, g, needs_f64(opts->flags), st);
+        GridPlanes P = run_relayout(ctx, tgrid, tgrid64, g, needs_f64(opts->flags), st);
         const SearchState s = run_search(ctx, P, g, weights, bones, points, n, sp, opts->flags, st);
         DenseOut d{out->x_c, out->jinv, out->resid, out->iters, out->converged, out->keep, out->n_roots};
         FSK_LAUNCH(ctx, st, k_scatter_dense, blocks_for(n * g.nb, 256), 256, 0, n, g.nb, s.sp, s.perm, d);
@@ -1390,7 +1429,7 @@ int fsk_batch_search(fsk_ctx* ctx, const float* tgrid, const double* tgrid64, co
         if (n < 0) fail(FSK_EINVAL, "fsk: negative point count");
         if (!offsets || (n > 0 && (!points || !bones))) fail(FSK_EINVAL, "fsk: null buffer");
         cudaStream_t st = (cudaStream_t)stream;
-        const GridPlanes P = run_relayout(ctx, tgrid, tgrid64, g, needs_f64(opts->flags), st);
+        GridPlanes P = run_relayout(ctx, tgrid, tgrid64, g, needs_f64(opts->flags), st);
         const SearchState s = run_search(ctx, P, g, weights, bones, points, n, sp, opts->flags, st);
         compact(ctx, s, n, g.nb, offsets, roots, cap, st);
     });
@@ -1407,8 +1446,9 @@ int fsk_deform(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* desc, co
         if (n < 0) fail(FSK_EINVAL, "fsk: negative point count");
         if (!offsets || !bones || (n > 0 && !points)) fail(FSK_EINVAL, "fsk: null buffer");
         cudaStream_t st = (cudaStream_t)stream;
-        const GridPlanes P = run_precompute(ctx, weights, g, bones, tgrid, nullptr, true, needs_f64(opts->flags), st);
-        const SearchState s = run_search(ctx, P, g, weights, bones, points, n, sp, opts->flags, st);
+        GridPlanes P;  // K1 runs inside run_search, beside the spatial sort
+        const PrecomputeReq pre{weights, bones, tgrid, needs_f64(opts->flags)};
+        const SearchState s = run_search(ctx, P, g, weights, bones, points, n, sp, opts->flags, st, &pre);
         compact(ctx, s, n, g.nb, offsets, roots, cap, st);
     });
 }
@@ -1498,7 +1538,7 @@ int fsk_deform_host(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* des
                            "H2D points");
             cuda_check(cudaEventRecord(up[c], ctx->upload), "cudaEventRecord");
         }
-        const GridPlanes P = run_precompute(ctx, dW, g, dB, nullptr, nullptr, true, needs_f64(opts->flags), st);
+        GridPlanes P = run_precompute(ctx, dW, g, dB, nullptr, nullptr, true, needs_f64(opts->flags), st);
         for (int64_t c = 0; c < nchunks; ++c) {
             const int64_t p0 = c * csz, m = std::max<int64_t>(0, std::min(csz, n - p0));
             cuda_check(cudaStreamWaitEvent(st, up[c], 0), "cudaStreamWaitEvent");
@@ -1614,8 +1654,9 @@ int fsk_deform_host_frames(fsk_ctx* ctx, const float* weights, const fsk_grid_de
             cuda_check(cudaEventRecord(up[f], ctx->upload), "cudaEventRecord");
             cuda_check(cudaStreamWaitEvent(st, up[f], 0), "cudaStreamWaitEvent");
             if (f >= 2) cuda_check(cudaStreamWaitEvent(st, fetched[f - 2], 0), "cudaStreamWaitEvent");
-            const GridPlanes P = run_precompute(ctx, dW, g, slot_b(f), nullptr, nullptr, true, needs_f64(opts->flags), st);
-            const SearchState s = run_search(ctx, P, g, dW, slot_b(f), slot_p(f), n, sp, opts->flags, st);
+            GridPlanes P;  // K1 runs inside run_search, beside the spatial sort
+            const PrecomputeReq pre{dW, slot_b(f), nullptr, needs_f64(opts->flags)};
+            const SearchState s = run_search(ctx, P, g, dW, slot_b(f), slot_p(f), n, sp, opts->flags, st, &pre);
             compact(ctx, s, n, nb, slot_o(f), slot_r(f), n * nb, st);
             cuda_check(cudaEventRecord(done[f], st), "cudaEventRecord");
         };
