@@ -38,7 +38,7 @@ GATHER_BYTES = 384  # 8 corners x 48 B of transform grid per d(x) evaluation
 # dram__bytes_read.sum + dram__bytes_write.sum of one k_search_fast launch (C2), from the
 # ncu --set full capture profiles/r01_final_search.ncu-rep (6.8 MB read + 205.0 MB written:
 # the bone-major search planes; the gather itself is L1/L2-resident)
-NCU_TRAFFIC_K2 = 211.8e6
+NCU_TRAFFIC_K2 = 7.6672e6 + 204.605952e6  # dram read + write per k_search_fast launch, profiles/r01_final_search.ncu-rep
 
 
 def parse():
@@ -371,7 +371,7 @@ def run_ours(args, rank, world, local_rank):
                                                "32-B slots of an L1-resident table, all SMs",
                                 "cell_cache_hit_frac": 1 - fills32 / max(it32, 1),
                                 "note": "bytes actually gathered (init + iterations that left the register-cached "
-                                        "cell); ncu: L1 data pipe 68 %, issue slots 47 % (profiles/r01_final_summary.md)"},
+                                        "cell); ncu: L1 hit 78 %, L1 data pipe 72 %, issue slots 52 % (profiles/r01_final_summary.md)"},
                      "k2_share_of_step": k2_ms / max(all_ms, 1e-9),
                      "k2_escalated_share_of_step": k2e_ms / max(all_ms, 1e-9),
                      "kernel_ms_per_step": breakdown,
