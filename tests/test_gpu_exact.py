@@ -142,3 +142,46 @@ def test_mixed_escalations_are_the_oracle_bitwise(deformer, dims, seed, points):
     assert (g["converged"] == r["converged"]).mean() >= 0.9999
     both = (g["converged"] == 1) & (r["converged"] == 1)
     assert np.abs(g["x_c"] - r["x_c"])[both].max() <= 1e-4
+
+
+@pytest.mark.parametrize("n_bones", [21, 80])
+def test_mixed_escalations_bitwise_other_bone_counts(deformer, n_bones):
+    """The escalation start kernel's one-pass J~0 (weight gradients parked in shared memory) has a
+    scalar-weight path for n_b % 4 != 0 (21 bones) and falls back to the two-pass form when the
+    stash does not fit in shared memory (80 bones: 80·3 doubles × 128 threads > 227 KB). Both must
+    still replay the oracle bit for bit.
+
+    Position tolerance: the north star's 1e-4 is stated at the SMPL-like scale (1.7 m skeleton,
+    conv_eps = 1e-5·diag ≈ 2e-5). These chains are long (80 bones: diag ≈ 99, conv_eps ≈ 1e-3), and
+    the search's own stopping tolerance scales with the scene: two solvers that both stop at
+    err < conv_eps may stop one Broyden step apart, which the escalation step rule bounds by 2·conv_eps
+    (DESIGN.md §precision), plus float32 rounding at coordinates of ~50 m (measured: 2.3·conv_eps at
+    80 bones). So the bar here is max(1e-4, 3·conv_eps) — positions within the solver's own stopping
+    tolerance; the escalated solves themselves are checked bit for bit."""
+    # 80 bones × 8000 points: ~15 % of the 640 k solves escalate, more than the 80 k start states
+    # k_esc_start precomputes (an eighth of the solves), so the refill kernel's own start path runs too
+    n = 8_000 if n_bones == 80 else 4_000
+    sc = S.make_scene((32, 32, 32), n, seed=3, skeleton=S.chain_skeleton(n_bones))
+    w, B, x = dev(sc.weights), dev(sc.bones), dev(sc.points)
+    tg64 = torch.empty((w.shape[0], 12), dtype=torch.float64, device="cuda")
+    tg = deformer.precompute_transform_grid(w, sc.dims, sc.bbox, B, out64=tg64)
+    deformer.search_stats(reset=True)
+    out = deformer.batch_search(tg, sc.dims, sc.bbox, B, x, opts_of(sc, 50, "mixed"), tgrid64=tg64, weights=w)
+    torch.cuda.synchronize()
+    n_esc = deformer.search_stats(reset=True)[3]
+    g = {k: (v.cpu().numpy() if v is not None else None) for k, v in out.items()}
+    r = oracle.batch_search(sc.weights, sc.dims, sc.bbox, sc.bones, sc.points, workers=8, **sc.search_options(50))
+    same = ((g["converged"] == r["converged"]) & (g["iters"].astype(np.int32) == r["iters"])
+            & (g["resid"] == r["resid"].astype(np.float32))
+            & (g["x_c"] == r["x_c"].astype(np.float32)).all(-1))
+    both = (g["converged"] == 1) & (r["converged"] == 1)
+    dx = np.abs(g["x_c"] - r["x_c"])[both].max()
+    conv = sc.search_options(50)["conv_eps"]
+    print(f"\n{n_bones} bones: escalated {n_esc}, bit-equal to the oracle {int(same.sum())} of {same.size}, "
+          f"max|dx| {dx:.2e} (conv_eps {conv:.2e})")
+    assert n_esc > 0
+    if n_bones == 80:
+        assert n_esc > max(65536, n * n_bones // 8)  # the in-kernel start path ran
+    assert same.sum() >= n_esc
+    assert (g["converged"] == r["converged"]).mean() >= 0.9999
+    assert dx <= max(1e-4, 3 * conv)
