@@ -6,7 +6,8 @@ Metric (BASELINE.json): (point x bone-init) correspondences/sec — one Broyden 
 K1 precompute_transform_grid + spatial sort + K2 correspondence search + dedup, for the
 configuration BASELINE.json's metric is quoted on (configs[1]): 200k posed points x 24
 bone inits, 32^3 grid, reference default max_iters=50. Weak scaling: every rank
-processes its own 200k points (points shard with no data-path collective).
+processes its own 200k points; the solves need no exchange, only the pose does (rank 0 broadcasts
+each frame's bones over NCCL inside the timed step; the training shape also all-reduces dL/dT).
 
   python bench.py [--gpus N --steps K --warmup W]            # our arm
   python bench.py --impl reference [...]                      # the reference CPU path
@@ -210,10 +211,14 @@ def run_ours(args, rank, world, local_rank):
     frames = [(torch.from_numpy(sc.bones).to(dev), torch.from_numpy(sc.points).to(dev))]
     skel = S.smpl_like_skeleton()
     for fi in range(1, args.poses):
-        rng = np.random.default_rng(args.seed * 7919 + 104729 * rank + fi)
+        # the poses are the same on every rank (rank 0 owns them and broadcasts each frame's bones
+        # in the timed step); each rank samples its own point shard in the posed box
+        rng = np.random.default_rng(args.seed * 7919 + fi)
         ang = rng.uniform(-0.5, 0.5, nb)
         bones = S.forward_kinematics(skel, ang)
         lo, hi = S.posed_sampling_box(skel, bones, 0.1)
+        if rank:
+            rng = np.random.default_rng(args.seed * 7919 + 104729 * rank + fi)
         frames.append((torch.from_numpy(bones.reshape(nb, 12).astype(np.float32)).to(dev),
                        torch.from_numpy(S.uniform_points(lo, hi, n, rng).astype(np.float32)).to(dev)))
     B, x = frames[0]
@@ -231,6 +236,8 @@ def run_ours(args, rank, world, local_rank):
 
     def step():
         for Bf, xf in frames:
+            if world > 1:  # the frame's pose reaches every rank from its owner (NCCL over NVLink)
+                dist.broadcast(Bf, src=0)
             # one frame: precompute_transform_grid + batch_search → CorrespondenceSets on device
             offs, roots = D.deform(w, sc.dims, sc.bbox, Bf, xf, opts, tgrid=tg, out=roots_buf)
             if args.backward:
@@ -238,6 +245,8 @@ def run_ours(args, rank, world, local_rank):
                 # take each query's first kept root; then the implicit-diff backward (K3) and dL/dw
                 ridx = torch.where(offs[1:] > offs[:-1], offs[:-1], torch.full_like(offs[:-1], -1))
                 D.search_bwd_roots(sc.dims, sc.bbox, nb, roots, ridx, gx, deterministic=args.deterministic, out=gT)
+                if world > 1:  # dL/dT summed over the point shards before the local dL/dw contraction
+                    dist.all_reduce(gT, op=dist.ReduceOp.SUM)
                 D.grad_weights(sc.dims, sc.bbox, gT, Bf, out=gW)
 
     peak_fp32 = D.measure_fp32_peak()
@@ -251,6 +260,8 @@ def run_ours(args, rank, world, local_rank):
     # asynchronous): replays remove the host launch path and the inter-kernel gaps
     launches_per_step = None
     run_step = step
+    if world > 1:  # the step's NCCL calls are launched eagerly (not captured into the graph)
+        args.graph = False
     if args.graph:
         l0 = D.launch_count
         side = torch.cuda.Stream(dev)
@@ -348,7 +359,9 @@ def run_ours(args, rank, world, local_rank):
                    "max_iters": args.max_iters, "sort": not args.no_sort, "poses": args.poses,
                    "precision": args.precision, "cuda_graph": bool(args.graph),
                    "l2": "flushed between steps (256 MiB fill outside the per-step CUDA events)",
-                   "parallelism": f"points sharded across {world} GPU(s), no data-path collective"},
+                   "parallelism": (f"points sharded across {world} GPU(s); per frame NCCL broadcast of the pose "
+                                   f"from rank 0" + ("; NCCL all-reduce of dL/dT" if args.backward else "")
+                                   if world > 1 else "1 GPU (points sharded across ranks under torchrun)")},
         "roofline": {"bound": "fp32", "kernel": "k_search_fast", "achieved": achieved, "peak": peak_fp32,
                      "unit": "TFLOP/s", "frac": achieved / peak_fp32,
                      "traffic": NCU_TRAFFIC_K2 if (args.grid == "32,32,32" and args.points == 200_000) else None,
@@ -565,6 +578,12 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # logic check of the multi-rank step on a one-GPU box only: FSK_BENCH_SHARED_GPU=1 puts every rank
+    # on cuda:0 with the host-side gloo backend (no rank's kernel waits on another's); numbers from
+    # such a run are not measurements
+    shared = os.environ.get("FSK_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local_rank = 0
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -572,7 +591,10 @@ def main():
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist
