@@ -225,7 +225,8 @@ int fsk_ctx_create(int device, fsk_ctx** out) {
             cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
             cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
-            delete c;
+            cudaGetLastError();
+            fsk_ctx_destroy(c);  // releases whatever was created
             fail(FSK_ECUDA, "fsk: cannot allocate context state");
         }
         *out = c;
