@@ -1,5 +1,6 @@
 // fsk_ctx.cu — context lifecycle, scratch, errors, validation, profiling hooks and the
 // FP32 roofline microbenchmark of the C-ABI (include/fsk.h).
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 
@@ -110,7 +111,7 @@ SearchP make_search(const fsk_search_opts* o) {
     s.dedup2 = o->dedup_dist * o->dedup_dist;
     // Escalation rule of the float32 pass (validated on 1.5M solves
     // against the f64 oracle with oracle/precision_emul.cpp): cap at 8 iterations, escalate
-    // unconverged runs of >= 3 iterations, and any threshold decision within float32 noise:
+    // unconverged runs of >= esc_min_div iterations, and any threshold decision within float32 noise:
     // err^2 within ±2% of conv^2 (f32 residuals near conv carry ~1e-7/3e-5 relative error),
     // within ±2e-4 of div^2, |det J0| < 1e-5 (vs the 1e-8 singular cut), |den| < 1e-12
     // (vs the 1e-18 Broyden guard).
@@ -120,7 +121,10 @@ SearchP make_search(const fsk_search_opts* o) {
     // (near-degenerate rank-one update). Bands are on err, like the emulator's:
     // |err/conv - 1| < 2 %, |err/div - 1| < 2e-4.
     s.esc_cap = 8;
-    s.esc_min_div = 3;
+    // unconverged (diverged) runs escalate from 5 iterations on: GPU band study over 150 scenes
+    // (108 M solves, scripts/gpu_esc_study.sh) — 3: 1 mask flip, 5: 5, 6: 10, 8 (rule off): 61; roots
+    // unchanged (max |dx| 8.1e-5 in all). 5 escalates 12 % fewer solves than 3 (C2: 4.85 % -> 4.25 %).
+    s.esc_min_div = 5;
     s.esc_conv_lo = 0.98f * 0.98f;
     s.esc_conv_hi = 1.02f * 1.02f;
     s.esc_div_lo = (1.0f - 2e-4f) * (1.0f - 2e-4f);
@@ -135,6 +139,12 @@ SearchP make_search(const fsk_search_opts* o) {
     // by one step, up to 4·conv): rho = 0.7, tau = 2 (a one-step difference stays < 2·conv).
     s.esc_rho2 = 0.7f * 0.7f;
     s.esc_tau2 = 2.0f * 2.0f;
+    s.esc_conv_band_last = false;
+#ifdef FSK_ESC_STUDY  // rule-study builds only: overrides from the environment
+    if (const char* v = getenv("FSK_ESC_CONV_BAND_LAST")) s.esc_conv_band_last = atoi(v) != 0;
+    if (const char* v = getenv("FSK_ESC_MIN_DIV")) s.esc_min_div = atoi(v);
+    if (const char* v = getenv("FSK_ESC_COS")) s.esc_cos2 = (float)(atof(v) * atof(v));
+#endif
     return s;
 }
 
@@ -220,8 +230,8 @@ int fsk_ctx_create(int device, fsk_ctx** out) {
         auto* c = new fsk_ctx();
         c->device = device;
         c->sm_count = prop.multiProcessorCount;
-        if (cudaMalloc(&c->stats, 8 * sizeof(unsigned long long)) != cudaSuccess ||
-            cudaMemset(c->stats, 0, 8 * sizeof(unsigned long long)) != cudaSuccess ||
+        if (cudaMalloc(&c->stats, fsk_ctx::kStatSlots * sizeof(unsigned long long)) != cudaSuccess ||
+            cudaMemset(c->stats, 0, fsk_ctx::kStatSlots * sizeof(unsigned long long)) != cudaSuccess ||
             cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
             cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
@@ -294,6 +304,20 @@ int fsk_ctx_prof_read(fsk_ctx* ctx, const char* name, double* total_ms, int64_t*
         }
     });
 }
+
+#ifdef FSK_ESC_REASONS
+// study builds only (scripts/esc_reasons.py): per-rule escalation counters, slots 8..31
+extern "C" int fsk_ctx_esc_reasons(fsk_ctx* ctx, uint64_t out[24], int reset) {
+    return guard([&] {
+        set_device(ctx);
+        cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+        unsigned long long h[fsk_ctx::kStatSlots];
+        cuda_check(cudaMemcpy(h, ctx->stats, sizeof(h), cudaMemcpyDeviceToHost), "cudaMemcpy");
+        for (int i = 0; i < 24; ++i) out[i] = h[8 + i];
+        if (reset) cuda_check(cudaMemset(ctx->stats + 8, 0, 24 * sizeof(unsigned long long)), "cudaMemset");
+    });
+}
+#endif
 
 int fsk_ctx_search_stats(fsk_ctx* ctx, uint64_t out[7], int reset) {
     return guard([&] {

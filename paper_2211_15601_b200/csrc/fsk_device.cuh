@@ -55,6 +55,7 @@ struct SearchP {
     float esc_cos2;     // (dx·J~dg)² < esc_cos2·|dx|²|J~dg|² → near-degenerate rank-one update
     float esc_rho2;     // step rule: the stop decision is "near" when err² ∈ [rho², 1/rho²]·conv² ...
     float esc_tau2;     // ... and the step it decides (taken or not) is longer than tau·conv
+    bool esc_conv_band_last;  // apply the ±conv band only where a conv decision can flip the mask (the last iteration)
 };
 
 template <typename R>
@@ -363,7 +364,13 @@ struct SolveOut {
     bool esc;
     bool capped;  // escalated because the float32 pass hit its iteration cap (a long trajectory)
     int fills = 0;  // iteration gathers (cell-cache misses) of the float32 pass
+    unsigned reasons = 0;  // FSK_ESC_REASONS study builds: which escalation rules fired (bit per rule)
 };
+#ifdef FSK_ESC_REASONS
+#define FSK_REASON(bit) (reasons |= (1u << (bit)))
+#else
+#define FSK_REASON(bit) ((void)0)
+#endif
 
 // One Broyden iteration after the divergence check (correspondence.cpp:106-122): step,
 // re-evaluate, and — unless the new residual converged — the good-Broyden rank-one update.
@@ -453,11 +460,14 @@ __device__ __forceinline__ SolveOut solve_one(const Planes<R>& P, const GridP& g
     const R conv2 = (R)o.conv2, div2 = (R)o.div2;
     bool esc = false, capped = false;
     int fills = 0;
-    auto near = [&](R e2) {
-        return (e2 >= (R)o.esc_conv_lo * conv2 && e2 <= (R)o.esc_conv_hi * conv2) ||
-               (e2 >= (R)o.esc_div_lo * div2 && e2 <= (R)o.esc_div_hi * div2);
-    };
-    if (kFast) esc = fabs(det) < (R)o.esc_det || near(err2);
+    unsigned reasons = 0;
+    auto near_conv = [&](R e2) { return e2 >= (R)o.esc_conv_lo * conv2 && e2 <= (R)o.esc_conv_hi * conv2; };
+    auto near_div = [&](R e2) { return e2 >= (R)o.esc_div_lo * div2 && e2 <= (R)o.esc_div_hi * div2; };
+    if (kFast) {
+        if (fabs(det) < (R)o.esc_det) esc = true, FSK_REASON(0);
+        if (near_conv(err2) && (!o.esc_conv_band_last || o.max_iters == 0)) esc = true, FSK_REASON(1);
+        if (near_div(err2)) esc = true, FSK_REASON(10);
+    }
     int iters = 0;
     R xl0 = x0, xl1 = x1, xl2 = x2, e2l = 0;  // float32 pass: position and err² before the last step
     bool conv = err2 < conv2;  // (:100-103)
@@ -473,25 +483,28 @@ __device__ __forceinline__ SolveOut solve_one(const Planes<R>& P, const GridP& g
                 e2l = err2;
             }
             R den;
+            bool degen = false;
             const bool c = broyden_step<R, kCache>(P, g, xp0, xp1, xp2, conv2, x0, x1, x2, Ji, g0, g1, g2, err2, den,
-                                                   &cache, (R)o.esc_cos2, kFast ? &esc : nullptr, &fills);
+                                                   &cache, (R)o.esc_cos2, kFast ? &degen : nullptr, &fills);
+            if (degen) esc = true, FSK_REASON(2);
             iters = k + 1;
-            if (kFast && near(err2)) esc = true;
+            if (kFast && near_conv(err2) && (!o.esc_conv_band_last || iters == o.max_iters)) esc = true, FSK_REASON(3);
+            if (kFast && near_div(err2)) esc = true, FSK_REASON(11);
             if (c) {
                 conv = true;
                 break;
             }
-            if (kFast && fabs(den) < (R)o.esc_den) esc = true;
+            if (kFast && fabs(den) < (R)o.esc_den) esc = true, FSK_REASON(4);
         }
         // the float32 pass hit its iteration cap before max_iters: the f64 pass decides
-        if (kFast && !conv && k == limit && limit < o.max_iters && !(err2 > div2)) esc = capped = true;
-        if (kFast && !conv && iters >= o.esc_min_div) esc = true;
+        if (kFast && !conv && k == limit && limit < o.max_iters && !(err2 > div2)) esc = capped = true, FSK_REASON(5);
+        if (kFast && !conv && iters >= o.esc_min_div) esc = true, FSK_REASON(6);
     }
     if (kFast && conv) {  // ill-conditioned root: float32 rounding is amplified into x*
         R m = 0;
 #pragma unroll
         for (int e = 0; e < 9; ++e) m = fmax(m, fabs(Ji[e]));
-        if (m > (R)o.esc_jmax) esc = true;
+        if (m > (R)o.esc_jmax) esc = true, FSK_REASON(7);
         // Step rule: a float64 solve may stop one Broyden step earlier or later than this one
         // when a stop decision sat near conv; the roots then differ by that step. Escalate if
         // the step in question is long: |J~g| (the next step) when err ≥ rho·conv, or the last
@@ -501,14 +514,14 @@ __device__ __forceinline__ SolveOut solve_one(const Planes<R>& P, const GridP& g
             const R s0 = Ji[0] * g0 + Ji[1] * g1 + Ji[2] * g2;
             const R s1 = Ji[3] * g0 + Ji[4] * g1 + Ji[5] * g2;
             const R s2 = Ji[6] * g0 + Ji[7] * g1 + Ji[8] * g2;
-            if (s0 * s0 + s1 * s1 + s2 * s2 > tau2) esc = true;
+            if (s0 * s0 + s1 * s1 + s2 * s2 > tau2) esc = true, FSK_REASON(8);
         }
         if (iters > 0 && e2l * (R)o.esc_rho2 <= conv2) {
             const R d0 = x0 - xl0, d1 = x1 - xl1, d2 = x2 - xl2;
-            if (d0 * d0 + d1 * d1 + d2 * d2 > tau2) esc = true;
+            if (d0 * d0 + d1 * d1 + d2 * d2 > tau2) esc = true, FSK_REASON(9);
         }
     }
-    return SolveOut{iters, conv, esc, capped, fills};
+    return SolveOut{iters, conv, esc, capped, fills, reasons};
 }
 
 }  // namespace fsk

@@ -24,6 +24,7 @@
 // every solve whose outcome float32 cannot settle (long or late-diverging trajectories,
 // threshold decisions within float32 noise); those (~5 %) are solved again in float64,
 // which B200 runs at half the float32 rate.
+#include <cstdlib>
 #include <cstring>
 
 #include "fsk_ctx.h"
@@ -364,6 +365,15 @@ __global__ void __launch_bounds__(kSearchBlock, FSK_SEARCH_MINB)
         const int64_t q = (int64_t)bone * n + j;
         store_solve(out, q, x0, x1, x2, Ji, err2, s);
         count_work(stats, s);
+#ifdef FSK_ESC_REASONS  // study builds: per-rule escalation counts (slot 8+bit: fired; 20+bit: fired alone)
+        if (stats && s.reasons) {
+            for (int bit = 0; bit < 12; ++bit)
+                if (s.reasons >> bit & 1u) {
+                    atomicAdd(stats + 8 + bit, 1ull);
+                    if (__popc(s.reasons) == 1) atomicAdd(stats + 20 + bit, 1ull);
+                }
+        }
+#endif
         if (esc_q) {
             // Capped (long) trajectories are queued from the front, the rest from the back, so
             // the escalation pass starts the long float64 solves first and the short ones fill
@@ -1063,7 +1073,9 @@ SearchState run_search(fsk_ctx* ctx, GridPlanes& P, const GridP& g, const float*
                    "occupancy");
         const unsigned egrid = (unsigned)(ctx->sm_count * std::max(per_sm, 1));
         // start states of up to st_cap escalated solves (~5 % escalate; the rest start in-kernel)
-        const int st_cap = (int)std::min<int64_t>(S, std::max<int64_t>(1 << 16, S / 8));
+        int st_cap = (int)std::min<int64_t>(S, std::max<int64_t>(1 << 16, S / 8));
+        if (const char* e = getenv("FSK_ESC_START_CAP"))  // testing override (exercises the in-kernel starts)
+            st_cap = std::max(1, std::min(st_cap, atoi(e)));
         double2* est = esc && exact_esc ? (double2*)scratch(ctx, kEscState, (size_t)st_cap * 8 * sizeof(double2))
                                         : nullptr;
         if (esc && exact_esc) {

@@ -145,7 +145,7 @@ def test_mixed_escalations_are_the_oracle_bitwise(deformer, dims, seed, points):
 
 
 @pytest.mark.parametrize("n_bones", [21, 80])
-def test_mixed_escalations_bitwise_other_bone_counts(deformer, n_bones):
+def test_mixed_escalations_bitwise_other_bone_counts(deformer, n_bones, monkeypatch):
     """The escalation start kernel's one-pass J~0 (weight gradients parked in shared memory) has a
     scalar-weight path for n_b % 4 != 0 (21 bones) and falls back to the two-pass form when the
     stash does not fit in shared memory (80 bones: 80·3 doubles × 128 threads > 227 KB). Both must
@@ -158,9 +158,11 @@ def test_mixed_escalations_bitwise_other_bone_counts(deformer, n_bones):
     (DESIGN.md §precision), plus float32 rounding at coordinates of ~50 m (measured: 2.3·conv_eps at
     80 bones). So the bar here is max(1e-4, 3·conv_eps) — positions within the solver's own stopping
     tolerance; the escalated solves themselves are checked bit for bit."""
-    # 80 bones × 8000 points: ~15 % of the 640 k solves escalate, more than the 80 k start states
-    # k_esc_start precomputes (an eighth of the solves), so the refill kernel's own start path runs too
+    # 80 bones: the start states k_esc_start precomputes are capped below the escalation count
+    # (FSK_ESC_START_CAP, a testing override), so the refill kernel's own start path runs too
     n = 8_000 if n_bones == 80 else 4_000
+    if n_bones == 80:
+        monkeypatch.setenv("FSK_ESC_START_CAP", "20000")
     sc = S.make_scene((32, 32, 32), n, seed=3, skeleton=S.chain_skeleton(n_bones))
     w, B, x = dev(sc.weights), dev(sc.bones), dev(sc.points)
     tg64 = torch.empty((w.shape[0], 12), dtype=torch.float64, device="cuda")
@@ -181,7 +183,7 @@ def test_mixed_escalations_bitwise_other_bone_counts(deformer, n_bones):
           f"max|dx| {dx:.2e} (conv_eps {conv:.2e})")
     assert n_esc > 0
     if n_bones == 80:
-        assert n_esc > max(65536, n * n_bones // 8)  # the in-kernel start path ran
+        assert n_esc > 20000  # the in-kernel start path ran
     assert same.sum() >= n_esc
     assert (g["converged"] == r["converged"]).mean() >= 0.9999
     assert dx <= max(1e-4, 3 * conv)
