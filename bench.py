@@ -39,7 +39,7 @@ GATHER_BYTES = 384  # 8 corners x 48 B of transform grid per d(x) evaluation
 # dram__bytes_read.sum + dram__bytes_write.sum of one k_search_fast launch (C2), from the
 # ncu --set full capture profiles/r01_final_search.ncu-rep (6.8 MB read + 205.0 MB written:
 # the bone-major search planes; the gather itself is L1/L2-resident)
-NCU_TRAFFIC_K2 = 7.6672e6 + 204.605952e6  # dram read + write per k_search_fast launch, profiles/r01_final_search.ncu-rep
+NCU_TRAFFIC_K2 = 7.091456e6 + 180.12288e6  # dram read + write per k_search_fast launch, profiles/r01_final_search.ncu-rep
 
 
 def parse():
