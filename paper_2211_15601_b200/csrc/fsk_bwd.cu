@@ -100,9 +100,9 @@ __device__ __forceinline__ double fixed_scale(unsigned int maxbits, int64_t n) {
 // 2. exclusive scan of the counts → bucket starts.
 // 3. k_bwd_bucket_fill: roots written into their cell's bucket as {x*, u} (order inside a
 //    bucket is arbitrary — the sums below are integer and therefore order-independent).
-// 4. k_bwd_gather_fixed: one thread per grid vertex sums, over the ≤ 8 cells it is a corner
-//    of, every bucketed root's fixed-point term φ_c·u_r·x̃_col·scale in int64 registers, and
-//    writes dL/dT[v] once. Bitwise reproducible, identical to the scattered fixed-point sum.
+// 4. k_bwd_chunk_reduce: per warp of 32 bucketed roots, per-cell runs of fixed-point terms
+//    φ_c·u_r·x̃_col·scale summed in int64 registers and flushed with integer atomics.
+//    Bitwise reproducible, identical to the scattered fixed-point sum.
 struct BwdRec {
     float x[3];
     float u[3];
@@ -144,45 +144,75 @@ __global__ void __launch_bounds__(256) k_bwd_bucket_fill(RootRef R, const float*
     rec[pos] = BwdRec{{xs[0], xs[1], xs[2]}, {u[0], u[1], u[2]}};
 }
 
-// One warp per non-empty cell: lane L owns the outputs o = L, L+32, L+64 of the cell's
-// 8 corners × 12 entries (o = 12·corner + entry) and sums their fixed-point terms over every
-// root in the cell's bucket (broadcast loads; no imbalance from dense cells beyond the warp);
-// the per-cell sums then go to the corner vertices with integer atomics — 96 per cell instead
-// of 96 per root, and integer addition keeps the result bitwise order-independent.
-__global__ void __launch_bounds__(256) k_bwd_cell_reduce(GridP g, const int64_t* __restrict__ start,
-                                                         const BwdRec* __restrict__ rec,
-                                                         const unsigned int* __restrict__ maxbits, int64_t n,
-                                                         unsigned long long* __restrict__ acc) {
+// One warp per 32 consecutive bucketed roots (the buckets are contiguous and cell-ordered, so a
+// warp's records form a few runs of equal cell): lane L loads record L, then the warp walks the
+// records in order with shuffles; lane L owns the outputs o = L, L+32, L+64 of the run's cell's
+// 8 corners × 12 entries (o = 12·corner + entry) and flushes the run's fixed-point sums to the
+// corner vertices with integer atomics at each cell change. Dense cells are split across warps
+// (no load imbalance); integer addition keeps the result bitwise order- and split-independent.
+__global__ void __launch_bounds__(256) k_bwd_chunk_reduce(GridP g, const int64_t* __restrict__ start,
+                                                          const BwdRec* __restrict__ rec,
+                                                          const unsigned int* __restrict__ maxbits, int64_t n,
+                                                          unsigned long long* __restrict__ acc) {
     const int64_t V = (int64_t)g.nx * g.ny * g.nz;
+    const int64_t M = start[V];  // bucketed roots
     const int lane = threadIdx.x & 31;
-    const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t r0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * 32;
+    if (r0 >= M) return;
+    const int cnt = (int)(M - r0 < 32 ? M - r0 : 32);
+    BwdRec b{};
+    Cell<float> c{};
+    int cell = -1;
+    if (lane < cnt) {
+        b = rec[r0 + lane];
+        c = locate<false>(g, b.x[0], b.x[1], b.x[2]);
+        cell = c.base;
+    }
     const double scale = fixed_scale(*maxbits, n);
     const int nxy = g.nx * g.ny;
-    for (int64_t cell = warp0; cell < V; cell += nwarps) {
-        const int64_t r0 = start[cell], r1 = start[cell + 1];
-        if (r0 == r1) continue;
-        long long s[3] = {0, 0, 0};
-        for (int64_t r = r0; r < r1; ++r) {
-            const BwdRec b = rec[r];
-            const Cell c = locate<false>(g, b.x[0], b.x[1], b.x[2]);  // c.base == cell
+    int q3[3], e3[3];
 #pragma unroll
-            for (int t = 0; t < 3; ++t) {
-                const int o = lane + 32 * t, q = o / 12, e = o - 12 * q;
-                const int di = q & 1, dj = (q >> 1) & 1, dk = q >> 2, row = e >> 2, col = e & 3;
-                const float phi = ((dk ? c.tz : 1.f - c.tz) * (dj ? c.ty : 1.f - c.ty)) * (di ? c.tx : 1.f - c.tx);
-                const double a = (double)phi * (double)b.u[row] * scale;
-                const double xc = col == 3 ? 1.0 : (double)b.x[col];
-                s[t] += __double2ll_rn(a * xc);
-            }
+    for (int t = 0; t < 3; ++t) {
+        const int o = lane + 32 * t;
+        q3[t] = o / 12;
+        e3[t] = o - 12 * q3[t];
+    }
+    auto flush = [&](int cl, const long long s[3]) {
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+            const int q = q3[t];
+            const int64_t v = cl + (q >> 2) * nxy + ((q >> 1) & 1) * g.nx + (q & 1);
+            if (s[t]) atomicAdd(acc + 12 * v + e3[t], (unsigned long long)s[t]);
+        }
+    };
+    long long s[3] = {0, 0, 0};
+    int cur = __shfl_sync(0xffffffffu, cell, 0);
+    for (int j = 0; j < cnt; ++j) {
+        const int cj = __shfl_sync(0xffffffffu, cell, j);
+        if (cj != cur) {  // warp-uniform
+            flush(cur, s);
+            s[0] = s[1] = s[2] = 0;
+            cur = cj;
+        }
+        const float tx = __shfl_sync(0xffffffffu, c.tx, j), ty = __shfl_sync(0xffffffffu, c.ty, j),
+                    tz = __shfl_sync(0xffffffffu, c.tz, j);
+        float x[3], u[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            x[k] = __shfl_sync(0xffffffffu, b.x[k], j);
+            u[k] = __shfl_sync(0xffffffffu, b.u[k], j);
         }
 #pragma unroll
         for (int t = 0; t < 3; ++t) {
-            const int o = lane + 32 * t, q = o / 12, e = o - 12 * q;
-            const int64_t v = cell + (q >> 2) * nxy + ((q >> 1) & 1) * g.nx + (q & 1);
-            if (s[t]) atomicAdd(acc + 12 * v + e, (unsigned long long)s[t]);
+            const int q = q3[t], e = e3[t];
+            const int di = q & 1, dj = (q >> 1) & 1, dk = q >> 2, row = e >> 2, col = e & 3;
+            const float phi = ((dk ? tz : 1.f - tz) * (dj ? ty : 1.f - ty)) * (di ? tx : 1.f - tx);
+            const double a = (double)phi * (double)u[row] * scale;
+            const double xc = col == 3 ? 1.0 : (double)x[col];
+            s[t] += __double2ll_rn(a * xc);
         }
     }
+    flush(cur, s);
 }
 
 __global__ void k_bwd_fixed_to_float(const long long* __restrict__ acc, int64_t m,
@@ -252,8 +282,7 @@ void run_bwd(fsk_ctx* ctx, const GridP& g, const RootRef& R, const float* grad_x
     scan_i32_to_i64(ctx, cnt, V, start, st);
     if (n > 0) {
         FSK_LAUNCH(ctx, st, k_bwd_bucket_fill, blocks_for(n, 256), 256, 0, R, grad_xc, n, cell_of, start, fill, rec);
-        FSK_LAUNCH(ctx, st, k_bwd_cell_reduce, std::min(blocks_for(32 * V, 256), cap_blocks * 2), 256, 0, g, start, rec,
-                   mx, n, acc);
+        FSK_LAUNCH(ctx, st, k_bwd_chunk_reduce, blocks_for(n, 256), 256, 0, g, start, rec, mx, n, acc);
     }
     FSK_LAUNCH(ctx, st, k_bwd_fixed_to_float, std::min(blocks_for(12 * V, 256), cap_blocks), 256, 0,
                reinterpret_cast<const long long*>(acc), 12 * V, mx, n, grad_tgrid);
