@@ -359,12 +359,22 @@ __global__ void __launch_bounds__(kSearchBlock, FSK_SEARCH_MINB)
     if (j >= n) return;
     const float4 xq = __ldg(xs + j);
     const int b_end = min(g.nb, (grp + 1) * bpg);
+#ifndef FSK_PER_SOLVE_STATS
+    unsigned w_solves = 0, w_iters = 0, w_fin = 0, w_fills = 0;  // work counters, flushed once per thread
+#endif
     for (int bone = grp * bpg; bone < b_end; ++bone) {
         float x0, x1, x2, Ji[9], err2;
         const SolveOut s = solve_one<float, true>(P, g, bones + 12 * bone, xq.x, xq.y, xq.z, o, x0, x1, x2, Ji, err2);
         const int64_t q = (int64_t)bone * n + j;
         store_solve(out, q, x0, x1, x2, Ji, err2, s);
+#ifdef FSK_PER_SOLVE_STATS
         count_work(stats, s);
+#else
+        w_solves += 1;
+        w_iters += s.iters;
+        w_fin += (s.conv && s.iters > 0);
+        w_fills += s.fills;
+#endif
 #ifdef FSK_ESC_REASONS  // study builds: per-rule escalation counts (slot 8+bit: fired; 20+bit: fired alone)
         if (stats && s.reasons) {
             for (int bit = 0; bit < 12; ++bit)
@@ -393,6 +403,23 @@ __global__ void __launch_bounds__(kSearchBlock, FSK_SEARCH_MINB)
             else if (s.esc) esc_q[esc_cap - 1 - (bs + __popc(ms & lt))] = rec;
         }
     }
+#ifndef FSK_PER_SOLVE_STATS
+    // one warp-aggregated flush of the thread's counters (per solve, 4 same-address atomics per warp
+    // were ~600 k L2 atomics per C2 launch)
+    if (stats) {
+        const unsigned act = __activemask();
+        w_solves = __reduce_add_sync(act, w_solves);
+        w_iters = __reduce_add_sync(act, w_iters);
+        w_fin = __reduce_add_sync(act, w_fin);
+        w_fills = __reduce_add_sync(act, w_fills);
+        if ((threadIdx.x & 31) == __ffs(act) - 1) {
+            atomicAdd(stats + 0, (unsigned long long)w_solves);
+            atomicAdd(stats + 1, (unsigned long long)w_iters);
+            atomicAdd(stats + 2, (unsigned long long)w_fin);
+            if (w_fills) atomicAdd(stats + 6, (unsigned long long)w_fills);
+        }
+    }
+#endif
 }
 
 // Escalation pass: the flagged solves from scratch in float64 (persistent warps over the
