@@ -42,10 +42,10 @@ CPU oracle (f64, {c2['cpu_baseline']['cores']} host threads): {c2['cpu_baseline'
 
 ## What changed during the round's last part (each output bitwise-identical, except the rule change)
 
-* `k_search_fast` 0.633 → 0.561 ms live: tile-major blocks (one CTA solves 8 bone inits of the same 128
+* `k_search_fast` 0.633 → 0.549 ms live: tile-major blocks (one CTA solves 8 bone inits of the same 128
   sorted queries back to back): L1 hit 63.6 % → 77.9 %, issue busy 46.5 % → 51.9 %, long-scoreboard
   stalls 38 % → 30 %; J~/meta stored with streaming hints, x/residual with L2 evict-last (DRAM writes
-  205 → 180 MB per launch).
+  205 → 180 MB per launch); work counters flushed once per thread instead of 4 atomics per warp per solve.
 * `k_esc_start` 0.107 → 0.093 ms: one pass over the weight grid (∇w parked in shared memory), 2 CTAs/SM.
 * `k_search_escalated<exact>` 0.302 → 0.259 ms: 254 registers at 2 CTAs/SM instead of 168 with
   loop-carried spills (the hottest instruction of the old capture was a local-memory reload at the loop
