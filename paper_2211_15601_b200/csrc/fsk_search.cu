@@ -534,6 +534,13 @@ __global__ void __launch_bounds__(kEscBlock, kExact ? FSK_ESC_EXACT_MINB : FSK_E
     const int cnt_long = esc_count[3], cnt = esc_count[3] + esc_count[2];
     const double* bones64 = kExact ? stage_bones64(bones, g.nb) : nullptr;
     int* work = const_cast<int*>(esc_count) + 1;
+#ifdef FSK_ESC_TIMELINE  // probe builds: kernel start, queue-dry and exit times (globaltimer, ns)
+    if (threadIdx.x == 0 && stats) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        atomicMax(stats + 24, ~t);  // kernel start (min as max of ~t)
+    }
+#endif
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const double conv2 = o.conv2, div2 = o.div2;
@@ -569,7 +576,17 @@ __global__ void __launch_bounds__(kEscBlock, kExact ? FSK_ESC_EXACT_MINB : FSK_E
             const int idx = __shfl_sync(full, buf_idx, min(bused + rank, 31));
             const bool got = take && idx < cnt;
             bused += __popc(__ballot_sync(full, take));
-            if (__any_sync(full, take && !got)) dry = true;  // queue exhausted
+            if (__any_sync(full, take && !got)) {  // queue exhausted
+#ifdef FSK_ESC_TIMELINE
+                if (!dry && lane == 0 && stats) {
+                    unsigned long long t;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                    atomicMax(stats + 25, ~t);  // first warp to find the queue dry (min as max of ~t)
+                    atomicMax(stats + 26, t);  // last warp to find it dry
+                }
+#endif
+                dry = true;
+            }
             if (got) {  // start of the solve (correspondence.cpp:135-137, :43-54)
                 const int4 rec = esc_q[idx < cnt_long ? idx : esc_cap - 1 - (idx - cnt_long)];
                 q = rec.x;
@@ -634,6 +651,13 @@ __global__ void __launch_bounds__(kEscBlock, kExact ? FSK_ESC_EXACT_MINB : FSK_E
             }
         }
     }
+#ifdef FSK_ESC_TIMELINE
+    if (lane == 0 && stats) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        atomicMax(stats + 27, t);  // last warp exit
+    }
+#endif
     if (stats) {
         n_solves = __reduce_add_sync(full, n_solves);
         n_iters = __reduce_add_sync(full, n_iters);
