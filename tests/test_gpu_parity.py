@@ -343,6 +343,14 @@ def test_device_correspondence_sets_match_dense_path(deformer, c1):
     np.testing.assert_array_equal(r[:, 4:13], d["jinv"][keep[:, 0], keep[:, 1]].reshape(-1, 9))
     np.testing.assert_array_equal(r[:, 13].view(np.int32), keep[:, 1])
     np.testing.assert_array_equal(r[:, 14].view(np.int32), d["iters"][keep[:, 0], keep[:, 1]])
+    # fsk_deform runs the spatial sort on a side stream beside K1; without the sort (identity order,
+    # K1 on the caller's stream) the CorrespondenceSets and the transform grid are the same bits
+    o.sort = False
+    tg3 = torch.empty_like(tg)
+    offs3, roots3 = (t.cpu().numpy() for t in deformer.deform(w, c1.dims, c1.bbox, B, x, o, tgrid=tg3))
+    np.testing.assert_array_equal(tg3.cpu().numpy(), tg.cpu().numpy())
+    np.testing.assert_array_equal(offs3, offs2)
+    np.testing.assert_array_equal(roots3[:total], roots2[:total])
 
 
 def test_backward_from_compact_roots_matches_dense(deformer, c3):
