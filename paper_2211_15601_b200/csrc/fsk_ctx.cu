@@ -140,10 +140,16 @@ SearchP make_search(const fsk_search_opts* o) {
     s.esc_rho2 = 0.7f * 0.7f;
     s.esc_tau2 = 2.0f * 2.0f;
     s.esc_conv_band_last = false;
+    // Converged on the cap iteration with a last step > tau·conv: as chaotic as a capped trajectory.
+    // Band study on seeds 52-81 (108 M solves): without it one root 1.6e-4 from the oracle's (float32
+    // stopped at iteration 8 with err 0.52·conv, float64 needed 9); with it max |dx| 8.7e-5.
+    // Escalation on C2 4.25 % -> 5.15 %.
+    s.esc_capconv = 2;
 #ifdef FSK_ESC_STUDY  // rule-study builds only: overrides from the environment
     if (const char* v = getenv("FSK_ESC_CONV_BAND_LAST")) s.esc_conv_band_last = atoi(v) != 0;
     if (const char* v = getenv("FSK_ESC_MIN_DIV")) s.esc_min_div = atoi(v);
     if (const char* v = getenv("FSK_ESC_COS")) s.esc_cos2 = (float)(atof(v) * atof(v));
+    if (const char* v = getenv("FSK_ESC_CAPCONV")) s.esc_capconv = atoi(v);
 #endif
     return s;
 }
@@ -306,15 +312,15 @@ int fsk_ctx_prof_read(fsk_ctx* ctx, const char* name, double* total_ms, int64_t*
 }
 
 #ifdef FSK_ESC_REASONS
-// study builds only (scripts/esc_reasons.py): per-rule escalation counters, slots 8..31
-extern "C" int fsk_ctx_esc_reasons(fsk_ctx* ctx, uint64_t out[24], int reset) {
+// study builds only (scripts/esc_reasons.py, esc_timeline.py): debug counters, slots 8..47
+extern "C" int fsk_ctx_esc_reasons(fsk_ctx* ctx, uint64_t out[40], int reset) {
     return guard([&] {
         set_device(ctx);
         cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
         unsigned long long h[fsk_ctx::kStatSlots];
         cuda_check(cudaMemcpy(h, ctx->stats, sizeof(h), cudaMemcpyDeviceToHost), "cudaMemcpy");
-        for (int i = 0; i < 24; ++i) out[i] = h[8 + i];
-        if (reset) cuda_check(cudaMemset(ctx->stats + 8, 0, 24 * sizeof(unsigned long long)), "cudaMemset");
+        for (int i = 0; i < 40; ++i) out[i] = h[8 + i];
+        if (reset) cuda_check(cudaMemset(ctx->stats + 8, 0, 40 * sizeof(unsigned long long)), "cudaMemset");
     });
 }
 #endif

@@ -35,7 +35,7 @@ struct fsk_ctx {
     std::vector<cudaEvent_t> pool;
     // search work counters [solves32, iters32, final32, solves64, iters64, final64, fills32, -],
     // then (FSK_ESC_REASONS study builds) per-rule escalation counters
-    static constexpr int kStatSlots = 32;
+    static constexpr int kStatSlots = 48;
     unsigned long long* stats = nullptr;
     // device→host copy stream of the host-buffer entry point (created on first use)
     cudaStream_t copy = nullptr;

@@ -56,6 +56,7 @@ struct SearchP {
     float esc_rho2;     // step rule: the stop decision is "near" when err² ∈ [rho², 1/rho²]·conv² ...
     float esc_tau2;     // ... and the step it decides (taken or not) is longer than tau·conv
     bool esc_conv_band_last;  // apply the ±conv band only where a conv decision can flip the mask (the last iteration)
+    int esc_capconv;    // converged exactly at the float32 cap iteration: 0 keep, 1 escalate, 2 escalate if the last step > tau·conv
 };
 
 template <typename R>
@@ -519,6 +520,11 @@ __device__ __forceinline__ SolveOut solve_one(const Planes<R>& P, const GridP& g
         if (iters > 0 && e2l * (R)o.esc_rho2 <= conv2) {
             const R d0 = x0 - xl0, d1 = x1 - xl1, d2 = x2 - xl2;
             if (d0 * d0 + d1 * d1 + d2 * d2 > tau2) esc = true, FSK_REASON(9);
+        }
+        if (o.esc_capconv && iters >= o.esc_cap && o.esc_cap < o.max_iters) {
+            // converged on the cap iteration: as long as a capped trajectory
+            const R d0 = x0 - xl0, d1 = x1 - xl1, d2 = x2 - xl2;
+            if (o.esc_capconv == 1 || d0 * d0 + d1 * d1 + d2 * d2 > tau2) esc = true, FSK_REASON(12);
         }
     }
     return SolveOut{iters, conv, esc, capped, fills, reasons};

@@ -375,12 +375,12 @@ __global__ void __launch_bounds__(kSearchBlock, FSK_SEARCH_MINB)
         w_fin += (s.conv && s.iters > 0);
         w_fills += s.fills;
 #endif
-#ifdef FSK_ESC_REASONS  // study builds: per-rule escalation counts (slot 8+bit: fired; 20+bit: fired alone)
+#ifdef FSK_ESC_REASONS  // study builds: per-rule escalation counts (slot 8+bit: fired; 24+bit: fired alone)
         if (stats && s.reasons) {
-            for (int bit = 0; bit < 12; ++bit)
+            for (int bit = 0; bit < 13; ++bit)
                 if (s.reasons >> bit & 1u) {
                     atomicAdd(stats + 8 + bit, 1ull);
-                    if (__popc(s.reasons) == 1) atomicAdd(stats + 20 + bit, 1ull);
+                    if (__popc(s.reasons) == 1) atomicAdd(stats + 24 + bit, 1ull);
                 }
         }
 #endif
@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(kEscBlock, kExact ? FSK_ESC_EXACT_MINB : FSK_E
     if (threadIdx.x == 0 && stats) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        atomicMax(stats + 24, ~t);  // kernel start (min as max of ~t)
+        atomicMax(stats + 40, ~t);  // kernel start (min as max of ~t)
     }
 #endif
     const unsigned full = 0xffffffffu;
@@ -581,8 +581,8 @@ __global__ void __launch_bounds__(kEscBlock, kExact ? FSK_ESC_EXACT_MINB : FSK_E
                 if (!dry && lane == 0 && stats) {
                     unsigned long long t;
                     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-                    atomicMax(stats + 25, ~t);  // first warp to find the queue dry (min as max of ~t)
-                    atomicMax(stats + 26, t);  // last warp to find it dry
+                    atomicMax(stats + 41, ~t);  // first warp to find the queue dry (min as max of ~t)
+                    atomicMax(stats + 42, t);  // last warp to find it dry
                 }
 #endif
                 dry = true;
@@ -655,7 +655,7 @@ __global__ void __launch_bounds__(kEscBlock, kExact ? FSK_ESC_EXACT_MINB : FSK_E
     if (lane == 0 && stats) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        atomicMax(stats + 27, t);  // last warp exit
+        atomicMax(stats + 43, t);  // last warp exit
     }
 #endif
     if (stats) {

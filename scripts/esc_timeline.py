@@ -18,13 +18,12 @@ o = sc.search_options(50)
 w, B, x = (torch.from_numpy(a).cuda() for a in (sc.weights, sc.bones, sc.points))
 so = SearchOptions(50, o["conv_eps"], o["div_eps"], o["dedup_dist"])
 for rep in range(3):
-    buf = (ctypes.c_uint64 * 24)()
+    buf = (ctypes.c_uint64 * 40)()
     f(D._ctx, buf, 1)
-    # slots 24..29 = buf[16..21]; min slots must start high
     D.deform(w, sc.dims, sc.bbox, B, x, so)
     torch.cuda.synchronize()
     f(D._ctx, buf, 1)
-    t0, dry0, dry1, tend = (buf[16 + i] for i in range(4))
+    t0, dry0, dry1, tend = (buf[32 + i] for i in range(4))
     t0, dry0 = (~t0) & (2**64 - 1), (~dry0) & (2**64 - 1)
     print(f"rep {rep}: queue dry after {(dry0 - t0) / 1e3:.1f} us (last warp to notice +{(dry1 - t0) / 1e3:.1f}), "
           f"last warp exit +{(tend - t0) / 1e3:.1f} us")
