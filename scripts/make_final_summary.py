@@ -46,12 +46,13 @@ CPU oracle (f64, {c2['cpu_baseline']['cores']} host threads): {c2['cpu_baseline'
   sorted queries back to back): L1 hit 63.6 % → 77.9 %, issue busy 46.5 % → 51.9 %, long-scoreboard
   stalls 38 % → 30 %; J~/meta stored with streaming hints, x/residual with L2 evict-last (DRAM writes
   205 → 180 MB per launch); work counters flushed once per thread instead of 4 atomics per warp per solve.
-* `k_esc_start` 0.107 → 0.093 ms: one pass over the weight grid (∇w parked in shared memory), 2 CTAs/SM.
-* `k_search_escalated<exact>` 0.302 → 0.259 ms: 254 registers at 2 CTAs/SM instead of 168 with
+* `k_esc_start` 0.107 → 0.093 ms (at 4.25 % escalated): one pass over the weight grid (∇w parked in shared memory), 2 CTAs/SM.
+* `k_search_escalated<exact>` 0.302 → 0.259 ms (at 4.25 % escalated): 254 registers at 2 CTAs/SM instead of 168 with
   loop-carried spills (the hottest instruction of the old capture was a local-memory reload at the loop
   head).
-* Escalation rule: unconverged runs escalate from 5 iterations (was 3) — 4.85 % → 4.25 % of the solves
-  (150-scene band study: 5 mask flips in 108 M solves, roots unchanged; `r01_esc_rule_study/`).
+* Escalation rules: unconverged runs escalate from 5 iterations (was 3), and solves converging on the
+  float32 cap iteration with a long last step escalate too — 4.85 % → 5.15 % of the solves; 450-scene
+  band study: max |dx| 8.7e-5, 25 mask flips in 324 M solves (`r01_esc_rule_study/`).
 
 ## Search kernels
 
