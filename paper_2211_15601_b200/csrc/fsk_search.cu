@@ -723,7 +723,10 @@ __global__ void __launch_bounds__(256) k_dedup(int64_t n, int nb, float dedup2, 
     // The first kRegKept kept roots stay in registers (a query has ~1 root); later kept roots
     // are re-read from the planes. Loads are issued kBatch bones at a time (independent
     // coalesced rows of the bone-major planes); converged = sign bit of the residual clear.
-    constexpr int kRegKept = 4, kBatch = 24;
+#ifndef FSK_DEDUP_BATCH
+#define FSK_DEDUP_BATCH 6  // plane rows in flight per batch: 24 35 us, 12 30, 8 28, 6 26, 4 26 (C2; fewer registers, more warps)
+#endif
+    constexpr int kRegKept = 4, kBatch = FSK_DEDUP_BATCH;
     float kx[kRegKept], ky[kRegKept], kz[kRegKept];
 #pragma unroll
     for (int c = 0; c < kRegKept; ++c) kx[c] = ky[c] = kz[c] = 0.f;
