@@ -52,7 +52,7 @@ namespace fsk {
 enum Slot {
     kHist, kBbox, kKeys, kPerm, kXs, kScanPart, kBwdAcc, kBwdMax, kPlanes, kPlanes64, kEscQ, kEscN, kEscState,
     kBwdStart, kBwdCell, kBwdRec, kPeakTable,
-    kOXr, kOJa, kOJb, kOJc, kOMeta, kOKeep, kNRoots, kOffs, kRootsTmp,
+    kOXr, kOJa, kOJb, kOJc, kOMeta, kOKeep, kOKeepMask, kNRoots, kOffs, kRootsTmp,
     kHW, kHB, kHP, kHT, kHOffs, kHRoots, kFB, kFP, kFOffs, kFRoots,
     kMlpPack, kMlpWidths, kMlpOcc, kMlpAct, kMlpD0, kMlpD1, kMlpOnes,
     kMvPos, kMvPosNext, kMvW, kMvX, kMvG, kMvJ, kMvDx, kMvK, kMvAct, kMvActNext, kMvCnt,

@@ -276,6 +276,7 @@ struct SearchPlanes {
     float* jc;       // J~[8]
     uint16_t* meta;  // iterations | converged << 8
     uint8_t* keep;   // dedup survivors
+    uint32_t* kmask = nullptr;  // per sorted query: bit b = bone b's root kept (n_b <= 32), for k_emit
 };
 
 #ifndef FSK_SEARCH_BLOCK
@@ -731,6 +732,7 @@ __global__ void __launch_bounds__(256) k_dedup(int64_t n, int nb, float dedup2, 
 #pragma unroll
     for (int c = 0; c < kRegKept; ++c) kx[c] = ky[c] = kz[c] = 0.f;
     int count = 0;
+    uint32_t kept = 0;  // bit b: bone b's root kept (used when n_b <= 32)
     for (int b0 = 0; b0 < nb; b0 += kBatch) {
         float4 xv[kBatch];
 #pragma unroll
@@ -770,9 +772,11 @@ __global__ void __launch_bounds__(256) k_dedup(int64_t n, int nb, float dedup2, 
                 }
             }
             sp.keep[(int64_t)b * n + j] = (uint8_t)k;
+            kept |= (uint32_t)k << (b & 31);
             count += k;
         }
     }
+    if (sp.kmask) sp.kmask[j] = kept;
     n_roots_p[perm[j]] = count;
 }
 
@@ -873,6 +877,19 @@ __global__ void __launch_bounds__(256) k_emit(int64_t n, int nb, SearchPlanes sp
     const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (j >= n) return;
     int64_t o = offs[perm[j]];
+    if (sp.kmask) {  // the kept bones straight from dedup's mask (≈ 1 per query) instead of n_b keep bytes
+        for (uint32_t m = sp.kmask[j]; m; m &= m - 1) {
+            const int b = __ffs(m) - 1;
+            const int64_t q = (int64_t)b * n + j;
+            if (o < cap) {
+                float4 xr = sp.xr[q];
+                xr.w = fabsf(xr.w);
+                store_root(roots + o, xr, sp.ja[q], sp.jb[q], sp.jc[q], b, sp.meta[q] & 0xff);
+            }
+            ++o;
+        }
+        return;
+    }
     for (int b = 0; b < nb; ++b) {
         const int64_t q = (int64_t)b * n + j;
         if (!sp.keep[q]) continue;
@@ -1059,6 +1076,7 @@ SearchState run_search(fsk_ctx* ctx, GridPlanes& P, const GridP& g, const float*
     s.sp.jc = (float*)scratch(ctx, kOJc, S * sizeof(float));
     s.sp.meta = (uint16_t*)scratch(ctx, kOMeta, S * sizeof(uint16_t));
     s.sp.keep = (uint8_t*)scratch(ctx, kOKeep, S);
+    s.sp.kmask = g.nb <= 32 ? (uint32_t*)scratch(ctx, kOKeepMask, std::max<int64_t>(1, n) * sizeof(uint32_t)) : nullptr;
     s.perm = (int*)scratch(ctx, kPerm, std::max<int64_t>(1, n) * sizeof(int));
     s.n_roots_p = (int32_t*)scratch(ctx, kNRoots, std::max<int64_t>(1, n) * sizeof(int32_t));
     if (n == 0) {
