@@ -23,8 +23,9 @@ for seed in seeds:
     for dims in GRIDS:
         pts = ["uniform", "training"][seed % 2]
         sc = S.make_scene(dims, n, seed=seed, points=pts)
-        o = sc.search_options(50)
-        _, g = run_gpu(D, sc, 50, precision=os.environ.get("BAND_PRECISION", "mixed"))
+        MI = int(os.environ.get("BAND_MAX_ITERS", "50"))
+        o = sc.search_options(MI)
+        _, g = run_gpu(D, sc, MI, precision=os.environ.get("BAND_PRECISION", "mixed"))
         r = oracle.batch_search(sc.weights, sc.dims, sc.bbox, sc.bones, sc.points, workers=os.cpu_count(), **o)
         both = (g["converged"] == 1) & (r["converged"] == 1)
         rg = g["resid"] / o["conv_eps"]
