@@ -48,14 +48,14 @@ typedef struct fsk_ctx fsk_ctx;
 typedef struct fsk_grid_desc {
     int32_t nx, ny, nz;   /* >= 2 per axis (skinning.cpp:62-64) */
     int32_t n_bones;      /* n_b of the weight grid */
-    float bbox_min[3];
-    float bbox_max[3];
+    double bbox_min[3];   /* the reference's float64 Aabb (geometry.hpp:14-39); the float32 pass */
+    double bbox_max[3];   /* rounds it, the float64 re-solves use it as given */
 } fsk_grid_desc;
 
 /* SearchOptions (correspondence.hpp:14-26); fill from fsk_search_opts_defaults()
  * = SearchOptions::defaults_for(bbox) (correspondence.cpp:10-17). */
 typedef struct fsk_search_opts {
-    int32_t max_iters;    /* >= 1, <= 255 */
+    int32_t max_iters;    /* >= 1 (correspondence.cpp:20) */
     int32_t flags;        /* FSK_SEARCH_* */
     double conv_eps;      /* > 0 */
     double div_eps;       /* > conv_eps */
@@ -86,7 +86,7 @@ typedef struct fsk_search_out {
     float* x_c;           /* [N][n_b][3] canonical root (Root::x) */
     float* jinv;          /* [N][n_b][9] Broyden inverse-Jacobian estimate (Root::inv_jacobian) */
     float* resid;         /* [N][n_b] ||d(x)-x'|| at termination (Root::residual) */
-    uint8_t* iters;       /* [N][n_b] iterations executed (Root::iterations) */
+    int32_t* iters;       /* [N][n_b] iterations executed (Root::iterations) */
     uint8_t* converged;   /* [N][n_b] 1 iff residual < conv_eps was reached */
     uint8_t* keep;        /* [N][n_b] dedup survivors */
     int32_t* n_roots;     /* [N] kept roots per point */
@@ -212,6 +212,15 @@ int fsk_eval_points(fsk_ctx* ctx, const float* tgrid, const fsk_grid_desc* desc,
 int fsk_init_states(fsk_ctx* ctx, const float* tgrid, const fsk_grid_desc* desc, const float* bones,
                     int32_t n_bones_pose, const float* points, int64_t n, float* x0, float* jinv0,
                     void* stream);
+
+/* init_states in float64, in the reference's own operation order (the exact replay's start,
+ * DESIGN §precision): x0 = B_i^-1 x' (geometry.hpp:51-61) and jinv0 = J(x0)^-1 or I, J from the
+ * n_b-wide weight grid (deformer.cpp:117-136, correspondence.cpp:43-54) — bit-identical to the
+ * oracle's init_states. weights [V][n_b] float32, bones float32, points [N][3] float64; outputs
+ * float64 point-major [N][n_b][3] / [N][n_b][9], either may be NULL. All dev. */
+int fsk_init_states64(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* desc, const float* bones,
+                      int32_t n_bones_pose, const double* points, int64_t n, double* x0, double* jinv0,
+                      void* stream);
 
 /* ---- K3: implicit-differentiation backward (diff.cpp:43-51, :336-359), grid-routed.
  * For each point p with root_sel[p] >= 0 (init index into the dense result), with

@@ -31,13 +31,13 @@ EXPORTS = [
     "fsk_multi_create", "fsk_multi_destroy", "fsk_multi_device_count", "fsk_multi_deform_host",
     "fsk_multi_grad_weights_host", "fsk_search_fwd_mlp",
     "fsk_io_last_error", "fsk_sknv_read", "fsk_sknv_write", "fsk_points_bin_read", "fsk_points_bin_write",
-    "fsk_write_correspondence_dump", "fsk_deform_files",
+    "fsk_write_correspondence_dump", "fsk_deform_files", "fsk_init_states64",
 ]
 
 
 class GridDesc(ctypes.Structure):
     _fields_ = [("nx", ctypes.c_int32), ("ny", ctypes.c_int32), ("nz", ctypes.c_int32),
-                ("n_bones", ctypes.c_int32), ("bbox_min", ctypes.c_float * 3), ("bbox_max", ctypes.c_float * 3)]
+                ("n_bones", ctypes.c_int32), ("bbox_min", ctypes.c_double * 3), ("bbox_max", ctypes.c_double * 3)]
 
 
 class SearchOpts(ctypes.Structure):
@@ -94,6 +94,7 @@ def load():
     L.fsk_deform_host_frames.argtypes = [_vp, _vp, G, _i32, _vp, _i32, _vp, _vp, O, _vp, _vp, _vp, _vp, _vp]
     L.fsk_eval_points.argtypes = [_vp, _vp, G, _vp, _i64, _vp, _vp, _vp, _vp]
     L.fsk_init_states.argtypes = [_vp, _vp, G, _vp, _i32, _vp, _i64, _vp, _vp, _vp]
+    L.fsk_init_states64.argtypes = [_vp, _vp, G, _vp, _i32, _vp, _i64, _vp, _vp, _vp]
     L.fsk_search_bwd.argtypes = [_vp, G, _vp, _vp, _i32, _vp, _vp, _i64, _vp, ctypes.c_int, _vp]
     L.fsk_grad_weights.argtypes = [_vp, G, _vp, _vp, _i32, _vp, _vp]
     L.fsk_batch_search.argtypes = [_vp, _vp, _vp, _vp, G, _vp, _i32, _vp, _i64, O, _vp, _vp, _i64, _vp]

@@ -76,12 +76,14 @@ GridP make_grid(const fsk_grid_desc* d) {
     g.nb = d->n_bones;
     const int n[3] = {d->nx, d->ny, d->nz};
     for (int a = 0; a < 3; ++a) {
-        g.lo[a] = d->bbox_min[a];
-        g.hi[a] = d->bbox_max[a];
-        const float ext = g.hi[a] - g.lo[a];
-        if (!(ext > 0.f)) fail(FSK_EINVAL, "SkinningVoxelGrid: bbox must have positive extent");
+        // the reference's float64 Aabb as given (the exact replay and the float64 re-solves use it);
+        // the float32 pass works on its rounding
         g.lod[a] = d->bbox_min[a];
         g.hid[a] = d->bbox_max[a];
+        if (!(g.hid[a] - g.lod[a] > 0.0)) fail(FSK_EINVAL, "SkinningVoxelGrid: bbox must have positive extent");
+        g.lo[a] = (float)g.lod[a];
+        g.hi[a] = (float)g.hid[a];
+        if (!(g.hi[a] - g.lo[a] > 0.f)) fail(FSK_EINVAL, "fsk: bbox extent below float32 resolution");
         g.scaled[a] = (double)(n[a] - 1) / (g.hid[a] - g.lod[a]);  // skinning.cpp:109 in f64
         g.scale[a] = (float)g.scaled[a];
     }
@@ -95,7 +97,6 @@ SearchP make_search(const fsk_search_opts* o) {
     if (!(o->conv_eps > 0.0)) fail(FSK_EINVAL, "search: conv_eps must be > 0");
     if (!(o->div_eps > o->conv_eps)) fail(FSK_EINVAL, "search: div_eps must exceed conv_eps");
     if (!(o->dedup_dist >= 0.0)) fail(FSK_EINVAL, "search: dedup_dist must be >= 0");
-    if (o->max_iters > 255) fail(FSK_EINVAL, "fsk: max_iters must be <= 255 (uint8 iteration counts)");
     if ((o->flags & FSK_SEARCH_FP32_ONLY) && (o->flags & FSK_SEARCH_FP64))
         fail(FSK_EINVAL, "fsk: FSK_SEARCH_FP32_ONLY and FSK_SEARCH_FP64 are exclusive");
     SearchP s;
@@ -139,6 +140,11 @@ SearchP make_search(const fsk_search_opts* o) {
     // by one step, up to 4·conv): rho = 0.7, tau = 2 (a one-step difference stays < 2·conv).
     s.esc_rho2 = 0.7f * 0.7f;
     s.esc_tau2 = 2.0f * 2.0f;
+    // Absolute bar: the step rule bounds a one-step disagreement by tau·conv = 2·conv_eps, which is
+    // within the north star's 1e-4 only while conv_eps <= 5e-5 (SMPL scale: conv 3.4e-5). On larger
+    // scenes (conv_eps = 1e-5·diag, e.g. 40-80-bone chains of 50-100 m, where float32 also resolves
+    // coordinates only to ~4e-6) every converged float32 solve is re-solved by the float64 pass.
+    s.esc_conv_all = o->conv_eps > 5e-5;
     s.esc_conv_band_last = false;
     // Converged on the cap iteration with a last step > tau·conv: as chaotic as a capped trajectory.
     // Band study on seeds 52-81 (108 M solves): without it one root 1.6e-4 from the oracle's (float32

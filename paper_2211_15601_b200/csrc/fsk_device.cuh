@@ -57,6 +57,7 @@ struct SearchP {
     float esc_tau2;     // ... and the step it decides (taken or not) is longer than tau·conv
     bool esc_conv_band_last;  // apply the ±conv band only where a conv decision can flip the mask (the last iteration)
     int esc_capconv;    // converged exactly at the float32 cap iteration: 0 keep, 1 escalate, 2 escalate if the last step > tau·conv
+    bool esc_conv_all;  // every converged float32 solve escalates (scenes whose conv_eps is too coarse for 1e-4 abs)
 };
 
 template <typename R>
@@ -501,6 +502,7 @@ __device__ __forceinline__ SolveOut solve_one(const Planes<R>& P, const GridP& g
         if (kFast && !conv && k == limit && limit < o.max_iters && !(err2 > div2)) esc = capped = true, FSK_REASON(5);
         if (kFast && !conv && iters >= o.esc_min_div) esc = true, FSK_REASON(6);
     }
+    if (kFast && conv && o.esc_conv_all) esc = true, FSK_REASON(7);
     if (kFast && conv) {  // ill-conditioned root: float32 rounding is amplified into x*
         R m = 0;
 #pragma unroll

@@ -113,8 +113,11 @@ int fsk_sknv_write(const char* path, const fsk_grid_desc* desc, const float* wei
         out.write("SKNV", 4);
         const uint32_t h[5] = {1u, (uint32_t)desc->nx, (uint32_t)desc->ny, (uint32_t)desc->nz, (uint32_t)desc->n_bones};
         out.write(reinterpret_cast<const char*>(h), sizeof(h));
-        const float bb[6] = {desc->bbox_min[0], desc->bbox_min[1], desc->bbox_min[2],
-                             desc->bbox_max[0], desc->bbox_max[1], desc->bbox_max[2]};
+        float bb[6];  // SKNV stores the bbox in float32 (skinning.cpp:248-252)
+        for (int a = 0; a < 3; ++a) {
+            bb[a] = (float)desc->bbox_min[a];
+            bb[3 + a] = (float)desc->bbox_max[a];
+        }
         out.write(reinterpret_cast<const char*>(bb), sizeof(bb));
         const int64_t n = (int64_t)desc->nx * desc->ny * desc->nz * desc->n_bones;
         out.write(reinterpret_cast<const char*>(weights), (std::streamsize)(n * sizeof(float)));

@@ -773,7 +773,7 @@ int fsk_distill(fsk_ctx* ctx, const float* theta, const int32_t* widths, int32_t
         R.ny = desc->ny;
         const int n3[3] = {desc->nx, desc->ny, desc->nz};
         for (int a = 0; a < 3; ++a) {
-            R.lo[a] = desc->bbox_min[a];
+            R.lo[a] = (float)desc->bbox_min[a];
             R.h[a] = (float)(((double)desc->bbox_max[a] - (double)desc->bbox_min[a]) / (n3[a] - 1));
         }
         run_fwd(ctx, s, widths, n_widths, pk, R, weights, st);
@@ -835,7 +835,7 @@ int fsk_distill_bwd(fsk_ctx* ctx, const float* theta, const int32_t* widths, int
         R.ny = desc->ny;
         const int n3[3] = {desc->nx, desc->ny, desc->nz};
         for (int a = 0; a < 3; ++a) {
-            R.lo[a] = desc->bbox_min[a];
+            R.lo[a] = (float)desc->bbox_min[a];
             R.h[a] = (float)(((double)desc->bbox_max[a] - (double)desc->bbox_min[a]) / (n3[a] - 1));
         }
         run_fwd(ctx, s, widths, n_widths, pk, R, w, st, act);

@@ -274,7 +274,7 @@ struct SearchPlanes {
     float4* ja;      // J~[0..3]
     float4* jb;      // J~[4..7]
     float* jc;       // J~[8]
-    uint16_t* meta;  // iterations | converged << 8
+    uint32_t* meta;  // iterations | converged << 31 (any max_iters >= 1, correspondence.cpp:20)
     uint8_t* keep;   // dedup survivors
     uint32_t* kmask = nullptr;  // per sorted query: bit b = bone b's root kept (n_b <= 32), for k_emit
 };
@@ -297,7 +297,7 @@ __device__ __forceinline__ void store_solve(const SearchPlanes& out, int64_t q, 
     out.ja[q] = make_float4((float)Ji[0], (float)Ji[1], (float)Ji[2], (float)Ji[3]);
     out.jb[q] = make_float4((float)Ji[4], (float)Ji[5], (float)Ji[6], (float)Ji[7]);
     out.jc[q] = (float)Ji[8];
-    out.meta[q] = (uint16_t)(s.iters | (s.conv ? 0x100 : 0));
+    out.meta[q] = (uint32_t)s.iters | (s.conv ? 0x80000000u : 0u);
 #else
     // x / residual stay in L2 for dedup (read right after the search); J~ and meta are read only
     // for the ~1 kept root per query (emit), so they stream out (evict-first). Measured on C2:
@@ -312,7 +312,7 @@ __device__ __forceinline__ void store_solve(const SearchPlanes& out, int64_t q, 
     __stcs(out.ja + q, make_float4((float)Ji[0], (float)Ji[1], (float)Ji[2], (float)Ji[3]));
     __stcs(out.jb + q, make_float4((float)Ji[4], (float)Ji[5], (float)Ji[6], (float)Ji[7]));
     __stcs(out.jc + q, (float)Ji[8]);
-    __stcs(reinterpret_cast<unsigned short*>(out.meta) + q, (unsigned short)(s.iters | (s.conv ? 0x100 : 0)));
+    __stcs(reinterpret_cast<unsigned int*>(out.meta) + q, (unsigned int)s.iters | (s.conv ? 0x80000000u : 0u));
 #endif
 }
 
@@ -322,7 +322,7 @@ __device__ __forceinline__ void store_exact(const SearchPlanes& out, int64_t q, 
     out.ja[q] = make_float4((float)s.Ji[0], (float)s.Ji[1], (float)s.Ji[2], (float)s.Ji[3]);
     out.jb[q] = make_float4((float)s.Ji[4], (float)s.Ji[5], (float)s.Ji[6], (float)s.Ji[7]);
     out.jc[q] = (float)s.Ji[8];
-    out.meta[q] = (uint16_t)(s.k | (conv ? 0x100 : 0));
+    out.meta[q] = (uint32_t)s.k | (conv ? 0x80000000u : 0u);
 }
 
 // Work counters for the roofline (bench.py): per pass, solves / Broyden iterations /
@@ -884,7 +884,7 @@ __global__ void __launch_bounds__(256) k_emit(int64_t n, int nb, SearchPlanes sp
             if (o < cap) {
                 float4 xr = sp.xr[q];
                 xr.w = fabsf(xr.w);
-                store_root(roots + o, xr, sp.ja[q], sp.jb[q], sp.jc[q], b, sp.meta[q] & 0xff);
+                store_root(roots + o, xr, sp.ja[q], sp.jb[q], sp.jc[q], b, (int)(sp.meta[q] & 0x7fffffffu));
             }
             ++o;
         }
@@ -896,7 +896,7 @@ __global__ void __launch_bounds__(256) k_emit(int64_t n, int nb, SearchPlanes sp
         if (o < cap) {
             float4 xr = sp.xr[q];
             xr.w = fabsf(xr.w);
-            store_root(roots + o, xr, sp.ja[q], sp.jb[q], sp.jc[q], b, sp.meta[q] & 0xff);
+            store_root(roots + o, xr, sp.ja[q], sp.jb[q], sp.jc[q], b, (int)(sp.meta[q] & 0x7fffffffu));
         }
         ++o;
     }
@@ -907,7 +907,7 @@ struct DenseOut {
     float* x_c;
     float* jinv;
     float* resid;
-    uint8_t* iters;
+    int32_t* iters;
     uint8_t* converged;
     uint8_t* keep;
     int32_t* n_roots;
@@ -934,9 +934,9 @@ __global__ void __launch_bounds__(256) k_scatter_dense(int64_t n, int nb, Search
         J[4] = c.x; J[5] = c.y; J[6] = c.z; J[7] = c.w;
         J[8] = sp.jc[q];
     }
-    const uint16_t m = sp.meta[q];
-    if (d.iters) d.iters[s] = (uint8_t)(m & 0xff);
-    d.converged[s] = (uint8_t)(m >> 8);
+    const uint32_t m = sp.meta[q];
+    if (d.iters) d.iters[s] = (int32_t)(m & 0x7fffffffu);
+    d.converged[s] = (uint8_t)(m >> 31);
     if (d.keep) d.keep[s] = sp.keep[q];
 }
 
@@ -987,6 +987,30 @@ __global__ void __launch_bounds__(256) k_init_states(Planes<float> P, GridP g, c
     const int bone = (int)(s - p * g.nb);
     float x0, x1, x2, Ji[9], T[12];
     solve_init<float>(P, g, bones + 12 * bone, pts[3 * p], pts[3 * p + 1], pts[3 * p + 2], x0, x1, x2, Ji, T);
+    if (x0o) {
+        x0o[3 * s] = x0;
+        x0o[3 * s + 1] = x1;
+        x0o[3 * s + 2] = x2;
+    }
+    if (jo)
+        for (int e = 0; e < 9; ++e) jo[9 * s + e] = Ji[e];
+}
+
+// init_states in float64 with the reference's operation order (fsk_exact.cuh): x0 = B_i^-1 x' and
+// J~0 = J(x0)^-1 from the n_b-wide weight grid (correspondence.cpp:43-70), one thread per (point,
+// bone), point-major output — what the drop-in's init_states returns.
+__global__ void __launch_bounds__(128) k_init_states64(GridP g, const float* __restrict__ W, const float* __restrict__ bones,
+                                                       const double* __restrict__ pts, int64_t n,
+                                                       double* __restrict__ x0o, double* __restrict__ jo) {
+    const double* bones64 = stage_bones64(bones, g.nb);
+    const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (s >= n * g.nb) return;
+    const int64_t p = s / g.nb;
+    const int bone = (int)(s - p * g.nb);
+    double x0, x1, x2, J[9], Ji[9];
+    exact::inverse_apply(bones64 + 12 * bone, pts[3 * p], pts[3 * p + 1], pts[3 * p + 2], x0, x1, x2);
+    exact::jacobian(g, W, bones64, x0, x1, x2, J);
+    exact::inverse_or_identity(J, Ji);
     if (x0o) {
         x0o[3 * s] = x0;
         x0o[3 * s + 1] = x1;
@@ -1074,7 +1098,7 @@ SearchState run_search(fsk_ctx* ctx, GridPlanes& P, const GridP& g, const float*
     s.sp.ja = (float4*)scratch(ctx, kOJa, S * sizeof(float4));
     s.sp.jb = (float4*)scratch(ctx, kOJb, S * sizeof(float4));
     s.sp.jc = (float*)scratch(ctx, kOJc, S * sizeof(float));
-    s.sp.meta = (uint16_t*)scratch(ctx, kOMeta, S * sizeof(uint16_t));
+    s.sp.meta = (uint32_t*)scratch(ctx, kOMeta, S * sizeof(uint32_t));
     s.sp.keep = (uint8_t*)scratch(ctx, kOKeep, S);
     s.sp.kmask = g.nb <= 32 ? (uint32_t*)scratch(ctx, kOKeepMask, std::max<int64_t>(1, n) * sizeof(uint32_t)) : nullptr;
     s.perm = (int*)scratch(ctx, kPerm, std::max<int64_t>(1, n) * sizeof(int));
@@ -1468,7 +1492,7 @@ int fsk_search_fwd_mlp(fsk_ctx* ctx, const float* theta, const int32_t* widths, 
         ss.sp.ja = (float4*)scratch(ctx, kOJa, S * sizeof(float4));
         ss.sp.jb = (float4*)scratch(ctx, kOJb, S * sizeof(float4));
         ss.sp.jc = (float*)scratch(ctx, kOJc, S * sizeof(float));
-        ss.sp.meta = (uint16_t*)scratch(ctx, kOMeta, S * sizeof(uint16_t));
+        ss.sp.meta = (uint32_t*)scratch(ctx, kOMeta, S * sizeof(uint32_t));
         ss.sp.keep = (uint8_t*)scratch(ctx, kOKeep, S);
         ss.perm = (int*)scratch(ctx, kPerm, n * sizeof(int));
         ss.n_roots_p = (int32_t*)scratch(ctx, kNRoots, n * sizeof(int32_t));
@@ -1618,16 +1642,21 @@ int fsk_deform_host(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* des
             cuda_check(cudaEventCreateWithFlags(&offs_ready[c], cudaEventDisableTiming), "cudaEventCreate");
             cuda_check(cudaEventCreateWithFlags(&up[c], cudaEventDisableTiming), "cudaEventCreate");
         }
-        struct Events {
+        struct Events {  // on every exit (errors included): drain the three streams, then free the events
+            fsk_ctx* ctx;
+            cudaStream_t st;
             std::vector<cudaEvent_t>* a;
             std::vector<cudaEvent_t>* b;
             std::vector<cudaEvent_t>* c;
             ~Events() {
+                cudaStreamSynchronize(ctx->upload);
+                cudaStreamSynchronize(st);
+                cudaStreamSynchronize(ctx->copy);
                 for (auto e : *a) cudaEventDestroy(e);
                 for (auto e : *b) cudaEventDestroy(e);
                 for (auto e : *c) cudaEventDestroy(e);
             }
-        } cleanup{&done, &offs_ready, &up};
+        } cleanup{ctx, st, &done, &offs_ready, &up};
         // each chunk's points upload on their own stream, ahead of (and overlapping) the
         // previous chunks' searches
         cuda_check(cudaEventRecord(up[0], st), "cudaEventRecord");
@@ -1803,6 +1832,20 @@ int fsk_init_states(fsk_ctx* ctx, const float* tgrid, const fsk_grid_desc* desc,
         cudaStream_t st = (cudaStream_t)stream;
         const GridPlanes P = run_relayout(ctx, tgrid, nullptr, g, false, st);
         FSK_LAUNCH(ctx, st, k_init_states, blocks_for(n * g.nb, 256), 256, 0, P.p32, g, bones, points, n, x0, jinv0);
+    });
+}
+
+int fsk_init_states64(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* desc, const float* bones,
+                      int32_t n_bones_pose, const double* points, int64_t n, double* x0, double* jinv0, void* stream) {
+    return guard([&] {
+        set_device(ctx);
+        const GridP g = make_grid(desc);
+        check_search_args(g, n_bones_pose, weights, "search: grid bone count mismatch");
+        if (n < 0) fail(FSK_EINVAL, "fsk: negative point count");
+        if (n == 0) return;
+        if (!points || !bones) fail(FSK_EINVAL, "fsk: null buffer");
+        FSK_LAUNCH(ctx, (cudaStream_t)stream, k_init_states64, blocks_for(n * g.nb, 128), 128,
+                   (size_t)g.nb * 12 * sizeof(double), g, weights, bones, points, n, x0, jinv0);
     });
 }
 

@@ -5,7 +5,9 @@
 // std::runtime_error otherwise). There is no CPU implementation of the search here.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
+#include <mutex>
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
@@ -80,8 +82,8 @@ fsk_grid_desc desc_of(const GridDims& d, const Aabb& bb, int nb) {
     g.nz = d.nz;
     g.n_bones = nb;
     for (int a = 0; a < 3; ++a) {
-        g.bbox_min[a] = static_cast<float>(bb.min[a]);
-        g.bbox_max[a] = static_cast<float>(bb.max[a]);
+        g.bbox_min[a] = bb.min[a];
+        g.bbox_max[a] = bb.max[a];
     }
     return g;
 }
@@ -348,29 +350,60 @@ std::shared_ptr<void> dev_buffer(size_t bytes) {
 }  // namespace
 
 void TransformGrid::sync_device() const {
+    // caller holds mu_
     const size_t V = static_cast<size_t>(dims_.vertex_count());
     if (!dev_ || !dev64_) {
         dev_ = dev_buffer(V * 12 * sizeof(float));
         dev64_ = dev_buffer(V * 12 * sizeof(double));
-        host_dirty_ = true;
+        uploaded_.clear();
     }
-    if (host_dirty_) {
+    if (uploaded_ != data_) {  // host copy changed since the last upload (through any pointer)
         std::vector<float> f(data_.begin(), data_.end());
         h2d(static_cast<DevBuf*>(dev_.get())->p, f.data(), f.size() * sizeof(float));
         h2d(static_cast<DevBuf*>(dev64_.get())->p, data_.data(), data_.size() * sizeof(double));
-        host_dirty_ = false;
+        uploaded_ = data_;
     }
 }
 
 const float* TransformGrid::device_data() const {
+    std::lock_guard<std::mutex> lk(mu_);
     sync_device();
     return static_cast<DevBuf*>(dev_.get())->as<float>();
 }
 
 const double* TransformGrid::device_data64() const {
+    std::lock_guard<std::mutex> lk(mu_);
     sync_device();
     return static_cast<DevBuf*>(dev64_.get())->as<double>();
 }
+
+namespace {
+/// float32 device copy of a SkinningVoxelGrid's weights (SearchContext::grid), per thread: the
+/// search's exact-replay escalation and its initial Jacobians read the weight grid, as the
+/// reference's search_one does (correspondence.cpp:43-54). Re-uploaded whenever the grid's values
+/// differ from the last upload.
+struct WeightsMirror {
+    std::vector<float> host;
+    std::shared_ptr<void> dev;
+    size_t cap = 0;
+};
+
+const float* device_weights(const SkinningVoxelGrid& grid) {
+    thread_local WeightsMirror m;
+    const std::vector<double>& w = grid.raw();
+    std::vector<float> f(w.begin(), w.end());
+    if (!m.dev || m.cap < f.size()) {
+        m.dev = dev_buffer(std::max<size_t>(f.size(), 1) * sizeof(float));
+        m.cap = f.size();
+        m.host.clear();
+    }
+    if (f != m.host) {
+        h2d(static_cast<DevBuf*>(m.dev.get())->p, f.data(), f.size() * sizeof(float));
+        m.host = std::move(f);
+    }
+    return static_cast<DevBuf*>(m.dev.get())->as<float>();
+}
+}  // namespace
 
 // K1 on the GPU in float32 (the fast search's grid) and float64 (the reference's
 // TransformGrid precision: the host copy and the float64 re-solves read it).
@@ -380,18 +413,17 @@ TransformGrid precompute_transform_grid(const SkinningVoxelGrid& grid, std::span
     TransformGrid tg(grid.dims(), grid.bbox());
     const std::int64_t V = grid.dims().vertex_count();
     const int nb = grid.bone_count();
-    std::vector<float> w(grid.raw().begin(), grid.raw().end());
     const std::vector<float> b = bones_f32(bones);
-    DevBuf dw(w.size() * sizeof(float)), db(b.size() * sizeof(float));
+    const float* dw = device_weights(grid);
+    DevBuf db(b.size() * sizeof(float));
     tg.dev_ = dev_buffer(static_cast<size_t>(V) * 12 * sizeof(float));
     tg.dev64_ = dev_buffer(static_cast<size_t>(V) * 12 * sizeof(double));
-    h2d(dw.p, w.data(), w.size() * sizeof(float));
     h2d(db.p, b.data(), b.size() * sizeof(float));
     const fsk_grid_desc d = desc_of(grid.dims(), grid.bbox(), nb);
-    check(fsk_precompute_tgrid(ctx(), dw.as<float>(), &d, db.as<float>(), nb, static_cast<DevBuf*>(tg.dev_.get())->as<float>(),
+    check(fsk_precompute_tgrid(ctx(), dw, &d, db.as<float>(), nb, static_cast<DevBuf*>(tg.dev_.get())->as<float>(),
                                static_cast<DevBuf*>(tg.dev64_.get())->as<double>(), nullptr));
     d2h(tg.data_.data(), static_cast<DevBuf*>(tg.dev64_.get())->p, tg.data_.size() * sizeof(double));
-    tg.host_dirty_ = false;
+    tg.uploaded_ = tg.data_;
     return tg;
 }
 
@@ -411,10 +443,22 @@ void eval_batch(const TransformGrid& tg, std::span<const Vec3> x, float* t12, fl
 }
 }  // namespace
 
+// Single-point host evaluation of the float64 host copy (deformer.cpp:79-94): corners in (dk, dj, di)
+// order, each of the 12 entries accumulated corner by corner.
 void trilerp_transform_into(const TransformGrid& tgrid, const Vec3& x, double* out12) {
-    float t[12];
-    eval_batch(tgrid, {&x, 1}, t, nullptr, nullptr);
-    for (int e = 0; e < 12; ++e) out12[e] = t[e];
+    const CellLocator c = locate_cell(tgrid.dims(), tgrid.bbox(), x);
+    for (int e = 0; e < 12; ++e) out12[e] = 0.0;
+    for (int dk = 0; dk < 2; ++dk) {
+        const double fz = dk ? c.tz : 1.0 - c.tz;
+        for (int dj = 0; dj < 2; ++dj) {
+            const double fyz = fz * (dj ? c.ty : 1.0 - c.ty);
+            for (int di = 0; di < 2; ++di) {
+                const double f = fyz * (di ? c.tx : 1.0 - c.tx);
+                const double* t = tgrid.vertex_transform(tgrid.vertex_index(c.i0 + di, c.j0 + dj, c.k0 + dk));
+                for (int e = 0; e < 12; ++e) out12[e] += f * t[e];
+            }
+        }
+    }
 }
 
 Affine3 trilerp_transform(const TransformGrid& tgrid, const Vec3& x) {
@@ -436,7 +480,14 @@ std::vector<Vec3> forward_deform_batch(std::span<const Vec3> x, const TransformG
     return out;
 }
 
-Vec3 forward_deform(const Vec3& x, const TransformGrid& tgrid) { return forward_deform_batch({&x, 1}, tgrid)[0]; }
+// d = T(x)·[x;1] on the unclamped x (deformer.cpp:107-113), float64 host copy
+Vec3 forward_deform(const Vec3& x, const TransformGrid& tgrid) {
+    double m[12];
+    trilerp_transform_into(tgrid, x, m);
+    Vec3 d;
+    for (int r = 0; r < 3; ++r) d[r] = m[4 * r] * x[0] + m[4 * r + 1] * x[1] + m[4 * r + 2] * x[2] + m[4 * r + 3];
+    return d;
+}
 
 std::vector<Mat3> deform_jacobian_batch(std::span<const Vec3> x, const TransformGrid& tgrid) {
     std::vector<float> j(x.size() * 9);
@@ -448,9 +499,18 @@ std::vector<Mat3> deform_jacobian_batch(std::span<const Vec3> x, const Transform
     return out;
 }
 
+// J = Σ_i w_i R_i + Σ_i (B_i x)(∇w_i)ᵀ in bone order (deformer.cpp:117-136), float64 on the host
 Mat3 deform_jacobian(const Vec3& x, const SkinningVoxelGrid& grid, std::span<const RigidTransform> bones) {
-    const TransformGrid tg = precompute_transform_grid(grid, bones);
-    return deform_jacobian_batch({&x, 1}, tg)[0];
+    const VectorXd w = trilerp_weights(grid, x);
+    const MatrixXd gw = weight_spatial_gradient(grid, x);
+    Mat3 J = Mat3::Zero();
+    for (size_t i = 0; i < bones.size(); ++i) J += w[static_cast<std::int64_t>(i)] * bones[i].rotation;
+    for (size_t i = 0; i < bones.size(); ++i) {
+        const Vec3 bx = bones[i].apply(x);
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) J(r, c) += bx[r] * gw(static_cast<std::int64_t>(i), c);
+    }
+    return J;
 }
 
 // ------------------------------------------------------------------------ correspondence
@@ -468,23 +528,25 @@ void SearchOptions::validate() const {
     if (!(conv_eps > 0.0)) throw std::invalid_argument("search: conv_eps must be > 0");
     if (!(div_eps > conv_eps)) throw std::invalid_argument("search: div_eps must exceed conv_eps");
     if (!(dedup_dist >= 0.0)) throw std::invalid_argument("search: dedup_dist must be >= 0");
-    if (max_iters > 255) throw std::invalid_argument("fsk: max_iters must be <= 255 (uint8 iteration counts)");
 }
 
+// init_states (correspondence.cpp:58-70) on the GPU in float64 with the reference's operation order
+// (fsk_init_states64: x0 = B_i^-1 x', J~0 from the weight grid's Jacobian) — the oracle's values.
 std::vector<InitState> init_states(const Vec3& x_prime, const SearchContext& c, SearchVariant variant) {
     check_context(c, variant);
     const int nb = static_cast<int>(c.bones.size());
     const std::vector<float> b = bones_f32(c.bones);
-    const std::vector<float> p = points_f32({&x_prime, 1});
-    DevBuf db(b.size() * 4), dp(12), dx(nb * 12), dj(nb * 36);
+    const double p[3] = {x_prime[0], x_prime[1], x_prime[2]};
+    const float* dw = device_weights(*c.grid);
+    DevBuf db(b.size() * 4), dp(sizeof(p)), dx(nb * 3 * sizeof(double)), dj(nb * 9 * sizeof(double));
     h2d(db.p, b.data(), b.size() * 4);
-    h2d(dp.p, p.data(), 12);
-    const fsk_grid_desc d = desc_of(c.tgrid->dims(), c.tgrid->bbox(), nb);
-    check(fsk_init_states(ctx(), c.tgrid->device_data(), &d, db.as<float>(), nb, dp.as<float>(), 1, dx.as<float>(),
-                          dj.as<float>(), nullptr));
-    std::vector<float> x0(nb * 3), j0(nb * 9);
-    d2h(x0.data(), dx.p, x0.size() * 4);
-    d2h(j0.data(), dj.p, j0.size() * 4);
+    h2d(dp.p, p, sizeof(p));
+    const fsk_grid_desc d = desc_of(c.grid->dims(), c.grid->bbox(), nb);
+    check(fsk_init_states64(ctx(), dw, &d, db.as<float>(), nb, dp.as<double>(), 1, dx.as<double>(), dj.as<double>(),
+                            nullptr));
+    std::vector<double> x0(nb * 3), j0(nb * 9);
+    d2h(x0.data(), dx.p, x0.size() * sizeof(double));
+    d2h(j0.data(), dj.p, j0.size() * sizeof(double));
     std::vector<InitState> out(nb);
     for (int i = 0; i < nb; ++i) {
         out[i].x0 = Vec3(x0[3 * i], x0[3 * i + 1], x0[3 * i + 2]);
@@ -511,7 +573,10 @@ std::vector<CorrespondenceSet> batch_search(std::span<const Vec3> queries, const
     h2d(dp.p, p.data(), p.size() * 4);
     const fsk_grid_desc d = desc_of(c.tgrid->dims(), c.tgrid->bbox(), nb);
     const fsk_search_opts so = c_opts(opts);
-    check(fsk_batch_search(ctx(), c.tgrid->device_data(), c.tgrid->device_data64(), nullptr, &d, db.as<float>(), nb,
+    // SearchContext::grid's weights go to the search like the reference's (J~0 from the weight grid,
+    // correspondence.cpp:43-54): the escalated solves then replay the reference's operation order
+    const float* dw = device_weights(*c.grid);
+    check(fsk_batch_search(ctx(), c.tgrid->device_data(), c.tgrid->device_data64(), dw, &d, db.as<float>(), nb,
                            dp.as<float>(), n, &so, offs.as<std::int64_t>(), dr.as<fsk_root>(), cap, nullptr));
     std::vector<std::int64_t> h_offs(n + 1);
     d2h(h_offs.data(), offs.p, h_offs.size() * 8);

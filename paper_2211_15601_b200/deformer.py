@@ -179,7 +179,7 @@ class Deformer:
             x_c=torch.empty((n, nb, 3), dtype=torch.float32, device=dev),
             jinv=torch.empty((n, nb, 3, 3), dtype=torch.float32, device=dev) if jinv else None,
             resid=torch.empty((n, nb), dtype=torch.float32, device=dev) if resid else None,
-            iters=torch.empty((n, nb), dtype=torch.uint8, device=dev) if iters else None,
+            iters=torch.empty((n, nb), dtype=torch.int32, device=dev) if iters else None,
             converged=torch.empty((n, nb), dtype=torch.uint8, device=dev),
             keep=torch.empty((n, nb), dtype=torch.uint8, device=dev) if keep else None,
             n_roots=torch.empty((n,), dtype=torch.int32, device=dev) if keep else None,

@@ -3,6 +3,7 @@
 // fskin_cli.cpp:395-408, diff.cpp:278-289), on inputs written by tests/test_cpp_api.py.
 // Writes the CorrespondenceSets as text for the Python side to compare with the oracle,
 // and checks the API's own contracts (soundness, error messages, identity pose).
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <fstream>
@@ -94,17 +95,61 @@ int main(int argc, char** argv) {
     const CorrespondenceSet one = broyden_search(queries[0], ctx, opts);
     CHECK(one.roots.size() == sets[0].roots.size());
     for (size_t k = 0; k < one.roots.size(); ++k) CHECK(one.roots[k].x == sets[0].roots[k].x);
-    // init_states: x0 = B_i^-1 x'
+    // init_states: x0 = B_i^-1 x' (float64; the values are compared with the oracle's by the test)
     const auto st = init_states(queries[1], ctx, SearchVariant::Voxel);
     CHECK(st.size() == static_cast<size_t>(nb));
-    for (int i = 0; i < nb; ++i) CHECK((st[i].x0 - bones[i].inverse().apply(queries[1])).norm() < 1e-5);
-    // host evaluator agrees with the GPU evaluator (lossless precomputation, FP32)
+    for (int i = 0; i < nb; ++i) CHECK((st[i].x0 - bones[i].inverse().apply(queries[1])).norm() < 1e-12);
+    if (argc > 3) {
+        std::FILE* g = std::fopen(argv[3], "wb");
+        for (const auto& s : st) {
+            const double x3[3] = {s.x0[0], s.x0[1], s.x0[2]};
+            std::fwrite(x3, sizeof(double), 3, g);
+        }
+        for (const auto& s : st)
+            for (int r = 0; r < 3; ++r)
+                for (int c = 0; c < 3; ++c) {
+                    const double v = s.inv_jacobian(r, c);
+                    std::fwrite(&v, sizeof(double), 1, g);
+                }
+        std::fclose(g);
+    }
+    // TransformGrid is a value type (deformer.hpp:27-49): a modified copy leaves the original's
+    // device mirror alone, and writes through vertex_transform() after a search are seen
+    {
+        const Vec3 probe = queries[2];
+        const Vec3 before = forward_deform_batch({&probe, 1}, tgrid)[0];
+        TransformGrid t2 = tgrid;
+        for (std::int64_t v = 0; v < t2.dims().vertex_count(); ++v) t2.set_vertex(v, Affine3::from(RigidTransform::identity()));
+        const Vec3 id = forward_deform_batch({&probe, 1}, t2)[0];
+        CHECK((id - probe).norm() < 1e-5);
+        CHECK(forward_deform_batch({&probe, 1}, tgrid)[0] == before);
+        double* m = t2.vertex_transform(0);
+        for (std::int64_t v = 0; v < t2.dims().vertex_count(); ++v) {
+            m = t2.vertex_transform(v);
+            m[3] += 1.0;  // translate every vertex by +1 in x, through the raw pointer
+        }
+        const Vec3 moved = forward_deform_batch({&probe, 1}, t2)[0];
+        CHECK(std::abs(moved[0] - probe[0] - 1.0) < 1e-5);
+        CHECK(forward_deform_batch({&probe, 1}, tgrid)[0] == before);
+    }
+    // max_iters beyond 255 (correspondence.cpp:20 accepts any value >= 1)
+    {
+        SearchOptions o = opts;
+        o.max_iters = 300;
+        const std::vector<CorrespondenceSet> s300 = batch_search(std::span<const Vec3>(queries).first(200), ctx, o);
+        CHECK(s300.size() == 200);
+    }
+    // lossless precomputation: the weight-grid and transform-grid evaluators agree
+    // to 1e-10 in float64; the GPU batch evaluator (float32) to 1e-5
     for (int p = 0; p < 50; ++p) {
         const Vec3 a = forward_deform(queries[p], grid, bones);
         const Vec3 g = forward_deform(queries[p], tgrid);
-        CHECK((a - g).norm() < 1e-5);
+        CHECK((a - g).norm() < 1e-10);
+        CHECK((forward_deform_batch({&queries[p], 1}, tgrid)[0] - g).norm() < 1e-5);
         const Mat3 J = deform_jacobian(queries[p], grid, bones);
-        CHECK(std::isfinite(J.determinant()));
+        const Mat3 Jb = deform_jacobian_batch({&queries[p], 1}, tgrid)[0];
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) CHECK(std::abs(J(r, c) - Jb(r, c)) < 1e-4);
     }
     // dedup_roots
     std::vector<Root> rr(3);

@@ -45,8 +45,8 @@ def test_mlp_variant_matches_oracle(deformer):
     print(f"\nmlp variant: converged {r['converged'].mean():.3f}, mask agreement {agree:.6f}, keep {keep_agree:.6f}, "
           f"|dx| p50 {np.median(dx):.1e} p99.9 {np.percentile(dx, 99.9):.1e} max {dx.max():.1e}")
     # float32 trajectories through a float32 network: no float64 escalation on this path
-    assert agree >= 0.999 and keep_agree >= 0.999
-    assert np.percentile(dx, 99.9) <= 1e-4
+    assert agree >= 0.9999 and keep_agree >= 0.9999
+    assert dx.max() <= 1e-4
 
 
 def _match_sets(xa, ka, xb, kb, tol):

@@ -69,9 +69,9 @@ def test_no_cpu_fallback_without_device(lib):
 
 
 def test_search_defaults_match_reference(lib):
-    d = _lib.GridDesc(4, 4, 4, 2, (ctypes.c_float * 3)(0, 0, 0), (ctypes.c_float * 3)(3, 4, 0))
+    d = _lib.GridDesc(4, 4, 4, 2, (ctypes.c_double * 3)(0, 0, 0), (ctypes.c_double * 3)(3, 4, 0))
     o = lib.fsk_search_opts_defaults(ctypes.byref(d))
     # SearchOptions::defaults_for (correspondence.cpp:10-17) with diag = 5
     assert o.max_iters == 50
     for got, want in ((o.conv_eps, 5e-5), (o.div_eps, 2.5), (o.dedup_dist, 0.05)):
-        assert abs(got - want) <= 1e-7 * want  # float32 fields
+        assert abs(got - want) <= 1e-15 * want  # float64 bbox (geometry.hpp:14-39)
