@@ -65,17 +65,21 @@ typedef struct fsk_search_opts {
 #define FSK_SEARCH_NO_SORT 0x1    /* ablation: skip the spatial ordering of queries */
 #define FSK_SEARCH_FP32_ONLY 0x2  /* ablation: float32 only, no float64 escalation */
 #define FSK_SEARCH_FP64 0x4       /* parity mode: every solve in float64 */
-#define FSK_SEARCH_EXACT64 0x8    /* replay mode: every solve in float64 in the reference's own
-                                     operation order (unfused, J~0 from the n_b-wide weight grid),
-                                     bit-identical to a float64 build of the reference given the same
-                                     transform grid; needs the weight grid (fsk_search_fwd /
-                                     fsk_batch_search `weights`, always present in fsk_deform*) */
+#define FSK_SEARCH_EXACT64 0x8    /* replay mode: every solve in float64 in the oracle's operation order
+                                     (oracle/fskin_oracle.cpp: the reference's code with Eigen's closed
+                                     forms, unfused, J~0 from the n_b-wide weight grid), bit-identical to
+                                     the oracle given the same transform grid. The reference's own
+                                     operation order is not pinned (Eigen unpinned, -march=native): its
+                                     plausible builds differ from each other by ~1 mask flip per 2M solves
+                                     (scripts/oracle_variants.py). Needs the weight
+                                     grid (fsk_search_fwd / fsk_batch_search `weights`; always present in
+                                     fsk_deform*) */
 #define FSK_SEARCH_FAST_ESC 0x10  /* mixed mode, ablation: escalate to the fused float64 solver
                                      (transform-grid J~0) even when the weight grid is given. By
-                                     default the escalation pass replays the reference exactly
-                                     whenever the weight grid is available (always in fsk_deform*;
-                                     fsk_search_fwd / fsk_batch_search when `weights` != NULL), so
-                                     escalated solves equal the reference bit for bit */
+                                     default the escalation pass is the exact replay whenever the weight
+                                     grid is available (always in fsk_deform*; fsk_search_fwd /
+                                     fsk_batch_search when `weights` != NULL), so escalated solves equal
+                                     the oracle's bit for bit */
 
 /* Dense per-(point, init) search result (the GPU form of Root / CorrespondenceSet,
  * correspondence.hpp:29-42). All pointers dev, [N][n_b] point-major; any may be NULL

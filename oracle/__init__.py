@@ -16,7 +16,11 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB = os.path.join(_HERE, "liboracle.so")
-_lib = None
+# operation-order variants of the same restatement (oracle/Makefile): the reference's
+# Eigen version and build flags are not pinned, so its exact float64 operation order is not either
+VARIANTS = ("eigen", "invrow0", "pairsum", "fma")
+_libs = {}
+_variant = None  # module-wide default for every call below (None = "eigen"); see use_variant()
 
 _d = ctypes.POINTER(ctypes.c_double)
 _u8 = ctypes.POINTER(ctypes.c_uint8)
@@ -25,18 +29,33 @@ _i64 = ctypes.c_int64
 _int = ctypes.c_int
 
 
+def _path(variant):
+    return _LIB if variant in (None, "eigen") else os.path.join(_HERE, f"liboracle_{variant}.so")
+
+
 def build(force: bool = False) -> str:
     srcs = [os.path.join(_HERE, f) for f in ("fskin_oracle.cpp", "precision_emul.cpp", "mlp_oracle.cpp", "Makefile")]
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(os.path.getmtime(s) for s in srcs):
+    newest = max(os.path.getmtime(s) for s in srcs)
+    if force or any(not os.path.exists(_path(v)) or os.path.getmtime(_path(v)) < newest for v in VARIANTS):
         subprocess.run(["make", "-s", "-C", _HERE], check=True)
     return _LIB
 
 
-def lib():
-    global _lib
-    if _lib is None:
+def use_variant(variant):
+    """Route every oracle call of this process to an operation-order variant (None = default)."""
+    global _variant
+    if variant not in (None,) + VARIANTS:
+        raise ValueError(variant)
+    _variant = None if variant == "eigen" else variant
+
+
+def lib(variant=None):
+    variant = variant if variant is not None else _variant
+    key = variant or "eigen"
+    if key not in _libs:
         build()
-        L = ctypes.CDLL(_LIB)
+        L = ctypes.CDLL(_path(variant))
+        L.orc_variant.restype = ctypes.c_char_p
         L.orc_last_error.restype = ctypes.c_char_p
         L.orc_precompute_tgrid.argtypes = [_d, _int, _int, _int, _int, _d, _d, _int, _d, _int]
         L.orc_lbs_blend.argtypes = [_d, _d, _int, _int, _d]
@@ -58,8 +77,8 @@ def lib():
         L.orc_mlp_weights_jacobian.argtypes = [_d, _pi, _int, _d, _i64, _d, _d, _int]
         L.orc_batch_search_mlp.argtypes = [_d, _pi, _int, _d, _int, _d, _i64, _int, ctypes.c_double,
                                            ctypes.c_double, ctypes.c_double, _int, _d, _d, _d, _i32, _u8, _u8]
-        _lib = L
-    return _lib
+        _libs[key] = L
+    return _libs[key]
 
 
 class OracleError(Exception):
@@ -72,7 +91,7 @@ class OracleInvalidArgument(OracleError, ValueError):
 
 def _check(rc):
     if rc != 0:
-        msg = lib().orc_last_error().decode()
+        msg = lib().orc_last_error().decode()  # errors are raised by the validation shared by all variants
         raise (OracleInvalidArgument if rc == 1 else OracleError)(msg)
 
 
@@ -84,13 +103,13 @@ def _f64(a):
     return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
 
 
-def precompute_transform_grid(weights, dims, bbox, bones, workers=1):
+def precompute_transform_grid(weights, dims, bbox, bones, workers=1, variant=None):
     """deformer.cpp:61-77 → tgrid [V,12] float64."""
     w, bb, B = _f64(weights), _f64(bbox), _f64(bones).reshape(-1, 12)
     nx, ny, nz = dims
     nb = w.shape[1] if w.ndim == 2 else B.shape[0]
     out = np.zeros((nx * ny * nz, 12))
-    _check(lib().orc_precompute_tgrid(_p(w), nx, ny, nz, nb, _p(bb), _p(B), B.shape[0], _p(out), workers))
+    _check(lib(variant).orc_precompute_tgrid(_p(w), nx, ny, nz, nb, _p(bb), _p(B), B.shape[0], _p(out), workers))
     return out
 
 
@@ -114,24 +133,24 @@ def eval_points(weights, dims, bbox, bones, tgrid, x):
     return out
 
 
-def init_states(weights, dims, bbox, bones, x_prime):
+def init_states(weights, dims, bbox, bones, x_prime, variant=None):
     w, bb, B, x = _f64(weights), _f64(bbox), _f64(bones).reshape(-1, 12), _f64(x_prime).reshape(-1, 3)
     n, nb = x.shape[0], B.shape[0]
     x0, j0 = np.zeros((n, nb, 3)), np.zeros((n, nb, 3, 3))
-    _check(lib().orc_init_states(_p(w), *dims, w.shape[1], _p(bb), _p(B), nb, _p(x), n, _p(x0), _p(j0)))
+    _check(lib(variant).orc_init_states(_p(w), *dims, w.shape[1], _p(bb), _p(B), nb, _p(x), n, _p(x0), _p(j0)))
     return x0, j0
 
 
 def batch_search(weights, dims, bbox, bones, x_prime, max_iters, conv_eps, div_eps, dedup_dist,
-                 workers=1, tgrid=None):
+                 workers=1, tgrid=None, variant=None):
     """correspondence.cpp:178-192 with per-(point, init) dense outputs."""
     w, bb, B, x = _f64(weights), _f64(bbox), _f64(bones).reshape(-1, 12), _f64(x_prime).reshape(-1, 3)
-    tg = _f64(tgrid) if tgrid is not None else precompute_transform_grid(w, dims, bb, B, workers)
+    tg = _f64(tgrid) if tgrid is not None else precompute_transform_grid(w, dims, bb, B, workers, variant)
     n, nb = x.shape[0], B.shape[0]
     out = dict(x_c=np.zeros((n, nb, 3)), jinv=np.zeros((n, nb, 3, 3)), resid=np.zeros((n, nb)),
                iters=np.zeros((n, nb), np.int32), converged=np.zeros((n, nb), np.uint8),
                keep=np.zeros((n, nb), np.uint8))
-    _check(lib().orc_batch_search(_p(w), *dims, w.shape[1], _p(bb), _p(tg), _p(B), nb, _p(x), n,
+    _check(lib(variant).orc_batch_search(_p(w), *dims, w.shape[1], _p(bb), _p(tg), _p(B), nb, _p(x), n,
                                   int(max_iters), conv_eps, div_eps, dedup_dist, workers,
                                   _p(out["x_c"]), _p(out["jinv"]), _p(out["resid"]), _p(out["iters"], _i32),
                                   _p(out["converged"], _u8), _p(out["keep"], _u8)))

@@ -33,6 +33,19 @@
 namespace orc {
 
 // ---------------------------------------------------------------- tiny linear algebra
+// Eigen's fixed-size 3-term reductions (mat-vec coefficients, dot, squaredNorm) sum either left to
+// right, (a+b)+c — the packet path with a 2-wide double packet plus a scalar tail, the default
+// here — or as a+(b+c) — the unvectorized redux unroller (HalfLength = 1). Which one a build uses
+// depends on the Eigen version, the compiler flags (`-march=native`, proj/CMakeLists.txt:10-14)
+// and the CPU; ORC_SUM_PAIR builds the second (oracle variant "pairsum": the
+// reference is not pinned to one operation order).
+static inline double sum3(double a, double b, double c) {
+#ifdef ORC_SUM_PAIR
+    return a + (b + c);
+#else
+    return (a + b) + c;
+#endif
+}
 struct V3 {
     double v[3] = {0, 0, 0};
     double& operator[](int i) { return v[i]; }
@@ -48,20 +61,22 @@ struct M3 {
 };
 static inline V3 mul(const M3& a, const V3& x) {
     V3 r;
-    for (int i = 0; i < 3; ++i) r[i] = a.m[i][0] * x[0] + a.m[i][1] * x[1] + a.m[i][2] * x[2];
+    for (int i = 0; i < 3; ++i) r[i] = sum3(a.m[i][0] * x[0], a.m[i][1] * x[1], a.m[i][2] * x[2]);
     return r;
 }
-static inline double dot(const V3& a, const V3& b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
+static inline double dot(const V3& a, const V3& b) { return sum3(a[0] * b[0], a[1] * b[1], a[2] * b[2]); }
 static inline double norm(const V3& a) { return std::sqrt(dot(a, a)); }
 
-// Eigen's closed-form 3×3 determinant (expansion along the first row).
+// Eigen's closed-form 3×3 determinant (Determinant.h: expansion along the first row).
 static inline double det3(const M3& a) {
     auto h = [&](int c0, int c1, int c2) {
         return a.m[0][c0] * (a.m[1][c1] * a.m[2][c2] - a.m[1][c2] * a.m[2][c1]);
     };
     return h(0, 1, 2) - h(1, 0, 2) + h(2, 0, 1);
 }
-// Cofactor inverse (adjugate / det).
+// Eigen's 3×3 inverse (InverseImpl.h compute_inverse<.., 3>): the cofactors of column 0, their
+// determinant (cofactors_col0 · col(0), a 3-term redux), 1/det, then every cofactor times 1/det.
+// ORC_INV_ROW0 (variant "invrow0", the round-1 oracle) takes that determinant along row 0.
 static inline M3 inv3(const M3& a) {
     M3 c;
     c.m[0][0] = a.m[1][1] * a.m[2][2] - a.m[1][2] * a.m[2][1];
@@ -73,11 +88,52 @@ static inline M3 inv3(const M3& a) {
     c.m[2][0] = a.m[1][0] * a.m[2][1] - a.m[1][1] * a.m[2][0];
     c.m[2][1] = a.m[0][1] * a.m[2][0] - a.m[0][0] * a.m[2][1];
     c.m[2][2] = a.m[0][0] * a.m[1][1] - a.m[0][1] * a.m[1][0];
+#ifdef ORC_INV_ROW0
     const double det = a.m[0][0] * c.m[0][0] + a.m[0][1] * c.m[1][0] + a.m[0][2] * c.m[2][0];
+#else
+    const double det = sum3(c.m[0][0] * a.m[0][0], c.m[0][1] * a.m[1][0], c.m[0][2] * a.m[2][0]);
+#endif
     const double inv = 1.0 / det;
     for (int i = 0; i < 3; ++i)
         for (int j = 0; j < 3; ++j) c.m[i][j] *= inv;
     return c;
+}
+
+// Jᵀu = v by Eigen's PartialPivLU (PartialPivLU.h unblocked_lu: per column k the first largest |.|
+// below the diagonal is the pivot, rows swapped, the column below divided by the pivot, rank-1
+// update of the trailing block; then P·v, unit-lower forward and upper back substitution, column
+// oriented) — `jac.transpose().partialPivLu().solve(cotangent)` (diff.cpp:36).
+static inline V3 lu_solve_transposed(const M3& J, const V3& v) {
+    double m[3][3];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) m[i][j] = J.m[j][i];
+    int perm[3] = {0, 1, 2};
+    for (int k = 0; k < 3; ++k) {
+        int p = k;
+        double big = std::abs(m[k][k]);
+        for (int i = k + 1; i < 3; ++i)
+            if (std::abs(m[i][k]) > big) {
+                big = std::abs(m[i][k]);
+                p = i;
+            }
+        if (big != 0.0) {
+            if (p != k) {
+                for (int j = 0; j < 3; ++j) std::swap(m[k][j], m[p][j]);
+                std::swap(perm[k], perm[p]);
+            }
+            for (int i = k + 1; i < 3; ++i) m[i][k] /= m[k][k];
+        }
+        for (int i = k + 1; i < 3; ++i)
+            for (int j = k + 1; j < 3; ++j) m[i][j] -= m[i][k] * m[k][j];
+    }
+    double x[3] = {v[perm[0]], v[perm[1]], v[perm[2]]};
+    for (int j = 0; j < 3; ++j)  // unit lower
+        for (int i = j + 1; i < 3; ++i) x[i] -= x[j] * m[i][j];
+    for (int j = 2; j >= 0; --j) {  // upper
+        x[j] /= m[j][j];
+        for (int i = 0; i < j; ++i) x[i] -= x[j] * m[i][j];
+    }
+    return V3{{x[0], x[1], x[2]}};
 }
 
 // Rigid transform [R | t] stored as 12 doubles row-major (geometry.hpp:42-78).
@@ -321,7 +377,7 @@ static void iterate(State& st, const V3& xp, const Grid& g, const double* tgrid,
             for (int i = 0; i < 3; ++i) r[i] = (dx[i] - jdg[i]) / denom;
             V3 wrow;  // dxᵀ J̃
             for (int c = 0; c < 3; ++c)
-                wrow[c] = dx[0] * st.inv_jac.m[0][c] + dx[1] * st.inv_jac.m[1][c] + dx[2] * st.inv_jac.m[2][c];
+                wrow[c] = sum3(dx[0] * st.inv_jac.m[0][c], dx[1] * st.inv_jac.m[1][c], dx[2] * st.inv_jac.m[2][c]);
             for (int i = 0; i < 3; ++i)
                 for (int c = 0; c < 3; ++c) st.inv_jac.m[i][c] += r[i] * wrow[c];
         }
@@ -527,6 +583,16 @@ int orc_batch_search(const double* w, int nx, int ny, int nz, int nb, const doub
 }
 
 // dedup_roots (correspondence.cpp:162-176) over m roots xs[m][3].
+// Which operation-order variant this build is (oracle/Makefile): "eigen" (default), "invrow0",
+// "pairsum", "fma".
+const char* orc_variant(void) {
+#if defined(ORC_VARIANT_NAME)
+    return ORC_VARIANT_NAME;
+#else
+    return "eigen";
+#endif
+}
+
 int orc_dedup_roots(const double* xs, int m, double dedup_dist, uint8_t* keep) {
     return guard([&] { dedup(xs, nullptr, m, dedup_dist, keep); });
 }
@@ -557,7 +623,7 @@ int orc_grid_vjp(int nx, int ny, int nz, int nb, const double* bbox6, const doub
                 for (int c = 0; c < 3; ++c) J.m[r][c] = jinv[9 * p + 3 * r + c];
             V3 u;  // u = −J̃ᵀ v (diff.cpp:351)
             for (int c = 0; c < 3; ++c)
-                u[c] = -(J.m[0][c] * v[3 * p] + J.m[1][c] * v[3 * p + 1] + J.m[2][c] * v[3 * p + 2]);
+                u[c] = -sum3(J.m[0][c] * v[3 * p], J.m[1][c] * v[3 * p + 1], J.m[2][c] * v[3 * p + 2]);
             std::vector<double> uw(nb);
             for (int i = 0; i < nb; ++i) uw[i] = dot(u, B[i].apply(xs));  // diff.cpp:354-356
             const Cell c = locate(g, xs, false);
@@ -583,7 +649,8 @@ int orc_grid_vjp(int nx, int ny, int nz, int nb, const double* bbox6, const doub
 }
 
 // Exact implicit cotangent (implicit_grad_exact, diff.cpp:31-41) on the grid field:
-// u = −J⁻ᵀ v with J = deform_jacobian(x*, grid, B); ok[p]=0 if |det J| < 1e-10 (SingularRootError).
+// u = −J⁻ᵀ v with J = deform_jacobian(x*, grid, B) solved by partial-pivot LU of Jᵀ (:36);
+// ok[p]=0 if |det J| < 1e-10 (SingularRootError, :34-35).
 int orc_implicit_u_exact(const double* w, int nx, int ny, int nz, int nb, const double* bbox6,
                          const double* bones, const double* x_star, const double* v, int64_t n, double* u_out,
                          uint8_t* ok) {
@@ -601,9 +668,8 @@ int orc_implicit_u_exact(const double* w, int nx, int ny, int nz, int nb, const 
                 continue;
             }
             ok[p] = 1;
-            const M3 Ji = inv3(J);
-            for (int c = 0; c < 3; ++c)
-                u_out[3 * p + c] = -(Ji.m[0][c] * v[3 * p] + Ji.m[1][c] * v[3 * p + 1] + Ji.m[2][c] * v[3 * p + 2]);
+            const V3 u = lu_solve_transposed(J, V3{{v[3 * p], v[3 * p + 1], v[3 * p + 2]}});  // diff.cpp:36
+            for (int c = 0; c < 3; ++c) u_out[3 * p + c] = -u[c];  // acc.scale(-1.0) (diff.cpp:39)
         }
     });
 }

@@ -362,8 +362,8 @@ __device__ __forceinline__ void jacobian_stash_vec(const GridP& g, const float* 
     }
 }
 
-// initial_inverse_jacobian (correspondence.cpp:43-54): Eigen's det (expansion along row 0)
-// against 1e-8, then the cofactor inverse with its own det (adjugate / det)
+// initial_inverse_jacobian (correspondence.cpp:43-54): Eigen's determinant() (expansion along row 0)
+// against 1e-8, then Eigen's cofactor inverse with its own det (column-0 cofactors; adjugate · 1/det)
 __device__ __forceinline__ void inverse_or_identity(const double a[9], double Ji[9]) {
     auto h = [&](int c0, int c1, int c2) {
         return mul(a[c0], sub(mul(a[3 + c1], a[6 + c2]), mul(a[3 + c2], a[6 + c1])));
@@ -384,7 +384,9 @@ __device__ __forceinline__ void inverse_or_identity(const double a[9], double Ji
     c[6] = sub(mul(a[3], a[7]), mul(a[4], a[6]));
     c[7] = sub(mul(a[1], a[6]), mul(a[0], a[7]));
     c[8] = sub(mul(a[0], a[4]), mul(a[1], a[3]));
-    const double d2 = add(add(mul(a[0], c[0]), mul(a[1], c[3])), mul(a[2], c[6]));
+    // Eigen's inverse() takes its own determinant from the column-0 cofactors (InverseImpl.h
+    // compute_inverse<.., 3>: cofactors_col0 · col(0)), summed left to right
+    const double d2 = add(add(mul(c[0], a[0]), mul(c[1], a[3])), mul(c[2], a[6]));
     const double inv = div(1.0, d2);
 #pragma unroll
     for (int e = 0; e < 9; ++e) Ji[e] = mul(c[e], inv);

@@ -685,8 +685,8 @@ __global__ void __launch_bounds__(128) k_search_f64(Planes<double> P, GridP g, c
     count_work(stats ? stats + 3 : nullptr, s);
 }
 
-// Exact replay mode (FSK_SEARCH_EXACT64): every solve in float64 with the reference's own
-// operation order (fsk_exact.cuh), J~0 from the n_b-wide weight grid — bit-identical to the
+// Exact replay mode (FSK_SEARCH_EXACT64): every solve in float64 with the oracle's restatement of the
+// reference's operation order (fsk_exact.cuh), J~0 from the n_b-wide weight grid — bit-identical to the
 // oracle's search_one (correspondence.cpp:126-150) given the same float64 transform grid.
 __global__ void __launch_bounds__(128) k_search_exact(Planes<double> P, GridP g, const float* __restrict__ W,
                                                       const float* __restrict__ bones, const float4* __restrict__ xs,
