@@ -242,6 +242,25 @@ int fsk_search_bwd_roots(fsk_ctx* ctx, const fsk_grid_desc* desc, const fsk_root
                          const int64_t* root_index, const float* grad_xc, int64_t n,
                          float* grad_tgrid, int deterministic, void* stream);
 
+/* ---- B2: implicit_grad_exact (diff.cpp:31-41; SingularRootError diff.hpp:20-22), grid-routed.
+ * Per point p: J = deform_jacobian(x*_p, grid, bones) in float64 in the reference's operation order
+ * (weight-grid form, deformer.cpp:117-136), det = Mat3::determinant; |det| < 1e-10 (or NaN) →
+ * ok[p] = 0 and u = 0 (the reference throws SingularRootError; its callers skip the sample), else
+ * u = −J⁻ᵀ v by partial-pivot LU of Jᵀ (:36, the sign of :39 folded in) and ok[p] = 1.
+ * weights [V][n_b], bones, x_star [N][3] and grad_xc (v) [N][3] float32; u [N][3] float64; ok [N],
+ * det [N] float64 (either may be NULL). All dev. */
+int fsk_implicit_u_exact(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* desc, const float* bones,
+                         int32_t n_bones_pose, const float* x_star, const float* grad_xc, int64_t n, double* u,
+                         uint8_t* ok, double* det, void* stream);
+
+/* fsk_search_bwd_roots with the exact cotangent (fsk_implicit_u_exact) instead of −J~ᵀv: the
+ * implicit_grad_exact form of the training backward. Singular roots contribute nothing (ok[p] = 0
+ * when ok != NULL). grad_tgrid [V][12] overwritten. */
+int fsk_search_bwd_exact_roots(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* desc, const float* bones,
+                               int32_t n_bones_pose, const fsk_root* roots, const int64_t* root_index,
+                               const float* grad_xc, int64_t n, float* grad_tgrid, uint8_t* ok, int deterministic,
+                               void* stream);
+
 /* dL/dw[v][i] = <dL/dT[v], B_i>_F  (chain rule through deformer.cpp:70-74). [V][n_b] dev. */
 int fsk_grad_weights(fsk_ctx* ctx, const fsk_grid_desc* desc, const float* grad_tgrid,
                      const float* bones, int32_t n_bones_pose, float* grad_w, void* stream);

@@ -32,6 +32,7 @@ EXPORTS = [
     "fsk_multi_grad_weights_host", "fsk_search_fwd_mlp",
     "fsk_io_last_error", "fsk_sknv_read", "fsk_sknv_write", "fsk_points_bin_read", "fsk_points_bin_write",
     "fsk_write_correspondence_dump", "fsk_deform_files", "fsk_init_states64",
+    "fsk_implicit_u_exact", "fsk_search_bwd_exact_roots",
 ]
 
 
@@ -97,6 +98,8 @@ def load():
     L.fsk_init_states64.argtypes = [_vp, _vp, G, _vp, _i32, _vp, _i64, _vp, _vp, _vp]
     L.fsk_search_bwd.argtypes = [_vp, G, _vp, _vp, _i32, _vp, _vp, _i64, _vp, ctypes.c_int, _vp]
     L.fsk_grad_weights.argtypes = [_vp, G, _vp, _vp, _i32, _vp, _vp]
+    L.fsk_implicit_u_exact.argtypes = [_vp, _vp, G, _vp, _i32, _vp, _vp, _i64, _vp, _vp, _vp, _vp]
+    L.fsk_search_bwd_exact_roots.argtypes = [_vp, _vp, G, _vp, _i32, _vp, _vp, _vp, _i64, _vp, _vp, ctypes.c_int, _vp]
     L.fsk_batch_search.argtypes = [_vp, _vp, _vp, _vp, G, _vp, _i32, _vp, _i64, O, _vp, _vp, _i64, _vp]
     L.fsk_deform.argtypes = [_vp, _vp, G, _vp, _i32, _vp, _i64, O, _vp, _vp, _vp, _i64, _vp]
     L.fsk_search_bwd_roots.argtypes = [_vp, G, _vp, _vp, _vp, _i64, _vp, ctypes.c_int, _vp]

@@ -11,6 +11,7 @@
 // rounded to int64 fixed point with a data-derived power-of-two scale and accumulated with
 // integer reductions — associative, so bitwise reproducible for any order or GPU count.
 #include "fsk_ctx.h"
+#include "fsk_exact.cuh"
 
 namespace fsk {
 
@@ -23,11 +24,24 @@ struct RootRef {  // where the selected root of each query lives
     // compact form: roots [M], ridx [N] root index (int64) or -1
     const fsk_root* roots;
     const int64_t* ridx;
+    // exact mode (implicit_grad_exact, diff.cpp:31-41): the cotangent u [N][3] was computed by
+    // k_implicit_exact (u = −J⁻ᵀv from the Jacobian at x*) instead of −J~ᵀv; ok [N] = 0 marks a
+    // singular root, skipped (SingularRootError: "caller skips this sample")
+    const float* u_ex = nullptr;
+    const uint8_t* ok = nullptr;
+    // x*-only form (fsk_implicit_u_exact): x_star [N][3]
+    const float* xs_direct = nullptr;
 };
 
-__device__ __forceinline__ bool bwd_load(const RootRef& R, int64_t p, const float* __restrict__ gx, float xs[3],
-                                         float u[3]) {
-    const float* J;
+// x* of query p (false: no root selected)
+__device__ __forceinline__ bool root_x(const RootRef& R, int64_t p, float xs[3], const float** J) {
+    if (R.xs_direct) {
+        xs[0] = R.xs_direct[3 * p];
+        xs[1] = R.xs_direct[3 * p + 1];
+        xs[2] = R.xs_direct[3 * p + 2];
+        *J = nullptr;
+        return true;
+    }
     if (R.roots) {
         const int64_t k = R.ridx[p];
         if (k < 0) return false;
@@ -35,21 +49,139 @@ __device__ __forceinline__ bool bwd_load(const RootRef& R, int64_t p, const floa
         xs[0] = r.x[0];
         xs[1] = r.x[1];
         xs[2] = r.x[2];
-        J = r.inv_jacobian;
-    } else {
-        const int sidx = R.sel[p];
-        if (sidx < 0 || sidx >= R.n_init) return false;
-        const int64_t s = p * R.n_init + sidx;
-        J = R.jinv + 9 * s;
-        xs[0] = R.x_c[3 * s];
-        xs[1] = R.x_c[3 * s + 1];
-        xs[2] = R.x_c[3 * s + 2];
+        *J = r.inv_jacobian;
+        return true;
+    }
+    const int sidx = R.sel[p];
+    if (sidx < 0 || sidx >= R.n_init) return false;
+    const int64_t s = p * R.n_init + sidx;
+    *J = R.jinv + 9 * s;
+    xs[0] = R.x_c[3 * s];
+    xs[1] = R.x_c[3 * s + 1];
+    xs[2] = R.x_c[3 * s + 2];
+    return true;
+}
+
+__device__ __forceinline__ bool bwd_load(const RootRef& R, int64_t p, const float* __restrict__ gx, float xs[3],
+                                         float u[3]) {
+    const float* J;
+    if (!root_x(R, p, xs, &J)) return false;
+    if (R.u_ex) {
+        if (R.ok && !R.ok[p]) return false;
+        u[0] = R.u_ex[3 * p];
+        u[1] = R.u_ex[3 * p + 1];
+        u[2] = R.u_ex[3 * p + 2];
+        return true;
     }
     const float v0 = gx[3 * p], v1 = gx[3 * p + 1], v2 = gx[3 * p + 2];
     u[0] = -(J[0] * v0 + J[3] * v1 + J[6] * v2);
     u[1] = -(J[1] * v0 + J[4] * v1 + J[7] * v2);
     u[2] = -(J[2] * v0 + J[5] * v1 + J[8] * v2);
     return true;
+}
+
+// ---- implicit_grad_exact (diff.cpp:31-41), grid-routed: per selected root, J = deform_jacobian(x*,
+// grid, bones) in float64 in the reference's operation order (deformer.cpp:117-136; fsk_exact.cuh),
+// its determinant (Eigen's, row 0); |det| < 1e-10 → singular (ok = 0, SingularRootError, :34-35);
+// else u = −J⁻ᵀv by partial-pivot LU of Jᵀ like `jac.transpose().partialPivLu().solve(v)` (:36,
+// Eigen PartialPivLU: first largest |pivot| per column, row swap, column divided by the pivot,
+// rank-1 trailing update; P·v, unit-lower then upper substitution, column oriented).
+__device__ __forceinline__ void lu_solve_T(const double J[9], const double v[3], double x[3]) {
+    using namespace exact;
+    double m[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) m[i][j] = J[3 * j + i];
+    int perm[3] = {0, 1, 2};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        int p = k;
+        double big = fabs(m[k][k]);
+#pragma unroll
+        for (int i = k + 1; i < 3; ++i)
+            if (fabs(m[i][k]) > big) {
+                big = fabs(m[i][k]);
+                p = i;
+            }
+        if (big != 0.0) {
+            if (p != k) {
+#pragma unroll
+                for (int j = 0; j < 3; ++j) {
+                    const double t = m[k][j];
+                    m[k][j] = m[p][j];
+                    m[p][j] = t;
+                }
+                const int t = perm[k];
+                perm[k] = perm[p];
+                perm[p] = t;
+            }
+#pragma unroll
+            for (int i = k + 1; i < 3; ++i) m[i][k] = div(m[i][k], m[k][k]);
+        }
+#pragma unroll
+        for (int i = k + 1; i < 3; ++i)
+#pragma unroll
+            for (int j = k + 1; j < 3; ++j) m[i][j] = sub(m[i][j], mul(m[i][k], m[k][j]));
+    }
+    double y[3] = {v[perm[0]], v[perm[1]], v[perm[2]]};
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+#pragma unroll
+        for (int i = j + 1; i < 3; ++i) y[i] = sub(y[i], mul(y[j], m[i][j]));
+#pragma unroll
+    for (int j = 2; j >= 0; --j) {
+        y[j] = div(y[j], m[j][j]);
+#pragma unroll
+        for (int i = 0; i < j; ++i) y[i] = sub(y[i], mul(y[j], m[i][j]));
+    }
+    x[0] = y[0];
+    x[1] = y[1];
+    x[2] = y[2];
+}
+
+__global__ void __launch_bounds__(128) k_implicit_exact(GridP g, const float* __restrict__ W,
+                                                        const float* __restrict__ bones, RootRef R,
+                                                        const float* __restrict__ gx, int64_t n,
+                                                        float* __restrict__ u32, double* __restrict__ u64,
+                                                        uint8_t* __restrict__ ok, double* __restrict__ det_out) {
+    extern __shared__ double s_b64[];  // float64 copies of the bones (widening is exact)
+    for (int e = threadIdx.x; e < 12 * g.nb; e += blockDim.x) s_b64[e] = (double)__ldg(bones + e);
+    __syncthreads();
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    float xs[3];
+    const float* Jt;
+    double u[3] = {0.0, 0.0, 0.0}, det = 0.0;
+    bool good = false;
+    if (root_x(R, p, xs, &Jt)) {
+        double J[9];
+        exact::jacobian(g, W, s_b64, (double)xs[0], (double)xs[1], (double)xs[2], J);
+        using namespace exact;
+        auto h = [&](int c0, int c1, int c2) { return mul(J[c0], sub(mul(J[3 + c1], J[6 + c2]), mul(J[3 + c2], J[6 + c1]))); };
+        det = add(sub(h(0, 1, 2), h(1, 0, 2)), h(2, 0, 1));  // Mat3::determinant (diff.cpp:34)
+        if (fabs(det) >= 1e-10) {  // (:35) NaN det: singular as well
+            const double v[3] = {(double)gx[3 * p], (double)gx[3 * p + 1], (double)gx[3 * p + 2]};
+            double x[3];
+            lu_solve_T(J, v, x);
+            u[0] = -x[0];  // acc.scale(-1.0) (:39)
+            u[1] = -x[1];
+            u[2] = -x[2];
+            good = true;
+        }
+    }
+    if (u32) {
+        u32[3 * p] = (float)u[0];
+        u32[3 * p + 1] = (float)u[1];
+        u32[3 * p + 2] = (float)u[2];
+    }
+    if (u64) {
+        u64[3 * p] = u[0];
+        u64[3 * p + 1] = u[1];
+        u64[3 * p + 2] = u[2];
+    }
+    if (ok) ok[p] = good ? 1 : 0;
+    if (det_out) det_out[p] = det;
 }
 
 __global__ void k_zero(float4* __restrict__ p, int64_t n4) {
@@ -318,6 +450,47 @@ int fsk_search_bwd_roots(fsk_ctx* ctx, const fsk_grid_desc* desc, const fsk_root
         if (!grad_tgrid || (n > 0 && (!roots || !root_index || !grad_xc))) fail(FSK_EINVAL, "fsk: null buffer");
         RootRef R{nullptr, nullptr, nullptr, 0, roots, root_index};
         run_bwd(ctx, g, R, grad_xc, n, grad_tgrid, deterministic, (cudaStream_t)stream);
+    });
+}
+
+int fsk_implicit_u_exact(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* desc, const float* bones,
+                         int32_t n_bones_pose, const float* x_star, const float* grad_xc, int64_t n, double* u,
+                         uint8_t* ok, double* det, void* stream) {
+    return guard([&] {
+        set_device(ctx);
+        const GridP g = make_grid(desc);
+        if (n_bones_pose != g.nb) fail(FSK_EINVAL, "deform vjp: bone count mismatch");
+        if (n < 0) fail(FSK_EINVAL, "fsk: negative point count");
+        if (n == 0) return;
+        if (!weights || !bones || !x_star || !grad_xc) fail(FSK_EINVAL, "fsk: null buffer");
+        RootRef R{nullptr, nullptr, nullptr, 0, nullptr, nullptr};
+        R.xs_direct = x_star;
+        FSK_LAUNCH(ctx, (cudaStream_t)stream, k_implicit_exact, blocks_for(n, 128), 128,
+                   (size_t)g.nb * 12 * sizeof(double), g, weights, bones, R, grad_xc, n, nullptr, u, ok, det);
+    });
+}
+
+int fsk_search_bwd_exact_roots(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* desc, const float* bones,
+                               int32_t n_bones_pose, const fsk_root* roots, const int64_t* root_index,
+                               const float* grad_xc, int64_t n, float* grad_tgrid, uint8_t* ok, int deterministic,
+                               void* stream) {
+    return guard([&] {
+        set_device(ctx);
+        const GridP g = make_grid(desc);
+        if (n_bones_pose != g.nb) fail(FSK_EINVAL, "deform vjp: bone count mismatch");
+        if (n < 0) fail(FSK_EINVAL, "fsk: negative point count");
+        if (!grad_tgrid || !weights || !bones || (n > 0 && (!roots || !root_index || !grad_xc)))
+            fail(FSK_EINVAL, "fsk: null buffer");
+        cudaStream_t st = (cudaStream_t)stream;
+        RootRef R{nullptr, nullptr, nullptr, 0, roots, root_index};
+        float* u = (float*)scratch(ctx, kBwdU, std::max<int64_t>(1, n) * 3 * sizeof(float));
+        uint8_t* okp = ok ? ok : (uint8_t*)scratch(ctx, kBwdOk, std::max<int64_t>(1, n));
+        if (n > 0)
+            FSK_LAUNCH(ctx, st, k_implicit_exact, blocks_for(n, 128), 128, (size_t)g.nb * 12 * sizeof(double), g,
+                       weights, bones, R, grad_xc, n, u, nullptr, okp, nullptr);
+        R.u_ex = u;
+        R.ok = okp;
+        run_bwd(ctx, g, R, grad_xc, n, grad_tgrid, deterministic, st);
     });
 }
 

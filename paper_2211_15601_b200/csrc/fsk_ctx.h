@@ -51,7 +51,7 @@ namespace fsk {
 // Scratch slots (one growable device buffer each).
 enum Slot {
     kHist, kBbox, kKeys, kPerm, kXs, kScanPart, kBwdAcc, kBwdMax, kPlanes, kPlanes64, kEscQ, kEscN, kEscState,
-    kBwdStart, kBwdCell, kBwdRec, kPeakTable,
+    kBwdStart, kBwdCell, kBwdRec, kPeakTable, kBwdU, kBwdOk,
     kOXr, kOJa, kOJb, kOJc, kOMeta, kOKeep, kOKeepMask, kNRoots, kOffs, kRootsTmp,
     kHW, kHB, kHP, kHT, kHOffs, kHRoots, kFB, kFP, kFOffs, kFRoots,
     kMlpPack, kMlpWidths, kMlpOcc, kMlpAct, kMlpD0, kMlpD1, kMlpOnes,

@@ -19,6 +19,7 @@
 #include "fsk.h"
 #include "fskin/correspondence.hpp"
 #include "fskin/deformer.hpp"
+#include "fskin/diff.hpp"
 #include "fskin/geometry.hpp"
 #include "fskin/skinning.hpp"
 
@@ -602,6 +603,96 @@ std::vector<CorrespondenceSet> batch_search(std::span<const Vec3> queries, const
 
 CorrespondenceSet broyden_search(const Vec3& x_prime, const SearchContext& c, const SearchOptions& opts) {
     return batch_search({&x_prime, 1}, c, opts)[0];
+}
+
+// ------------------------------------------------------------------------ implicit differentiation
+SingularRootError::SingularRootError(double det)
+    : std::runtime_error("implicit gradient: deformation Jacobian is singular (det " + std::to_string(det) + ")") {}
+
+Vec3 implicit_cotangent_exact(const Vec3& x_star, const SkinningVoxelGrid& grid, std::span<const RigidTransform> bones,
+                              const Vec3& cotangent) {
+    if (static_cast<int>(bones.size()) != grid.bone_count()) throw std::invalid_argument("deform vjp: bone count mismatch");
+    const std::vector<float> b = bones_f32(bones);
+    const float xv[6] = {static_cast<float>(x_star[0]), static_cast<float>(x_star[1]), static_cast<float>(x_star[2]),
+                         static_cast<float>(cotangent[0]), static_cast<float>(cotangent[1]),
+                         static_cast<float>(cotangent[2])};
+    const float* dw = device_weights(grid);
+    DevBuf db(b.size() * 4), dx(sizeof(xv)), du(3 * sizeof(double)), dok(1), ddet(sizeof(double));
+    h2d(db.p, b.data(), b.size() * 4);
+    h2d(dx.p, xv, sizeof(xv));
+    const fsk_grid_desc d = desc_of(grid.dims(), grid.bbox(), grid.bone_count());
+    check(fsk_implicit_u_exact(ctx(), dw, &d, db.as<float>(), grid.bone_count(), dx.as<float>(), dx.as<float>() + 3, 1,
+                               du.as<double>(), dok.as<std::uint8_t>(), ddet.as<double>(), nullptr));
+    double u[3], det;
+    std::uint8_t ok;
+    d2h(u, du.p, sizeof(u));
+    d2h(&ok, dok.p, 1);
+    d2h(&det, ddet.p, sizeof(det));
+    if (!ok) throw SingularRootError(det);
+    return Vec3(u[0], u[1], u[2]);
+}
+
+Vec3 implicit_cotangent_approx(const Mat3& inv_jacobian, const Vec3& cotangent) {
+    return -(inv_jacobian.transpose() * cotangent);
+}
+
+GridGradient implicit_grad_grid(std::span<const CorrespondenceSet> sets, std::span<const int> root_of_query,
+                                std::span<const Vec3> cotangents, const SkinningVoxelGrid& grid,
+                                std::span<const RigidTransform> bones, bool exact) {
+    const std::int64_t n = static_cast<std::int64_t>(sets.size());
+    if (root_of_query.size() != sets.size() || cotangents.size() != sets.size())
+        throw std::invalid_argument("implicit_grad_grid: one root index and one cotangent per query");
+    const int nb = grid.bone_count();
+    if (static_cast<int>(bones.size()) != nb) throw std::invalid_argument("deform vjp: bone count mismatch");
+    std::vector<fsk_root> recs;
+    std::vector<std::int64_t> ridx(static_cast<size_t>(n), -1);
+    std::vector<float> v(static_cast<size_t>(3 * n));
+    for (std::int64_t q = 0; q < n; ++q) {
+        for (int a = 0; a < 3; ++a) v[3 * q + a] = static_cast<float>(cotangents[q][a]);
+        const int k = root_of_query[q];
+        if (k < 0) continue;
+        if (k >= static_cast<int>(sets[q].roots.size())) throw std::invalid_argument("implicit_grad_grid: root index out of range");
+        const Root& r = sets[q].roots[k];
+        fsk_root f{};
+        for (int a = 0; a < 3; ++a) f.x[a] = static_cast<float>(r.x[a]);
+        f.residual = static_cast<float>(r.residual);
+        for (int a = 0; a < 3; ++a)
+            for (int e = 0; e < 3; ++e) f.inv_jacobian[3 * a + e] = static_cast<float>(r.inv_jacobian(a, e));
+        f.source_bone = r.source_bone;
+        f.iterations = r.iterations;
+        ridx[q] = static_cast<std::int64_t>(recs.size());
+        recs.push_back(f);
+    }
+    const std::int64_t V = grid.dims().vertex_count();
+    const std::vector<float> b = bones_f32(bones);
+    const float* dw = exact ? device_weights(grid) : nullptr;
+    DevBuf db(b.size() * 4), dr(std::max<size_t>(recs.size(), 1) * sizeof(fsk_root)), di(ridx.size() * 8 + 8),
+        dv(v.size() * 4 + 4), dT(static_cast<size_t>(V) * 12 * sizeof(float)), dW(static_cast<size_t>(V) * nb * sizeof(float)),
+        dok(static_cast<size_t>(n) + 1);
+    h2d(db.p, b.data(), b.size() * 4);
+    h2d(dr.p, recs.data(), recs.size() * sizeof(fsk_root));
+    h2d(di.p, ridx.data(), ridx.size() * 8);
+    h2d(dv.p, v.data(), v.size() * 4);
+    const fsk_grid_desc d = desc_of(grid.dims(), grid.bbox(), nb);
+    if (exact)
+        check(fsk_search_bwd_exact_roots(ctx(), dw, &d, db.as<float>(), nb, dr.as<fsk_root>(), di.as<std::int64_t>(),
+                                         dv.as<float>(), n, dT.as<float>(), dok.as<std::uint8_t>(), 1, nullptr));
+    else
+        check(fsk_search_bwd_roots(ctx(), &d, dr.as<fsk_root>(), di.as<std::int64_t>(), dv.as<float>(), n, dT.as<float>(),
+                                   1, nullptr));
+    check(fsk_grad_weights(ctx(), &d, dT.as<float>(), db.as<float>(), nb, dW.as<float>(), nullptr));
+    std::vector<float> t(static_cast<size_t>(V) * 12), w(static_cast<size_t>(V) * nb);
+    d2h(t.data(), dT.p, t.size() * 4);
+    d2h(w.data(), dW.p, w.size() * 4);
+    GridGradient out;
+    out.d_tgrid.assign(t.begin(), t.end());
+    out.d_weights.assign(w.begin(), w.end());
+    if (exact && n > 0) {
+        std::vector<std::uint8_t> ok(static_cast<size_t>(n));
+        d2h(ok.data(), dok.p, ok.size());
+        for (std::int64_t q = 0; q < n; ++q) out.skipped += (ridx[q] >= 0 && !ok[q]) ? 1 : 0;
+    }
+    return out;
 }
 
 std::vector<Root> dedup_roots(std::vector<Root> roots, double dedup_dist) {

@@ -310,6 +310,41 @@ class Deformer:
                                     _ptr(out), 1 if deterministic else 0, _stream(self.device)))
         return out
 
+    def implicit_u_exact(self, weights, dims, bbox, bones, x_star, grad_xc):
+        """``implicit_grad_exact``'s cotangent (diff.cpp:31-41), grid-routed: u = −(∂d/∂x*)⁻ᵀ v in
+        float64 from the weight-grid Jacobian at x* → (u [N,3] float64, ok [N] uint8, det [N] float64);
+        ok = 0 marks a singular root (|det| < 1e-10, the reference's SingularRootError)."""
+        nb = bones.numel() // 12
+        desc = grid_desc(dims, bbox, nb)
+        n = x_star.shape[0]
+        u = torch.empty((n, 3), dtype=torch.float64, device=self.device)
+        ok = torch.empty((n,), dtype=torch.uint8, device=self.device)
+        det = torch.empty((n,), dtype=torch.float64, device=self.device)
+        check(self.L.fsk_implicit_u_exact(self._ctx, _ptr(_f32(weights, "weights", self.device)), ctypes.byref(desc),
+                                          _ptr(_f32(bones, "bones", self.device)), nb,
+                                          _ptr(_f32(x_star, "x_star", self.device)),
+                                          _ptr(_f32(grad_xc, "grad_xc", self.device)), n, _ptr(u), _ptr(ok), _ptr(det),
+                                          _stream(self.device)))
+        return u, ok, det
+
+    def search_bwd_exact_roots(self, weights, dims, bbox, bones, roots, root_index, grad_xc, deterministic=False,
+                               out=None):
+        """Backward from compact roots with the exact cotangent (implicit_grad_exact) → (dL/dT [V,12],
+        ok [N] uint8: 0 = singular root, skipped)."""
+        nb = bones.numel() // 12
+        desc = grid_desc(dims, bbox, nb)
+        V = desc.nx * desc.ny * desc.nz
+        n = grad_xc.shape[0]
+        if out is None:
+            out = torch.empty((V, 12), dtype=torch.float32, device=self.device)
+        ok = torch.empty((n,), dtype=torch.uint8, device=self.device)
+        ri = root_index.to(device=self.device, dtype=torch.int64).contiguous()
+        check(self.L.fsk_search_bwd_exact_roots(self._ctx, _ptr(_f32(weights, "weights", self.device)),
+                                                ctypes.byref(desc), _ptr(_f32(bones, "bones", self.device)), nb,
+                                                _ptr(roots), _ptr(ri), _ptr(_f32(grad_xc, "grad_xc", self.device)), n,
+                                                _ptr(out), _ptr(ok), 1 if deterministic else 0, _stream(self.device)))
+        return out, ok
+
     def grad_weights(self, dims, bbox, grad_tgrid, bones, out=None):
         """dL/dw [V, n_b] = <dL/dT_v, B_i>_F."""
         nb = bones.numel() // 12

@@ -13,6 +13,7 @@
 
 #include "fskin/correspondence.hpp"
 #include "fskin/deformer.hpp"
+#include "fskin/diff.hpp"
 
 using namespace fskin;
 
@@ -150,6 +151,50 @@ int main(int argc, char** argv) {
         const Mat3 Jb = deform_jacobian_batch({&queries[p], 1}, tgrid)[0];
         for (int r = 0; r < 3; ++r)
             for (int c = 0; c < 3; ++c) CHECK(std::abs(J(r, c) - Jb(r, c)) < 1e-4);
+    }
+    // implicit differentiation (diff.cpp:31-51): exact vs approx cotangent at a converged root, and the
+    // singular-root error
+    {
+        int checked = 0;
+        double cos_sum = 0.0;
+        for (int p = 0; p < n && checked < 200; ++p)
+            for (const Root& r : sets[p].roots) {
+                if (r.residual > opts.conv_eps / 10) continue;
+                const Vec3 v(0.3, -0.7, 0.5);
+                const Vec3 ue = implicit_cotangent_exact(r.x, grid, bones, v);
+                const Vec3 ua = implicit_cotangent_approx(r.inv_jacobian, v);
+                cos_sum += ue.dot(ua) / (ue.norm() * ua.norm());
+                ++checked;
+                break;
+            }
+        CHECK(checked > 50);
+        CHECK(cos_sum / checked > 0.9);
+        SkinningVoxelGrid g1(GridDims{3, 3, 3}, Aabb{{0, 0, 0}, {1, 1, 1}}, 1);
+        for (auto& e : g1.raw()) e = 1.0;
+        RigidTransform flat;
+        flat.rotation = Mat3::Identity() * 1e-4;
+        bool threw = false;
+        try {
+            implicit_cotangent_exact(Vec3(0.5, 0.5, 0.5), g1, {&flat, 1}, Vec3(1, 0, 0));
+        } catch (const SingularRootError&) {
+            threw = true;
+        }
+        CHECK(threw);
+        // grid gradient through the API: exact and approx agree in direction on the whole batch
+        std::vector<int> first(n, -1);
+        std::vector<Vec3> cot(n, Vec3(0.1, 0.2, -0.3));
+        for (int p = 0; p < n; ++p)
+            if (!sets[p].roots.empty()) first[p] = 0;
+        const GridGradient ge = implicit_grad_grid(sets, first, cot, grid, bones, true);
+        const GridGradient ga = implicit_grad_grid(sets, first, cot, grid, bones, false);
+        double dotv = 0, na = 0, nb2 = 0;
+        for (size_t e = 0; e < ge.d_weights.size(); ++e) {
+            dotv += ge.d_weights[e] * ga.d_weights[e];
+            na += ge.d_weights[e] * ge.d_weights[e];
+            nb2 += ga.d_weights[e] * ga.d_weights[e];
+        }
+        CHECK(ge.d_tgrid.size() == static_cast<size_t>(grid.dims().vertex_count()) * 12);
+        CHECK(dotv / std::sqrt(na * nb2) > 0.9);
     }
     // dedup_roots
     std::vector<Root> rr(3);

@@ -465,3 +465,18 @@ def test_oracle_mlp_variant_known_answers():
     r = oracle.batch_search_mlp(oracle.mlp_init([3, 8, 8, 1], 2), [3, 8, 8, 1], T.reshape(1, 12), S.apply(T, x),
                                 50, 1e-9, 10.0, 1e-2)
     np.testing.assert_allclose(r["x_c"][:, 0], x, atol=1e-9)
+
+
+def test_oracle_operation_order_variants_agree_at_c1():
+    """The four plausible operation orders of the reference (oracle/Makefile) give the same masks
+    and roots to ~1e-14 on the oracle configuration (C1 shape, max_iters 10); at max_iters 50 they
+    differ by a few mask flips per 4.8M solves (profiles/r02_oracle_variants.log)."""
+    from paper_2211_15601_b200 import synthetic as S
+    sc = S.make_scene((32, 32, 32), 2000, seed=1)
+    res = [oracle.batch_search(sc.weights, sc.dims, sc.bbox, sc.bones, sc.points, workers=4, variant=v,
+                               **sc.search_options(10)) for v in oracle.VARIANTS]
+    for r in res[1:]:
+        np.testing.assert_array_equal(r["converged"], res[0]["converged"])
+        np.testing.assert_array_equal(r["keep"], res[0]["keep"])
+        conv = r["converged"] == 1  # (unconverged iterates of diverging solves may go anywhere)
+        np.testing.assert_allclose(r["x_c"][conv], res[0]["x_c"][conv], rtol=0, atol=1e-12)
