@@ -9,8 +9,11 @@
 // an order of magnitude more host time than the GPU search: it is formatted by all host cores
 // in blocks (std::to_chars, general format, 17 significant digits == printf "%.17g") and
 // written in query order. Errors carry the reference's std::runtime_error texts.
+#include <cuda_runtime.h>
+
 #include <algorithm>
 #include <charconv>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <fstream>
@@ -158,55 +161,98 @@ int fsk_points_bin_write(const char* path, const float* points, int64_t n) {
 // save_correspondence_dump (pointio.cpp:97-117): per query "x y z count" then per root
 // " x y z residual source_bone iterations", all reals "%.17g" of the double values. Formatted
 // by `threads` host threads (0 = all cores) in blocks of queries, written in query order.
+}  // extern "C"
+
+namespace {
+void dump_block(std::ofstream& out, const float* queries, int64_t n, const int64_t* offsets, const fsk_root* roots,
+                int T, std::vector<std::string>& buf) {
+    constexpr int64_t kBlock = 1 << 18;  // queries per thread per block
+    buf.resize(T);
+    for (int64_t b0 = 0; b0 < n; b0 += kBlock * T) {
+        std::vector<std::thread> pool;
+        for (int t = 0; t < T; ++t)
+            pool.emplace_back([&, t] {
+                std::string& s = buf[t];
+                s.clear();
+                const int64_t q0 = b0 + (int64_t)t * kBlock, q1 = std::min(n, q0 + kBlock);
+                for (int64_t q = q0; q < q1; ++q) {
+                    for (int a = 0; a < 3; ++a) {
+                        if (a) s.push_back(' ');
+                        put_g17(s, (double)queries[3 * q + a]);
+                    }
+                    s.push_back(' ');
+                    put_int(s, (long long)(offsets[q + 1] - offsets[q]));
+                    for (int64_t r = offsets[q]; r < offsets[q + 1]; ++r) {
+                        const fsk_root& R = roots[r];
+                        for (int a = 0; a < 3; ++a) {
+                            s.push_back(' ');
+                            put_g17(s, (double)R.x[a]);
+                        }
+                        s.push_back(' ');
+                        put_g17(s, (double)R.residual);
+                        s.push_back(' ');
+                        put_int(s, R.source_bone);
+                        s.push_back(' ');
+                        put_int(s, R.iterations);
+                    }
+                    s.push_back('\n');
+                }
+            });
+        for (auto& th : pool) th.join();
+        for (int t = 0; t < T; ++t) out.write(buf[t].data(), (std::streamsize)buf[t].size());
+    }
+}
+
+int host_threads(int threads) { return threads > 0 ? threads : (int)std::max(1u, std::thread::hardware_concurrency()); }
+
+// pinned host block (H2D/D2H at full PCIe rate); plain allocation when no device is usable
+struct HostBlock {
+    void* p = nullptr;
+    size_t bytes = 0;
+    bool pinned = false;
+    void ensure(size_t b) {
+        if (b <= bytes) return;
+        release();
+        pinned = cudaMallocHost(&p, b) == cudaSuccess;
+        if (!pinned) {
+            cudaGetLastError();
+            p = std::malloc(b);
+            if (!p) throw std::runtime_error("fsk: out of host memory");
+        }
+        bytes = b;
+    }
+    void release() {
+        if (p) pinned ? (void)cudaFreeHost(p) : std::free(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    ~HostBlock() { release(); }
+    template <typename T>
+    T* as() const { return static_cast<T*>(p); }
+};
+}  // namespace
+
+extern "C" {
+
 int fsk_write_correspondence_dump(const char* path, const float* queries, int64_t n, const int64_t* offsets,
                                   const fsk_root* roots, int32_t threads) {
     return io_guard([&] {
         if (!path || (n > 0 && (!queries || !offsets))) throw std::invalid_argument("fsk: null buffer");
         std::ofstream out(path, std::ios::binary);
         if (!out) throw std::runtime_error(std::string("cannot write correspondence dump: ") + path);
-        int T = threads > 0 ? threads : (int)std::max(1u, std::thread::hardware_concurrency());
-        constexpr int64_t kBlock = 1 << 18;  // queries per thread per block
-        std::vector<std::string> buf(T);
-        for (int64_t b0 = 0; b0 < n; b0 += kBlock * T) {
-            std::vector<std::thread> pool;
-            for (int t = 0; t < T; ++t)
-                pool.emplace_back([&, t] {
-                    std::string& s = buf[t];
-                    s.clear();
-                    const int64_t q0 = b0 + (int64_t)t * kBlock, q1 = std::min(n, q0 + kBlock);
-                    for (int64_t q = q0; q < q1; ++q) {
-                        for (int a = 0; a < 3; ++a) {
-                            if (a) s.push_back(' ');
-                            put_g17(s, (double)queries[3 * q + a]);
-                        }
-                        s.push_back(' ');
-                        put_int(s, (long long)(offsets[q + 1] - offsets[q]));
-                        for (int64_t r = offsets[q]; r < offsets[q + 1]; ++r) {
-                            const fsk_root& R = roots[r];
-                            for (int a = 0; a < 3; ++a) {
-                                s.push_back(' ');
-                                put_g17(s, (double)R.x[a]);
-                            }
-                            s.push_back(' ');
-                            put_g17(s, (double)R.residual);
-                            s.push_back(' ');
-                            put_int(s, R.source_bone);
-                            s.push_back(' ');
-                            put_int(s, R.iterations);
-                        }
-                        s.push_back('\n');
-                    }
-                });
-            for (auto& th : pool) th.join();
-            for (int t = 0; t < T; ++t) out.write(buf[t].data(), (std::streamsize)buf[t].size());
-        }
+        std::vector<std::string> buf;
+        dump_block(out, queries, n, offsets, roots, host_threads(threads), buf);
         if (!out) throw std::runtime_error(std::string("short write to correspondence dump: ") + path);
     });
 }
 
-// One cmd_deform frame from files to file (fskin_cli.cpp:395-429 without the occupancy
-// column): SKNV grid + .bin points in, fsk_deform_host (chunked H2D / search / D2H pipeline),
-// correspondence dump out. Returns the query and root counts.
+// One cmd_deform frame from files to file (fskin_cli.cpp:395-429 without the occupancy column):
+// SKNV grid + .bin points in, correspondence dump out, streamed in blocks of points so host memory
+// is bounded by the block size, not by the frame (64M points: ~10^10 dump characters): block k+1 is
+// read and searched (fsk_deform_host's chunked H2D / search / D2H pipeline) while block k is
+// formatted and written by a writer thread. Root buffers are count-then-allocate: a block's first
+// try holds 2 roots per query, a block with more kept roots is re-run with the reported total.
+// Returns the query and root counts. FSK_IO_BLOCK_POINTS overrides the block size (testing).
 int fsk_deform_files(fsk_ctx* ctx, const char* grid_path, const float* bones, int32_t n_bones,
                      const char* points_path, const fsk_search_opts* opts, const char* dump_path, int64_t* n_queries,
                      int64_t* n_roots) {
@@ -223,19 +269,66 @@ int fsk_deform_files(fsk_ctx* ctx, const char* grid_path, const float* bones, in
         };
         rc(fsk_sknv_read(grid_path, &d, nullptr, 0), true);
         const int64_t V = (int64_t)d.nx * d.ny * d.nz;
-        std::vector<float> w(V * d.n_bones);
-        rc(fsk_sknv_read(grid_path, &d, w.data(), (int64_t)w.size()), true);
+        HostBlock w;
+        w.ensure(std::max<int64_t>(1, V * d.n_bones) * sizeof(float));
+        rc(fsk_sknv_read(grid_path, &d, w.as<float>(), V * d.n_bones), true);
         int64_t n = 0;
         rc(fsk_points_bin_read(points_path, nullptr, 0, &n), true);
-        std::vector<float> pts(std::max<int64_t>(1, 3 * n));
-        rc(fsk_points_bin_read(points_path, pts.data(), n, &n), true);
-        std::vector<int64_t> offs(n + 1);
-        std::vector<fsk_root> roots(std::max<int64_t>(1, n * d.n_bones));
-        int64_t total = 0;
-        rc(fsk_deform_host(ctx, w.data(), &d, bones, n_bones, pts.data(), n, opts, offs.data(), roots.data(),
-                           (int64_t)roots.size(), &total, nullptr),
-           false);
-        rc(fsk_write_correspondence_dump(dump_path, pts.data(), n, offs.data(), roots.data(), 0), true);
+        std::ifstream in(points_path, std::ios::binary);
+        if (!in) throw std::runtime_error(std::string("cannot open points file: ") + points_path);
+        std::ofstream out(dump_path, std::ios::binary);
+        if (!out) throw std::runtime_error(std::string("cannot write correspondence dump: ") + dump_path);
+        int64_t blk = int64_t(1) << 23;  // 8M points per block
+        if (const char* e = getenv("FSK_IO_BLOCK_POINTS")) blk = std::max<int64_t>(1, atoll(e));
+        blk = std::max<int64_t>(1, std::min(blk, n));
+        HostBlock pts[2], offs[2], roots[2];
+        int64_t cnt[2] = {0, 0}, total = 0;
+        std::vector<std::string> text;
+        std::thread writer;
+        std::string werr;
+        auto join = [&] {
+            if (writer.joinable()) writer.join();
+            if (!werr.empty()) throw std::runtime_error(werr);
+        };
+        const int T = host_threads(0);
+        try {
+            for (int64_t p0 = 0, k = 0; p0 < n || (n == 0 && k == 0); p0 += blk, ++k) {
+                const int s = (int)(k & 1);
+                const int64_t m = std::min(blk, n - p0);
+                pts[s].ensure(std::max<int64_t>(1, 3 * m) * sizeof(float));
+                offs[s].ensure((m + 1) * sizeof(int64_t));
+                in.read(pts[s].as<char>(), (std::streamsize)(m * 3 * sizeof(float)));
+                if (!in) throw std::runtime_error(std::string(points_path) + ": truncated read");
+                int64_t cap = std::max<int64_t>(1, 2 * m), t = 0;
+                for (int attempt = 0;; ++attempt) {  // count-then-allocate
+                    roots[s].ensure(cap * sizeof(fsk_root));
+                    const int r = fsk_deform_host(ctx, w.as<float>(), &d, bones, n_bones, pts[s].as<float>(), m, opts,
+                                                  offs[s].as<int64_t>(), roots[s].as<fsk_root>(), cap, &t, nullptr);
+                    if (r == FSK_EINVAL && t > cap && attempt == 0) {
+                        cap = t;
+                        continue;
+                    }
+                    rc(r, false);
+                    break;
+                }
+                cnt[s] = t;
+                total += t;
+                join();  // block k-1 written; its buffers (slot s^1) are free again after this
+                writer = std::thread([&, s, m] {
+                    try {
+                        dump_block(out, pts[s].as<float>(), m, offs[s].as<int64_t>(), roots[s].as<fsk_root>(), T, text);
+                    } catch (const std::exception& e) {
+                        werr = e.what();
+                    }
+                });
+                if (n == 0) break;
+            }
+            join();
+        } catch (...) {
+            if (writer.joinable()) writer.join();
+            throw;
+        }
+        if (!out) throw std::runtime_error(std::string("short write to correspondence dump: ") + dump_path);
         if (n_queries) *n_queries = n;
         if (n_roots) *n_roots = total;
     });

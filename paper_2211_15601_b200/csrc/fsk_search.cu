@@ -1427,6 +1427,177 @@ void scan_i32_to_i64(fsk_ctx* ctx, const int32_t* in, int64_t n, int64_t* out, c
 
 }  // namespace fsk
 
+// Host-buffer pipeline shared by fsk_deform_host (one frame) and fsk_deform_host_frames (the pose
+// loop of cmd_bench, fskin_cli.cpp:663-678, with cmd_deform's host copies, :395-429). Every frame is
+// split into chunks of at most kHostChunkMax points (one work item each); items alternate between
+// two device slots {bones, points, offsets, roots}, so device memory is bounded by the chunk size,
+// not by N·n_b: item i+1 uploads and searches while item i's CorrespondenceSets download. The roots
+// slot holds kSlotRootsPerQuery records per query (≈ 1.05 are kept on average); an item with more
+// kept roots than that (counted by the compaction's scan) is re-run into a buffer of exactly its
+// count (count-then-allocate, synchronous, rare). Host buffers are the caller's; a frame whose kept
+// roots exceed its capacity still reports its total and the call returns FSK_EINVAL ("root buffer
+// too small") after all frames ran — call again with cap >= total.
+namespace fsk {
+namespace {
+#ifndef FSK_HOST_CHUNK_MAX
+#define FSK_HOST_CHUNK_MAX (int64_t(1) << 22)  // 4M points per work item
+#endif
+
+int64_t host_chunks(int64_t n) {
+    // whole below 2M points (each chunk pays its own launches and float64 tail; C2 200k: 1 chunk
+    // 1.63 ms vs 4 chunks 1.99 ms), then ~2M-point chunks, at most FSK_HOST_CHUNK_MAX each
+    int64_t k = std::max<int64_t>(1, std::min<int64_t>(8, n / (1 << 21)));
+    if (const char* e = getenv("FSK_HOST_CHUNKS")) k = std::max<int64_t>(1, std::min<int64_t>(64, atoll(e)));
+    k = std::max<int64_t>(k, (n + FSK_HOST_CHUNK_MAX - 1) / FSK_HOST_CHUNK_MAX);
+    return std::max<int64_t>(1, std::min(k, std::max<int64_t>(1, n)));
+}
+
+void deform_host_pipeline(fsk_ctx* ctx, const float* weights, const GridP& g, int n_frames, const float* const* bones,
+                          const float* const* points, const int64_t* n_points, const SearchP& sp, int flags,
+                          int64_t* const* offsets, fsk_root* const* roots, const int64_t* caps, int64_t* totals,
+                          cudaStream_t st) {
+    struct Item {
+        int f;
+        int64_t p0, m;
+        bool first, last;
+    };
+    std::vector<Item> items;
+    int64_t cmax = 1;
+    for (int f = 0; f < n_frames; ++f) {
+        const int64_t n = n_points[f], k = host_chunks(n), csz = (n + k - 1) / k;
+        for (int64_t c = 0; c < k; ++c) {
+            const int64_t p0 = std::min(n, c * csz), m = std::max<int64_t>(0, std::min(csz, n - p0));
+            items.push_back({f, p0, m, c == 0, c == k - 1});
+            cmax = std::max(cmax, m);
+        }
+    }
+    const int nb = g.nb;
+    const int64_t V = vertex_count(g);
+    int64_t per_q = 4;  // kSlotRootsPerQuery
+    if (const char* e = getenv("FSK_SLOT_ROOTS_PER_QUERY")) per_q = std::max<int64_t>(0, atoll(e));  // testing override
+    const int64_t slotcap = std::max<int64_t>(1, std::min<int64_t>(cmax * nb, cmax * per_q));
+    float* dW = (float*)scratch(ctx, kHW, V * nb * sizeof(float));
+    float* dB = (float*)scratch(ctx, kFB, 2 * nb * 12 * sizeof(float));
+    float* dP = (float*)scratch(ctx, kFP, 2 * cmax * 3 * sizeof(float));
+    int64_t* dOff = (int64_t*)scratch(ctx, kFOffs, 2 * (cmax + 1) * sizeof(int64_t));
+    fsk_root* dR = (fsk_root*)scratch(ctx, kFRoots, 2 * slotcap * sizeof(fsk_root));
+    if (!ctx->copy) cuda_check(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking), "cudaStreamCreate");
+    if (!ctx->upload) cuda_check(cudaStreamCreateWithFlags(&ctx->upload, cudaStreamNonBlocking), "cudaStreamCreate");
+    if (!ctx->hcount) cuda_check(cudaMallocHost(&ctx->hcount, 64 * sizeof(int64_t)), "cudaMallocHost");
+    const int N = (int)items.size();
+    // per item: uploaded, searched, offsets downloaded, roots downloaded
+    std::vector<cudaEvent_t> ev(4 * (size_t)N + 1, nullptr);
+    struct Cleanup {  // on every exit (errors included): drain the three streams, then free the events
+        fsk_ctx* ctx;
+        cudaStream_t st;
+        std::vector<cudaEvent_t>* ev;
+        ~Cleanup() {
+            cudaStreamSynchronize(ctx->upload);
+            cudaStreamSynchronize(st);
+            cudaStreamSynchronize(ctx->copy);
+            for (auto e : *ev)
+                if (e) cudaEventDestroy(e);
+        }
+    } cleanup{ctx, st, &ev};
+    for (auto& e : ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    cudaEvent_t* up = ev.data();
+    cudaEvent_t* done = up + N;
+    cudaEvent_t* offs_ready = done + N;
+    cudaEvent_t* fetched = offs_ready + N;
+    cudaEvent_t start = ev.back();
+    cuda_check(cudaEventRecord(start, st), "cudaEventRecord");  // order after prior use of the buffers
+    cuda_check(cudaStreamWaitEvent(ctx->upload, start, 0), "cudaStreamWaitEvent");
+    cuda_check(cudaStreamWaitEvent(ctx->copy, start, 0), "cudaStreamWaitEvent");
+    cuda_check(cudaMemcpyAsync(dW, weights, V * nb * sizeof(float), cudaMemcpyHostToDevice, st), "H2D weights");
+    auto slot_b = [&](int i) { return dB + (i & 1) * nb * 12; };
+    auto slot_p = [&](int i) { return dP + (i & 1) * cmax * 3; };
+    auto slot_o = [&](int i) { return dOff + (i & 1) * (cmax + 1); };
+    auto slot_r = [&](int i) { return dR + (i & 1) * slotcap; };
+    GridPlanes P;  // the current frame's gather planes (K1 runs with the frame's first chunk)
+    auto search_item = [&](int i, fsk_root* out, int64_t cap) {
+        const Item& it = items[i];
+        const PrecomputeReq pre{dW, slot_b(i), nullptr, needs_f64(flags)};
+        const SearchState s =
+            run_search(ctx, P, g, dW, slot_b(i), slot_p(i), it.m, sp, flags, st, it.first ? &pre : nullptr);
+        compact(ctx, s, it.m, nb, slot_o(i), out, cap, st);
+    };
+    auto enqueue = [&](int i) {
+        const Item& it = items[i];
+        if (i >= 2) cuda_check(cudaStreamWaitEvent(ctx->upload, done[i - 2], 0), "cudaStreamWaitEvent");
+        cuda_check(cudaMemcpyAsync(slot_b(i), bones[it.f], nb * 12 * sizeof(float), cudaMemcpyHostToDevice, ctx->upload),
+                   "H2D bones");
+        if (it.m > 0)
+            cuda_check(cudaMemcpyAsync(slot_p(i), points[it.f] + 3 * it.p0, it.m * 3 * sizeof(float),
+                                       cudaMemcpyHostToDevice, ctx->upload),
+                       "H2D points");
+        cuda_check(cudaEventRecord(up[i], ctx->upload), "cudaEventRecord");
+        cuda_check(cudaStreamWaitEvent(st, up[i], 0), "cudaStreamWaitEvent");
+        if (i >= 2) cuda_check(cudaStreamWaitEvent(st, fetched[i - 2], 0), "cudaStreamWaitEvent");
+        search_item(i, slot_r(i), slotcap);
+        cuda_check(cudaEventRecord(done[i], st), "cudaEventRecord");
+        cuda_check(cudaStreamWaitEvent(ctx->copy, done[i], 0), "cudaStreamWaitEvent");
+        if (it.m > 0)
+            cuda_check(cudaMemcpyAsync(offsets[it.f] + it.p0, slot_o(i), it.m * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                       ctx->copy),
+                       "D2H offsets");
+        cuda_check(cudaMemcpyAsync(ctx->hcount + (i % 64), slot_o(i) + it.m, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                   ctx->copy),
+                   "D2H count");
+        cuda_check(cudaEventRecord(offs_ready[i], ctx->copy), "cudaEventRecord");
+    };
+    bool overflow = false;
+    int64_t base = 0;
+    if (N > 0) enqueue(0);
+    for (int i = 0; i < N; ++i) {
+        const Item& it = items[i];
+        if (i + 1 < N) enqueue(i + 1);  // the device runs ahead while we wait
+        cuda_check(cudaEventSynchronize(offs_ready[i]), "cudaEventSynchronize");
+        const int64_t cnt = ctx->hcount[i % 64];  // the item's kept roots
+        if (it.first) base = 0;
+        const fsk_root* src = slot_r(i);
+        if (cnt > slotcap) {
+            // more kept roots than the slot holds (k_emit dropped the rest): re-run the item into a
+            // buffer of exactly `cnt` records. Its inputs are still in slot i&1 (item i+2 is not
+            // enqueued yet); the device is drained first (item i+1 shares the search scratch).
+            cuda_check(cudaStreamSynchronize(ctx->upload), "cudaStreamSynchronize");
+            cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+            cuda_check(cudaStreamSynchronize(ctx->copy), "cudaStreamSynchronize");
+            fsk_root* big = (fsk_root*)scratch(ctx, kHRoots, cnt * sizeof(fsk_root));
+            const PrecomputeReq pre{dW, slot_b(i), nullptr, needs_f64(flags)};
+            GridPlanes Pr;
+            const SearchState s = run_search(ctx, Pr, g, dW, slot_b(i), slot_p(i), it.m, sp, flags, st, &pre);
+            compact(ctx, s, it.m, nb, slot_o(i), big, cnt, st);
+            if (i + 1 < N) {  // restore the planes of the frame of the last enqueued item (its later chunks read them)
+                const PrecomputeReq pre1{dW, slot_b(i + 1), nullptr, needs_f64(flags)};
+                P = run_precompute(ctx, pre1.w, g, pre1.bones, nullptr, nullptr, true, pre1.f64, st);
+            }
+            cuda_check(cudaEventRecord(done[i], st), "cudaEventRecord");
+            cuda_check(cudaStreamWaitEvent(ctx->copy, done[i], 0), "cudaStreamWaitEvent");
+            src = big;
+        }
+        if (base + cnt > caps[it.f] || (cnt > 0 && !roots[it.f])) {
+            overflow = true;
+        } else if (cnt > 0) {
+            cuda_check(cudaMemcpyAsync(roots[it.f] + base, src, cnt * sizeof(fsk_root), cudaMemcpyDeviceToHost, ctx->copy),
+                       "D2H roots");
+        }
+        if (base)
+            for (int64_t q = 0; q < it.m; ++q) offsets[it.f][it.p0 + q] += base;
+        base += cnt;
+        cuda_check(cudaEventRecord(fetched[i], ctx->copy), "cudaEventRecord");
+        if (cnt > slotcap) cuda_check(cudaStreamSynchronize(ctx->copy), "cudaStreamSynchronize");  // `big` is reused
+        if (it.last) {
+            offsets[it.f][n_points[it.f]] = base;
+            totals[it.f] = base;
+        }
+    }
+    cuda_check(cudaStreamSynchronize(ctx->copy), "cudaStreamSynchronize");
+    cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    if (overflow) fail(FSK_EINVAL, "fsk: root buffer too small");
+}
+}  // namespace
+}  // namespace fsk
+
 using namespace fsk;
 
 extern "C" {
@@ -1612,108 +1783,16 @@ int fsk_deform_host(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* des
         const SearchP sp = make_search(opts);
         if (n < 0) fail(FSK_EINVAL, "fsk: negative point count");
         if (!bones || !offsets || !total_out || (n > 0 && !points)) fail(FSK_EINVAL, "fsk: null buffer");
-        cudaStream_t st = (cudaStream_t)stream;
-        const int64_t V = vertex_count(g);
-        const int nb = g.nb;
-        // Pipelined over point chunks for large batches: the searches run back to back on `st`
-        // while the CorrespondenceSets of finished chunks stream to the host on the copy stream.
-        // Each chunk pays its own launches and float64-tail, so batches below 2M queries stay
-        // whole (measured on C2, 200k queries: 4 chunks 1.99 ms vs 1 chunk 1.63 ms).
-        int64_t nchunks = std::max<int64_t>(1, std::min<int64_t>(8, n / (1 << 21)));
-        if (const char* e = getenv("FSK_HOST_CHUNKS"))  // tuning override
-            nchunks = std::max<int64_t>(1, std::min<int64_t>(64, atoll(e)));
-        if (n < nchunks) nchunks = std::max<int64_t>(1, n);
-        const int64_t csz = (n + nchunks - 1) / nchunks;
-        float* dW = (float*)scratch(ctx, kHW, V * nb * sizeof(float));
-        float* dB = (float*)scratch(ctx, kHB, nb * 12 * sizeof(float));
-        float* dP = (float*)scratch(ctx, kHP, std::max<int64_t>(1, n) * 3 * sizeof(float));
-        int64_t* dOff = (int64_t*)scratch(ctx, kHOffs, (n + nchunks) * sizeof(int64_t));
-        // every root a query can have fits: no second pass after the count is known
-        fsk_root* dR = (fsk_root*)scratch(ctx, kHRoots, std::max<int64_t>(1, n * nb) * sizeof(fsk_root));
-        if (!ctx->copy) cuda_check(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking), "cudaStreamCreate");
-        if (!ctx->upload)
-            cuda_check(cudaStreamCreateWithFlags(&ctx->upload, cudaStreamNonBlocking), "cudaStreamCreate");
-        if (!ctx->hcount) cuda_check(cudaMallocHost(&ctx->hcount, 64 * sizeof(int64_t)), "cudaMallocHost");
-        cuda_check(cudaMemcpyAsync(dW, weights, V * nb * sizeof(float), cudaMemcpyHostToDevice, st), "H2D weights");
-        cuda_check(cudaMemcpyAsync(dB, bones, nb * 12 * sizeof(float), cudaMemcpyHostToDevice, st), "H2D bones");
-        std::vector<cudaEvent_t> done(nchunks), offs_ready(nchunks), up(nchunks);
-        for (int64_t c = 0; c < nchunks; ++c) {
-            cuda_check(cudaEventCreateWithFlags(&done[c], cudaEventDisableTiming), "cudaEventCreate");
-            cuda_check(cudaEventCreateWithFlags(&offs_ready[c], cudaEventDisableTiming), "cudaEventCreate");
-            cuda_check(cudaEventCreateWithFlags(&up[c], cudaEventDisableTiming), "cudaEventCreate");
-        }
-        struct Events {  // on every exit (errors included): drain the three streams, then free the events
-            fsk_ctx* ctx;
-            cudaStream_t st;
-            std::vector<cudaEvent_t>* a;
-            std::vector<cudaEvent_t>* b;
-            std::vector<cudaEvent_t>* c;
-            ~Events() {
-                cudaStreamSynchronize(ctx->upload);
-                cudaStreamSynchronize(st);
-                cudaStreamSynchronize(ctx->copy);
-                for (auto e : *a) cudaEventDestroy(e);
-                for (auto e : *b) cudaEventDestroy(e);
-                for (auto e : *c) cudaEventDestroy(e);
-            }
-        } cleanup{ctx, st, &done, &offs_ready, &up};
-        // each chunk's points upload on their own stream, ahead of (and overlapping) the
-        // previous chunks' searches
-        cuda_check(cudaEventRecord(up[0], st), "cudaEventRecord");
-        cuda_check(cudaStreamWaitEvent(ctx->upload, up[0], 0), "cudaStreamWaitEvent");  // order after prior use
-        for (int64_t c = 0; c < nchunks; ++c) {
-            const int64_t p0 = c * csz, m = std::max<int64_t>(0, std::min(csz, n - p0));
-            if (m > 0)
-                cuda_check(cudaMemcpyAsync(dP + 3 * p0, points + 3 * p0, m * 3 * sizeof(float), cudaMemcpyHostToDevice,
-                                           ctx->upload),
-                           "H2D points");
-            cuda_check(cudaEventRecord(up[c], ctx->upload), "cudaEventRecord");
-        }
-        GridPlanes P = run_precompute(ctx, dW, g, dB, nullptr, nullptr, true, needs_f64(opts->flags), st);
-        for (int64_t c = 0; c < nchunks; ++c) {
-            const int64_t p0 = c * csz, m = std::max<int64_t>(0, std::min(csz, n - p0));
-            cuda_check(cudaStreamWaitEvent(st, up[c], 0), "cudaStreamWaitEvent");
-            const SearchState s = run_search(ctx, P, g, dW, dB, dP + 3 * p0, m, sp, opts->flags, st);
-            compact(ctx, s, m, nb, dOff + p0 + c, dR + p0 * nb, m * nb, st);
-            cuda_check(cudaEventRecord(done[c], st), "cudaEventRecord");
-            cuda_check(cudaStreamWaitEvent(ctx->copy, done[c], 0), "cudaStreamWaitEvent");
-            if (m > 0)
-                cuda_check(cudaMemcpyAsync(offsets + p0, dOff + p0 + c, m * sizeof(int64_t), cudaMemcpyDeviceToHost,
-                                           ctx->copy),
-                           "D2H offsets");
-            cuda_check(cudaMemcpyAsync(ctx->hcount + c, dOff + p0 + c + m, sizeof(int64_t), cudaMemcpyDeviceToHost,
-                                       ctx->copy),
-                       "D2H count");
-            cuda_check(cudaEventRecord(offs_ready[c], ctx->copy), "cudaEventRecord");
-        }
-        int64_t base = 0;
-        for (int64_t c = 0; c < nchunks; ++c) {  // chunk c's roots stream out while later chunks compute
-            const int64_t p0 = c * csz, m = std::max<int64_t>(0, std::min(csz, n - p0));
-            cuda_check(cudaEventSynchronize(offs_ready[c]), "cudaEventSynchronize");
-            const int64_t cnt = ctx->hcount[c];  // chunk-local total
-            if (base + cnt > cap) fail(FSK_EINVAL, "fsk: root buffer too small");
-            if (cnt > 0) {
-                if (!roots) fail(FSK_EINVAL, "fsk: null buffer");
-                cuda_check(cudaMemcpyAsync(roots + base, dR + p0 * nb, cnt * sizeof(fsk_root), cudaMemcpyDeviceToHost,
-                                           ctx->copy),
-                           "D2H roots");
-            }
-            if (base)
-                for (int64_t i = 0; i < m; ++i) offsets[p0 + i] += base;
-            base += cnt;
-        }
-        offsets[n] = base;
-        *total_out = base;
-        cuda_check(cudaStreamSynchronize(ctx->copy), "cudaStreamSynchronize");
-        cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+        *total_out = 0;
+        deform_host_pipeline(ctx, weights, g, 1, &bones, &points, &n, sp, opts->flags, &offsets, &roots, &cap, total_out,
+                             (cudaStream_t)stream);
     });
 }
 
-// A sequence of frames of one subject (cmd_bench's pose loop, fskin_cli.cpp:663-678, with the
-// host copies of cmd_deform, :395-429): the weights are uploaded once, then every frame is
-// fsk_deform_host's H2D → K1 + search + compaction → D2H, double-buffered over two device
-// slots so frame f+1's upload and search run while frame f's CorrespondenceSets download.
-// Per frame the results are identical to a fsk_deform_host call.
+// A sequence of frames of one subject: the weights are uploaded once, then every frame is
+// fsk_deform_host's H2D → K1 + search + compaction → D2H, pipelined over two device slots so item
+// i+1's upload and search run while item i's CorrespondenceSets download. Per frame the results are
+// identical to a fsk_deform_host call.
 int fsk_deform_host_frames(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* desc, int32_t n_frames,
                            const float* const* bones, int32_t n_bones_pose, const float* const* points,
                            const int64_t* n_points, const fsk_search_opts* opts, int64_t* const* offsets,
@@ -1727,96 +1806,13 @@ int fsk_deform_host_frames(fsk_ctx* ctx, const float* weights, const fsk_grid_de
         if (n_frames == 0) return;
         if (!bones || !points || !n_points || !offsets || !roots || !caps || !totals)
             fail(FSK_EINVAL, "fsk: null buffer");
-        int64_t nmax = 1;
         for (int f = 0; f < n_frames; ++f) {
             if (n_points[f] < 0) fail(FSK_EINVAL, "fsk: negative point count");
             if (!bones[f] || !offsets[f] || (n_points[f] > 0 && !points[f])) fail(FSK_EINVAL, "fsk: null buffer");
-            nmax = std::max(nmax, n_points[f]);
+            totals[f] = 0;
         }
-        cudaStream_t st = (cudaStream_t)stream;
-        const int64_t V = vertex_count(g);
-        const int nb = g.nb;
-        float* dW = (float*)scratch(ctx, kHW, V * nb * sizeof(float));
-        float* dB = (float*)scratch(ctx, kFB, 2 * nb * 12 * sizeof(float));
-        float* dP = (float*)scratch(ctx, kFP, 2 * nmax * 3 * sizeof(float));
-        int64_t* dOff = (int64_t*)scratch(ctx, kFOffs, 2 * (nmax + 1) * sizeof(int64_t));
-        fsk_root* dR = (fsk_root*)scratch(ctx, kFRoots, 2 * nmax * nb * sizeof(fsk_root));
-        if (!ctx->copy) cuda_check(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking), "cudaStreamCreate");
-        if (!ctx->upload)
-            cuda_check(cudaStreamCreateWithFlags(&ctx->upload, cudaStreamNonBlocking), "cudaStreamCreate");
-        // per frame: points/bones uploaded, search done, offsets downloaded, roots downloaded
-        std::vector<cudaEvent_t> ev(4 * (size_t)n_frames + 1, nullptr);
-        struct Cleanup {  // on every exit: drain the three streams, then free the events
-            fsk_ctx* ctx;
-            cudaStream_t st;
-            std::vector<cudaEvent_t>* ev;
-            ~Cleanup() {
-                cudaStreamSynchronize(ctx->upload);
-                cudaStreamSynchronize(st);
-                cudaStreamSynchronize(ctx->copy);
-                for (auto e : *ev)
-                    if (e) cudaEventDestroy(e);
-            }
-        } cleanup{ctx, st, &ev};
-        for (auto& e : ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
-        cudaEvent_t* up = ev.data();
-        cudaEvent_t* done = up + n_frames;
-        cudaEvent_t* offs_ready = done + n_frames;
-        cudaEvent_t* fetched = offs_ready + n_frames;
-        cudaEvent_t start = ev.back();
-        cuda_check(cudaEventRecord(start, st), "cudaEventRecord");  // order after prior use of the buffers
-        cuda_check(cudaStreamWaitEvent(ctx->upload, start, 0), "cudaStreamWaitEvent");
-        cuda_check(cudaStreamWaitEvent(ctx->copy, start, 0), "cudaStreamWaitEvent");
-        cuda_check(cudaMemcpyAsync(dW, weights, V * nb * sizeof(float), cudaMemcpyHostToDevice, st), "H2D weights");
-        auto slot_b = [&](int f) { return dB + (f & 1) * nb * 12; };
-        auto slot_p = [&](int f) { return dP + (f & 1) * nmax * 3; };
-        auto slot_o = [&](int f) { return dOff + (f & 1) * (nmax + 1); };
-        auto slot_r = [&](int f) { return dR + (f & 1) * nmax * nb; };
-        auto enqueue_frame = [&](int f) {
-            const int64_t n = n_points[f];
-            if (f >= 2) cuda_check(cudaStreamWaitEvent(ctx->upload, done[f - 2], 0), "cudaStreamWaitEvent");
-            cuda_check(cudaMemcpyAsync(slot_b(f), bones[f], nb * 12 * sizeof(float), cudaMemcpyHostToDevice,
-                                       ctx->upload),
-                       "H2D bones");
-            if (n > 0)
-                cuda_check(cudaMemcpyAsync(slot_p(f), points[f], n * 3 * sizeof(float), cudaMemcpyHostToDevice,
-                                           ctx->upload),
-                           "H2D points");
-            cuda_check(cudaEventRecord(up[f], ctx->upload), "cudaEventRecord");
-            cuda_check(cudaStreamWaitEvent(st, up[f], 0), "cudaStreamWaitEvent");
-            if (f >= 2) cuda_check(cudaStreamWaitEvent(st, fetched[f - 2], 0), "cudaStreamWaitEvent");
-            GridPlanes P;  // K1 runs inside run_search, beside the spatial sort
-            const PrecomputeReq pre{dW, slot_b(f), nullptr, needs_f64(opts->flags)};
-            const SearchState s = run_search(ctx, P, g, dW, slot_b(f), slot_p(f), n, sp, opts->flags, st, &pre);
-            compact(ctx, s, n, nb, slot_o(f), slot_r(f), n * nb, st);
-            cuda_check(cudaEventRecord(done[f], st), "cudaEventRecord");
-        };
-        auto enqueue_offsets = [&](int f) {
-            cuda_check(cudaStreamWaitEvent(ctx->copy, done[f], 0), "cudaStreamWaitEvent");
-            cuda_check(cudaMemcpyAsync(offsets[f], slot_o(f), (n_points[f] + 1) * sizeof(int64_t),
-                                       cudaMemcpyDeviceToHost, ctx->copy),
-                       "D2H offsets");
-            cuda_check(cudaEventRecord(offs_ready[f], ctx->copy), "cudaEventRecord");
-        };
-        enqueue_frame(0);
-        enqueue_offsets(0);
-        for (int f = 0; f < n_frames; ++f) {
-            if (f + 1 < n_frames) enqueue_frame(f + 1);  // the device runs ahead while we wait
-            cuda_check(cudaEventSynchronize(offs_ready[f]), "cudaEventSynchronize");
-            const int64_t cnt = offsets[f][n_points[f]];
-            totals[f] = cnt;
-            if (cnt > caps[f]) fail(FSK_EINVAL, "fsk: root buffer too small");
-            if (cnt > 0) {
-                if (!roots[f]) fail(FSK_EINVAL, "fsk: null buffer");
-                cuda_check(cudaMemcpyAsync(roots[f], slot_r(f), cnt * sizeof(fsk_root), cudaMemcpyDeviceToHost,
-                                           ctx->copy),
-                           "D2H roots");
-            }
-            cuda_check(cudaEventRecord(fetched[f], ctx->copy), "cudaEventRecord");
-            if (f + 1 < n_frames) enqueue_offsets(f + 1);
-        }
-        cuda_check(cudaStreamSynchronize(ctx->copy), "cudaStreamSynchronize");
-        cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+        deform_host_pipeline(ctx, weights, g, n_frames, bones, points, n_points, sp, opts->flags, offsets, roots, caps,
+                             totals, (cudaStream_t)stream);
     });
 }
 

@@ -57,3 +57,52 @@ def test_frames_root_buffer_too_small(deformer):
     totals = deformer.deform_host_frames(hw, base.dims, base.bbox, [frames[0][0]], [frames[0][1]], _opts(base),
                                          offs[:1], roots[:1])
     assert totals[0] > 0
+
+
+@pytest.mark.parametrize("chunks,per_q", [(3, 4), (3, 0), (1, 1)])
+def test_chunked_items_and_slot_overflow_redo(deformer, monkeypatch, chunks, per_q):
+    """The host pipeline splits frames into chunk items over two bounded device slots; an item whose
+    kept roots overflow its slot (FSK_SLOT_ROOTS_PER_QUERY, here forced down to 0-1 roots per query)
+    is re-run into an exact-size buffer. Results equal the whole-frame call bit for bit."""
+    base, frames = _frames([20000, 0, 9000, 20000])
+    hw = torch.from_numpy(base.weights).pin_memory()
+    nb, o = base.n_bones, _opts(base)
+
+    def run():
+        offs = [torch.empty(p.shape[0] + 1, dtype=torch.int64).pin_memory() for _, p in frames]
+        roots = [torch.zeros((max(p.shape[0] * 2, 1), 16), dtype=torch.float32).pin_memory() for _, p in frames]
+        t = deformer.deform_host_frames(hw, base.dims, base.bbox, [b for b, _ in frames], [p for _, p in frames], o,
+                                        offs, roots)
+        return t, offs, roots
+
+    ref_t, ref_o, ref_r = run()
+    monkeypatch.setenv("FSK_HOST_CHUNKS", str(chunks))
+    monkeypatch.setenv("FSK_SLOT_ROOTS_PER_QUERY", str(per_q))
+    t, offs, roots = run()
+    assert t == ref_t
+    for f in range(len(frames)):
+        np.testing.assert_array_equal(offs[f].numpy(), ref_o[f].numpy())
+        np.testing.assert_array_equal(roots[f][:t[f]].numpy().view(np.uint32), ref_r[f][:t[f]].numpy().view(np.uint32))
+
+
+def test_host_call_reports_total_when_buffer_too_small(deformer):
+    """Count-then-allocate from the caller's side: a too-small root buffer fails with FSK_EINVAL
+    after the whole frame ran, and the reported total is exactly the capacity the retry needs."""
+    import ctypes
+
+    from paper_2211_15601_b200.deformer import _ptr, _stream, grid_desc
+    base, frames = _frames([12000])
+    b, p = frames[0]
+    hw = torch.from_numpy(base.weights).pin_memory()
+    o = _opts(base)
+    n = p.shape[0]
+    offs = torch.empty(n + 1, dtype=torch.int64).pin_memory()
+    small = torch.zeros((100, 16), dtype=torch.float32).pin_memory()
+    total = ctypes.c_int64()
+    desc = grid_desc(base.dims, base.bbox, base.n_bones)
+    rc = deformer.L.fsk_deform_host(deformer._ctx, _ptr(hw), ctypes.byref(desc), _ptr(b), base.n_bones, _ptr(p), n,
+                                    ctypes.byref(o.c()), _ptr(offs), _ptr(small), 100, ctypes.byref(total),
+                                    _stream(deformer.device))
+    assert rc == 1 and total.value > 100
+    exact = torch.zeros((total.value, 16), dtype=torch.float32).pin_memory()
+    assert deformer.deform_host(hw, base.dims, base.bbox, b, p, o, offs, exact) == total.value

@@ -34,7 +34,7 @@ def scene(deformer):
     offs_h = offs.cpu().numpy()
     has = np.diff(offs_h) > 0
     ridx = np.where(has, offs_h[:-1], -1).astype(np.int64)
-    rh = roots.cpu().numpy()
+    rh = roots[: int(offs_h[-1])].cpu().numpy()
     return sc, w, B, roots, rh, ridx, o
 
 
@@ -88,12 +88,13 @@ def test_exact_gradient_scatter_matches_oracle(deformer, scene):
 
 def test_exact_gradient_matches_finite_differences(deformer, scene):
     """SPEC.md:570 (#5a): 100 trials, each a (root, grid entry, cotangent): the exact gradient of v·x*
-    w.r.t. the entry vs central differences (h = 1e-4) of tightly re-solved roots (GPU exact replay,
-    conv_eps 1e-11·diag) on the perturbed float64 transform grid."""
+    w.r.t. the entry (the largest-gradient entry of the largest-gradient corner, as the oracle's own
+    FD test) vs central differences (h = 1e-4) of tightly re-solved roots (GPU exact replay, conv_eps
+    1e-13·diag: root noise ≪ h·gradient) on the perturbed float64 transform grid."""
     sc, w, B, roots, rh, ridx, o = scene
     tg64 = torch.empty((w.shape[0], 12), dtype=torch.float64, device="cuda")
     deformer.precompute_transform_grid(w, sc.dims, sc.bbox, B, out64=tg64)
-    tight = SearchOptions(100, 1e-11 * sc.diag, o["div_eps"], o["dedup_dist"])
+    tight = SearchOptions(200, 1e-13 * sc.diag, o["div_eps"], o["dedup_dist"])
     tight.precision = "exact64"
     rng = np.random.default_rng(11)
     qs = rng.choice(np.nonzero(ridx >= 0)[0], 100, replace=False)
@@ -118,7 +119,7 @@ def test_exact_gradient_matches_finite_differences(deformer, scene):
         vv = v.astype(np.float32).astype(np.float64)
         gT, _ = oracle.grid_vjp(sc.dims, sc.bbox, sc.bones, x0[None], np.eye(3)[None], -u[None])
         c = int(np.argmax(np.abs(gT).sum(1)))
-        e = int(rng.integers(12)) if rng.random() < 0.5 else int(np.argmax(np.abs(gT[c])))
+        e = int(np.argmax(np.abs(gT[c])))
         vals = []
         for sgn in (1, -1):
             tp = tg64.clone()
