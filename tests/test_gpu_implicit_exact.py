@@ -89,16 +89,25 @@ def test_exact_gradient_scatter_matches_oracle(deformer, scene):
 def test_exact_gradient_matches_finite_differences(deformer, scene):
     """SPEC.md:570 (#5a): 100 trials, each a (root, grid entry, cotangent): the exact gradient of v·x*
     w.r.t. the entry (the largest-gradient entry of the largest-gradient corner, as the oracle's own
-    FD test) vs central differences (h = 1e-4) of tightly re-solved roots (GPU exact replay, conv_eps
-    1e-13·diag: root noise ≪ h·gradient) on the perturbed float64 transform grid."""
+    FD test) vs central differences (h = 1e-3) of tightly re-solved roots (GPU exact replay, conv_eps
+    1e-13·diag) on the perturbed float64 transform grid."""
     sc, w, B, roots, rh, ridx, o = scene
     tg64 = torch.empty((w.shape[0], 12), dtype=torch.float64, device="cuda")
     deformer.precompute_transform_grid(w, sc.dims, sc.bbox, B, out64=tg64)
     tight = SearchOptions(200, 1e-13 * sc.diag, o["div_eps"], o["dedup_dist"])
     tight.precision = "exact64"
     rng = np.random.default_rng(11)
-    qs = rng.choice(np.nonzero(ridx >= 0)[0], 100, replace=False)
-    rel, h = [], 1e-4
+    # roots strictly inside the canonical bbox: outside it the cell lookup clamps x, so d(x) is constant
+    # along the clamped axis in T while the reference's analytic Jacobian keeps the ±1/h stencil
+    # (skinning.cpp:164-193) — there neither the reference's nor this exact gradient is d(v·x*)/dT
+    xr = rh[np.maximum(ridx, 0), :3]
+    lo, hi = sc.bbox[:3].astype(np.float64), sc.bbox[3:].astype(np.float64)
+    margin = 1e-3 * (hi - lo)
+    inside = (ridx >= 0) & ((xr > lo + margin) & (xr < hi - margin)).all(1)
+    qs = rng.choice(np.nonzero(inside)[0], 120, replace=False)
+    # h = 1e-3: the GPU returns roots in float32 (ulp 6e-8 at |x| ~ 1), so h = 1e-4 would leave 3e-4 of
+    # rounding noise in the difference; the O(h^2) truncation at 1e-3 stays ~1e-5
+    rel, h = [], 1e-3
     for q in qs:
         bone = int(rh[ridx[q], 13].view(np.int32))
         xq = dev(sc.points[q:q + 1])
@@ -128,10 +137,12 @@ def test_exact_gradient_matches_finite_differences(deformer, scene):
             vals.append(xp @ vv)
         fd = (vals[0] - vals[1]) / (2 * h)
         rel.append(abs(fd - gT[c, e]) / max(abs(gT[c, e]), 1e-12))
+        if len(rel) == 100:
+            break
     rel = np.array(rel)
     print(f"\nexact vs FD: {len(rel)} trials, rel. error median {np.median(rel):.1e}, "
           f"share < 1e-3: {(rel < 1e-3).mean():.3f}")
-    assert len(rel) >= 95
+    assert len(rel) == 100
     assert (rel < 1e-3).mean() >= 0.95
 
 
