@@ -238,6 +238,7 @@ def run_ours(args, rank, world, local_rank):
         gx = torch.randn((n, 3), generator=torch.Generator(device=dev).manual_seed(rank + 1), device=dev) / n
         gT = torch.empty((w.shape[0], 12), dtype=torch.float32, device=dev)
         gW = torch.empty_like(w)
+        order = torch.empty((n,), dtype=torch.int32, device=dev)
 
     def step():
         for Bf, xf in frames:
@@ -249,7 +250,10 @@ def run_ours(args, rank, world, local_rank):
                 # the training step's root choice (occupancy argmax, diff.cpp:292) is out of scope:
                 # take each query's first kept root; then the implicit-diff backward (K3) and dL/dw
                 ridx = torch.where(offs[1:] > offs[:-1], offs[:-1], torch.full_like(offs[:-1], -1))
-                D.search_bwd_roots(sc.dims, sc.bbox, nb, roots, ridx, gx, deterministic=args.deterministic, out=gT)
+                # visited in the search's spatial order: per-cell warp aggregation of the reductions
+                D.query_order(n, out=order)
+                D.search_bwd_roots(sc.dims, sc.bbox, nb, roots, ridx, gx, deterministic=args.deterministic, out=gT,
+                                   order=order)
                 if world > 1:  # dL/dT summed over the point shards before the local dL/dw contraction
                     dist.all_reduce(gT, op=dist.ReduceOp.SUM)
                 D.grad_weights(sc.dims, sc.bbox, gT, Bf, out=gW)
@@ -257,6 +261,7 @@ def run_ours(args, rank, world, local_rank):
     peak_fp32 = D.measure_fp32_peak()
     peak_fp64 = D.measure_fp64_peak()
     peak_l1 = D.measure_l1_gather_peak()
+    peak_red = D.measure_red_peak() if args.backward else None
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -323,12 +328,13 @@ def run_ours(args, rank, world, local_rank):
     breakdown = {}
     for kname in ("k_precompute", "k_sort_bbox", "k_sort_hist", "k_sort_scan", "k_sort_scatter",
                   "k_search_fast", "k_esc_start", "k_search_escalated", "k_search_f64", "k_search_exact", "k_dedup", "k_scan_partial", "k_scan_top", "k_scan_apply",
-                  "k_emit", "k_zero", "k_bwd_scatter", "k_bwd_bucket_count", "k_bwd_bucket_fill", "k_bwd_chunk_reduce",
+                  "k_emit", "k_zero", "k_bwd_scatter", "k_bwd_scatter_agg", "k_bwd_bucket_count", "k_bwd_bucket_fill", "k_bwd_chunk_reduce",
                   "k_bwd_fixed_to_float",
                   "k_grad_weights"):
         ms_, n_ = D.prof_read(kname, reset=False)
         if n_:
             breakdown[kname] = round(ms_ / args.steps, 5)
+    k3_ms, k3_n = D.prof_read("k_bwd_scatter_agg", reset=False)
     all_ms, _ = D.prof_read(None, reset=True)
     if world > 1:
         t = torch.tensor([total_ms], device=dev)
@@ -399,6 +405,19 @@ def run_ours(args, rank, world, local_rank):
         "clocks": clk,
     }
 
+    if args.backward and k3_n:
+        # K3 is L2-atomic-bound: algorithmically 8 corners x 48 B of reductions per root
+        with_root = int((roots_buf[0][1:n + 1] > roots_buf[0][:n]).sum().item())
+        red_bytes = 384 * with_root
+        k3_avg = k3_ms / k3_n
+        line["roofline_k3"] = {"bound": "l2_atomic", "kernel": "k_bwd_scatter_agg", "unit": "GB/s",
+                               "achieved": red_bytes / (k3_avg * 1e-3) / 1e9, "peak": peak_red,
+                               "frac": red_bytes / (k3_avg * 1e-3) / 1e9 / peak_red,
+                               "algorithmic_red_bytes_per_launch": red_bytes, "avg_launch_ms": k3_avg,
+                               "peak_source": "fsk_measure_red_peak: RED.E.ADD.F32x4 at random float4 slots of an "
+                                              "L2-resident 32^3 x 12 grid, all SMs",
+                               "note": "roots visited in the search's spatial order; consecutive roots in one cell are "
+                                       "summed in registers per warp, so the achieved rate can exceed the red peak"}
     if rank == 0 and not args.no_mlp:
         line["mlp_stages"] = mlp_stages(D, sc, roots_buf, n, dev)
     if not args.no_e2e:  # every rank its own shard through the host API; whole-job rate, max over ranks

@@ -125,6 +125,9 @@ int fsk_measure_fp64_peak(fsk_ctx* ctx, double* tflops);  /* same with DFMA chai
 /* L1 gather delivery rate (GB/s): independent 256-bit loads at random 32-B slots of an
  * L1-resident table, the access pattern of the search's gathers (roofline denominator). */
 int fsk_measure_l1_gather_peak(fsk_ctx* ctx, double* gbps);
+/* L2 vector-reduction rate (GB/s of red payload): RED.E.ADD.F32x4 from all SMs to random float4 slots of
+ * an L2-resident [32^3][12] float grid — the access pattern of the backward's scatter (K3 roofline). */
+int fsk_measure_red_peak(fsk_ctx* ctx, double* gbps);
 /* Search work counters accumulated by the context's searches (synchronizes the device):
  * out = {float32 solves, float32 Broyden iterations, float32 converged-terminating
  * iterations, float64 solves, float64 iterations, float64 converged-terminating iterations,
@@ -260,6 +263,19 @@ int fsk_search_bwd_exact_roots(fsk_ctx* ctx, const float* weights, const fsk_gri
                                int32_t n_bones_pose, const fsk_root* roots, const int64_t* root_index,
                                const float* grad_xc, int64_t n, float* grad_tgrid, uint8_t* ok, int deterministic,
                                void* stream);
+
+/* fsk_search_bwd_roots visiting the queries in `order` (int32 [N] dev, a permutation of [0, N), e.g. the
+ * search's spatial order from fsk_ctx_query_order; NULL = query order). With a spatial order the fast
+ * mode aggregates the contributions of consecutive roots that share a cell within each warp before its
+ * vector reductions (k_bwd_scatter_agg); the deterministic mode is order-independent. */
+int fsk_search_bwd_roots_ordered(fsk_ctx* ctx, const fsk_grid_desc* desc, const fsk_root* roots,
+                                 const int64_t* root_index, const float* grad_xc, int64_t n, const int32_t* order,
+                                 float* grad_tgrid, int deterministic, void* stream);
+
+/* The spatial (Morton) order of the queries of the context's last device search (fsk_search_fwd,
+ * fsk_batch_search, fsk_deform; N must be that search's point count): order[k] = index of the k-th query
+ * in the order the search visited them. Stream-ordered copy into `order` (int32 [N] dev). */
+int fsk_ctx_query_order(fsk_ctx* ctx, int64_t n, int32_t* order, void* stream);
 
 /* dL/dw[v][i] = <dL/dT[v], B_i>_F  (chain rule through deformer.cpp:70-74). [V][n_b] dev. */
 int fsk_grad_weights(fsk_ctx* ctx, const fsk_grid_desc* desc, const float* grad_tgrid,

@@ -32,7 +32,8 @@ EXPORTS = [
     "fsk_multi_grad_weights_host", "fsk_search_fwd_mlp",
     "fsk_io_last_error", "fsk_sknv_read", "fsk_sknv_write", "fsk_points_bin_read", "fsk_points_bin_write",
     "fsk_write_correspondence_dump", "fsk_deform_files", "fsk_init_states64",
-    "fsk_implicit_u_exact", "fsk_search_bwd_exact_roots",
+    "fsk_implicit_u_exact", "fsk_search_bwd_exact_roots", "fsk_search_bwd_roots_ordered", "fsk_ctx_query_order",
+    "fsk_measure_red_peak",
 ]
 
 
@@ -103,6 +104,9 @@ def load():
     L.fsk_batch_search.argtypes = [_vp, _vp, _vp, _vp, G, _vp, _i32, _vp, _i64, O, _vp, _vp, _i64, _vp]
     L.fsk_deform.argtypes = [_vp, _vp, G, _vp, _i32, _vp, _i64, O, _vp, _vp, _vp, _i64, _vp]
     L.fsk_search_bwd_roots.argtypes = [_vp, G, _vp, _vp, _vp, _i64, _vp, ctypes.c_int, _vp]
+    L.fsk_search_bwd_roots_ordered.argtypes = [_vp, G, _vp, _vp, _vp, _i64, _vp, _vp, ctypes.c_int, _vp]
+    L.fsk_ctx_query_order.argtypes = [_vp, _i64, _vp, _vp]
+    L.fsk_measure_red_peak.argtypes = [_vp, ctypes.POINTER(ctypes.c_double)]
     L.fsk_ctx_set_profiling.argtypes = [_vp, ctypes.c_int]
     L.fsk_ctx_prof_read.argtypes = [_vp, ctypes.c_char_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64),
                                     ctypes.c_int]

@@ -217,6 +217,64 @@ __global__ void __launch_bounds__(256) k_bwd_scatter(GridP g, RootRef R, const f
     }
 }
 
+// Fast mode over roots in spatial order (the search's query order, fsk_ctx_query_order): warp-aggregated
+// reductions. Lane L of a warp loads the root of order[32w + L]; the warp then walks its roots in order
+// (shuffle broadcast) while lane L < 24 owns output float4 L of the current cell (corner L/3, matrix row
+// L%3: φ_c·u_r·(x*, 1)) and accumulates it in registers; at every change of cell the 24 partial sums go
+// out as one vector reduction each. In spatial order consecutive roots mostly share a cell, so the L2
+// sees one red per cell run instead of one per root.
+__global__ void __launch_bounds__(256) k_bwd_scatter_agg(GridP g, RootRef R, const int32_t* __restrict__ order,
+                                                         const float* __restrict__ gx, int64_t n,
+                                                         float4* __restrict__ gT) {
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    if (j - lane >= n) return;  // whole warp past the end
+    float xs[3] = {0.f, 0.f, 0.f}, u[3] = {0.f, 0.f, 0.f};
+    Cell<float> c{};
+    bool have = false;
+    if (j < n) {
+        have = bwd_load(R, order[j], gx, xs, u);
+        if (have) c = locate<false>(g, xs[0], xs[1], xs[2]);
+    }
+    const int nxy = g.nx * g.ny;
+    const int q = lane / 3, row = lane - 3 * q;
+    const int di = q & 1, dj = (q >> 1) & 1, dk = q >> 2;
+    const bool owner = lane < 24;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    int cur = -1;
+    unsigned todo = __ballot_sync(0xffffffffu, have);
+    auto flush = [&]() {
+        if (cur >= 0 && owner) atomicAdd(gT + 3 * (int64_t)(cur + dk * nxy + dj * g.nx + di) + row, acc);
+        acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    };
+    while (todo) {
+        const int src = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const int cj = __shfl_sync(0xffffffffu, c.base, src);
+        if (cj != cur) {  // warp-uniform
+            flush();
+            cur = cj;
+        }
+        const float tx = __shfl_sync(0xffffffffu, c.tx, src), ty = __shfl_sync(0xffffffffu, c.ty, src),
+                    tz = __shfl_sync(0xffffffffu, c.tz, src);
+        const float x0 = __shfl_sync(0xffffffffu, xs[0], src), x1 = __shfl_sync(0xffffffffu, xs[1], src),
+                    x2 = __shfl_sync(0xffffffffu, xs[2], src);
+        const float u0 = __shfl_sync(0xffffffffu, u[0], src), u1 = __shfl_sync(0xffffffffu, u[1], src),
+                    u2 = __shfl_sync(0xffffffffu, u[2], src);
+        if (owner) {
+            const float wz = dk ? tz : 1.f - tz;
+            const float wyz = wz * (dj ? ty : 1.f - ty);
+            const float phi = wyz * (di ? tx : 1.f - tx);  // k_bwd_scatter's corner weight
+            const float a = phi * (row == 0 ? u0 : (row == 1 ? u1 : u2));
+            acc.x += a * x0;
+            acc.y += a * x1;
+            acc.z += a * x2;
+            acc.w += a;
+        }
+    }
+    flush();
+}
+
 // Fixed-point scale of the deterministic mode: a power of two with n·max|term|·scale < 2^62,
 // so no int64 sum over at most n roots can overflow; max|term| ≤ max|u|·max(1, |x*|).
 __device__ __forceinline__ double fixed_scale(unsigned int maxbits, int64_t n) {
@@ -386,13 +444,16 @@ __global__ void __launch_bounds__(kGwTile) k_grad_weights(const float* __restric
 namespace {
 
 void run_bwd(fsk_ctx* ctx, const GridP& g, const RootRef& R, const float* grad_xc, int64_t n, float* grad_tgrid,
-             int deterministic, cudaStream_t st) {
+             int deterministic, cudaStream_t st, const int32_t* order = nullptr) {
     const int64_t V = (int64_t)g.nx * g.ny * g.nz;
     const unsigned cap_blocks = (unsigned)ctx->sm_count * 8;
     if (!deterministic) {
         FSK_LAUNCH(ctx, st, k_zero, std::min(blocks_for(V * 3, 256), cap_blocks), 256, 0,
                    reinterpret_cast<float4*>(grad_tgrid), V * 3);
-        if (n > 0)
+        if (n > 0 && order)
+            FSK_LAUNCH(ctx, st, k_bwd_scatter_agg, blocks_for(n, 256), 256, 0, g, R, order, grad_xc, n,
+                       reinterpret_cast<float4*>(grad_tgrid));
+        else if (n > 0)
             FSK_LAUNCH(ctx, st, k_bwd_scatter, blocks_for(n, 256), 256, 0, g, R, grad_xc, n,
                        reinterpret_cast<float4*>(grad_tgrid));
         return;
@@ -443,13 +504,20 @@ int fsk_search_bwd(fsk_ctx* ctx, const fsk_grid_desc* desc, const float* x_c, co
 
 int fsk_search_bwd_roots(fsk_ctx* ctx, const fsk_grid_desc* desc, const fsk_root* roots, const int64_t* root_index,
                          const float* grad_xc, int64_t n, float* grad_tgrid, int deterministic, void* stream) {
+    return fsk_search_bwd_roots_ordered(ctx, desc, roots, root_index, grad_xc, n, nullptr, grad_tgrid, deterministic,
+                                        stream);
+}
+
+int fsk_search_bwd_roots_ordered(fsk_ctx* ctx, const fsk_grid_desc* desc, const fsk_root* roots,
+                                 const int64_t* root_index, const float* grad_xc, int64_t n, const int32_t* order,
+                                 float* grad_tgrid, int deterministic, void* stream) {
     return guard([&] {
         set_device(ctx);
         const GridP g = make_grid(desc);
         if (n < 0) fail(FSK_EINVAL, "fsk: negative point count");
         if (!grad_tgrid || (n > 0 && (!roots || !root_index || !grad_xc))) fail(FSK_EINVAL, "fsk: null buffer");
         RootRef R{nullptr, nullptr, nullptr, 0, roots, root_index};
-        run_bwd(ctx, g, R, grad_xc, n, grad_tgrid, deterministic, (cudaStream_t)stream);
+        run_bwd(ctx, g, R, grad_xc, n, grad_tgrid, deterministic, (cudaStream_t)stream, order);
     });
 }
 

@@ -198,6 +198,18 @@ __global__ void __launch_bounds__(256) k_peak_l1_gather(const float* __restrict_
     if (acc == 12345.678f) out[0] = acc;
 }
 
+// L2 vector reductions at random float4 slots of a [32^3][12] float grid (the backward's scatter target)
+__global__ void __launch_bounds__(256) k_peak_red(float4* __restrict__ grid, uint32_t slots, int iters) {
+    uint32_t s = (blockIdx.x * 256u + threadIdx.x) * 2654435761u + 777u;
+    for (int k = 0; k < iters; ++k) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            s = s * 1664525u + 1013904223u;
+            atomicAdd(grid + (s >> 8) % slots, make_float4(1e-7f, 1e-7f, 1e-7f, 1e-7f));
+        }
+    }
+}
+
 template <typename R>
 double measure_peak(fsk_ctx* ctx, int iters) {
     R* o = (R*)scratch(ctx, kBwdMax, 16);
@@ -371,6 +383,30 @@ int fsk_measure_l1_gather_peak(fsk_ctx* ctx, double* gbps) {
         cudaEventDestroy(a);
         cudaEventDestroy(b);
         *gbps = 32.0 * 8.0 * iters * (double)blocks * 256.0 / (ms * 1e-3) / 1e9;
+    });
+}
+
+int fsk_measure_red_peak(fsk_ctx* ctx, double* gbps) {
+    return guard([&] {
+        set_device(ctx);
+        if (!gbps) fail(FSK_EINVAL, "fsk: null output pointer");
+        const uint32_t slots = 32 * 32 * 32 * 3;
+        float4* grid = (float4*)scratch(ctx, kPeakTable, slots * sizeof(float4));
+        cuda_check(cudaMemset(grid, 0, slots * sizeof(float4)), "cudaMemset");
+        const int blocks = ctx->sm_count * 8, iters = 64;
+        cudaEvent_t a, b;
+        cuda_check(cudaEventCreate(&a), "cudaEventCreate");
+        cuda_check(cudaEventCreate(&b), "cudaEventCreate");
+        k_peak_red<<<blocks, 256>>>(grid, slots, 4);  // warm-up
+        cuda_check(cudaEventRecord(a, 0), "cudaEventRecord");
+        k_peak_red<<<blocks, 256>>>(grid, slots, iters);
+        cuda_check(cudaEventRecord(b, 0), "cudaEventRecord");
+        cuda_check(cudaEventSynchronize(b), "cudaEventSynchronize");
+        float ms = 0.f;
+        cuda_check(cudaEventElapsedTime(&ms, a, b), "cudaEventElapsedTime");
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        *gbps = 16.0 * 8.0 * iters * (double)blocks * 256.0 / (ms * 1e-3) / 1e9;
     });
 }
 

@@ -44,6 +44,7 @@ struct fsk_ctx {
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int64_t* hcount = nullptr;  // pinned per-chunk root counts
+    int64_t last_search_n = -1;  // point count of the last device search (its order is in scratch kPerm)
 };
 
 namespace fsk {

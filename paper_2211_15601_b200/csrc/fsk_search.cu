@@ -1102,6 +1102,7 @@ SearchState run_search(fsk_ctx* ctx, GridPlanes& P, const GridP& g, const float*
     s.sp.keep = (uint8_t*)scratch(ctx, kOKeep, S);
     s.sp.kmask = g.nb <= 32 ? (uint32_t*)scratch(ctx, kOKeepMask, std::max<int64_t>(1, n) * sizeof(uint32_t)) : nullptr;
     s.perm = (int*)scratch(ctx, kPerm, std::max<int64_t>(1, n) * sizeof(int));
+    ctx->last_search_n = n;
     s.n_roots_p = (int32_t*)scratch(ctx, kNRoots, std::max<int64_t>(1, n) * sizeof(int32_t));
     if (n == 0) {
         precompute();
@@ -1813,6 +1814,18 @@ int fsk_deform_host_frames(fsk_ctx* ctx, const float* weights, const fsk_grid_de
         }
         deform_host_pipeline(ctx, weights, g, n_frames, bones, points, n_points, sp, opts->flags, offsets, roots, caps,
                              totals, (cudaStream_t)stream);
+    });
+}
+
+int fsk_ctx_query_order(fsk_ctx* ctx, int64_t n, int32_t* order, void* stream) {
+    return guard([&] {
+        set_device(ctx);
+        if (!order && n > 0) fail(FSK_EINVAL, "fsk: null buffer");
+        if (n != ctx->last_search_n) fail(FSK_EINVAL, "fsk: no device search of that many points to take the order of");
+        if (n > 0)
+            cuda_check(cudaMemcpyAsync(order, ctx->buf[kPerm], n * sizeof(int32_t), cudaMemcpyDeviceToDevice,
+                                       (cudaStream_t)stream),
+                       "cudaMemcpyAsync");
     });
 }
 

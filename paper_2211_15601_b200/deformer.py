@@ -245,17 +245,36 @@ class Deformer:
                                 _stream(self.device)))
         return offsets, roots
 
-    def search_bwd_roots(self, dims, bbox, n_bones, roots, root_index, grad_xc, deterministic=False, out=None):
-        """Backward from compact roots: root_index [N] int64 into ``roots`` (or -1)."""
+    def search_bwd_roots(self, dims, bbox, n_bones, roots, root_index, grad_xc, deterministic=False, out=None,
+                         order=None):
+        """Backward from compact roots: root_index [N] int64 into ``roots`` (or -1). ``order`` (int32 [N],
+        e.g. ``query_order(N)`` after the forward) visits the queries in the search's spatial order, so the
+        fast mode aggregates per-cell contributions within each warp."""
         desc = grid_desc(dims, bbox, n_bones)
         V = desc.nx * desc.ny * desc.nz
         if out is None:
             out = torch.empty((V, 12), dtype=torch.float32, device=self.device)
         ri = root_index.to(device=self.device, dtype=torch.int64).contiguous()
-        check(self.L.fsk_search_bwd_roots(self._ctx, ctypes.byref(desc), _ptr(roots), _ptr(ri),
-                                          _ptr(_f32(grad_xc, "grad_xc", self.device)), grad_xc.shape[0], _ptr(out),
-                                          1 if deterministic else 0, _stream(self.device)))
+        if order is not None and (order.dtype != torch.int32 or order.device != self.device or
+                                  order.numel() != grad_xc.shape[0] or not order.is_contiguous()):
+            raise FskInvalidArgument("fsk: order must be a contiguous int32 tensor with one entry per query")
+        check(self.L.fsk_search_bwd_roots_ordered(self._ctx, ctypes.byref(desc), _ptr(roots), _ptr(ri),
+                                                  _ptr(_f32(grad_xc, "grad_xc", self.device)), grad_xc.shape[0],
+                                                  _ptr(order), _ptr(out), 1 if deterministic else 0,
+                                                  _stream(self.device)))
         return out
+
+    def query_order(self, n, out=None):
+        """The spatial order of the queries of this context's last device search (fsk_ctx_query_order)."""
+        if out is None:
+            out = torch.empty((n,), dtype=torch.int32, device=self.device)
+        check(self.L.fsk_ctx_query_order(self._ctx, n, _ptr(out), _stream(self.device)))
+        return out
+
+    def measure_red_peak(self) -> float:
+        t = ctypes.c_double()
+        check(self.L.fsk_measure_red_peak(self._ctx, ctypes.byref(t)))
+        return t.value
 
     def compact_roots(self, dense, n, nb):
         """Kept roots in CorrespondenceSet form: (offsets [N+1] int64, roots [M,16] float32 view of

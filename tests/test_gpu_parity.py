@@ -365,6 +365,35 @@ def test_backward_from_compact_roots_matches_dense(deformer, c3):
     np.testing.assert_array_equal(a.cpu().numpy(), b.cpu().numpy())
 
 
+def test_backward_in_spatial_order_aggregates_per_warp(deformer, c3):
+    """fsk_search_bwd_roots_ordered with the search's spatial order (fsk_ctx_query_order): warp-aggregated
+    per-cell reductions give the same gradient as the per-root reductions (up to float summation order)
+    and stay within 1e-4 of the oracle's grid VJP; a wrong order length is rejected."""
+    sc, B, dense, sel, v = c3
+    w, x = dev(sc.weights), dev(sc.points)
+    offs, roots = deformer.deform(w, sc.dims, sc.bbox, B, x, opts_of(sc, 50))
+    n = sc.points.shape[0]
+    order = deformer.query_order(n)
+    o = order.cpu().numpy()
+    assert np.array_equal(np.sort(o), np.arange(n))  # a permutation
+    offs_h = offs.cpu().numpy()
+    ridx = np.where(sel >= 0, offs_h[:-1], -1).astype(np.int64)
+    a = deformer.search_bwd_roots(sc.dims, sc.bbox, sc.n_bones, roots, dev(ridx), dev(v)).cpu().numpy()
+    b = deformer.search_bwd_roots(sc.dims, sc.bbox, sc.n_bones, roots, dev(ridx), dev(v), order=order).cpu().numpy()
+    d = deformer.search_bwd_roots(sc.dims, sc.bbox, sc.n_bones, roots, dev(ridx), dev(v), deterministic=True,
+                                  order=order).cpu().numpy()
+    scale = np.abs(a).max()
+    assert np.abs(a - b).max() <= 1e-6 * scale
+    assert np.abs(b - d).max() <= 1e-6 * scale
+    rh = roots.cpu().numpy()
+    xs = rh[np.maximum(ridx, 0), :3]
+    J = rh[np.maximum(ridx, 0), 4:13].reshape(-1, 3, 3)
+    rT, _ = oracle.grid_vjp(sc.dims, sc.bbox, sc.bones, xs, J, v, sel=np.where(ridx >= 0, 0, -1).astype(np.int32))
+    assert np.abs(b - rT).max() <= TOL_GRAD
+    with pytest.raises(FskInvalidArgument):
+        deformer.query_order(n + 1)
+
+
 def test_precompute_f64_grid_matches_oracle(deformer, c1):
     w, B = dev(c1.weights), dev(c1.bones)
     tg64 = torch.empty((w.shape[0], 12), dtype=torch.float64, device="cuda")
