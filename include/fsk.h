@@ -94,6 +94,9 @@ typedef struct fsk_search_out {
     uint8_t* converged;   /* [N][n_b] 1 iff residual < conv_eps was reached */
     uint8_t* keep;        /* [N][n_b] dedup survivors */
     int32_t* n_roots;     /* [N] kept roots per point */
+    double* x_c64;        /* [N][n_b][3] optional: Root::x in float64 — the float64 state of the solves the
+                             float64 pass ran (escalated / FSK_SEARCH_FP64 / EXACT64), the float32 root
+                             widened otherwise */
 } fsk_search_out;
 
 /* Compact root record — one kept Root, in bone order per query (CorrespondenceSet). */
@@ -276,6 +279,30 @@ int fsk_search_bwd_roots_ordered(fsk_ctx* ctx, const fsk_grid_desc* desc, const 
  * fsk_batch_search, fsk_deform; N must be that search's point count): order[k] = index of the k-th query
  * in the order the search visited them. Stream-ordered copy into `order` (int32 [N] dev). */
 int fsk_ctx_query_order(fsk_ctx* ctx, int64_t n, int32_t* order, void* stream);
+
+/* ---- deterministic backward across devices or ranks. The deterministic mode rounds every term to int64
+ * fixed point with a power-of-two scale from (max term, n): scale = 2^(61 - floor(log2(max·n))). With
+ * the max over ALL shards and n = the total point count on every shard, the int64 sums of the shards add
+ * up (ncclInt64 sum) to exactly the one-device sums, so the gradient is bitwise the same for any number
+ * of devices. Per shard: fsk_search_bwd_max_term → all-reduce MAX of the float → fsk_search_bwd_fixed
+ * (accumulates into acc, which the caller zeroes) → all-reduce SUM of acc → fsk_fixed_to_float.
+ * Roots are given densely (x_c, jinv, root_sel, n_init as fsk_search_bwd) or compact (roots,
+ * root_index as fsk_search_bwd_roots, when roots != NULL). */
+typedef struct fsk_bwd_src {
+    const float* x_c;
+    const float* jinv;
+    const int32_t* root_sel;
+    int32_t n_init;
+    const fsk_root* roots;
+    const int64_t* root_index;
+} fsk_bwd_src;
+int fsk_search_bwd_max_term(fsk_ctx* ctx, const fsk_grid_desc* desc, const fsk_bwd_src* src, const float* grad_xc,
+                            int64_t n, float* max_term /* dev, 1 float, overwritten */, void* stream);
+int fsk_search_bwd_fixed(fsk_ctx* ctx, const fsk_grid_desc* desc, const fsk_bwd_src* src, const float* grad_xc,
+                         int64_t n, int64_t n_scale, const float* max_term /* dev */, int64_t* acc /* dev [V][12] */,
+                         void* stream);
+int fsk_fixed_to_float(fsk_ctx* ctx, const int64_t* acc, int64_t m, int64_t n_scale, const float* max_term,
+                       float* out, void* stream);
 
 /* dL/dw[v][i] = <dL/dT[v], B_i>_F  (chain rule through deformer.cpp:70-74). [V][n_b] dev. */
 int fsk_grad_weights(fsk_ctx* ctx, const fsk_grid_desc* desc, const float* grad_tgrid,

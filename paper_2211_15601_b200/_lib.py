@@ -33,7 +33,7 @@ EXPORTS = [
     "fsk_io_last_error", "fsk_sknv_read", "fsk_sknv_write", "fsk_points_bin_read", "fsk_points_bin_write",
     "fsk_write_correspondence_dump", "fsk_deform_files", "fsk_init_states64",
     "fsk_implicit_u_exact", "fsk_search_bwd_exact_roots", "fsk_search_bwd_roots_ordered", "fsk_ctx_query_order",
-    "fsk_measure_red_peak",
+    "fsk_measure_red_peak", "fsk_search_bwd_max_term", "fsk_search_bwd_fixed", "fsk_fixed_to_float",
 ]
 
 
@@ -50,7 +50,12 @@ class SearchOpts(ctypes.Structure):
 class SearchOut(ctypes.Structure):
     _fields_ = [("x_c", ctypes.c_void_p), ("jinv", ctypes.c_void_p), ("resid", ctypes.c_void_p),
                 ("iters", ctypes.c_void_p), ("converged", ctypes.c_void_p), ("keep", ctypes.c_void_p),
-                ("n_roots", ctypes.c_void_p)]
+                ("n_roots", ctypes.c_void_p), ("x_c64", ctypes.c_void_p)]
+
+
+class BwdSrc(ctypes.Structure):
+    _fields_ = [("x_c", ctypes.c_void_p), ("jinv", ctypes.c_void_p), ("root_sel", ctypes.c_void_p),
+                ("n_init", ctypes.c_int32), ("roots", ctypes.c_void_p), ("root_index", ctypes.c_void_p)]
 
 
 class Root(ctypes.Structure):
@@ -107,6 +112,10 @@ def load():
     L.fsk_search_bwd_roots_ordered.argtypes = [_vp, G, _vp, _vp, _vp, _i64, _vp, _vp, ctypes.c_int, _vp]
     L.fsk_ctx_query_order.argtypes = [_vp, _i64, _vp, _vp]
     L.fsk_measure_red_peak.argtypes = [_vp, ctypes.POINTER(ctypes.c_double)]
+    BS = ctypes.POINTER(BwdSrc)
+    L.fsk_search_bwd_max_term.argtypes = [_vp, G, BS, _vp, _i64, _vp, _vp]
+    L.fsk_search_bwd_fixed.argtypes = [_vp, G, BS, _vp, _i64, _i64, _vp, _vp, _vp]
+    L.fsk_fixed_to_float.argtypes = [_vp, _vp, _i64, _i64, _vp, _vp, _vp]
     L.fsk_ctx_set_profiling.argtypes = [_vp, ctypes.c_int]
     L.fsk_ctx_prof_read.argtypes = [_vp, ctypes.c_char_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64),
                                     ctypes.c_int]

@@ -320,6 +320,23 @@ __global__ void __launch_bounds__(256) k_bwd_bucket_count(GridP g, RootRef R, co
     if ((threadIdx.x & 31) == 0) atomicMax(maxbits, __float_as_uint(m));
 }
 
+__global__ void __launch_bounds__(256) k_bwd_max_term(RootRef R, const float* __restrict__ gx, int64_t n,
+                                                      unsigned int* __restrict__ maxbits) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    float m = 0.f;
+    if (p < n) {
+        float xs[3], u[3];
+        if (bwd_load(R, p, gx, xs, u)) {  // the max term of k_bwd_bucket_count
+            const float mu = fmaxf(fabsf(u[0]), fmaxf(fabsf(u[1]), fabsf(u[2])));
+            const float mx = fmaxf(1.f, fmaxf(fabsf(xs[0]), fmaxf(fabsf(xs[1]), fabsf(xs[2]))));
+            m = mu * mx;
+            if (!isfinite(m)) m = 3.0e38f;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffff, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(maxbits, __float_as_uint(m));
+}
+
 __global__ void __launch_bounds__(256) k_bwd_bucket_fill(RootRef R, const float* __restrict__ gx, int64_t n,
                                                          const int32_t* __restrict__ cell_of,
                                                          const int64_t* __restrict__ start, int32_t* __restrict__ fill,
@@ -443,6 +460,41 @@ __global__ void __launch_bounds__(kGwTile) k_grad_weights(const float* __restric
 
 namespace {
 
+// Deterministic accumulation: zero, bucket the roots by cell (per-warp max term into this call's own
+// max slot), scan, fill, reduce into int64 fixed point. The scale comes from (max term, n_scale):
+// this call's max and n unless `max_ext` (a float on the device, e.g. the max over all devices or
+// ranks) is given, and the sums go into `acc_ext` ([V][12] int64, accumulated into) when given, else
+// into the context's zeroed scratch (returned). Integer sums: any split of the roots over devices,
+// with the same (max, n_scale), adds up to the same bits.
+unsigned long long* det_accumulate(fsk_ctx* ctx, const GridP& g, const RootRef& R, const float* grad_xc, int64_t n,
+                                   int64_t n_scale, const float* max_ext, long long* acc_ext, cudaStream_t st,
+                                   unsigned int** mx_out) {
+    const int64_t V = (int64_t)g.nx * g.ny * g.nz;
+    const unsigned cap_blocks = (unsigned)ctx->sm_count * 8;
+    const int64_t V4 = (V + 3) / 4 * 4;  // fixed-point accumulators, counts, fill cursors: zeroed together
+    const int64_t words = 2 * (12 * V4) + 2 * V4 + 8;  // int32 words
+    int32_t* base = (int32_t*)scratch(ctx, kBwdAcc, words * sizeof(int32_t));
+    unsigned long long* acc = acc_ext ? reinterpret_cast<unsigned long long*>(acc_ext)
+                                      : reinterpret_cast<unsigned long long*>(base);
+    int32_t* cnt = base + 2 * (12 * V4);
+    int32_t* fill = cnt + V4;
+    unsigned int* mx = (unsigned int*)(fill + V4);
+    int64_t* start = (int64_t*)scratch(ctx, kBwdStart, (V + 1) * sizeof(int64_t));
+    int32_t* cell_of = (int32_t*)scratch(ctx, kBwdCell, std::max<int64_t>(1, n) * sizeof(int32_t));
+    BwdRec* rec = (BwdRec*)scratch(ctx, kBwdRec, std::max<int64_t>(1, n) * sizeof(BwdRec));
+    FSK_LAUNCH(ctx, st, k_zero, std::min(blocks_for(words / 4, 256), cap_blocks), 256, 0,
+               reinterpret_cast<float4*>(base), words / 4);
+    if (n > 0) FSK_LAUNCH(ctx, st, k_bwd_bucket_count, blocks_for(n, 256), 256, 0, g, R, grad_xc, n, cnt, cell_of, mx);
+    scan_i32_to_i64(ctx, cnt, V, start, st);
+    const unsigned int* mscale = max_ext ? reinterpret_cast<const unsigned int*>(max_ext) : mx;
+    if (n > 0) {
+        FSK_LAUNCH(ctx, st, k_bwd_bucket_fill, blocks_for(n, 256), 256, 0, R, grad_xc, n, cell_of, start, fill, rec);
+        FSK_LAUNCH(ctx, st, k_bwd_chunk_reduce, blocks_for(n, 256), 256, 0, g, start, rec, mscale, n_scale, acc);
+    }
+    if (mx_out) *mx_out = mx;
+    return acc;
+}
+
 void run_bwd(fsk_ctx* ctx, const GridP& g, const RootRef& R, const float* grad_xc, int64_t n, float* grad_tgrid,
              int deterministic, cudaStream_t st, const int32_t* order = nullptr) {
     const int64_t V = (int64_t)g.nx * g.ny * g.nz;
@@ -459,24 +511,8 @@ void run_bwd(fsk_ctx* ctx, const GridP& g, const RootRef& R, const float* grad_x
         return;
     }
     // deterministic: bucket the roots by cell, reduce per cell, integer atomics to vertices
-    const int64_t V4 = (V + 3) / 4 * 4;  // fixed-point accumulators, counts, fill cursors: zeroed together
-    const int64_t words = 2 * (12 * V4) + 2 * V4 + 8;  // int32 words
-    int32_t* base = (int32_t*)scratch(ctx, kBwdAcc, words * sizeof(int32_t));
-    unsigned long long* acc = reinterpret_cast<unsigned long long*>(base);
-    int32_t* cnt = base + 2 * (12 * V4);
-    int32_t* fill = cnt + V4;
-    unsigned int* mx = (unsigned int*)(fill + V4);
-    int64_t* start = (int64_t*)scratch(ctx, kBwdStart, (V + 1) * sizeof(int64_t));
-    int32_t* cell_of = (int32_t*)scratch(ctx, kBwdCell, std::max<int64_t>(1, n) * sizeof(int32_t));
-    BwdRec* rec = (BwdRec*)scratch(ctx, kBwdRec, std::max<int64_t>(1, n) * sizeof(BwdRec));
-    FSK_LAUNCH(ctx, st, k_zero, std::min(blocks_for(words / 4, 256), cap_blocks), 256, 0,
-               reinterpret_cast<float4*>(base), words / 4);
-    if (n > 0) FSK_LAUNCH(ctx, st, k_bwd_bucket_count, blocks_for(n, 256), 256, 0, g, R, grad_xc, n, cnt, cell_of, mx);
-    scan_i32_to_i64(ctx, cnt, V, start, st);
-    if (n > 0) {
-        FSK_LAUNCH(ctx, st, k_bwd_bucket_fill, blocks_for(n, 256), 256, 0, R, grad_xc, n, cell_of, start, fill, rec);
-        FSK_LAUNCH(ctx, st, k_bwd_chunk_reduce, blocks_for(n, 256), 256, 0, g, start, rec, mx, n, acc);
-    }
+    unsigned int* mx = nullptr;
+    unsigned long long* acc = det_accumulate(ctx, g, R, grad_xc, n, n, nullptr, nullptr, st, &mx);
     FSK_LAUNCH(ctx, st, k_bwd_fixed_to_float, std::min(blocks_for(12 * V, 256), cap_blocks), 256, 0,
                reinterpret_cast<const long long*>(acc), 12 * V, mx, n, grad_tgrid);
 }
@@ -559,6 +595,59 @@ int fsk_search_bwd_exact_roots(fsk_ctx* ctx, const float* weights, const fsk_gri
         R.u_ex = u;
         R.ok = okp;
         run_bwd(ctx, g, R, grad_xc, n, grad_tgrid, deterministic, st);
+    });
+}
+
+namespace {
+RootRef ref_of(const fsk_bwd_src* src) {
+    if (!src) fail(FSK_EINVAL, "fsk: null buffer");
+    if (src->roots) return RootRef{nullptr, nullptr, nullptr, 0, src->roots, src->root_index};
+    if (src->n_init < 1) fail(FSK_EINVAL, "fsk: n_init must be >= 1");
+    return RootRef{src->x_c, src->jinv, src->root_sel, src->n_init, nullptr, nullptr};
+}
+bool src_ok(const fsk_bwd_src* s) { return s->roots ? s->root_index != nullptr : (s->x_c && s->jinv && s->root_sel); }
+}  // namespace
+
+int fsk_search_bwd_max_term(fsk_ctx* ctx, const fsk_grid_desc* desc, const fsk_bwd_src* src, const float* grad_xc,
+                            int64_t n, float* max_term, void* stream) {
+    return guard([&] {
+        set_device(ctx);
+        make_grid(desc);
+        if (n < 0) fail(FSK_EINVAL, "fsk: negative point count");
+        const RootRef R = ref_of(src);
+        if (!max_term || (n > 0 && (!grad_xc || !src_ok(src)))) fail(FSK_EINVAL, "fsk: null buffer");
+        cudaStream_t st = (cudaStream_t)stream;
+        cuda_check(cudaMemsetAsync(max_term, 0, sizeof(float), st), "cudaMemsetAsync");
+        if (n > 0)
+            FSK_LAUNCH(ctx, st, k_bwd_max_term, blocks_for(n, 256), 256, 0, R, grad_xc, n,
+                       reinterpret_cast<unsigned int*>(max_term));
+    });
+}
+
+int fsk_search_bwd_fixed(fsk_ctx* ctx, const fsk_grid_desc* desc, const fsk_bwd_src* src, const float* grad_xc,
+                         int64_t n, int64_t n_scale, const float* max_term, int64_t* acc, void* stream) {
+    return guard([&] {
+        set_device(ctx);
+        const GridP g = make_grid(desc);
+        if (n < 0 || n_scale < n) fail(FSK_EINVAL, "fsk: need 0 <= n <= n_scale");
+        const RootRef R = ref_of(src);
+        if (!max_term || !acc || (n > 0 && (!grad_xc || !src_ok(src)))) fail(FSK_EINVAL, "fsk: null buffer");
+        det_accumulate(ctx, g, R, grad_xc, n, n_scale, max_term, reinterpret_cast<long long*>(acc),
+                       (cudaStream_t)stream, nullptr);
+    });
+}
+
+int fsk_fixed_to_float(fsk_ctx* ctx, const int64_t* acc, int64_t m, int64_t n_scale, const float* max_term, float* out,
+                       void* stream) {
+    return guard([&] {
+        set_device(ctx);
+        if (m < 0) fail(FSK_EINVAL, "fsk: negative count");
+        if (m > 0 && (!acc || !max_term || !out)) fail(FSK_EINVAL, "fsk: null buffer");
+        if (m > 0)
+            FSK_LAUNCH(ctx, (cudaStream_t)stream, k_bwd_fixed_to_float,
+                       std::min(blocks_for(m, 256), (unsigned)ctx->sm_count * 8), 256, 0,
+                       reinterpret_cast<const long long*>(acc), m, reinterpret_cast<const unsigned int*>(max_term),
+                       n_scale, out);
     });
 }
 

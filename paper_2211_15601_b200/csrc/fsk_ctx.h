@@ -53,7 +53,7 @@ namespace fsk {
 enum Slot {
     kHist, kBbox, kKeys, kPerm, kXs, kScanPart, kBwdAcc, kBwdMax, kPlanes, kPlanes64, kEscQ, kEscN, kEscState,
     kBwdStart, kBwdCell, kBwdRec, kPeakTable, kBwdU, kBwdOk,
-    kOXr, kOJa, kOJb, kOJc, kOMeta, kOKeep, kOKeepMask, kNRoots, kOffs, kRootsTmp,
+    kOXr, kOJa, kOJb, kOJc, kOMeta, kOKeep, kOKeepMask, kNRoots, kOffs, kRootsTmp, kOXd,
     kHW, kHB, kHP, kHT, kHOffs, kHRoots, kFB, kFP, kFOffs, kFRoots,
     kMlpPack, kMlpWidths, kMlpOcc, kMlpAct, kMlpD0, kMlpD1, kMlpOnes,
     kMvPos, kMvPosNext, kMvW, kMvX, kMvG, kMvJ, kMvDx, kMvK, kMvAct, kMvActNext, kMvCnt,

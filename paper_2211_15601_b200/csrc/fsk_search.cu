@@ -277,6 +277,8 @@ struct SearchPlanes {
     uint32_t* meta;  // iterations | converged << 31 (any max_iters >= 1, correspondence.cpp:20)
     uint8_t* keep;   // dedup survivors
     uint32_t* kmask = nullptr;  // per sorted query: bit b = bone b's root kept (n_b <= 32), for k_emit
+    double* xd = nullptr;       // optional [S][3] float64 root (fsk_search_out::x_c64): the float64 state of
+                                // the float64-solved solves, the float32 root widened otherwise
 };
 
 #ifndef FSK_SEARCH_BLOCK
@@ -292,6 +294,11 @@ __device__ __forceinline__ void store_solve(const SearchPlanes& out, int64_t q, 
                                             const SolveOut& s) {
     // the residual's sign bit carries the converged flag (dedup reads one float4 per solve)
     const float4 xr = make_float4((float)x0, (float)x1, (float)x2, copysignf((float)sqrt(err2), s.conv ? 1.f : -1.f));
+    if (out.xd) {
+        out.xd[3 * q] = (double)x0;
+        out.xd[3 * q + 1] = (double)x1;
+        out.xd[3 * q + 2] = (double)x2;
+    }
 #ifdef FSK_NO_STORE_HINTS
     out.xr[q] = xr;
     out.ja[q] = make_float4((float)Ji[0], (float)Ji[1], (float)Ji[2], (float)Ji[3]);
@@ -318,6 +325,11 @@ __device__ __forceinline__ void store_solve(const SearchPlanes& out, int64_t q, 
 
 // Final state of an exact-replay solve (fsk_exact.cuh): the residual is the replay's own norm.
 __device__ __forceinline__ void store_exact(const SearchPlanes& out, int64_t q, const exact::XState& s, bool conv) {
+    if (out.xd) {
+        out.xd[3 * q] = s.x0;
+        out.xd[3 * q + 1] = s.x1;
+        out.xd[3 * q + 2] = s.x2;
+    }
     out.xr[q] = make_float4((float)s.x0, (float)s.x1, (float)s.x2, copysignf((float)s.err, conv ? 1.f : -1.f));
     out.ja[q] = make_float4((float)s.Ji[0], (float)s.Ji[1], (float)s.Ji[2], (float)s.Ji[3]);
     out.jb[q] = make_float4((float)s.Ji[4], (float)s.Ji[5], (float)s.Ji[6], (float)s.Ji[7]);
@@ -904,6 +916,7 @@ __global__ void __launch_bounds__(256) k_emit(int64_t n, int nb, SearchPlanes sp
 
 // Dense per-(point, init) form, point-major (fsk_search_out). One thread per solve.
 struct DenseOut {
+    double* x_c64;
     float* x_c;
     float* jinv;
     float* resid;
@@ -921,6 +934,11 @@ __global__ void __launch_bounds__(256) k_scatter_dense(int64_t n, int nb, Search
     const int64_t j = q - (int64_t)b * n;
     const int64_t s = (int64_t)perm[j] * nb + b;
     const float4 xr = sp.xr[q];
+    if (d.x_c64) {
+        d.x_c64[3 * s] = sp.xd ? sp.xd[3 * q] : (double)xr.x;
+        d.x_c64[3 * s + 1] = sp.xd ? sp.xd[3 * q + 1] : (double)xr.y;
+        d.x_c64[3 * s + 2] = sp.xd ? sp.xd[3 * q + 2] : (double)xr.z;
+    }
     if (d.x_c) {
         d.x_c[3 * s] = xr.x;
         d.x_c[3 * s + 1] = xr.y;
@@ -1080,7 +1098,7 @@ struct PrecomputeReq {
 // P is filled in here.
 SearchState run_search(fsk_ctx* ctx, GridPlanes& P, const GridP& g, const float* weights, const float* bones,
                        const float* pts, int64_t n, const SearchP& sp, int flags, cudaStream_t st,
-                       const PrecomputeReq* pre = nullptr) {
+                       const PrecomputeReq* pre = nullptr, bool want_x64 = false) {
     if ((flags & FSK_SEARCH_EXACT64) && !weights)
         fail(FSK_EINVAL, "fsk: FSK_SEARCH_EXACT64 needs the weight grid (J~0 from the skinning weights)");
     // the exact replay reads the weight grid and float64 copies of the bones (shared memory)
@@ -1101,6 +1119,7 @@ SearchState run_search(fsk_ctx* ctx, GridPlanes& P, const GridP& g, const float*
     s.sp.meta = (uint32_t*)scratch(ctx, kOMeta, S * sizeof(uint32_t));
     s.sp.keep = (uint8_t*)scratch(ctx, kOKeep, S);
     s.sp.kmask = g.nb <= 32 ? (uint32_t*)scratch(ctx, kOKeepMask, std::max<int64_t>(1, n) * sizeof(uint32_t)) : nullptr;
+    s.sp.xd = want_x64 ? (double*)scratch(ctx, kOXd, S * 3 * sizeof(double)) : nullptr;
     s.perm = (int*)scratch(ctx, kPerm, std::max<int64_t>(1, n) * sizeof(int));
     ctx->last_search_n = n;
     s.n_roots_p = (int32_t*)scratch(ctx, kNRoots, std::max<int64_t>(1, n) * sizeof(int32_t));
@@ -1631,8 +1650,9 @@ int fsk_search_fwd(fsk_ctx* ctx, const float* tgrid, const double* tgrid64, cons
         if (n == 0) return;
         cudaStream_t st = (cudaStream_t)stream;
         GridPlanes P = run_relayout(ctx, tgrid, tgrid64, g, needs_f64(opts->flags), st);
-        const SearchState s = run_search(ctx, P, g, weights, bones, points, n, sp, opts->flags, st);
-        DenseOut d{out->x_c, out->jinv, out->resid, out->iters, out->converged, out->keep, out->n_roots};
+        const SearchState s = run_search(ctx, P, g, weights, bones, points, n, sp, opts->flags, st, nullptr,
+                                         out->x_c64 != nullptr);
+        DenseOut d{out->x_c64, out->x_c, out->jinv, out->resid, out->iters, out->converged, out->keep, out->n_roots};
         FSK_LAUNCH(ctx, st, k_scatter_dense, blocks_for(n * g.nb, 256), 256, 0, n, g.nb, s.sp, s.perm, d);
         if (out->n_roots)
             cuda_check(cudaMemcpyAsync(out->n_roots, s.n_roots_p, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st),
@@ -1706,7 +1726,7 @@ int fsk_search_fwd_mlp(fsk_ctx* ctx, const float* theta, const int32_t* widths, 
             cur = nxt;
         }
         FSK_LAUNCH(ctx, st, k_dedup, blocks_for(n, 256), 256, 0, n, nb, (float)sp.dedup2, ss.sp, ss.perm, ss.n_roots_p);
-        DenseOut d{out->x_c, out->jinv, out->resid, out->iters, out->converged, out->keep, out->n_roots};
+        DenseOut d{out->x_c64, out->x_c, out->jinv, out->resid, out->iters, out->converged, out->keep, out->n_roots};
         FSK_LAUNCH(ctx, st, k_scatter_dense, blocks_for(S, 256), 256, 0, n, nb, ss.sp, ss.perm, d);
         if (out->n_roots)
             cuda_check(cudaMemcpyAsync(out->n_roots, ss.n_roots_p, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st),
@@ -1767,7 +1787,7 @@ int fsk_compact_roots(fsk_ctx* ctx, const fsk_search_out* dense, int64_t n, int3
         if (total > cap) fail(FSK_EINVAL, "fsk: root buffer too small");
         if (n > 0 && total > 0) {
             if (!roots) fail(FSK_EINVAL, "fsk: null buffer");
-            DenseOut d{dense->x_c, dense->jinv, dense->resid, dense->iters, dense->converged, dense->keep,
+            DenseOut d{nullptr, dense->x_c, dense->jinv, dense->resid, dense->iters, dense->converged, dense->keep,
                        dense->n_roots};
             FSK_LAUNCH(ctx, st, k_emit_dense, blocks_for(n, 256), 256, 0, n, n_init, d, offsets, roots);
         }

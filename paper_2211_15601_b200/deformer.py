@@ -173,9 +173,10 @@ class Deformer:
         return out
 
     # ---------------------------------------------------------------- K2 + dedup
-    def alloc_search_out(self, n, nb, jinv=True, resid=True, iters=True, keep=True):
+    def alloc_search_out(self, n, nb, jinv=True, resid=True, iters=True, keep=True, x64=False):
         dev = self.device
         return dict(
+            x_c64=torch.empty((n, nb, 3), dtype=torch.float64, device=dev) if x64 else None,
             x_c=torch.empty((n, nb, 3), dtype=torch.float32, device=dev),
             jinv=torch.empty((n, nb, 3, 3), dtype=torch.float32, device=dev) if jinv else None,
             resid=torch.empty((n, nb), dtype=torch.float32, device=dev) if resid else None,
@@ -188,7 +189,7 @@ class Deformer:
     @staticmethod
     def _c_out(o) -> SearchOut:
         return SearchOut(*[o[k].data_ptr() if o.get(k) is not None else None
-                           for k in ("x_c", "jinv", "resid", "iters", "converged", "keep", "n_roots")])
+                           for k in ("x_c", "jinv", "resid", "iters", "converged", "keep", "n_roots", "x_c64")])
 
     def batch_search(self, tgrid, dims, bbox, bones, points, opts: SearchOptions, out=None, tgrid64=None,
                      weights=None):
@@ -363,6 +364,43 @@ class Deformer:
                                                 _ptr(roots), _ptr(ri), _ptr(_f32(grad_xc, "grad_xc", self.device)), n,
                                                 _ptr(out), _ptr(ok), 1 if deterministic else 0, _stream(self.device)))
         return out, ok
+
+    # ---------------------------------------------------------------- deterministic backward across ranks
+    def _bwd_src(self, dense=None, root_sel=None, roots=None, root_index=None):
+        if roots is not None:
+            ri = root_index.to(device=self.device, dtype=torch.int64).contiguous()
+            return _lib.BwdSrc(None, None, None, 0, roots.data_ptr(), ri.data_ptr()), ri
+        rs = root_sel.to(device=self.device, dtype=torch.int32).contiguous()
+        return _lib.BwdSrc(dense["x_c"].data_ptr(), dense["jinv"].data_ptr(), rs.data_ptr(), dense["x_c"].shape[1],
+                           None, None), rs
+
+    def search_bwd_max_term(self, dims, bbox, n_bones, grad_xc, **src):
+        """Max term of the deterministic backward's fixed-point scale over this shard's roots → [1] float32
+        (dense=..., root_sel=... or roots=..., root_index=...)."""
+        desc = grid_desc(dims, bbox, n_bones)
+        c, keep = self._bwd_src(**src)
+        m = torch.empty((1,), dtype=torch.float32, device=self.device)
+        check(self.L.fsk_search_bwd_max_term(self._ctx, ctypes.byref(desc), ctypes.byref(c),
+                                             _ptr(_f32(grad_xc, "grad_xc", self.device)), grad_xc.shape[0], _ptr(m),
+                                             _stream(self.device)))
+        return m
+
+    def search_bwd_fixed(self, dims, bbox, n_bones, grad_xc, n_scale, max_term, acc, **src):
+        """Accumulate this shard's int64 fixed-point dL/dT into ``acc`` [V,12] int64 with the scale of
+        (max_term, n_scale) — the max over all shards and the total point count."""
+        desc = grid_desc(dims, bbox, n_bones)
+        c, keep = self._bwd_src(**src)
+        check(self.L.fsk_search_bwd_fixed(self._ctx, ctypes.byref(desc), ctypes.byref(c),
+                                          _ptr(_f32(grad_xc, "grad_xc", self.device)), grad_xc.shape[0], int(n_scale),
+                                          _ptr(max_term), _ptr(acc), _stream(self.device)))
+        return acc
+
+    def fixed_to_float(self, acc, n_scale, max_term, out=None):
+        if out is None:
+            out = torch.empty(acc.shape, dtype=torch.float32, device=self.device)
+        check(self.L.fsk_fixed_to_float(self._ctx, _ptr(acc), acc.numel(), int(n_scale), _ptr(max_term), _ptr(out),
+                                        _stream(self.device)))
+        return out
 
     def grad_weights(self, dims, bbox, grad_tgrid, bones, out=None):
         """dL/dw [V, n_b] = <dL/dT_v, B_i>_F."""

@@ -92,8 +92,27 @@ class MultiGPUDeformer:
                                    gather=gather, group=self.group)
         return tg, res, rng
 
-    def backward(self, dims, bbox, bones, local_dense, grad_xc_local, root_sel_local, deterministic=False):
+    def backward(self, dims, bbox, bones, local_dense, grad_xc_local, root_sel_local, deterministic=False,
+                 n_total=None):
+        """dL/dT (and dL/dw) of the whole batch on every rank. ``deterministic``: every rank rounds its
+        terms to int64 fixed point with the SAME scale (the max term all-reduced with MAX, n = the total
+        point count) and the int64 sums are all-reduced exactly, so the result is bitwise the
+        single-process deterministic gradient for any world size."""
         nb = bones.numel() // 12
-        return sharded_backward(
-            lambda: self.D.search_bwd(dims, bbox, nb, local_dense, grad_xc_local, root_sel_local, deterministic),
-            lambda g: self.D.grad_weights(dims, bbox, g, bones), group=self.group)
+        if not deterministic:
+            return sharded_backward(
+                lambda: self.D.search_bwd(dims, bbox, nb, local_dense, grad_xc_local, root_sel_local, False),
+                lambda g: self.D.grad_weights(dims, bbox, g, bones), group=self.group)
+        src = dict(dense=local_dense, root_sel=root_sel_local)
+        if n_total is None:
+            t = torch.tensor([grad_xc_local.shape[0]], dtype=torch.int64, device=grad_xc_local.device)
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+            n_total = int(t.item())
+        mt = self.D.search_bwd_max_term(dims, bbox, nb, grad_xc_local, **src)
+        dist.all_reduce(mt, op=dist.ReduceOp.MAX, group=self.group)
+        V = dims[0] * dims[1] * dims[2]
+        acc = torch.zeros((V, 12), dtype=torch.int64, device=grad_xc_local.device)
+        self.D.search_bwd_fixed(dims, bbox, nb, grad_xc_local, n_total, mt, acc, **src)
+        dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=self.group)
+        g = self.D.fixed_to_float(acc, n_total, mt)
+        return g, self.D.grad_weights(dims, bbox, g, bones)

@@ -33,7 +33,8 @@ def exact_search(deformer, sc, max_iters, tg64=None):
     if tg64 is None:
         tg64 = torch.empty((w.shape[0], 12), dtype=torch.float64, device="cuda")
         deformer.precompute_transform_grid(w, sc.dims, sc.bbox, B, out64=tg64)
-    out = deformer.batch_search(None, sc.dims, sc.bbox, B, x, opts_of(sc, max_iters), tgrid64=tg64, weights=w)
+    out = deformer.batch_search(None, sc.dims, sc.bbox, B, x, opts_of(sc, max_iters), tgrid64=tg64, weights=w,
+                                out=deformer.alloc_search_out(x.shape[0], sc.n_bones, x64=True))
     torch.cuda.synchronize()
     return {k: (v.cpu().numpy() if v is not None else None) for k, v in out.items()}
 
@@ -43,6 +44,8 @@ def assert_bitwise(g, r):
     np.testing.assert_array_equal(g["converged"], r["converged"])
     np.testing.assert_array_equal(g["iters"].astype(np.int32), r["iters"])
     np.testing.assert_array_equal(g["x_c"], r["x_c"].astype(np.float32))
+    if g.get("x_c64") is not None:  # the replay's float64 roots themselves (Root::x), not just their rounding
+        np.testing.assert_array_equal(g["x_c64"], r["x_c"])
     np.testing.assert_array_equal(g["jinv"], r["jinv"].astype(np.float32).reshape(g["jinv"].shape))
     np.testing.assert_array_equal(g["resid"], r["resid"].astype(np.float32))
     np.testing.assert_array_equal(g["keep"], r["keep"])
@@ -127,15 +130,16 @@ def test_mixed_escalations_are_the_oracle_bitwise(deformer, dims, seed, points):
     tg64 = torch.empty((w.shape[0], 12), dtype=torch.float64, device="cuda")
     tg = deformer.precompute_transform_grid(w, sc.dims, sc.bbox, B, out64=tg64)
     deformer.search_stats(reset=True)
-    out = deformer.batch_search(tg, sc.dims, sc.bbox, B, x, opts_of(sc, 50, "mixed"), tgrid64=tg64, weights=w)
+    out = deformer.batch_search(tg, sc.dims, sc.bbox, B, x, opts_of(sc, 50, "mixed"), tgrid64=tg64, weights=w,
+                                out=deformer.alloc_search_out(x.shape[0], sc.n_bones, x64=True))
     torch.cuda.synchronize()
     n_esc = deformer.search_stats(reset=True)[3]
     g = {k: (v.cpu().numpy() if v is not None else None) for k, v in out.items()}
     r = oracle.batch_search(sc.weights, sc.dims, sc.bbox, sc.bones, sc.points, workers=8, **sc.search_options(50))
     same = ((g["converged"] == r["converged"]) & (g["iters"].astype(np.int32) == r["iters"])
             & (g["resid"] == r["resid"].astype(np.float32))
-            & (g["x_c"] == r["x_c"].astype(np.float32)).all(-1))
-    print(f"\n{dims} {points}: escalated {n_esc}, bit-equal to the oracle {int(same.sum())} of {same.size}, "
+            & (g["x_c64"] == r["x_c"]).all(-1))  # the float64 root itself (Root::x)
+    print(f"\n{dims} {points}: escalated {n_esc}, bit-equal to the oracle in float64 {int(same.sum())} of {same.size}, "
           f"mask agreement {(g['converged'] == r['converged']).mean():.7f}")
     assert n_esc > 0
     assert same.sum() >= n_esc

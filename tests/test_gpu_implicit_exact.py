@@ -89,7 +89,7 @@ def test_exact_gradient_scatter_matches_oracle(deformer, scene):
 def test_exact_gradient_matches_finite_differences(deformer, scene):
     """SPEC.md:570 (#5a): 100 trials, each a (root, grid entry, cotangent): the exact gradient of v·x*
     w.r.t. the entry (the largest-gradient entry of the largest-gradient corner, as the oracle's own
-    FD test) vs central differences (h = 1e-3) of tightly re-solved roots (GPU exact replay, conv_eps
+    FD test) vs central differences (h = 1e-4) of tightly re-solved roots (GPU exact replay, conv_eps
     1e-13·diag) on the perturbed float64 transform grid."""
     sc, w, B, roots, rh, ridx, o = scene
     tg64 = torch.empty((w.shape[0], 12), dtype=torch.float64, device="cuda")
@@ -105,16 +105,16 @@ def test_exact_gradient_matches_finite_differences(deformer, scene):
     margin = 1e-3 * (hi - lo)
     inside = (ridx >= 0) & ((xr > lo + margin) & (xr < hi - margin)).all(1)
     qs = rng.choice(np.nonzero(inside)[0], 120, replace=False)
-    # h = 1e-3: the GPU returns roots in float32 (ulp 6e-8 at |x| ~ 1), so h = 1e-4 would leave 3e-4 of
-    # rounding noise in the difference; the O(h^2) truncation at 1e-3 stays ~1e-5
-    rel, h = [], 1e-3
+    # roots read in float64 (fsk_search_out::x_c64: the exact replay's own state), h = 1e-4 as SPEC.md:421
+    rel, h = [], 1e-4
     for q in qs:
         bone = int(rh[ridx[q], 13].view(np.int32))
         xq = dev(sc.points[q:q + 1])
 
         def solve(tg):
-            out = deformer.batch_search(None, sc.dims, sc.bbox, B, xq, tight, tgrid64=tg, weights=w)
-            return out["x_c"][0, bone].double().cpu().numpy(), bool(out["converged"][0, bone].item())
+            out = deformer.batch_search(None, sc.dims, sc.bbox, B, xq, tight, tgrid64=tg, weights=w,
+                                        out=deformer.alloc_search_out(1, sc.n_bones, x64=True))
+            return out["x_c64"][0, bone].cpu().numpy(), bool(out["converged"][0, bone].item())
 
         x0, c0 = solve(tg64)
         if not c0:
