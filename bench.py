@@ -79,15 +79,31 @@ def scene_for_rank(args, rank):
 
 
 def workload_name(args):
+    """The workload alone (the same string in both arms); how each arm runs it is in its `pipeline`."""
     name = "C3" if args.backward else ("C4" if args.poses > 1 else "C2")
     if args.grid == "128,128,32" and not args.backward and args.poses == 1:
         name = "C5 (per-GPU shard of the 64M-point ray-sample workload)"
     s = (f"{name}: {args.poses} pose(s) x {args.points // 1000}k posed points x 24 bone inits per GPU, "
-         f"{args.grid.replace(',', 'x')} grid, max_iters {args.max_iters}; step = per pose: precompute + sort + "
-         f"search (fp32 pass + fp64 escalation replaying the reference exactly) + dedup + compaction to CorrespondenceSets")
+         f"{args.grid.replace(',', 'x')} grid, max_iters {args.max_iters}; step = per pose precompute_transform_grid "
+         f"+ batch_search (every (point, bone-init) Broyden solve, dedup_roots) into CorrespondenceSets")
     if args.backward:
-        s += " + implicit-diff backward (dL/dT scatter + dL/dw)"
+        s += " + implicit-diff backward (dL/dT + dL/dw)"
     return s
+
+
+def config_of(args, n, nb, dims, world):
+    return {"workload": workload_name(args), "points_per_gpu": n, "n_init": nb, "grid": list(dims),
+            "max_iters": args.max_iters, "poses": args.poses}
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 # ------------------------------------------------------------------------------ clocks
@@ -190,9 +206,12 @@ def run_reference(args, rank, world):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / len(times) * sc.points.shape[0] / m,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic SMPL-like skeleton, analytic capsule weights, uniform posed points",
-            "config": {"workload": workload_name(args), "points_per_gpu": args.points, "n_init": sc.n_bones,
-                       "grid": list(sc.dims), "max_iters": args.max_iters},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port", "sample": sample},
+            "config": {**config_of(args, args.points, sc.n_bones, sc.dims, world),
+                       "l2": "n/a (host CPU path)", "parallelism": f"{workers} host threads (parallel_for)"},
+            "pipeline": "oracle/fskin_oracle.cpp: f64 restatement of precompute_transform_grid + batch_search "
+                        "(search_one per query, dedup_roots), std::thread over all host cores",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port", "sample": sample,
+                             "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "note": "oracle/fskin_oracle.cpp: f64 restatement of the reference batch_search "
                     "(reference needs Eigen3, absent; see DESIGN.md)"}
@@ -363,16 +382,19 @@ def run_ours(args, rank, world, local_rank):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32",
+        "vs_baseline": None, "dtype": "mixed f32/f64" if args.precision in ("mixed", "mixed-fast") else
+        {"fp32": "f32", "fp64": "f64", "exact64": "f64"}[args.precision],
         "data": "synthetic: SMPL-like 24-bone skeleton, random pose U(-0.5,0.5) rad, analytic capsule weight grid, "
                 "uniform posed points (seeded; same inputs the oracle parity tests use)",
-        "config": {"workload": workload_name(args), "points_per_gpu": n, "n_init": nb, "grid": list(sc.dims),
-                   "max_iters": args.max_iters, "sort": not args.no_sort, "poses": args.poses,
-                   "precision": args.precision, "cuda_graph": bool(args.graph),
+        "config": {**config_of(args, n, nb, sc.dims, world),
                    "l2": "flushed between steps (256 MiB fill outside the per-step CUDA events)",
                    "parallelism": (f"points sharded across {world} GPU(s); per frame NCCL broadcast of the pose "
                                    f"from rank 0" + ("; NCCL all-reduce of dL/dT" if args.backward else "")
                                    if world > 1 else "1 GPU (points sharded across ranks under torchrun)")},
+        "pipeline": {"stages": "K1 precompute (+ float64 planes) beside the spatial sort, float32 search pass, "
+                               "float64 escalation replaying the oracle's operation order, dedup, compaction"
+                               + (", K3 backward in the search's spatial order + dL/dw" if args.backward else ""),
+                     "sort": not args.no_sort, "precision": args.precision, "cuda_graph": bool(args.graph)},
         "roofline": {"bound": "fp32", "kernel": "k_search_fast", "achieved": achieved, "peak": peak_fp32,
                      "unit": "TFLOP/s", "frac": achieved / peak_fp32,
                      "traffic": NCU_TRAFFIC_K2 if (args.grid == "32,32,32" and args.points == 200_000) else None,
@@ -427,7 +449,7 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         workers = os.cpu_count() or 1
         rate, m, dt = cpu_rate(sc, args, args.cpu_seconds, workers)
-        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": workers, "kind": "port",
+        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": workers, "kind": "port", "cpu_model": cpu_model(),
                                 "sample": f"{m} of {n} points x {nb} inits (precompute + search + dedup), repeated over {dt:.1f} s, "
                                           "f64 oracle restatement of batch_search, std::thread over all host cores"}
     if rank == 0:

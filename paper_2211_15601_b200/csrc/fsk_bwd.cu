@@ -7,9 +7,12 @@
 // skinning field is the voxel grid itself, so the cotangent is scattered to the grid:
 //   dL/dT_c += φ_c(x*) · u (x*, 1)ᵀ        (3×4, the 8 corners of locate_cell(x*))
 //   dL/dw_{c,i} = <dL/dT_c, B_i>_F          (k_grad_weights; T_c = Σ_i w_{c,i} B_i)
-// Fast mode: float4 vector reductions (REDG.E.ADD.F32x4). Deterministic mode: every term is
-// rounded to int64 fixed point with a data-derived power-of-two scale and accumulated with
-// integer reductions — associative, so bitwise reproducible for any order or GPU count.
+// Fast mode: float4 vector reductions (REDG.E.ADD.F32x4), warp-aggregated per cell when the roots come
+// in spatial order. Deterministic mode: every term is rounded to int64 fixed point with a data-derived
+// power-of-two scale and accumulated with integer reductions — associative, so bitwise reproducible for
+// any order on one device; across devices or ranks when every shard uses the same scale (max term
+// all-reduced, n = all points) and the int64 sums are all-reduced (fsk_search_bwd_fixed, fsk_multi,
+// dist.py).
 #include "fsk_ctx.h"
 #include "fsk_exact.cuh"
 

@@ -94,6 +94,20 @@ def _f32(t, name, device):
     return t
 
 
+def _check_roots_out(out, n, device):
+    """Caller-supplied CorrespondenceSet buffers: offsets [N+1] int64 and roots [cap,16] float32, contiguous,
+    on the context's device (a short or mistyped buffer would be an out-of-bounds device write)."""
+    offsets, roots = out
+    for t, name, dt in ((offsets, "offsets", torch.int64), (roots, "roots", torch.float32)):
+        if not isinstance(t, torch.Tensor) or t.device != device or t.dtype != dt or not t.is_contiguous():
+            raise FskInvalidArgument(f"fsk: {name} must be a contiguous {dt} tensor on {device}")
+    if offsets.numel() < n + 1:
+        raise FskInvalidArgument("fsk: offsets needs n+1 entries")
+    if roots.dim() != 2 or roots.shape[1] != 16:
+        raise FskInvalidArgument("fsk: roots must be [cap, 16] float32 (fsk_root records)")
+    return offsets, roots
+
+
 class Deformer:
     """One context (``fsk_ctx``) on one GPU. The methods mirror the reference free
     functions; results are dense per-(point, init) tensors plus dedup masks."""
@@ -175,8 +189,9 @@ class Deformer:
     # ---------------------------------------------------------------- K2 + dedup
     def alloc_search_out(self, n, nb, jinv=True, resid=True, iters=True, keep=True, x64=False):
         dev = self.device
+        extra = {"x_c64": torch.empty((n, nb, 3), dtype=torch.float64, device=dev)} if x64 else {}
         return dict(
-            x_c64=torch.empty((n, nb, 3), dtype=torch.float64, device=dev) if x64 else None,
+            **extra,
             x_c=torch.empty((n, nb, 3), dtype=torch.float32, device=dev),
             jinv=torch.empty((n, nb, 3, 3), dtype=torch.float32, device=dev) if jinv else None,
             resid=torch.empty((n, nb), dtype=torch.float32, device=dev) if resid else None,
@@ -223,7 +238,7 @@ class Deformer:
         """``batch_search`` straight to CorrespondenceSets on the device (fsk_batch_search):
         returns (offsets, roots); roots of query p are roots[offsets[p]:offsets[p+1]]."""
         nb, n = bones.numel() // 12, points.shape[0]
-        offsets, roots = out if out is not None else self.alloc_roots(n, nb)
+        offsets, roots = _check_roots_out(out, n, self.device) if out is not None else self.alloc_roots(n, nb)
         desc = grid_desc(dims, bbox, nb)
         weights = None if weights is None else _f32(weights, "weights", self.device)
         tgrid = None if tgrid is None and tgrid64 is not None else _f32(tgrid, "tgrid", self.device)
@@ -236,9 +251,12 @@ class Deformer:
 
     def deform(self, weights, dims, bbox, bones, points, opts: SearchOptions, tgrid=None, out=None):
         """One deformer frame on device buffers (fsk_deform): precompute_transform_grid +
-        batch_search → (offsets, roots). ``tgrid`` [V,12] receives the transform grid if given."""
+        batch_search → (offsets, roots). ``tgrid`` [V,12] receives the transform grid if given.
+        Kept roots beyond the capacity of ``roots`` are dropped: check offsets[N] <= roots.shape[0]."""
         nb, n = bones.numel() // 12, points.shape[0]
-        offsets, roots = out if out is not None else self.alloc_roots(n, nb)
+        offsets, roots = _check_roots_out(out, n, self.device) if out is not None else self.alloc_roots(n, nb)
+        if tgrid is not None:
+            tgrid = _f32(tgrid, "tgrid", self.device)
         desc = grid_desc(dims, bbox, nb)
         check(self.L.fsk_deform(self._ctx, _ptr(_f32(weights, "weights", self.device)), ctypes.byref(desc),
                                 _ptr(_f32(bones, "bones", self.device)), nb, _ptr(_f32(points, "points", self.device)),
@@ -256,6 +274,8 @@ class Deformer:
         if out is None:
             out = torch.empty((V, 12), dtype=torch.float32, device=self.device)
         ri = root_index.to(device=self.device, dtype=torch.int64).contiguous()
+        if ri.numel() != grad_xc.shape[0]:
+            raise FskInvalidArgument("fsk: root_index needs one entry per query")
         if order is not None and (order.dtype != torch.int32 or order.device != self.device or
                                   order.numel() != grad_xc.shape[0] or not order.is_contiguous()):
             raise FskInvalidArgument("fsk: order must be a contiguous int32 tensor with one entry per query")

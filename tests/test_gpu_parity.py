@@ -547,3 +547,44 @@ def test_disagreement_within_reference_build_spread(deformer, c2_full):
     for v in oracle.VARIANTS:
         both = (g["converged"] == 1) & (res[v]["converged"] == 1)
         assert np.abs(g["x_c"] - res[v]["x_c"])[both].max() <= TOL_X
+
+
+def test_cuda_graph_replay_equals_eager(deformer):
+    """The bench replays one step from a CUDA graph (fsk_deform's K1 beside the sort on a side stream,
+    fork/join by events, the float64 tail's persistent kernels): a replayed step's CorrespondenceSets
+    and transform grid are the eager call's bit for bit, also after the inputs change in place."""
+    sc = S.make_scene((32, 32, 32), 30_000, seed=13, points="training")
+    w, B, x = dev(sc.weights), dev(sc.bones), dev(sc.points)
+    o = opts_of(sc, 50)
+    n, nb = x.shape[0], sc.n_bones
+    out = deformer.alloc_roots(n, nb)
+    tg = torch.empty((w.shape[0], 12), dtype=torch.float32, device="cuda")
+    eager_offs, eager_roots = (t.clone() for t in deformer.deform(w, sc.dims, sc.bbox, B, x, o, tgrid=tg, out=out))
+    eager_tg = tg.clone()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        deformer.deform(w, sc.dims, sc.bbox, B, x, o, tgrid=tg, out=out)
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        deformer.deform(w, sc.dims, sc.bbox, B, x, o, tgrid=tg, out=out)
+    out[0].zero_()
+    out[1].zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    total = int(eager_offs[-1].item())
+    assert torch.equal(out[0], eager_offs)
+    assert torch.equal(out[1][:total], eager_roots[:total])
+    assert torch.equal(tg, eager_tg)
+    # new pose and points written into the captured buffers: the replay follows them
+    sc2 = S.make_scene((32, 32, 32), 30_000, seed=14, points="uniform")
+    B.copy_(dev(sc2.bones))
+    x.copy_(dev(sc2.points))
+    ref_offs, ref_roots = (t.clone() for t in deformer.deform(w, sc.dims, sc.bbox, B, x, o))
+    g.replay()
+    torch.cuda.synchronize()
+    total = int(ref_offs[-1].item())
+    assert torch.equal(out[0], ref_offs)
+    assert torch.equal(out[1][:total], ref_roots[:total])
