@@ -88,7 +88,8 @@ typedef struct fsk_search_opts {
  * [N] int32 = number of kept roots per point. */
 typedef struct fsk_search_out {
     float* x_c;           /* [N][n_b][3] canonical root (Root::x) */
-    float* jinv;          /* [N][n_b][9] Broyden inverse-Jacobian estimate (Root::inv_jacobian) */
+    float* jinv;          /* [N][n_b][9] Broyden inverse-Jacobian estimate (Root::inv_jacobian) of the
+                             converged solves; NaN for the others (no Root) */
     float* resid;         /* [N][n_b] ||d(x)-x'|| at termination (Root::residual) */
     int32_t* iters;       /* [N][n_b] iterations executed (Root::iterations) */
     uint8_t* converged;   /* [N][n_b] 1 iff residual < conv_eps was reached */

@@ -274,7 +274,7 @@ struct SearchPlanes {
     float4* ja;      // J~[0..3]
     float4* jb;      // J~[4..7]
     float* jc;       // J~[8]
-    uint32_t* meta;  // iterations | converged << 31 (any max_iters >= 1, correspondence.cpp:20)
+    uint32_t* meta;  // iterations (30 bits; any max_iters >= 1, correspondence.cpp:20) | J~ stored << 30 | converged << 31
     uint8_t* keep;   // dedup survivors
     uint32_t* kmask = nullptr;  // per sorted query: bit b = bone b's root kept (n_b <= 32), for k_emit
     double* xd = nullptr;       // optional [S][3] float64 root (fsk_search_out::x_c64): the float64 state of
@@ -291,7 +291,7 @@ constexpr int kSearchBlock = FSK_SEARCH_BLOCK;
 
 template <typename R>
 __device__ __forceinline__ void store_solve(const SearchPlanes& out, int64_t q, R x0, R x1, R x2, const R Ji[9], R err2,
-                                            const SolveOut& s) {
+                                            const SolveOut& s, bool store_jt = true) {
     // the residual's sign bit carries the converged flag (dedup reads one float4 per solve)
     const float4 xr = make_float4((float)x0, (float)x1, (float)x2, copysignf((float)sqrt(err2), s.conv ? 1.f : -1.f));
     if (out.xd) {
@@ -304,7 +304,7 @@ __device__ __forceinline__ void store_solve(const SearchPlanes& out, int64_t q, 
     out.ja[q] = make_float4((float)Ji[0], (float)Ji[1], (float)Ji[2], (float)Ji[3]);
     out.jb[q] = make_float4((float)Ji[4], (float)Ji[5], (float)Ji[6], (float)Ji[7]);
     out.jc[q] = (float)Ji[8];
-    out.meta[q] = (uint32_t)s.iters | (s.conv ? 0x80000000u : 0u);
+    out.meta[q] = (uint32_t)s.iters | (s.conv ? 0x80000000u : 0u) | (store_jt ? 0x40000000u : 0u);
 #else
     // x / residual stay in L2 for dedup (read right after the search); J~ and meta are read only
     // for the ~1 kept root per query (emit), so they stream out (evict-first). Measured on C2:
@@ -316,10 +316,13 @@ __device__ __forceinline__ void store_solve(const SearchPlanes& out, int64_t q, 
 #else
     out.xr[q] = xr;
 #endif
-    __stcs(out.ja + q, make_float4((float)Ji[0], (float)Ji[1], (float)Ji[2], (float)Ji[3]));
-    __stcs(out.jb + q, make_float4((float)Ji[4], (float)Ji[5], (float)Ji[6], (float)Ji[7]));
-    __stcs(out.jc + q, (float)Ji[8]);
-    __stcs(reinterpret_cast<unsigned int*>(out.meta) + q, (unsigned int)s.iters | (s.conv ? 0x80000000u : 0u));
+    if (store_jt) {  // J~ is read only for roots (converged solves); the float32 pass skips it otherwise
+        __stcs(out.ja + q, make_float4((float)Ji[0], (float)Ji[1], (float)Ji[2], (float)Ji[3]));
+        __stcs(out.jb + q, make_float4((float)Ji[4], (float)Ji[5], (float)Ji[6], (float)Ji[7]));
+        __stcs(out.jc + q, (float)Ji[8]);
+    }
+    __stcs(reinterpret_cast<unsigned int*>(out.meta) + q,
+           (unsigned int)s.iters | (s.conv ? 0x80000000u : 0u) | (store_jt ? 0x40000000u : 0u));
 #endif
 }
 
@@ -334,7 +337,7 @@ __device__ __forceinline__ void store_exact(const SearchPlanes& out, int64_t q, 
     out.ja[q] = make_float4((float)s.Ji[0], (float)s.Ji[1], (float)s.Ji[2], (float)s.Ji[3]);
     out.jb[q] = make_float4((float)s.Ji[4], (float)s.Ji[5], (float)s.Ji[6], (float)s.Ji[7]);
     out.jc[q] = (float)s.Ji[8];
-    out.meta[q] = (uint32_t)s.k | (conv ? 0x80000000u : 0u);
+    out.meta[q] = (uint32_t)s.k | (conv ? 0x80000000u : 0u) | 0x40000000u;
 }
 
 // Work counters for the roofline (bench.py): per pass, solves / Broyden iterations /
@@ -379,7 +382,9 @@ __global__ void __launch_bounds__(kSearchBlock, FSK_SEARCH_MINB)
         float x0, x1, x2, Ji[9], err2;
         const SolveOut s = solve_one<float, true>(P, g, bones + 12 * bone, xq.x, xq.y, xq.z, o, x0, x1, x2, Ji, err2);
         const int64_t q = (int64_t)bone * n + j;
-        store_solve(out, q, x0, x1, x2, Ji, err2, s);
+        // J~ only for a root the float32 pass settles (an escalated solve is stored again by the float64
+        // pass; an unconverged one has no root): C2 DRAM writes of the pass fall by ~half of 36 B per solve
+        store_solve(out, q, x0, x1, x2, Ji, err2, s, s.conv && !s.esc);
 #ifdef FSK_PER_SOLVE_STATS
         count_work(stats, s);
 #else
@@ -896,7 +901,7 @@ __global__ void __launch_bounds__(256) k_emit(int64_t n, int nb, SearchPlanes sp
             if (o < cap) {
                 float4 xr = sp.xr[q];
                 xr.w = fabsf(xr.w);
-                store_root(roots + o, xr, sp.ja[q], sp.jb[q], sp.jc[q], b, (int)(sp.meta[q] & 0x7fffffffu));
+                store_root(roots + o, xr, sp.ja[q], sp.jb[q], sp.jc[q], b, (int)(sp.meta[q] & 0x3fffffffu));
             }
             ++o;
         }
@@ -908,7 +913,7 @@ __global__ void __launch_bounds__(256) k_emit(int64_t n, int nb, SearchPlanes sp
         if (o < cap) {
             float4 xr = sp.xr[q];
             xr.w = fabsf(xr.w);
-            store_root(roots + o, xr, sp.ja[q], sp.jb[q], sp.jc[q], b, (int)(sp.meta[q] & 0x7fffffffu));
+            store_root(roots + o, xr, sp.ja[q], sp.jb[q], sp.jc[q], b, (int)(sp.meta[q] & 0x3fffffffu));
         }
         ++o;
     }
@@ -945,7 +950,10 @@ __global__ void __launch_bounds__(256) k_scatter_dense(int64_t n, int nb, Search
         d.x_c[3 * s + 2] = xr.z;
     }
     if (d.resid) d.resid[s] = fabsf(xr.w);
-    if (d.jinv) {
+    const uint32_t mq = sp.meta[q];
+    if (d.jinv && !(mq & 0x40000000u)) {  // J~ not stored (an unconverged float32 solve: no Root): NaN
+        for (int e = 0; e < 9; ++e) d.jinv[9 * s + e] = __int_as_float(0x7fc00000);
+    } else if (d.jinv) {
         const float4 a = sp.ja[q], c = sp.jb[q];
         float* J = d.jinv + 9 * s;
         J[0] = a.x; J[1] = a.y; J[2] = a.z; J[3] = a.w;
@@ -953,7 +961,7 @@ __global__ void __launch_bounds__(256) k_scatter_dense(int64_t n, int nb, Search
         J[8] = sp.jc[q];
     }
     const uint32_t m = sp.meta[q];
-    if (d.iters) d.iters[s] = (int32_t)(m & 0x7fffffffu);
+    if (d.iters) d.iters[s] = (int32_t)(m & 0x3fffffffu);
     d.converged[s] = (uint8_t)(m >> 31);
     if (d.keep) d.keep[s] = sp.keep[q];
 }
@@ -1555,6 +1563,11 @@ void deform_host_pipeline(fsk_ctx* ctx, const float* weights, const GridP& g, in
         if (i >= 2) cuda_check(cudaStreamWaitEvent(st, fetched[i - 2], 0), "cudaStreamWaitEvent");
         search_item(i, slot_r(i), slotcap);
         cuda_check(cudaEventRecord(done[i], st), "cudaEventRecord");
+    };
+    // the offsets download of item i is queued on the (in-order) copy stream only after item i-1's roots
+    // download, so that one never waits behind item i's search
+    auto enqueue_offsets = [&](int i) {
+        const Item& it = items[i];
         cuda_check(cudaStreamWaitEvent(ctx->copy, done[i], 0), "cudaStreamWaitEvent");
         if (it.m > 0)
             cuda_check(cudaMemcpyAsync(offsets[it.f] + it.p0, slot_o(i), it.m * sizeof(int64_t), cudaMemcpyDeviceToHost,
@@ -1567,7 +1580,10 @@ void deform_host_pipeline(fsk_ctx* ctx, const float* weights, const GridP& g, in
     };
     bool overflow = false;
     int64_t base = 0;
-    if (N > 0) enqueue(0);
+    if (N > 0) {
+        enqueue(0);
+        enqueue_offsets(0);
+    }
     for (int i = 0; i < N; ++i) {
         const Item& it = items[i];
         if (i + 1 < N) enqueue(i + 1);  // the device runs ahead while we wait
@@ -1610,6 +1626,7 @@ void deform_host_pipeline(fsk_ctx* ctx, const float* weights, const GridP& g, in
             offsets[it.f][n_points[it.f]] = base;
             totals[it.f] = base;
         }
+        if (i + 1 < N) enqueue_offsets(i + 1);
     }
     cuda_check(cudaStreamSynchronize(ctx->copy), "cudaStreamSynchronize");
     cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
