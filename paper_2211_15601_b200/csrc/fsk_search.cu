@@ -362,15 +362,27 @@ __device__ __forceinline__ void count_work(unsigned long long* stats, const Solv
 // same few canonical roots, and the iterations' gathers hit the cells the previous init left in
 // L1. B_i^-1 stays a block-uniform broadcast load. Solves flagged for escalation are appended
 // (warp-aggregated) to esc_q.
+#ifndef FSK_FAST_MAP
+#define FSK_FAST_MAP 1  // C2 fast pass: 0.556 -> 0.551 ms (bone groups of a tile on one SM in the first wave)
+#endif
 #ifndef FSK_FAST_BPG
 #define FSK_FAST_BPG 8  // bone inits per block (0: all). C2 fast pass: 1 0.638 ms, 2 0.594, 4 0.575, 8 0.572, 12 0.581, 24 0.601 (bone-major blocks: 0.633)
 #endif
 __global__ void __launch_bounds__(kSearchBlock, FSK_SEARCH_MINB)
     k_search_fast(Planes<float> P, GridP g, const float* __restrict__ bones, const float4* __restrict__ xs, int64_t n,
                   int bpg, SearchP o, SearchPlanes out, int4* __restrict__ esc_q, int64_t esc_cap,
-                  int* __restrict__ esc_count, unsigned long long* __restrict__ stats) {
+                  int* __restrict__ esc_count, unsigned long long* __restrict__ stats, int wave_sms) {
     const int ngroups = (g.nb + bpg - 1) / bpg;
+#if FSK_FAST_MAP == 1
+    // wave-aligned: blocks b, b + W, b + 2W, ... (W = SM count) land on one SM in the first wave under the
+    // breadth-first block dispatch — they take the bone groups of the same tile, so an SM's resident
+    // CTAs share that tile's cells in L1
+    const int W = wave_sms;
+    const int chunk = blockIdx.x / (W * ngroups), r = blockIdx.x - chunk * (W * ngroups);
+    const int grp = r / W, tile = chunk * W + (r - grp * W);
+#else
     const int tile = blockIdx.x / ngroups, grp = blockIdx.x - tile * ngroups;
+#endif
     const int64_t j = (int64_t)tile * kSearchBlock + threadIdx.x;
     if (j >= n) return;
     const float4 xq = __ldg(xs + j);
@@ -1179,14 +1191,20 @@ SearchState run_search(fsk_ctx* ctx, GridPlanes& P, const GridP& g, const float*
         const bool esc = needs_f64(flags);
         int4* esc_q = esc ? (int4*)scratch(ctx, kEscQ, S * sizeof(int4)) : nullptr;
         const int bpg = (FSK_FAST_BPG > 0) ? std::min(FSK_FAST_BPG, g.nb) : g.nb;
-        const int64_t nblocks = (int64_t)blocks_for(n, kSearchBlock) * ((g.nb + bpg - 1) / bpg);
+        const int ngrp = (g.nb + bpg - 1) / bpg;
+#if FSK_FAST_MAP == 1
+        const int64_t ntiles = blocks_for(n, kSearchBlock);
+        const int64_t nblocks = (ntiles + ctx->sm_count - 1) / ctx->sm_count * ctx->sm_count * ngrp;
+#else
+        const int64_t nblocks = (int64_t)blocks_for(n, kSearchBlock) * ngrp;
+#endif
         if (nblocks >= (int64_t(1) << 31)) fail(FSK_EINVAL, "fsk: search grid too large");
         SearchP spf = sp;
         if (!esc) {  // float32 only (ablation): no cap, no flags
             spf.esc_cap = sp.max_iters;
         }
         FSK_LAUNCH(ctx, st, k_search_fast, (unsigned)nblocks, kSearchBlock, 0, P.p32, g, bones, xs, n, bpg, spf, s.sp,
-                   esc_q, S, esc_n, ctx->stats);
+                   esc_q, S, esc_n, ctx->stats, ctx->sm_count);
         int per_sm = 0;  // persistent kernel: exactly the resident capacity
         // exact replay of the reference whenever the weight grid is at hand
         const bool exact_esc = weights && !(flags & FSK_SEARCH_FAST_ESC);

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <mutex>
+#include <random>
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
@@ -110,7 +111,10 @@ std::vector<float> points_f32(std::span<const Vec3> x) {
 void check_context(const SearchContext& c, SearchVariant variant) {
     if (c.bones.empty()) throw std::invalid_argument("search: no bone transforms");
     if (variant == SearchVariant::Mlp) {
-        throw std::invalid_argument("search: the MLP variant is not provided by fskin-b200 (voxel variant only)");
+        if (c.mlp == nullptr) throw std::invalid_argument("search: mlp variant needs a skinning mlp");
+        if (static_cast<size_t>(c.mlp->bone_count()) != c.bones.size())
+            throw std::invalid_argument("search: mlp bone count mismatch");
+        return;
     }
     if (c.grid == nullptr || c.tgrid == nullptr)
         throw std::invalid_argument("search: voxel variant needs skinning and transform grids");
@@ -306,6 +310,149 @@ SkinningVoxelGrid load_sknv(const std::string& path) {
     return grid;
 }
 
+// ------------------------------------------------------------------------ skinning MLP (host float64 utilities)
+namespace {
+int64_t mlp_param_count(const std::vector<int>& w) {
+    int64_t p = 0;
+    for (size_t l = 0; l + 1 < w.size(); ++l) p += (int64_t)w[l + 1] * w[l] + w[l + 1];
+    return p;
+}
+double softplus(double x) { return x > 0 ? x + std::log1p(std::exp(-x)) : std::log1p(std::exp(x)); }  // mlp.cpp
+double sigmoid(double x) { return x >= 0 ? 1.0 / (1.0 + std::exp(-x)) : std::exp(x) / (1.0 + std::exp(x)); }
+
+// forward (mlp.cpp:96-138) at one point with optional forward-mode tangents dX (3 columns): logits, and
+// d logits / dx when `tangent` (n_out x 3, row-major)
+std::vector<double> mlp_forward(const std::vector<int>& w, const std::vector<double>& th, const double* x,
+                                std::vector<double>* tangent) {
+    std::vector<double> h(x, x + w[0]), dh;
+    if (tangent) {
+        dh.assign((size_t)w[0] * 3, 0.0);
+        for (int a = 0; a < 3 && a < w[0]; ++a) dh[(size_t)a * 3 + a] = 1.0;
+    }
+    size_t off = 0;
+    for (size_t l = 0; l + 1 < w.size(); ++l) {
+        const int ni = w[l], no = w[l + 1];
+        const double* W = th.data() + off;  // column-major [no x ni]
+        const double* b = W + (size_t)no * ni;
+        off += (size_t)no * ni + no;
+        std::vector<double> z(no), dz(tangent ? (size_t)no * 3 : 0, 0.0);
+        for (int i = 0; i < no; ++i) {
+            double acc = 0.0;
+            for (int j = 0; j < ni; ++j) acc += W[(size_t)j * no + i] * h[j];
+            z[i] = acc + b[i];
+            if (tangent)
+                for (int c = 0; c < 3; ++c) {
+                    double t = 0.0;
+                    for (int j = 0; j < ni; ++j) t += W[(size_t)j * no + i] * dh[(size_t)j * 3 + c];
+                    dz[(size_t)i * 3 + c] = t;
+                }
+        }
+        const bool hidden = l + 2 < w.size();
+        if (hidden) {
+            for (int i = 0; i < no; ++i) {
+                if (tangent)
+                    for (int c = 0; c < 3; ++c) dz[(size_t)i * 3 + c] *= sigmoid(z[i]);
+                z[i] = softplus(z[i]);
+            }
+        }
+        h.swap(z);
+        if (tangent) dh.swap(dz);
+    }
+    if (tangent) *tangent = dh;
+    return h;
+}
+}  // namespace
+
+SkinningMlp::SkinningMlp(std::vector<int> widths, std::vector<double> parameters)
+    : widths_(std::move(widths)), theta_(std::move(parameters)) {
+    if (widths_.size() < 2) throw std::invalid_argument("Mlp: need at least input and output widths");
+    if (widths_.front() != 3) throw std::invalid_argument("SkinningMlp: network input width must be 3");
+    if ((int64_t)theta_.size() != mlp_param_count(widths_))
+        throw std::invalid_argument("Mlp::set_parameters: wrong parameter count");
+}
+
+SkinningMlp::SkinningMlp(int n_bones, std::uint64_t seed) {
+    if (n_bones < 1) throw std::invalid_argument("SkinningMlp: n_bones must be >= 1");
+    widths_ = {3, 64, 64, 64, n_bones};
+    theta_.assign((size_t)mlp_param_count(widths_), 0.0);
+    std::mt19937_64 rng(seed);  // Mlp::Mlp (mlp.cpp:81-94)
+    size_t off = 0;
+    for (size_t l = 0; l + 1 < widths_.size(); ++l) {
+        const int fan_in = widths_[l], no = widths_[l + 1];
+        std::normal_distribution<double> dist(0.0, std::sqrt(2.0 / fan_in));
+        for (size_t i = 0; i < (size_t)no * fan_in; ++i) theta_[off + i] = dist(rng);  // column-major data()
+        off += (size_t)no * fan_in + no;                                             // biases stay zero
+    }
+    // scale_output_layer(0.05) (skinning.cpp:16, mlp.cpp:225-228)
+    const size_t head = theta_.size() - ((size_t)widths_[3] * n_bones + n_bones);
+    for (size_t i = head; i < theta_.size(); ++i) theta_[i] *= 0.05;
+}
+
+SkinningMlp::SkinningMlp(int n_bones, std::uint64_t seed, const Aabb& domain) : SkinningMlp(n_bones, seed) {
+    // condition_input(center, half_extent) (mlp.cpp:230-239): W0.col(j) /= half_j; b0 -= W0 · center
+    const int no = widths_[1];
+    double* W0 = theta_.data();
+    double* b0 = W0 + (size_t)no * 3;
+    const Vec3 c = 0.5 * (domain.min + domain.max), h = 0.5 * domain.extent();
+    for (int j = 0; j < 3; ++j)
+        for (int i = 0; i < no; ++i) W0[(size_t)j * no + i] /= std::max(h[j], 1e-12);
+    for (int i = 0; i < no; ++i) b0[i] -= W0[i] * c[0] + W0[(size_t)no + i] * c[1] + W0[(size_t)2 * no + i] * c[2];
+}
+
+VectorXd SkinningMlp::weights(const Vec3& x) const {
+    const double xv[3] = {x[0], x[1], x[2]};
+    std::vector<double> z = mlp_forward(widths_, theta_, xv, nullptr);
+    double m = z[0];
+    for (double v : z) m = std::max(m, v);
+    VectorXd w((int64_t)z.size());
+    double sum = 0.0;
+    for (size_t i = 0; i < z.size(); ++i) sum += (w[(int64_t)i] = std::exp(z[i] - m));
+    for (size_t i = 0; i < z.size(); ++i) w[(int64_t)i] /= sum;
+    return w;
+}
+
+MatrixXd SkinningMlp::weight_jacobian(const Vec3& x) const {
+    const double xv[3] = {x[0], x[1], x[2]};
+    std::vector<double> dz;
+    mlp_forward(widths_, theta_, xv, &dz);
+    const VectorXd w = weights(x);
+    const int nb = bone_count();
+    MatrixXd J(nb, 3);
+    for (int c = 0; c < 3; ++c) {  // softmax head: dw_i = w_i (dz_i - sum_k w_k dz_k)
+        double s = 0.0;
+        for (int k = 0; k < nb; ++k) s += w[k] * dz[(size_t)k * 3 + c];
+        for (int i = 0; i < nb; ++i) J(i, c) = w[i] * (dz[(size_t)i * 3 + c] - s);
+    }
+    return J;
+}
+
+namespace {
+struct DevMlp {  // float32 device copy of a network's flat parameters (re-uploaded per call)
+    std::vector<float> th;
+    std::vector<int32_t> widths;
+    std::unique_ptr<DevBuf> buf;
+    explicit DevMlp(const SkinningMlp& m) : th(m.parameters().begin(), m.parameters().end()),
+                                            widths(m.widths().begin(), m.widths().end()) {
+        buf = std::make_unique<DevBuf>(th.size() * sizeof(float));
+        h2d(buf->p, th.data(), th.size() * sizeof(float));
+    }
+};
+}  // namespace
+
+SkinningVoxelGrid distill(const SkinningMlp& mlp, GridDims dims, const Aabb& bbox) {
+    SkinningVoxelGrid grid(dims, bbox, mlp.bone_count());
+    const DevMlp d(mlp);
+    const int64_t V = dims.vertex_count();
+    DevBuf out(static_cast<size_t>(V) * mlp.bone_count() * sizeof(float));
+    const fsk_grid_desc desc = desc_of(dims, bbox, mlp.bone_count());
+    check(fsk_distill(ctx(), d.buf->as<float>(), d.widths.data(), (int32_t)d.widths.size(), &desc, out.as<float>(),
+                      nullptr));
+    std::vector<float> w(static_cast<size_t>(V) * mlp.bone_count());
+    d2h(w.data(), out.p, w.size() * sizeof(float));
+    std::copy(w.begin(), w.end(), grid.raw().begin());
+    return grid;
+}
+
 // ------------------------------------------------------------------------ deformer
 Affine3 lbs_blend(std::span<const double> weights, std::span<const RigidTransform> bones) {
     if (weights.size() != bones.size()) throw std::invalid_argument("lbs_blend: weight/bone count mismatch");
@@ -320,6 +467,24 @@ Affine3 lbs_blend(std::span<const double> weights, std::span<const RigidTransfor
 Vec3 forward_deform(const Vec3& x, const SkinningVoxelGrid& grid, std::span<const RigidTransform> bones) {
     const VectorXd w = trilerp_weights(grid, x);
     return lbs_blend({w.data(), static_cast<size_t>(w.size())}, bones).apply(x);
+}
+
+Vec3 forward_deform(const Vec3& x, const SkinningMlp& mlp, std::span<const RigidTransform> bones) {
+    const VectorXd w = mlp.weights(x);
+    return lbs_blend({w.data(), static_cast<size_t>(w.size())}, bones).apply(x);
+}
+
+Mat3 deform_jacobian(const Vec3& x, const SkinningMlp& mlp, std::span<const RigidTransform> bones) {
+    const VectorXd w = mlp.weights(x);  // jacobian_from_weights (deformer.cpp:117-141)
+    const MatrixXd gw = mlp.weight_jacobian(x);
+    Mat3 J = Mat3::Zero();
+    for (size_t i = 0; i < bones.size(); ++i) J += w[static_cast<std::int64_t>(i)] * bones[i].rotation;
+    for (size_t i = 0; i < bones.size(); ++i) {
+        const Vec3 bx = bones[i].apply(x);
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) J(r, c) += bx[r] * gw(static_cast<std::int64_t>(i), c);
+    }
+    return J;
 }
 
 TransformGrid::TransformGrid(GridDims dims, Aabb bbox) : dims_(dims), bbox_(bbox) {
@@ -536,6 +701,15 @@ void SearchOptions::validate() const {
 std::vector<InitState> init_states(const Vec3& x_prime, const SearchContext& c, SearchVariant variant) {
     check_context(c, variant);
     const int nb = static_cast<int>(c.bones.size());
+    if (variant == SearchVariant::Mlp) {  // float64 host: J from the network's input tangents (:43-54)
+        std::vector<InitState> out(nb);
+        for (int i = 0; i < nb; ++i) {
+            out[i].x0 = c.bones[i].inverse().apply(x_prime);
+            const Mat3 J = deform_jacobian(out[i].x0, *c.mlp, c.bones);
+            out[i].inv_jacobian = std::abs(J.determinant()) < 1e-8 ? Mat3::Identity() : J.inverse();
+        }
+        return out;
+    }
     const std::vector<float> b = bones_f32(c.bones);
     const double p[3] = {x_prime[0], x_prime[1], x_prime[2]};
     const float* dw = device_weights(*c.grid);
@@ -557,35 +731,13 @@ std::vector<InitState> init_states(const Vec3& x_prime, const SearchContext& c, 
     return out;
 }
 
-std::vector<CorrespondenceSet> batch_search(std::span<const Vec3> queries, const SearchContext& c,
-                                            const SearchOptions& opts, int) {
-    check_context(c, opts.variant);
-    opts.validate();
-    const std::int64_t n = static_cast<std::int64_t>(queries.size());
+namespace {
+std::vector<CorrespondenceSet> to_sets(std::span<const Vec3> queries, const std::vector<std::int64_t>& h_offs,
+                                       const std::vector<fsk_root>& roots) {
     std::vector<CorrespondenceSet> out(queries.size());
-    for (size_t q = 0; q < queries.size(); ++q) out[q].query = queries[q];
-    if (n == 0) return out;
-    const int nb = static_cast<int>(c.bones.size());
-    const std::vector<float> b = bones_f32(c.bones);
-    const std::vector<float> p = points_f32(queries);
-    const std::int64_t cap = n * nb;  // every init of every query: no overflow possible
-    DevBuf db(b.size() * 4), dp(p.size() * 4), offs((n + 1) * 8), dr(cap * sizeof(fsk_root));
-    h2d(db.p, b.data(), b.size() * 4);
-    h2d(dp.p, p.data(), p.size() * 4);
-    const fsk_grid_desc d = desc_of(c.tgrid->dims(), c.tgrid->bbox(), nb);
-    const fsk_search_opts so = c_opts(opts);
-    // SearchContext::grid's weights go to the search like the reference's (J~0 from the weight grid,
-    // correspondence.cpp:43-54): the escalated solves then replay the reference's operation order
-    const float* dw = device_weights(*c.grid);
-    check(fsk_batch_search(ctx(), c.tgrid->device_data(), c.tgrid->device_data64(), dw, &d, db.as<float>(), nb,
-                           dp.as<float>(), n, &so, offs.as<std::int64_t>(), dr.as<fsk_root>(), cap, nullptr));
-    std::vector<std::int64_t> h_offs(n + 1);
-    d2h(h_offs.data(), offs.p, h_offs.size() * 8);
-    const std::int64_t total = h_offs[n];
-    std::vector<fsk_root> roots(static_cast<size_t>(total));
-    if (total > 0) d2h(roots.data(), dr.p, roots.size() * sizeof(fsk_root));
-    for (std::int64_t q = 0; q < n; ++q) {
-        auto& set = out[static_cast<size_t>(q)];
+    for (size_t q = 0; q < queries.size(); ++q) {
+        auto& set = out[q];
+        set.query = queries[q];
         for (std::int64_t k = h_offs[q]; k < h_offs[q + 1]; ++k) {
             const fsk_root& r = roots[static_cast<size_t>(k)];
             Root root;
@@ -599,6 +751,65 @@ std::vector<CorrespondenceSet> batch_search(std::span<const Vec3> queries, const
         }
     }
     return out;
+}
+}  // namespace
+
+// batch_search (correspondence.cpp:178-192) on the GPU. Voxel variant: K1's grids (the TransformGrid's
+// device mirrors), SearchContext::grid's weights for J~0 and the float64 replay, K2 + dedup + compaction;
+// root records count-then-allocate (4 per query first, the exact count on a rerun). Mlp variant: the
+// network at every Broyden iterate on the tensor cores (fsk_search_fwd_mlp), compacted likewise.
+std::vector<CorrespondenceSet> batch_search(std::span<const Vec3> queries, const SearchContext& c,
+                                            const SearchOptions& opts, int) {
+    check_context(c, opts.variant);
+    opts.validate();
+    const std::int64_t n = static_cast<std::int64_t>(queries.size());
+    if (n == 0) return to_sets(queries, {0}, {});
+    const int nb = static_cast<int>(c.bones.size());
+    const std::vector<float> b = bones_f32(c.bones);
+    const std::vector<float> p = points_f32(queries);
+    DevBuf db(b.size() * 4), dp(p.size() * 4), offs((n + 1) * 8);
+    h2d(db.p, b.data(), b.size() * 4);
+    h2d(dp.p, p.data(), p.size() * 4);
+    const fsk_search_opts so = c_opts(opts);
+    std::vector<std::int64_t> h_offs(n + 1);
+    std::vector<fsk_root> roots;
+    if (opts.variant == SearchVariant::Mlp) {
+        const DevMlp net(*c.mlp);
+        DevBuf xc(n * nb * 12), ji(n * nb * 36), rs(n * nb * 4), it(n * nb * 4), cv(n * nb), kp(n * nb), nr(n * 4);
+        fsk_search_out o{xc.as<float>(), ji.as<float>(), rs.as<float>(), it.as<std::int32_t>(), cv.as<std::uint8_t>(),
+                         kp.as<std::uint8_t>(), nr.as<std::int32_t>(), nullptr};
+        check(fsk_search_fwd_mlp(ctx(), net.buf->as<float>(), net.widths.data(), (int32_t)net.widths.size(),
+                                 db.as<float>(), nb, dp.as<float>(), n, &so, &o, nullptr));
+        std::int64_t total = 0;
+        const int rc = fsk_compact_roots(ctx(), &o, n, nb, offs.as<std::int64_t>(), nullptr, 0, &total, nullptr);
+        if (rc != FSK_OK && total == 0) check(rc);
+        DevBuf dr(std::max<std::int64_t>(1, total) * sizeof(fsk_root));
+        check(fsk_compact_roots(ctx(), &o, n, nb, offs.as<std::int64_t>(), dr.as<fsk_root>(), total, &total, nullptr));
+        d2h(h_offs.data(), offs.p, h_offs.size() * 8);
+        roots.resize(static_cast<size_t>(total));
+        if (total > 0) d2h(roots.data(), dr.p, roots.size() * sizeof(fsk_root));
+        return to_sets(queries, h_offs, roots);
+    }
+    const fsk_grid_desc d = desc_of(c.tgrid->dims(), c.tgrid->bbox(), nb);
+    // SearchContext::grid's weights go to the search like the reference's (J~0 from the weight grid,
+    // correspondence.cpp:43-54): the escalated solves then replay the reference's operation order
+    const float* dw = device_weights(*c.grid);
+    std::int64_t cap = std::min<std::int64_t>(n * nb, 4 * n);
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        DevBuf dr(cap * sizeof(fsk_root));
+        check(fsk_batch_search(ctx(), c.tgrid->device_data(), c.tgrid->device_data64(), dw, &d, db.as<float>(), nb,
+                               dp.as<float>(), n, &so, offs.as<std::int64_t>(), dr.as<fsk_root>(), cap, nullptr));
+        d2h(h_offs.data(), offs.p, h_offs.size() * 8);
+        const std::int64_t total = h_offs[n];
+        if (total > cap) {  // more kept roots than records: search again into exactly that many
+            cap = total;
+            continue;
+        }
+        roots.resize(static_cast<size_t>(total));
+        if (total > 0) d2h(roots.data(), dr.p, roots.size() * sizeof(fsk_root));
+        break;
+    }
+    return to_sets(queries, h_offs, roots);
 }
 
 CorrespondenceSet broyden_search(const Vec3& x_prime, const SearchContext& c, const SearchOptions& opts) {

@@ -196,6 +196,52 @@ int main(int argc, char** argv) {
         CHECK(ge.d_tgrid.size() == static_cast<size_t>(grid.dims().vertex_count()) * 12);
         CHECK(dotv / std::sqrt(na * nb2) > 0.9);
     }
+    // SearchVariant::Mlp (correspondence.cpp:77-79): the reference's SkinningMlp init, distilled to a grid
+    // (skinning.cpp:195-221); the MLP-variant search through the same API; its root sets vs the voxel
+    // variant on the distilled grid (SPEC acceptance 3); init_states of the MLP variant
+    if (argc > 5) {
+        const SkinningMlp mlp(nb, 7, grid.bbox());
+        CHECK(mlp.bone_count() == nb && mlp.widths().front() == 3);
+        double wsum = 0.0;
+        const VectorXd w0 = mlp.weights(queries[0]);
+        for (std::int64_t i = 0; i < w0.size(); ++i) wsum += w0[i];
+        CHECK(std::abs(wsum - 1.0) < 1e-12);
+        const SkinningVoxelGrid dg = distill(mlp, GridDims{64, 64, 16}, grid.bbox());
+        const TransformGrid dtg = precompute_transform_grid(dg, bones);
+        const int m = std::min(n, 2000);
+        const std::span<const Vec3> q(queries.data(), m);
+        SearchOptions mo = opts;
+        mo.variant = SearchVariant::Mlp;
+        const SearchContext mctx{bones, &mlp, nullptr, nullptr};
+        const std::vector<CorrespondenceSet> ms = batch_search(q, mctx, mo);
+        const std::vector<CorrespondenceSet> vs = batch_search(q, SearchContext{bones, nullptr, &dg, &dtg}, opts);
+        int match = 0;
+        for (int p = 0; p < m; ++p) {
+            bool ok = ms[p].roots.size() == vs[p].roots.size();
+            for (size_t k = 0; ok && k < ms[p].roots.size(); ++k)
+                ok = (ms[p].roots[k].x - vs[p].roots[k].x).norm() < 1e-2 * grid.bbox().diagonal();
+            match += ok;
+        }
+        std::printf("mlp vs voxel (64x64x16 distilled): %d / %d root sets match\n", match, m);
+        CHECK(match >= 0.99 * m);
+        const auto st = init_states(queries[3], mctx, SearchVariant::Mlp);
+        CHECK(st.size() == static_cast<size_t>(nb));
+        for (int i = 0; i < nb; ++i) CHECK((st[i].x0 - bones[i].inverse().apply(queries[3])).norm() < 1e-12);
+        expect_invalid([&] { SearchContext c2 = mctx; c2.mlp = nullptr; batch_search(q, c2, mo); },
+                       "search: mlp variant needs a skinning mlp");
+        std::FILE* th = std::fopen(argv[4], "wb");
+        std::fwrite(mlp.parameters().data(), sizeof(double), mlp.parameters().size(), th);
+        std::fclose(th);
+        std::FILE* f2 = std::fopen(argv[5], "w");
+        for (const auto& sset : ms) {
+            std::fprintf(f2, "%zu", sset.roots.size());
+            for (const Root& r : sset.roots)
+                std::fprintf(f2, " %d %.9g %.9g %.9g %.9g %d", r.source_bone, r.x.x(), r.x.y(), r.x.z(), r.residual,
+                             r.iterations);
+            std::fprintf(f2, "\n");
+        }
+        std::fclose(f2);
+    }
     // dedup_roots
     std::vector<Root> rr(3);
     rr[0].x = Vec3(0, 0, 0);
@@ -214,7 +260,7 @@ int main(int argc, char** argv) {
     expect_invalid([&] { precompute_transform_grid(grid, std::span<const RigidTransform>(bones).first(nb - 1)); },
                    "precompute_transform_grid: bone count mismatch");
     expect_invalid([&] { SearchOptions o = opts; o.variant = SearchVariant::Mlp; batch_search(queries, ctx, o); },
-                   "MLP variant");
+                   "search: mlp variant needs a skinning mlp");
     // empty query list → empty result
     CHECK(batch_search(std::span<const Vec3>(), ctx, opts).empty());
     std::printf("fskin_api_check: %d failures\n", fails);

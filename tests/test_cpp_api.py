@@ -60,7 +60,9 @@ def test_cpp_api_batch_search_matches_oracle(tmp_path, max_iters, seed, points):
     sc = S.make_scene((32, 32, 32), n, seed=seed, points=points)
     inp, out, ist = tmp_path / "in.bin", tmp_path / "sets.txt", tmp_path / "init.bin"
     _write_input(inp, sc, max_iters)
-    r = subprocess.run([exe, str(inp), str(out), str(ist)], capture_output=True, text=True, timeout=600)
+    th_path, ms_path = tmp_path / "mlp_theta.bin", tmp_path / "mlp_sets.txt"
+    r = subprocess.run([exe, str(inp), str(out), str(ist), str(th_path), str(ms_path)], capture_output=True, text=True,
+                       timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     ref = oracle.batch_search(sc.weights, sc.dims, sc.bbox, sc.bones, sc.points, workers=os.cpu_count() or 8,
                               **sc.search_options(max_iters))
@@ -89,3 +91,16 @@ def test_cpp_api_batch_search_matches_oracle(tmp_path, max_iters, seed, points):
     rx0, rj0 = oracle.init_states(sc.weights, sc.dims, sc.bbox, sc.bones, sc.points[1:2])
     np.testing.assert_array_equal(a[:3 * nb].reshape(nb, 3), rx0[0])
     np.testing.assert_array_equal(a[3 * nb:].reshape(nb, 3, 3), rj0[0])
+    # SearchVariant::Mlp through the API: the reference's SkinningMlp(n_b, seed, domain) init, its search on the
+    # tensor cores, vs the oracle's MLP-variant search on the same (float32-rounded) parameters
+    theta = np.fromfile(th_path, np.float64).astype(np.float32).astype(np.float64)
+    widths = [3, 64, 64, 64, sc.n_bones]
+    m = 2000
+    mr = oracle.batch_search_mlp(theta, widths, sc.bones, sc.points[:m], workers=os.cpu_count() or 8,
+                                 **sc.search_options(max_iters))
+    msets = _read_sets(ms_path, m)
+    same = sum([b for b, _, _ in s_] == list(np.where(mr["keep"][p] == 1)[0]) for p, s_ in enumerate(msets))
+    mdx = max((float(np.abs(x - mr["x_c"][p, b]).max()) for p, s_ in enumerate(msets) for b, x, _ in s_
+               if mr["keep"][p, b]), default=0.0)
+    print(f"C++ API MLP variant: identical root sets {same}/{m} vs the oracle, max|dx| {mdx:.2e}")
+    assert same / m >= 0.999 and mdx <= 1e-4
