@@ -18,9 +18,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB = os.path.join(_HERE, "liboracle.so")
 # operation-order variants of the same restatement (oracle/Makefile): the reference's
 # Eigen version and build flags are not pinned, so its exact float64 operation order is not either
-VARIANTS = ("eigen", "invrow0", "pairsum", "fma")
+VARIANTS = ("fma", "unfused", "invrow0", "pairsum", "gccfma")
 _libs = {}
-_variant = None  # module-wide default for every call below (None = "eigen"); see use_variant()
+_variant = None  # module-wide default for every call below (None = "fma", the default build); see use_variant()
 
 _d = ctypes.POINTER(ctypes.c_double)
 _u8 = ctypes.POINTER(ctypes.c_uint8)
@@ -30,7 +30,7 @@ _int = ctypes.c_int
 
 
 def _path(variant):
-    return _LIB if variant in (None, "eigen") else os.path.join(_HERE, f"liboracle_{variant}.so")
+    return _LIB if variant in (None, "fma") else os.path.join(_HERE, f"liboracle_{variant}.so")
 
 
 def build(force: bool = False) -> str:
@@ -46,12 +46,12 @@ def use_variant(variant):
     global _variant
     if variant not in (None,) + VARIANTS:
         raise ValueError(variant)
-    _variant = None if variant == "eigen" else variant
+    _variant = None if variant == "fma" else variant
 
 
 def lib(variant=None):
     variant = variant if variant is not None else _variant
-    key = variant or "eigen"
+    key = variant or "fma"
     if key not in _libs:
         build()
         L = ctypes.CDLL(_path(variant))

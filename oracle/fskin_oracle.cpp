@@ -33,17 +33,31 @@
 namespace orc {
 
 // ---------------------------------------------------------------- tiny linear algebra
-// Eigen's fixed-size 3-term reductions (mat-vec coefficients, dot, squaredNorm) sum either left to
-// right, (a+b)+c — the packet path with a 2-wide double packet plus a scalar tail, the default
-// here — or as a+(b+c) — the unvectorized redux unroller (HalfLength = 1). Which one a build uses
-// depends on the Eigen version, the compiler flags (`-march=native`, proj/CMakeLists.txt:10-14)
-// and the CPU; ORC_SUM_PAIR builds the second (oracle variant "pairsum": the
-// reference is not pinned to one operation order).
-static inline double sum3(double a, double b, double c) {
-#ifdef ORC_SUM_PAIR
-    return a + (b + c);
+// Operation order. The reference is built with -march=native under CMake's default -std=gnu++20
+// (proj/CMakeLists.txt:3-14): GCC contracts `a*b + c` into FMA (-ffp-contract=fast is the GNU-mode
+// default) and Eigen's products accumulate with pmadd, so the reference binary on any FMA-capable
+// host computes with fused multiply-adds. The default restatement states one such contraction
+// explicitly and compiler-independently (std::fma): every addition (or subtraction) whose right
+// operand is a product is one FMA —
+//   acc + a·b -> fma(a, b, acc);  a0b0 + a1b1 + a2b2 -> fma(a2, b2, fma(a1, b1, a0·b0));
+//   a·b − c·d -> fma(−c, d, a·b).
+// Builds of other plausible operation orders (oracle/Makefile; Eigen unpinned):
+//   ORC_UNFUSED — no contraction (each product rounded; the round-1 oracle), with
+//     ORC_INV_ROW0 — inverse()'s determinant along row 0,  ORC_SUM_PAIR — 3-term sums as a+(b+c)
+//     (Eigen's unvectorized redux unroller), or GCC's own -ffp-contract=fast on the unfused source.
+#if defined(ORC_UNFUSED)
+static inline double madd(double acc, double a, double b) { return acc + a * b; }
+static inline double msub(double a, double b, double c, double d) { return a * b - c * d; }
 #else
-    return (a + b) + c;
+static inline double madd(double acc, double a, double b) { return std::fma(a, b, acc); }
+static inline double msub(double a, double b, double c, double d) { return std::fma(-c, d, a * b); }
+#endif
+// a0·b0 + a1·b1 + a2·b2 (Eigen's 3-term redux: mat-vec coefficients, dot, squaredNorm)
+static inline double dot3(double a0, double b0, double a1, double b1, double a2, double b2) {
+#if defined(ORC_SUM_PAIR)
+    return a0 * b0 + (a1 * b1 + a2 * b2);
+#else
+    return madd(madd(a0 * b0, a1, b1), a2, b2);
 #endif
 }
 struct V3 {
@@ -61,37 +75,36 @@ struct M3 {
 };
 static inline V3 mul(const M3& a, const V3& x) {
     V3 r;
-    for (int i = 0; i < 3; ++i) r[i] = sum3(a.m[i][0] * x[0], a.m[i][1] * x[1], a.m[i][2] * x[2]);
+    for (int i = 0; i < 3; ++i) r[i] = dot3(a.m[i][0], x[0], a.m[i][1], x[1], a.m[i][2], x[2]);
     return r;
 }
-static inline double dot(const V3& a, const V3& b) { return sum3(a[0] * b[0], a[1] * b[1], a[2] * b[2]); }
+static inline double dot(const V3& a, const V3& b) { return dot3(a[0], b[0], a[1], b[1], a[2], b[2]); }
 static inline double norm(const V3& a) { return std::sqrt(dot(a, a)); }
 
-// Eigen's closed-form 3×3 determinant (Determinant.h: expansion along the first row).
+// Eigen's closed-form 3×3 determinant (Determinant.h: expansion along the first row),
+// h(0,1,2) − h(1,0,2) + h(2,0,1) with h(c0,c1,c2) = a0c0·(a1c1·a2c2 − a1c2·a2c1).
 static inline double det3(const M3& a) {
-    auto h = [&](int c0, int c1, int c2) {
-        return a.m[0][c0] * (a.m[1][c1] * a.m[2][c2] - a.m[1][c2] * a.m[2][c1]);
-    };
-    return h(0, 1, 2) - h(1, 0, 2) + h(2, 0, 1);
+    auto X = [&](int c1, int c2) { return msub(a.m[1][c1], a.m[2][c2], a.m[1][c2], a.m[2][c1]); };
+    return madd(madd(a.m[0][0] * X(1, 2), -a.m[0][1], X(0, 2)), a.m[0][2], X(0, 1));
 }
 // Eigen's 3×3 inverse (InverseImpl.h compute_inverse<.., 3>): the cofactors of column 0, their
 // determinant (cofactors_col0 · col(0), a 3-term redux), 1/det, then every cofactor times 1/det.
 // ORC_INV_ROW0 (variant "invrow0", the round-1 oracle) takes that determinant along row 0.
 static inline M3 inv3(const M3& a) {
     M3 c;
-    c.m[0][0] = a.m[1][1] * a.m[2][2] - a.m[1][2] * a.m[2][1];
-    c.m[0][1] = a.m[0][2] * a.m[2][1] - a.m[0][1] * a.m[2][2];
-    c.m[0][2] = a.m[0][1] * a.m[1][2] - a.m[0][2] * a.m[1][1];
-    c.m[1][0] = a.m[1][2] * a.m[2][0] - a.m[1][0] * a.m[2][2];
-    c.m[1][1] = a.m[0][0] * a.m[2][2] - a.m[0][2] * a.m[2][0];
-    c.m[1][2] = a.m[0][2] * a.m[1][0] - a.m[0][0] * a.m[1][2];
-    c.m[2][0] = a.m[1][0] * a.m[2][1] - a.m[1][1] * a.m[2][0];
-    c.m[2][1] = a.m[0][1] * a.m[2][0] - a.m[0][0] * a.m[2][1];
-    c.m[2][2] = a.m[0][0] * a.m[1][1] - a.m[0][1] * a.m[1][0];
+    c.m[0][0] = msub(a.m[1][1], a.m[2][2], a.m[1][2], a.m[2][1]);
+    c.m[0][1] = msub(a.m[0][2], a.m[2][1], a.m[0][1], a.m[2][2]);
+    c.m[0][2] = msub(a.m[0][1], a.m[1][2], a.m[0][2], a.m[1][1]);
+    c.m[1][0] = msub(a.m[1][2], a.m[2][0], a.m[1][0], a.m[2][2]);
+    c.m[1][1] = msub(a.m[0][0], a.m[2][2], a.m[0][2], a.m[2][0]);
+    c.m[1][2] = msub(a.m[0][2], a.m[1][0], a.m[0][0], a.m[1][2]);
+    c.m[2][0] = msub(a.m[1][0], a.m[2][1], a.m[1][1], a.m[2][0]);
+    c.m[2][1] = msub(a.m[0][1], a.m[2][0], a.m[0][0], a.m[2][1]);
+    c.m[2][2] = msub(a.m[0][0], a.m[1][1], a.m[0][1], a.m[1][0]);
 #ifdef ORC_INV_ROW0
-    const double det = a.m[0][0] * c.m[0][0] + a.m[0][1] * c.m[1][0] + a.m[0][2] * c.m[2][0];
+    const double det = dot3(a.m[0][0], c.m[0][0], a.m[0][1], c.m[1][0], a.m[0][2], c.m[2][0]);
 #else
-    const double det = sum3(c.m[0][0] * a.m[0][0], c.m[0][1] * a.m[1][0], c.m[0][2] * a.m[2][0]);
+    const double det = dot3(c.m[0][0], a.m[0][0], c.m[0][1], a.m[1][0], c.m[0][2], a.m[2][0]);
 #endif
     const double inv = 1.0 / det;
     for (int i = 0; i < 3; ++i)
@@ -124,14 +137,14 @@ static inline V3 lu_solve_transposed(const M3& J, const V3& v) {
             for (int i = k + 1; i < 3; ++i) m[i][k] /= m[k][k];
         }
         for (int i = k + 1; i < 3; ++i)
-            for (int j = k + 1; j < 3; ++j) m[i][j] -= m[i][k] * m[k][j];
+            for (int j = k + 1; j < 3; ++j) m[i][j] = madd(m[i][j], -m[i][k], m[k][j]);
     }
     double x[3] = {v[perm[0]], v[perm[1]], v[perm[2]]};
     for (int j = 0; j < 3; ++j)  // unit lower
-        for (int i = j + 1; i < 3; ++i) x[i] -= x[j] * m[i][j];
+        for (int i = j + 1; i < 3; ++i) x[i] = madd(x[i], -x[j], m[i][j]);
     for (int j = 2; j >= 0; --j) {  // upper
         x[j] /= m[j][j];
-        for (int i = 0; i < j; ++i) x[i] -= x[j] * m[i][j];
+        for (int i = 0; i < j; ++i) x[i] = madd(x[i], -x[j], m[i][j]);
     }
     return V3{{x[0], x[1], x[2]}};
 }
@@ -218,7 +231,7 @@ static void trilerp_weights_into(const Grid& g, const V3& x, double* out) {
             for (int di = 0; di < 2; ++di) {
                 const double w = wyz * (di ? c.tx : 1.0 - c.tx);
                 const double* v = g.w + g.vidx(c.i0 + di, c.j0 + dj, c.k0 + dk) * g.nb;
-                for (int b = 0; b < g.nb; ++b) out[b] += w * v[b];
+                for (int b = 0; b < g.nb; ++b) out[b] = madd(out[b], w, v[b]);
             }
         }
     }
@@ -243,9 +256,9 @@ static void weight_spatial_gradient(const Grid& g, const V3& x, double* out) {
                 const double gy = fx[di] * dy[dj] * fz[dk];
                 const double gz = fx[di] * fy[dj] * dz[dk];
                 for (int b = 0; b < g.nb; ++b) {
-                    out[b * 3 + 0] += gx * v[b];
-                    out[b * 3 + 1] += gy * v[b];
-                    out[b * 3 + 2] += gz * v[b];
+                    out[b * 3 + 0] = madd(out[b * 3 + 0], gx, v[b]);
+                    out[b * 3 + 1] = madd(out[b * 3 + 1], gy, v[b]);
+                    out[b * 3 + 2] = madd(out[b * 3 + 2], gz, v[b]);
                 }
             }
 }
@@ -255,8 +268,8 @@ static void lbs_blend(const double* w, const std::vector<Rigid>& bones, double* 
     for (int e = 0; e < 12; ++e) out12[e] = 0.0;
     for (size_t i = 0; i < bones.size(); ++i) {
         for (int r = 0; r < 3; ++r) {
-            for (int c = 0; c < 3; ++c) out12[r * 4 + c] += w[i] * bones[i].r.m[r][c];
-            out12[r * 4 + 3] += w[i] * bones[i].t[r];
+            for (int c = 0; c < 3; ++c) out12[r * 4 + c] = madd(out12[r * 4 + c], w[i], bones[i].r.m[r][c]);
+            out12[r * 4 + 3] = madd(out12[r * 4 + 3], w[i], bones[i].t[r]);
         }
     }
 }
@@ -291,7 +304,7 @@ static void trilerp_transform_into(const Grid& g, const double* tgrid, const V3&
             for (int di = 0; di < 2; ++di) {
                 const double w = wyz * (di ? c.tx : 1.0 - c.tx);
                 const double* m = tgrid + g.vidx(c.i0 + di, c.j0 + dj, c.k0 + dk) * 12;
-                for (int e = 0; e < 12; ++e) out12[e] += w * m[e];
+                for (int e = 0; e < 12; ++e) out12[e] = madd(out12[e], w, m[e]);
             }
         }
     }
@@ -302,9 +315,8 @@ static void trilerp_transform_into(const Grid& g, const double* tgrid, const V3&
 static V3 forward_deform_tgrid(const Grid& g, const double* tgrid, const V3& x) {
     double m[12];
     trilerp_transform_into(g, tgrid, x, m);
-    return V3{{m[0] * x[0] + m[1] * x[1] + m[2] * x[2] + m[3],
-               m[4] * x[0] + m[5] * x[1] + m[6] * x[2] + m[7],
-               m[8] * x[0] + m[9] * x[1] + m[10] * x[2] + m[11]}};
+    return V3{{dot3(m[0], x[0], m[1], x[1], m[2], x[2]) + m[3], dot3(m[4], x[0], m[5], x[1], m[6], x[2]) + m[7],
+               dot3(m[8], x[0], m[9], x[1], m[10], x[2]) + m[11]}};
 }
 
 // deform_jacobian(x, grid, bones) (deformer.cpp:117-136) via jacobian_from_weights:
@@ -316,11 +328,11 @@ static M3 deform_jacobian(const Grid& g, const std::vector<Rigid>& bones, const 
     M3 jac;
     for (size_t i = 0; i < bones.size(); ++i)
         for (int r = 0; r < 3; ++r)
-            for (int c = 0; c < 3; ++c) jac.m[r][c] += wbuf[i] * bones[i].r.m[r][c];
+            for (int c = 0; c < 3; ++c) jac.m[r][c] = madd(jac.m[r][c], wbuf[i], bones[i].r.m[r][c]);
     for (size_t i = 0; i < bones.size(); ++i) {
         const V3 bx = bones[i].apply(x);
         for (int r = 0; r < 3; ++r)
-            for (int c = 0; c < 3; ++c) jac.m[r][c] += bx[r] * gbuf[i * 3 + c];
+            for (int c = 0; c < 3; ++c) jac.m[r][c] = madd(jac.m[r][c], bx[r], gbuf[i * 3 + c]);
     }
     return jac;
 }
@@ -377,9 +389,9 @@ static void iterate(State& st, const V3& xp, const Grid& g, const double* tgrid,
             for (int i = 0; i < 3; ++i) r[i] = (dx[i] - jdg[i]) / denom;
             V3 wrow;  // dxᵀ J̃
             for (int c = 0; c < 3; ++c)
-                wrow[c] = sum3(dx[0] * st.inv_jac.m[0][c], dx[1] * st.inv_jac.m[1][c], dx[2] * st.inv_jac.m[2][c]);
+                wrow[c] = dot3(dx[0], st.inv_jac.m[0][c], dx[1], st.inv_jac.m[1][c], dx[2], st.inv_jac.m[2][c]);
             for (int i = 0; i < 3; ++i)
-                for (int c = 0; c < 3; ++c) st.inv_jac.m[i][c] += r[i] * wrow[c];
+                for (int c = 0; c < 3; ++c) st.inv_jac.m[i][c] = madd(st.inv_jac.m[i][c], r[i], wrow[c]);
         }
     }
 }
@@ -499,7 +511,7 @@ int orc_eval_points(const double* w, int nx, int ny, int nz, int nb, const doubl
                 double m[12];
                 lbs_blend(wb.data(), B, m);
                 for (int r = 0; r < 3; ++r)
-                    d_grid_out[3 * p + r] = m[r * 4] * xp[0] + m[r * 4 + 1] * xp[1] + m[r * 4 + 2] * xp[2] + m[r * 4 + 3];
+                    d_grid_out[3 * p + r] = dot3(m[r * 4], xp[0], m[r * 4 + 1], xp[1], m[r * 4 + 2], xp[2]) + m[r * 4 + 3];
             }
             if (jac_out) {
                 const M3 j = deform_jacobian(g, B, xp, wb, gb);
@@ -583,13 +595,13 @@ int orc_batch_search(const double* w, int nx, int ny, int nz, int nb, const doub
 }
 
 // dedup_roots (correspondence.cpp:162-176) over m roots xs[m][3].
-// Which operation-order variant this build is (oracle/Makefile): "eigen" (default), "invrow0",
-// "pairsum", "fma".
+// Which operation-order variant this build is (oracle/Makefile): "fma" (default), "unfused",
+// "invrow0", "pairsum", "gccfma".
 const char* orc_variant(void) {
 #if defined(ORC_VARIANT_NAME)
     return ORC_VARIANT_NAME;
 #else
-    return "eigen";
+    return "fma";
 #endif
 }
 
@@ -623,7 +635,7 @@ int orc_grid_vjp(int nx, int ny, int nz, int nb, const double* bbox6, const doub
                 for (int c = 0; c < 3; ++c) J.m[r][c] = jinv[9 * p + 3 * r + c];
             V3 u;  // u = −J̃ᵀ v (diff.cpp:351)
             for (int c = 0; c < 3; ++c)
-                u[c] = -sum3(J.m[0][c] * v[3 * p], J.m[1][c] * v[3 * p + 1], J.m[2][c] * v[3 * p + 2]);
+                u[c] = -dot3(J.m[0][c], v[3 * p], J.m[1][c], v[3 * p + 1], J.m[2][c], v[3 * p + 2]);
             std::vector<double> uw(nb);
             for (int i = 0; i < nb; ++i) uw[i] = dot(u, B[i].apply(xs));  // diff.cpp:354-356
             const Cell c = locate(g, xs, false);
@@ -636,11 +648,12 @@ int orc_grid_vjp(int nx, int ny, int nz, int nb, const double* bbox6, const doub
                         const int64_t vi = g.vidx(c.i0 + di, c.j0 + dj, c.k0 + dk);
                         if (grad_T)
                             for (int r = 0; r < 3; ++r) {
-                                for (int col = 0; col < 3; ++col) grad_T[vi * 12 + r * 4 + col] += phi * u[r] * xs[col];
-                                grad_T[vi * 12 + r * 4 + 3] += phi * u[r];
+                                for (int col = 0; col < 3; ++col)
+                                    grad_T[vi * 12 + r * 4 + col] = madd(grad_T[vi * 12 + r * 4 + col], phi * u[r], xs[col]);
+                                grad_T[vi * 12 + r * 4 + 3] = madd(grad_T[vi * 12 + r * 4 + 3], phi, u[r]);
                             }
                         if (grad_w)
-                            for (int i = 0; i < nb; ++i) grad_w[vi * nb + i] += phi * uw[i];
+                            for (int i = 0; i < nb; ++i) grad_w[vi * nb + i] = madd(grad_w[vi * nb + i], phi, uw[i]);
                     }
                 }
             }

@@ -125,18 +125,18 @@ __device__ __forceinline__ void lu_solve_T(const double J[9], const double v[3],
 #pragma unroll
         for (int i = k + 1; i < 3; ++i)
 #pragma unroll
-            for (int j = k + 1; j < 3; ++j) m[i][j] = sub(m[i][j], mul(m[i][k], m[k][j]));
+            for (int j = k + 1; j < 3; ++j) m[i][j] = madd(m[i][j], -m[i][k], m[k][j]);
     }
     double y[3] = {v[perm[0]], v[perm[1]], v[perm[2]]};
 #pragma unroll
     for (int j = 0; j < 3; ++j)
 #pragma unroll
-        for (int i = j + 1; i < 3; ++i) y[i] = sub(y[i], mul(y[j], m[i][j]));
+        for (int i = j + 1; i < 3; ++i) y[i] = madd(y[i], -y[j], m[i][j]);
 #pragma unroll
     for (int j = 2; j >= 0; --j) {
         y[j] = div(y[j], m[j][j]);
 #pragma unroll
-        for (int i = 0; i < j; ++i) y[i] = sub(y[i], mul(y[j], m[i][j]));
+        for (int i = 0; i < j; ++i) y[i] = madd(y[i], -y[j], m[i][j]);
     }
     x[0] = y[0];
     x[1] = y[1];
@@ -161,8 +161,8 @@ __global__ void __launch_bounds__(128) k_implicit_exact(GridP g, const float* __
         double J[9];
         exact::jacobian(g, W, s_b64, (double)xs[0], (double)xs[1], (double)xs[2], J);
         using namespace exact;
-        auto h = [&](int c0, int c1, int c2) { return mul(J[c0], sub(mul(J[3 + c1], J[6 + c2]), mul(J[3 + c2], J[6 + c1]))); };
-        det = add(sub(h(0, 1, 2), h(1, 0, 2)), h(2, 0, 1));  // Mat3::determinant (diff.cpp:34)
+        auto X = [&](int c1, int c2) { return msub(J[3 + c1], J[6 + c2], J[3 + c2], J[6 + c1]); };
+        det = madd(madd(mul(J[0], X(1, 2)), -J[1], X(0, 2)), J[2], X(0, 1));  // Mat3::determinant (diff.cpp:34)
         if (fabs(det) >= 1e-10) {  // (:35) NaN det: singular as well
             const double v[3] = {(double)gx[3 * p], (double)gx[3 * p + 1], (double)gx[3 * p + 2]};
             double x[3];

@@ -33,9 +33,15 @@ __device__ __forceinline__ double div(double a, double b) { return a * __drcp_rn
 #else
 __device__ __forceinline__ double div(double a, double b) { return __ddiv_rn(a, b); }
 #endif
-// a0*b0 + a1*b1 + a2*b2, left to right
+// The oracle's contraction rule (oracle/fskin_oracle.cpp): every addition whose right operand is a
+// product is one fused multiply-add, the reference's -march=native/gnu++20 build contracting its
+// scalar code and Eigen accumulating with pmadd:
+//   acc + a·b -> fma(a, b, acc);  a0b0 + a1b1 + a2b2 -> fma(a2, b2, fma(a1, b1, a0·b0));  a·b − c·d -> fma(−c, d, a·b)
+__device__ __forceinline__ double madd(double acc, double a, double b) { return __fma_rn(a, b, acc); }
+__device__ __forceinline__ double msub(double a, double b, double c, double d) { return __fma_rn(-c, d, mul(a, b)); }
+// a0*b0 + a1*b1 + a2*b2 (argument order as the round-1 replay: a0 a1 a2 then b0 b1 b2)
 __device__ __forceinline__ double dot3(double a0, double a1, double a2, double b0, double b1, double b2) {
-    return add(add(mul(a0, b0), mul(a1, b1)), mul(a2, b2));
+    return madd(madd(mul(a0, b0), a1, b1), a2, b2);
 }
 
 struct XCell {
@@ -89,14 +95,14 @@ __device__ __forceinline__ void deform(const Planes<double>& P, const GridP& g, 
             V4<double> a, b;
             load_edge(P, vidx(g, c.i, c.j + (e & 1), c.k + (e >> 1)), r, a, b);
             const double w0 = mul(wyz[e], w0x), w1 = mul(wyz[e], w1x);
-            m[4 * r + 0] = add(m[4 * r + 0], mul(w0, a.x));
-            m[4 * r + 1] = add(m[4 * r + 1], mul(w0, a.y));
-            m[4 * r + 2] = add(m[4 * r + 2], mul(w0, a.z));
-            m[4 * r + 3] = add(m[4 * r + 3], mul(w0, a.w));
-            m[4 * r + 0] = add(m[4 * r + 0], mul(w1, b.x));
-            m[4 * r + 1] = add(m[4 * r + 1], mul(w1, b.y));
-            m[4 * r + 2] = add(m[4 * r + 2], mul(w1, b.z));
-            m[4 * r + 3] = add(m[4 * r + 3], mul(w1, b.w));
+            m[4 * r + 0] = madd(m[4 * r + 0], w0, a.x);
+            m[4 * r + 1] = madd(m[4 * r + 1], w0, a.y);
+            m[4 * r + 2] = madd(m[4 * r + 2], w0, a.z);
+            m[4 * r + 3] = madd(m[4 * r + 3], w0, a.w);
+            m[4 * r + 0] = madd(m[4 * r + 0], w1, b.x);
+            m[4 * r + 1] = madd(m[4 * r + 1], w1, b.y);
+            m[4 * r + 2] = madd(m[4 * r + 2], w1, b.z);
+            m[4 * r + 3] = madd(m[4 * r + 3], w1, b.w);
         }
     }
 #else
@@ -114,14 +120,14 @@ __device__ __forceinline__ void deform(const Planes<double>& P, const GridP& g, 
                 const double w0 = mul(wyz, sub(1.0, c.tx)), w1 = mul(wyz, c.tx);
                 // corner di = 0 then di = 1, entries in row order (the oracle's e loop per corner;
                 // each entry's sum runs over corners in the same (dk, dj, di) order)
-                m[4 * r + 0] = add(m[4 * r + 0], mul(w0, a.x));
-                m[4 * r + 1] = add(m[4 * r + 1], mul(w0, a.y));
-                m[4 * r + 2] = add(m[4 * r + 2], mul(w0, a.z));
-                m[4 * r + 3] = add(m[4 * r + 3], mul(w0, a.w));
-                m[4 * r + 0] = add(m[4 * r + 0], mul(w1, b.x));
-                m[4 * r + 1] = add(m[4 * r + 1], mul(w1, b.y));
-                m[4 * r + 2] = add(m[4 * r + 2], mul(w1, b.z));
-                m[4 * r + 3] = add(m[4 * r + 3], mul(w1, b.w));
+                m[4 * r + 0] = madd(m[4 * r + 0], w0, a.x);
+                m[4 * r + 1] = madd(m[4 * r + 1], w0, a.y);
+                m[4 * r + 2] = madd(m[4 * r + 2], w0, a.z);
+                m[4 * r + 3] = madd(m[4 * r + 3], w0, a.w);
+                m[4 * r + 0] = madd(m[4 * r + 0], w1, b.x);
+                m[4 * r + 1] = madd(m[4 * r + 1], w1, b.y);
+                m[4 * r + 2] = madd(m[4 * r + 2], w1, b.z);
+                m[4 * r + 3] = madd(m[4 * r + 3], w1, b.w);
             }
         }
     }
@@ -213,7 +219,7 @@ __device__ __forceinline__ void jacobian_vec(const GridP& g, const float* __rest
             double q[kVec];
             corner_weights<kVec>(W, vc[k8], nb, b0, q);
 #pragma unroll
-            for (int u = 0; u < kVec; ++u) wb[u] = add(wb[u], mul(w8[k8], q[u]));
+            for (int u = 0; u < kVec; ++u) wb[u] = madd(wb[u], w8[k8], q[u]);
         }
 #pragma unroll
         for (int u = 0; u < kVec; ++u) {
@@ -221,7 +227,7 @@ __device__ __forceinline__ void jacobian_vec(const GridP& g, const float* __rest
 #pragma unroll
             for (int r = 0; r < 3; ++r)
 #pragma unroll
-                for (int cc = 0; cc < 3; ++cc) J[3 * r + cc] = add(J[3 * r + cc], mul(wb[u], B[4 * r + cc]));
+                for (int cc = 0; cc < 3; ++cc) J[3 * r + cc] = madd(J[3 * r + cc], wb[u], B[4 * r + cc]);
         }
     }
     const double fx[2] = {sub(1.0, cl.tx), cl.tx}, fy[2] = {sub(1.0, cl.ty), cl.ty}, fz[2] = {sub(1.0, cl.tz), cl.tz};
@@ -241,9 +247,9 @@ __device__ __forceinline__ void jacobian_vec(const GridP& g, const float* __rest
 #pragma unroll
             for (int u = 0; u < kVec; ++u) {
                 const double v = q[u];
-                gg[u][0] = add(gg[u][0], mul(gx, v));
-                gg[u][1] = add(gg[u][1], mul(gy, v));
-                gg[u][2] = add(gg[u][2], mul(gz, v));
+                gg[u][0] = madd(gg[u][0], gx, v);
+                gg[u][1] = madd(gg[u][1], gy, v);
+                gg[u][2] = madd(gg[u][2], gz, v);
             }
         }
 #pragma unroll
@@ -256,7 +262,7 @@ __device__ __forceinline__ void jacobian_vec(const GridP& g, const float* __rest
 #pragma unroll
             for (int r = 0; r < 3; ++r)
 #pragma unroll
-                for (int cc = 0; cc < 3; ++cc) J[3 * r + cc] = add(J[3 * r + cc], mul(bx[r], gg[u][cc]));
+                for (int cc = 0; cc < 3; ++cc) J[3 * r + cc] = madd(J[3 * r + cc], bx[r], gg[u][cc]);
         }
     }
 }
@@ -330,10 +336,10 @@ __device__ __forceinline__ void jacobian_stash_vec(const GridP& g, const float* 
             corner_weights<kVec>(W, vc[k8], nb, b0, q);
 #pragma unroll
             for (int u = 0; u < kVec; ++u) {
-                wb[u] = add(wb[u], mul(w8[k8], q[u]));
-                gg[u][0] = add(gg[u][0], mul(gx, q[u]));
-                gg[u][1] = add(gg[u][1], mul(gy, q[u]));
-                gg[u][2] = add(gg[u][2], mul(gz, q[u]));
+                wb[u] = madd(wb[u], w8[k8], q[u]);
+                gg[u][0] = madd(gg[u][0], gx, q[u]);
+                gg[u][1] = madd(gg[u][1], gy, q[u]);
+                gg[u][2] = madd(gg[u][2], gz, q[u]);
             }
         }
 #pragma unroll
@@ -342,7 +348,7 @@ __device__ __forceinline__ void jacobian_stash_vec(const GridP& g, const float* 
 #pragma unroll
             for (int r = 0; r < 3; ++r)
 #pragma unroll
-                for (int cc = 0; cc < 3; ++cc) J[3 * r + cc] = add(J[3 * r + cc], mul(wb[u], B[4 * r + cc]));
+                for (int cc = 0; cc < 3; ++cc) J[3 * r + cc] = madd(J[3 * r + cc], wb[u], B[4 * r + cc]);
 #pragma unroll
             for (int cc = 0; cc < 3; ++cc) stash[(3 * (b0 + u) + cc) * ld] = gg[u][cc];
         }
@@ -355,9 +361,9 @@ __device__ __forceinline__ void jacobian_stash_vec(const GridP& g, const float* 
         for (int r = 0; r < 3; ++r) bx[r] = add(dot3(B[4 * r], B[4 * r + 1], B[4 * r + 2], x0, x1, x2), B[4 * r + 3]);
 #pragma unroll
         for (int r = 0; r < 3; ++r) {
-            J[3 * r + 0] = add(J[3 * r + 0], mul(bx[r], gg0));
-            J[3 * r + 1] = add(J[3 * r + 1], mul(bx[r], gg1));
-            J[3 * r + 2] = add(J[3 * r + 2], mul(bx[r], gg2));
+            J[3 * r + 0] = madd(J[3 * r + 0], bx[r], gg0);
+            J[3 * r + 1] = madd(J[3 * r + 1], bx[r], gg1);
+            J[3 * r + 2] = madd(J[3 * r + 2], bx[r], gg2);
         }
     }
 }
@@ -365,35 +371,33 @@ __device__ __forceinline__ void jacobian_stash_vec(const GridP& g, const float* 
 // initial_inverse_jacobian (correspondence.cpp:43-54): Eigen's determinant() (expansion along row 0)
 // against 1e-8, then Eigen's cofactor inverse with its own det (column-0 cofactors; adjugate · 1/det)
 __device__ __forceinline__ void inverse_or_identity(const double a[9], double Ji[9]) {
-    auto h = [&](int c0, int c1, int c2) {
-        return mul(a[c0], sub(mul(a[3 + c1], a[6 + c2]), mul(a[3 + c2], a[6 + c1])));
-    };
-    const double det = add(sub(h(0, 1, 2), h(1, 0, 2)), h(2, 0, 1));
+    auto X = [&](int c1, int c2) { return msub(a[3 + c1], a[6 + c2], a[3 + c2], a[6 + c1]); };
+    const double det = madd(madd(mul(a[0], X(1, 2)), -a[1], X(0, 2)), a[2], X(0, 1));  // oracle det3
     if (fabs(det) < 1e-8) {
 #pragma unroll
         for (int e = 0; e < 9; ++e) Ji[e] = (e % 4 == 0) ? 1.0 : 0.0;
         return;
     }
     double c[9];
-    c[0] = sub(mul(a[4], a[8]), mul(a[5], a[7]));
-    c[1] = sub(mul(a[2], a[7]), mul(a[1], a[8]));
-    c[2] = sub(mul(a[1], a[5]), mul(a[2], a[4]));
-    c[3] = sub(mul(a[5], a[6]), mul(a[3], a[8]));
-    c[4] = sub(mul(a[0], a[8]), mul(a[2], a[6]));
-    c[5] = sub(mul(a[2], a[3]), mul(a[0], a[5]));
-    c[6] = sub(mul(a[3], a[7]), mul(a[4], a[6]));
-    c[7] = sub(mul(a[1], a[6]), mul(a[0], a[7]));
-    c[8] = sub(mul(a[0], a[4]), mul(a[1], a[3]));
+    c[0] = msub(a[4], a[8], a[5], a[7]);
+    c[1] = msub(a[2], a[7], a[1], a[8]);
+    c[2] = msub(a[1], a[5], a[2], a[4]);
+    c[3] = msub(a[5], a[6], a[3], a[8]);
+    c[4] = msub(a[0], a[8], a[2], a[6]);
+    c[5] = msub(a[2], a[3], a[0], a[5]);
+    c[6] = msub(a[3], a[7], a[4], a[6]);
+    c[7] = msub(a[1], a[6], a[0], a[7]);
+    c[8] = msub(a[0], a[4], a[1], a[3]);
     // Eigen's inverse() takes its own determinant from the column-0 cofactors (InverseImpl.h
-    // compute_inverse<.., 3>: cofactors_col0 · col(0)), summed left to right
-    const double d2 = add(add(mul(c[0], a[0]), mul(c[1], a[3])), mul(c[2], a[6]));
+    // compute_inverse<.., 3>: cofactors_col0 · col(0))
+    const double d2 = madd(madd(mul(c[0], a[0]), c[1], a[3]), c[2], a[6]);
     const double inv = div(1.0, d2);
 #pragma unroll
     for (int e = 0; e < 9; ++e) Ji[e] = mul(c[e], inv);
 }
 
 __device__ __forceinline__ double norm3(double g0, double g1, double g2) {
-    return __dsqrt_rn(add(add(mul(g0, g0), mul(g1, g1)), mul(g2, g2)));
+    return __dsqrt_rn(dot3(g0, g1, g2, g0, g1, g2));
 }
 
 // Solve state of the replay (search_one's per-init body, correspondence.cpp:132-146)
@@ -461,7 +465,7 @@ __device__ __forceinline__ bool step(const Planes<double>& P, const GridP& g, do
 #pragma unroll
         for (int i = 0; i < 3; ++i)
 #pragma unroll
-            for (int c = 0; c < 3; ++c) s.Ji[3 * i + c] = add(s.Ji[3 * i + c], mul(r[i], w[c]));
+            for (int c = 0; c < 3; ++c) s.Ji[3 * i + c] = madd(s.Ji[3 * i + c], r[i], w[c]);
     }
     return false;
 }

@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(256) k_precompute(const float* __restrict__ w,
         for (int e = 0; e < 4; ++e) T[e] = fmaf(wi, Bi[e], T[e]);  // lbs_blend bone order (deformer.cpp:9-19)
         if (f64)
 #pragma unroll
-            for (int e = 0; e < 4; ++e) D[e] = __dadd_rn(D[e], __dmul_rn((double)wi, (double)Bi[e]));  // unfused, as lbs_blend
+            for (int e = 0; e < 4; ++e) D[e] = __fma_rn((double)wi, (double)Bi[e], D[e]);  // lbs_blend as the oracle contracts it
     }
     const bool has_left = (v % nx) != 0;
     if (tg) tg[3 * v + r] = make_float4(T[0], T[1], T[2], T[3]);

@@ -2,7 +2,7 @@
 
 The reference is Eigen3 (version unpinned) built with -march=native (proj/CMakeLists.txt:10-16); it
 cannot be built here. oracle/Makefile builds the same f64 restatement in four plausible operation
-orders (default "eigen", "invrow0", "pairsum", "fma"). This script runs each on the BASELINE
+orders (default "fma", "unfused", "invrow0", "pairsum", "gccfma"). This script runs each on the BASELINE
 configurations' scenes and reports, against the default: converged-mask flips, keep-mask flips,
 iteration-count changes and root moves (max |dx|, count beyond 1e-4) — the spread any
 implementation of the reference must be judged against. Usage:
@@ -50,11 +50,12 @@ def main():
             res[v] = oracle.batch_search(sc.weights, sc.dims, sc.bbox, sc.bones, sc.points, workers=args.workers,
                                          variant=v, **sc.search_options(mi))
             print(f"# {name} {v}: {time.time() - t:.1f} s", flush=True)
-        total = res["eigen"]["converged"].size
+        d0 = oracle.VARIANTS[0]
+        total = res[d0]["converged"].size
         print(f"{name}: {dims} x {n} points x {sc.n_bones} inits = {total} solves, max_iters {mi}")
         for v in oracle.VARIANTS[1:]:
-            c = compare(res[v], res["eigen"])
-            print(f"  {v:8s} vs eigen: mask flips {c['mask']} ({c['mask'] / total:.2e}), keep flips {c['keep']}, "
+            c = compare(res[v], res[d0])
+            print(f"  {v:8s} vs {d0}: mask flips {c['mask']} ({c['mask'] / total:.2e}), keep flips {c['keep']}, "
                   f"iteration changes {c['iters']}, max|dx| {c['dx_max']:.2e}, roots beyond 1e-4 {c['dx_gt_1e4']}, "
                   f"bit-equal roots {c['bitwise']:.4f}", flush=True)
         worst = {k: max(compare(res[a], res[b])[k] for a in oracle.VARIANTS for b in oracle.VARIANTS if a < b)
