@@ -30,6 +30,23 @@
 #include "fsk_ctx.h"
 #include "fsk_exact.cuh"
 
+// FSK_CHECKED builds (scripts: the GPU suite under FSK_LIB=build/variants/checked.so) trap on any
+// out-of-range index at the places a logic error would write out of bounds: the sort's scatter, the
+// escalation queue's two ends, its start states and the refill buffer, the CorrespondenceSet emission.
+// compute-sanitizer is not available on the GPU pool.
+#ifdef FSK_CHECKED
+#define FSK_CHECK(c)                                                                          \
+    do {                                                                                      \
+        if (!(c)) {                                                                           \
+            printf("FSK_CHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__,      \
+                   (int)blockIdx.x, (int)threadIdx.x, #c);                                     \
+            __trap();                                                                         \
+        }                                                                                     \
+    } while (0)
+#else
+#define FSK_CHECK(c) ((void)0)
+#endif
+
 namespace fsk {
 
 // ============================================================================ K1
@@ -253,6 +270,7 @@ __global__ void __launch_bounds__(256) k_sort_scatter(const float* __restrict__ 
     const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (p >= n) return;
     const int pos = atomicAdd(offs + keys[p], 1);
+    FSK_CHECK(pos >= 0 && pos < n);
     perm[pos] = (int)p;
     xs[pos] = make_float4(x[3 * p], x[3 * p + 1], x[3 * p + 2], 0.f);
 }
@@ -429,6 +447,8 @@ __global__ void __launch_bounds__(kSearchBlock, FSK_SEARCH_MINB)
             b = __shfl_sync(act, b, leader);
             const int bl = (int)(b >> 32), bs = (int)(b & 0xffffffffu);
             const int4 rec = make_int4((int)q, __float_as_int(xq.x), __float_as_int(xq.y), __float_as_int(xq.z));
+            FSK_CHECK(!(s.esc && s.capped) || bl + __popc(ml & lt) < esc_cap - (bs + __popc(ms)));
+            FSK_CHECK(!(s.esc && !s.capped) || esc_cap - 1 - (bs + __popc(ms & lt)) >= bl + __popc(ml));
             if (s.esc && s.capped) esc_q[bl + __popc(ml & lt)] = rec;
             else if (s.esc) esc_q[esc_cap - 1 - (bs + __popc(ms & lt))] = rec;
         }
@@ -522,7 +542,9 @@ __global__ void __launch_bounds__(128, FSK_ESC_START_MINB)
     double* stash = (kExact && stash_on) ? const_cast<double*>(bones64) + 12 * g.nb + threadIdx.x : nullptr;
     unsigned n_solves = 0;
     for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < cnt; idx += gridDim.x * blockDim.x) {
+        FSK_CHECK(idx < cnt && idx < st_cap && cnt <= esc_cap);
         const int4 rec = esc_q[idx < cnt_long ? idx : esc_cap - 1 - (idx - cnt_long)];
+        FSK_CHECK(rec.x >= 0 && rec.x < n * g.nb);
         double s[16];
         bool stop, conv;
         esc_start_one<kExact>(P, g, W, bones, bones64, n, o, rec, s, stop, conv, stash);
@@ -618,8 +640,10 @@ __global__ void __launch_bounds__(kEscBlock, kExact ? FSK_ESC_EXACT_MINB : FSK_E
                 dry = true;
             }
             if (got) {  // start of the solve (correspondence.cpp:135-137, :43-54)
+                FSK_CHECK(idx >= 0 && idx < cnt && cnt <= esc_cap);
                 const int4 rec = esc_q[idx < cnt_long ? idx : esc_cap - 1 - (idx - cnt_long)];
                 q = rec.x;
+                FSK_CHECK(q >= 0 && q < n * g.nb);
                 xq = make_float4(__int_as_float(rec.y), __int_as_float(rec.z), __int_as_float(rec.w), 0.f);
                 k = 0;
                 double s[16];
@@ -910,6 +934,7 @@ __global__ void __launch_bounds__(256) k_emit(int64_t n, int nb, SearchPlanes sp
         for (uint32_t m = sp.kmask[j]; m; m &= m - 1) {
             const int b = __ffs(m) - 1;
             const int64_t q = (int64_t)b * n + j;
+            FSK_CHECK(b < nb && o >= offs[perm[j]] && o < offs[perm[j]] + nb);
             if (o < cap) {
                 float4 xr = sp.xr[q];
                 xr.w = fabsf(xr.w);
