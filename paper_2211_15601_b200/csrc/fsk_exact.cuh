@@ -74,10 +74,24 @@ __device__ __forceinline__ XCell locate(const GridP& g, double x0, double x1, do
 
 __device__ __forceinline__ int vidx(const GridP& g, int i, int j, int k) { return (k * g.ny + j) * g.nx + i; }
 
+// Register cache of the first FSK_EXACT_CACHE_ROWS matrix rows of the 4 x-pair edges of one cell
+// (the float64 planes' values themselves, so results are unchanged): a Broyden step that stays in
+// the cell of the previous evaluation skips those loads. The refill kernel is L1-bound on its
+// 768-B gathers; its registers beyond the replay's own ~168 hold the cache.
+#ifndef FSK_EXACT_CACHE_ROWS
+#define FSK_EXACT_CACHE_ROWS 0
+#endif
+struct XCache {
+    int base = -1;  // vertex index of the cached cell's corner (i, j, k); -1: empty
+    V4<double> a[4][FSK_EXACT_CACHE_ROWS > 0 ? FSK_EXACT_CACHE_ROWS : 1], b[4][FSK_EXACT_CACHE_ROWS > 0 ? FSK_EXACT_CACHE_ROWS : 1];
+};
+
 // forward_deform(x, tgrid) (deformer.cpp:79-94, :107-113) from the float64 x-pair planes
 __device__ __forceinline__ void deform(const Planes<double>& P, const GridP& g, double x0, double x1, double x2,
-                                       double d[3]) {
+                                       double d[3], XCache* C = nullptr) {
     const XCell c = locate(g, x0, x1, x2, false);
+    const int cbase = vidx(g, c.i, c.j, c.k);
+    const bool hit = FSK_EXACT_CACHE_ROWS > 0 && C && C->base == cbase;
     double m[12];
 #pragma unroll
     for (int e = 0; e < 12; ++e) m[e] = 0.0;
@@ -116,7 +130,16 @@ __device__ __forceinline__ void deform(const Planes<double>& P, const GridP& g, 
 #pragma unroll
             for (int r = 0; r < 3; ++r) {
                 V4<double> a, b;
-                load_edge(P, v, r, a, b);
+                if (r < FSK_EXACT_CACHE_ROWS && hit) {
+                    a = C->a[2 * dk + dj][r < FSK_EXACT_CACHE_ROWS ? r : 0];
+                    b = C->b[2 * dk + dj][r < FSK_EXACT_CACHE_ROWS ? r : 0];
+                } else {
+                    load_edge(P, v, r, a, b);
+                    if (r < FSK_EXACT_CACHE_ROWS && C) {
+                        C->a[2 * dk + dj][r < FSK_EXACT_CACHE_ROWS ? r : 0] = a;
+                        C->b[2 * dk + dj][r < FSK_EXACT_CACHE_ROWS ? r : 0] = b;
+                    }
+                }
                 const double w0 = mul(wyz, sub(1.0, c.tx)), w1 = mul(wyz, c.tx);
                 // corner di = 0 then di = 1, entries in row order (the oracle's e loop per corner;
                 // each entry's sum runs over corners in the same (dk, dj, di) order)
@@ -132,6 +155,7 @@ __device__ __forceinline__ void deform(const Planes<double>& P, const GridP& g, 
         }
     }
 #endif
+    if (FSK_EXACT_CACHE_ROWS > 0 && C) C->base = cbase;
 #pragma unroll
     for (int r = 0; r < 3; ++r) d[r] = add(dot3(m[4 * r], m[4 * r + 1], m[4 * r + 2], x0, x1, x2), m[4 * r + 3]);
 }
@@ -434,7 +458,7 @@ __device__ __forceinline__ void start(const Planes<double>& P, const GridP& g, c
 // one pass of iterate's loop body after the divergence check (correspondence.cpp:106-122);
 // returns true iff converged
 __device__ __forceinline__ bool step(const Planes<double>& P, const GridP& g, double xp0, double xp1, double xp2,
-                                     double conv_eps, XState& s) {
+                                     double conv_eps, XState& s, XCache* C = nullptr) {
     const double* J = s.Ji;
     const double dx0 = -dot3(J[0], J[1], J[2], s.g0, s.g1, s.g2);
     const double dx1 = -dot3(J[3], J[4], J[5], s.g0, s.g1, s.g2);
@@ -443,7 +467,7 @@ __device__ __forceinline__ bool step(const Planes<double>& P, const GridP& g, do
     s.x1 = add(s.x1, dx1);
     s.x2 = add(s.x2, dx2);
     double d[3];
-    deform(P, g, s.x0, s.x1, s.x2, d);
+    deform(P, g, s.x0, s.x1, s.x2, d, C);
     const double n0 = sub(d[0], xp0), n1 = sub(d[1], xp1), n2 = sub(d[2], xp2);
     const double dg0 = sub(n0, s.g0), dg1 = sub(n1, s.g1), dg2 = sub(n2, s.g2);
     s.g0 = n0;

@@ -605,6 +605,7 @@ __global__ void __launch_bounds__(kEscBlock, kExact ? FSK_ESC_EXACT_MINB : FSK_E
 #pragma unroll
     for (int e = 0; e < 9; ++e) Ji[e] = 0;
     exact::XState xs{};
+    exact::XCache xcache;  // grid values of the last evaluated cell (valid for any solve)
     // Warp-local buffer of 32 queue slots (lane i holds slot base+i): one atomic per 32 solves.
     // Idle lanes are refilled in batches (>= kRefillIdle idle, or the whole warp), so the
     // divergent init path (x0, Jacobian stencil, inverse) runs for many lanes at once and the
@@ -687,7 +688,7 @@ __global__ void __launch_bounds__(kEscBlock, kExact ? FSK_ESC_EXACT_MINB : FSK_E
         if (active) {  // one Broyden iteration (:106-122)
             bool conv, div;
             if constexpr (kExact) {
-                conv = exact::step(P, g, xq.x, xq.y, xq.z, o.conv_eps, xs);
+                conv = exact::step(P, g, xq.x, xq.y, xq.z, o.conv_eps, xs, &xcache);
                 div = xs.err > o.div_eps;
             } else {
                 double den;
