@@ -86,9 +86,12 @@ class MultiGPUDeformer:
 
     def forward(self, weights, dims, bbox, bones, points_full, opts, src=0, gather=True):
         broadcast_inputs([weights, bones], src=src, group=self.group)
-        tg = self.D.precompute_transform_grid(weights, dims, bbox, bones)
+        tg64 = torch.empty((weights.shape[0], 12), dtype=torch.float64, device=weights.device)
+        tg = self.D.precompute_transform_grid(weights, dims, bbox, bones, out64=tg64)
+        # the weight grid goes along (J~0 and the float64 re-solves in the oracle's operation order)
         res, rng = sharded_forward(points_full,
-                                   lambda x: self.D.batch_search(tg, dims, bbox, bones, x, opts),
+                                   lambda x: self.D.batch_search(tg, dims, bbox, bones, x, opts, tgrid64=tg64,
+                                                                 weights=weights),
                                    gather=gather, group=self.group)
         return tg, res, rng
 

@@ -48,6 +48,14 @@ def _worker(rank, world, port, out_dir):
     v = torch.from_numpy((np.random.default_rng(9).normal(size=(n, 3)) / n).astype(np.float32)[a:b]).cuda()
     gT, gW = MultiGPUDeformer(D).backward(sc.dims, sc.bbox, B, dense, v, sel, deterministic=True)
     np.save(os.path.join(out_dir, f"gT{rank}.npy"), gT.cpu().numpy())
+    # the sharded forward through dist.py (broadcast pose inputs from rank 0, per-rank search with the
+    # GPU kernels, all-gather of the dense results): equal to the single-process search
+    wb = w.clone() if rank == 0 else torch.zeros_like(w)
+    Bb = B.clone() if rank == 0 else torch.zeros_like(B)
+    _, res, _ = MultiGPUDeformer(D).forward(wb, sc.dims, sc.bbox, Bb, torch.from_numpy(sc.points).cuda(),
+                                            SearchOptions(50, o["conv_eps"], o["div_eps"], o["dedup_dist"]))
+    if rank == 0:
+        np.savez(os.path.join(out_dir, "fwd.npz"), **{k: t.cpu().numpy() for k, t in res.items() if t is not None})
     dist.destroy_process_group()
 
 
@@ -64,7 +72,14 @@ def test_deterministic_backward_is_bitwise_across_rank_counts(deformer, tmp_path
     sel = torch.from_numpy(np.where(keep.any(1), np.argmax(keep, 1), -1).astype(np.int32)).cuda()
     v = torch.from_numpy((np.random.default_rng(9).normal(size=(n, 3)) / n).astype(np.float32)).cuda()
     ref = deformer.search_bwd(sc.dims, sc.bbox, sc.n_bones, dense, v, sel, deterministic=True).cpu().numpy()
+    tg64 = torch.empty((w.shape[0], 12), dtype=torch.float64, device="cuda")
+    tg = deformer.precompute_transform_grid(w, sc.dims, sc.bbox, B, out64=tg64)
+    full = deformer.batch_search(tg, sc.dims, sc.bbox, B, torch.from_numpy(sc.points).cuda(),
+                                 SearchOptions(50, o["conv_eps"], o["div_eps"], o["dedup_dist"]), tgrid64=tg64, weights=w)
     for world in (2, 3):
         mp.spawn(_worker, args=(world, _port(), str(tmp_path)), nprocs=world, join=True)
         for r in range(world):
             np.testing.assert_array_equal(np.load(tmp_path / f"gT{r}.npy").view(np.uint32), ref.view(np.uint32))
+        fwd = np.load(tmp_path / "fwd.npz")
+        for k in ("x_c", "converged", "keep", "iters", "n_roots"):
+            np.testing.assert_array_equal(fwd[k], full[k].cpu().numpy())
