@@ -446,6 +446,8 @@ def run_ours(args, rank, world, local_rank):
         e2e = e2e_ours(D, sc, opts, args, world=world, roots_hint=total_roots)
         if rank == 0:
             line["e2e"] = e2e
+            if world == 1 and args.poses == 1:
+                line["e2e"]["cpp_api"] = cpp_api_e2e(sc, args)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         workers = os.cpu_count() or 1
         rate, m, dt = cpu_rate(sc, args, args.cpu_seconds, workers)
@@ -617,6 +619,36 @@ def e2e_ours(D, sc, opts, args, steps=None, world=1, roots_hint=None):
             "single_frame_call": {"value": world * n * nb / dt1, "ms_per_step": 1e3 * dt1,
                                   "h2d_bytes_per_step": int(hw.numel() * 4 + hb.numel() * 4 + hx.numel() * 4),
                                   "api": "fsk_deform_host, one synchronous call per frame"}}
+
+
+def cpp_api_e2e(sc, args, frames=10):
+    """The same frame through the reference-facing C++ API (include/fskin): a C++ client
+    (tests/cpp/fskin_api_bench.cpp) times precompute_transform_grid + batch_search per frame — f64
+    queries in, the reference's std::vector<CorrespondenceSet> out, every copy and the host build of
+    the result sets inside the timed loop."""
+    import tempfile
+
+    from paper_2211_15601_b200 import build as B
+    d = tempfile.mkdtemp()
+    exe, inp = os.path.join(d, "fskin_api_bench"), os.path.join(d, "in.bin")
+    try:
+        subprocess.run(["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "tests", "cpp", "fskin_api_bench.cpp"), "-o", exe, B.LIB,
+                        f"-Wl,-rpath,{os.path.dirname(B.LIB)}"], check=True, capture_output=True)
+        with open(inp, "wb") as f:
+            np.array([*sc.dims, sc.n_bones, sc.points.shape[0]], np.int32).tofile(f)
+            sc.bbox.astype(np.float32).tofile(f)
+            np.array([args.max_iters], np.int32).tofile(f)
+            sc.weights.tofile(f)
+            sc.bones.tofile(f)
+            sc.points.tofile(f)
+        r = subprocess.run([exe, inp, str(frames)], capture_output=True, text=True, timeout=600)
+        out = json.loads(r.stdout.strip().splitlines()[-1])
+        return {"value": out["solves_per_s"], "unit": UNIT, "ms_per_step": out["ms_per_frame"], "frames": frames,
+                "api": "fskin::precompute_transform_grid + fskin::batch_search (include/fskin C++ API, host f64 "
+                       "queries in, std::vector<CorrespondenceSet> out), one frame per step"}
+    except Exception as e:  # the API client is an extra measurement; never fail the bench line on it
+        return {"unavailable": f"{type(e).__name__}: {e}"[:200]}
 
 
 def main():

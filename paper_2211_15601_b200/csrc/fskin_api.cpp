@@ -70,6 +70,41 @@ struct DevBuf {
     T* as() const { return static_cast<T*>(p); }
 };
 
+/// Per-thread device and pinned host staging of batch_search, grown on demand and reused across calls
+/// (no cudaMalloc / pageable copy per call).
+struct Workspace {
+    void* dev[4] = {};
+    size_t dcap[4] = {};
+    void* pin[4] = {};
+    size_t pcap[4] = {};
+    void* d(int i, size_t bytes) {
+        if (dcap[i] < bytes) {
+            if (dev[i]) cudaFree(dev[i]);
+            dev[i] = nullptr;
+            dcap[i] = 0;
+            cuda_ok(cudaMalloc(&dev[i], bytes), "cudaMalloc");
+            dcap[i] = bytes;
+        }
+        return dev[i];
+    }
+    void* h(int i, size_t bytes) {
+        if (pcap[i] < bytes) {
+            if (pin[i]) cudaFreeHost(pin[i]);
+            pin[i] = nullptr;
+            pcap[i] = 0;
+            cuda_ok(cudaMallocHost(&pin[i], bytes), "cudaMallocHost");
+            pcap[i] = bytes;
+        }
+        return pin[i];
+    }
+    ~Workspace() {
+        for (int i = 0; i < 4; ++i) {
+            if (dev[i]) cudaFree(dev[i]);
+            if (pin[i]) cudaFreeHost(pin[i]);
+        }
+    }
+};
+
 void h2d(void* dst, const void* src, size_t bytes) {
     if (bytes) cuda_ok(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice), "cudaMemcpy H2D");
 }
@@ -732,8 +767,8 @@ std::vector<InitState> init_states(const Vec3& x_prime, const SearchContext& c, 
 }
 
 namespace {
-std::vector<CorrespondenceSet> to_sets(std::span<const Vec3> queries, const std::vector<std::int64_t>& h_offs,
-                                       const std::vector<fsk_root>& roots) {
+std::vector<CorrespondenceSet> to_sets(std::span<const Vec3> queries, std::span<const std::int64_t> h_offs,
+                                       std::span<const fsk_root> roots) {
     std::vector<CorrespondenceSet> out(queries.size());
     for (size_t q = 0; q < queries.size(); ++q) {
         auto& set = out[q];
@@ -754,6 +789,46 @@ std::vector<CorrespondenceSet> to_sets(std::span<const Vec3> queries, const std:
 }
 }  // namespace
 
+// The voxel search through the per-thread workspace: queries converted into pinned staging, one H2D,
+// fsk_batch_search, D2H of offsets and kept roots into pinned staging, CorrespondenceSets built from it.
+std::vector<CorrespondenceSet> batch_search_voxel(std::span<const Vec3> queries, const SearchContext& c,
+                                                  const fsk_grid_desc& d, const fsk_search_opts& so, const float* dw) {
+    thread_local Workspace w;
+    const std::int64_t n = static_cast<std::int64_t>(queries.size());
+    const int nb = static_cast<int>(c.bones.size());
+    const std::vector<float> b = bones_f32(c.bones);
+    float* hp = static_cast<float*>(w.h(0, n * 3 * sizeof(float)));
+    for (std::int64_t i = 0; i < n; ++i)
+        for (int a = 0; a < 3; ++a) hp[3 * i + a] = static_cast<float>(queries[i][a]);
+    float* dp = static_cast<float*>(w.d(0, n * 3 * sizeof(float)));
+    float* db = static_cast<float*>(w.d(1, b.size() * sizeof(float)));
+    std::int64_t* doffs = static_cast<std::int64_t*>(w.d(2, (n + 1) * sizeof(std::int64_t)));
+    std::int64_t* hoffs = static_cast<std::int64_t*>(w.h(1, (n + 1) * sizeof(std::int64_t)));
+    cuda_ok(cudaMemcpyAsync(dp, hp, n * 3 * sizeof(float), cudaMemcpyHostToDevice, 0), "H2D points");
+    h2d(db, b.data(), b.size() * sizeof(float));
+    std::int64_t cap = std::min<std::int64_t>(n * nb, 4 * n);  // count-then-allocate: ~1.05 roots are kept per query
+    std::vector<std::int64_t> h_offs;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        fsk_root* dr = static_cast<fsk_root*>(w.d(3, cap * sizeof(fsk_root)));
+        check(fsk_batch_search(ctx(), c.tgrid->device_data(), c.tgrid->device_data64(), dw, &d, db, nb, dp, n, &so,
+                               doffs, dr, cap, nullptr));
+        cuda_ok(cudaMemcpyAsync(hoffs, doffs, (n + 1) * sizeof(std::int64_t), cudaMemcpyDeviceToHost, 0), "D2H offsets");
+        cuda_ok(cudaStreamSynchronize(0), "cudaStreamSynchronize");
+        const std::int64_t total = hoffs[n];
+        if (total > cap) {  // more kept roots than records: search again into exactly that many
+            cap = total;
+            continue;
+        }
+        fsk_root* hr = static_cast<fsk_root*>(w.h(2, std::max<std::int64_t>(1, total) * sizeof(fsk_root)));
+        if (total > 0) {
+            cuda_ok(cudaMemcpyAsync(hr, dr, total * sizeof(fsk_root), cudaMemcpyDeviceToHost, 0), "D2H roots");
+            cuda_ok(cudaStreamSynchronize(0), "cudaStreamSynchronize");
+        }
+        return to_sets(queries, std::span<const std::int64_t>(hoffs, n + 1), std::span<const fsk_root>(hr, total));
+    }
+    throw std::runtime_error("fsk: root count changed between identical searches");
+}
+
 // batch_search (correspondence.cpp:178-192) on the GPU. Voxel variant: K1's grids (the TransformGrid's
 // device mirrors), SearchContext::grid's weights for J~0 and the float64 replay, K2 + dedup + compaction;
 // root records count-then-allocate (4 per query first, the exact count on a rerun). Mlp variant: the
@@ -763,17 +838,20 @@ std::vector<CorrespondenceSet> batch_search(std::span<const Vec3> queries, const
     check_context(c, opts.variant);
     opts.validate();
     const std::int64_t n = static_cast<std::int64_t>(queries.size());
-    if (n == 0) return to_sets(queries, {0}, {});
+    if (n == 0) {
+        const std::int64_t zero = 0;
+        return to_sets(queries, {&zero, 1}, {});
+    }
     const int nb = static_cast<int>(c.bones.size());
-    const std::vector<float> b = bones_f32(c.bones);
-    const std::vector<float> p = points_f32(queries);
-    DevBuf db(b.size() * 4), dp(p.size() * 4), offs((n + 1) * 8);
-    h2d(db.p, b.data(), b.size() * 4);
-    h2d(dp.p, p.data(), p.size() * 4);
     const fsk_search_opts so = c_opts(opts);
-    std::vector<std::int64_t> h_offs(n + 1);
-    std::vector<fsk_root> roots;
     if (opts.variant == SearchVariant::Mlp) {
+        const std::vector<float> b = bones_f32(c.bones);
+        const std::vector<float> p = points_f32(queries);
+        DevBuf db(b.size() * 4), dp(p.size() * 4), offs((n + 1) * 8);
+        h2d(db.p, b.data(), b.size() * 4);
+        h2d(dp.p, p.data(), p.size() * 4);
+        std::vector<std::int64_t> h_offs(n + 1);
+        std::vector<fsk_root> roots;
         const DevMlp net(*c.mlp);
         DevBuf xc(n * nb * 12), ji(n * nb * 36), rs(n * nb * 4), it(n * nb * 4), cv(n * nb), kp(n * nb), nr(n * 4);
         fsk_search_out o{xc.as<float>(), ji.as<float>(), rs.as<float>(), it.as<std::int32_t>(), cv.as<std::uint8_t>(),
@@ -794,22 +872,7 @@ std::vector<CorrespondenceSet> batch_search(std::span<const Vec3> queries, const
     // SearchContext::grid's weights go to the search like the reference's (J~0 from the weight grid,
     // correspondence.cpp:43-54): the escalated solves then replay the reference's operation order
     const float* dw = device_weights(*c.grid);
-    std::int64_t cap = std::min<std::int64_t>(n * nb, 4 * n);
-    for (int attempt = 0; attempt < 2; ++attempt) {
-        DevBuf dr(cap * sizeof(fsk_root));
-        check(fsk_batch_search(ctx(), c.tgrid->device_data(), c.tgrid->device_data64(), dw, &d, db.as<float>(), nb,
-                               dp.as<float>(), n, &so, offs.as<std::int64_t>(), dr.as<fsk_root>(), cap, nullptr));
-        d2h(h_offs.data(), offs.p, h_offs.size() * 8);
-        const std::int64_t total = h_offs[n];
-        if (total > cap) {  // more kept roots than records: search again into exactly that many
-            cap = total;
-            continue;
-        }
-        roots.resize(static_cast<size_t>(total));
-        if (total > 0) d2h(roots.data(), dr.p, roots.size() * sizeof(fsk_root));
-        break;
-    }
-    return to_sets(queries, h_offs, roots);
+    return batch_search_voxel(queries, c, d, so, dw);
 }
 
 CorrespondenceSet broyden_search(const Vec3& x_prime, const SearchContext& c, const SearchOptions& opts) {
