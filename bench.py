@@ -36,10 +36,11 @@ UNIT = "solves/s"
 # terminating (converged) iteration that skips the rank-one update.
 FLOPS_INIT, FLOPS_ITER, FLOPS_FINAL_SAVING = 674, 332, 66
 GATHER_BYTES = 384  # 8 corners x 48 B of transform grid per d(x) evaluation
-# dram__bytes_read.sum + dram__bytes_write.sum of one k_search_fast launch (C2), from the
-# ncu --set full capture profiles/r01_final_search.ncu-rep (6.8 MB read + 205.0 MB written:
-# the bone-major search planes; the gather itself is L1/L2-resident)
-NCU_TRAFFIC_K2 = 7.091456e6 + 180.12288e6  # dram read + write per k_search_fast launch, profiles/r01_final_search.ncu-rep
+# dram__bytes_read.sum + dram__bytes_write.sum of one k_search_fast launch (C2) from the ncu --set full
+# capture profiles/r02_search.ncu-rep: 14.3 MB read + 176.8 MB written (the bone-major search planes;
+# the gather itself is L1/L2-resident)
+NCU_TRAFFIC_K2 = 14.345984e6 + 176.782336e6
+NCU_TRAFFIC_SRC = "ncu --set full, profiles/r02_search.ncu-rep (C2 only)"
 
 
 def parse():
@@ -398,7 +399,7 @@ def run_ours(args, rank, world, local_rank):
         "roofline": {"bound": "fp32", "kernel": "k_search_fast", "achieved": achieved, "peak": peak_fp32,
                      "unit": "TFLOP/s", "frac": achieved / peak_fp32,
                      "traffic": NCU_TRAFFIC_K2 if (args.grid == "32,32,32" and args.points == 200_000) else None,
-                     "traffic_source": "ncu --set full, profiles/r01_final_search.ncu-rep (C2 only)",
+                     "traffic_source": NCU_TRAFFIC_SRC,
                      "peak_source": "measured live: FFMA-chain kernel over all SMs (fsk_measure_fp32_peak); "
                                     "MEASURED_PEAKS.json has no FP32 figure",
                      "algorithmic_flops_per_launch": flops, "avg_launch_ms": k2_avg,

@@ -272,3 +272,76 @@ def batch_search_mlp(theta, widths, bones, x_prime, max_iters, conv_eps, div_eps
                                           _p(out["jinv"]), _p(out["resid"]), _p(out["iters"], _i32),
                                           _p(out["converged"], _u8), _p(out["keep"], _u8)))
     return out
+
+
+# ---------------------------------------------------------------- the reference's own sources (oracle/_ref)
+_REF = os.path.join(_HERE, "_ref", "libfskin_ref.so")
+_ref = None
+
+
+def ref_available() -> bool:
+    """oracle/_ref/libfskin_ref.so: the reference's proj/src/{geometry,skinning,deformer,correspondence}.cpp
+    compiled unmodified against oracle/eigen_shim (oracle/ref_build.sh; built here, travels to the box)."""
+    deps = [os.path.join(_HERE, f) for f in ("ref_capi.cpp", "ref_stubs.cpp", "ref_build.sh",
+                                              os.path.join("eigen_shim", "Eigen", "Dense"))]
+    stale = not os.path.exists(_REF) or os.path.getmtime(_REF) < max(os.path.getmtime(d) for d in deps)
+    if stale and os.path.isdir("/root/reference/proj/src"):
+        subprocess.run(["sh", os.path.join(_HERE, "ref_build.sh")], check=True, capture_output=True)
+    return os.path.exists(_REF)
+
+
+def ref_lib():
+    global _ref
+    if _ref is None:
+        if not ref_available():
+            raise OracleError("oracle/_ref/libfskin_ref.so not built (needs /root/reference at build time)")
+        L = ctypes.CDLL(_REF)
+        L.ref_last_error.restype = ctypes.c_char_p
+        L.ref_precompute_tgrid.argtypes = [_d, _int, _int, _int, _int, _d, _d, _int, _d]
+        L.ref_batch_search.argtypes = [_d, _int, _int, _int, _int, _d, _d, _d, _i64, _int, ctypes.c_double,
+                                       ctypes.c_double, ctypes.c_double, _int, ctypes.POINTER(ctypes.c_int64), _d, _d,
+                                       _d, _i32, _i32, _i64, ctypes.POINTER(ctypes.c_int64)]
+        L.ref_init_states.argtypes = [_d, _int, _int, _int, _int, _d, _d, _d, _i64, _d, _d]
+        _ref = L
+    return _ref
+
+
+def _ref_check(rc):
+    if rc != 0:
+        msg = ref_lib().ref_last_error().decode()
+        raise (OracleInvalidArgument if rc == 1 else OracleError)(msg)
+
+
+def ref_precompute_transform_grid(weights, dims, bbox, bones, workers=1):
+    w, bb, B = _f64(weights), _f64(bbox), _f64(bones).reshape(-1, 12)
+    out = np.zeros((dims[0] * dims[1] * dims[2], 12))
+    _ref_check(ref_lib().ref_precompute_tgrid(_p(w), *dims, w.shape[1], _p(bb), _p(B), workers, _p(out)))
+    return out
+
+
+def ref_batch_search(weights, dims, bbox, bones, x_prime, max_iters, conv_eps, div_eps, dedup_dist, workers=1):
+    """The reference's precompute_transform_grid + batch_search (its own code): CorrespondenceSets as
+    dict(offsets [n+1], x [M,3], resid [M], jinv [M,3,3], bone [M], iters [M])."""
+    w, bb, B, x = _f64(weights), _f64(bbox), _f64(bones).reshape(-1, 12), _f64(x_prime).reshape(-1, 3)
+    n, nb = x.shape[0], B.shape[0]
+    cap = max(1, n * nb)
+    offs = np.zeros(n + 1, np.int64)
+    out = dict(x=np.zeros((cap, 3)), resid=np.zeros(cap), jinv=np.zeros((cap, 3, 3)), bone=np.zeros(cap, np.int32),
+               iters=np.zeros(cap, np.int32))
+    total = ctypes.c_int64()
+    _ref_check(ref_lib().ref_batch_search(_p(w), *dims, w.shape[1], _p(bb), _p(B), _p(x), n, int(max_iters), conv_eps,
+                                          div_eps, dedup_dist, workers,
+                                          offs.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), _p(out["x"]),
+                                          _p(out["resid"]), _p(out["jinv"]), _p(out["bone"], _i32),
+                                          _p(out["iters"], _i32), cap, ctypes.byref(total)))
+    m = total.value
+    return dict(offsets=offs, **{k: v[:m] for k, v in out.items()})
+
+
+def ref_init_states(weights, dims, bbox, bones, x_prime):
+    w, bb, B, x = _f64(weights), _f64(bbox), _f64(bones).reshape(-1, 12), _f64(x_prime).reshape(-1, 3)
+    n, nb = x.shape[0], B.shape[0]
+    x0, j0 = np.zeros((n, nb, 3)), np.zeros((n, nb, 3, 3))
+    _ref_check(ref_lib().ref_init_states(_p(w), *dims, nb, _p(bb), _p(B), _p(x), n, _p(x0), _p(j0)))
+    return x0, j0
+
