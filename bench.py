@@ -159,15 +159,31 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------ CPU side
-def cpu_rate(sc, args, seconds, workers):
-    """Reference CPU path (the oracle's f64 restatement of batch_search, all host threads)
-    on a bounded sample of the same workload → (solves/s, points sampled, wall s)."""
+def cpu_impl():
+    """The CPU implementation of the path timed beside the GPU: the reference's own sources (oracle/_ref:
+    proj/src/{geometry,skinning,deformer,correspondence}.cpp compiled unmodified against the restated Eigen
+    subset, oracle/ref_build.sh) when built, else the oracle's f64 restatement. → (kind, step fn, note)."""
     import oracle
+    if oracle.ref_available():
+        def step(sc, pts, opts, workers):  # precompute_transform_grid + batch_search, the reference's code
+            oracle.ref_batch_search(sc.weights, sc.dims, sc.bbox, sc.bones, pts, workers=workers, **opts)
+        return "reference", step, ("the reference's own precompute_transform_grid + batch_search (proj/src, "
+                                   "oracle/_ref: Eigen3 restated by oracle/eigen_shim), parallel_for over all host threads")
+
+    def step(sc, pts, opts, workers):
+        tg = oracle.precompute_transform_grid(sc.weights, sc.dims, sc.bbox, sc.bones, workers)
+        oracle.batch_search(sc.weights, sc.dims, sc.bbox, sc.bones, pts, workers=workers, tgrid=tg, **opts)
+    return "port", step, "oracle/fskin_oracle.cpp: f64 restatement of precompute + batch_search, all host threads"
+
+
+def cpu_rate(sc, args, seconds, workers):
+    """The reference's CPU path on a bounded sample of the same workload, all host threads →
+    (solves/s, points sampled, wall s, kind, note)."""
+    kind, step, note = cpu_impl()
     opts = sc.search_options(args.max_iters)
-    tg = oracle.precompute_transform_grid(sc.weights, sc.dims, sc.bbox, sc.bones, workers)
     m = min(2000, sc.points.shape[0])
     t0 = time.perf_counter()
-    oracle.batch_search(sc.weights, sc.dims, sc.bbox, sc.bones, sc.points[:m], workers=workers, tgrid=tg, **opts)
+    step(sc, sc.points[:m], opts, workers)
     dt = time.perf_counter() - t0
     m2 = int(min(sc.points.shape[0], max(m, m * seconds / max(dt, 1e-6))))
     # repeat the (precompute + search) pass until `seconds` of CPU work are timed, so a workload the
@@ -175,29 +191,27 @@ def cpu_rate(sc, args, seconds, workers):
     reps, t_all = 0, 0.0
     while reps == 0 or t_all < seconds:
         t0 = time.perf_counter()
-        tgt = oracle.precompute_transform_grid(sc.weights, sc.dims, sc.bbox, sc.bones, workers)  # per-pose precompute
-        oracle.batch_search(sc.weights, sc.dims, sc.bbox, sc.bones, sc.points[:m2], workers=workers, tgrid=tgt, **opts)
+        step(sc, sc.points[:m2], opts, workers)
         t_all += time.perf_counter() - t0
         reps += 1
-    return reps * m2 * sc.n_bones / t_all, m2, t_all
+    return reps * m2 * sc.n_bones / t_all, m2, t_all, kind, note
 
 
 def run_reference(args, rank, world):
-    """``--impl reference``: the reference's CPU implementation of the path (the oracle port —
-    the reference itself cannot be built here) on this box's host cores."""
+    """``--impl reference``: the reference's CPU implementation of the path on this box's host cores —
+    its own sources (oracle/_ref) when built, else the oracle port."""
     if rank != 0:
         return
     sc = scene_for_rank(args, 0)
     workers = os.cpu_count() or 1
-    rate, m, dt = cpu_rate(sc, args, 2.0, workers)  # calibrate one step to ~2 s
-    import oracle
+    rate, m, dt, kind, note = cpu_rate(sc, args, 2.0, workers)  # calibrate one step to ~2 s
+    _, step, _ = cpu_impl()
     opts = sc.search_options(args.max_iters)
     m = max(1, min(sc.points.shape[0], int(rate * 2.0 / sc.n_bones)))
     times = []
     for it in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        tg = oracle.precompute_transform_grid(sc.weights, sc.dims, sc.bbox, sc.bones, workers)
-        oracle.batch_search(sc.weights, sc.dims, sc.bbox, sc.bones, sc.points[:m], workers=workers, tgrid=tg, **opts)
+        step(sc, sc.points[:m], opts, workers)
         if it >= args.warmup:
             times.append(time.perf_counter() - t0)
     t = float(np.sum(times))
@@ -209,13 +223,10 @@ def run_reference(args, rank, world):
             "data": "synthetic SMPL-like skeleton, analytic capsule weights, uniform posed points",
             "config": {**config_of(args, args.points, sc.n_bones, sc.dims, world),
                        "l2": "n/a (host CPU path)", "parallelism": f"{workers} host threads (parallel_for)"},
-            "pipeline": "oracle/fskin_oracle.cpp: f64 restatement of precompute_transform_grid + batch_search "
-                        "(search_one per query, dedup_roots), std::thread over all host cores",
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port", "sample": sample,
+            "pipeline": note,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": kind, "sample": sample,
                              "cpu_model": cpu_model()},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "note": "oracle/fskin_oracle.cpp: f64 restatement of the reference batch_search "
-                    "(reference needs Eigen3, absent; see DESIGN.md)"}
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
@@ -451,10 +462,10 @@ def run_ours(args, rank, world, local_rank):
                 line["e2e"]["cpp_api"] = cpp_api_e2e(sc, args)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         workers = os.cpu_count() or 1
-        rate, m, dt = cpu_rate(sc, args, args.cpu_seconds, workers)
-        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": workers, "kind": "port", "cpu_model": cpu_model(),
-                                "sample": f"{m} of {n} points x {nb} inits (precompute + search + dedup), repeated over {dt:.1f} s, "
-                                          "f64 oracle restatement of batch_search, std::thread over all host cores"}
+        rate, m, dt, kind, note = cpu_rate(sc, args, args.cpu_seconds, workers)
+        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": workers, "kind": kind, "cpu_model": cpu_model(),
+                                "sample": f"{m} of {n} points x {nb} inits (precompute + search + dedup), repeated over "
+                                          f"{dt:.1f} s; {note}"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     D.close()

@@ -324,18 +324,22 @@ def ref_batch_search(weights, dims, bbox, bones, x_prime, max_iters, conv_eps, d
     dict(offsets [n+1], x [M,3], resid [M], jinv [M,3,3], bone [M], iters [M])."""
     w, bb, B, x = _f64(weights), _f64(bbox), _f64(bones).reshape(-1, 12), _f64(x_prime).reshape(-1, 3)
     n, nb = x.shape[0], B.shape[0]
-    cap = max(1, n * nb)
-    offs = np.zeros(n + 1, np.int64)
-    out = dict(x=np.zeros((cap, 3)), resid=np.zeros(cap), jinv=np.zeros((cap, 3, 3)), bone=np.zeros(cap, np.int32),
-               iters=np.zeros(cap, np.int32))
-    total = ctypes.c_int64()
-    _ref_check(ref_lib().ref_batch_search(_p(w), *dims, w.shape[1], _p(bb), _p(B), _p(x), n, int(max_iters), conv_eps,
-                                          div_eps, dedup_dist, workers,
-                                          offs.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), _p(out["x"]),
-                                          _p(out["resid"]), _p(out["jinv"]), _p(out["bone"], _i32),
-                                          _p(out["iters"], _i32), cap, ctypes.byref(total)))
-    m = total.value
-    return dict(offsets=offs, **{k: v[:m] for k, v in out.items()})
+    cap = max(1, min(n * nb, 4 * n + 1024))  # ~1.05 roots are kept per query; rerun with the exact count if not
+    while True:
+        offs = np.zeros(n + 1, np.int64)
+        out = dict(x=np.empty((cap, 3)), resid=np.empty(cap), jinv=np.empty((cap, 3, 3)), bone=np.empty(cap, np.int32),
+                   iters=np.empty(cap, np.int32))
+        total = ctypes.c_int64()
+        rc = ref_lib().ref_batch_search(_p(w), *dims, w.shape[1], _p(bb), _p(B), _p(x), n, int(max_iters), conv_eps,
+                                        div_eps, dedup_dist, workers, offs.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                        _p(out["x"]), _p(out["resid"]), _p(out["jinv"]), _p(out["bone"], _i32),
+                                        _p(out["iters"], _i32), cap, ctypes.byref(total))
+        if rc == 1 and total.value > cap:
+            cap = total.value
+            continue
+        _ref_check(rc)
+        m = total.value
+        return dict(offsets=offs, **{k: v[:m] for k, v in out.items()})
 
 
 def ref_init_states(weights, dims, bbox, bones, x_prime):

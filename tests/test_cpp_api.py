@@ -84,6 +84,13 @@ def test_cpp_api_batch_search_matches_oracle(tmp_path, max_iters, seed, points):
     assert per_solve >= 0.9999
     assert same_set / n >= 0.9999
     assert maxdx <= 1e-4
+    if oracle.ref_available():  # and against the reference's own sources (oracle/_ref, tests/test_oracle_ref.py)
+        rr = oracle.ref_batch_search(sc.weights, sc.dims, sc.bbox, sc.bones, sc.points, workers=os.cpu_count() or 8,
+                                     **sc.search_options(max_iters))
+        same_ref = sum([b_ for b_, _, _ in s_] == list(rr["bone"][rr["offsets"][p]:rr["offsets"][p + 1]])
+                       for p, s_ in enumerate(sets))
+        print(f"C++ API vs the reference's own code: identical root sets {same_ref}/{n}")
+        assert same_ref / n >= 0.9999
     # init_states (correspondence.cpp:58-70) through the drop-in: float64, the reference's operation
     # order (weight-grid Jacobian) -> the oracle's values bit for bit
     a = np.fromfile(ist, np.float64)
