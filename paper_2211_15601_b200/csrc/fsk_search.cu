@@ -116,6 +116,78 @@ __global__ void __launch_bounds__(256) k_precompute(const float* __restrict__ w,
         for (int e = 0; e < 4; ++e) tg64[12 * v + 4 * r + e] = D[e];
 }
 
+// K1, one thread per vertex (FSK_K1_V1 keeps the thread-per-(vertex, row) kernel above): the vertex's
+// n_b weights in 16-B loads (a warp reads 32 consecutive weight rows, one contiguous span), all 12
+// entries in float32 and float64 accumulated in bone order exactly as k_precompute (same bits), then
+// per matrix row one 16-B (float32) / 32-B (float64) store to record v and one to record v-1 of the
+// x-pair planes — a warp's stores to a row plane cover one contiguous span. Bones staged in shared
+// memory (float32 and float64 copies).
+__global__ void __launch_bounds__(128) k_precompute_v(const float* __restrict__ w, const float* __restrict__ bones,
+                                                     int nb, int nx, int64_t V, float4* __restrict__ tg,
+                                                     float* __restrict__ p32, double* __restrict__ p64,
+                                                     double* __restrict__ tg64) {
+    extern __shared__ float sB[];
+    for (int e = threadIdx.x; e < nb * 12; e += blockDim.x) sB[e] = bones[e];
+    __syncthreads();
+    const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (v >= V) return;
+    const float* wv = w + v * nb;
+    float T[12];
+    double D[12];
+#pragma unroll
+    for (int e = 0; e < 12; ++e) {
+        T[e] = 0.f;
+        D[e] = 0.0;
+    }
+    const bool f64 = p64 || tg64;
+    auto bone = [&](int i, float wi) {
+        const float* Bi = sB + 12 * i;
+#pragma unroll
+        for (int e = 0; e < 12; ++e) T[e] = fmaf(wi, Bi[e], T[e]);  // lbs_blend bone order (deformer.cpp:9-19)
+        if (f64)
+#pragma unroll
+            for (int e = 0; e < 12; ++e) D[e] = __fma_rn((double)wi, (double)Bi[e], D[e]);
+    };
+    if ((nb & 3) == 0) {
+        for (int i = 0; i < nb; i += 4) {
+            const float4 q = __ldg(reinterpret_cast<const float4*>(wv + i));
+            bone(i, q.x);
+            bone(i + 1, q.y);
+            bone(i + 2, q.z);
+            bone(i + 3, q.w);
+        }
+    } else {
+        for (int i = 0; i < nb; ++i) bone(i, __ldg(wv + i));
+    }
+    const bool has_left = (v % nx) != 0;
+    if (tg)
+#pragma unroll
+        for (int r = 0; r < 3; ++r) tg[3 * v + r] = make_float4(T[4 * r], T[4 * r + 1], T[4 * r + 2], T[4 * r + 3]);
+    const int64_t stride = 8 * V;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        if (p32) {
+            float4* lo = reinterpret_cast<float4*>(p32 + r * stride + 8 * v);
+            const float4 t4 = make_float4(T[4 * r], T[4 * r + 1], T[4 * r + 2], T[4 * r + 3]);
+            lo[0] = t4;
+            if (has_left) lo[-1] = t4;
+        }
+        if (p64) {
+            double2* lo = reinterpret_cast<double2*>(p64 + r * stride + 8 * v);
+            const double2 a = make_double2(D[4 * r], D[4 * r + 1]), b = make_double2(D[4 * r + 2], D[4 * r + 3]);
+            lo[0] = a;
+            lo[1] = b;
+            if (has_left) {
+                lo[-2] = a;
+                lo[-1] = b;
+            }
+        }
+        if (tg64)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) tg64[12 * v + 4 * r + e] = D[4 * r + e];
+    }
+}
+
 // Relayout of a caller-provided [V][12] grid (float32, or float64 when tg64 != null) into
 // the gather planes of both precisions.
 __global__ void __launch_bounds__(256) k_relayout(const float* __restrict__ tg, const double* __restrict__ tg64, int nx,
@@ -1111,9 +1183,15 @@ GridPlanes run_precompute(fsk_ctx* ctx, const float* w, const GridP& g, const fl
                           bool planes, bool f64, cudaStream_t st) {
     const int64_t V = vertex_count(g);
     GridPlanes P = planes_scratch(ctx, g);
+#ifdef FSK_K1_V1
     FSK_LAUNCH(ctx, st, k_precompute, blocks_for(3 * V, 256), 256, g.nb * 12 * sizeof(float), w, bones, g.nb, g.nx, V,
                reinterpret_cast<float4*>(tg), planes ? (float*)P.p32.p : nullptr,
                planes && f64 ? (double*)P.p64.p : nullptr, tg64);
+#else
+    FSK_LAUNCH(ctx, st, k_precompute_v, blocks_for(V, 128), 128, g.nb * 12 * sizeof(float), w, bones, g.nb, g.nx, V,
+               reinterpret_cast<float4*>(tg), planes ? (float*)P.p32.p : nullptr,
+               planes && f64 ? (double*)P.p64.p : nullptr, tg64);
+#endif
     return P;
 }
 

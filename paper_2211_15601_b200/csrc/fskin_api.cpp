@@ -12,6 +12,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <map>
+#include <thread>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -55,14 +57,57 @@ fsk_ctx* ctx() {
     return t.ctx;
 }
 
+/// Device buffers of the C++ API come from a small process-wide pool (per device and size): a frame's
+/// temporaries and TransformGrid mirrors reuse the previous frame's allocations instead of a
+/// cudaMalloc/cudaFree pair (cudaFree synchronizes the device).
+struct DevPool {
+    std::mutex mu;
+    struct Key {
+        int dev;
+        size_t bytes;
+        bool operator<(const Key& o) const { return dev != o.dev ? dev < o.dev : bytes < o.bytes; }
+    };
+    std::map<Key, std::vector<void*>> free;
+    void* get(size_t bytes) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            auto it = free.find(Key{dev, bytes});
+            if (it != free.end() && !it->second.empty()) {
+                void* p = it->second.back();
+                it->second.pop_back();
+                return p;
+            }
+        }
+        void* p = nullptr;
+        cuda_ok(cudaMalloc(&p, bytes), "cudaMalloc");
+        return p;
+    }
+    void put(void* p, size_t bytes) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        std::lock_guard<std::mutex> lk(mu);
+        auto& v = free[Key{dev, bytes}];
+        if (v.size() < 8) v.push_back(p);
+        else cudaFree(p);
+    }
+};
+DevPool& dev_pool() {
+    static DevPool* pool = new DevPool;  // leaked on purpose: outlives thread-local contexts at exit
+    return *pool;
+}
+
 struct DevBuf {
     void* p = nullptr;
-    explicit DevBuf(size_t bytes) {
+    size_t bytes = 0;
+    explicit DevBuf(size_t n) {
         ctx();  // selects the device
-        cuda_ok(cudaMalloc(&p, bytes ? bytes : 16), "cudaMalloc");
+        bytes = n ? n : 16;
+        p = dev_pool().get(bytes);
     }
     ~DevBuf() {
-        if (p) cudaFree(p);
+        if (p) dev_pool().put(p, bytes);
     }
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
@@ -623,7 +668,24 @@ TransformGrid precompute_transform_grid(const SkinningVoxelGrid& grid, std::span
     const fsk_grid_desc d = desc_of(grid.dims(), grid.bbox(), nb);
     check(fsk_precompute_tgrid(ctx(), dw, &d, db.as<float>(), nb, static_cast<DevBuf*>(tg.dev_.get())->as<float>(),
                                static_cast<DevBuf*>(tg.dev64_.get())->as<double>(), nullptr));
-    d2h(tg.data_.data(), static_cast<DevBuf*>(tg.dev64_.get())->p, tg.data_.size() * sizeof(double));
+    // the float64 host copy through pinned staging (a pageable D2H of V·96 B is several times slower)
+    thread_local struct Pinned {
+        void* p = nullptr;
+        size_t cap = 0;
+        ~Pinned() {
+            if (p) cudaFreeHost(p);
+        }
+    } stage;
+    const size_t bytes = tg.data_.size() * sizeof(double);
+    if (stage.cap < bytes) {
+        if (stage.p) cudaFreeHost(stage.p);
+        stage.p = nullptr;
+        stage.cap = 0;
+        cuda_ok(cudaMallocHost(&stage.p, bytes), "cudaMallocHost");
+        stage.cap = bytes;
+    }
+    cuda_ok(cudaMemcpy(stage.p, static_cast<DevBuf*>(tg.dev64_.get())->p, bytes, cudaMemcpyDeviceToHost), "D2H tgrid");
+    std::memcpy(tg.data_.data(), stage.p, bytes);
     tg.uploaded_ = tg.data_;
     return tg;
 }
@@ -767,12 +829,34 @@ std::vector<InitState> init_states(const Vec3& x_prime, const SearchContext& c, 
 }
 
 namespace {
+void fill_set(CorrespondenceSet& set, const Vec3& query, std::span<const std::int64_t> h_offs,
+              std::span<const fsk_root> roots, int64_t q);
+
 std::vector<CorrespondenceSet> to_sets(std::span<const Vec3> queries, std::span<const std::int64_t> h_offs,
                                        std::span<const fsk_root> roots) {
     std::vector<CorrespondenceSet> out(queries.size());
-    for (size_t q = 0; q < queries.size(); ++q) {
-        auto& set = out[q];
-        set.query = queries[q];
+    // the reference's batch_search builds its sets inside parallel_for's workers: so does this, over the
+    // host cores (contiguous query ranges; the result does not depend on the split)
+    const int64_t n = static_cast<int64_t>(queries.size());
+    const int T = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(std::thread::hardware_concurrency(), n / 8192)));
+    auto fill = [&](int64_t q0, int64_t q1) {
+        for (int64_t q = q0; q < q1; ++q) fill_set(out[static_cast<size_t>(q)], queries[q], h_offs, roots, q);
+    };
+    if (T == 1) {
+        fill(0, n);
+    } else {
+        std::vector<std::thread> pool;
+        for (int t = 0; t < T; ++t) pool.emplace_back(fill, n * t / T, n * (t + 1) / T);
+        for (auto& th : pool) th.join();
+    }
+    return out;
+}
+
+void fill_set(CorrespondenceSet& set, const Vec3& query, std::span<const std::int64_t> h_offs,
+              std::span<const fsk_root> roots, int64_t q) {
+    {
+        set.query = query;
+        set.roots.reserve(static_cast<size_t>(h_offs[q + 1] - h_offs[q]));
         for (std::int64_t k = h_offs[q]; k < h_offs[q + 1]; ++k) {
             const fsk_root& r = roots[static_cast<size_t>(k)];
             Root root;
@@ -785,7 +869,6 @@ std::vector<CorrespondenceSet> to_sets(std::span<const Vec3> queries, std::span<
             set.roots.push_back(root);
         }
     }
-    return out;
 }
 }  // namespace
 
