@@ -23,6 +23,7 @@ void* scratch(fsk_ctx* ctx, int slot, size_t bytes) {
         const size_t b = bytes + bytes / 8;
         cuda_check(cudaMalloc(&ctx->buf[slot], b), "cudaMalloc");
         ctx->cap[slot] = b;
+        ctx->scratch_gen++;
     }
     return ctx->buf[slot];
 }
@@ -285,6 +286,9 @@ int fsk_ctx_destroy(fsk_ctx* ctx) {
         if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
         if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
         if (ctx->hcount) cudaFreeHost(ctx->hcount);
+        for (auto& pg : ctx->pipe_graphs)
+            if (pg.exec) cudaGraphExecDestroy(pg.exec);
+        if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
         delete ctx;
     });
 }

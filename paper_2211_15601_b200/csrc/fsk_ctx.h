@@ -45,6 +45,20 @@ struct fsk_ctx {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int64_t* hcount = nullptr;  // pinned per-chunk root counts
     int64_t last_search_n = -1;  // point count of the last device search (its order is in scratch kPerm)
+    // bumped on every scratch (re)allocation: the host pipeline's captured graphs key on it
+    uint64_t scratch_gen = 0;
+    // CUDA graphs of the host pipeline's per-chunk device work (search + dedup + compaction),
+    // keyed on everything the captured launches bake in (fsk_search.cu, deform_host_pipeline)
+    struct PipeGraph {
+        std::vector<unsigned char> key;
+        cudaGraphExec_t exec = nullptr;  // null: seen once (ran eagerly); captured on the next sight
+        int64_t launches = 0;
+        unsigned char planes[64];
+        uint64_t last_use = 0;
+    };
+    std::vector<PipeGraph> pipe_graphs;
+    uint64_t pipe_clock = 0;
+    cudaStream_t cap_stream = nullptr;  // capture stream (the caller's may be the legacy default stream)
 };
 
 namespace fsk {

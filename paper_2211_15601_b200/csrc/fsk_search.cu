@@ -1664,12 +1664,97 @@ void deform_host_pipeline(fsk_ctx* ctx, const float* weights, const GridP& g, in
     auto slot_o = [&](int i) { return dOff + (i & 1) * (cmax + 1); };
     auto slot_r = [&](int i) { return dR + (i & 1) * slotcap; };
     GridPlanes P;  // the current frame's gather planes (K1 runs with the frame's first chunk)
-    auto search_item = [&](int i, fsk_root* out, int64_t cap) {
+    auto search_eager = [&](int i, fsk_root* out, int64_t cap, cudaStream_t s_) {
         const Item& it = items[i];
         const PrecomputeReq pre{dW, slot_b(i), nullptr, needs_f64(flags)};
         const SearchState s =
-            run_search(ctx, P, g, dW, slot_b(i), slot_p(i), it.m, sp, flags, st, it.first ? &pre : nullptr);
-        compact(ctx, s, it.m, nb, slot_o(i), out, cap, st);
+            run_search(ctx, P, g, dW, slot_b(i), slot_p(i), it.m, sp, flags, s_, it.first ? &pre : nullptr);
+        compact(ctx, s, it.m, nb, slot_o(i), out, cap, s_);
+    };
+    // A chunk's device work (K1 on a frame's first chunk, sort, search, escalation, dedup, scan,
+    // emit: ~20 launches) is replayed from a CUDA graph once the same launch set has been seen
+    // before — same slot buffers, chunk size, options and scratch generation (a scratch regrow
+    // frees buffers the graph points into, so it changes the key). First sight runs eagerly
+    // (warms the scratch sizes), the second captures. FSK_PIPE_GRAPH=0 turns it off.
+    const bool graphs_on = [] {
+        const char* e = getenv("FSK_PIPE_GRAPH");
+        return !(e && e[0] == '0');
+    }();
+    static_assert(sizeof(GridPlanes) <= sizeof(fsk_ctx::PipeGraph::planes), "planes record");
+    auto search_item = [&](int i, fsk_root* out, int64_t cap) {
+        const Item& it = items[i];
+        if (!graphs_on || ctx->prof_on) return search_eager(i, out, cap, st);
+        std::vector<unsigned char> key;
+        auto put = [&](const void* p, size_t b) {
+            key.insert(key.end(), (const unsigned char*)p, (const unsigned char*)p + b);
+        };
+        const void* ptrs[6] = {dW, slot_b(i), slot_p(i), slot_o(i), out, nullptr};
+        const int64_t ints[3] = {it.m, cap, (int64_t)it.first};
+        put(&ctx->scratch_gen, sizeof ctx->scratch_gen);
+        put(ptrs, sizeof ptrs);
+        put(ints, sizeof ints);
+        put(&flags, sizeof flags);
+        put(&sp, sizeof sp);
+        put(&g, sizeof g);
+        if (!it.first) put(&P, sizeof P);  // later chunks read the frame's planes
+        auto& cache = ctx->pipe_graphs;
+        fsk_ctx::PipeGraph* hit = nullptr;
+        for (auto& pg : cache)
+            if (pg.key == key) hit = &pg;
+        if (hit && hit->exec) {
+            hit->last_use = ++ctx->pipe_clock;
+            if (it.first) memcpy(&P, hit->planes, sizeof P);
+            ctx->launches += hit->launches;
+            ctx->last_search_n = it.m;
+            cuda_check(cudaGraphLaunch(hit->exec, st), "cudaGraphLaunch");
+            return;
+        }
+        if (!hit) {  // first sight: run eagerly, remember the key
+            search_eager(i, out, cap, st);
+            if (ctx->scratch_gen != *(const uint64_t*)key.data()) return;  // grew while running: key is stale
+            if (cache.size() >= 8) {
+                auto lru = std::min_element(cache.begin(), cache.end(), [](const auto& a, const auto& b) {
+                    return a.last_use < b.last_use;
+                });
+                if (lru->exec) cudaGraphExecDestroy(lru->exec);
+                cache.erase(lru);
+            }
+            cache.push_back({});
+            cache.back().key = std::move(key);
+            cache.back().last_use = ++ctx->pipe_clock;
+            return;
+        }
+        // second sight: capture on the private stream, instantiate, launch on the caller's
+        if (!ctx->cap_stream)
+            cuda_check(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        const int64_t l0 = ctx->launches;
+        const uint64_t gen0 = ctx->scratch_gen;
+        cudaGraph_t graph = nullptr;
+        cuda_check(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeRelaxed), "cudaStreamBeginCapture");
+        try {
+            search_eager(i, out, cap, ctx->cap_stream);
+        } catch (...) {
+            cudaStreamEndCapture(ctx->cap_stream, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            cudaGetLastError();
+            throw;
+        }
+        cuda_check(cudaStreamEndCapture(ctx->cap_stream, &graph), "cudaStreamEndCapture");
+        cudaGraphExec_t exec = nullptr;
+        const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        cuda_check(ie, "cudaGraphInstantiate");
+        if (ctx->scratch_gen != gen0) {  // buffers moved under the capture: do not keep it
+            cudaGraphExecDestroy(exec);
+            ctx->launches = l0;
+            return search_eager(i, out, cap, st);
+        }
+        hit->exec = exec;
+        hit->launches = ctx->launches - l0;
+        hit->last_use = ++ctx->pipe_clock;
+        if (it.first) memcpy(hit->planes, &P, sizeof P);
+        ctx->last_search_n = it.m;
+        cuda_check(cudaGraphLaunch(exec, st), "cudaGraphLaunch");
     };
     auto enqueue = [&](int i) {
         const Item& it = items[i];

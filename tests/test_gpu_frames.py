@@ -106,3 +106,39 @@ def test_host_call_reports_total_when_buffer_too_small(deformer):
     assert rc == 1 and total.value > 100
     exact = torch.zeros((total.value, 16), dtype=torch.float32).pin_memory()
     assert deformer.deform_host(hw, base.dims, base.bbox, b, p, o, offs, exact) == total.value
+
+
+@pytest.mark.parametrize("chunks", [1, 3])
+def test_graph_replayed_items_equal_eager(deformer, monkeypatch, chunks):
+    """The host pipeline replays a chunk's device work from a CUDA graph once it has seen the same
+    launch set (slot buffers, chunk size, options, scratch generation) before. Ten frames of
+    distinct poses, called twice (the second call replays from the first call's graphs), equal
+    the eager pipeline (FSK_PIPE_GRAPH=0) bit for bit; so does a call after a scratch regrow."""
+    base, frames = _frames([6000 + 100 * (i % 2) for i in range(10)])
+    hw = torch.from_numpy(base.weights).pin_memory()
+    o = _opts(base)
+    monkeypatch.setenv("FSK_HOST_CHUNKS", str(chunks))
+
+    def run():
+        offs = [torch.empty(p.shape[0] + 1, dtype=torch.int64).pin_memory() for _, p in frames]
+        roots = [torch.zeros((p.shape[0] * 3, 16), dtype=torch.float32).pin_memory() for _, p in frames]
+        t = deformer.deform_host_frames(hw, base.dims, base.bbox, [b for b, _ in frames], [p for _, p in frames], o,
+                                        offs, roots)
+        return t, [x.numpy().copy() for x in offs], [r[:n].numpy().view(np.uint32).copy() for r, n in zip(roots, t)]
+
+    monkeypatch.setenv("FSK_PIPE_GRAPH", "0")
+    ref = run()
+    monkeypatch.setenv("FSK_PIPE_GRAPH", "1")
+    got = [run(), run()]
+    # a bigger search in between regrows the scratch (new generation: the cached graphs are not reused)
+    big = S.make_scene(base.dims, 60000, seed=7)
+    x = torch.from_numpy(big.points).cuda()
+    w, B = torch.from_numpy(base.weights).cuda(), torch.from_numpy(big.bones).cuda()
+    deformer.deform(w, base.dims, base.bbox, B, x, o)
+    torch.cuda.synchronize()
+    got.append(run())
+    for t, offs, roots in got:
+        assert t == ref[0]
+        for f in range(len(frames)):
+            np.testing.assert_array_equal(offs[f], ref[1][f])
+            np.testing.assert_array_equal(roots[f], ref[2][f])
