@@ -130,6 +130,29 @@ __device__ __forceinline__ void fma4(R* T, R w, const V4<R>& a) {
     T[3] = fma(w, a.w, T[3]);
 }
 
+#ifndef FSK_NO_FFMA2
+// Blackwell's packed FP32 FMA (FFMA2): two independent fma.rn.f32 per issue slot — the same
+// two roundings as the scalar form, so results are bitwise unchanged. The trilinear accumulate
+// (96 FMAs per evaluation) is the bulk of the float32 pass's FP instructions.
+__device__ __forceinline__ void ffma2(float& c0, float& c1, float a0, float a1, float b0, float b1) {
+    // c0 = fma(a0, b0, c0), c1 = fma(a1, b1, c1)
+    asm("{\n\t.reg .b64 pa, pb, pc;\n\t"
+        "mov.b64 pa, {%2, %3};\n\t"
+        "mov.b64 pb, {%4, %5};\n\t"
+        "mov.b64 pc, {%0, %1};\n\t"
+        "fma.rn.f32x2 pc, pa, pb, pc;\n\t"
+        "mov.b64 {%0, %1}, pc;\n\t}"
+        : "+f"(c0), "+f"(c1)
+        : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+
+template <>
+__device__ __forceinline__ void fma4<float>(float* T, float w, const V4<float>& a) {
+    ffma2(T[0], T[1], w, w, a.x, a.y);
+    ffma2(T[2], T[3], w, w, a.z, a.w);
+}
+#endif
+
 template <typename R>
 __device__ __forceinline__ R row_dot(const V4<R>& a, R x, R y, R z) {
     return a.x * x + a.y * y + a.z * z + a.w;
@@ -231,6 +254,17 @@ __device__ __forceinline__ void grad_term(R G[9], R y0, R y1, R y2, R gx, R gy, 
     G[3] = fma(y1, gx, G[3]); G[4] = fma(y1, gy, G[4]); G[5] = fma(y1, gz, G[5]);
     G[6] = fma(y2, gx, G[6]); G[7] = fma(y2, gy, G[7]); G[8] = fma(y2, gz, G[8]);
 }
+#if !defined(FSK_NO_FFMA2) && defined(FSK_FFMA2_GRAD)  // ablation: spills 16 B in k_search_fast (pair constraints)
+template <>
+__device__ __forceinline__ void grad_term<float>(float G[9], float y0, float y1, float y2, float gx, float gy,
+                                                 float gz) {
+    ffma2(G[0], G[1], y0, y0, gx, gy);
+    ffma2(G[2], G[3], y0, y1, gz, gx);
+    ffma2(G[4], G[5], y1, y1, gy, gz);
+    ffma2(G[6], G[7], y2, y2, gx, gy);
+    G[8] = fmaf(y2, gz, G[8]);
+}
+#endif
 
 // Analytic Jacobian and T(p) at x:
 //   J = T_lin(p) + Σ_c (T_c x̃) ∇φ_c(p)ᵀ
@@ -374,6 +408,25 @@ struct SolveOut {
 #define FSK_REASON(bit) ((void)0)
 #endif
 
+// J~ += q wᵀ (the good-Broyden rank-one update, correspondence.cpp:120-121), one FMA per entry
+template <typename R>
+__device__ __forceinline__ void rank1_update(R Ji[9], R q0, R q1, R q2, R w0, R w1, R w2) {
+    Ji[0] = fma(q0, w0, Ji[0]); Ji[1] = fma(q0, w1, Ji[1]); Ji[2] = fma(q0, w2, Ji[2]);
+    Ji[3] = fma(q1, w0, Ji[3]); Ji[4] = fma(q1, w1, Ji[4]); Ji[5] = fma(q1, w2, Ji[5]);
+    Ji[6] = fma(q2, w0, Ji[6]); Ji[7] = fma(q2, w1, Ji[7]); Ji[8] = fma(q2, w2, Ji[8]);
+}
+#if !defined(FSK_NO_FFMA2) && defined(FSK_FFMA2_RANK1)  // ablation: no fewer SASS instructions (pair moves)
+template <>
+__device__ __forceinline__ void rank1_update<float>(float Ji[9], float q0, float q1, float q2, float w0, float w1,
+                                                    float w2) {
+    ffma2(Ji[0], Ji[1], q0, q0, w0, w1);
+    ffma2(Ji[2], Ji[3], q0, q1, w2, w0);
+    ffma2(Ji[4], Ji[5], q1, q1, w1, w2);
+    ffma2(Ji[6], Ji[7], q2, q2, w0, w1);
+    Ji[8] = fmaf(q2, w2, Ji[8]);
+}
+#endif
+
 // One Broyden iteration after the divergence check (correspondence.cpp:106-122): step,
 // re-evaluate, and — unless the new residual converged — the good-Broyden rank-one update.
 // Returns true iff converged; `den` receives dx·J~dg (0 when converged).
@@ -425,9 +478,7 @@ __device__ __forceinline__ bool broyden_step(const Planes<R>& P, const GridP& g,
         const R w0 = dx0 * Ji[0] + dx1 * Ji[3] + dx2 * Ji[6];
         const R w1 = dx0 * Ji[1] + dx1 * Ji[4] + dx2 * Ji[7];
         const R w2 = dx0 * Ji[2] + dx1 * Ji[5] + dx2 * Ji[8];
-        Ji[0] = fma(q0, w0, Ji[0]); Ji[1] = fma(q0, w1, Ji[1]); Ji[2] = fma(q0, w2, Ji[2]);
-        Ji[3] = fma(q1, w0, Ji[3]); Ji[4] = fma(q1, w1, Ji[4]); Ji[5] = fma(q1, w2, Ji[5]);
-        Ji[6] = fma(q2, w0, Ji[6]); Ji[7] = fma(q2, w1, Ji[7]); Ji[8] = fma(q2, w2, Ji[8]);
+        rank1_update(Ji, q0, q1, q2, w0, w1, w2);
     }
     return false;
 }
