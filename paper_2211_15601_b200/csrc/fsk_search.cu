@@ -458,6 +458,30 @@ __device__ __forceinline__ void count_work(unsigned long long* stats, const Solv
 #ifndef FSK_FAST_BPG
 #define FSK_FAST_BPG 8  // bone inits per block (0: all). C2 fast pass: 1 0.638 ms, 2 0.594, 4 0.575, 8 0.572, 12 0.581, 24 0.601 (bone-major blocks: 0.633)
 #endif
+#ifndef FSK_INIT_PREFETCH
+#define FSK_INIT_PREFETCH 0  // measured slower: C2 fast pass 0.544 -> 0.583 ms, C4-grid 2.905 -> 3.121 ms (hashes equal)
+#endif
+// (ablation) L1 prefetch of the next init's cell: x0 = B^-1 x' of the next bone (an address hint only — the
+// solve recomputes it exactly), its 4 x-pair edges × 3 rows. The init gathers are the pass's
+// L1 misses (the cell is new for every bone); issued one solve ahead, they land during it.
+__device__ __forceinline__ void prefetch_init(const Planes<float>& P, const GridP& g, const float* __restrict__ B,
+                                              const float4& xq) {
+    const float t0 = __ldg(B + 3), t1 = __ldg(B + 7), t2 = __ldg(B + 11);
+    const float d0 = xq.x - t0, d1 = xq.y - t1, d2 = xq.z - t2;
+    const float x0 = __ldg(B + 0) * d0 + __ldg(B + 4) * d1 + __ldg(B + 8) * d2;
+    const float x1 = __ldg(B + 1) * d0 + __ldg(B + 5) * d1 + __ldg(B + 9) * d2;
+    const float x2 = __ldg(B + 2) * d0 + __ldg(B + 6) * d1 + __ldg(B + 10) * d2;
+    const Cell<float> c = locate<false, float>(g, x0, x1, x2);
+    const int nxy = g.nx * g.ny;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const int v = c.base + (e >> 1) * nxy + (e & 1) * g.nx;
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(P.p + r * P.stride + (int64_t)v * 8));
+    }
+}
+
 __global__ void __launch_bounds__(kSearchBlock, FSK_SEARCH_MINB)
     k_search_fast(Planes<float> P, GridP g, const float* __restrict__ bones, const float4* __restrict__ xs, int64_t n,
                   int bpg, SearchP o, SearchPlanes out, int4* __restrict__ esc_q, int64_t esc_cap,
@@ -480,7 +504,13 @@ __global__ void __launch_bounds__(kSearchBlock, FSK_SEARCH_MINB)
 #ifndef FSK_PER_SOLVE_STATS
     unsigned w_solves = 0, w_iters = 0, w_fin = 0, w_fills = 0;  // work counters, flushed once per thread
 #endif
+#if FSK_INIT_PREFETCH
+    prefetch_init(P, g, bones + 12 * (grp * bpg), xq);
+#endif
     for (int bone = grp * bpg; bone < b_end; ++bone) {
+#if FSK_INIT_PREFETCH
+        if (bone + 1 < b_end) prefetch_init(P, g, bones + 12 * (bone + 1), xq);
+#endif
         float x0, x1, x2, Ji[9], err2;
         const SolveOut s = solve_one<float, true>(P, g, bones + 12 * bone, xq.x, xq.y, xq.z, o, x0, x1, x2, Ji, err2);
         const int64_t q = (int64_t)bone * n + j;
