@@ -250,9 +250,28 @@ __global__ void __launch_bounds__(256) k_bwd_scatter_agg(GridP g, RootRef R, con
         if (cur >= 0 && owner) atomicAdd(gT + 3 * (int64_t)(cur + dk * nxy + dj * g.nx + di) + row, acc);
         acc = make_float4(0.f, 0.f, 0.f, 0.f);
     };
+#ifndef FSK_K3_SHFL
+    // the warp's 32 root records staged in shared memory: the walk reads each with three
+    // broadcast LDS.128 instead of ten shuffles (C3 K3: fewer MIO instructions per root)
+    __shared__ float4 s_rec[256 / 32][32][3];
+    float4(&rec)[32][3] = s_rec[threadIdx.x >> 5];
+    rec[lane][0] = make_float4(__int_as_float(c.base), c.tx, c.ty, c.tz);
+    rec[lane][1] = make_float4(xs[0], xs[1], xs[2], u[0]);
+    rec[lane][2] = make_float4(u[1], u[2], 0.f, 0.f);
+    __syncwarp();
+#endif
     while (todo) {
         const int src = __ffs(todo) - 1;
         todo &= todo - 1;
+#ifndef FSK_K3_SHFL
+        const float4 r0 = rec[src][0], r1 = rec[src][1], r2 = rec[src][2];
+        const int cj = __float_as_int(r0.x);
+        const float tx = r0.y, ty = r0.z, tz = r0.w, x0 = r1.x, x1 = r1.y, x2 = r1.z, u0 = r1.w, u1 = r2.x, u2 = r2.y;
+        if (cj != cur) {  // warp-uniform
+            flush();
+            cur = cj;
+        }
+#else
         const int cj = __shfl_sync(0xffffffffu, c.base, src);
         if (cj != cur) {  // warp-uniform
             flush();
@@ -264,6 +283,7 @@ __global__ void __launch_bounds__(256) k_bwd_scatter_agg(GridP g, RootRef R, con
                     x2 = __shfl_sync(0xffffffffu, xs[2], src);
         const float u0 = __shfl_sync(0xffffffffu, u[0], src), u1 = __shfl_sync(0xffffffffu, u[1], src),
                     u2 = __shfl_sync(0xffffffffu, u[2], src);
+#endif
         if (owner) {
             const float wz = dk ? tz : 1.f - tz;
             const float wyz = wz * (dj ? ty : 1.f - ty);

@@ -65,7 +65,7 @@ namespace fsk {
 
 // Scratch slots (one growable device buffer each).
 enum Slot {
-    kHist, kBbox, kKeys, kPerm, kXs, kScanPart, kBwdAcc, kBwdMax, kPlanes, kPlanes64, kEscQ, kEscN, kEscState,
+    kHist, kBbox, kKeys, kPerm, kXs, kScanPart, kScanLB, kBwdAcc, kBwdMax, kPlanes, kPlanes64, kEscQ, kEscN, kEscState,
     kBwdStart, kBwdCell, kBwdRec, kPeakTable, kBwdU, kBwdOk,
     kOXr, kOJa, kOJb, kOJc, kOMeta, kOKeep, kOKeepMask, kNRoots, kOffs, kRootsTmp, kOXd,
     kHW, kHB, kHP, kHT, kHOffs, kHRoots, kFB, kFP, kFOffs, kFRoots,

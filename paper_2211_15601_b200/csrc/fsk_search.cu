@@ -1015,6 +1015,83 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_apply(const int32_t* __re
     if (blockIdx.x == nblocks - 1 && threadIdx.x == 0) out[n] = part[nblocks];
 }
 
+// Single-pass form of the scan for the search's root counts (decoupled look-back): each block
+// takes a tile by ticket (so every tile it waits on has started), publishes its aggregate, then
+// walks back over its predecessors' published aggregates / inclusive prefixes. Status word per
+// tile: flag (bits 62-63: 1 aggregate, 2 inclusive prefix) | epoch (bits 32-61) | value (bits
+// 0-31; the counts total at most n·n_b < 2^31). The epoch (advanced by the last tile) retires
+// the previous launch's words without a memset, so the launch is graph-replayable.
+// ctl[0] = ticket, ctl[1] = epoch; the buffer is zeroed when allocated.
+#ifndef FSK_SCAN_LOOKBACK
+#define FSK_SCAN_LOOKBACK 1
+#endif
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_lookback(const int32_t* __restrict__ in, int64_t n,
+                                                                unsigned* __restrict__ ctl,
+                                                                unsigned long long* __restrict__ status,
+                                                                int64_t* __restrict__ out) {
+    __shared__ int64_t wt[32];
+    __shared__ int64_t tot;
+    __shared__ unsigned s_tile, s_epoch;
+    __shared__ int64_t s_prefix;
+    const unsigned ntiles = (unsigned)((n + kScanTile - 1) / kScanTile);
+    if (threadIdx.x == 0) {
+        s_epoch = *(volatile unsigned*)(ctl + 1);
+        s_tile = atomicAdd(ctl, 1u);
+    }
+    __syncthreads();
+    const unsigned tile = s_tile;
+    const unsigned long long ep = (unsigned long long)(s_epoch & 0x3fffffffu) << 32;
+    const int64_t base = tile * (int64_t)kScanTile + threadIdx.x * kScanPer;
+    int64_t v[kScanPer];
+    int64_t sum = 0;
+#pragma unroll
+    for (int i = 0; i < kScanPer; ++i) {
+        v[i] = (base + i < n) ? in[base + i] : 0;
+        sum += v[i];
+    }
+    const int64_t excl = block_excl_scan(sum, wt, &tot);
+    if (threadIdx.x == 0) {
+        const unsigned long long agg = (unsigned long long)(uint32_t)tot;
+        int64_t pre = 0;
+        if (tile == 0) {
+            st_relaxed_u64(status, (2ull << 62) | ep | agg);
+        } else {
+            st_relaxed_u64(status + tile, (1ull << 62) | ep | agg);
+            for (int64_t t = (int64_t)tile - 1;; --t) {
+                unsigned long long w;
+                do {
+                    w = ld_relaxed_u64(status + t);
+                } while ((w & 0x3fffffff00000000ull) != ep || (w >> 62) == 0);
+                pre += (int64_t)(w & 0xffffffffull);
+                if ((w >> 62) == 2) break;
+            }
+            st_relaxed_u64(status + tile, (2ull << 62) | ep | (unsigned long long)(uint32_t)(pre + tot));
+        }
+        s_prefix = pre;
+        if (tile == ntiles - 1) {  // the last ticket: every block has read the epoch and taken its ticket
+            out[n] = pre + tot;
+            ctl[0] = 0;
+            ctl[1] = (s_epoch + 1) & 0x3fffffffu;
+        }
+    }
+    __syncthreads();
+    int64_t run = s_prefix + excl;
+#pragma unroll
+    for (int i = 0; i < kScanPer; ++i) {
+        if (base + i < n) out[base + i] = run;
+        run += v[i];
+    }
+}
+
 // ============================================================================ compaction
 __device__ __forceinline__ void store_root(fsk_root* dst, float4 xr, float4 ja, float4 jb, float jc, int bone,
                                            int iters) {
@@ -1392,9 +1469,25 @@ void run_scan(fsk_ctx* ctx, const int32_t* in, int64_t n, int64_t* out, cudaStre
     FSK_LAUNCH(ctx, st, k_scan_apply, (unsigned)nb, kScanThreads, 0, in, n, part, out);
 }
 
+// exclusive scan of the search's per-query root counts (each <= n_b, total < 2^31)
+void scan_root_counts(fsk_ctx* ctx, const int32_t* in, int64_t n, int64_t* out, cudaStream_t st) {
+#if FSK_SCAN_LOOKBACK
+    if (n > 0) {
+        const int64_t ntiles = (n + kScanTile - 1) / kScanTile;
+        const uint64_t gen0 = ctx->scratch_gen;
+        auto* buf = (unsigned long long*)scratch(ctx, kScanLB, (ntiles + 1) * sizeof(unsigned long long));
+        if (ctx->scratch_gen != gen0)  // fresh allocation: zero ticket, epoch and status words
+            cuda_check(cudaMemsetAsync(buf, 0, ctx->cap[kScanLB], st), "cudaMemsetAsync");
+        FSK_LAUNCH(ctx, st, k_scan_lookback, (unsigned)ntiles, kScanThreads, 0, in, n, (unsigned*)buf, buf + 1, out);
+        return;
+    }
+#endif
+    run_scan(ctx, in, n, out, st);
+}
+
 void compact(fsk_ctx* ctx, const SearchState& s, int64_t n, int nb, int64_t* offsets, fsk_root* roots, int64_t cap,
              cudaStream_t st) {
-    run_scan(ctx, s.n_roots_p, n, offsets, st);
+    scan_root_counts(ctx, s.n_roots_p, n, offsets, st);
     if (n > 0 && roots && cap > 0)
         FSK_LAUNCH(ctx, st, k_emit, blocks_for(n, 256), 256, 0, n, nb, s.sp, s.perm, offsets, roots, cap);
 }
