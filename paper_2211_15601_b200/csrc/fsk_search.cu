@@ -24,11 +24,14 @@
 // every solve whose outcome float32 cannot settle (long or late-diverging trajectories,
 // threshold decisions within float32 noise); those (~5 %) are solved again in float64,
 // which B200 runs at half the float32 rate.
+#include <cooperative_groups.h>
 #include <cstdlib>
 #include <cstring>
 
 #include "fsk_ctx.h"
 #include "fsk_exact.cuh"
+
+namespace cg = cooperative_groups;
 
 // FSK_CHECKED builds (scripts: the GPU suite under FSK_LIB=build/variants/checked.so) trap on any
 // out-of-range index at the places a logic error would write out of bounds: the sort's scatter, the
@@ -224,8 +227,10 @@ __device__ __forceinline__ float ord2f(int i) { return __int_as_float(i >= 0 ? i
 //   [0, kSortBuckets) histogram, then bbox (6 words), escalation counters (4), scan barrier (2).
 // The bbox is kept in a zero-identity encoding: u = f2ord(f) ^ 0x80000000 (unsigned order);
 // max stored as u, min stored as ~u, both reduced with atomicMax.
-constexpr int kSortStateInts = kSortBuckets + 64;  // + bbox, counters, barrier + 32 block sums
-constexpr int kBboxOff = kSortBuckets, kEscOff = kSortBuckets + 8, kScanBarOff = kSortBuckets + 16;
+constexpr int kSortMaxBlocks = 1024;  // block sums of the fused sort's bucket scan
+constexpr int kSortStateInts = kSortBuckets + 64 + kSortMaxBlocks;  // + bbox, counters, barrier + 32 block sums, fused-sort sums
+constexpr int kBboxOff = kSortBuckets, kEscOff = kSortBuckets + 8, kScanBarOff = kSortBuckets + 16,
+              kSortSumsOff = kSortBuckets + 64;
 __device__ __forceinline__ unsigned bb_enc(float f) { return (unsigned)f2ord(f) ^ 0x80000000u; }
 __device__ __forceinline__ float bb_dec(unsigned u) { return ord2f((int)(u ^ 0x80000000u)); }
 
@@ -827,6 +832,152 @@ __global__ void __launch_bounds__(kEscBlock, kExact ? FSK_ESC_EXACT_MINB : FSK_E
     }
 }
 
+// Exact-replay refill with prefetched work (ablation, off by default): every lane keeps
+// its NEXT queue entry — the {q, x'} record and its precomputed start state, 144 B — in a shared-
+// memory slot, fetched with cp.async while it iterates. A lane whose solve ends swaps the slot in
+// (nine LDS.128, no global latency on the warp) and issues the fetch for the entry after, so lanes
+// are refilled as soon as FSK_REFILL_IDLE_PF of them are idle instead of waiting for half the warp
+// to idle behind one batched global load. Arithmetic per solve is k_search_escalated<true>'s.
+#ifndef FSK_ESC_PREFETCH
+#define FSK_ESC_PREFETCH 0  // measured slower on C2: refill 0.268 -> ~0.32-0.36 ms (idle threshold 1/4/8/16), hashes equal
+#endif
+#ifndef FSK_REFILL_IDLE_PF
+#define FSK_REFILL_IDLE_PF 4
+#endif
+constexpr int kEscSlotF4 = 9;  // float4 words per prefetch slot: record + 8 double2 of start state
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+__global__ void __launch_bounds__(kEscBlock, FSK_ESC_EXACT_MINB)
+    k_search_escalated_pf(Planes<double> P, GridP g, const float* __restrict__ W, const float* __restrict__ bones,
+                          int64_t n, SearchP o, SearchPlanes out, const int4* __restrict__ esc_q, int64_t esc_cap,
+                          const int* __restrict__ esc_count, const double2* __restrict__ st, int st_cap,
+                          unsigned long long* __restrict__ stats) {
+    const int cnt_long = esc_count[3], cnt = esc_count[3] + esc_count[2];
+    const double* bones64 = stage_bones64(bones, g.nb);
+    float4* slot = reinterpret_cast<float4*>(const_cast<double*>(bones64) + 12 * g.nb + ((12 * g.nb) & 1)) +
+                   kEscSlotF4 * threadIdx.x;
+    int* work = const_cast<int*>(esc_count) + 1;
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1;
+    unsigned n_solves = 0, n_iters = 0, n_final = 0;
+    exact::XState xs{};
+    exact::XCache xcache;
+    int64_t q = 0;
+    float4 xq = make_float4(0.f, 0.f, 0.f, 0.f);
+    bool active = false;
+    int pend = -1;  // queue index of the entry in this lane's slot (-1: none)
+    // warp-local buffer of 32 claimed queue indices (lane i holds base + i): one atomic per 32 claims
+    int buf_idx = 0, bused = 32;
+    // claim one queue index for every lane with `want` (warp-collective), prefetch it into the slot
+    auto claim_and_fetch = [&](bool want) {
+        unsigned m = __ballot_sync(full, want);
+        int got = -1;
+        while (m) {
+            if (bused == 32) {
+                int base = 0;
+                if (lane == 0) base = atomicAdd(work, 32);
+                base = __shfl_sync(full, base, 0);
+                buf_idx = base + lane;
+                bused = 0;
+            }
+            const int rank = __popc(m & lt);
+            const bool take = ((m >> lane) & 1u) && rank < 32 - bused;
+            const int idx = __shfl_sync(full, buf_idx, min(bused + rank, 31));
+            if (take) got = idx;
+            const unsigned tk = __ballot_sync(full, take);
+            bused += __popc(tk);
+            m &= ~tk;
+        }
+        if (want) {
+            pend = got < cnt ? got : -1;
+            if (pend >= 0) {
+                FSK_CHECK(pend < cnt && cnt <= esc_cap);
+                cp_async16(slot, esc_q + (pend < cnt_long ? pend : esc_cap - 1 - (pend - cnt_long)));
+                if (pend < st_cap) {
+                    const double2* d = st + 8 * (int64_t)pend;
+#pragma unroll
+                    for (int h = 0; h < 8; ++h) cp_async16(slot + 1 + h, d + h);
+                }
+                cp_async_commit();
+            }
+        }
+    };
+    claim_and_fetch(true);
+    while (true) {
+        const bool ready = !active && pend >= 0;
+        const unsigned rdy = __ballot_sync(full, ready);
+        const unsigned act = __ballot_sync(full, active);
+        if (!rdy && !act) break;  // nothing running, nothing fetched: the queue is drained for this warp
+        if (rdy && (__popc(rdy) >= FSK_REFILL_IDLE_PF || !act || __popc(~act) == 32)) {
+            bool refetch = false;
+            if (ready) {  // start of the solve (correspondence.cpp:135-137, :43-54): the prefetched slot
+                cp_async_wait_all();
+                const int idx = pend;
+                const float4 r0 = slot[0];
+                const int4 rec = make_int4(__float_as_int(r0.x), __float_as_int(r0.y), __float_as_int(r0.z),
+                                           __float_as_int(r0.w));
+                q = rec.x;
+                FSK_CHECK(q >= 0 && q < n * g.nb);
+                xq = make_float4(__int_as_float(rec.y), __int_as_float(rec.z), __int_as_float(rec.w), 0.f);
+                double sv[16];
+                bool conv = false, stop;
+                if (idx < st_cap) {  // started by k_esc_start (stopped ones are already stored)
+#pragma unroll
+                    for (int h = 0; h < 8; ++h) {
+                        const float4 v = slot[1 + h];
+                        sv[2 * h] = __hiloint2double(__float_as_int(v.y), __float_as_int(v.x));
+                        sv[2 * h + 1] = __hiloint2double(__float_as_int(v.w), __float_as_int(v.z));
+                    }
+                    stop = sv[6] < 0.0;
+                    active = !stop;
+                } else {
+                    esc_start_one<true>(P, g, W, bones, bones64, n, o, rec, sv, stop, conv);
+                    active = true;
+                }
+                xs.x0 = sv[0], xs.x1 = sv[1], xs.x2 = sv[2], xs.g0 = sv[3], xs.g1 = sv[4], xs.g2 = sv[5];
+                xs.err = sv[6], xs.k = 0;
+#pragma unroll
+                for (int e = 0; e < 9; ++e) xs.Ji[e] = sv[7 + e];
+                if (active && stop) {
+                    store_exact(out, q, xs, conv);
+                    n_solves += 1;
+                    active = false;
+                }
+                refetch = true;
+            }
+            claim_and_fetch(refetch);
+        }
+        if (active) {  // one Broyden iteration (:106-122)
+            const bool conv = exact::step(P, g, xq.x, xq.y, xq.z, o.conv_eps, xs, &xcache);
+            const bool div = xs.err > o.div_eps;
+            if (conv || xs.k >= o.max_iters || div) {
+                store_exact(out, q, xs, conv);
+                n_solves += 1;
+                n_iters += xs.k;
+                n_final += (conv && xs.k > 0);
+                active = false;
+            }
+        }
+    }
+    cp_async_wait_all();
+    if (stats) {
+        n_solves = __reduce_add_sync(full, n_solves);
+        n_iters = __reduce_add_sync(full, n_iters);
+        n_final = __reduce_add_sync(full, n_final);
+        if (lane == 0 && n_solves) {
+            atomicAdd(stats + 3, (unsigned long long)n_solves);
+            atomicAdd(stats + 4, (unsigned long long)n_iters);
+            atomicAdd(stats + 5, (unsigned long long)n_final);
+        }
+    }
+}
+
 // Parity mode: every solve in float64.
 __global__ void __launch_bounds__(128) k_search_f64(Planes<double> P, GridP g, const float* __restrict__ bones,
                                                     const float4* __restrict__ xs, int64_t n, int blocks_per_bone,
@@ -1013,6 +1164,116 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_apply(const int32_t* __re
     }
     const int64_t nblocks = n > 0 ? (n + kScanTile - 1) / kScanTile : 1;
     if (blockIdx.x == nblocks - 1 && threadIdx.x == 0) out[n] = part[nblocks];
+}
+
+// The spatial sort in one cooperative launch (grid = one 1024-thread block per SM, all
+// co-resident): bbox → grid sync → Morton keys + histogram → grid sync → bucket scan (block
+// sums, grid sync, prefix) → grid sync → scatter. Same keys, buckets and within-bucket
+// atomics as the four-kernel form (k_sort_bbox/_hist/_scan/_scatter). Ablation (off by default).
+#ifndef FSK_SORT_FUSED
+#define FSK_SORT_FUSED 0  // measured slower: C2 step 0.967 -> 0.988 ms (38.9 us alone vs 41.6 for the four kernels, and it no longer overlaps K1); C5 sort 365 -> 379 us
+#endif
+__global__ void __launch_bounds__(1024) k_sort_fused(const float* __restrict__ x, int64_t n, int* __restrict__ state,
+                                                     uint16_t* __restrict__ keys, int* __restrict__ perm,
+                                                     float4* __restrict__ xs) {
+    cg::grid_group grid = cg::this_grid();
+    unsigned* bbox = (unsigned*)(state + kBboxOff);
+    int* hist = state;
+    int* sums = state + kSortSumsOff;
+    const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __shared__ float s_lo[3][32], s_hi[3][32];
+    __shared__ int64_t wt[32];
+    __shared__ int64_t tot;
+    __shared__ int s_prefix;
+    {  // 1. bbox of the finite coordinates (k_sort_bbox)
+        float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        for (int64_t p = t0; p < n; p += stride) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const float v = x[3 * p + a];
+                if (isfinite(v)) {
+                    lo[a] = fminf(lo[a], v);
+                    hi[a] = fmaxf(hi[a], v);
+                }
+            }
+        }
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            for (int o = 16; o > 0; o >>= 1) {
+                lo[a] = fminf(lo[a], __shfl_xor_sync(0xffffffff, lo[a], o));
+                hi[a] = fmaxf(hi[a], __shfl_xor_sync(0xffffffff, hi[a], o));
+            }
+            if (lane == 0) {
+                s_lo[a][warp] = lo[a];
+                s_hi[a][warp] = hi[a];
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x < 3) {
+            const int a = threadIdx.x;
+            float l = s_lo[a][0], h = s_hi[a][0];
+            for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+                l = fminf(l, s_lo[a][w]);
+                h = fmaxf(h, s_hi[a][w]);
+            }
+            atomicMax(bbox + a, ~bb_enc(l));
+            atomicMax(bbox + 3 + a, bb_enc(h));
+        }
+    }
+    grid.sync();
+    {  // 2. Morton keys + bucket histogram (k_sort_hist)
+        float lo[3], sc[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = bb_dec(~__ldcg(bbox + a));
+            const float hi = bb_dec(__ldcg(bbox + 3 + a));
+            sc[a] = (float)(1 << kSortBitsPerAxis) / fmaxf(hi - lo[a], 1e-30f);
+        }
+        for (int64_t p = t0; p < n; p += stride) {
+            uint32_t q[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const float u = (x[3 * p + a] - lo[a]) * sc[a];
+                const int qi = isfinite(u) ? __float2int_rd(u) : 0;
+                q[a] = (uint32_t)max(0, min(qi, (1 << kSortBitsPerAxis) - 1));
+            }
+            const uint32_t k = spread3(q[0]) | (spread3(q[1]) << 1) | (spread3(q[2]) << 2);
+            keys[p] = (uint16_t)k;
+            atomicAdd(hist + k, 1);
+        }
+    }
+    grid.sync();
+    // 3. exclusive scan of the buckets: block b owns a contiguous chunk (at most one bucket per thread)
+    const int chunk = (kSortBuckets + gridDim.x - 1) / gridDim.x;
+    const int bk = blockIdx.x * chunk + threadIdx.x;
+    const bool mine = threadIdx.x < chunk && bk < kSortBuckets;
+    const int v = mine ? __ldcg(hist + bk) : 0;
+    const int64_t ex = block_excl_scan(v, wt, &tot);
+    if (threadIdx.x == 0) sums[blockIdx.x] = (int)tot;
+    grid.sync();
+    {
+        int64_t pre = 0;
+        for (int i = threadIdx.x; i < (int)blockIdx.x; i += blockDim.x) pre += __ldcg(sums + i);
+        for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(0xffffffff, pre, o);
+        if (lane == 0) wt[warp] = pre;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int64_t p = 0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) p += wt[w];
+            s_prefix = (int)p;
+        }
+        __syncthreads();
+    }
+    if (mine) hist[bk] = s_prefix + (int)ex;
+    grid.sync();
+    // 4. scatter into sorted order (k_sort_scatter)
+    for (int64_t p = t0; p < n; p += stride) {
+        const int pos = atomicAdd(hist + keys[p], 1);
+        FSK_CHECK(pos >= 0 && pos < n);
+        perm[pos] = (int)p;
+        xs[pos] = make_float4(x[3 * p], x[3 * p + 1], x[3 * p + 2], 0.f);
+    }
 }
 
 // Single-pass form of the scan for the search's root counts (decoupled look-back): each block
@@ -1327,6 +1588,24 @@ struct PrecomputeReq {
 // sort + K2 (+ K2b escalation) + dedup into the ctx's search planes. With `pre`, K1 runs on `st`
 // while the sort runs on the ctx's side stream (fork/join by events, capturable in a graph), and
 // P is filled in here.
+// cooperative launch of k_sort_fused: one block per SM (all co-resident; capturable in graphs)
+void sort_fused(fsk_ctx* ctx, cudaStream_t st, const float* pts, int64_t n, int* state, uint16_t* keys, int* perm,
+                float4* xs) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)ctx->sm_count);
+    cfg.blockDim = dim3(1024);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    prof_begin(ctx, st);
+    cuda_check(cudaLaunchKernelEx(&cfg, k_sort_fused, pts, n, state, keys, perm, xs), "k_sort_fused");
+    after_launch(ctx, "k_sort_fused");
+}
+
 SearchState run_search(fsk_ctx* ctx, GridPlanes& P, const GridP& g, const float* weights, const float* bones,
                        const float* pts, int64_t n, const SearchP& sp, int flags, cudaStream_t st,
                        const PrecomputeReq* pre = nullptr, bool want_x64 = false) {
@@ -1373,11 +1652,15 @@ SearchState run_search(fsk_ctx* ctx, GridPlanes& P, const GridP& g, const float*
             ss = ctx->side;
         }
         cuda_check(cudaMemsetAsync(hist, 0, kSortStateInts * sizeof(int), ss), "cudaMemsetAsync");
-        const unsigned gb = (unsigned)std::min<int64_t>(blocks_for(n, 256), (int64_t)ctx->sm_count * 8);
-        FSK_LAUNCH(ctx, ss, k_sort_bbox, gb, 256, 0, pts, n, bbox);
-        FSK_LAUNCH(ctx, ss, k_sort_hist, blocks_for(n, 256), 256, 0, pts, n, bbox, keys, hist);
-        FSK_LAUNCH(ctx, ss, k_sort_scan, kScanBlocks, 1024, 0, hist, hist + kScanBarOff);
-        FSK_LAUNCH(ctx, ss, k_sort_scatter, blocks_for(n, 256), 256, 0, pts, keys, n, hist, s.perm, xs);
+        if (FSK_SORT_FUSED && ctx->sm_count <= kSortMaxBlocks) {
+            sort_fused(ctx, ss, pts, n, hist, keys, s.perm, xs);
+        } else {
+            const unsigned gb = (unsigned)std::min<int64_t>(blocks_for(n, 256), (int64_t)ctx->sm_count * 8);
+            FSK_LAUNCH(ctx, ss, k_sort_bbox, gb, 256, 0, pts, n, bbox);
+            FSK_LAUNCH(ctx, ss, k_sort_hist, blocks_for(n, 256), 256, 0, pts, n, bbox, keys, hist);
+            FSK_LAUNCH(ctx, ss, k_sort_scan, kScanBlocks, 1024, 0, hist, hist + kScanBarOff);
+            FSK_LAUNCH(ctx, ss, k_sort_scatter, blocks_for(n, 256), 256, 0, pts, keys, n, hist, s.perm, xs);
+        }
         if (pre) {  // join
             cuda_check(cudaEventRecord(ctx->ev_join, ss), "cudaEventRecord");
             precompute();
@@ -1419,10 +1702,17 @@ SearchState run_search(fsk_ctx* ctx, GridPlanes& P, const GridP& g, const float*
         int per_sm = 0;  // persistent kernel: exactly the resident capacity
         // exact replay of the reference whenever the weight grid is at hand
         const bool exact_esc = weights && !(flags & FSK_SEARCH_FAST_ESC);
-        cuda_check(exact_esc ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search_escalated<true>,
-                                                                             kEscBlock, smem64)
-                             : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search_escalated<false>,
-                                                                             kEscBlock, 0),
+        // exact refill with prefetch slots: bones + 144 B per thread of shared memory
+        const size_t smem_pf = smem64 + (size_t)kEscBlock * kEscSlotF4 * sizeof(float4);
+        const bool pf = FSK_ESC_PREFETCH && exact_esc && smem_pf <= 227 * 1024;
+        if (pf && smem_pf > 48 * 1024)
+            cuda_check(cudaFuncSetAttribute(k_search_escalated_pf, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)smem_pf), "cudaFuncSetAttribute");
+        cuda_check(pf ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search_escalated_pf, kEscBlock, smem_pf)
+                   : exact_esc ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search_escalated<true>,
+                                                                               kEscBlock, smem64)
+                               : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search_escalated<false>,
+                                                                               kEscBlock, 0),
                    "occupancy");
         const unsigned egrid = (unsigned)(ctx->sm_count * std::max(per_sm, 1));
         // start states of up to st_cap escalated solves (~5 % escalate; the rest start in-kernel)
@@ -1450,8 +1740,12 @@ SearchState run_search(fsk_ctx* ctx, GridPlanes& P, const GridP& g, const float*
             const unsigned sgrid = (unsigned)(ctx->sm_count * std::max(1, std::min(per_sm_s, FSK_ESC_START_MINB)));
             FSK_LAUNCH(ctx, st, k_esc_start<true>, sgrid, 128, smem_s, P.p64, g, Wx, bones, n, sp, s.sp, esc_q, S,
                        esc_n, est, st_cap, ctx->stats, stash_on);
-            FSK_LAUNCH(ctx, st, k_search_escalated<true>, egrid, kEscBlock, smem64, P.p64, g, Wx, bones, n, sp, s.sp,
-                       esc_q, S, esc_n, est, st_cap, ctx->stats);
+            if (pf)
+                FSK_LAUNCH(ctx, st, k_search_escalated_pf, egrid, kEscBlock, smem_pf, P.p64, g, Wx, bones, n, sp, s.sp,
+                           esc_q, S, esc_n, est, st_cap, ctx->stats);
+            else
+                FSK_LAUNCH(ctx, st, k_search_escalated<true>, egrid, kEscBlock, smem64, P.p64, g, Wx, bones, n, sp,
+                           s.sp, esc_q, S, esc_n, est, st_cap, ctx->stats);
         } else if (esc) {  // cheap starts (transform-grid J~0): measured faster inside the refill kernel
             FSK_LAUNCH(ctx, st, k_search_escalated<false>, egrid, kEscBlock, 0, P.p64, g, nullptr, bones, n, sp, s.sp,
                        esc_q, S, esc_n, nullptr, 0, ctx->stats);
