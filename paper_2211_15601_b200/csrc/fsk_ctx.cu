@@ -157,6 +157,7 @@ SearchP make_search(const fsk_search_opts* o) {
     if (const char* v = getenv("FSK_ESC_MIN_DIV")) s.esc_min_div = atoi(v);
     if (const char* v = getenv("FSK_ESC_COS")) s.esc_cos2 = (float)(atof(v) * atof(v));
     if (const char* v = getenv("FSK_ESC_CAPCONV")) s.esc_capconv = atoi(v);
+    if (const char* v = getenv("FSK_ESC_CAP")) s.esc_cap = atoi(v);
 #endif
     return s;
 }
