@@ -445,6 +445,77 @@ __global__ void __launch_bounds__(256) k_bwd_chunk_reduce(GridP g, const int64_t
     flush(cur, s);
 }
 
+// Deterministic mode over roots in spatial order (the search's query order): k_bwd_scatter_agg's
+// walk with k_bwd_chunk_reduce's fixed-point terms — lane L < 24 owns float4 L (corner L/3, matrix
+// row L%3) of the current cell as four int64 sums and flushes them with integer atomics at each
+// cell change. Every term is computed exactly as in k_bwd_chunk_reduce and integer addition is
+// order-free, so the result is bitwise the bucketed path's, without bucketing the roots by cell
+// (count, scan, fill). Needs the max term (scale) first: k_bwd_max_term.
+#ifndef FSK_DET_ORDERED
+#define FSK_DET_ORDERED 1
+#endif
+__global__ void __launch_bounds__(256) k_bwd_fixed_agg(GridP g, RootRef R, const int32_t* __restrict__ order,
+                                                       const float* __restrict__ gx, int64_t n,
+                                                       const unsigned int* __restrict__ maxbits, int64_t n_scale,
+                                                       unsigned long long* __restrict__ acc) {
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    if (j - lane >= n) return;  // whole warp past the end
+    float xs[3] = {0.f, 0.f, 0.f}, u[3] = {0.f, 0.f, 0.f};
+    Cell<float> c{};
+    bool have = false;
+    if (j < n) {
+        have = bwd_load(R, order[j], gx, xs, u);
+        if (have) c = locate<false>(g, xs[0], xs[1], xs[2]);
+    }
+    const double scale = fixed_scale(*maxbits, n_scale);
+    const int nxy = g.nx * g.ny;
+    const int q = lane / 3, row = lane - 3 * q;
+    const int di = q & 1, dj = (q >> 1) & 1, dk = q >> 2;
+    const bool owner = lane < 24;
+    long long s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+    int cur = -1;
+    unsigned todo = __ballot_sync(0xffffffffu, have);
+    __shared__ float4 s_rec[256 / 32][32][3];
+    float4(&rec)[32][3] = s_rec[threadIdx.x >> 5];
+    rec[lane][0] = make_float4(__int_as_float(c.base), c.tx, c.ty, c.tz);
+    rec[lane][1] = make_float4(xs[0], xs[1], xs[2], u[0]);
+    rec[lane][2] = make_float4(u[1], u[2], 0.f, 0.f);
+    __syncwarp();
+    auto flush = [&]() {
+        if (cur >= 0 && owner) {
+            unsigned long long* d = acc + 12 * (int64_t)(cur + dk * nxy + dj * g.nx + di) + 4 * row;
+            if (s0) atomicAdd(d, (unsigned long long)s0);
+            if (s1) atomicAdd(d + 1, (unsigned long long)s1);
+            if (s2) atomicAdd(d + 2, (unsigned long long)s2);
+            if (s3) atomicAdd(d + 3, (unsigned long long)s3);
+        }
+        s0 = s1 = s2 = s3 = 0;
+    };
+    while (todo) {
+        const int src = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const float4 r0 = rec[src][0], r1 = rec[src][1], r2 = rec[src][2];
+        const int cj = __float_as_int(r0.x);
+        if (cj != cur) {  // warp-uniform
+            flush();
+            cur = cj;
+        }
+        if (owner) {
+            const float tx = r0.y, ty = r0.z, tz = r0.w;
+            const float ur = row == 0 ? r1.w : (row == 1 ? r2.x : r2.y);
+            // k_bwd_chunk_reduce's term, entry (row, col): φ·u_row·scale·(x_col or 1)
+            const float phi = ((dk ? tz : 1.f - tz) * (dj ? ty : 1.f - ty)) * (di ? tx : 1.f - tx);
+            const double a = (double)phi * (double)ur * scale;
+            s0 += __double2ll_rn(a * (double)r1.x);
+            s1 += __double2ll_rn(a * (double)r1.y);
+            s2 += __double2ll_rn(a * (double)r1.z);
+            s3 += __double2ll_rn(a * 1.0);
+        }
+    }
+    flush();
+}
+
 __global__ void k_bwd_fixed_to_float(const long long* __restrict__ acc, int64_t m,
                                      const unsigned int* __restrict__ maxbits, int64_t n, float* __restrict__ out) {
     const double inv = 1.0 / fixed_scale(*maxbits, n);
@@ -533,9 +604,23 @@ void run_bwd(fsk_ctx* ctx, const GridP& g, const RootRef& R, const float* grad_x
                        reinterpret_cast<float4*>(grad_tgrid));
         return;
     }
-    // deterministic: bucket the roots by cell, reduce per cell, integer atomics to vertices
     unsigned int* mx = nullptr;
-    unsigned long long* acc = det_accumulate(ctx, g, R, grad_xc, n, n, nullptr, nullptr, st, &mx);
+    unsigned long long* acc = nullptr;
+    if (FSK_DET_ORDERED && order) {  // deterministic, spatial order: max term, then per-run integer sums
+        const int64_t V4 = (V + 3) / 4 * 4;
+        const int64_t words = 2 * (12 * V4) + 8;  // int64 accumulators + the max slot, zeroed together
+        int32_t* base = (int32_t*)scratch(ctx, kBwdAcc, words * sizeof(int32_t));
+        acc = reinterpret_cast<unsigned long long*>(base);
+        mx = (unsigned int*)(base + 2 * (12 * V4));
+        FSK_LAUNCH(ctx, st, k_zero, std::min(blocks_for(words / 4, 256), cap_blocks), 256, 0,
+                   reinterpret_cast<float4*>(base), words / 4);
+        if (n > 0) {
+            FSK_LAUNCH(ctx, st, k_bwd_max_term, blocks_for(n, 256), 256, 0, R, grad_xc, n, mx);
+            FSK_LAUNCH(ctx, st, k_bwd_fixed_agg, blocks_for(n, 256), 256, 0, g, R, order, grad_xc, n, mx, n, acc);
+        }
+    } else {  // deterministic: bucket the roots by cell, reduce per cell, integer atomics to vertices
+        acc = det_accumulate(ctx, g, R, grad_xc, n, n, nullptr, nullptr, st, &mx);
+    }
     FSK_LAUNCH(ctx, st, k_bwd_fixed_to_float, std::min(blocks_for(12 * V, 256), cap_blocks), 256, 0,
                reinterpret_cast<const long long*>(acc), 12 * V, mx, n, grad_tgrid);
 }

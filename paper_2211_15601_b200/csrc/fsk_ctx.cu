@@ -158,6 +158,7 @@ SearchP make_search(const fsk_search_opts* o) {
     if (const char* v = getenv("FSK_ESC_COS")) s.esc_cos2 = (float)(atof(v) * atof(v));
     if (const char* v = getenv("FSK_ESC_CAPCONV")) s.esc_capconv = atoi(v);
     if (const char* v = getenv("FSK_ESC_CAP")) s.esc_cap = atoi(v);
+    if (const char* v = getenv("FSK_ESC_JMAX")) s.esc_jmax = (float)atof(v);
 #endif
     return s;
 }

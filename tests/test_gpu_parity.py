@@ -385,6 +385,10 @@ def test_backward_in_spatial_order_aggregates_per_warp(deformer, c3):
     scale = np.abs(a).max()
     assert np.abs(a - b).max() <= 1e-6 * scale
     assert np.abs(b - d).max() <= 1e-6 * scale
+    # deterministic mode: the spatial-order walk (k_bwd_fixed_agg) sums the same int64 terms as the
+    # bucketed path, so it is bitwise the bucketed result
+    d0 = deformer.search_bwd_roots(sc.dims, sc.bbox, sc.n_bones, roots, dev(ridx), dev(v), deterministic=True)
+    np.testing.assert_array_equal(d, d0.cpu().numpy())
     rh = roots.cpu().numpy()
     xs = rh[np.maximum(ridx, 0), :3]
     J = rh[np.maximum(ridx, 0), 4:13].reshape(-1, 3, 3)
