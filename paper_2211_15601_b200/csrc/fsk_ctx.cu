@@ -133,7 +133,9 @@ SearchP make_search(const fsk_search_opts* o) {
     s.esc_div_hi = (1.0f + 2e-4f) * (1.0f + 2e-4f);
     s.esc_det = 1e-5f;
     s.esc_den = 1e-12f;
-    s.esc_jmax = 6.0f;
+    // 6 until round 2; the round-2 band study (seeds 112-141, FMA oracle) found one 3-iteration root
+    // 1.01e-4 from the oracle's with max|J~| 5.17 — at 5 it is escalated (+0.006 % of solves on C2)
+    s.esc_jmax = 5.0f;
     s.esc_cos2 = 0.1f * 0.1f;
     // Step rule (scripts/band_study.py on the GPU, 30 scenes × 720k solves: converged solves
     // whose iteration count differed from the oracle's by one had the float32 err/conv as low
