@@ -118,7 +118,7 @@ SearchP make_search(const fsk_search_opts* o) {
     // within ±2e-4 of div^2, |det J0| < 1e-5 (vs the 1e-8 singular cut), |den| < 1e-12
     // (vs the 1e-18 Broyden guard).
     // Conditioning (scripts/escalation_rules.py, 72 scenes × 720k solves: without it
-    // max|dx| reached 4.8e-4 on 64^3 / 128x128x32 grids): a converged root with max|J~| > 6
+    // max|dx| reached 4.8e-4 on 64^3 / 128x128x32 grids): a converged root with max|J~| > 6 (5 since round 2)
     // (rounding amplified into x*), or any Broyden update with |cos(dx, J~dg)| < 0.1
     // (near-degenerate rank-one update). Bands are on err, like the emulator's:
     // |err/conv - 1| < 2 %, |err/div - 1| < 2e-4.
