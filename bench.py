@@ -173,8 +173,9 @@ def hbm_peak():
 
 def k1_line(V, nb, alg_bytes, ms):
     """K1 is HBM-bound: algorithmic bytes are the reference's (weights in, [V][12] float32 grid out); the
-    kernel moves the weights and writes the float32 and float64 x-pair gather planes (every vertex row twice)."""
-    moved = V * (4 * nb + 2 * 3 * 16 + 2 * 3 * 32)
+    kernel moves the weights, writes the [V][12] float32 grid the step asks for (`tgrid=`) and the float32
+    and float64 x-pair gather planes (every vertex row twice)."""
+    moved = V * (4 * nb + 48 + 2 * 3 * 16 + 2 * 3 * 32)
     peak, src = hbm_peak()
     return {"bytes_per_launch": alg_bytes, "moved_bytes_per_launch": moved, "avg_launch_ms": ms,
             "achieved_GBps": alg_bytes / (ms * 1e-3) / 1e9, "moved_GBps": moved / (ms * 1e-3) / 1e9,

@@ -125,6 +125,18 @@ __global__ void __launch_bounds__(256) k_precompute(const float* __restrict__ w,
 // per matrix row one 16-B (float32) / 32-B (float64) store to record v and one to record v-1 of the
 // x-pair planes — a warp's stores to a row plane cover one contiguous span. Bones staged in shared
 // memory (float32 and float64 copies).
+#ifndef FSK_K1_WIDE
+#define FSK_K1_WIDE 1
+#endif
+__device__ __forceinline__ void st_v8f32(float* p, const float4& a, const float4& b) {
+    asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(a.x), "f"(a.y), "f"(a.z),
+                 "f"(a.w), "f"(b.x), "f"(b.y), "f"(b.z), "f"(b.w)
+                 : "memory");
+}
+__device__ __forceinline__ void st_v4f64(double* p, double a, double b, double c, double d) {
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+
 __global__ void __launch_bounds__(128) k_precompute_v(const float* __restrict__ w, const float* __restrict__ bones,
                                                      int nb, int nx, int64_t V, float4* __restrict__ tg,
                                                      float* __restrict__ p32, double* __restrict__ p64,
@@ -133,7 +145,13 @@ __global__ void __launch_bounds__(128) k_precompute_v(const float* __restrict__ 
     for (int e = threadIdx.x; e < nb * 12; e += blockDim.x) sB[e] = bones[e];
     __syncthreads();
     const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+#if FSK_K1_WIDE
+    if (v - (threadIdx.x & 31) >= V) return;  // whole warp past the end (the stores below shuffle)
+    const bool valid = v < V;
+#else
     if (v >= V) return;
+    const bool valid = true;
+#endif
     const float* wv = w + v * nb;
     float T[12];
     double D[12];
@@ -151,22 +169,64 @@ __global__ void __launch_bounds__(128) k_precompute_v(const float* __restrict__ 
 #pragma unroll
             for (int e = 0; e < 12; ++e) D[e] = __fma_rn((double)wi, (double)Bi[e], D[e]);
     };
-    if ((nb & 3) == 0) {
-        for (int i = 0; i < nb; i += 4) {
-            const float4 q = __ldg(reinterpret_cast<const float4*>(wv + i));
-            bone(i, q.x);
-            bone(i + 1, q.y);
-            bone(i + 2, q.z);
-            bone(i + 3, q.w);
+    if (valid) {
+        if ((nb & 3) == 0) {
+            for (int i = 0; i < nb; i += 4) {
+                const float4 q = __ldg(reinterpret_cast<const float4*>(wv + i));
+                bone(i, q.x);
+                bone(i + 1, q.y);
+                bone(i + 2, q.z);
+                bone(i + 3, q.w);
+            }
+        } else {
+            for (int i = 0; i < nb; ++i) bone(i, __ldg(wv + i));
         }
-    } else {
-        for (int i = 0; i < nb; ++i) bone(i, __ldg(wv + i));
     }
     const bool has_left = (v % nx) != 0;
-    if (tg)
+    if (tg && valid)
 #pragma unroll
         for (int r = 0; r < 3; ++r) tg[3 * v + r] = make_float4(T[4 * r], T[4 * r + 1], T[4 * r + 2], T[4 * r + 3]);
     const int64_t stride = 8 * V;
+#if FSK_K1_WIDE
+    // x-pair rows written whole by their owner: pair v = {row r of T_v, row r of T_{v+1}} in one
+    // 32-B (float32) / 2 × 32-B (float64) store per row, T_{v+1} from the next lane; lane 31 writes
+    // the first half only and lane 0 of the next warp the second half (its own row) — the same
+    // bytes as the per-half stores, in full sectors.
+    const int lane = threadIdx.x & 31;
+    const bool has_right = v + 1 < V && ((v + 1) % nx) != 0;
+    const bool whole = lane < 31 && has_right;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        if (p32) {
+            const float4 own = make_float4(T[4 * r], T[4 * r + 1], T[4 * r + 2], T[4 * r + 3]);
+            float4 nxt;
+            nxt.x = __shfl_down_sync(0xffffffffu, own.x, 1);
+            nxt.y = __shfl_down_sync(0xffffffffu, own.y, 1);
+            nxt.z = __shfl_down_sync(0xffffffffu, own.z, 1);
+            nxt.w = __shfl_down_sync(0xffffffffu, own.w, 1);
+            float* row = p32 + r * stride + 8 * v;
+            if (valid) {
+                if (whole) st_v8f32(row, own, nxt);
+                else *reinterpret_cast<float4*>(row) = own;
+                if (lane == 0 && has_left) *reinterpret_cast<float4*>(row - 4) = own;
+            }
+        }
+        if (p64) {
+            double nxt[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) nxt[e] = __shfl_down_sync(0xffffffffu, D[4 * r + e], 1);
+            double* row = p64 + r * stride + 8 * v;
+            if (valid) {
+                st_v4f64(row, D[4 * r], D[4 * r + 1], D[4 * r + 2], D[4 * r + 3]);
+                if (whole) st_v4f64(row + 4, nxt[0], nxt[1], nxt[2], nxt[3]);
+                if (lane == 0 && has_left) st_v4f64(row - 4, D[4 * r], D[4 * r + 1], D[4 * r + 2], D[4 * r + 3]);
+            }
+        }
+        if (tg64 && valid)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) tg64[12 * v + 4 * r + e] = D[4 * r + e];
+    }
+#else
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
         if (p32) {
@@ -189,6 +249,7 @@ __global__ void __launch_bounds__(128) k_precompute_v(const float* __restrict__ 
 #pragma unroll
             for (int e = 0; e < 4; ++e) tg64[12 * v + 4 * r + e] = D[4 * r + e];
     }
+#endif
 }
 
 // Relayout of a caller-provided [V][12] grid (float32, or float64 when tg64 != null) into
