@@ -450,9 +450,9 @@ __global__ void __launch_bounds__(256) k_bwd_chunk_reduce(GridP g, const int64_t
 // row L%3) of the current cell as four int64 sums and flushes them with integer atomics at each
 // cell change. Every term is computed exactly as in k_bwd_chunk_reduce and integer addition is
 // order-free, so the result is bitwise the bucketed path's, without bucketing the roots by cell
-// (count, scan, fill). Needs the max term (scale) first: k_bwd_max_term.
+// (count, scan, fill). Needs the max term (scale) first: k_bwd_max_term. Ablation (off by default).
 #ifndef FSK_DET_ORDERED
-#define FSK_DET_ORDERED 1
+#define FSK_DET_ORDERED 0  // measured slower on C3 det: 86 us for this kernel vs 86 us for count + fill + chunk reduce (four int64 atomics per lane per run, shorter runs than whole buckets)
 #endif
 __global__ void __launch_bounds__(256) k_bwd_fixed_agg(GridP g, RootRef R, const int32_t* __restrict__ order,
                                                        const float* __restrict__ gx, int64_t n,
