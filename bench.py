@@ -602,7 +602,9 @@ def e2e_ours(D, sc, opts, args, steps=None, world=1, roots_hint=None):
     frame f+1's upload and search overlap frame f's download). Also reported: one synchronous
     fsk_deform_host call per step (no cross-frame overlap)."""
     import torch
-    steps = steps or max(3, min(args.steps, 20))
+    # 20 frames per call whatever --steps is (one call's first upload and last download are not
+    # overlapped; over 20 frames they are a few per cent of the call)
+    steps = steps or 20
     n, nb = sc.points.shape[0], sc.n_bones
     hw = torch.from_numpy(sc.weights).pin_memory()
     hb = torch.from_numpy(sc.bones).pin_memory()

@@ -183,10 +183,10 @@ __global__ void __launch_bounds__(128) k_precompute_v(const float* __restrict__ 
         }
     }
     const bool has_left = (v % nx) != 0;
-    if (tg && valid)
+    const int64_t stride = 8 * V;
+    if (tg && valid)  // (staging these rows through shared memory for full-line stores measured no faster)
 #pragma unroll
         for (int r = 0; r < 3; ++r) tg[3 * v + r] = make_float4(T[4 * r], T[4 * r + 1], T[4 * r + 2], T[4 * r + 3]);
-    const int64_t stride = 8 * V;
 #if FSK_K1_WIDE
     // x-pair rows written whole by their owner: pair v = {row r of T_v, row r of T_{v+1}} in one
     // 32-B (float32) / 2 × 32-B (float64) store per row, T_{v+1} from the next lane; lane 31 writes
