@@ -252,8 +252,12 @@ struct MlpRows {
 };
 
 constexpr int kTile = 128;
-constexpr int kThreads = 256;            // two warps per TMEM lane quarter: each owns half the columns
+#ifndef FSK_MLP_THREADS
+#define FSK_MLP_THREADS 256  // kSplit warps per TMEM lane quarter, each owning H / kSplit columns of every layer
+#endif
+constexpr int kThreads = FSK_MLP_THREADS;
 constexpr int kSplit = kThreads / kTile;
+static_assert(kSplit == 2 || kSplit == 4, "MLP CTA: 256 or 512 threads");
 
 __device__ __forceinline__ void row_input(const MlpRows& R, int64_t r, float* x) {
     if (R.source == kRowsGrid) {
@@ -311,10 +315,10 @@ __global__ void __launch_bounds__(kThreads, H == 64 ? 2 : 1)  // H = 64: two CTA
     const int tid = threadIdx.x, warp = tid >> 5;
     // warp w reads/writes TMEM lanes [32 (w % 4), +32) (tcgen05 lane-quarter rule) and the
     // column half w / 4 of every layer; tile row = its TMEM lane
-    const int quarter = warp & 3, half = warp >> 2;
+    const int quarter = warp & 3, half = warp >> 2;  // half: the warp's column part (0 .. kSplit-1)
     const int trow = quarter * 32 + (tid & 31);
     constexpr int HC = H / kSplit;  // columns per thread
-    __shared__ float s_logit[kTile];
+    __shared__ float s_logit[kSplit - 1][kTile];
     const uint32_t b_mma = smem_u32(&bar_mma), b_w = smem_u32(&bar_w);
 
     for (int i = tid; i < H * m.K0; i += kThreads) s_w0[i] = pk[m.off_W0 + i];
@@ -507,13 +511,17 @@ __global__ void __launch_bounds__(kThreads, H == 64 ? 2 : 1)  // H = 64: two CTA
                 }
             }
         }
-        if (!m.softmax && half == 1) s_logit[trow] = logit;  // partial over the upper columns
+        if (!m.softmax && half > 0) s_logit[half - 1][trow] = logit;  // partials over the upper column parts
         tmem_wait_st();
         tc_fence_before();
         __syncthreads();  // TMEM A/D reuse by the next tile
         tc_fence_after();
-        if (!m.softmax && half == 0 && row < R.n)  // OccupancyMlp (shape.cpp:208-228)
-            out[row] = sigmoid_f(logit + s_logit[trow] + s_headv[H]);
+        if (!m.softmax && half == 0 && row < R.n) {  // OccupancyMlp (shape.cpp:208-228)
+            float z = logit;
+#pragma unroll
+            for (int p = 0; p < kSplit - 1; ++p) z += s_logit[p][trow];
+            out[row] = sigmoid_f(z + s_headv[H]);
+        }
     }
     if (kStream && tid == 0 && !w_ready) mbar_wait(b_w, ph_w);  // drain the last prefetch
     tc_fence_before();
