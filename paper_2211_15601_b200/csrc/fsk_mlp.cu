@@ -291,8 +291,9 @@ __device__ __forceinline__ float act_fwd(float z, bool tangent, int role) {
     return role == 0 ? sp : sv * z;
 }
 
-// One 128-row tile per iteration of a persistent CTA (128 threads; thread t owns TMEM lane t =
-// tile row t). TMEM columns: D [0, H), A_hi [H, 2H), A_lo [2H, 3H).
+// One 128-row tile per iteration of a persistent CTA (kThreads threads: lane l of warp w owns TMEM
+// lane 32·(w % 4) + l = tile row, and column part w / 4 of every layer). TMEM columns: D [0, H),
+// A_hi [H, 2H), A_lo [2H, 3H).
 // act (optional, for the backward): x [n][4] then the softplus outputs h_l [(n_hidden+1)][n][H].
 template <int H, bool kStream, bool kTangent>
 __global__ void __launch_bounds__(kThreads, H == 64 ? 2 : 1)  // H = 64: two CTAs per SM (256 TMEM columns each)
