@@ -259,6 +259,10 @@ int fsk_ctx_create(int device, fsk_ctx** out) {
         auto* c = new fsk_ctx();
         c->device = device;
         c->sm_count = prop.multiProcessorCount;
+#ifdef FSK_L2_PERSIST_STUDY  // study builds: L2 set-aside for evict_last lines (FSK_L2_PERSIST_MB)
+        if (const char* e = getenv("FSK_L2_PERSIST_MB"))
+            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)atoll(e) << 20);
+#endif
         if (cudaMalloc(&c->stats, fsk_ctx::kStatSlots * sizeof(unsigned long long)) != cudaSuccess ||
             cudaMemset(c->stats, 0, fsk_ctx::kStatSlots * sizeof(unsigned long long)) != cudaSuccess ||
             cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
