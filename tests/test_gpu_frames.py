@@ -142,3 +142,29 @@ def test_graph_replayed_items_equal_eager(deformer, monkeypatch, chunks):
         for f in range(len(frames)):
             np.testing.assert_array_equal(offs[f], ref[1][f])
             np.testing.assert_array_equal(roots[f], ref[2][f])
+
+
+def test_graph_cache_eviction_keeps_results(deformer, monkeypatch):
+    """More distinct chunk shapes than the context caches graphs for (8): every shape is seen twice per
+    call sequence, so graphs are captured, evicted (least recently used) and re-captured; results stay
+    equal to the eager pipeline."""
+    sizes = [3000 + 500 * i for i in range(10)]
+    base, frames = _frames(sizes)
+    hw = torch.from_numpy(base.weights).pin_memory()
+    o = _opts(base)
+
+    def run(f):
+        b, p = frames[f]
+        offs = torch.empty(p.shape[0] + 1, dtype=torch.int64).pin_memory()
+        roots = torch.zeros((p.shape[0] * 3, 16), dtype=torch.float32).pin_memory()
+        t = deformer.deform_host(hw, base.dims, base.bbox, b, p, o, offs, roots)
+        return offs.numpy().copy(), roots[:t].numpy().view(np.uint32).copy()
+
+    monkeypatch.setenv("FSK_PIPE_GRAPH", "0")
+    ref = [run(f) for f in range(len(frames))]
+    monkeypatch.setenv("FSK_PIPE_GRAPH", "1")
+    for _ in range(3):
+        for f in list(range(len(frames))) + list(range(len(frames)))[::-1]:
+            offs, roots = run(f)
+            np.testing.assert_array_equal(offs, ref[f][0])
+            np.testing.assert_array_equal(roots, ref[f][1])
