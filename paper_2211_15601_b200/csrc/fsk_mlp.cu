@@ -445,12 +445,14 @@ __global__ void __launch_bounds__(kThreads, H == 64 ? 2 : 1)  // H = 64: two CTA
             mbar_wait(b_mma, ph_mma);
             ph_mma ^= 1;
             tc_fence_after();
+#ifndef FSK_MLP_PROBE_NO_STREAM  // timing probe only (wrong results): every layer reuses the first layer's weights
             if (!head && kStream) {
                 // the MMAs have read this layer's weights: stream the next hidden layer's
                 // (the first hidden layer again after the last), overlapping this epilogue
                 if (tid == 0) load_hidden(l + 1 < m.n_hidden ? l + 1 : 0, 0);
                 w_ready = false;
             }
+#endif
             if (head && half == 0) {  // softmax head (SkinningMlp::weights_batch, skinning.cpp:47-51)
                 float z[64];
 #pragma unroll
