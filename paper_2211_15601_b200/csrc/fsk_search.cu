@@ -1082,20 +1082,19 @@ __global__ void __launch_bounds__(128) k_search_exact(Planes<double> P, GridP g,
 }
 
 // ============================================================================ dedup
-// dedup_roots over each query's converged inits in bone order: a root is kept iff
-// ||x − k|| >= dedup_dist for every already-kept k (strict '<' drops; :162-176).
-// One thread per sorted query; all loads of a warp are coalesced rows of the planes.
-__global__ void __launch_bounds__(256) k_dedup(int64_t n, int nb, float dedup2, SearchPlanes sp,
-                                               const int* __restrict__ perm, int32_t* __restrict__ n_roots_p) {
-    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (j >= n) return;
-    // The first kRegKept kept roots stay in registers (a query has ~1 root); later kept roots
-    // are re-read from the planes. Loads are issued kBatch bones at a time (independent
-    // coalesced rows of the bone-major planes); converged = sign bit of the residual clear.
 #ifndef FSK_DEDUP_BATCH
 #define FSK_DEDUP_BATCH 6  // plane rows in flight per batch: 24 35 us, 12 30, 8 28, 6 26, 4 26 (C2; fewer registers, more warps)
 #endif
-    constexpr int kRegKept = 4, kBatch = FSK_DEDUP_BATCH;
+// One query's dedup. kStaged: the query's n_b plane rows were bulk-copied to shared memory
+// (row b at srow[b * kDedupTile]); else they are loaded from the planes kBatch bones at a time.
+template <bool kStaged>
+__device__ __forceinline__ void dedup_query(int64_t j, int64_t n, int nb, float dedup2, const SearchPlanes& sp,
+                                            const int* __restrict__ perm, int32_t* __restrict__ n_roots_p,
+                                            const float4* srow = nullptr) {
+    // The first kRegKept kept roots stay in registers (a query has ~1 root); later kept roots
+    // are re-read from the planes. Converged = sign bit of the residual clear.
+    constexpr int kRegKept = 4, kBatch = kStaged ? 1 : FSK_DEDUP_BATCH;
+    constexpr int kStride = 128;  // kDedupTile
     float kx[kRegKept], ky[kRegKept], kz[kRegKept];
 #pragma unroll
     for (int c = 0; c < kRegKept; ++c) kx[c] = ky[c] = kz[c] = 0.f;
@@ -1105,7 +1104,7 @@ __global__ void __launch_bounds__(256) k_dedup(int64_t n, int nb, float dedup2, 
         float4 xv[kBatch];
 #pragma unroll
         for (int i = 0; i < kBatch; ++i)
-            if (b0 + i < nb) xv[i] = __ldcs(sp.xr + (int64_t)(b0 + i) * n + j);
+            if (b0 + i < nb) xv[i] = kStaged ? srow[(b0 + i) * kStride] : __ldcs(sp.xr + (int64_t)(b0 + i) * n + j);
 #pragma unroll
         for (int i = 0; i < kBatch; ++i) {
             const int b = b0 + i;
@@ -1146,6 +1145,70 @@ __global__ void __launch_bounds__(256) k_dedup(int64_t n, int nb, float dedup2, 
     }
     if (sp.kmask) sp.kmask[j] = kept;
     n_roots_p[perm[j]] = count;
+}
+
+// dedup_roots over each query's converged inits in bone order: a root is kept iff
+// ||x − k|| >= dedup_dist for every already-kept k (strict '<' drops; :162-176).
+// One thread per sorted query; all loads of a warp are coalesced rows of the planes.
+__global__ void __launch_bounds__(256) k_dedup(int64_t n, int nb, float dedup2, SearchPlanes sp,
+                                               const int* __restrict__ perm, int32_t* __restrict__ n_roots_p) {
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    dedup_query<false>(j, n, nb, dedup2, sp, perm, n_roots_p);
+}
+
+// The same with the block's n_b plane rows (128 queries × 16 B each) brought into shared memory by
+// n_b TMA bulk copies (cp.async.bulk, one mbarrier): long DRAM bursts instead of 24 interleaved
+// 512-B streams per warp. Ablation (off by default).
+#ifndef FSK_DEDUP_BULK
+#define FSK_DEDUP_BULK 0  // measured slower on C2: 36.0 us vs 26.3 for k_dedup (outputs bitwise equal)
+#endif
+constexpr int kDedupTile = 128;
+__device__ __forceinline__ uint32_t sm_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__global__ void __launch_bounds__(kDedupTile) k_dedup_bulk(int64_t n, int nb, float dedup2, SearchPlanes sp,
+                                                          const int* __restrict__ perm,
+                                                          int32_t* __restrict__ n_roots_p) {
+    extern __shared__ __align__(16) float4 s_rows[];  // [nb][kDedupTile]
+    __shared__ __align__(8) uint64_t bar;
+    const int64_t j0 = blockIdx.x * (int64_t)kDedupTile;
+    const int cnt = (int)min((int64_t)kDedupTile, n - j0);
+    const uint32_t b = sm_u32(&bar);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t bytes = (uint32_t)cnt * 16u;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes * (uint32_t)nb)
+                     : "memory");
+        for (int r = 0; r < nb; ++r)
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    sm_u32(s_rows + r * kDedupTile)),
+                "l"(sp.xr + (int64_t)r * n + j0), "r"(bytes), "r"(b)
+                : "memory");
+    }
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}" ::"r"(b)
+        : "memory");
+    if ((int)threadIdx.x < cnt) dedup_query<true>(j0 + threadIdx.x, n, nb, dedup2, sp, perm, n_roots_p, s_rows + threadIdx.x);
+}
+
+void launch_dedup(fsk_ctx* ctx, cudaStream_t st, int64_t n, int nb, float dedup2, const SearchPlanes& sp,
+                  const int* perm, int32_t* n_roots) {
+    const size_t smem = (size_t)nb * kDedupTile * sizeof(float4);
+    if (FSK_DEDUP_BULK && n > 0 && smem <= 96 * 1024) {
+        // (the static mbarrier counts against the 48 KB default too: always raise the limit)
+        cuda_check(cudaFuncSetAttribute(k_dedup_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024),
+                   "cudaFuncSetAttribute");
+        FSK_LAUNCH(ctx, st, k_dedup_bulk, blocks_for(n, kDedupTile), kDedupTile, smem, n, nb, dedup2, sp, perm, n_roots);
+    } else {
+        FSK_LAUNCH(ctx, st, k_dedup, blocks_for(n, 256), 256, 0, n, nb, dedup2, sp, perm, n_roots);
+    }
 }
 
 // ============================================================================ scan (int32 -> int64 exclusive)
@@ -1812,7 +1875,7 @@ SearchState run_search(fsk_ctx* ctx, GridPlanes& P, const GridP& g, const float*
                        esc_q, S, esc_n, nullptr, 0, ctx->stats);
         }
     }
-    FSK_LAUNCH(ctx, st, k_dedup, blocks_for(n, 256), 256, 0, n, g.nb, (float)sp.dedup2, s.sp, s.perm, s.n_roots_p);
+    launch_dedup(ctx, st, n, g.nb, (float)sp.dedup2, s.sp, s.perm, s.n_roots_p);
     return s;
 }
 
@@ -2427,7 +2490,7 @@ int fsk_search_fwd_mlp(fsk_ctx* ctx, const float* theta, const int32_t* widths, 
                        w, ss.sp, mv, cnt + nxt, act[nxt], pos[nxt]);
             cur = nxt;
         }
-        FSK_LAUNCH(ctx, st, k_dedup, blocks_for(n, 256), 256, 0, n, nb, (float)sp.dedup2, ss.sp, ss.perm, ss.n_roots_p);
+        launch_dedup(ctx, st, n, nb, (float)sp.dedup2, ss.sp, ss.perm, ss.n_roots_p);
         DenseOut d{out->x_c64, out->x_c, out->jinv, out->resid, out->iters, out->converged, out->keep, out->n_roots};
         FSK_LAUNCH(ctx, st, k_scatter_dense, blocks_for(S, 256), 256, 0, n, nb, ss.sp, ss.perm, d);
         if (out->n_roots)
