@@ -297,6 +297,7 @@ int fsk_ctx_destroy(fsk_ctx* ctx) {
         for (auto& pg : ctx->pipe_graphs)
             if (pg.exec) cudaGraphExecDestroy(pg.exec);
         if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
+        if (ctx->pre) cudaStreamDestroy(ctx->pre);
         delete ctx;
     });
 }

@@ -20,7 +20,7 @@ struct fsk_ctx {
     int device = 0;
     int sm_count = 0;
     int64_t launches = 0;
-    static constexpr int kSlots = 64;
+    static constexpr int kSlots = 80;
     void* buf[kSlots] = {};
     size_t cap[kSlots] = {};
     // optional per-launch CUDA-event profiling (bench.py reads per-kernel device time)
@@ -59,6 +59,7 @@ struct fsk_ctx {
     std::vector<PipeGraph> pipe_graphs;
     uint64_t pipe_clock = 0;
     cudaStream_t cap_stream = nullptr;  // capture stream (the caller's may be the legacy default stream)
+    cudaStream_t pre = nullptr;  // host pipeline: sort + K1 of the next item, beside the current item's search
 };
 
 namespace fsk {
@@ -71,6 +72,8 @@ enum Slot {
     kHW, kHB, kHP, kHT, kHOffs, kHRoots, kFB, kFP, kFOffs, kFRoots,
     kMlpPack, kMlpWidths, kMlpOcc, kMlpAct, kMlpD0, kMlpD1, kMlpOnes,
     kMvPos, kMvPosNext, kMvW, kMvX, kMvG, kMvJ, kMvDx, kMvK, kMvAct, kMvActNext, kMvCnt,
+    // second copies of the sort / K1 scratch: the host pipeline stages item i+1 while item i searches
+    kHistB, kKeysB, kPermB, kXsB, kEscNB, kPlanesB, kPlanes64B,
     kSlotCount
 };
 static_assert(kSlotCount <= fsk_ctx::kSlots, "scratch slots");

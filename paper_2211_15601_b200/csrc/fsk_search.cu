@@ -27,6 +27,7 @@
 #include <cooperative_groups.h>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 
 #include "fsk_ctx.h"
 #include "fsk_exact.cuh"
@@ -1658,12 +1659,27 @@ struct GridPlanes {
     Planes<double> p64;
 };
 
-GridPlanes planes_scratch(fsk_ctx* ctx, const GridP& g) {
+// scratch of the sort / K1 stage: slot 1 is the second copy the host pipeline stages into
+int sslot(int base, int slot) {
+    if (!slot) return base;
+    switch (base) {
+        case kHist: return kHistB;
+        case kKeys: return kKeysB;
+        case kPerm: return kPermB;
+        case kXs: return kXsB;
+        case kEscN: return kEscNB;
+        case kPlanes: return kPlanesB;
+        case kPlanes64: return kPlanes64B;
+        default: return base;
+    }
+}
+
+GridPlanes planes_scratch(fsk_ctx* ctx, const GridP& g, int slot = 0) {
     const int64_t V = vertex_count(g);
     GridPlanes P;
-    P.p32.p = (const float*)scratch(ctx, kPlanes, 3 * V * 8 * sizeof(float));
+    P.p32.p = (const float*)scratch(ctx, sslot(kPlanes, slot), 3 * V * 8 * sizeof(float));
     P.p32.stride = V * 8;
-    P.p64.p = (const double*)scratch(ctx, kPlanes64, 3 * V * 8 * sizeof(double));
+    P.p64.p = (const double*)scratch(ctx, sslot(kPlanes64, slot), 3 * V * 8 * sizeof(double));
     P.p64.stride = V * 8;
     return P;
 }
@@ -1672,9 +1688,9 @@ bool needs_f64(int flags) { return !(flags & FSK_SEARCH_FP32_ONLY); }
 
 // K1: tg / tg64 outputs optional; planes in both precisions when `planes`.
 GridPlanes run_precompute(fsk_ctx* ctx, const float* w, const GridP& g, const float* bones, float* tg, double* tg64,
-                          bool planes, bool f64, cudaStream_t st) {
+                          bool planes, bool f64, cudaStream_t st, int slot = 0) {
     const int64_t V = vertex_count(g);
-    GridPlanes P = planes_scratch(ctx, g);
+    GridPlanes P = planes_scratch(ctx, g, slot);
 #ifdef FSK_K1_V1
     FSK_LAUNCH(ctx, st, k_precompute, blocks_for(3 * V, 256), 256, g.nb * 12 * sizeof(float), w, bones, g.nb, g.nx, V,
                reinterpret_cast<float4*>(tg), planes ? (float*)P.p32.p : nullptr,
@@ -1730,9 +1746,12 @@ void sort_fused(fsk_ctx* ctx, cudaStream_t st, const float* pts, int64_t n, int*
     after_launch(ctx, "k_sort_fused");
 }
 
+// mode: the whole search (kRunFull), only its sort + K1 stage into the given scratch slot (kRunStage),
+// or everything after a stage already done into that slot (kRunAfterStage: P = the slot's planes)
+enum { kRunFull = 0, kRunStage = 1, kRunAfterStage = 2 };
 SearchState run_search(fsk_ctx* ctx, GridPlanes& P, const GridP& g, const float* weights, const float* bones,
                        const float* pts, int64_t n, const SearchP& sp, int flags, cudaStream_t st,
-                       const PrecomputeReq* pre = nullptr, bool want_x64 = false) {
+                       const PrecomputeReq* pre = nullptr, bool want_x64 = false, int mode = kRunFull, int slot = 0) {
     if ((flags & FSK_SEARCH_EXACT64) && !weights)
         fail(FSK_EINVAL, "fsk: FSK_SEARCH_EXACT64 needs the weight grid (J~0 from the skinning weights)");
     // the exact replay reads the weight grid and float64 copies of the bones (shared memory)
@@ -1744,8 +1763,13 @@ SearchState run_search(fsk_ctx* ctx, GridPlanes& P, const GridP& g, const float*
     const int64_t S = std::max<int64_t>(1, n * g.nb);
     SearchState s;
     auto precompute = [&] {
-        if (pre) P = run_precompute(ctx, pre->w, g, pre->bones, pre->tg, nullptr, true, pre->f64, st);
+        if (pre && mode != kRunAfterStage)
+            P = run_precompute(ctx, pre->w, g, pre->bones, pre->tg, nullptr, true, pre->f64, st, slot);
     };
+    if (mode == kRunStage) {  // sort + K1 only (the search scratch belongs to the item searching meanwhile)
+        s.perm = (int*)scratch(ctx, sslot(kPerm, slot), std::max<int64_t>(1, n) * sizeof(int));
+        s.n_roots_p = nullptr;
+    } else {
     s.sp.xr = (float4*)scratch(ctx, kOXr, S * sizeof(float4));
     s.sp.ja = (float4*)scratch(ctx, kOJa, S * sizeof(float4));
     s.sp.jb = (float4*)scratch(ctx, kOJb, S * sizeof(float4));
@@ -1754,21 +1778,25 @@ SearchState run_search(fsk_ctx* ctx, GridPlanes& P, const GridP& g, const float*
     s.sp.keep = (uint8_t*)scratch(ctx, kOKeep, S);
     s.sp.kmask = g.nb <= 32 ? (uint32_t*)scratch(ctx, kOKeepMask, std::max<int64_t>(1, n) * sizeof(uint32_t)) : nullptr;
     s.sp.xd = want_x64 ? (double*)scratch(ctx, kOXd, S * 3 * sizeof(double)) : nullptr;
-    s.perm = (int*)scratch(ctx, kPerm, std::max<int64_t>(1, n) * sizeof(int));
-    ctx->last_search_n = n;
+    s.perm = (int*)scratch(ctx, sslot(kPerm, slot), std::max<int64_t>(1, n) * sizeof(int));
+    if (slot == 0) ctx->last_search_n = n;  // fsk_ctx_query_order reads slot 0
     s.n_roots_p = (int32_t*)scratch(ctx, kNRoots, std::max<int64_t>(1, n) * sizeof(int32_t));
+    }
     if (n == 0) {
         precompute();
         return s;
     }
-    float4* xs = (float4*)scratch(ctx, kXs, n * sizeof(float4));
-    int* esc_n = (int*)scratch(ctx, kEscN, 4 * sizeof(int));  // {-, work cursor, short count, long count}
+    float4* xs = (float4*)scratch(ctx, sslot(kXs, slot), n * sizeof(float4));
+    int* esc_n = (int*)scratch(ctx, sslot(kEscN, slot), 4 * sizeof(int));  // {-, work cursor, short count, long count}
     // (with the spatial sort, the counters live in the sort state and are zeroed with it)
-    if (!(flags & FSK_SEARCH_NO_SORT)) {
-        int* hist = (int*)scratch(ctx, kHist, kSortStateInts * sizeof(int));
+    if (mode == kRunAfterStage) {
+        if (!(flags & FSK_SEARCH_NO_SORT))
+            esc_n = (int*)scratch(ctx, sslot(kHist, slot), kSortStateInts * sizeof(int)) + kEscOff;
+    } else if (!(flags & FSK_SEARCH_NO_SORT)) {
+        int* hist = (int*)scratch(ctx, sslot(kHist, slot), kSortStateInts * sizeof(int));
         unsigned* bbox = (unsigned*)(hist + kBboxOff);
         esc_n = hist + kEscOff;  // zeroed with the histogram
-        uint16_t* keys = (uint16_t*)scratch(ctx, kKeys, n * sizeof(uint16_t));
+        uint16_t* keys = (uint16_t*)scratch(ctx, sslot(kKeys, slot), n * sizeof(uint16_t));
         cudaStream_t ss = st;
         if (pre) {  // fork: the sort on the side stream, K1 on st
             cuda_check(cudaEventRecord(ctx->ev_fork, st), "cudaEventRecord");
@@ -1794,6 +1822,7 @@ SearchState run_search(fsk_ctx* ctx, GridPlanes& P, const GridP& g, const float*
         precompute();
         FSK_LAUNCH(ctx, st, k_identity_order, blocks_for(n, 256), 256, 0, pts, n, s.perm, xs, esc_n);
     }
+    if (mode == kRunStage) return s;
     if (flags & FSK_SEARCH_EXACT64) {
         const int bpb = (int)blocks_for(n, 128);
         const int64_t nblocks = (int64_t)bpb * g.nb;
@@ -2184,6 +2213,7 @@ void deform_host_pipeline(fsk_ctx* ctx, const float* weights, const GridP& g, in
         std::vector<cudaEvent_t>* ev;
         ~Cleanup() {
             cudaStreamSynchronize(ctx->upload);
+            if (ctx->pre) cudaStreamSynchronize(ctx->pre);
             cudaStreamSynchronize(st);
             cudaStreamSynchronize(ctx->copy);
             for (auto e : *ev)
@@ -2205,54 +2235,67 @@ void deform_host_pipeline(fsk_ctx* ctx, const float* weights, const GridP& g, in
     auto slot_o = [&](int i) { return dOff + (i & 1) * (cmax + 1); };
     auto slot_r = [&](int i) { return dR + (i & 1) * slotcap; };
     GridPlanes P;  // the current frame's gather planes (K1 runs with the frame's first chunk)
-    auto search_eager = [&](int i, fsk_root* out, int64_t cap, cudaStream_t s_) {
+    // Staged pipeline (default with the spatial sort): item i's sort + K1 (its "stage") run on ctx->pre into
+    // scratch slot i & 1 while item i-1 is still searching on st, and item i's search starts from the staged
+    // slot — the sort and K1 leave the critical path. FSK_PIPE_STAGE=0 (or FSK_SEARCH_NO_SORT): each item
+    // whole on st, K1 once per frame (the fsk_deform order).
+    const bool staged = !(flags & FSK_SEARCH_NO_SORT) && [] {
+        const char* e = getenv("FSK_PIPE_STAGE");
+        return !(e && e[0] == '0');
+    }();
+    if (staged && !ctx->pre) cuda_check(cudaStreamCreateWithFlags(&ctx->pre, cudaStreamNonBlocking), "cudaStreamCreate");
+    GridPlanes Ps[2];  // the staged slots' gather planes
+    auto body_full = [&](int i, fsk_root* out, int64_t cap, cudaStream_t s_) {
         const Item& it = items[i];
         const PrecomputeReq pre{dW, slot_b(i), nullptr, needs_f64(flags)};
         const SearchState s =
             run_search(ctx, P, g, dW, slot_b(i), slot_p(i), it.m, sp, flags, s_, it.first ? &pre : nullptr);
         compact(ctx, s, it.m, nb, slot_o(i), out, cap, s_);
     };
-    // A chunk's device work (K1 on a frame's first chunk, sort, search, escalation, dedup, scan,
-    // emit: ~20 launches) is replayed from a CUDA graph once the same launch set has been seen
-    // before — same slot buffers, chunk size, options and scratch generation (a scratch regrow
-    // frees buffers the graph points into, so it changes the key). First sight runs eagerly
-    // (warms the scratch sizes), the second captures. FSK_PIPE_GRAPH=0 turns it off.
+    auto body_stage = [&](int i, cudaStream_t s_) {
+        const PrecomputeReq pre{dW, slot_b(i), nullptr, needs_f64(flags)};
+        run_search(ctx, Ps[i & 1], g, dW, slot_b(i), slot_p(i), items[i].m, sp, flags, s_, &pre, false, kRunStage,
+                   i & 1);
+    };
+    auto body_search = [&](int i, fsk_root* out, int64_t cap, cudaStream_t s_) {
+        const SearchState s = run_search(ctx, Ps[i & 1], g, dW, slot_b(i), slot_p(i), items[i].m, sp, flags, s_,
+                                         nullptr, false, kRunAfterStage, i & 1);
+        compact(ctx, s, items[i].m, nb, slot_o(i), out, cap, s_);
+    };
+    // Each item's device work is replayed from a CUDA graph once the same launch set has been seen before —
+    // same slot buffers, chunk size, options and scratch generation (a scratch regrow frees buffers a graph
+    // points into, so it changes the key). First sight runs eagerly (warms the scratch sizes), the second
+    // captures. FSK_PIPE_GRAPH=0 turns it off.
     const bool graphs_on = [] {
         const char* e = getenv("FSK_PIPE_GRAPH");
         return !(e && e[0] == '0');
     }();
     static_assert(sizeof(GridPlanes) <= sizeof(fsk_ctx::PipeGraph::planes), "planes record");
-    auto search_item = [&](int i, fsk_root* out, int64_t cap) {
-        const Item& it = items[i];
-        if (!graphs_on || ctx->prof_on) return search_eager(i, out, cap, st);
-        std::vector<unsigned char> key;
-        auto put = [&](const void* p, size_t b) {
-            key.insert(key.end(), (const unsigned char*)p, (const unsigned char*)p + b);
+    // key: everything the body's launches bake in besides the scratch generation; p_out: planes the body
+    // produces (restored on replay)
+    auto cached = [&](std::vector<unsigned char> key, GridPlanes* p_out, const std::function<void(cudaStream_t)>& body,
+                      cudaStream_t launch, int64_t search_n) {
+        auto note_search = [&] {
+            if (search_n >= 0) ctx->last_search_n = search_n;
         };
-        const void* ptrs[6] = {dW, slot_b(i), slot_p(i), slot_o(i), out, nullptr};
-        const int64_t ints[3] = {it.m, cap, (int64_t)it.first};
-        put(&ctx->scratch_gen, sizeof ctx->scratch_gen);
-        put(ptrs, sizeof ptrs);
-        put(ints, sizeof ints);
-        put(&flags, sizeof flags);
-        put(&sp, sizeof sp);
-        put(&g, sizeof g);
-        if (!it.first) put(&P, sizeof P);  // later chunks read the frame's planes
+        if (!graphs_on || ctx->prof_on) return body(launch);
+        const uint64_t gen = ctx->scratch_gen;
+        key.insert(key.begin(), (const unsigned char*)&gen, (const unsigned char*)&gen + sizeof gen);
         auto& cache = ctx->pipe_graphs;
         fsk_ctx::PipeGraph* hit = nullptr;
         for (auto& pg : cache)
             if (pg.key == key) hit = &pg;
         if (hit && hit->exec) {
             hit->last_use = ++ctx->pipe_clock;
-            if (it.first) memcpy(&P, hit->planes, sizeof P);
+            if (p_out) memcpy(p_out, hit->planes, sizeof *p_out);
             ctx->launches += hit->launches;
-            ctx->last_search_n = it.m;
-            cuda_check(cudaGraphLaunch(hit->exec, st), "cudaGraphLaunch");
+            note_search();
+            cuda_check(cudaGraphLaunch(hit->exec, launch), "cudaGraphLaunch");
             return;
         }
         if (!hit) {  // first sight: run eagerly, remember the key
-            search_eager(i, out, cap, st);
-            if (ctx->scratch_gen != *(const uint64_t*)key.data()) return;  // grew while running: key is stale
+            body(launch);
+            if (ctx->scratch_gen != gen) return;  // grew while running: the key is stale
             if (cache.size() >= 8) {
                 auto lru = std::min_element(cache.begin(), cache.end(), [](const auto& a, const auto& b) {
                     return a.last_use < b.last_use;
@@ -2269,11 +2312,10 @@ void deform_host_pipeline(fsk_ctx* ctx, const float* weights, const GridP& g, in
         if (!ctx->cap_stream)
             cuda_check(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking), "cudaStreamCreate");
         const int64_t l0 = ctx->launches;
-        const uint64_t gen0 = ctx->scratch_gen;
         cudaGraph_t graph = nullptr;
         cuda_check(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeRelaxed), "cudaStreamBeginCapture");
         try {
-            search_eager(i, out, cap, ctx->cap_stream);
+            body(ctx->cap_stream);
         } catch (...) {
             cudaStreamEndCapture(ctx->cap_stream, &graph);
             if (graph) cudaGraphDestroy(graph);
@@ -2285,18 +2327,64 @@ void deform_host_pipeline(fsk_ctx* ctx, const float* weights, const GridP& g, in
         const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
         cudaGraphDestroy(graph);
         cuda_check(ie, "cudaGraphInstantiate");
-        if (ctx->scratch_gen != gen0) {  // buffers moved under the capture: do not keep it
+        if (ctx->scratch_gen != gen) {  // buffers moved under the capture: do not keep it
             cudaGraphExecDestroy(exec);
             ctx->launches = l0;
-            return search_eager(i, out, cap, st);
+            return body(launch);
         }
         hit->exec = exec;
         hit->launches = ctx->launches - l0;
         hit->last_use = ++ctx->pipe_clock;
-        if (it.first) memcpy(hit->planes, &P, sizeof P);
-        ctx->last_search_n = it.m;
-        cuda_check(cudaGraphLaunch(exec, st), "cudaGraphLaunch");
+        if (p_out) memcpy(hit->planes, p_out, sizeof *p_out);
+        note_search();
+        cuda_check(cudaGraphLaunch(exec, launch), "cudaGraphLaunch");
     };
+    auto key_of = [&](int kind, int i, const fsk_root* out, int64_t cap, const GridPlanes* p_in) {
+        std::vector<unsigned char> key;
+        auto put = [&](const void* p, size_t b) {
+            key.insert(key.end(), (const unsigned char*)p, (const unsigned char*)p + b);
+        };
+        const Item& it = items[i];
+        const void* ptrs[6] = {dW, slot_b(i), slot_p(i), slot_o(i), out, nullptr};
+        const int64_t ints[4] = {(int64_t)kind, it.m, cap, (int64_t)it.first};
+        put(ptrs, sizeof ptrs);
+        put(ints, sizeof ints);
+        put(&flags, sizeof flags);
+        put(&sp, sizeof sp);
+        put(&g, sizeof g);
+        if (p_in) put(p_in, sizeof *p_in);
+        return key;
+    };
+    auto stage_item = [&](int i) {
+        cached(key_of(1, i, nullptr, 0, nullptr), &Ps[i & 1], [&](cudaStream_t s_) { body_stage(i, s_); }, ctx->pre, -1);
+    };
+    auto search_item = [&](int i, fsk_root* out, int64_t cap) {
+        if (staged) {
+            cached(key_of(2, i, out, cap, &Ps[i & 1]), nullptr, [&](cudaStream_t s_) { body_search(i, out, cap, s_); },
+                   st, -1);
+        } else {
+            const Item& it = items[i];
+            cached(key_of(0, i, out, cap, it.first ? nullptr : &P), it.first ? &P : nullptr,
+                   [&](cudaStream_t s_) { body_full(i, out, cap, s_); }, st, it.m);
+        }
+    };
+    cudaEvent_t w_up = nullptr;  // the weights are on the device (the stages read them on ctx->pre)
+    std::vector<cudaEvent_t> staged_ev(staged ? (size_t)N : 0, nullptr);
+    struct EvFree {
+        std::vector<cudaEvent_t>* v;
+        cudaEvent_t* w;
+        ~EvFree() {
+            for (auto e : *v)
+                if (e) cudaEventDestroy(e);
+            if (*w) cudaEventDestroy(*w);
+        }
+    } ev_free{&staged_ev, &w_up};
+    if (staged) {
+        for (auto& e : staged_ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+        cuda_check(cudaEventCreateWithFlags(&w_up, cudaEventDisableTiming), "cudaEventCreate");
+        cuda_check(cudaEventRecord(w_up, st), "cudaEventRecord");
+        cuda_check(cudaStreamWaitEvent(ctx->pre, w_up, 0), "cudaStreamWaitEvent");
+    }
     auto enqueue = [&](int i) {
         const Item& it = items[i];
         if (i >= 2) cuda_check(cudaStreamWaitEvent(ctx->upload, done[i - 2], 0), "cudaStreamWaitEvent");
@@ -2307,7 +2395,15 @@ void deform_host_pipeline(fsk_ctx* ctx, const float* weights, const GridP& g, in
                                        cudaMemcpyHostToDevice, ctx->upload),
                        "H2D points");
         cuda_check(cudaEventRecord(up[i], ctx->upload), "cudaEventRecord");
-        cuda_check(cudaStreamWaitEvent(st, up[i], 0), "cudaStreamWaitEvent");
+        if (staged) {  // stage on ctx->pre once the inputs landed and slot i & 1 is free (item i-2 searched)
+            cuda_check(cudaStreamWaitEvent(ctx->pre, up[i], 0), "cudaStreamWaitEvent");
+            if (i >= 2) cuda_check(cudaStreamWaitEvent(ctx->pre, done[i - 2], 0), "cudaStreamWaitEvent");
+            stage_item(i);
+            cuda_check(cudaEventRecord(staged_ev[i], ctx->pre), "cudaEventRecord");
+            cuda_check(cudaStreamWaitEvent(st, staged_ev[i], 0), "cudaStreamWaitEvent");
+        } else {
+            cuda_check(cudaStreamWaitEvent(st, up[i], 0), "cudaStreamWaitEvent");
+        }
         if (i >= 2) cuda_check(cudaStreamWaitEvent(st, fetched[i - 2], 0), "cudaStreamWaitEvent");
         search_item(i, slot_r(i), slotcap);
         cuda_check(cudaEventRecord(done[i], st), "cudaEventRecord");
@@ -2344,16 +2440,22 @@ void deform_host_pipeline(fsk_ctx* ctx, const float* weights, const GridP& g, in
             // buffer of exactly `cnt` records. Its inputs are still in slot i&1 (item i+2 is not
             // enqueued yet); the device is drained first (item i+1 shares the search scratch).
             cuda_check(cudaStreamSynchronize(ctx->upload), "cudaStreamSynchronize");
+            if (ctx->pre) cuda_check(cudaStreamSynchronize(ctx->pre), "cudaStreamSynchronize");
             cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
             cuda_check(cudaStreamSynchronize(ctx->copy), "cudaStreamSynchronize");
             fsk_root* big = (fsk_root*)scratch(ctx, kHRoots, cnt * sizeof(fsk_root));
-            const PrecomputeReq pre{dW, slot_b(i), nullptr, needs_f64(flags)};
-            GridPlanes Pr;
-            const SearchState s = run_search(ctx, Pr, g, dW, slot_b(i), slot_p(i), it.m, sp, flags, st, &pre);
-            compact(ctx, s, it.m, nb, slot_o(i), big, cnt, st);
-            if (i + 1 < N) {  // restore the planes of the frame of the last enqueued item (its later chunks read them)
-                const PrecomputeReq pre1{dW, slot_b(i + 1), nullptr, needs_f64(flags)};
-                P = run_precompute(ctx, pre1.w, g, pre1.bones, nullptr, nullptr, true, pre1.f64, st);
+            if (staged) {  // re-stage into slot i & 1 (zeroes its escalation counters; item i+1 owns the other slot)
+                body_stage(i, st);
+                body_search(i, big, cnt, st);
+            } else {
+                const PrecomputeReq pre{dW, slot_b(i), nullptr, needs_f64(flags)};
+                GridPlanes Pr;
+                const SearchState s = run_search(ctx, Pr, g, dW, slot_b(i), slot_p(i), it.m, sp, flags, st, &pre);
+                compact(ctx, s, it.m, nb, slot_o(i), big, cnt, st);
+                if (i + 1 < N) {  // restore the planes of the frame of the last enqueued item (its later chunks read them)
+                    const PrecomputeReq pre1{dW, slot_b(i + 1), nullptr, needs_f64(flags)};
+                    P = run_precompute(ctx, pre1.w, g, pre1.bones, nullptr, nullptr, true, pre1.f64, st);
+                }
             }
             cuda_check(cudaEventRecord(done[i], st), "cudaEventRecord");
             cuda_check(cudaStreamWaitEvent(ctx->copy, done[i], 0), "cudaStreamWaitEvent");

@@ -110,10 +110,11 @@ def test_host_call_reports_total_when_buffer_too_small(deformer):
 
 @pytest.mark.parametrize("chunks", [1, 3])
 def test_graph_replayed_items_equal_eager(deformer, monkeypatch, chunks):
-    """The host pipeline replays a chunk's device work from a CUDA graph once it has seen the same
-    launch set (slot buffers, chunk size, options, scratch generation) before. Ten frames of
-    distinct poses, called twice (the second call replays from the first call's graphs), equal
-    the eager pipeline (FSK_PIPE_GRAPH=0) bit for bit; so does a call after a scratch regrow."""
+    """The host pipeline stages each item's sort + K1 on a second stream ahead of its search and replays
+    an item's device work from CUDA graphs once it has seen the same launch set (slot buffers, chunk
+    size, options, scratch generation) before. Ten frames of distinct poses — staged eagerly, then
+    twice from graphs (the second call replays the first call's) — equal the unstaged eager pipeline
+    (FSK_PIPE_STAGE=0, FSK_PIPE_GRAPH=0) bit for bit; so does a call after a scratch regrow."""
     base, frames = _frames([6000 + 100 * (i % 2) for i in range(10)])
     hw = torch.from_numpy(base.weights).pin_memory()
     o = _opts(base)
@@ -127,9 +128,12 @@ def test_graph_replayed_items_equal_eager(deformer, monkeypatch, chunks):
         return t, [x.numpy().copy() for x in offs], [r[:n].numpy().view(np.uint32).copy() for r, n in zip(roots, t)]
 
     monkeypatch.setenv("FSK_PIPE_GRAPH", "0")
+    monkeypatch.setenv("FSK_PIPE_STAGE", "0")  # reference: every item whole on one stream, eagerly
     ref = run()
+    monkeypatch.setenv("FSK_PIPE_STAGE", "1")  # items staged (sort + K1) on a second stream ahead of their search
+    got = [run()]
     monkeypatch.setenv("FSK_PIPE_GRAPH", "1")
-    got = [run(), run()]
+    got += [run(), run()]
     # a bigger search in between regrows the scratch (new generation: the cached graphs are not reused)
     big = S.make_scene(base.dims, 60000, seed=7)
     x = torch.from_numpy(big.points).cuda()
