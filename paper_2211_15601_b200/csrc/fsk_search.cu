@@ -1,15 +1,17 @@
 // fsk_search.cu — forward hot path of the deformer on sm_100a and its C-ABI entry points.
 //
-//   K1  k_precompute        precompute_transform_grid (deformer.cpp:61-77, lbs_blend :9-19)
-//                           fused with the x-pair gather-plane relayout (fsk_device.cuh), in
-//                           float32 and (for the escalation pass) float64
+//   K1  k_precompute_v      precompute_transform_grid (deformer.cpp:61-77, lbs_blend :9-19), one
+//                           thread per vertex, fused with the x-pair gather-plane relayout
+//                           (fsk_device.cuh), in float32 and (for the escalation pass) float64
 //   S*  k_sort_*            spatial (Morton) ordering of the queries — performance only
 //   K2  k_search_fast       search_one per (point, bone-init) (correspondence.cpp:126-150)
 //                           with iterate (:97-124) in registers, float32, iteration-capped,
 //                           flags solves whose float32 outcome is not trustworthy
-//   K2b k_search_escalated  the flagged solves re-run from scratch in float64
+//   K2b k_esc_start,        the flagged solves re-run from scratch in float64, replaying the
+//       k_search_escalated  oracle's operation order (fsk_exact.cuh)
 //   D   k_dedup             dedup_roots (correspondence.cpp:162-176)
-//   C*  k_scan_*, k_emit    compaction into CorrespondenceSets (correspondence.hpp:29-42)
+//   C*  k_scan_lookback,    compaction into CorrespondenceSets (correspondence.hpp:29-42)
+//       k_emit
 //   k_scatter_dense         the dense per-(point, init) form (fsk_search_out)
 //   E   k_eval_points, k_init_states
 //
