@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--no-sort", action="store_true", help="ablation: no spatial ordering")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-stage-frames", action="store_true",
+                    help="several poses per step: one fsk_deform per pose instead of fsk_deform_frames (ablation)")
     ap.add_argument("--no-mlp", action="store_true", help="skip the MLP-stage measurements (SURVEY 8(f))")
     ap.add_argument("--poses", type=int, default=1, help="poses per step (C4: 16 poses x 1M points, 64^3 grid)")
     ap.add_argument("--backward", action="store_true", help="C3: add the implicit-diff backward to each frame")
@@ -294,7 +296,17 @@ def run_ours(args, rank, world, local_rank):
         gW = torch.empty_like(w)
         order = torch.empty((n,), dtype=torch.int32, device=dev)
 
+    # several poses per step (C4): fsk_deform_frames stages pose f+1's sort + K1 beside pose f's search
+    staged_frames = len(frames) > 1 and not args.backward and not args.no_stage_frames
+
     def step():
+        if staged_frames:
+            if world > 1:  # the poses reach every rank from their owner (NCCL over NVLink)
+                for Bf, _ in frames:
+                    dist.broadcast(Bf, src=0)
+            D.deform_frames(w, sc.dims, sc.bbox, [Bf for Bf, _ in frames], [xf for _, xf in frames], opts, tgrid=tg,
+                            outs=[roots_buf] * len(frames))
+            return
         for Bf, xf in frames:
             if world > 1:  # the frame's pose reaches every rank from its owner (NCCL over NVLink)
                 dist.broadcast(Bf, src=0)
@@ -431,7 +443,8 @@ def run_ours(args, rank, world, local_rank):
         "pipeline": {"stages": "K1 precompute (+ float64 planes) beside the spatial sort, float32 search pass, "
                                "float64 escalation replaying the oracle's operation order, dedup, compaction"
                                + (", K3 backward in the search's spatial order + dL/dw" if args.backward else ""),
-                     "sort": not args.no_sort, "precision": args.precision, "cuda_graph": bool(args.graph)},
+                     "sort": not args.no_sort, "precision": args.precision, "cuda_graph": bool(args.graph),
+                     "poses_per_step": len(frames), "poses_staged": staged_frames},
         "roofline": {"bound": "fp32", "kernel": "k_search_fast", "achieved": achieved, "peak": peak_fp32,
                      "unit": "TFLOP/s", "frac": achieved / peak_fp32,
                      "traffic": NCU_TRAFFIC_K2 if (args.grid == "32,32,32" and args.points == 200_000) else None,

@@ -183,6 +183,18 @@ int fsk_deform(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* desc, co
                int32_t n_bones_pose, const float* points, int64_t n, const fsk_search_opts* opts,
                float* tgrid, int64_t* offsets, fsk_root* roots, int64_t cap, void* stream);
 
+/* Several frames (poses) of one subject on device buffers — fsk_deform per frame (cmd_deform over
+ * a pose sequence, fskin_cli.cpp:395-429), with frame f+1's sort and K1 run on a second stream while
+ * frame f searches. bones[f] [n_b][12], points[f] [n_points[f]][3], offsets[f] [n_points[f]+1],
+ * roots[f] with capacity caps[f] (records beyond it are dropped: check offsets[f][n_points[f]]);
+ * the arrays of device pointers are host arrays. tgrid [V][12] (dev) receives the last frame's
+ * float32 transform grid, or NULL. Results equal per-frame fsk_deform calls bit for bit. Fully
+ * asynchronous (capturable in a CUDA graph). */
+int fsk_deform_frames(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* desc, int32_t n_frames,
+                      const float* const* bones, int32_t n_bones_pose, const float* const* points,
+                      const int64_t* n_points, const fsk_search_opts* opts, float* tgrid,
+                      int64_t* const* offsets, fsk_root* const* roots, const int64_t* caps, void* stream);
+
 /* Stream-compaction of a dense result's kept roots into CorrespondenceSet form: offsets
  * [N+1] int64 (dev), roots [total] (dev, capacity `cap`). *total_out (host) receives the
  * number of kept roots; this call synchronizes `stream` to read it. Returns FSK_EINVAL if

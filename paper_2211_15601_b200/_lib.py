@@ -26,6 +26,7 @@ EXPORTS = [
     "fsk_search_opts_defaults", "fsk_precompute_tgrid", "fsk_search_fwd", "fsk_compact_roots",
     "fsk_deform_host", "fsk_deform_host_frames", "fsk_eval_points", "fsk_init_states", "fsk_search_bwd", "fsk_grad_weights",
     "fsk_ctx_set_profiling", "fsk_ctx_prof_read", "fsk_measure_fp32_peak", "fsk_batch_search", "fsk_deform",
+    "fsk_deform_frames",
     "fsk_search_bwd_roots", "fsk_ctx_search_stats", "fsk_measure_fp64_peak", "fsk_measure_l1_gather_peak",
     "fsk_distill", "fsk_posed_occupancy", "fsk_distill_bwd",
     "fsk_multi_create", "fsk_multi_destroy", "fsk_multi_device_count", "fsk_multi_deform_host",
@@ -108,6 +109,7 @@ def load():
     L.fsk_search_bwd_exact_roots.argtypes = [_vp, _vp, G, _vp, _i32, _vp, _vp, _vp, _i64, _vp, _vp, ctypes.c_int, _vp]
     L.fsk_batch_search.argtypes = [_vp, _vp, _vp, _vp, G, _vp, _i32, _vp, _i64, O, _vp, _vp, _i64, _vp]
     L.fsk_deform.argtypes = [_vp, _vp, G, _vp, _i32, _vp, _i64, O, _vp, _vp, _vp, _i64, _vp]
+    L.fsk_deform_frames.argtypes = [_vp, _vp, G, _i32, _vp, _i32, _vp, _vp, O, _vp, _vp, _vp, _vp, _vp]
     L.fsk_search_bwd_roots.argtypes = [_vp, G, _vp, _vp, _vp, _i64, _vp, ctypes.c_int, _vp]
     L.fsk_search_bwd_roots_ordered.argtypes = [_vp, G, _vp, _vp, _vp, _i64, _vp, _vp, ctypes.c_int, _vp]
     L.fsk_ctx_query_order.argtypes = [_vp, _i64, _vp, _vp]

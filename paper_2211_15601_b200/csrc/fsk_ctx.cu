@@ -298,6 +298,7 @@ int fsk_ctx_destroy(fsk_ctx* ctx) {
             if (pg.exec) cudaGraphExecDestroy(pg.exec);
         if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
         if (ctx->pre) cudaStreamDestroy(ctx->pre);
+        for (auto e : ctx->frame_ev) cudaEventDestroy(e);
         delete ctx;
     });
 }

@@ -60,6 +60,7 @@ struct fsk_ctx {
     uint64_t pipe_clock = 0;
     cudaStream_t cap_stream = nullptr;  // capture stream (the caller's may be the legacy default stream)
     cudaStream_t pre = nullptr;  // host pipeline: sort + K1 of the next item, beside the current item's search
+    std::vector<cudaEvent_t> frame_ev;  // fsk_deform_frames' fork/join events
 };
 
 namespace fsk {

@@ -2640,6 +2640,53 @@ int fsk_deform(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* desc, co
     });
 }
 
+int fsk_deform_frames(fsk_ctx* ctx, const float* weights, const fsk_grid_desc* desc, int32_t n_frames,
+                      const float* const* bones, int32_t n_bones_pose, const float* const* points,
+                      const int64_t* n_points, const fsk_search_opts* opts, float* tgrid, int64_t* const* offsets,
+                      fsk_root* const* roots, const int64_t* caps, void* stream) {
+    return guard([&] {
+        set_device(ctx);
+        const GridP g = make_grid(desc);
+        check_search_args(g, n_bones_pose, weights, "precompute_transform_grid: bone count mismatch");
+        const SearchP sp = make_search(opts);
+        if (n_frames < 0) fail(FSK_EINVAL, "fsk: negative frame count");
+        if (n_frames > 0 && (!bones || !points || !n_points || !offsets || !roots || !caps))
+            fail(FSK_EINVAL, "fsk: null buffer");
+        for (int f = 0; f < n_frames; ++f) {
+            if (n_points[f] < 0) fail(FSK_EINVAL, "fsk: negative point count");
+            if (!offsets[f] || !bones[f] || (n_points[f] > 0 && !points[f])) fail(FSK_EINVAL, "fsk: null buffer");
+        }
+        cudaStream_t st = (cudaStream_t)stream;
+        if (!ctx->pre) cuda_check(cudaStreamCreateWithFlags(&ctx->pre, cudaStreamNonBlocking), "cudaStreamCreate");
+        // events: start, then per frame {staged, searched}; pooled on the context (graph-capturable)
+        const size_t need = 1 + 2 * (size_t)n_frames;
+        while (ctx->frame_ev.size() < need) {
+            cudaEvent_t e;
+            cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+            ctx->frame_ev.push_back(e);
+        }
+        cudaEvent_t* ev = ctx->frame_ev.data();
+        cuda_check(cudaEventRecord(ev[0], st), "cudaEventRecord");  // after prior work on the caller's stream
+        cuda_check(cudaStreamWaitEvent(ctx->pre, ev[0], 0), "cudaStreamWaitEvent");
+        GridPlanes Ps[2];
+        for (int f = 0; f < n_frames; ++f) {
+            const int slot = f & 1;
+            cudaEvent_t staged = ev[1 + 2 * f], searched = ev[2 + 2 * f];
+            // frame f's sort + K1 on ctx->pre into slot f & 1, once frame f-2 (the slot's last user) searched
+            if (f >= 2) cuda_check(cudaStreamWaitEvent(ctx->pre, ev[2 + 2 * (f - 2)], 0), "cudaStreamWaitEvent");
+            const PrecomputeReq pre{weights, bones[f], tgrid, needs_f64(opts->flags)};
+            run_search(ctx, Ps[slot], g, weights, bones[f], points[f], n_points[f], sp, opts->flags, ctx->pre, &pre,
+                       false, kRunStage, slot);
+            cuda_check(cudaEventRecord(staged, ctx->pre), "cudaEventRecord");
+            cuda_check(cudaStreamWaitEvent(st, staged, 0), "cudaStreamWaitEvent");
+            const SearchState s = run_search(ctx, Ps[slot], g, weights, bones[f], points[f], n_points[f], sp,
+                                             opts->flags, st, nullptr, false, kRunAfterStage, slot);
+            compact(ctx, s, n_points[f], g.nb, offsets[f], roots[f], caps[f], st);
+            cuda_check(cudaEventRecord(searched, st), "cudaEventRecord");
+        }
+    });
+}
+
 int fsk_compact_roots(fsk_ctx* ctx, const fsk_search_out* dense, int64_t n, int32_t n_init, int64_t* offsets,
                       fsk_root* roots, int64_t cap, int64_t* total_out, void* stream) {
     return guard([&] {

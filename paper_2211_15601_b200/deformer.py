@@ -264,6 +264,33 @@ class Deformer:
                                 _stream(self.device)))
         return offsets, roots
 
+    def deform_frames(self, weights, dims, bbox, bones, points, opts: SearchOptions, tgrid=None, outs=None):
+        """``fsk_deform_frames``: F frames (lists of device tensors bones [n_b,12], points [N_f,3]) of one
+        subject; frame f+1's sort + K1 run beside frame f's search. Returns [(offsets, roots)] per frame
+        (``outs``: caller-provided pairs, checked like ``deform``'s ``out``)."""
+        F = len(points)
+        if len(bones) != F or (outs is not None and len(outs) != F):
+            raise FskInvalidArgument("fsk: one bones/points (and out) entry per frame")
+        nb = bones[0].numel() // 12 if F else 1
+        if outs is None:
+            outs = [self.alloc_roots(p.shape[0], nb) for p in points]
+        else:
+            outs = [_check_roots_out(o, p.shape[0], self.device) for o, p in zip(outs, points)]
+        bones = [_f32(b, "bones", self.device) for b in bones]
+        points = [_f32(p, "points", self.device) for p in points]
+        if tgrid is not None:
+            tgrid = _f32(tgrid, "tgrid", self.device)
+        desc = grid_desc(dims, bbox, nb)
+        vp = ctypes.c_void_p
+        arr = lambda ts: (vp * max(F, 1))(*[t.data_ptr() for t in ts])  # noqa: E731
+        n = (ctypes.c_int64 * max(F, 1))(*[p.shape[0] for p in points])
+        caps = (ctypes.c_int64 * max(F, 1))(*[r.shape[0] for _, r in outs])
+        check(self.L.fsk_deform_frames(self._ctx, _ptr(_f32(weights, "weights", self.device)), ctypes.byref(desc), F,
+                                       arr(bones), nb, arr(points), n, ctypes.byref(opts.c()), _ptr(tgrid),
+                                       arr([o for o, _ in outs]), arr([r for _, r in outs]), caps,
+                                       _stream(self.device)))
+        return outs
+
     def search_bwd_roots(self, dims, bbox, n_bones, roots, root_index, grad_xc, deterministic=False, out=None,
                          order=None):
         """Backward from compact roots: root_index [N] int64 into ``roots`` (or -1). ``order`` (int32 [N],

@@ -172,3 +172,40 @@ def test_graph_cache_eviction_keeps_results(deformer, monkeypatch):
             offs, roots = run(f)
             np.testing.assert_array_equal(offs, ref[f][0])
             np.testing.assert_array_equal(roots, ref[f][1])
+
+
+def test_device_frames_equal_per_frame_deform(deformer):
+    """fsk_deform_frames (device buffers, frame f+1's sort + K1 staged beside frame f's search) equals one
+    fsk_deform per frame bit for bit, with ragged and empty frames, eagerly and replayed from a CUDA graph."""
+    base, frames = _frames([5000, 0, 7000, 3000, 6000])
+    w = torch.from_numpy(base.weights).cuda()
+    o = _opts(base)
+    B = [b.cuda() for b, _ in frames]
+    X = [p.cuda() for _, p in frames]
+    ref = []
+    for b, x in zip(B, X):
+        offs, roots = deformer.deform(w, base.dims, base.bbox, b, x, o)
+        torch.cuda.synchronize()
+        ref.append((offs.cpu().numpy(), roots[: int(offs[-1])].cpu().numpy().view(np.uint32)))
+
+    def check(outs):
+        torch.cuda.synchronize()
+        for (offs, roots), (ro, rr) in zip(outs, ref):
+            o_h = offs.cpu().numpy()
+            np.testing.assert_array_equal(o_h, ro)
+            np.testing.assert_array_equal(roots[: int(o_h[-1])].cpu().numpy().view(np.uint32), rr)
+
+    outs = deformer.deform_frames(w, base.dims, base.bbox, B, X, o)
+    check(outs)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            deformer.deform_frames(w, base.dims, base.bbox, B, X, o, outs=outs)
+    for _ in range(2):
+        for offs, roots in outs:
+            offs.fill_(-1)
+            roots.zero_()
+        g.replay()
+        check(outs)
