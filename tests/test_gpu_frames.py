@@ -174,12 +174,15 @@ def test_graph_cache_eviction_keeps_results(deformer, monkeypatch):
             np.testing.assert_array_equal(roots, ref[f][1])
 
 
-def test_device_frames_equal_per_frame_deform(deformer):
+@pytest.mark.parametrize("sort", [True, False])
+def test_device_frames_equal_per_frame_deform(deformer, sort):
     """fsk_deform_frames (device buffers, frame f+1's sort + K1 staged beside frame f's search) equals one
-    fsk_deform per frame bit for bit, with ragged and empty frames, eagerly and replayed from a CUDA graph."""
+    fsk_deform per frame bit for bit, with ragged and empty frames, eagerly and replayed from a CUDA graph
+    (and without the spatial sort: the staged slot then holds the identity order)."""
     base, frames = _frames([5000, 0, 7000, 3000, 6000])
     w = torch.from_numpy(base.weights).cuda()
     o = _opts(base)
+    o.sort = sort
     B = [b.cuda() for b, _ in frames]
     X = [p.cuda() for _, p in frames]
     ref = []
