@@ -53,3 +53,73 @@ def test_gpu_correspondence_sets_equal_reference_sources(deformer, dims, n, seed
           f"{same:.6f} ({diff} queries differ), max|dx| {dx:.2e}, equal iteration counts {it_eq:.6f}")
     assert same >= 0.9999
     assert dx <= 1e-4
+
+
+def _compare_sets(go, gr, ro, rr):
+    """Vectorised CorrespondenceSet comparison: per query, identical root sets (same bones in the same
+    order); over the identical sets, max |Δx| and equal iteration counts."""
+    cg, cr = np.diff(go), np.diff(ro)
+    eq = cg == cr
+    q = np.nonzero(eq & (cg > 0))[0]
+    cnt = cg[q]
+    within = np.arange(int(cnt.sum())) - np.repeat(np.cumsum(cnt) - cnt, cnt)
+    ai = np.repeat(go[:-1][q], cnt) + within
+    bi = np.repeat(ro[:-1][q], cnt) + within
+    bone_eq = gr[ai, 13].view(np.int32) == rr["bone"][bi]
+    qbad = np.zeros(go.shape[0] - 1, bool)
+    qbad[np.repeat(q, cnt)[~bone_eq]] = True
+    same = eq & ~qbad
+    ok = ~qbad[np.repeat(q, cnt)]  # roots of identical sets
+    dx = float(np.abs(gr[ai[ok], :3] - rr["x"][bi[ok]]).max()) if ok.any() else 0.0
+    it_eq = float((gr[ai[ok], 14].view(np.int32) == rr["iters"][bi[ok]]).mean()) if ok.any() else 1.0
+    return int(same.sum()), dx, it_eq
+
+
+def _frames_c4(n_poses, n):
+    """bench.py's C4 workload (--poses 16 --points 1000000 --grid 64,64,64, rank 0): pose 0 is
+    make_scene(seed 1); poses 1.. are seeded random poses with their own uniform points."""
+    sc = S.make_scene((64, 64, 64), n, seed=1)
+    skel = S.smpl_like_skeleton()
+    frames = [(sc.bones, sc.points)]
+    for fi in range(1, n_poses):
+        rng = np.random.default_rng(1 * 7919 + fi)
+        bones = S.forward_kinematics(skel, rng.uniform(-0.5, 0.5, sc.n_bones))
+        lo, hi = S.posed_sampling_box(skel, bones, 0.1)
+        frames.append((bones.reshape(sc.n_bones, 12).astype(np.float32),
+                       S.uniform_points(lo, hi, n, rng).astype(np.float32)))
+    return sc, frames
+
+
+@pytest.mark.parametrize("workload", ["C4", "C5"])
+def test_full_bench_workloads_equal_reference_sources(deformer, workload):
+    """Every solve of the bench's large workloads against the reference's own code: C4 in full (16 poses ×
+    1 M points, 64³ — 384 M solves) and the C5 per-GPU shard in full (8 M points, 128×128×32 — 192 M
+    solves, in chunks of 2 M queries; solves are independent). North-star bar per query and per root."""
+    if workload == "C4":
+        sc, frames = _frames_c4(16, 1_000_000)
+        chunks = [(b, p) for b, p in frames]
+    else:
+        sc = S.make_scene((128, 128, 32), 8_000_000, seed=1)
+        chunks = [(sc.bones, sc.points[c:c + 2_000_000]) for c in range(0, 8_000_000, 2_000_000)]
+    o = sc.search_options(50)
+    so = SearchOptions(50, o["conv_eps"], o["div_eps"], o["dedup_dist"])
+    w = torch.from_numpy(sc.weights).cuda()
+    total_q = same_q = 0
+    dx_max, it_eqs = 0.0, []
+    for bones, pts in chunks:
+        B, x = torch.from_numpy(np.ascontiguousarray(bones)).cuda(), torch.from_numpy(np.ascontiguousarray(pts)).cuda()
+        offs, roots = deformer.deform(w, sc.dims, sc.bbox, B, x, so)
+        go = offs.cpu().numpy()
+        gr = roots[: int(go[-1])].cpu().numpy()
+        del offs, roots
+        rr = oracle.ref_batch_search(sc.weights, sc.dims, sc.bbox, bones, pts, workers=os.cpu_count() or 8, **o)
+        same, dx, it_eq = _compare_sets(go, gr, rr["offsets"], rr)
+        total_q += pts.shape[0]
+        same_q += same
+        dx_max = max(dx_max, dx)
+        it_eqs.append(it_eq)
+    print(f"\n{workload} in full ({total_q} queries, {total_q * sc.n_bones} solves) vs the reference's own code: "
+          f"identical root sets {same_q / total_q:.7f} ({total_q - same_q} queries differ), max|dx| {dx_max:.2e}, "
+          f"equal iteration counts {min(it_eqs):.6f}")
+    assert same_q / total_q >= 0.9999
+    assert dx_max <= 1e-4
