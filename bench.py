@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--grid", default="32,32,32")
     ap.add_argument("--max-iters", type=int, default=50)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--points-dist", choices=["auto", "uniform", "training", "rays"], default="auto",
+                    help="posed-point distribution; auto: ray samples (64 per ray) for the C5 grid, else uniform")
     ap.add_argument("--no-sort", action="store_true", help="ablation: no spatial ordering")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -70,14 +72,27 @@ def parse():
     return ap.parse_args()
 
 
+def points_dist(args):
+    if args.points_dist != "auto":
+        return args.points_dist
+    return "rays" if args.grid == "128,128,32" and args.poses == 1 and not args.backward else "uniform"
+
+
 def scene_for_rank(args, rank):
     dims = tuple(int(v) for v in args.grid.split(","))
     # same skeleton/pose/grid on every rank; each rank owns a distinct point shard
-    sc = S.make_scene(dims, args.points, seed=args.seed)
+    dist_ = points_dist(args)
+    sc = S.make_scene(dims, args.points, seed=args.seed, points=dist_)
     if rank:
         rng = np.random.default_rng(args.seed * 1000 + rank)
-        lo, hi = S.posed_sampling_box(S.smpl_like_skeleton(), S.forward_kinematics(S.smpl_like_skeleton(), sc.angles))
-        sc.points = S.uniform_points(lo, hi, args.points, rng).astype(np.float32)
+        skel = S.smpl_like_skeleton()
+        bones = S.forward_kinematics(skel, sc.angles)
+        if dist_ == "training":
+            sc.points = S.training_points(skel, bones, args.points, rng).astype(np.float32)
+        else:
+            lo, hi = S.posed_sampling_box(skel, bones, 0.1)
+            gen = S.ray_points if dist_ == "rays" else S.uniform_points
+            sc.points = gen(lo, hi, args.points, rng).astype(np.float32)
     return sc
 
 
@@ -86,7 +101,8 @@ def workload_name(args):
     name = "C3" if args.backward else ("C4" if args.poses > 1 else "C2")
     if args.grid == "128,128,32" and not args.backward and args.poses == 1:
         name = "C5 (per-GPU shard of the 64M-point ray-sample workload)"
-    s = (f"{name}: {args.poses} pose(s) x {args.points // 1000}k posed points x 24 bone inits per GPU, "
+    s = (f"{name}: {args.poses} pose(s) x {args.points // 1000}k posed points ({points_dist(args)}"
+         f"{', 64 samples per ray' if points_dist(args) == 'rays' else ''}) x 24 bone inits per GPU, "
          f"{args.grid.replace(',', 'x')} grid, max_iters {args.max_iters}; step = per pose precompute_transform_grid "
          f"+ batch_search (every (point, bone-init) Broyden solve, dedup_roots) into CorrespondenceSets")
     if args.backward:
@@ -245,7 +261,7 @@ def run_reference(args, rank, world):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / len(times) * sc.points.shape[0] / m,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic SMPL-like skeleton, analytic capsule weights, uniform posed points",
+            "data": f"synthetic SMPL-like skeleton, analytic capsule weights, {points_dist(args)} posed points",
             "config": {**config_of(args, args.points, sc.n_bones, sc.dims, world),
                        "l2": "n/a (host CPU path)", "parallelism": f"{workers} host threads (parallel_for)"},
             "pipeline": note,
@@ -434,7 +450,7 @@ def run_ours(args, rank, world, local_rank):
         "vs_baseline": None, "dtype": "mixed f32/f64" if args.precision in ("mixed", "mixed-fast") else
         {"fp32": "f32", "fp64": "f64", "exact64": "f64"}[args.precision],
         "data": "synthetic: SMPL-like 24-bone skeleton, random pose U(-0.5,0.5) rad, analytic capsule weight grid, "
-                "uniform posed points (seeded; same inputs the oracle parity tests use)",
+                f"{points_dist(args)} posed points (seeded; same inputs the oracle parity tests use)",
         "config": {**config_of(args, n, nb, sc.dims, world),
                    "l2": "flushed between steps (256 MiB fill outside the per-step CUDA events)",
                    "parallelism": (f"points sharded across {world} GPU(s); per frame NCCL broadcast of the pose "

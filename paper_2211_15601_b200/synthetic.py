@@ -248,6 +248,30 @@ def uniform_points(lo, hi, n, rng) -> np.ndarray:
     return lo + rng.random((n, 3)) * (hi - lo)
 
 
+def ray_points(lo, hi, n, rng, samples=64) -> np.ndarray:
+    """Dense ray samples (BASELINE configs[4]: "rays through the posed box, 64 samples per
+    ray"): n // samples rays, each from a point on the sphere around the box (radius = the box diagonal)
+    towards a uniform point in the box, sampled at `samples` stratified depths (jittered within each
+    stratum) over the ray's segment inside the box (slab intersection) — consecutive points are one
+    ray's samples, front to back."""
+    lo, hi = np.asarray(lo, np.float64), np.asarray(hi, np.float64)
+    n_rays = -(-n // samples)
+    c, diag = 0.5 * (lo + hi), np.linalg.norm(hi - lo)
+    d = rng.normal(size=(n_rays, 3))
+    o = c + diag * d / np.linalg.norm(d, axis=1, keepdims=True)
+    t = lo + rng.random((n_rays, 3)) * (hi - lo)
+    v = t - o
+    v /= np.linalg.norm(v, axis=1, keepdims=True)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        t0, t1 = (lo - o) / v, (hi - o) / v
+    near = np.nanmax(np.minimum(t0, t1), axis=1)
+    far = np.nanmin(np.maximum(t0, t1), axis=1)  # the ray hits the box: it aims at a point inside
+    u = (np.arange(samples) + rng.random((n_rays, samples))) / samples
+    depth = near[:, None] + u * (far - near)[:, None]
+    pts = o[:, None, :] + depth[..., None] * v[:, None, :]
+    return np.clip(pts.reshape(-1, 3)[:n], lo, hi)
+
+
 def training_points(skel: Skeleton, bones, n, rng, near_sigma_frac=0.01, pad_frac=0.1):
     """``make_training_frame`` point mix (diff.cpp:148-182): half uniform in the padded
     posed box, half near-surface (area-weighted capsule surface sample moved by its
@@ -327,6 +351,9 @@ def make_scene(dims=(32, 32, 32), n_points=10_000, seed=1, pose="random", points
         x = uniform_points(plo, phi, n_points, rng)
     elif points == "training":
         x = training_points(skel, bones, n_points, rng)
+    elif points == "rays":
+        plo, phi = posed_sampling_box(skel, bones, 0.1)
+        x = ray_points(plo, phi, n_points, rng)
     else:
         raise ValueError(points)
     return Scene(tuple(dims), bbox32, np.ascontiguousarray(w),
