@@ -137,6 +137,14 @@ SearchP make_search(const fsk_search_opts* o) {
     // 1.01e-4 from the oracle's with max|J~| 5.17 — at 5 it is escalated (+0.006 % of solves on C2)
     s.esc_jmax = 5.0f;
     s.esc_cos2 = 0.1f * 0.1f;
+    // Stagnation (round 2, C5 ray workload in full against the reference's own code, 192 M solves): one
+    // 6-iteration root 1.07e-4 from float64's — the two trajectories parted at iteration 2, where the
+    // residual barely fell (3.544e-3 -> 3.535e-3), and both stopped within conv of the root on opposite
+    // sides (|x - x*| ~ |J~|·conv with max|J~| 3.3). A converged solve with a step from iteration 2 on that
+    // cut err by < 10 % and max|J~| > 2.5 is escalated: +0.04 % of the solves (oracle trajectories, 480 k
+    // solves of the ray workload).
+    s.esc_stag2 = 0.9f * 0.9f;
+    s.esc_stag_jmax = 2.5f;
     // Step rule (scripts/band_study.py on the GPU, 30 scenes × 720k solves: converged solves
     // whose iteration count differed from the oracle's by one had the float32 err/conv as low
     // as 0.84 on one side and the oracle's as high as 0.93 on the other; the roots then differ
@@ -161,6 +169,7 @@ SearchP make_search(const fsk_search_opts* o) {
     if (const char* v = getenv("FSK_ESC_CAPCONV")) s.esc_capconv = atoi(v);
     if (const char* v = getenv("FSK_ESC_CAP")) s.esc_cap = atoi(v);
     if (const char* v = getenv("FSK_ESC_JMAX")) s.esc_jmax = (float)atof(v);
+    if (const char* v = getenv("FSK_ESC_STAG_JMAX")) s.esc_stag_jmax = (float)atof(v);
 #endif
     return s;
 }

@@ -53,6 +53,8 @@ struct SearchP {
     float esc_den;      // |dx·J~dg| below this → Broyden-guard decision too close to call
     float esc_jmax;     // converged root with max|J~| above this → ill-conditioned, x* not settled in fp32
     float esc_cos2;     // (dx·J~dg)² < esc_cos2·|dx|²|J~dg|² → near-degenerate rank-one update
+    float esc_stag2;    // a step from iteration 2 on with err² > esc_stag2·(err² before it): a stagnating,
+    float esc_stag_jmax;  // path-sensitive trajectory — escalated if it converges with max|J~| > esc_stag_jmax
     float esc_rho2;     // step rule: the stop decision is "near" when err² ∈ [rho², 1/rho²]·conv² ...
     float esc_tau2;     // ... and the step it decides (taken or not) is longer than tau·conv
     bool esc_conv_band_last;  // apply the ±conv band only where a conv decision can flip the mask (the last iteration)
@@ -523,6 +525,8 @@ __device__ __forceinline__ SolveOut solve_one(const Planes<R>& P, const GridP& g
     }
     int iters = 0;
     R xl0 = x0, xl1 = x1, xl2 = x2, e2l = 0;  // float32 pass: position and err² before the last step
+    // float32 pass: a stagnating step from iteration 2 on is flagged in bit 30 of `fills` (no extra register)
+    constexpr int kStagBit = 1 << 30;
     bool conv = err2 < conv2;  // (:100-103)
     if (!conv) {
         const int limit = kFast ? min(o.max_iters, o.esc_cap) : o.max_iters;
@@ -541,6 +545,7 @@ __device__ __forceinline__ SolveOut solve_one(const Planes<R>& P, const GridP& g
                                                    &cache, (R)o.esc_cos2, kFast ? &degen : nullptr, &fills);
             if (degen) esc = true, FSK_REASON(2);
             iters = k + 1;
+            if (kFast && iters >= 2 && err2 > (R)o.esc_stag2 * e2l) fills |= kStagBit;
             if (kFast && near_conv(err2) && (!o.esc_conv_band_last || iters == o.max_iters)) esc = true, FSK_REASON(3);
             if (kFast && near_div(err2)) esc = true, FSK_REASON(11);
             if (c) {
@@ -559,6 +564,7 @@ __device__ __forceinline__ SolveOut solve_one(const Planes<R>& P, const GridP& g
 #pragma unroll
         for (int e = 0; e < 9; ++e) m = fmax(m, fabs(Ji[e]));
         if (m > (R)o.esc_jmax) esc = true, FSK_REASON(7);
+        if ((fills & kStagBit) && m > (R)o.esc_stag_jmax) esc = true, FSK_REASON(13);
         // Step rule: a float64 solve may stop one Broyden step earlier or later than this one
         // when a stop decision sat near conv; the roots then differ by that step. Escalate if
         // the step in question is long: |J~g| (the next step) when err ≥ rho·conv, or the last
@@ -580,7 +586,7 @@ __device__ __forceinline__ SolveOut solve_one(const Planes<R>& P, const GridP& g
             if (o.esc_capconv == 1 || d0 * d0 + d1 * d1 + d2 * d2 > tau2) esc = true, FSK_REASON(12);
         }
     }
-    return SolveOut{iters, conv, esc, capped, fills, reasons};
+    return SolveOut{iters, conv, esc, capped, fills & ~kStagBit, reasons};
 }
 
 }  // namespace fsk

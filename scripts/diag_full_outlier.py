@@ -13,7 +13,7 @@ from paper_2211_15601_b200 import synthetic as S  # noqa: E402
 from paper_2211_15601_b200.deformer import Deformer, SearchOptions  # noqa: E402
 
 D = Deformer(0)
-sc = S.make_scene((128, 128, 32), 8_000_000, seed=1)
+sc = S.make_scene((128, 128, 32), 8_000_000, seed=1, points=os.environ.get("DIAG_POINTS", "uniform"))
 o = sc.search_options(50)
 so = SearchOptions(50, o["conv_eps"], o["div_eps"], o["dedup_dist"])
 w = torch.from_numpy(sc.weights).cuda()
@@ -54,4 +54,15 @@ for q, bone, d, gi, ri, gres, rres in bad:
               f"resid {float(out['resid'][0, bone]):.3e} x {out['x_c'][0, bone].cpu().numpy()} max|J~| "
               f"{np.abs(J).max():.2f}  escalated solves in the query: {st[3]}")
     r1 = oracle.batch_search(sc.weights, sc.dims, sc.bbox, sc.bones, sc.points[q:q + 1], workers=1, **o)
-    print(f"   oracle: conv {int(r1['converged'][0, bone])} iters {int(r1['iters'][0, bone])} x {r1['x_c'][0, bone]}")
+    print(f"   oracle: conv {int(r1['converged'][0, bone])} iters {int(r1['iters'][0, bone])} x {r1['x_c'][0, bone]} "
+          f"resid {r1['resid'][0, bone]:.3e} max|J~| {np.abs(r1['jinv'][0, bone]).max():.2f}")
+    # the float32 trajectory, iteration by iteration (max_iters = k), against the oracle's
+    for k in range(1, 12):
+        s1 = SearchOptions(k, o["conv_eps"], o["div_eps"], o["dedup_dist"])
+        s1.precision = "fp32"
+        g1 = D.batch_search(tg, sc.dims, sc.bbox, B, x1, s1, tgrid64=tg64, weights=w)
+        ok = dict(o, max_iters=k)
+        rk = oracle.batch_search(sc.weights, sc.dims, sc.bbox, sc.bones, sc.points[q:q + 1], workers=1, **ok)
+        print(f"     k={k}: f32 x {g1['x_c'][0, bone].cpu().numpy()} resid {float(g1['resid'][0, bone]):.3e} conv "
+              f"{int(g1['converged'][0, bone])} | f64 x {rk['x_c'][0, bone]} resid {rk['resid'][0, bone]:.3e} conv "
+              f"{int(rk['converged'][0, bone])}")
