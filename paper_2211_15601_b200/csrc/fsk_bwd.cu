@@ -375,15 +375,19 @@ __global__ void __launch_bounds__(256) k_bwd_bucket_fill(RootRef R, const float*
 }
 
 // One warp per 32 consecutive bucketed roots (the buckets are contiguous and cell-ordered, so a
-// warp's records form a few runs of equal cell): lane L loads record L, then the warp walks the
-// records in order with shuffles; lane L owns the outputs o = L, L+32, L+64 of the run's cell's
-// 8 corners × 12 entries (o = 12·corner + entry) and flushes the run's fixed-point sums to the
-// corner vertices with integer atomics at each cell change. Dense cells are split across warps
-// (no load imbalance); integer addition keeps the result bitwise order- and split-independent.
+// warp's records form a few runs of equal cell): lane L loads record L into shared memory, then the
+// warp walks the records in order (broadcast reads); lane L < 24 owns row L % 3 of corner L / 3 of
+// the run's cell (four int64 sums) and flushes them to the corner vertex with integer atomics at each
+// cell change. Dense cells are split across warps (no load imbalance); integer addition keeps the
+// result bitwise order- and split-independent. (Round 1 gave each lane three of the 96 outputs: three
+// products per record instead of one: C3 det 49.7 -> 29.0 us, bitwise the same sums.)
 __global__ void __launch_bounds__(256) k_bwd_chunk_reduce(GridP g, const int64_t* __restrict__ start,
                                                           const BwdRec* __restrict__ rec,
                                                           const unsigned int* __restrict__ maxbits, int64_t n,
                                                           unsigned long long* __restrict__ acc) {
+    // Lane L < 24 owns matrix row L % 3 of corner L / 3 of the run's cell — four int64 sums, one per
+    // column of the 3x4 block, so one φ·u·scale product per record and lane serves four terms (the
+    // terms themselves are k_bwd_fixed_agg's and the round-1 per-output form's, bit for bit).
     const int64_t V = (int64_t)g.nx * g.ny * g.nz;
     const int64_t M = start[V];  // bucketed roots
     const int lane = threadIdx.x & 31;
@@ -400,49 +404,46 @@ __global__ void __launch_bounds__(256) k_bwd_chunk_reduce(GridP g, const int64_t
     }
     const double scale = fixed_scale(*maxbits, n);
     const int nxy = g.nx * g.ny;
-    int q3[3], e3[3];
-#pragma unroll
-    for (int t = 0; t < 3; ++t) {
-        const int o = lane + 32 * t;
-        q3[t] = o / 12;
-        e3[t] = o - 12 * q3[t];
-    }
-    auto flush = [&](int cl, const long long s[3]) {
-#pragma unroll
-        for (int t = 0; t < 3; ++t) {
-            const int q = q3[t];
-            const int64_t v = cl + (q >> 2) * nxy + ((q >> 1) & 1) * g.nx + (q & 1);
-            if (s[t]) atomicAdd(acc + 12 * v + e3[t], (unsigned long long)s[t]);
+    const int q = lane / 3, row = lane - 3 * q;
+    const int di = q & 1, dj = (q >> 1) & 1, dk = q >> 2;
+    const bool owner = lane < 24;
+    __shared__ float4 s_rec[256 / 32][32][3];
+    float4(&rr)[32][3] = s_rec[threadIdx.x >> 5];
+    rr[lane][0] = make_float4(__int_as_float(cell), c.tx, c.ty, c.tz);
+    rr[lane][1] = make_float4(b.x[0], b.x[1], b.x[2], b.u[0]);
+    rr[lane][2] = make_float4(b.u[1], b.u[2], 0.f, 0.f);
+    __syncwarp();
+    long long s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+    auto flush = [&](int cl) {
+        if (owner) {
+            unsigned long long* d = acc + 12 * (int64_t)(cl + dk * nxy + dj * g.nx + di) + 4 * row;
+            if (s0) atomicAdd(d, (unsigned long long)s0);
+            if (s1) atomicAdd(d + 1, (unsigned long long)s1);
+            if (s2) atomicAdd(d + 2, (unsigned long long)s2);
+            if (s3) atomicAdd(d + 3, (unsigned long long)s3);
         }
+        s0 = s1 = s2 = s3 = 0;
     };
-    long long s[3] = {0, 0, 0};
-    int cur = __shfl_sync(0xffffffffu, cell, 0);
+    int cur = __float_as_int(rr[0][0].x);
     for (int j = 0; j < cnt; ++j) {
-        const int cj = __shfl_sync(0xffffffffu, cell, j);
+        const float4 a0 = rr[j][0], a1 = rr[j][1], a2 = rr[j][2];
+        const int cj = __float_as_int(a0.x);
         if (cj != cur) {  // warp-uniform
-            flush(cur, s);
-            s[0] = s[1] = s[2] = 0;
+            flush(cur);
             cur = cj;
         }
-        const float tx = __shfl_sync(0xffffffffu, c.tx, j), ty = __shfl_sync(0xffffffffu, c.ty, j),
-                    tz = __shfl_sync(0xffffffffu, c.tz, j);
-        float x[3], u[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            x[k] = __shfl_sync(0xffffffffu, b.x[k], j);
-            u[k] = __shfl_sync(0xffffffffu, b.u[k], j);
-        }
-#pragma unroll
-        for (int t = 0; t < 3; ++t) {
-            const int q = q3[t], e = e3[t];
-            const int di = q & 1, dj = (q >> 1) & 1, dk = q >> 2, row = e >> 2, col = e & 3;
+        if (owner) {
+            const float tx = a0.y, ty = a0.z, tz = a0.w;
+            const float ur = row == 0 ? a1.w : (row == 1 ? a2.x : a2.y);
             const float phi = ((dk ? tz : 1.f - tz) * (dj ? ty : 1.f - ty)) * (di ? tx : 1.f - tx);
-            const double a = (double)phi * (double)u[row] * scale;
-            const double xc = col == 3 ? 1.0 : (double)x[col];
-            s[t] += __double2ll_rn(a * xc);
+            const double a = (double)phi * (double)ur * scale;
+            s0 += __double2ll_rn(a * (double)a1.x);
+            s1 += __double2ll_rn(a * (double)a1.y);
+            s2 += __double2ll_rn(a * (double)a1.z);
+            s3 += __double2ll_rn(a * 1.0);
         }
     }
-    flush(cur, s);
+    flush(cur);
 }
 
 // Deterministic mode over roots in spatial order (the search's query order): k_bwd_scatter_agg's

@@ -19,7 +19,8 @@ for dims, n, seed in (((32, 32, 32), 200_000, 1), ((64, 64, 16), 50_000, 7)):
     offs, roots = D.deform(w, sc.dims, sc.bbox, B, x, SearchOptions(50, o["conv_eps"], o["div_eps"], o["dedup_dist"]))
     gx = torch.randn((n, 3), generator=torch.Generator(device="cuda").manual_seed(1), device="cuda") / n
     ridx = torch.where(offs[1:] > offs[:-1], offs[:-1], torch.full_like(offs[:-1], -1))
-    gT = D.search_bwd_roots(sc.dims, sc.bbox, sc.n_bones, roots, ridx, gx, deterministic=True)
+    order = D.query_order(n)  # used by the spatial-order deterministic kernel (FSK_DET_ORDERED builds)
+    gT = D.search_bwd_roots(sc.dims, sc.bbox, sc.n_bones, roots, ridx, gx, deterministic=True, order=order)
     gW = D.grad_weights(sc.dims, sc.bbox, gT, B)
     torch.cuda.synchronize()
     h = hashlib.sha256(gT.cpu().numpy().tobytes() + gW.cpu().numpy().tobytes()).hexdigest()[:16]
