@@ -321,24 +321,30 @@ struct BwdRec {
     float u[3];
 };
 
+// Roots visited in `order` when given (the search's spatial order: neighbouring lanes mostly share a
+// cell), else in index order; lanes of a warp in the same cell share one atomic (__match_any_sync).
 __global__ void __launch_bounds__(256) k_bwd_bucket_count(GridP g, RootRef R, const float* __restrict__ gx, int64_t n,
+                                                          const int32_t* __restrict__ order,
                                                           int32_t* __restrict__ cnt, int32_t* __restrict__ cell_of,
                                                           unsigned int* __restrict__ maxbits) {
-    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j - (threadIdx.x & 31) >= n) return;  // whole warp past the end
     float m = 0.f;
-    if (p < n) {
+    int cell = -1;
+    if (j < n) {
+        const int64_t p = order ? order[j] : j;
         float xs[3], u[3];
-        int cell = -1;
         if (bwd_load(R, p, gx, xs, u)) {
             cell = locate<false>(g, xs[0], xs[1], xs[2]).base;
-            atomicAdd(cnt + cell, 1);
             const float mu = fmaxf(fabsf(u[0]), fmaxf(fabsf(u[1]), fabsf(u[2])));
             const float mx = fmaxf(1.f, fmaxf(fabsf(xs[0]), fmaxf(fabsf(xs[1]), fabsf(xs[2]))));
             m = mu * mx;
             if (!isfinite(m)) m = 3.0e38f;
         }
-        cell_of[p] = cell;
+        cell_of[j] = cell;
     }
+    const unsigned peers = __match_any_sync(0xffffffffu, cell);
+    if (cell >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(cnt + cell, __popc(peers));
     for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffff, m, o));
     if ((threadIdx.x & 31) == 0) atomicMax(maxbits, __float_as_uint(m));
 }
@@ -361,16 +367,23 @@ __global__ void __launch_bounds__(256) k_bwd_max_term(RootRef R, const float* __
 }
 
 __global__ void __launch_bounds__(256) k_bwd_bucket_fill(RootRef R, const float* __restrict__ gx, int64_t n,
+                                                         const int32_t* __restrict__ order,
                                                          const int32_t* __restrict__ cell_of,
                                                          const int64_t* __restrict__ start, int32_t* __restrict__ fill,
                                                          BwdRec* __restrict__ rec) {
-    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (p >= n) return;
-    const int cell = cell_of[p];
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    if (j - lane >= n) return;  // whole warp past the end
+    const int cell = j < n ? cell_of[j] : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, cell);
+    const int leader = __ffs(peers) - 1;
+    int base = 0;
+    if (cell >= 0 && lane == leader) base = atomicAdd(fill + cell, __popc(peers));
+    base = __shfl_sync(0xffffffffu, base, leader);
     if (cell < 0) return;
     float xs[3], u[3];
-    bwd_load(R, p, gx, xs, u);
-    const int64_t pos = start[cell] + atomicAdd(fill + cell, 1);
+    bwd_load(R, order ? order[j] : j, gx, xs, u);
+    const int64_t pos = start[cell] + base + __popc(peers & ((1u << lane) - 1));
     rec[pos] = BwdRec{{xs[0], xs[1], xs[2]}, {u[0], u[1], u[2]}};
 }
 
@@ -563,7 +576,7 @@ namespace {
 // with the same (max, n_scale), adds up to the same bits.
 unsigned long long* det_accumulate(fsk_ctx* ctx, const GridP& g, const RootRef& R, const float* grad_xc, int64_t n,
                                    int64_t n_scale, const float* max_ext, long long* acc_ext, cudaStream_t st,
-                                   unsigned int** mx_out) {
+                                   unsigned int** mx_out, const int32_t* order = nullptr) {
     const int64_t V = (int64_t)g.nx * g.ny * g.nz;
     const unsigned cap_blocks = (unsigned)ctx->sm_count * 8;
     const int64_t V4 = (V + 3) / 4 * 4;  // fixed-point accumulators, counts, fill cursors: zeroed together
@@ -579,11 +592,13 @@ unsigned long long* det_accumulate(fsk_ctx* ctx, const GridP& g, const RootRef& 
     BwdRec* rec = (BwdRec*)scratch(ctx, kBwdRec, std::max<int64_t>(1, n) * sizeof(BwdRec));
     FSK_LAUNCH(ctx, st, k_zero, std::min(blocks_for(words / 4, 256), cap_blocks), 256, 0,
                reinterpret_cast<float4*>(base), words / 4);
-    if (n > 0) FSK_LAUNCH(ctx, st, k_bwd_bucket_count, blocks_for(n, 256), 256, 0, g, R, grad_xc, n, cnt, cell_of, mx);
+    if (n > 0)
+        FSK_LAUNCH(ctx, st, k_bwd_bucket_count, blocks_for(n, 256), 256, 0, g, R, grad_xc, n, order, cnt, cell_of, mx);
     scan_i32_to_i64(ctx, cnt, V, start, st);
     const unsigned int* mscale = max_ext ? reinterpret_cast<const unsigned int*>(max_ext) : mx;
     if (n > 0) {
-        FSK_LAUNCH(ctx, st, k_bwd_bucket_fill, blocks_for(n, 256), 256, 0, R, grad_xc, n, cell_of, start, fill, rec);
+        FSK_LAUNCH(ctx, st, k_bwd_bucket_fill, blocks_for(n, 256), 256, 0, R, grad_xc, n, order, cell_of, start, fill,
+                   rec);
         FSK_LAUNCH(ctx, st, k_bwd_chunk_reduce, blocks_for(n, 256), 256, 0, g, start, rec, mscale, n_scale, acc);
     }
     if (mx_out) *mx_out = mx;
@@ -620,7 +635,7 @@ void run_bwd(fsk_ctx* ctx, const GridP& g, const RootRef& R, const float* grad_x
             FSK_LAUNCH(ctx, st, k_bwd_fixed_agg, blocks_for(n, 256), 256, 0, g, R, order, grad_xc, n, mx, n, acc);
         }
     } else {  // deterministic: bucket the roots by cell, reduce per cell, integer atomics to vertices
-        acc = det_accumulate(ctx, g, R, grad_xc, n, n, nullptr, nullptr, st, &mx);
+        acc = det_accumulate(ctx, g, R, grad_xc, n, n, nullptr, nullptr, st, &mx, order);
     }
     FSK_LAUNCH(ctx, st, k_bwd_fixed_to_float, std::min(blocks_for(12 * V, 256), cap_blocks), 256, 0,
                reinterpret_cast<const long long*>(acc), 12 * V, mx, n, grad_tgrid);
