@@ -49,8 +49,8 @@ cold-cache and serialised: compare shares, not absolutes.
 out.append(row("C2: 200 k × 24, 32³ (bench default)", c2, f"{100 * esc['frac_of_solves']:.2f} % of solves re-solved in float64"))
 out.append(row("C3: C2 + implicit-diff backward", c3))
 out.append(row("C3, deterministic backward", c3d))
-out.append(row("C4: 16 poses × 1 M points, 64³", c4))
-out.append(row("C5 per-GPU shard: 8 M points, 128×128×32", c5))
+out.append(row("C4: 16 poses × 1 M points, 64³ (fsk_deform_frames)", c4))
+out.append(row("C5 per-GPU shard: 8 M ray samples (64 per ray), 128×128×32", c5))
 out.append(row("reference arm (`--impl reference`, reference sources on all host threads)", ref,
                f"{ref['cpu_baseline']['cores']} threads, {ref['cpu_baseline'].get('kind')}"))
 out.append(f"""
