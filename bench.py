@@ -414,7 +414,7 @@ def run_ours(args, rank, world, local_rank):
                   "k_search_fast", "k_esc_start", "k_search_escalated", "k_search_escalated_pf", "k_search_f64", "k_search_exact", "k_dedup", "k_dedup_bulk", "k_scan_lookback", "k_scan_partial", "k_scan_top", "k_scan_apply",
                   "k_emit", "k_zero", "k_bwd_scatter", "k_bwd_scatter_agg", "k_bwd_max_term", "k_bwd_fixed_agg", "k_bwd_bucket_count", "k_bwd_bucket_fill", "k_bwd_chunk_reduce",
                   "k_bwd_fixed_to_float",
-                  "k_grad_weights"):
+                  "k_grad_weights", "k_grad_weights_e"):
         ms_, n_ = D.prof_read(kname, reset=False)
         if n_:
             breakdown[kname] = round(ms_ / args.steps, 5)

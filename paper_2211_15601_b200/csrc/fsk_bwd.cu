@@ -566,6 +566,30 @@ __global__ void __launch_bounds__(kGwTile) k_grad_weights(const float* __restric
     for (int64_t e = threadIdx.x; e < cnt; e += blockDim.x) gw[v0 * nb + e] = sO[e];
 }
 
+// The same, one thread per (vertex, bone) element — consecutive threads write consecutive gw entries,
+// a vertex's 48-B gradient row is an L1 broadcast to its n_b threads; the same 12-term FMA chain as
+// k_grad_weights (bitwise equal), with ~n_b x the parallelism of one thread per vertex.
+#ifndef FSK_GW_PER_ELEMENT
+#define FSK_GW_PER_ELEMENT 1
+#endif
+__global__ void __launch_bounds__(256) k_grad_weights_e(const float* __restrict__ gT, const float* __restrict__ bones,
+                                                        int nb, int64_t V, float* __restrict__ gw) {
+    extern __shared__ float sB[];
+    for (int e = threadIdx.x; e < nb * 12; e += blockDim.x) sB[e] = bones[e];
+    __syncthreads();
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= V * nb) return;
+    const int64_t v = t / nb;
+    const int i = (int)(t - v * nb);
+    const float4* src = reinterpret_cast<const float4*>(gT) + 3 * v;
+    const float4 a = __ldg(src), b = __ldg(src + 1), c = __ldg(src + 2);
+    const float G[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
+    float s = 0.f;
+#pragma unroll
+    for (int e = 0; e < 12; ++e) s = fmaf(G[e], sB[i * 12 + e], s);
+    gw[t] = s;
+}
+
 namespace {
 
 // Deterministic accumulation: zero, bucket the roots by cell (per-warp max term into this call's own
@@ -789,6 +813,11 @@ int fsk_grad_weights(fsk_ctx* ctx, const fsk_grid_desc* desc, const float* grad_
             cuda_check(cudaFuncSetAttribute(k_grad_weights, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                        "cudaFuncSetAttribute");
         cudaStream_t st = (cudaStream_t)stream;
+        if (FSK_GW_PER_ELEMENT) {
+            FSK_LAUNCH(ctx, st, k_grad_weights_e, blocks_for(V * g.nb, 256), 256, g.nb * 12 * sizeof(float), grad_tgrid,
+                       bones, g.nb, V, grad_w);
+            return;
+        }
         FSK_LAUNCH(ctx, st, k_grad_weights, blocks_for(V, kGwTile), kGwTile, smem, grad_tgrid, bones, g.nb, V, grad_w);
     });
 }
