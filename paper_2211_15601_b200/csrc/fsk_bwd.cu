@@ -570,7 +570,7 @@ __global__ void __launch_bounds__(kGwTile) k_grad_weights(const float* __restric
 // a vertex's 48-B gradient row is an L1 broadcast to its n_b threads; the same 12-term FMA chain as
 // k_grad_weights (bitwise equal), with ~n_b x the parallelism of one thread per vertex.
 #ifndef FSK_GW_PER_ELEMENT
-#define FSK_GW_PER_ELEMENT 1
+#define FSK_GW_PER_ELEMENT 0  // measured equal on C3 (9.7 us both): kept as an ablation
 #endif
 __global__ void __launch_bounds__(256) k_grad_weights_e(const float* __restrict__ gT, const float* __restrict__ bones,
                                                         int nb, int64_t V, float* __restrict__ gw) {
