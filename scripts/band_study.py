@@ -21,7 +21,8 @@ D = Deformer(0)
 ratios, mism = [], []
 for seed in seeds:
     for dims in GRIDS:
-        pts = ["uniform", "training"][seed % 2]
+        kinds = os.environ.get("BAND_POINTS", "uniform,training").split(",")
+        pts = kinds[seed % len(kinds)]
         sc = S.make_scene(dims, n, seed=seed, points=pts)
         MI = int(os.environ.get("BAND_MAX_ITERS", "50"))
         o = sc.search_options(MI)
