@@ -155,6 +155,25 @@ __device__ __forceinline__ void fma4<float>(float* T, float w, const V4<float>& 
 }
 #endif
 
+// r0 = a·b0, r1 = a·b1 (the two x-corner weights of a cell edge); float: one packed FMUL2
+template <typename R>
+__device__ __forceinline__ void mul_pair(R a, R b0, R b1, R& r0, R& r1) {
+    r0 = a * b0;
+    r1 = a * b1;
+}
+#if !defined(FSK_NO_FFMA2) && !defined(FSK_NO_FMUL2)
+template <>
+__device__ __forceinline__ void mul_pair<float>(float a, float b0, float b1, float& r0, float& r1) {
+    asm("{\n\t.reg .b64 pa, pb, pr;\n\t"
+        "mov.b64 pa, {%2, %2};\n\t"
+        "mov.b64 pb, {%3, %4};\n\t"
+        "mul.rn.f32x2 pr, pa, pb;\n\t"
+        "mov.b64 {%0, %1}, pr;\n\t}"
+        : "=f"(r0), "=f"(r1)
+        : "f"(a), "f"(b0), "f"(b1));
+}
+#endif
+
 template <typename R>
 __device__ __forceinline__ R row_dot(const V4<R>& a, R x, R y, R z) {
     return a.x * x + a.y * y + a.z * z + a.w;
@@ -173,7 +192,8 @@ __device__ __forceinline__ void trilerp_T(const Planes<R>& P, const GridP& g, co
 #pragma unroll
         for (int dj = 0; dj < 2; ++dj) {
             const R wyz = wz * (dj ? c.ty : (R)1 - c.ty);
-            const R w0 = wyz * ((R)1 - c.tx), w1 = wyz * c.tx;
+            R w0, w1;
+            mul_pair(wyz, (R)1 - c.tx, c.tx, w0, w1);
             const int v = c.base + dk * nxy + dj * g.nx;
 #pragma unroll
             for (int r = 0; r < 3; ++r) {
@@ -225,7 +245,8 @@ __device__ __forceinline__ void trilerp_cached(const Planes<R>& P, const GridP& 
 #pragma unroll
         for (int dj = 0; dj < 2; ++dj) {
             const R wyz = wz * (dj ? c.ty : (R)1 - c.ty);
-            const R w0 = wyz * ((R)1 - c.tx), w1 = wyz * c.tx;
+            R w0, w1;
+            mul_pair(wyz, (R)1 - c.tx, c.tx, w0, w1);
 #pragma unroll
             for (int r = 0; r < 3; ++r) {
                 V4<R> a, b;
@@ -294,7 +315,8 @@ __device__ __forceinline__ void jacobian_and_T(const Planes<R>& P, const GridP& 
 #pragma unroll
         for (int dj = 0; dj < 2; ++dj) {
             const R wyz = wz * (dj ? c.ty : (R)1 - c.ty);
-            const R w0 = wyz * ((R)1 - c.tx), w1 = wyz * c.tx;
+            R w0, w1;
+            mul_pair(wyz, (R)1 - c.tx, c.tx, w0, w1);
             const R fy = dj ? cl.ty : (R)1 - cl.ty, gy_s = dj ? sy : -sy;
             const R fx0 = (R)1 - cl.tx, fx1 = cl.tx;
             const int v = c.base + dk * nxy + dj * g.nx;
