@@ -20,7 +20,9 @@ def free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("extra", [[], ["--backward", "--poses", "2", "--no-e2e"]])
+@pytest.mark.parametrize("extra", [[], ["--backward", "--poses", "2", "--no-e2e"],
+                                   ["--poses", "3", "--grid", "64,64,64", "--no-e2e"],      # C4 shape: staged poses
+                                   ["--grid", "128,128,32", "--no-e2e"]])                   # C5 shape: ray samples
 def test_two_rank_bench_step(extra):
     env = dict(os.environ, FSK_BENCH_SHARED_GPU="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
@@ -35,3 +37,7 @@ def test_two_rank_bench_step(extra):
     assert "broadcast" in d["config"]["parallelism"]
     if "--backward" in extra:
         assert "all-reduce" in d["config"]["parallelism"]
+    if "--poses" in extra and "--backward" not in extra:
+        assert d["pipeline"]["poses_staged"]
+    if "128,128,32" in extra:
+        assert "rays" in d["config"]["workload"]
