@@ -410,7 +410,7 @@ def run_ours(args, rank, world, local_rank):
     if not k1_n:
         k1_ms, k1_n = D.prof_read("k_precompute", reset=False)
     breakdown = {}
-    for kname in ("k_precompute", "k_precompute_v", "k_sort_fused", "k_sort_bbox", "k_sort_hist", "k_sort_scan", "k_sort_scatter",
+    for kname in ("k_precompute", "k_precompute_v", "k_sort_fused", "k_sort_bbox", "k_sort_hist", "k_sort_scan", "k_sort_scan1", "k_sort_scatter",
                   "k_search_fast", "k_esc_start", "k_search_escalated", "k_search_escalated_pf", "k_search_f64", "k_search_exact", "k_dedup", "k_dedup_bulk", "k_scan_lookback", "k_scan_partial", "k_scan_top", "k_scan_apply",
                   "k_emit", "k_zero", "k_bwd_scatter", "k_bwd_scatter_agg", "k_bwd_max_term", "k_bwd_fixed_agg", "k_bwd_bucket_count", "k_bwd_bucket_fill", "k_bwd_chunk_reduce",
                   "k_bwd_fixed_to_float",

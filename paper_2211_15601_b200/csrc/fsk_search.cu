@@ -404,6 +404,53 @@ __global__ void __launch_bounds__(1024) k_sort_scan(int* __restrict__ hist, int*
     hist[b * 1024 + t] = prefix + warp_tot[t >> 5] + incl - v;
 }
 
+// The same scan by one block of 1024 threads, 32 consecutive buckets per thread (no grid barrier).
+#ifndef FSK_SORT_SCAN1
+#define FSK_SORT_SCAN1 1
+#endif
+#ifndef FSK_SORT_BBOX_BLOCKS_PER_SM
+#define FSK_SORT_BBOX_BLOCKS_PER_SM 2  // was 8: fewer blocks, fewer same-address atomics
+#endif
+__global__ void __launch_bounds__(1024) k_sort_scan1(int* __restrict__ hist) {
+    __shared__ int warp_tot[32];
+    constexpr int kPer = kSortBuckets / 1024;
+    const int t = threadIdx.x;
+    int4 v[kPer / 4];
+    int sum = 0;
+#pragma unroll
+    for (int i = 0; i < kPer / 4; ++i) {
+        v[i] = reinterpret_cast<const int4*>(hist)[t * (kPer / 4) + i];
+        sum += v[i].x + v[i].y + v[i].z + v[i].w;
+    }
+    int incl = sum;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffff, incl, o);
+        if ((t & 31) >= o) incl += y;
+    }
+    if ((t & 31) == 31) warp_tot[t >> 5] = incl;
+    __syncthreads();
+    if (t < 32) {
+        const int w = warp_tot[t];
+        int wi = w;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffff, wi, o);
+            if (t >= o) wi += y;
+        }
+        warp_tot[t] = wi - w;
+    }
+    __syncthreads();
+    int run = warp_tot[t >> 5] + incl - sum;
+#pragma unroll
+    for (int i = 0; i < kPer / 4; ++i) {
+        int4 o;
+        o.x = run; run += v[i].x;
+        o.y = run; run += v[i].y;
+        o.z = run; run += v[i].z;
+        o.w = run; run += v[i].w;
+        reinterpret_cast<int4*>(hist)[t * (kPer / 4) + i] = o;
+    }
+}
+
 // Scatter into sorted order: perm[pos] = p, xs[pos] = (x_p, 0) as float4 (16-B loads in K2).
 __global__ void __launch_bounds__(256) k_sort_scatter(const float* __restrict__ x, const uint16_t* __restrict__ keys,
                                                       int64_t n, int* __restrict__ offs, int* __restrict__ perm,
@@ -1809,10 +1856,13 @@ SearchState run_search(fsk_ctx* ctx, GridPlanes& P, const GridP& g, const float*
         if (FSK_SORT_FUSED && ctx->sm_count <= kSortMaxBlocks) {
             sort_fused(ctx, ss, pts, n, hist, keys, s.perm, xs);
         } else {
-            const unsigned gb = (unsigned)std::min<int64_t>(blocks_for(n, 256), (int64_t)ctx->sm_count * 8);
+            const unsigned gb = (unsigned)std::min<int64_t>(blocks_for(n, 256), (int64_t)ctx->sm_count * FSK_SORT_BBOX_BLOCKS_PER_SM);
             FSK_LAUNCH(ctx, ss, k_sort_bbox, gb, 256, 0, pts, n, bbox);
             FSK_LAUNCH(ctx, ss, k_sort_hist, blocks_for(n, 256), 256, 0, pts, n, bbox, keys, hist);
-            FSK_LAUNCH(ctx, ss, k_sort_scan, kScanBlocks, 1024, 0, hist, hist + kScanBarOff);
+            if (FSK_SORT_SCAN1)
+                FSK_LAUNCH(ctx, ss, k_sort_scan1, 1, 1024, 0, hist);
+            else
+                FSK_LAUNCH(ctx, ss, k_sort_scan, kScanBlocks, 1024, 0, hist, hist + kScanBarOff);
             FSK_LAUNCH(ctx, ss, k_sort_scatter, blocks_for(n, 256), 256, 0, pts, keys, n, hist, s.perm, xs);
         }
         if (pre) {  // join
