@@ -405,11 +405,12 @@ __global__ void __launch_bounds__(1024) k_sort_scan(int* __restrict__ hist, int*
 }
 
 // The same scan by one block of 1024 threads, 32 consecutive buckets per thread (no grid barrier).
+// Ablation (off by default).
 #ifndef FSK_SORT_SCAN1
-#define FSK_SORT_SCAN1 1
+#define FSK_SORT_SCAN1 0  // measured slower: 14.6 us vs 9.7 for the 32-block scan (C2 step 0.9695 -> 0.9756 ms)
 #endif
 #ifndef FSK_SORT_BBOX_BLOCKS_PER_SM
-#define FSK_SORT_BBOX_BLOCKS_PER_SM 2  // was 8: fewer blocks, fewer same-address atomics
+#define FSK_SORT_BBOX_BLOCKS_PER_SM 8  // 2 measured the same (11.5 us)
 #endif
 __global__ void __launch_bounds__(1024) k_sort_scan1(int* __restrict__ hist) {
     __shared__ int warp_tot[32];
