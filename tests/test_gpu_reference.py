@@ -94,7 +94,7 @@ def _frames_c4(n_poses, n):
     return sc, frames
 
 
-@pytest.mark.parametrize("workload", ["C4", "C5"])
+@pytest.mark.parametrize("workload", ["C4", "C5", "C5-uniform"])
 def test_full_bench_workloads_equal_reference_sources(deformer, workload):
     """Every solve of the bench's large workloads against the reference's own code: C4 in full (16 poses ×
     1 M points, 64³ — 384 M solves) and the C5 per-GPU shard in full (8 M ray samples, 128×128×32 — 192 M
@@ -106,8 +106,8 @@ def test_full_bench_workloads_equal_reference_sources(deformer, workload):
     if workload == "C4":
         sc, frames = _frames_c4(16, 1_000_000)
         chunks = [(b, p) for b, p in frames]
-    else:
-        sc = S.make_scene((128, 128, 32), 8_000_000, seed=1, points="rays")  # bench.py's C5: 64 samples per ray
+    else:  # bench.py's C5: 64 samples per ray; C5-uniform: the same grid with uniform points (round-1 C5)
+        sc = S.make_scene((128, 128, 32), 8_000_000, seed=1, points="rays" if workload == "C5" else "uniform")
         chunks = [(sc.bones, sc.points[c:c + 2_000_000]) for c in range(0, 8_000_000, 2_000_000)]
     o = sc.search_options(50)
     so = SearchOptions(50, o["conv_eps"], o["div_eps"], o["dedup_dist"])
