@@ -519,9 +519,48 @@ def run_ours(args, rank, world, local_rank):
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": workers, "kind": kind, "cpu_model": cpu_model(),
                                 "sample": f"{m} of {n} points x {nb} inits (precompute + search + dedup), repeated over "
                                           f"{dt:.1f} s; {note}"}
+        if args.grid == "32,32,32" and args.poses == 1 and not args.backward:
+            line["c1"] = c1_line(D, workers)
     if rank == 0:
         print(json.dumps(line), flush=True)
     D.close()
+
+
+def c1_line(D, workers, reps=50):
+    """BASELINE configs[0], the reference's own CPU configuration (10 k posed points x 24 inits, 32^3,
+    max_iters 10): one frame (precompute + search + dedup + CorrespondenceSets) on the GPU (device
+    buffers, CUDA events, median of `reps`) and through the reference's code on the host cores (median of 5
+    after one warm-up, fskin_cli.cpp:655-707) — SURVEY §8(d)'s C1 comparison. Not the headline."""
+    import torch
+    from paper_2211_15601_b200.deformer import SearchOptions
+    kind, step, _ = cpu_impl()
+    sc = S.make_scene((32, 32, 32), 10_000, seed=1)
+    o = sc.search_options(10)
+    so = SearchOptions(10, o["conv_eps"], o["div_eps"], o["dedup_dist"])
+    w, B, x = (torch.from_numpy(a).cuda() for a in (sc.weights, sc.bones, sc.points))
+    out = D.alloc_roots(x.shape[0], sc.n_bones)
+    for _ in range(5):
+        D.deform(w, sc.dims, sc.bbox, B, x, so, out=out)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for a, b in ev:
+        a.record()
+        D.deform(w, sc.dims, sc.bbox, B, x, so, out=out)
+        b.record()
+    torch.cuda.synchronize()
+    gpu_ms = float(np.median([a.elapsed_time(b) for a, b in ev]))
+    step(sc, sc.points, o, workers)
+    cpu = []
+    for _ in range(5):
+        t0 = time.perf_counter()
+        step(sc, sc.points, o, workers)
+        cpu.append(time.perf_counter() - t0)
+    cpu_ms = 1e3 * float(np.median(cpu))
+    solves = sc.points.shape[0] * sc.n_bones
+    return {"workload": "C1: 10k posed points x 24 inits, 32x32x32, max_iters 10 (BASELINE configs[0])",
+            "gpu_ms_per_frame": gpu_ms, "gpu_solves_per_s": solves / (gpu_ms * 1e-3),
+            "cpu_ms_per_frame": cpu_ms, "cpu_solves_per_s": solves / (cpu_ms * 1e-3), "cpu_kind": kind,
+            "cpu_cores": workers, "note": "one eager frame on device buffers (launch-bound at this size); CPU: "
+                                          "median of 5 after one warm-up"}
 
 
 SKIN_WIDTHS = [3, 64, 64, 64, 24]   # SkinningMlp (skinning.cpp:10-17)
