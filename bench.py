@@ -541,10 +541,17 @@ def c1_line(D, workers, reps=50):
     out = D.alloc_roots(x.shape[0], sc.n_bones)
     for _ in range(5):
         D.deform(w, sc.dims, sc.bbox, B, x, so, out=out)
+    torch.cuda.synchronize()
+    stream = torch.cuda.Stream()
+    stream.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()  # the frame replayed from a CUDA graph, like the C2 step
+    with torch.cuda.stream(stream):
+        with torch.cuda.graph(graph, stream=stream):
+            D.deform(w, sc.dims, sc.bbox, B, x, so, out=out)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
     for a, b in ev:
         a.record()
-        D.deform(w, sc.dims, sc.bbox, B, x, so, out=out)
+        graph.replay()
         b.record()
     torch.cuda.synchronize()
     gpu_ms = float(np.median([a.elapsed_time(b) for a, b in ev]))
@@ -559,8 +566,8 @@ def c1_line(D, workers, reps=50):
     return {"workload": "C1: 10k posed points x 24 inits, 32x32x32, max_iters 10 (BASELINE configs[0])",
             "gpu_ms_per_frame": gpu_ms, "gpu_solves_per_s": solves / (gpu_ms * 1e-3),
             "cpu_ms_per_frame": cpu_ms, "cpu_solves_per_s": solves / (cpu_ms * 1e-3), "cpu_kind": kind,
-            "cpu_cores": workers, "note": "one eager frame on device buffers (launch-bound at this size); CPU: "
-                                          "median of 5 after one warm-up"}
+            "cpu_cores": workers, "note": "one frame on device buffers replayed from a CUDA graph (latency-bound "
+                                          "at this size); CPU: median of 5 after one warm-up"}
 
 
 SKIN_WIDTHS = [3, 64, 64, 64, 24]   # SkinningMlp (skinning.cpp:10-17)
