@@ -212,3 +212,25 @@ def test_device_frames_equal_per_frame_deform(deformer, sort):
             roots.zero_()
         g.replay()
         check(outs)
+
+
+def test_device_frames_validation_and_capacity(deformer):
+    """fsk_deform_frames: one bones/points entry per frame, zero frames is a no-op, and a roots buffer
+    smaller than a frame's kept roots keeps the first `cap` records with the full offsets (the caller
+    checks offsets[N] <= cap, as for fsk_deform)."""
+    base, frames = _frames([4000, 4000])
+    w = torch.from_numpy(base.weights).cuda()
+    o = _opts(base)
+    B = [b.cuda() for b, _ in frames]
+    X = [p.cuda() for _, p in frames]
+    with pytest.raises(FskInvalidArgument):
+        deformer.deform_frames(w, base.dims, base.bbox, B[:1], X, o)
+    assert deformer.deform_frames(w, base.dims, base.bbox, [], [], o) == []
+    full = deformer.deform_frames(w, base.dims, base.bbox, B, X, o)
+    small = [(torch.empty(4001, dtype=torch.int64, device="cuda"), torch.zeros((100, 16), device="cuda"))
+             for _ in range(2)]
+    deformer.deform_frames(w, base.dims, base.bbox, B, X, o, outs=small)
+    torch.cuda.synchronize()
+    for (fo, fr), (so, sr) in zip(full, small):
+        assert torch.equal(fo, so) and int(so[-1]) > 100
+        assert torch.equal(fr[:100].view(torch.int32), sr.view(torch.int32))
