@@ -23,6 +23,10 @@
 #include "fsk_device.cuh"
 
 namespace fsk {
+#ifndef FSK_EXACT_PREFETCH
+#define FSK_EXACT_PREFETCH 1
+#endif
+
 namespace exact {
 
 __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
@@ -92,6 +96,17 @@ __device__ __forceinline__ void deform(const Planes<double>& P, const GridP& g, 
     const XCell c = locate(g, x0, x1, x2, false);
     const int cbase = vidx(g, c.i, c.j, c.k);
     const bool hit = FSK_EXACT_CACHE_ROWS > 0 && C && C->base == cbase;
+#if FSK_EXACT_PREFETCH
+    // all 12 corner rows (4 x-pair edges x 3 matrix rows, 64 B each) requested up front, so their L2
+    // latencies overlap instead of stalling the accumulate chain edge by edge (no effect on the values)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const int v = vidx(g, c.i, c.j + (e & 1), c.k + (e >> 1));
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(P.p + r * P.stride + (int64_t)v * 8));
+    }
+#endif
     double m[12];
 #pragma unroll
     for (int e = 0; e < 12; ++e) m[e] = 0.0;
