@@ -482,8 +482,13 @@ def run_ours(args, rank, world, local_rank):
                                 "peak_source": "fsk_measure_l1_gather_peak: independent LDG.256 at random "
                                                "32-B slots of an L1-resident table, all SMs",
                                 "cell_cache_hit_frac": 1 - fills32 / max(it32, 1),
+                                # SURVEY §8(d)'s algorithmic G = 384 B x (1 + k) per solve: the gather demand of every
+                                # evaluation, served here partly from the register cell cache (so this can exceed 1)
+                                "algorithmic_bytes_per_launch": (s32 + it32) * GATHER_BYTES,
+                                "algorithmic_frac": (s32 + it32) * GATHER_BYTES / (k2_avg * 1e-3) / 1e9 / peak_l1,
                                 "note": "bytes actually gathered (init + iterations that left the register-cached "
-                                        "cell); ncu: L1 hit 78 %, L1 data pipe 72 %, issue slots 52 % (profiles/r01_final_summary.md)"},
+                                        "cell); ncu: L1 hit 78 %, L1 data pipe 75 %, issue slots 47 % "
+                                        "(profiles/r02_final_summary.md)"},
                      "k2_share_of_step": k2_ms / max(all_ms, 1e-9),
                      "k2_escalated_share_of_step": k2e_ms / max(all_ms, 1e-9),
                      "kernel_ms_per_step": breakdown,
