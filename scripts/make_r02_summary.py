@@ -83,6 +83,22 @@ for kname in ("k_search_fast", "k_esc_start", "k_search_escalated", "k_bwd_scatt
     tmp = f"/tmp/_src_{kname}.csv"
     open(tmp, "w").write(csv)
     out.append(f"\n### {kname} stalls\n```\n" + "\n".join(run("scripts/ncu_stalls.py", tmp).splitlines()[:12]) + "\n```\n")
+out.append("""
+## What the round changed (measured; details and the rejected ones in DESIGN.md §4a″)
+
+Kept: FFMA2 trilinear accumulate (K2 0.549 → 0.542 ms); K1 one thread per vertex with whole x-pair row
+stores (C5 K1 101 → 70 µs, 49 % of HBM); host pipeline on cached CUDA graphs and staged (sort + K1 of
+item i+1 beside item i's search): C2 e2e 4.67e9 → 4.93e9; `fsk_deform_frames` (C4 68.2 → 67.9 ms);
+look-back scan; K3 records in shared memory; deterministic backward one product per record and lane
+(49.7 → 29.0 µs); 512-thread MLP CTAs (MLP-variant search 28.1 → 23.1 ms); escalation rules: conditioning
+max|J~| > 5, stagnation + max|J~| > 2.5 (full C5 ray workload then within 5.6e-5 of the reference's code).
+
+Measured and rejected (bitwise-equal outputs, slower): next-init L1 prefetch (+7 %), fused cooperative
+sort, cp.async-prefetched refill, TMA bulk dedup, L2 set-aside, ordered deterministic backward, smaller
+host chunks, float32 cap 9–12 (faster, but the band study finds roots up to 4.1e-4 off), exact-replay
+corner prefetch, FMUL2 weight pairs, single-block sort scan; shared-memory staging of the tile sub-grid
+was studied (`r02_staging_study.log`) and not built.
+""")
 out.append("\n## Launch list (`r02_final_launches.csv`, incl. the peak probes)\n\n")
 out.append(run("scripts/ncu_summary.py", os.path.join(P, "r02_final_launches.csv"), "--launches"))
 open(os.path.join(P, "r02_final_summary.md"), "w").write("".join(out))
