@@ -513,7 +513,8 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0 and not args.no_mlp:
         line["mlp_stages"] = mlp_stages(D, sc, roots_buf, n, dev)
     if not args.no_e2e:  # every rank its own shard through the host API; whole-job rate, max over ranks
-        e2e = e2e_ours(D, sc, opts, args, world=world, roots_hint=total_roots)
+        e2e = e2e_ours(D, sc, opts, args, world=world, roots_hint=total_roots,
+                       poses=[(Bf.cpu().numpy(), xf.cpu().numpy()) for Bf, xf in frames])
         if rank == 0:
             line["e2e"] = e2e
             if world == 1 and args.poses == 1:
@@ -675,7 +676,7 @@ def mlp_stages(D, sc, roots_buf, n, dev, reps=20):
     return out
 
 
-def e2e_ours(D, sc, opts, args, steps=None, world=1, roots_hint=None):
+def e2e_ours(D, sc, opts, args, steps=None, world=1, roots_hint=None, poses=None):
     """Same metric through the C-ABI host-buffer entry points: pinned host weights/bones/points
     in, CorrespondenceSets (offsets + kept roots) out, every copy inside the timed region.
     Headline: fsk_deform_host_frames over `steps` frames of the subject (one frame = one step;
@@ -684,11 +685,16 @@ def e2e_ours(D, sc, opts, args, steps=None, world=1, roots_hint=None):
     import torch
     # 20 frames per call whatever --steps is (one call's first upload and last download are not
     # overlapped; over 20 frames they are a few per cent of the call)
-    steps = steps or 20
+    # several poses (C4): the frames cycle through the same poses the device step runs, a whole number
+    # of times per call
+    poses = poses or [(sc.bones, sc.points)]
+    P = len(poses)
+    steps = steps or P * -(-20 // P)
     n, nb = sc.points.shape[0], sc.n_bones
     hw = torch.from_numpy(sc.weights).pin_memory()
-    hb = torch.from_numpy(sc.bones).pin_memory()
-    hx = torch.from_numpy(sc.points).pin_memory()
+    hbs = [torch.from_numpy(np.ascontiguousarray(b)).pin_memory() for b, _ in poses]
+    hxs = [torch.from_numpy(np.ascontiguousarray(x)).pin_memory() for _, x in poses]
+    hb, hx = hbs[0], hxs[0]
     # two output sets, alternated across frames (a consumer reads frame f while f+1 downloads)
     hoffs = [torch.empty(n + 1, dtype=torch.int64).pin_memory() for _ in range(2)]
     # root capacity: every (query, init) when that is small, else twice this frame's kept-root
@@ -697,7 +703,8 @@ def e2e_ours(D, sc, opts, args, steps=None, world=1, roots_hint=None):
     hroots = [torch.empty((cap, 16), dtype=torch.float32).pin_memory() for _ in range(2)]
 
     def frames_call():
-        return D.deform_host_frames(hw, sc.dims, sc.bbox, [hb] * steps, [hx] * steps, opts,
+        return D.deform_host_frames(hw, sc.dims, sc.bbox, [hbs[f % P] for f in range(steps)],
+                                    [hxs[f % P] for f in range(steps)], opts,
                                     [hoffs[f % 2] for f in range(steps)], [hroots[f % 2] for f in range(steps)])
 
     def timed(fn):
@@ -723,15 +730,15 @@ def e2e_ours(D, sc, opts, args, steps=None, world=1, roots_hint=None):
     total = totals[-1]
 
     def singles():
-        for _ in range(steps):
-            t = D.deform_host(hw, sc.dims, sc.bbox, hb, hx, opts, hoffs[0], hroots[0])
+        for f in range(steps):
+            t = D.deform_host(hw, sc.dims, sc.bbox, hbs[f % P], hxs[f % P], opts, hoffs[0], hroots[0])
         return t
 
     dt1 = sorted(timed(singles)[1] for _ in range(3))[1] / steps
     return {"value": world * n * nb / dt, "unit": UNIT, "ms_per_step": 1e3 * dt,
             "h2d_bytes_per_step": int(hw.numel() * 4 / steps + hb.numel() * 4 + hx.numel() * 4),
             "d2h_bytes_per_step": int((n + 1) * 8 + total * 64),
-            "frames_per_call": steps,
+            "frames_per_call": steps, "poses_cycled": P,
             "api": "fsk_deform_host_frames (C-ABI, pinned host buffers; median of three calls of `frames_per_call` "
                    "frames timed on the host clock; weights uploaded once per call, bones + points + results per frame)",
             "single_frame_call": {"value": world * n * nb / dt1, "ms_per_step": 1e3 * dt1,
