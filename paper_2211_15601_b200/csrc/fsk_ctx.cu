@@ -143,6 +143,11 @@ SearchP make_search(const fsk_search_opts* o) {
     // sides (|x - x*| ~ |J~|·conv with max|J~| 3.3). A converged solve with a step from iteration 2 on that
     // cut err by < 10 % and max|J~| > 2.5 is escalated: +0.04 % of the solves (oracle trajectories, 480 k
     // solves of the ray workload).
+    // Init on a cell face (round 2, 150-scene ray-sample band study, seed 252): an init point whose y sat
+    // on a grid plane to float32 precision took the other cell's (piecewise) Jacobian in float32 — J0
+    // differed by 0.15 in one column, the first steps parted, and the solve converged to another root
+    // 0.22 away. Init points within 1e-4 cells of a grid plane escalate (~0.06 % of the solves).
+    s.esc_face = 1e-4f;
     s.esc_stag2 = 0.9f * 0.9f;
     s.esc_stag_jmax = 2.5f;
     // Step rule (scripts/band_study.py on the GPU, 30 scenes × 720k solves: converged solves
@@ -170,6 +175,7 @@ SearchP make_search(const fsk_search_opts* o) {
     if (const char* v = getenv("FSK_ESC_CAP")) s.esc_cap = atoi(v);
     if (const char* v = getenv("FSK_ESC_JMAX")) s.esc_jmax = (float)atof(v);
     if (const char* v = getenv("FSK_ESC_STAG_JMAX")) s.esc_stag_jmax = (float)atof(v);
+    if (const char* v = getenv("FSK_ESC_FACE")) s.esc_face = (float)atof(v);
 #endif
     return s;
 }

@@ -53,6 +53,8 @@ struct SearchP {
     float esc_den;      // |dx·J~dg| below this → Broyden-guard decision too close to call
     float esc_jmax;     // converged root with max|J~| above this → ill-conditioned, x* not settled in fp32
     float esc_cos2;     // (dx·J~dg)² < esc_cos2·|dx|²|J~dg|² → near-degenerate rank-one update
+    float esc_face;     // init point within this many cells of a grid plane: the cell (and so the
+                        // piecewise Jacobian J0) is chosen within float32 noise
     float esc_stag2;    // a step from iteration 2 on with err² > esc_stag2·(err² before it): a stagnating,
     float esc_stag_jmax;  // path-sensitive trajectory — escalated if it converges with max|J~| > esc_stag_jmax
     float esc_rho2;     // step rule: the stop decision is "near" when err² ∈ [rho², 1/rho²]·conv² ...
@@ -542,6 +544,18 @@ __device__ __forceinline__ SolveOut solve_one(const Planes<R>& P, const GridP& g
     auto near_div = [&](R e2) { return e2 >= (R)o.esc_div_lo * div2 && e2 <= (R)o.esc_div_hi * div2; };
     if (kFast) {
         if (fabs(det) < (R)o.esc_det) esc = true, FSK_REASON(0);
+        // J0 is piecewise (the trilinear gradient jumps across cell faces): an init point within float32
+        // noise of a grid plane may take the other cell's Jacobian than float64 does
+        {
+            const R xi[3] = {x0, x1, x2};
+            const int nn[3] = {g.nx, g.ny, g.nz};
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const R u = (xi[a] - g_lo<R>(g, a)) * g_scale<R>(g, a);
+                const R r = rint(u);
+                if (r >= (R)0 && r <= (R)(nn[a] - 1) && fabs(u - r) < (R)o.esc_face) esc = true, FSK_REASON(14);
+            }
+        }
         if (near_conv(err2) && (!o.esc_conv_band_last || o.max_iters == 0)) esc = true, FSK_REASON(1);
         if (near_div(err2)) esc = true, FSK_REASON(10);
     }
