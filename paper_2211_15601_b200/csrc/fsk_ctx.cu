@@ -148,6 +148,11 @@ SearchP make_search(const fsk_search_opts* o) {
     // differed by 0.15 in one column, the first steps parted, and the solve converged to another root
     // 0.22 away. Init points within 1e-4 cells of a grid plane escalate (~0.06 % of the solves).
     s.esc_face = 1e-4f;
+    // Transient J~ spike (round 2, 600-scene band study, seeds 322-441, and seed 265): converged roots
+    // 1.1-1.9e-4 from float64's whose Broyden matrices reached max|J~| 7-36 on the way (ending at 1.3-1.7):
+    // the spike amplified float32 rounding into the path. Converged solves whose matrix exceeded 7 at any
+    // iteration escalate (~0.07 % of the solves on oracle trajectories).
+    s.esc_spike = 7.0f;
     s.esc_stag2 = 0.9f * 0.9f;
     s.esc_stag_jmax = 2.5f;
     // Step rule (scripts/band_study.py on the GPU, 30 scenes × 720k solves: converged solves
@@ -176,6 +181,7 @@ SearchP make_search(const fsk_search_opts* o) {
     if (const char* v = getenv("FSK_ESC_JMAX")) s.esc_jmax = (float)atof(v);
     if (const char* v = getenv("FSK_ESC_STAG_JMAX")) s.esc_stag_jmax = (float)atof(v);
     if (const char* v = getenv("FSK_ESC_FACE")) s.esc_face = (float)atof(v);
+    if (const char* v = getenv("FSK_ESC_SPIKE")) s.esc_spike = (float)atof(v);
 #endif
     return s;
 }

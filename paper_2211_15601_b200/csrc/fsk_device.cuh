@@ -55,6 +55,8 @@ struct SearchP {
     float esc_cos2;     // (dx·J~dg)² < esc_cos2·|dx|²|J~dg|² → near-degenerate rank-one update
     float esc_face;     // init point within this many cells of a grid plane: the cell (and so the
                         // piecewise Jacobian J0) is chosen within float32 noise
+    float esc_spike;    // max|J~| above this at any iteration (a transient spike of the Broyden matrix) on a
+                        // converged solve: float32 rounding was amplified on the way
     float esc_stag2;    // a step from iteration 2 on with err² > esc_stag2·(err² before it): a stagnating,
     float esc_stag_jmax;  // path-sensitive trajectory — escalated if it converges with max|J~| > esc_stag_jmax
     float esc_rho2;     // step rule: the stop decision is "near" when err² ∈ [rho², 1/rho²]·conv² ...
@@ -563,6 +565,7 @@ __device__ __forceinline__ SolveOut solve_one(const Planes<R>& P, const GridP& g
     R xl0 = x0, xl1 = x1, xl2 = x2, e2l = 0;  // float32 pass: position and err² before the last step
     // float32 pass: a stagnating step from iteration 2 on is flagged in bit 30 of `fills` (no extra register)
     constexpr int kStagBit = 1 << 30;
+    constexpr int kSpikeBit = 1 << 29;  // a J~ spike above esc_spike on the way (also carried in `fills`)
     bool conv = err2 < conv2;  // (:100-103)
     if (!conv) {
         const int limit = kFast ? min(o.max_iters, o.esc_cap) : o.max_iters;
@@ -582,6 +585,12 @@ __device__ __forceinline__ SolveOut solve_one(const Planes<R>& P, const GridP& g
             if (degen) esc = true, FSK_REASON(2);
             iters = k + 1;
             if (kFast && iters >= 2 && err2 > (R)o.esc_stag2 * e2l) fills |= kStagBit;
+            if (kFast && !c) {  // the matrix after this iteration's rank-one update
+                R m = 0;
+#pragma unroll
+                for (int e = 0; e < 9; ++e) m = fmax(m, fabs(Ji[e]));
+                if (m > (R)o.esc_spike) fills |= kSpikeBit;
+            }
             if (kFast && near_conv(err2) && (!o.esc_conv_band_last || iters == o.max_iters)) esc = true, FSK_REASON(3);
             if (kFast && near_div(err2)) esc = true, FSK_REASON(11);
             if (c) {
@@ -601,6 +610,7 @@ __device__ __forceinline__ SolveOut solve_one(const Planes<R>& P, const GridP& g
         for (int e = 0; e < 9; ++e) m = fmax(m, fabs(Ji[e]));
         if (m > (R)o.esc_jmax) esc = true, FSK_REASON(7);
         if ((fills & kStagBit) && m > (R)o.esc_stag_jmax) esc = true, FSK_REASON(13);
+        if (fills & kSpikeBit) esc = true, FSK_REASON(15);
         // Step rule: a float64 solve may stop one Broyden step earlier or later than this one
         // when a stop decision sat near conv; the roots then differ by that step. Escalate if
         // the step in question is long: |J~g| (the next step) when err ≥ rho·conv, or the last
@@ -622,7 +632,7 @@ __device__ __forceinline__ SolveOut solve_one(const Planes<R>& P, const GridP& g
             if (o.esc_capconv == 1 || d0 * d0 + d1 * d1 + d2 * d2 > tau2) esc = true, FSK_REASON(12);
         }
     }
-    return SolveOut{iters, conv, esc, capped, fills & ~kStagBit, reasons};
+    return SolveOut{iters, conv, esc, capped, fills & ~(kStagBit | kSpikeBit), reasons};
 }
 
 }  // namespace fsk

@@ -644,7 +644,7 @@ __global__ void __launch_bounds__(kSearchBlock, FSK_SEARCH_MINB)
 #endif
 #ifdef FSK_ESC_REASONS  // study builds: per-rule escalation counts (slot 8+bit: fired; 24+bit: fired alone)
         if (stats && s.reasons) {
-            for (int bit = 0; bit < 15; ++bit)
+            for (int bit = 0; bit < 16; ++bit)
                 if (s.reasons >> bit & 1u) {
                     atomicAdd(stats + 8 + bit, 1ull);
                     if (__popc(s.reasons) == 1) atomicAdd(stats + 24 + bit, 1ull);
