@@ -462,7 +462,7 @@ template <typename R, bool kCache = false>
 __device__ __forceinline__ bool broyden_step(const Planes<R>& P, const GridP& g, R xp0, R xp1, R xp2, R conv2, R& x0,
                                              R& x1, R& x2, R Ji[9], R& g0, R& g1, R& g2, R& err2, R& den,
                                              CellCache<R>* C = nullptr, R cos2 = 0, bool* degenerate = nullptr,
-                                             int* fills = nullptr) {
+                                             int* fills = nullptr, R spike_at = 0) {
     // dx = −J~ g; x += dx (:106-107)
     const R dx0 = -(Ji[0] * g0 + Ji[1] * g1 + Ji[2] * g2);
     const R dx1 = -(Ji[3] * g0 + Ji[4] * g1 + Ji[5] * g2);
@@ -507,6 +507,12 @@ __device__ __forceinline__ bool broyden_step(const Planes<R>& P, const GridP& g,
         const R w1 = dx0 * Ji[1] + dx1 * Ji[4] + dx2 * Ji[7];
         const R w2 = dx0 * Ji[2] + dx1 * Ji[5] + dx2 * Ji[8];
         rank1_update(Ji, q0, q1, q2, w0, w1, w2);
+        if (fills && spike_at > (R)0) {  // float32 pass: a transient spike of the updated matrix
+            R m = 0;
+#pragma unroll
+            for (int e = 0; e < 9; ++e) m = fmax(m, fabs(Ji[e]));
+            if (m > spike_at) *fills |= 1 << 29;
+        }
     }
     return false;
 }
@@ -581,16 +587,18 @@ __device__ __forceinline__ SolveOut solve_one(const Planes<R>& P, const GridP& g
             R den;
             bool degen = false;
             const bool c = broyden_step<R, kCache>(P, g, xp0, xp1, xp2, conv2, x0, x1, x2, Ji, g0, g1, g2, err2, den,
-                                                   &cache, (R)o.esc_cos2, kFast ? &degen : nullptr, &fills);
+                                                   &cache, (R)o.esc_cos2, kFast ? &degen : nullptr, &fills,
+#if defined(FSK_NO_SPIKE)
+                                                   (R)0);
+#elif defined(FSK_SPIKE_EARLY)
+                                                   kFast && k < FSK_SPIKE_EARLY ? (R)o.esc_spike : (R)0);
+#else
+                                                   kFast ? (R)o.esc_spike : (R)0);
+#endif
             if (degen) esc = true, FSK_REASON(2);
             iters = k + 1;
             if (kFast && iters >= 2 && err2 > (R)o.esc_stag2 * e2l) fills |= kStagBit;
-            if (kFast && !c) {  // the matrix after this iteration's rank-one update
-                R m = 0;
-#pragma unroll
-                for (int e = 0; e < 9; ++e) m = fmax(m, fabs(Ji[e]));
-                if (m > (R)o.esc_spike) fills |= kSpikeBit;
-            }
+
             if (kFast && near_conv(err2) && (!o.esc_conv_band_last || iters == o.max_iters)) esc = true, FSK_REASON(3);
             if (kFast && near_div(err2)) esc = true, FSK_REASON(11);
             if (c) {
