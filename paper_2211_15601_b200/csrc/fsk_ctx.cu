@@ -152,7 +152,7 @@ SearchP make_search(const fsk_search_opts* o) {
     // 1.1-1.9e-4 from float64's whose Broyden matrices reached max|J~| 7-36 on the way (ending at 1.3-1.7):
     // the spike amplified float32 rounding into the path. Converged solves whose matrix exceeded 7 at any
     // iteration escalate (~0.07 % of the solves on oracle trajectories).
-    s.esc_spike = 7.0f;
+    s.esc_spike = FSK_ESC_SPIKE;  // informational: the float32 pass uses the compile-time constant
     s.esc_stag2 = 0.9f * 0.9f;
     s.esc_stag_jmax = 2.5f;
     // Step rule (scripts/band_study.py on the GPU, 30 scenes × 720k solves: converged solves
@@ -181,7 +181,6 @@ SearchP make_search(const fsk_search_opts* o) {
     if (const char* v = getenv("FSK_ESC_JMAX")) s.esc_jmax = (float)atof(v);
     if (const char* v = getenv("FSK_ESC_STAG_JMAX")) s.esc_stag_jmax = (float)atof(v);
     if (const char* v = getenv("FSK_ESC_FACE")) s.esc_face = (float)atof(v);
-    if (const char* v = getenv("FSK_ESC_SPIKE")) s.esc_spike = (float)atof(v);
 #endif
     return s;
 }

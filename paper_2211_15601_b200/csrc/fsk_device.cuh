@@ -455,6 +455,9 @@ __device__ __forceinline__ void rank1_update<float>(float Ji[9], float q0, float
 }
 #endif
 
+#ifndef FSK_ESC_SPIKE
+#define FSK_ESC_SPIKE 7.0f  // max|J~| of a transient Broyden-matrix spike that escalates a converged float32 solve
+#endif
 // One Broyden iteration after the divergence check (correspondence.cpp:106-122): step,
 // re-evaluate, and — unless the new residual converged — the good-Broyden rank-one update.
 // Returns true iff converged; `den` receives dx·J~dg (0 when converged).
@@ -590,10 +593,10 @@ __device__ __forceinline__ SolveOut solve_one(const Planes<R>& P, const GridP& g
                                                    &cache, (R)o.esc_cos2, kFast ? &degen : nullptr, &fills,
 #if defined(FSK_NO_SPIKE)
                                                    (R)0);
-#elif defined(FSK_SPIKE_EARLY)
-                                                   kFast && k < FSK_SPIKE_EARLY ? (R)o.esc_spike : (R)0);
 #else
-                                                   kFast ? (R)o.esc_spike : (R)0);
+                                                   // a compile-time threshold (an immediate operand: the
+                                                   // parameter held in a register spilled the loop)
+                                                   kFast ? (R)FSK_ESC_SPIKE : (R)0);
 #endif
             if (degen) esc = true, FSK_REASON(2);
             iters = k + 1;
