@@ -37,9 +37,9 @@ UNIT = "solves/s"
 FLOPS_INIT, FLOPS_ITER, FLOPS_FINAL_SAVING = 674, 332, 66
 GATHER_BYTES = 384  # 8 corners x 48 B of transform grid per d(x) evaluation
 # dram__bytes_read.sum + dram__bytes_write.sum of one k_search_fast launch (C2) from the ncu --set full
-# capture profiles/r02_final_search.ncu-rep: 14.1 MB read + 176.1 MB written (the bone-major search planes;
+# capture profiles/r02_final_search.ncu-rep: 14.0 MB read + 176.9 MB written (the bone-major search planes;
 # the gather itself is L1/L2-resident)
-NCU_TRAFFIC_K2 = 14.062336e6 + 176.142848e6
+NCU_TRAFFIC_K2 = 14.043648e6 + 176.929024e6
 NCU_TRAFFIC_SRC = "ncu --set full, profiles/r02_final_search.ncu-rep (C2 only)"
 
 
