@@ -90,8 +90,11 @@ Kept: FFMA2 trilinear accumulate (K2 0.549 → 0.542 ms); K1 one thread per vert
 stores (C5 K1 101 → 70 µs, 49 % of HBM); host pipeline on cached CUDA graphs and staged (sort + K1 of
 item i+1 beside item i's search): C2 e2e 4.67e9 → 4.93e9; `fsk_deform_frames` (C4 68.2 → 67.9 ms);
 look-back scan; K3 records in shared memory; deterministic backward one product per record and lane
-(49.7 → 29.0 µs); 512-thread MLP CTAs (MLP-variant search 28.1 → 23.1 ms); escalation rules: conditioning
-max|J~| > 5, stagnation + max|J~| > 2.5 (full C5 ray workload then within 5.6e-5 of the reference's code).
+(49.7 → 29.0 µs); 512-thread MLP CTAs (MLP-variant search 28.1 → 23.1 ms); escalation rules found by
+full-workload and 1 950-scene band studies: conditioning max|J~| > 5, stagnation + max|J~| > 2.5, init on a
+cell face (a 0.22-off root), transient J~ spike > 7 (roots 1.1–1.9e-4 off; costs +1 % C2 step in register
+spill) — after them no converged root beyond 8.9e-5 in 1.40 G band-study solves, and the full C4/C5
+workloads within 9.8e-5 of the reference's own code.
 
 Measured and rejected (bitwise-equal outputs, slower): next-init L1 prefetch (+7 %), fused cooperative
 sort, cp.async-prefetched refill, TMA bulk dedup, L2 set-aside, ordered deterministic backward, smaller
